@@ -1,0 +1,505 @@
+/*
+ * api.c -- ORACLE public entry points (TEST INFRASTRUCTURE ONLY; see orc.h).
+ *
+ * A context holds the nested hierarchy, each level's operator assembled
+ * by rediscretisation (reading R-coarse / SURVEY A5), its vertex-star patches
+ * (P:567-571), the prolongations and the coarse dense LU (stand-in for
+ * MUMPS; reading R-coarse).  Levels are numbered 0 = coarsest.
+ *
+ *   sweep   : one parallel subspace-correction step
+ *             r = b - A x;  y_i = A_i^-1 R_i r;  x_d <- fma(theta w_d, c_d, x_d)
+ *             with c_d = sum_{i ∋ d} y_i[k_i(d)] (ascending i), w_d = 1/m_d (R-weights)
+ *   vcycle  : V_l(b): l=0 coarse LU solve; else nu_pre sweeps from x = 0, restrict
+ *             r with P^T, recurse, prolong-add, nu_post sweeps (R-vcycle)
+ *   gmres   : right-preconditioned by the V-cycle, x0 = 0, modified Gram-Schmidt,
+ *             Givens, no restart; stop when |g_{k+1}| <= max(rtol |b|, atol)
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#include "orc.h"
+
+typedef struct {
+    OMesh m;
+    OSpace s;
+    OCsr A;
+    OPatches pt;
+    double **lu;      /* per patch n_i*n_i row-major factor (lazy) */
+    int **perm;
+    OCsr P, PT;       /* to the next coarser level (l >= 1) */
+    double *w;        /* potential of the advecting field on this level's vertices (R-w) */
+} OLevel;
+
+typedef struct {
+    int block, dim, nlev;
+    OParams p;
+    double theta;
+    OLevel *lv;
+    double *clu;      /* coarse LU (row-major n0*n0) */
+    int *cperm;
+    int status;
+} OCtx;
+
+static void level_free(OLevel *L) {
+    if (L->lu) {
+        for (i64 i = 0; i < L->pt.np; i++) { free(L->lu[i]); free(L->perm[i]); }
+        free(L->lu); free(L->perm);
+    }
+    oc_free(&L->A); oc_free(&L->P); oc_free(&L->PT);
+    opt_free(&L->pt); os_free(&L->s); om_free(&L->m); free(L->w);
+}
+
+void orc_destroy(OCtx *c) {
+    if (!c) return;
+    for (int l = 0; l < c->nlev; l++) level_free(&c->lv[l]);
+    free(c->lv); free(c->clu); free(c->cperm); free(c);
+}
+
+/* dparams: Re, Rem, S, gamma, sigma, mu, theta ; iparams: nu_pre, nu_post
+ * w_fine: potential of the advecting field at the finest vertices (vertex order of
+ *         R-mesh): 2D stream function psi (1 per vertex), 3D vector potential A (3 per vertex).
+ * cmask_fine: NULL, or a finest-level cell mask (only then: assemble the finest
+ * level restricted to it and build no coarser level; used for bounded samples). */
+OCtx *orc_create_masked(int block, int dim, int N, int nlev, const double *dparams, const int *iparams,
+                        const double *w_fine, const unsigned char *cmask_fine) {
+    if ((block != ORC_EB && block != ORC_VEL) || (dim != 2 && dim != 3) || nlev < 1 || N < 1) return NULL;
+    if (N % (1 << (nlev - 1))) return NULL;
+    OCtx *c = calloc(1, sizeof(OCtx));
+    c->block = block; c->dim = dim; c->nlev = nlev;
+    c->p.Re = dparams[0]; c->p.Rem = dparams[1]; c->p.S = dparams[2]; c->p.gamma = dparams[3];
+    c->p.sigma = dparams[4]; c->p.mu = dparams[5]; c->theta = dparams[6];
+    c->p.nu_pre = iparams[0]; c->p.nu_post = iparams[1];
+    c->lv = calloc((size_t)nlev, sizeof(OLevel));
+    int lo = cmask_fine ? nlev - 1 : 0;
+    for (int l = nlev - 1; l >= lo; l--) {
+        OLevel *L = &c->lv[l];
+        int Nl = N >> (nlev - 1 - l), step = 1 << (nlev - 1 - l);
+        om_build(&L->m, dim, Nl);
+        os_build(&L->s, &L->m, block);
+        /* w on this level: injection of the finest vertex values (R-w) */
+        int nc = dim == 2 ? 1 : 3;
+        L->w = malloc(sizeof(double) * nc * L->m.nv);
+        for (i64 v = 0; v < L->m.nv; v++) {
+            int i = L->m.lat[3 * v] * step, j = L->m.lat[3 * v + 1] * step, k = L->m.lat[3 * v + 2] * step;
+            i64 fv = dim == 2 ? i + (i64)(N + 1) * j : i + (i64)(N + 1) * (j + (i64)(N + 1) * k);
+            for (int t = 0; t < nc; t++) L->w[v * nc + t] = w_fine[fv * nc + t];
+        }
+        oa_assemble_masked(&L->A, &L->m, &L->s, &c->p, L->w, l == nlev - 1 ? cmask_fine : NULL);
+        opt_build(&L->pt, &L->m, &L->s);
+    }
+    if (!cmask_fine)
+        for (int l = 1; l < nlev; l++) {
+            op_prolongation(&c->lv[l].P, &c->lv[l].m, &c->lv[l].s, &c->lv[l - 1].m, &c->lv[l - 1].s);
+            oc_transpose(&c->lv[l].PT, &c->lv[l].P, c->lv[l - 1].s.n);
+        }
+    return c;
+}
+
+OCtx *orc_create(int block, int dim, int N, int nlev, const double *dparams, const int *iparams,
+                 const double *w_fine) {
+    return orc_create_masked(block, dim, N, nlev, dparams, iparams, w_fine, NULL);
+}
+
+/* out: n, nnz, npatch, sum_n, sum_n2, nE, nv, nc, ne, nf, P nnz */
+int orc_level_info(const OCtx *c, int l, i64 *out) {
+    if (!c || l < 0 || l >= c->nlev) return 1;
+    const OLevel *L = &c->lv[l];
+    i64 s2 = 0;
+    for (i64 i = 0; i < L->pt.np; i++) { i64 k = L->pt.ptr[i + 1] - L->pt.ptr[i]; s2 += k * k; }
+    out[0] = L->s.n; out[1] = L->A.nnz; out[2] = L->pt.np; out[3] = L->pt.np ? L->pt.ptr[L->pt.np] : 0;
+    out[4] = s2; out[5] = L->s.nE; out[6] = L->m.nv; out[7] = L->m.nc; out[8] = L->m.ne; out[9] = L->m.nf;
+    out[10] = L->P.nnz;
+    return 0;
+}
+
+int orc_export_csr(const OCtx *c, int l, i64 *rp, int *ci, double *v) {
+    const OCsr *A = &c->lv[l].A;
+    memcpy(rp, A->rp, sizeof(i64) * (A->n + 1));
+    memcpy(ci, A->ci, sizeof(int) * A->nnz);
+    memcpy(v, A->v, sizeof(double) * A->nnz);
+    return 0;
+}
+
+int orc_export_prolongation(const OCtx *c, int l, i64 *rp, int *ci, double *v) {
+    if (l < 1) return 1;
+    const OCsr *A = &c->lv[l].P;
+    memcpy(rp, A->rp, sizeof(i64) * (A->n + 1));
+    memcpy(ci, A->ci, sizeof(int) * A->nnz);
+    memcpy(v, A->v, sizeof(double) * A->nnz);
+    return 0;
+}
+
+int orc_export_patches(const OCtx *c, int l, i64 *ptr, int *dofs, int *vert, int *mult) {
+    const OPatches *pt = &c->lv[l].pt;
+    memcpy(ptr, pt->ptr, sizeof(i64) * (pt->np + 1));
+    memcpy(dofs, pt->dofs, sizeof(int) * pt->ptr[pt->np]);
+    memcpy(vert, pt->vert, sizeof(int) * pt->np);
+    memcpy(mult, pt->mult, sizeof(int) * c->lv[l].s.n);
+    return 0;
+}
+
+/* mesh export for tests: x (nv*3), cv (nc*(d+1)), ev (ne*2), fv (nf*3), fcell (nfacet*2),
+ * dof entity maps (n each) */
+int orc_export_mesh(const OCtx *c, int l, double *x, int *cv, int *ev, int *fv, int *fcell, int *dkind,
+                    int *dent, int *dsub) {
+    const OLevel *L = &c->lv[l];
+    const OMesh *m = &L->m;
+    if (x) memcpy(x, m->x, sizeof(double) * 3 * m->nv);
+    if (cv) memcpy(cv, m->cv, sizeof(int) * (m->dim + 1) * m->nc);
+    if (ev) memcpy(ev, m->ev, sizeof(int) * 2 * m->ne);
+    if (fv && m->nf) memcpy(fv, m->fv, sizeof(int) * 3 * m->nf);
+    if (fcell) memcpy(fcell, m->fcell, sizeof(int) * 2 * m->nfacet);
+    if (dkind) memcpy(dkind, L->s.dkind, sizeof(int) * L->s.n);
+    if (dent) memcpy(dent, L->s.dent, sizeof(int) * L->s.n);
+    if (dsub) memcpy(dsub, L->s.dsub, sizeof(int) * L->s.n);
+    return 0;
+}
+
+/* ---------------- order-defined kernels (R-order) ---------------- */
+
+/* r = b - A x: row sums as an fma chain from +0.0 in ascending column order */
+static void residual(const OCsr *A, const double *b, const double *x, double *r) {
+    for (i64 i = 0; i < A->n; i++) {
+        double s = 0.0;
+        for (i64 t = A->rp[i]; t < A->rp[i + 1]; t++) s = fma(A->v[t], x[A->ci[t]], s);
+        r[i] = b[i] - s;
+    }
+}
+
+int orc_spmv(const OCtx *c, int l, const double *x, double *y) {
+    const OCsr *A = &c->lv[l].A;
+    for (i64 i = 0; i < A->n; i++) {
+        double s = 0.0;
+        for (i64 t = A->rp[i]; t < A->rp[i + 1]; t++) s = fma(A->v[t], x[A->ci[t]], s);
+        y[i] = s;
+    }
+    return 0;
+}
+
+int orc_residual(const OCtx *c, int l, const double *b, const double *x, double *r) {
+    residual(&c->lv[l].A, b, x, r);
+    return 0;
+}
+
+/* dense principal submatrix A_i = R_i A R_i^T */
+static void patch_matrix(const OLevel *L, i64 i, double *a, double *amax) {
+    const OPatches *pt = &L->pt;
+    int n = (int)(pt->ptr[i + 1] - pt->ptr[i]);
+    const int *dofs = pt->dofs + pt->ptr[i];
+    double mx = 0;
+    for (int r = 0; r < n; r++)
+        for (int q = 0; q < n; q++) {
+            i64 p = oc_find(&L->A, dofs[r], dofs[q]);
+            a[(i64)r * n + q] = p >= 0 ? L->A.v[p] : 0.0;
+            if (fabs(a[(i64)r * n + q]) > mx) mx = fabs(a[(i64)r * n + q]);
+        }
+    *amax = mx;
+}
+
+int orc_patch_matrix(const OCtx *c, int l, i64 i, double *a) {
+    double amax;
+    patch_matrix(&c->lv[l], i, a, &amax);
+    return 0;
+}
+
+/* returns 0 or 1 + (patch index) of the first singular patch */
+static i64 factor_level(OCtx *c, int l) {
+    OLevel *L = &c->lv[l];
+    if (L->lu) return 0;
+    L->lu = calloc((size_t)L->pt.np, sizeof(double *));
+    L->perm = calloc((size_t)L->pt.np, sizeof(int *));
+    for (i64 i = 0; i < L->pt.np; i++) {
+        int n = (int)(L->pt.ptr[i + 1] - L->pt.ptr[i]);
+        double amax;
+        L->lu[i] = malloc(sizeof(double) * n * n);
+        L->perm[i] = malloc(sizeof(int) * n);
+        patch_matrix(L, i, L->lu[i], &amax);
+        if (od_lu(L->lu[i], n, L->perm[i], amax)) return i + 1;
+    }
+    return 0;
+}
+
+int orc_patch_lu(OCtx *c, int l, i64 i, double *lu, int *perm) {
+    OLevel *L = &c->lv[l];
+    int n = (int)(L->pt.ptr[i + 1] - L->pt.ptr[i]);
+    double amax;
+    patch_matrix(L, i, lu, &amax);
+    return od_lu(lu, n, perm, amax);
+}
+
+/* one sweep S(x; b) on level l (R-sweep). returns 0 / 1+patch if singular */
+static i64 sweep(OCtx *c, int l, int x_is_zero, const double *b, double *x) {
+    OLevel *L = &c->lv[l];
+    i64 bad = factor_level(c, l);
+    if (bad) return bad;
+    i64 n = L->s.n;
+    const OPatches *pt = &L->pt;
+    double *r = malloc(sizeof(double) * n);
+    double *y = malloc(sizeof(double) * (pt->ptr[pt->np] ? pt->ptr[pt->np] : 1));
+    double *rl = malloc(sizeof(double) * 512);
+    if (x_is_zero) { for (i64 d = 0; d < n; d++) { r[d] = b[d]; x[d] = 0.0; } }
+    else residual(&L->A, b, x, r);
+    for (i64 i = 0; i < pt->np; i++) {
+        int ni = (int)(pt->ptr[i + 1] - pt->ptr[i]);
+        for (int k = 0; k < ni; k++) rl[k] = r[pt->dofs[pt->ptr[i] + k]];
+        od_lu_solve(L->lu[i], ni, L->perm[i], rl, y + pt->ptr[i]);
+    }
+    for (i64 d = 0; d < n; d++) {
+        double cd = 0.0;
+        for (i64 t = pt->dptr[d]; t < pt->dptr[d + 1]; t++) cd += y[pt->dslot[t]];
+        double wd = c->theta * (1.0 / pt->mult[d]);
+        x[d] = fma(wd, cd, x[d]);
+    }
+    free(r); free(y); free(rl);
+    return 0;
+}
+
+i64 orc_sweep(OCtx *c, int l, int nsweeps, int x_is_zero, const double *b, double *x) {
+    for (int s = 0; s < nsweeps; s++) {
+        i64 st = sweep(c, l, x_is_zero && s == 0, b, x);
+        if (st) return st;
+    }
+    return 0;
+}
+
+/* x_new[d] for the sampled DoFs after ONE sweep, computing only the patches that
+ * contain them (same arithmetic as sweep(); used at full sizes). */
+i64 orc_sweep_sample(OCtx *c, int l, int x_is_zero, const double *b, const double *x, i64 ns, const int *dofs,
+                     double *out) {
+    OLevel *L = &c->lv[l];
+    const OPatches *pt = &L->pt;
+    double *a = malloc(sizeof(double) * 512 * 512);
+    int *perm = malloc(sizeof(int) * 512);
+    double *rl = malloc(sizeof(double) * 512), *yl = malloc(sizeof(double) * 512);
+    /* slot -> patch via binary search on ptr */
+    for (i64 s = 0; s < ns; s++) {
+        int d = dofs[s];
+        double cd = 0.0;
+        for (i64 t = pt->dptr[d]; t < pt->dptr[d + 1]; t++) {
+            i64 slot = pt->dslot[t], lo = 0, hi = pt->np - 1;
+            while (lo < hi) { i64 mid = (lo + hi + 1) / 2; if (pt->ptr[mid] <= slot) lo = mid; else hi = mid - 1; }
+            i64 i = lo;
+            int ni = (int)(pt->ptr[i + 1] - pt->ptr[i]);
+            double amax;
+            patch_matrix(L, i, a, &amax);
+            if (od_lu(a, ni, perm, amax)) { free(a); free(perm); free(rl); free(yl); return i + 1; }
+            for (int k = 0; k < ni; k++) {
+                int e = pt->dofs[pt->ptr[i] + k];
+                if (x_is_zero) rl[k] = b[e];
+                else {
+                    double sacc = 0.0;
+                    for (i64 q = L->A.rp[e]; q < L->A.rp[e + 1]; q++) sacc = fma(L->A.v[q], x[L->A.ci[q]], sacc);
+                    rl[k] = b[e] - sacc;
+                }
+            }
+            od_lu_solve(a, ni, perm, rl, yl);
+            cd += yl[slot - pt->ptr[i]];
+        }
+        double wd = c->theta * (1.0 / pt->mult[d]);
+        out[s] = fma(wd, cd, x_is_zero ? 0.0 : x[d]);
+    }
+    free(a); free(perm); free(rl); free(yl);
+    return 0;
+}
+
+/* ---------------- transfer (R-vcycle: ascending fma chains from +0.0) ---------------- */
+int orc_restrict(const OCtx *c, int l, const double *r, double *rc) {
+    const OCsr *T = &c->lv[l].PT;
+    for (i64 J = 0; J < T->n; J++) {
+        double s = 0.0;
+        for (i64 t = T->rp[J]; t < T->rp[J + 1]; t++) s = fma(T->v[t], r[T->ci[t]], s);
+        rc[J] = s;
+    }
+    return 0;
+}
+
+int orc_prolong_add(const OCtx *c, int l, const double *ec, double *x) {
+    const OCsr *P = &c->lv[l].P;
+    for (i64 I = 0; I < P->n; I++) {
+        double s = 0.0;
+        for (i64 t = P->rp[I]; t < P->rp[I + 1]; t++) s = fma(P->v[t], ec[P->ci[t]], s);
+        x[I] = x[I] + s;
+    }
+    return 0;
+}
+
+/* ---------------- coarse solve (dense LU, R-coarse) ---------------- */
+static int coarse_factor(OCtx *c) {
+    if (c->clu) return 0;
+    OLevel *L = &c->lv[0];
+    i64 n = L->s.n;
+    c->clu = calloc((size_t)((n * n) > 0 ? n * n : 1), sizeof(double));
+    c->cperm = malloc(sizeof(int) * (n ? n : 1));
+    double amax = 0;
+    for (i64 i = 0; i < n; i++)
+        for (i64 t = L->A.rp[i]; t < L->A.rp[i + 1]; t++) {
+            c->clu[i * n + L->A.ci[t]] = L->A.v[t];
+            if (fabs(L->A.v[t]) > amax) amax = fabs(L->A.v[t]);
+        }
+    return od_lu(c->clu, (int)n, c->cperm, amax);
+}
+
+int orc_coarse_solve(OCtx *c, const double *b, double *x) {
+    if (coarse_factor(c)) return 1;
+    od_lu_solve(c->clu, (int)c->lv[0].s.n, c->cperm, b, x);
+    return 0;
+}
+
+int orc_coarse_lu(OCtx *c, double *lu, int *perm) {
+    int st = coarse_factor(c);
+    i64 n = c->lv[0].s.n;
+    memcpy(lu, c->clu, sizeof(double) * n * n);
+    memcpy(perm, c->cperm, sizeof(int) * n);
+    return st;
+}
+
+static int vcycle(OCtx *c, int l, const double *b, double *x) {
+    if (l == 0) return orc_coarse_solve(c, b, x);
+    OLevel *L = &c->lv[l];
+    i64 n = L->s.n, nc = c->lv[l - 1].s.n;
+    for (i64 d = 0; d < n; d++) x[d] = 0.0;
+    int zero = 1;
+    for (int s = 0; s < c->p.nu_pre; s++) { if (sweep(c, l, zero, b, x)) return 1; zero = 0; }
+    double *r = malloc(sizeof(double) * n), *rc = malloc(sizeof(double) * nc), *ec = malloc(sizeof(double) * nc);
+    residual(&L->A, b, x, r);
+    orc_restrict(c, l, r, rc);
+    int st = vcycle(c, l - 1, rc, ec);
+    if (!st) {
+        orc_prolong_add(c, l, ec, x);
+        for (int s = 0; s < c->p.nu_post; s++) if (sweep(c, l, 0, b, x)) { st = 1; break; }
+    }
+    free(r); free(rc); free(ec);
+    return st;
+}
+
+int orc_vcycle(OCtx *c, const double *b, double *x) { return vcycle(c, c->nlev - 1, b, x); }
+int orc_vcycle_level(OCtx *c, int l, const double *b, double *x) { return vcycle(c, l, b, x); }
+
+/* right-preconditioned GMRES (R-gmres). hist[k] = |g_{k}| estimate, k = 0..its */
+int orc_gmres(OCtx *c, const double *b, double *x, double rtol, double atol, int maxit, int *its_out,
+              double *hist) {
+    OLevel *L = &c->lv[c->nlev - 1];
+    i64 n = L->s.n;
+    double beta = 0;
+    for (i64 i = 0; i < n; i++) beta += b[i] * b[i];
+    beta = sqrt(beta);
+    double tol = rtol * beta > atol ? rtol * beta : atol;
+    for (i64 i = 0; i < n; i++) x[i] = 0.0;
+    hist[0] = beta;
+    *its_out = 0;
+    if (beta <= tol) return 0;
+    double *V = malloc(sizeof(double) * n * (maxit + 1));
+    double *Z = malloc(sizeof(double) * n * maxit);
+    double *H = calloc((size_t)(maxit + 1) * maxit, sizeof(double));
+    double *cs = malloc(sizeof(double) * maxit), *sn = malloc(sizeof(double) * maxit);
+    double *g = calloc((size_t)maxit + 1, sizeof(double));
+    double *w = malloc(sizeof(double) * n);
+    for (i64 i = 0; i < n; i++) V[i] = b[i] / beta;
+    g[0] = beta;
+    int k, conv = 0;
+    for (k = 0; k < maxit; k++) {
+        if (vcycle(c, c->nlev - 1, V + k * n, Z + k * n)) { k = -1; break; }
+        orc_spmv(c, c->nlev - 1, Z + k * n, w);
+        for (int i = 0; i <= k; i++) {
+            double h = 0;
+            for (i64 t = 0; t < n; t++) h += w[t] * V[i * n + t];
+            H[i * maxit + k] = h;
+            for (i64 t = 0; t < n; t++) w[t] -= h * V[i * n + t];
+        }
+        double hn = 0;
+        for (i64 t = 0; t < n; t++) hn += w[t] * w[t];
+        hn = sqrt(hn);
+        H[(k + 1) * maxit + k] = hn;
+        for (i64 t = 0; t < n; t++) V[(k + 1) * n + t] = hn > 0 ? w[t] / hn : 0.0;
+        for (int i = 0; i < k; i++) {
+            double a = H[i * maxit + k], bb = H[(i + 1) * maxit + k];
+            H[i * maxit + k] = cs[i] * a + sn[i] * bb;
+            H[(i + 1) * maxit + k] = -sn[i] * a + cs[i] * bb;
+        }
+        double a = H[k * maxit + k], bb = H[(k + 1) * maxit + k];
+        double rr = sqrt(a * a + bb * bb);
+        cs[k] = a / rr; sn[k] = bb / rr;
+        H[k * maxit + k] = rr; H[(k + 1) * maxit + k] = 0;
+        g[k + 1] = -sn[k] * g[k];
+        g[k] = cs[k] * g[k];
+        hist[k + 1] = fabs(g[k + 1]);
+        if (fabs(g[k + 1]) <= tol) { k++; conv = 1; break; }
+    }
+    int st = 0;
+    if (k < 0) st = 2;
+    else {
+        double *yv = malloc(sizeof(double) * (k > 0 ? k : 1));
+        for (int i = k - 1; i >= 0; i--) {
+            double sacc = g[i];
+            for (int j = i + 1; j < k; j++) sacc -= H[i * maxit + j] * yv[j];
+            yv[i] = sacc / H[i * maxit + i];
+        }
+        for (int i = 0; i < k; i++)
+            for (i64 t = 0; t < n; t++) x[t] += yv[i] * Z[i * n + t];
+        free(yv);
+        *its_out = k;
+        if (!conv) st = 1;
+    }
+    free(V); free(Z); free(H); free(cs); free(sn); free(g); free(w);
+    return st;
+}
+
+/* manufactured-solution helpers: quadrature points/weights of every cell, load
+ * vector (f, phi_i) and evaluation of a discrete field at those points */
+int orc_quad_info(const OCtx *c, int l, i64 *out) {
+    const OLevel *L = &c->lv[l];
+    out[0] = L->m.nc * oa_nq(L->m.dim); out[1] = oa_ncomp(&L->s);
+    return 0;
+}
+int orc_quadrature(const OCtx *c, int l, double *pts, double *wts) {
+    oa_quadrature(&c->lv[l].m, pts, wts);
+    return 0;
+}
+int orc_load(const OCtx *c, int l, const double *fv, double *out) {
+    oa_load(&c->lv[l].m, &c->lv[l].s, fv, out);
+    return 0;
+}
+int orc_eval(const OCtx *c, int l, const double *coef, double *fv) {
+    oa_eval(&c->lv[l].m, &c->lv[l].s, coef, fv);
+    return 0;
+}
+
+double orc_duality_error(const OCtx *c, int l) { return oa_duality_error(&c->lv[l].m, &c->lv[l].s); }
+
+/* TEST HOOK: replace level l's subspace decomposition by the given one (ascending
+ * DoF lists); used to pin the sweep machinery against special decompositions
+ * (e.g. one patch covering every DoF => one sweep from zero is the direct solve). */
+int orc_set_patches(OCtx *c, int l, i64 np, const i64 *ptr, const int *dofs) {
+    OLevel *L = &c->lv[l];
+    if (L->lu) {
+        for (i64 i = 0; i < L->pt.np; i++) { free(L->lu[i]); free(L->perm[i]); }
+        free(L->lu); free(L->perm); L->lu = NULL; L->perm = NULL;
+    }
+    i64 n = L->s.n, used = ptr[np];
+    OPatches *pt = &L->pt;
+    opt_free(pt);
+    pt->np = np;
+    pt->vert = calloc((size_t)np + 1, sizeof(int));
+    pt->ptr = malloc(sizeof(i64) * (np + 1));
+    memcpy(pt->ptr, ptr, sizeof(i64) * (np + 1));
+    pt->dofs = malloc(sizeof(int) * (used ? used : 1));
+    memcpy(pt->dofs, dofs, sizeof(int) * used);
+    pt->mult = calloc((size_t)n, sizeof(int));
+    for (i64 t = 0; t < used; t++) pt->mult[dofs[t]]++;
+    pt->dptr = calloc((size_t)n + 1, sizeof(i64));
+    for (i64 d = 0; d < n; d++) pt->dptr[d + 1] = pt->dptr[d] + pt->mult[d];
+    pt->dslot = malloc(sizeof(i64) * (used ? used : 1));
+    i64 *f2 = calloc((size_t)n, sizeof(i64));
+    for (i64 t = 0; t < used; t++) { int d = dofs[t]; pt->dslot[pt->dptr[d] + f2[d]++] = t; }
+    free(f2);
+    return 0;
+}
+
+/* dense LU (R-lu) of a row-major n x n matrix and one solve; returns od_lu's status */
+int orc_dense_lu_solve(int n, const double *a, const double *b, double *x, double *lu_out, int *perm_out) {
+    double amax = 0;
+    for (i64 t = 0; t < (i64)n * n; t++) { lu_out[t] = a[t]; if (fabs(a[t]) > amax) amax = fabs(a[t]); }
+    int st = od_lu(lu_out, n, perm_out, amax);
+    if (!st) od_lu_solve(lu_out, n, perm_out, b, x);
+    return st;
+}

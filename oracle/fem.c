@@ -1,0 +1,927 @@
+/*
+ * fem.c -- ORACLE (test infrastructure only; see orc.h).
+ *
+ * Finite-element bases, quadrature and assembly of the two operators whose
+ * multigrid relaxation is the hot path:
+ *
+ *  E-B block  S~(u,p) = [[M_E, G~ - (1/Rem) A], [A^T, C]]
+ *      (M_E)_ij = (phi_j, phi_i)          G~_ik = (w x psi_k, phi_i)
+ *      A_ik     = (psi_k, vcurl phi_i)    (A^T)_ki = (vcurl phi_i, psi_k)
+ *      C_kl     = (1/Rem)(div psi_l, div psi_k)                   Table 1
+ *      2D conventions vcurl E = (d_y E, -d_x E), u x B = u1 B2 - u2 B1
+ *
+ *  AL velocity block (reading R-vel), trial u, test v:
+ *      (2/Re)(eps u, eps v)_K  + SIPG  a_h^DG
+ *      + gamma (div u, div v)
+ *      - (u, div(v (x) w))_K + upwind facet terms c_h^DG (w = advecting field) P:210-216
+ *
+ * Bases are the dual bases of the DoF functionals of reading R-basis (SURVEY
+ * §8c.2): CG1 nodal; NED1 Whitney (int_e E.t = 1); RT1 Whitney (int_f B.n = 1);
+ * BDM1 flux-nodal (|f| (u.n_f)(x_a) = 1).  Each local basis function is affine and
+ * stored as value at the first cell vertex plus its constant gradient.
+ *
+ * Integration: cell integrals with a collapsed (Duffy) 4x4(x4) Gauss-Legendre
+ * rule (exact for degree <= 5 in 3D, <= 6 in 2D; all cell integrands here have
+ * degree <= 2).  Facet integrals with a 3-point (2D) / collapsed 3x3 (3D)
+ * Gauss-Legendre rule (exact for degree <= 5 / 4; facet integrands have degree
+ * <= 2 because the advecting field w_h is constant per cell, reading R-w).
+ * The grad-div / div-div parts are the exact closed form of reading R-gamma:
+ * div of an RT/BDM basis function on K is s/(d|K|) (RT: s/|K|), so those entries
+ * equal (G * m) / d^2 with G = gamma/|K| and m an integer sum of orientation signs.
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#include "orc.h"
+
+/* ------------------------------------------------------------------------- */
+/* geometry                                                                   */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+    int dim;
+    double X[4][3];     /* vertices (ascending global id)   */
+    double Ji[3][3];    /* inverse Jacobian                  */
+    double det, vol;
+    double g[4][3];     /* gradients of barycentric coords   */
+} Cell;
+
+typedef struct { double v0[3]; double G[3][3]; } Aff;  /* f(x) = v0 + G (x - X0) */
+
+/* geometry of the simplex with vertices X (ascending global id) */
+static void cell_geom_from(int d, const double X[4][3], Cell *K) {
+    memset(K, 0, sizeof(*K));
+    K->dim = d;
+    memcpy(K->X, X, sizeof(K->X));
+    double J[3][3] = {{0}};
+    for (int r = 0; r < d; r++)
+        for (int col = 0; col < d; col++) J[r][col] = K->X[col + 1][r] - K->X[0][r];
+    if (d == 2) {
+        K->det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        K->Ji[0][0] = J[1][1] / K->det; K->Ji[0][1] = -J[0][1] / K->det;
+        K->Ji[1][0] = -J[1][0] / K->det; K->Ji[1][1] = J[0][0] / K->det;
+        K->vol = fabs(K->det) / 2.0;
+    } else {
+        double co[3][3];
+        co[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+        co[0][1] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+        co[0][2] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+        co[1][0] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+        co[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+        co[1][2] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+        co[2][0] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+        co[2][1] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+        co[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        K->det = J[0][0] * co[0][0] + J[0][1] * co[0][1] + J[0][2] * co[0][2];
+        for (int r = 0; r < 3; r++)
+            for (int col = 0; col < 3; col++) K->Ji[r][col] = co[col][r] / K->det;
+        K->vol = fabs(K->det) / 6.0;
+    }
+    for (int a = 1; a <= d; a++)
+        for (int k = 0; k < d; k++) K->g[a][k] = K->Ji[a - 1][k];
+    for (int k = 0; k < d; k++) {
+        double s = 0;
+        for (int a = 1; a <= d; a++) s += K->g[a][k];
+        K->g[0][k] = -s;
+    }
+}
+
+static void cell_geom(const OMesh *m, i64 c, Cell *K) {
+    int d = m->dim;
+    double X[4][3] = {{0}};
+    for (int a = 0; a <= d; a++)
+        for (int r = 0; r < 3; r++) X[a][r] = m->x[3 * m->cv[c * (d + 1) + a] + r];
+    cell_geom_from(d, X, K);
+}
+
+static void aff_eval(const Aff *f, const Cell *K, const double *x, double *out) {
+    for (int l = 0; l < 3; l++) {
+        double s = f->v0[l];
+        for (int k = 0; k < K->dim; k++) s += f->G[l][k] * (x[k] - K->X[0][k]);
+        out[l] = s;
+    }
+}
+
+static double dot3(const double *a, const double *b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+static void cross3(const double *a, const double *b, double *c) {
+    c[0] = a[1] * b[2] - a[2] * b[1]; c[1] = a[2] * b[0] - a[0] * b[2]; c[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+/* global facet area vector |f| n_f of the facet with ascending vertices P:
+ * 2D edge (a<b): n = (t_y, -t_x) (tangent rotated clockwise);
+ * 3D face (a<b<c): n ~ (x_b - x_a) x (x_c - x_a).         reading R-orient    */
+static void facet_area_vector(int dim, const double P[3][3], double *A) {
+    if (dim == 2) {
+        A[0] = P[1][1] - P[0][1]; A[1] = -(P[1][0] - P[0][0]); A[2] = 0;
+    } else {
+        double u[3], v[3];
+        for (int k = 0; k < 3; k++) { u[k] = P[1][k] - P[0][k]; v[k] = P[2][k] - P[0][k]; }
+        cross3(u, v, A);
+        for (int k = 0; k < 3; k++) A[k] *= 0.5;
+    }
+}
+
+/* Advecting field w_h on cell K (reading R-w): exactly divergence-free, as the
+ * paper requires of u^n ("we exactly enforce div u^n = 0"; BDM u^n).
+ *   2D: w_h = vcurl psi_h, psi_h the CG1 interpolant of the stream function
+ *       (pot = psi at the cell's vertices);
+ *   3D: w_h = curl A_h, A_h the NED1 interpolant of the P1 interpolant of the
+ *       vector potential (pot = A at the cell's vertices): edge circulation
+ *       c_e = (A_i + A_j)/2 . (X_j - X_i), curl(lam_i grad lam_j - lam_j grad lam_i)
+ *       = 2 grad lam_i x grad lam_j.
+ * w_h is constant on K, normal-continuous across facets, and lies in RT_0 in BDM_1. */
+static void cell_wind(const Cell *K, const double pot[4][3], double *wc) {
+    wc[0] = wc[1] = wc[2] = 0.0;
+    if (K->dim == 2) {
+        double gx = 0, gy = 0;
+        for (int a = 0; a < 3; a++) { gx += pot[a][0] * K->g[a][0]; gy += pot[a][0] * K->g[a][1]; }
+        wc[0] = gy; wc[1] = -gx;
+        return;
+    }
+    for (int q = 0; q < 6; q++) {
+        int lv[2];
+        om_edge_local_verts(3, q, lv);
+        int i = lv[0], j = lv[1];
+        double ce = 0;
+        for (int k = 0; k < 3; k++) ce += 0.5 * (pot[i][k] + pot[j][k]) * (K->X[j][k] - K->X[i][k]);
+        double cr[3];
+        cross3(K->g[i], K->g[j], cr);
+        for (int k = 0; k < 3; k++) wc[k] += ce * 2.0 * cr[k];
+    }
+}
+
+static void cell_pot(const OMesh *m, i64 c, const double *pot, double out[4][3]) {
+    int d = m->dim, nc = d == 2 ? 1 : 3;
+    memset(out, 0, sizeof(double) * 12);
+    for (int a = 0; a <= d; a++)
+        for (int k = 0; k < nc; k++) out[a][k] = pot[(i64)m->cv[c * (d + 1) + a] * nc + k];
+}
+
+/* ------------------------------------------------------------------------- */
+/* local bases (dual to the DoF functionals of R-basis)                        */
+/* ------------------------------------------------------------------------- */
+static Aff basis_cg1(const Cell *K, int a) {
+    Aff f; memset(&f, 0, sizeof(f));
+    f.v0[0] = a == 0 ? 1.0 : 0.0;
+    for (int k = 0; k < K->dim; k++) f.G[0][k] = K->g[a][k];
+    return f;
+}
+
+/* Whitney edge function lam_i grad lam_j - lam_j grad lam_i, local i < j */
+static Aff basis_ned1(const Cell *K, int i, int j) {
+    Aff f; memset(&f, 0, sizeof(f));
+    for (int l = 0; l < 3; l++) {
+        f.v0[l] = (i == 0 ? K->g[j][l] : 0.0) - (j == 0 ? K->g[i][l] : 0.0);
+        for (int k = 0; k < 3; k++) f.G[l][k] = K->g[j][l] * K->g[i][k] - K->g[i][l] * K->g[j][k];
+    }
+    return f;
+}
+
+/* orientation sign of local facet q: +1 if the global facet normal points out of K */
+static double facet_sign(const Cell *K, int q, const double A[3]) {
+    int d = K->dim, opp = om_facet_opp(d, q), lv[3];
+    om_facet_local_verts(d, q, lv);
+    double t[3];
+    for (int k = 0; k < 3; k++) t[k] = K->X[lv[0]][k] - K->X[opp][k];
+    return dot3(A, t) > 0 ? 1.0 : -1.0;
+}
+
+static void facet_points(const Cell *K, int q, double P[3][3]) {
+    int lv[3];
+    om_facet_local_verts(K->dim, q, lv);
+    memset(P, 0, sizeof(double) * 9);
+    for (int a = 0; a < K->dim; a++)
+        for (int k = 0; k < 3; k++) P[a][k] = K->X[lv[a]][k];
+}
+
+/* RT1: s (x - X_opp) / (d |K|)  (flux 1 through facet q along its global normal) */
+static Aff basis_rt(const Cell *K, int q, double *sign) {
+    Aff f; memset(&f, 0, sizeof(f));
+    double P[3][3], A[3];
+    facet_points(K, q, P);
+    facet_area_vector(K->dim, P, A);
+    double s = facet_sign(K, q, A);
+    int opp = om_facet_opp(K->dim, q);
+    double c = s / (K->dim * K->vol);
+    for (int l = 0; l < 3; l++) {
+        f.v0[l] = c * (K->X[0][l] - K->X[opp][l]);
+        for (int k = 0; k < 3; k++) f.G[l][k] = (l == k && l < K->dim) ? c : 0.0;
+    }
+    *sign = s;
+    return f;
+}
+
+/* BDM1 flux-nodal: lam_a psi, psi orthogonal to the normals of the other facets
+ * through vertex a, scaled so that psi . (|f| n_f) = 1.                         */
+static Aff basis_bdm(const Cell *K, int q, int ia, double *sign) {
+    Aff f; memset(&f, 0, sizeof(f));
+    int d = K->dim, lv[3];
+    om_facet_local_verts(d, q, lv);
+    double P[3][3], A[3], dir[3] = {0, 0, 0};
+    facet_points(K, q, P);
+    facet_area_vector(d, P, A);
+    int a = lv[ia];
+    if (d == 2) {
+        int b = lv[1 - ia];
+        dir[0] = -K->g[b][1]; dir[1] = K->g[b][0];
+    } else {
+        int b = lv[(ia + 1) % 3], c = lv[(ia + 2) % 3];
+        cross3(K->g[b], K->g[c], dir);
+    }
+    double sc = 1.0 / dot3(dir, A);
+    double psi[3] = {dir[0] * sc, dir[1] * sc, dir[2] * sc};
+    for (int l = 0; l < 3; l++) {
+        f.v0[l] = (a == 0 ? 1.0 : 0.0) * psi[l];
+        for (int k = 0; k < 3; k++) f.G[l][k] = k < d ? psi[l] * K->g[a][k] : 0.0;
+    }
+    *sign = facet_sign(K, q, A);
+    return f;
+}
+
+/* ------------------------------------------------------------------------- */
+/* quadrature                                                                  */
+/* ------------------------------------------------------------------------- */
+static void gauss01(int q, double *x, double *w) {
+    if (q == 3) {
+        double r = 0.5 * sqrt(0.6);
+        x[0] = 0.5 - r; x[1] = 0.5; x[2] = 0.5 + r;
+        w[0] = 5.0 / 18.0; w[1] = 8.0 / 18.0; w[2] = 5.0 / 18.0;
+    } else { /* q == 4 */
+        double a = sqrt(3.0 / 7.0 - 2.0 / 7.0 * sqrt(6.0 / 5.0));
+        double b = sqrt(3.0 / 7.0 + 2.0 / 7.0 * sqrt(6.0 / 5.0));
+        double wa = (18.0 + sqrt(30.0)) / 36.0, wb = (18.0 - sqrt(30.0)) / 36.0;
+        x[0] = 0.5 * (1 - b); x[1] = 0.5 * (1 - a); x[2] = 0.5 * (1 + a); x[3] = 0.5 * (1 + b);
+        w[0] = 0.5 * wb; w[1] = 0.5 * wa; w[2] = 0.5 * wa; w[3] = 0.5 * wb;
+    }
+}
+
+/* collapsed Gauss rule on the cell: fills points (physical) and weights (physical) */
+static int cell_rule(const Cell *K, double (*xq)[3], double *wq) {
+    double g[4], w[4];
+    gauss01(4, g, w);
+    int n = 0;
+    if (K->dim == 2) {
+        for (int i = 0; i < 4; i++)
+            for (int j = 0; j < 4; j++) {
+                double xi1 = g[i] * (1 - g[j]), xi2 = g[j];
+                double wt = w[i] * w[j] * (1 - g[j]) * fabs(K->det);
+                for (int k = 0; k < 3; k++)
+                    xq[n][k] = K->X[0][k] + xi1 * (K->X[1][k] - K->X[0][k]) + xi2 * (K->X[2][k] - K->X[0][k]);
+                wq[n++] = wt;
+            }
+    } else {
+        for (int i = 0; i < 4; i++)
+            for (int j = 0; j < 4; j++)
+                for (int l = 0; l < 4; l++) {
+                    double xi1 = g[i] * (1 - g[j]) * (1 - g[l]), xi2 = g[j] * (1 - g[l]), xi3 = g[l];
+                    double wt = w[i] * w[j] * w[l] * (1 - g[j]) * (1 - g[l]) * (1 - g[l]) * fabs(K->det);
+                    for (int k = 0; k < 3; k++)
+                        xq[n][k] = K->X[0][k] + xi1 * (K->X[1][k] - K->X[0][k]) + xi2 * (K->X[2][k] - K->X[0][k]) +
+                                   xi3 * (K->X[3][k] - K->X[0][k]);
+                    wq[n++] = wt;
+                }
+    }
+    return n;
+}
+
+/* pinned facet rule (R-quad) on the facet with ascending vertices P */
+static int facet_rule(int dim, const double P[3][3], double (*xq)[3], double *wq) {
+    double g[3], w[3];
+    gauss01(3, g, w);
+    int n = 0;
+    if (dim == 2) {
+        double t[3] = {P[1][0] - P[0][0], P[1][1] - P[0][1], 0};
+        double len = sqrt(dot3(t, t));
+        for (int i = 0; i < 3; i++) {
+            for (int k = 0; k < 3; k++) xq[n][k] = P[0][k] + g[i] * t[k];
+            wq[n++] = w[i] * len;
+        }
+    } else {
+        double A[3];
+        facet_area_vector(3, P, A);
+        double area = sqrt(dot3(A, A));
+        for (int i = 0; i < 3; i++)
+            for (int j = 0; j < 3; j++) {
+                double xi1 = g[i] * (1 - g[j]), xi2 = g[j];
+                for (int k = 0; k < 3; k++)
+                    xq[n][k] = P[0][k] + xi1 * (P[1][k] - P[0][k]) + xi2 * (P[2][k] - P[0][k]);
+                wq[n++] = w[i] * w[j] * (1 - g[j]) * 2.0 * area;
+            }
+    }
+    return n;
+}
+
+/* ------------------------------------------------------------------------- */
+/* CSR helpers and sparsity                                                   */
+/* ------------------------------------------------------------------------- */
+void oc_free(OCsr *a) { free(a->rp); free(a->ci); free(a->v); memset(a, 0, sizeof(*a)); }
+
+i64 oc_find(const OCsr *a, i64 row, int col) {
+    i64 lo = a->rp[row], hi = a->rp[row + 1] - 1;
+    while (lo <= hi) {
+        i64 mid = (lo + hi) / 2;
+        if (a->ci[mid] == col) return mid;
+        if (a->ci[mid] < col) lo = mid + 1; else hi = mid - 1;
+    }
+    return -1;
+}
+
+/* free DoFs (with -1 for constrained) of the local basis of cell c, in local order */
+static int cell_dofs(const OMesh *m, const OSpace *s, i64 c, int *out) {
+    int d = m->dim, n = 0;
+    if (s->block == ORC_EB) {
+        if (d == 2) for (int a = 0; a < 3; a++) out[n++] = s->vdof[m->cv[c * 3 + a]];
+        else for (int q = 0; q < 6; q++) out[n++] = s->edof[m->ce[c * 6 + q]];
+        for (int q = 0; q <= d; q++) out[n++] = s->fdof[om_facet_of_cell(m, c, q)];
+    } else {
+        for (int q = 0; q <= d; q++) {
+            int f0 = s->fdof[om_facet_of_cell(m, c, q)];
+            for (int a = 0; a < d; a++) out[n++] = f0 < 0 ? -1 : f0 + a;
+        }
+    }
+    return n;
+}
+
+static int cmp_int(const void *a, const void *b) {
+    int x = *(const int *)a, y = *(const int *)b;
+    return x < y ? -1 : x > y;
+}
+
+/* Sparsity: DoFs i, j couple iff their basis functions share a cell (E-B), or
+ * share a cell or the two cells of one facet (DG velocity).          */
+static void build_pattern(OCsr *A, const OMesh *m, const OSpace *s) {
+    i64 n = s->n;
+    int ld[32];
+    i64 *sp = calloc((size_t)n + 1, sizeof(i64));
+    for (i64 c = 0; c < m->nc; c++) {
+        int k = cell_dofs(m, s, c, ld);
+        for (int t = 0; t < k; t++) if (ld[t] >= 0) sp[ld[t] + 1]++;
+    }
+    for (i64 d = 0; d < n; d++) sp[d + 1] += sp[d];
+    int *sc = malloc(sizeof(int) * (sp[n] ? sp[n] : 1));
+    i64 *fill = calloc((size_t)n, sizeof(i64));
+    for (i64 c = 0; c < m->nc; c++) {
+        int k = cell_dofs(m, s, c, ld);
+        for (int t = 0; t < k; t++) if (ld[t] >= 0) sc[sp[ld[t]] + fill[ld[t]]++] = (int)c;
+    }
+    free(fill);
+    A->n = n;
+    A->rp = malloc(sizeof(i64) * (n + 1));
+    A->rp[0] = 0;
+    i64 cap = n * 16 + 16, used = 0;
+    A->ci = malloc(sizeof(int) * cap);
+    int *buf = malloc(sizeof(int) * 8192);
+    for (i64 d = 0; d < n; d++) {
+        int nb = 0;
+        for (i64 t = sp[d]; t < sp[d + 1]; t++) {
+            int cells[5], ncell = 0;
+            i64 c = sc[t];
+            cells[ncell++] = (int)c;
+            if (s->block == ORC_VEL)
+                for (int q = 0; q <= m->dim; q++) {
+                    int f = om_facet_of_cell(m, c, q);
+                    int o = m->fcell[2 * f] == c ? m->fcell[2 * f + 1] : m->fcell[2 * f];
+                    if (o >= 0) cells[ncell++] = o;
+                }
+            for (int u = 0; u < ncell; u++) {
+                int k = cell_dofs(m, s, cells[u], ld);
+                for (int v = 0; v < k; v++) if (ld[v] >= 0) buf[nb++] = ld[v];
+            }
+        }
+        qsort(buf, (size_t)nb, sizeof(int), cmp_int);
+        int nu = 0;
+        for (int u = 0; u < nb; u++) if (u == 0 || buf[u] != buf[u - 1]) buf[nu++] = buf[u];
+        while (used + nu > cap) { cap *= 2; A->ci = realloc(A->ci, sizeof(int) * cap); }
+        memcpy(A->ci + used, buf, sizeof(int) * nu);
+        used += nu;
+        A->rp[d + 1] = used;
+    }
+    A->nnz = used;
+    A->ci = realloc(A->ci, sizeof(int) * (used ? used : 1));
+    A->v = calloc((size_t)(used ? used : 1), sizeof(double));
+    free(buf); free(sp); free(sc);
+}
+
+static void scatter(OCsr *A, const int *gi, int ni, const int *gj, int nj, const double *loc, int ldl) {
+    for (int i = 0; i < ni; i++) {
+        if (gi[i] < 0) continue;
+        for (int j = 0; j < nj; j++) {
+            if (gj[j] < 0) continue;
+            i64 p = oc_find(A, gi[i], gj[j]);
+            A->v[p] += loc[i * ldl + j];
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* E-B block  (Table 1)                       */
+/* ------------------------------------------------------------------------- */
+static void assemble_eb(OCsr *A, signed char *cnt, const OMesh *m, const OSpace *s, const OParams *p,
+                        const double *w) {
+    int d = m->dim, nEl = d == 2 ? 3 : 6, nBl = d + 1;
+    double xq[64][3], wq[64];
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        Aff E[6], B[4];
+        double sB[4];
+        int gE[6], gB[4];
+        for (int a = 0; a < nEl; a++) {
+            if (d == 2) { E[a] = basis_cg1(&K, a); gE[a] = s->vdof[m->cv[c * 3 + a]]; }
+            else {
+                int lv[2];
+                om_edge_local_verts(3, a, lv);
+                E[a] = basis_ned1(&K, lv[0], lv[1]);
+                gE[a] = s->edof[m->ce[c * 6 + a]];
+            }
+        }
+        for (int q = 0; q < nBl; q++) { B[q] = basis_rt(&K, q, &sB[q]); gB[q] = s->fdof[om_facet_of_cell(m, c, q)]; }
+        /* vcurl / curl of the E basis (constant) */
+        double curlE[6][3];
+        for (int a = 0; a < nEl; a++) {
+            if (d == 2) { curlE[a][0] = E[a].G[0][1]; curlE[a][1] = -E[a].G[0][0]; curlE[a][2] = 0; }
+            else {
+                curlE[a][0] = E[a].G[2][1] - E[a].G[1][2];
+                curlE[a][1] = E[a].G[0][2] - E[a].G[2][0];
+                curlE[a][2] = E[a].G[1][0] - E[a].G[0][1];
+            }
+        }
+        double pot[4][3], wx[3];
+        cell_pot(m, c, w, pot);
+        cell_wind(&K, pot, wx);
+        double EE[6 * 6] = {0}, EB[6 * 4] = {0}, BE[4 * 6] = {0};
+        int nq = cell_rule(&K, xq, wq);
+        for (int t = 0; t < nq; t++) {
+            double ev[6][3], bv[4][3];
+            for (int a = 0; a < nEl; a++) aff_eval(&E[a], &K, xq[t], ev[a]);
+            for (int q = 0; q < nBl; q++) aff_eval(&B[q], &K, xq[t], bv[q]);
+            for (int i = 0; i < nEl; i++) {
+                for (int j = 0; j < nEl; j++)
+                    EE[i * 6 + j] += wq[t] * (d == 2 ? ev[j][0] * ev[i][0] : dot3(ev[j], ev[i]));
+                for (int k = 0; k < nBl; k++) {
+                    double wxb;
+                    if (d == 2) wxb = (wx[0] * bv[k][1] - wx[1] * bv[k][0]) * ev[i][0];
+                    else { double cr[3]; cross3(wx, bv[k], cr); wxb = dot3(cr, ev[i]); }
+                    double ab = dot3(bv[k], curlE[i]);
+                    EB[i * 4 + k] += wq[t] * (wxb - ab / p->Rem);
+                    BE[k * 6 + i] += wq[t] * ab;
+                }
+            }
+        }
+        scatter(A, gE, nEl, gE, nEl, EE, 6);
+        scatter(A, gE, nEl, gB, nBl, EB, 4);
+        scatter(A, gB, nBl, gE, nEl, BE, 6);
+        for (int k = 0; k < nBl; k++)
+            for (int l = 0; l < nBl; l++)
+                if (gB[k] >= 0 && gB[l] >= 0) cnt[oc_find(A, gB[k], gB[l])] += (signed char)(sB[k] * sB[l]);
+    }
+    /* C = (1/Rem)(div psi_l, div psi_k), div psi = s/|K|: exact value (Kinv*m)/Rem (R-gamma) */
+    double Kinv = d == 2 ? 2.0 * m->N * m->N : 6.0 * m->N * m->N * m->N;
+    for (i64 t = 0; t < A->nnz; t++)
+        if (cnt[t]) A->v[t] += (Kinv * cnt[t]) / p->Rem;
+}
+
+/* ------------------------------------------------------------------------- */
+/* AL velocity block (R-vel)                                                  */
+/* ------------------------------------------------------------------------- */
+static int vel_basis(const OMesh *m, const OSpace *s, i64 c, const Cell *K, Aff *F, double *sg, int *gi) {
+    int d = m->dim, n = 0;
+    for (int q = 0; q <= d; q++) {
+        int f0 = s->fdof[om_facet_of_cell(m, c, q)];
+        for (int a = 0; a < d; a++) {
+            double sgn;
+            F[n] = basis_bdm(K, q, a, &sgn);
+            if (sg) sg[n] = sgn;
+            gi[n] = f0 < 0 ? -1 : f0 + a;
+            n++;
+        }
+    }
+    return n;
+}
+
+static void sym_grad(const Aff *f, double e[3][3]) {
+    for (int l = 0; l < 3; l++) for (int k = 0; k < 3; k++) e[l][k] = 0.5 * (f->G[l][k] + f->G[k][l]);
+}
+
+static void assemble_vel(OCsr *A, signed char *cnt, const OMesh *m, const OSpace *s, const OParams *p,
+                         const double *w, const unsigned char *cmask) {
+    int d = m->dim;
+    double xq[64][3], wq[64];
+    const double nu2 = 2.0 / p->Re;
+    /* cell terms */
+    for (i64 c = 0; c < m->nc; c++) {
+        if (cmask && !cmask[c]) continue;
+        Cell K;
+        cell_geom(m, c, &K);
+        Aff F[12];
+        double sg[12];
+        int gi[12];
+        int nb = vel_basis(m, s, c, &K, F, sg, gi);
+        double eps[12][3][3];
+        for (int a = 0; a < nb; a++) sym_grad(&F[a], eps[a]);
+        double pot[4][3], wx[3];
+        cell_pot(m, c, w, pot);
+        cell_wind(&K, pot, wx);      /* constant on K, div w_h = 0 */
+        double loc[12 * 12] = {0};
+        int nq = cell_rule(&K, xq, wq);
+        for (int t = 0; t < nq; t++) {
+            double fv[12][3];
+            for (int a = 0; a < nb; a++) aff_eval(&F[a], &K, xq[t], fv[a]);
+            for (int i = 0; i < nb; i++) {
+                /* div(v (x) w)_l = sum_k (d_k v_l) w_k + v_l div w, div w_h = 0  (v = test fn i) */
+                double dvw[3];
+                for (int l = 0; l < 3; l++) {
+                    double sacc = 0.0;
+                    for (int k = 0; k < d; k++) sacc += F[i].G[l][k] * wx[k];
+                    dvw[l] = sacc;
+                }
+                for (int j = 0; j < nb; j++) {
+                    double ee = 0;
+                    for (int l = 0; l < 3; l++) for (int k = 0; k < 3; k++) ee += eps[j][l][k] * eps[i][l][k];
+                    loc[i * 12 + j] += wq[t] * (nu2 * ee - dot3(fv[j], dvw));
+                }
+            }
+        }
+        scatter(A, gi, nb, gi, nb, loc, 12);
+        for (int i = 0; i < nb; i++)
+            for (int j = 0; j < nb; j++)
+                if (gi[i] >= 0 && gi[j] >= 0) cnt[oc_find(A, gi[i], gi[j])] += (signed char)(sg[i] * sg[j]);
+    }
+    /* facet terms: SIPG + upwind (reading R-vel) */
+    for (i64 f = 0; f < m->nfacet; f++) {
+        int cp = m->fcell[2 * f], cm = m->fcell[2 * f + 1];
+        if (cmask && !cmask[cp] && !(cm >= 0 && cmask[cm])) continue;
+        int interior = cm >= 0;
+        Cell Kp, Km;
+        Aff F[24];
+        double sg[24];
+        int gi[24], side[24];
+        cell_geom(m, cp, &Kp);
+        int nb = vel_basis(m, s, cp, &Kp, F, sg, gi);
+        for (int a = 0; a < nb; a++) side[a] = +1;
+        if (interior) {
+            cell_geom(m, cm, &Km);
+            int nb2 = vel_basis(m, s, cm, &Km, F + nb, sg + nb, gi + nb);
+            for (int a = nb; a < nb + nb2; a++) side[a] = -1;
+            nb += nb2;
+        }
+        /* facet vertices (ascending global id) and K+'s outward unit normal */
+        int qf = -1;
+        for (int q = 0; q <= d; q++) if (om_facet_of_cell(m, cp, q) == f) qf = q;
+        double P[3][3], Av[3];
+        facet_points(&Kp, qf, P);
+        facet_area_vector(d, P, Av);
+        double an = sqrt(dot3(Av, Av)), n[3];
+        double sgn = facet_sign(&Kp, qf, Av);
+        for (int k = 0; k < 3; k++) n[k] = sgn * Av[k] / an;
+        double hF;
+        if (d == 2) hF = an;
+        else {
+            hF = 0;
+            for (int a = 0; a < 3; a++)
+                for (int b = a + 1; b < 3; b++) {
+                    double t[3] = {P[b][0] - P[a][0], P[b][1] - P[a][1], P[b][2] - P[a][2]};
+                    double l = sqrt(dot3(t, t));
+                    if (l > hF) hF = l;
+                }
+        }
+        double avg = interior ? 0.5 : 1.0;
+        double pen = (1.0 / p->Re) * (p->sigma / hF);
+        double pot[4][3], wx[3];
+        cell_pot(m, cp, w, pot);
+        cell_wind(&Kp, pot, wx);     /* w_h . n is continuous; K+'s value is used (R-w) */
+        double wn = dot3(wx, n), awn = fabs(wn);
+        double epsn[24][3];
+        for (int a = 0; a < nb; a++) {
+            double e[3][3];
+            sym_grad(&F[a], e);
+            for (int l = 0; l < 3; l++) epsn[a][l] = e[l][0] * n[0] + e[l][1] * n[1] + e[l][2] * n[2];
+        }
+        static double loc[24 * 24];
+        memset(loc, 0, sizeof(loc));
+        int nq = facet_rule(d, P, xq, wq);
+        for (int t = 0; t < nq; t++) {
+            double fv[24][3];
+            for (int a = 0; a < nb; a++) aff_eval(&F[a], side[a] > 0 ? &Kp : &Km, xq[t], fv[a]);
+            for (int i = 0; i < nb; i++) {
+                double Ji = side[i];
+                for (int j = 0; j < nb; j++) {
+                    double Jj = side[j];
+                    double vv = dot3(fv[j], fv[i]);
+                    double t1 = -nu2 * avg * dot3(epsn[j], fv[i]) * Ji;
+                    double t2 = -nu2 * avg * dot3(fv[j], epsn[i]) * Jj;
+                    double t3 = pen * Jj * Ji * vv;
+                    double up;
+                    if (interior) up = (side[j] > 0 ? 0.5 * (wn + awn) : -0.5 * (-wn + awn)) * vv * Ji;
+                    else up = 0.5 * (wn + awn) * vv;
+                    loc[i * 24 + j] += wq[t] * (t1 + t2 + t3 + up);
+                }
+            }
+        }
+        scatter(A, gi, nb, gi, nb, loc, 24);
+    }
+    /* gamma (div u, div v): div phi_{f,a} = s/(d|K|); exact value (G m)/d^2, G = gamma/|K| (R-gamma) */
+    double Kinv = d == 2 ? 2.0 * m->N * m->N : 6.0 * m->N * m->N * m->N;
+    double G = p->gamma * Kinv;
+    for (i64 t = 0; t < A->nnz; t++)
+        if (cnt[t]) A->v[t] += (G * cnt[t]) / (double)(d * d);
+}
+
+int oa_assemble_masked(OCsr *A, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
+                       const unsigned char *cmask) {
+    build_pattern(A, m, s);
+    signed char *cnt = calloc((size_t)(A->nnz ? A->nnz : 1), 1);
+    if (s->block == ORC_EB) assemble_eb(A, cnt, m, s, p, w);
+    else assemble_vel(A, cnt, m, s, p, w, cmask);
+    free(cnt);
+    return 0;
+}
+
+int oa_assemble(OCsr *A, const OMesh *m, const OSpace *s, const OParams *p, const double *w) {
+    return oa_assemble_masked(A, m, s, p, w, NULL);
+}
+
+/* ------------------------------------------------------------------------- */
+/* prolongation  ("standard prolongation operator induced by the FE     */
+/* discretization"; reading R-prol: (P)_IJ = N_I^fine(phi_J^coarse))           */
+/* Evaluated in integer lattice units of the fine mesh (h_fine = 1, coarse     */
+/* cells have edge 2) so that every entry is an exact dyadic rational.          */
+/* ------------------------------------------------------------------------- */
+static int cmp_ij(const void *a, const void *b) {
+    const long long *x = a, *y = b;
+    if (x[0] != y[0]) return x[0] < y[0] ? -1 : 1;
+    if (x[1] != y[1]) return x[1] < y[1] ? -1 : 1;
+    return 0;
+}
+
+/* coarse parent of fine cell cf: the coarse square/cube containing it, then the
+ * coarse simplex whose coordinate ordering the fine centroid satisfies (R-mesh) */
+static i64 parent_cell(const OMesh *mf, const OMesh *mc, i64 cf) {
+    int d = mf->dim, nvc = d + 1;
+    int csum[3] = {0, 0, 0};
+    for (int a = 0; a < nvc; a++)
+        for (int k = 0; k < d; k++) csum[k] += mf->lat[3 * mf->cv[cf * nvc + a] + k];
+    /* containing coarse square/cube: floor(centroid / 2) */
+    int cc[3] = {0, 0, 0}, rel[3];
+    for (int k = 0; k < d; k++) { cc[k] = csum[k] / (2 * nvc); rel[k] = csum[k] - 2 * nvc * cc[k]; }
+    int Nc = mc->N;
+    if (d == 2) {
+        i64 s = cc[0] + (i64)Nc * cc[1];
+        return rel[0] > rel[1] ? 2 * s : 2 * s + 1;
+    }
+    static const int PERM[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    i64 cube = cc[0] + (i64)Nc * (cc[1] + (i64)Nc * cc[2]);
+    for (int p = 0; p < 6; p++)
+        if (rel[PERM[p][0]] > rel[PERM[p][1]] && rel[PERM[p][1]] > rel[PERM[p][2]]) return 6 * cube + p;
+    return -1;
+}
+
+/* the fine DoF functional N_I (R-basis) applied to an affine field F on cell K;
+ * V holds the nev vertices of the DoF's entity (same units as K) */
+static double dof_functional(int block, int d, int kind, int sub, const double V[3][3], int nev, const Aff *F,
+                             const Cell *K) {
+    double fx[3];
+    if (kind == 0) { aff_eval(F, K, V[0], fx); return fx[0]; }          /* CG1: point value       */
+    if (kind == 1 && d == 3) {                                            /* NED1: int_e phi.t      */
+        double mid[3] = {0.5 * (V[0][0] + V[1][0]), 0.5 * (V[0][1] + V[1][1]), 0.5 * (V[0][2] + V[1][2])};
+        aff_eval(F, K, mid, fx);
+        double t[3] = {V[1][0] - V[0][0], V[1][1] - V[0][1], V[1][2] - V[0][2]};
+        return dot3(fx, t);
+    }
+    double A[3];
+    facet_area_vector(d, V, A);
+    if (block == ORC_VEL) { aff_eval(F, K, V[sub], fx); return dot3(fx, A); }   /* BDM: |f|(phi.n)(x_a) */
+    double sacc = 0;                                                      /* RT: flux of affine field */
+    for (int a = 0; a < nev; a++) { aff_eval(F, K, V[a], fx); sacc += dot3(fx, A); }
+    return sacc / nev;
+}
+
+int op_prolongation(OCsr *P, const OMesh *mf, const OSpace *sf, const OMesh *mc, const OSpace *sc) {
+    int d = mf->dim, nvc = d + 1, nle = om_nle(d);
+    memset(P, 0, sizeof(*P));
+    /* lowest-index fine cell containing each entity */
+    int *vfirst = malloc(sizeof(int) * mf->nv), *efirst = malloc(sizeof(int) * mf->ne),
+        *ffirst = malloc(sizeof(int) * mf->nfacet);
+    for (i64 t = 0; t < mf->nv; t++) vfirst[t] = -1;
+    for (i64 t = 0; t < mf->ne; t++) efirst[t] = -1;
+    for (i64 t = 0; t < mf->nfacet; t++) ffirst[t] = -1;
+    for (i64 c = 0; c < mf->nc; c++) {
+        for (int a = 0; a < nvc; a++) if (vfirst[mf->cv[c * nvc + a]] < 0) vfirst[mf->cv[c * nvc + a]] = (int)c;
+        for (int q = 0; q < nle; q++) if (efirst[mf->ce[c * nle + q]] < 0) efirst[mf->ce[c * nle + q]] = (int)c;
+        for (int q = 0; q < nvc; q++) { int f = om_facet_of_cell(mf, c, q); if (ffirst[f] < 0) ffirst[f] = (int)c; }
+    }
+    i64 cap = 1024, nt = 0;
+    long long *trip = malloc(sizeof(long long) * 2 * cap);
+    double *tv = malloc(sizeof(double) * cap);
+    for (i64 I = 0; I < sf->n; I++) {
+        int kind = sf->dkind[I], ent = sf->dent[I], sub = sf->dsub[I];
+        int cf = kind == 0 ? vfirst[ent] : (kind == 1 ? efirst[ent] : ffirst[ent]);
+        i64 ccell = parent_cell(mf, mc, cf);
+        /* coarse cell geometry in fine lattice units */
+        double X[4][3] = {{0}};
+        for (int a = 0; a < nvc; a++)
+            for (int k = 0; k < d; k++) X[a][k] = 2.0 * mc->lat[3 * mc->cv[ccell * nvc + a] + k];
+        Cell K;
+        cell_geom_from(d, X, &K);
+        /* coarse local basis functions of the same field as DoF I */
+        Aff F[12];
+        int gJ[12], nb = 0;
+        double sgn;
+        if (sf->block == ORC_VEL) {
+            for (int q = 0; q <= d; q++) {
+                int f0 = sc->fdof[om_facet_of_cell(mc, ccell, q)];
+                for (int a = 0; a < d; a++) { F[nb] = basis_bdm(&K, q, a, &sgn); gJ[nb++] = f0 < 0 ? -1 : f0 + a; }
+            }
+        } else if (kind == 2) {
+            for (int q = 0; q <= d; q++) { F[nb] = basis_rt(&K, q, &sgn); gJ[nb++] = sc->fdof[om_facet_of_cell(mc, ccell, q)]; }
+        } else if (d == 2) {
+            for (int a = 0; a < 3; a++) { F[nb] = basis_cg1(&K, a); gJ[nb++] = sc->vdof[mc->cv[ccell * 3 + a]]; }
+        } else {
+            for (int q = 0; q < 6; q++) {
+                int lv[2];
+                om_edge_local_verts(3, q, lv);
+                F[nb] = basis_ned1(&K, lv[0], lv[1]);
+                gJ[nb++] = sc->edof[mc->ce[ccell * 6 + q]];
+            }
+        }
+        /* fine entity vertices (lattice) */
+        double V[3][3] = {{0}};
+        int nev = 0;
+        if (kind == 0) { for (int k = 0; k < d; k++) V[0][k] = mf->lat[3 * ent + k]; nev = 1; }
+        else if (kind == 1 || (kind == 2 && d == 2)) {
+            for (int a = 0; a < 2; a++) for (int k = 0; k < d; k++) V[a][k] = mf->lat[3 * mf->ev[2 * ent + a] + k];
+            nev = 2;
+        } else {
+            for (int a = 0; a < 3; a++) for (int k = 0; k < 3; k++) V[a][k] = mf->lat[3 * mf->fv[3 * ent + a] + k];
+            nev = 3;
+        }
+        for (int b = 0; b < nb; b++) {
+            if (gJ[b] < 0) continue;
+            double val = dof_functional(sf->block, d, kind, sub, V, nev, &F[b], &K);
+            if (val == 0.0) continue;
+            if (nt == cap) { cap *= 2; trip = realloc(trip, sizeof(long long) * 2 * cap); tv = realloc(tv, sizeof(double) * cap); }
+            trip[2 * nt] = I; trip[2 * nt + 1] = gJ[b]; tv[nt] = val; nt++;
+        }
+    }
+    /* sort (I,J) keeping values attached */
+    long long *idx = malloc(sizeof(long long) * 3 * (nt ? nt : 1));
+    for (i64 t = 0; t < nt; t++) { idx[3 * t] = trip[2 * t]; idx[3 * t + 1] = trip[2 * t + 1]; idx[3 * t + 2] = t; }
+    qsort(idx, (size_t)nt, 3 * sizeof(long long), cmp_ij);
+    P->n = sf->n; P->nnz = nt;
+    P->rp = calloc((size_t)sf->n + 1, sizeof(i64));
+    P->ci = malloc(sizeof(int) * (nt ? nt : 1));
+    P->v = malloc(sizeof(double) * (nt ? nt : 1));
+    for (i64 t = 0; t < nt; t++) {
+        P->rp[idx[3 * t] + 1]++;
+        P->ci[t] = (int)idx[3 * t + 1];
+        P->v[t] = tv[idx[3 * t + 2]];
+    }
+    for (i64 I = 0; I < sf->n; I++) P->rp[I + 1] += P->rp[I];
+    free(idx); free(trip); free(tv); free(vfirst); free(efirst); free(ffirst);
+    return 0;
+}
+
+int oc_transpose(OCsr *T, const OCsr *A, i64 ncols) {
+    memset(T, 0, sizeof(*T));
+    T->n = ncols; T->nnz = A->nnz;
+    T->rp = calloc((size_t)ncols + 1, sizeof(i64));
+    T->ci = malloc(sizeof(int) * (A->nnz ? A->nnz : 1));
+    T->v = malloc(sizeof(double) * (A->nnz ? A->nnz : 1));
+    for (i64 t = 0; t < A->nnz; t++) T->rp[A->ci[t] + 1]++;
+    for (i64 j = 0; j < ncols; j++) T->rp[j + 1] += T->rp[j];
+    i64 *fill = calloc((size_t)ncols, sizeof(i64));
+    for (i64 i = 0; i < A->n; i++)            /* ascending rows => each T row ascending */
+        for (i64 t = A->rp[i]; t < A->rp[i + 1]; t++) {
+            int j = A->ci[t];
+            i64 p = T->rp[j] + fill[j]++;
+            T->ci[p] = (int)i; T->v[p] = A->v[t];
+        }
+    free(fill);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* load vectors and field evaluation at the cell quadrature points (used only   */
+/* by the manufactured-solution pins of tests/test_oracle_mms.py)               */
+/* layout per point: E-B 2D [E, B1, B2]; E-B 3D [E1,E2,E3, B1,B2,B3];           */
+/* velocity [u1, .., u_dim]                                                     */
+/* ------------------------------------------------------------------------- */
+static int local_basis(const OMesh *m, const OSpace *s, i64 c, const Cell *K, Aff *F, int *gi, int *off,
+                       int *ncomp) {
+    int d = m->dim, n = 0;
+    double sg;
+    if (s->block == ORC_VEL) {
+        n = vel_basis(m, s, c, K, F, NULL, gi);
+        for (int a = 0; a < n; a++) { off[a] = 0; ncomp[a] = d; }
+        return n;
+    }
+    int nE = d == 2 ? 1 : 3;
+    if (d == 2)
+        for (int a = 0; a < 3; a++) { F[n] = basis_cg1(K, a); gi[n] = s->vdof[m->cv[c * 3 + a]]; off[n] = 0; ncomp[n++] = 1; }
+    else
+        for (int q = 0; q < 6; q++) {
+            int lv[2];
+            om_edge_local_verts(3, q, lv);
+            F[n] = basis_ned1(K, lv[0], lv[1]); gi[n] = s->edof[m->ce[c * 6 + q]]; off[n] = 0; ncomp[n++] = 3;
+        }
+    for (int q = 0; q <= d; q++) {
+        F[n] = basis_rt(K, q, &sg); gi[n] = s->fdof[om_facet_of_cell(m, c, q)]; off[n] = nE; ncomp[n++] = d;
+    }
+    return n;
+}
+
+int oa_ncomp(const OSpace *s) { return s->block == ORC_VEL ? s->dim : (s->dim == 2 ? 3 : 6); }
+int oa_nq(int dim) { return dim == 2 ? 16 : 64; }
+
+void oa_quadrature(const OMesh *m, double *pts, double *wts) {
+    int nq = oa_nq(m->dim);
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        cell_rule(&K, (double(*)[3])(pts + 3 * nq * c), wts + nq * c);
+    }
+}
+
+void oa_load(const OMesh *m, const OSpace *s, const double *fv, double *out) {
+    int nq = oa_nq(m->dim), nc = oa_ncomp(s);
+    double xq[64][3], wq[64];
+    memset(out, 0, sizeof(double) * s->n);
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        Aff F[16];
+        int gi[16], off[16], ncp[16];
+        int nb = local_basis(m, s, c, &K, F, gi, off, ncp);
+        cell_rule(&K, xq, wq);
+        for (int a = 0; a < nb; a++) {
+            if (gi[a] < 0) continue;
+            double acc = 0;
+            for (int t = 0; t < nq; t++) {
+                double v[3];
+                aff_eval(&F[a], &K, xq[t], v);
+                const double *f = fv + ((i64)c * nq + t) * nc + off[a];
+                double dd = 0;
+                for (int k = 0; k < ncp[a]; k++) dd += f[k] * v[k];
+                acc += wq[t] * dd;
+            }
+            out[gi[a]] += acc;
+        }
+    }
+}
+
+void oa_eval(const OMesh *m, const OSpace *s, const double *coef, double *fv) {
+    int nq = oa_nq(m->dim), nc = oa_ncomp(s);
+    double xq[64][3], wq[64];
+    memset(fv, 0, sizeof(double) * m->nc * nq * nc);
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        Aff F[16];
+        int gi[16], off[16], ncp[16];
+        int nb = local_basis(m, s, c, &K, F, gi, off, ncp);
+        cell_rule(&K, xq, wq);
+        for (int a = 0; a < nb; a++) {
+            if (gi[a] < 0) continue;
+            for (int t = 0; t < nq; t++) {
+                double v[3];
+                aff_eval(&F[a], &K, xq[t], v);
+                double *f = fv + ((i64)c * nq + t) * nc + off[a];
+                for (int k = 0; k < ncp[a]; k++) f[k] += coef[gi[a]] * v[k];
+            }
+        }
+    }
+}
+
+/* max |N_i(phi_j) - delta_ij| over the local bases of every cell of the mesh
+ * (DoF duality of R-basis).  Each cell's functionals are applied to
+ * that cell's own basis functions, matched through the global DoF numbering.   */
+double oa_duality_error(const OMesh *m, const OSpace *s) {
+    int d = m->dim;
+    double worst = 0;
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        Aff F[16];
+        int gi[16], off[16], ncp[16];
+        int nb = local_basis(m, s, c, &K, F, gi, off, ncp);
+        for (int i = 0; i < nb; i++) {
+            if (gi[i] < 0) continue;
+            int kind = s->dkind[gi[i]], ent = s->dent[gi[i]], sub = s->dsub[gi[i]], nev;
+            double V[3][3] = {{0}};
+            if (kind == 0) { for (int k = 0; k < 3; k++) V[0][k] = m->x[3 * ent + k]; nev = 1; }
+            else if (kind == 1 || d == 2) {
+                for (int a = 0; a < 2; a++) for (int k = 0; k < 3; k++) V[a][k] = m->x[3 * m->ev[2 * ent + a] + k];
+                nev = 2;
+            } else {
+                for (int a = 0; a < 3; a++) for (int k = 0; k < 3; k++) V[a][k] = m->x[3 * m->fv[3 * ent + a] + k];
+                nev = 3;
+            }
+            for (int j = 0; j < nb; j++) {
+                if (gi[j] < 0 || off[j] != off[i]) continue;
+                double v = dof_functional(s->block, d, kind, sub, V, nev, &F[j], &K);
+                double e = fabs(v - (gi[i] == gi[j] ? 1.0 : 0.0));
+                if (e > worst) worst = e;
+            }
+        }
+    }
+    return worst;
+}

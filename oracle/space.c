@@ -1,0 +1,149 @@
+/*
+ * space.c -- ORACLE (test infrastructure only; see orc.h).
+ *
+ * Free DoFs and vertex-star patches.
+ *   - Spaces: E in CG1 (2D) / NED1_1 (3D), B in RT_1, velocity in
+ *     BDM_1.  Boundary conditions E=0 / E x n = 0, B.n = 0, u.n = 0 imposed
+ *     strongly by removing the constrained DoFs (reading R-bc).
+ *   - Free-DoF order (reading R-num): E-B: free E DoFs in entity order, then free
+ *     B DoFs in facet order.  Velocity: free facets in order, the `dim` DoFs of one
+ *     facet contiguous, ordered by the facet's ascending vertices.
+ *   - Patches (P:567-571 eq. stardecomp): V_i = { v in V_h : supp v subset K_i },
+ *     K_i = the cells sharing vertex i.  One patch per vertex in ascending order,
+ *     empty patches dropped (reading R-patch / SURVEY A1).  A free DoF lies in
+ *     V_i iff its entity contains vertex i.
+ */
+#include <stdlib.h>
+#include <string.h>
+#include "orc.h"
+
+int os_build(OSpace *s, const OMesh *m, int block) {
+    memset(s, 0, sizeof(*s));
+    s->block = block; s->dim = m->dim;
+    s->vdof = malloc(sizeof(int) * m->nv);
+    s->edof = malloc(sizeof(int) * m->ne);
+    s->fdof = malloc(sizeof(int) * m->nfacet);
+    for (i64 v = 0; v < m->nv; v++) s->vdof[v] = -1;
+    for (i64 e = 0; e < m->ne; e++) s->edof[e] = -1;
+    for (i64 f = 0; f < m->nfacet; f++) s->fdof[f] = -1;
+    i64 n = 0;
+    if (block == ORC_EB) {
+        if (m->dim == 2) {
+            for (i64 v = 0; v < m->nv; v++) if (!m->vbnd[v]) s->vdof[v] = (int)n++;
+        } else {
+            for (i64 e = 0; e < m->ne; e++) if (!m->ebnd[e]) s->edof[e] = (int)n++;
+        }
+        s->nE = n;
+        for (i64 f = 0; f < m->nfacet; f++) if (m->fcell[2 * f + 1] >= 0) s->fdof[f] = (int)n++;
+    } else {
+        for (i64 f = 0; f < m->nfacet; f++)
+            if (m->fcell[2 * f + 1] >= 0) { s->fdof[f] = (int)n; n += m->dim; }
+    }
+    s->n = n;
+    s->dkind = malloc(sizeof(int) * n);
+    s->dent = malloc(sizeof(int) * n);
+    s->dsub = malloc(sizeof(int) * n);
+    for (i64 v = 0; v < m->nv; v++) if (s->vdof[v] >= 0) { s->dkind[s->vdof[v]] = 0; s->dent[s->vdof[v]] = (int)v; s->dsub[s->vdof[v]] = 0; }
+    for (i64 e = 0; e < m->ne; e++) if (s->edof[e] >= 0) { s->dkind[s->edof[e]] = 1; s->dent[s->edof[e]] = (int)e; s->dsub[s->edof[e]] = 0; }
+    int nsub = block == ORC_VEL ? m->dim : 1;
+    for (i64 f = 0; f < m->nfacet; f++)
+        if (s->fdof[f] >= 0)
+            for (int a = 0; a < nsub; a++) {
+                s->dkind[s->fdof[f] + a] = 2; s->dent[s->fdof[f] + a] = (int)f; s->dsub[s->fdof[f] + a] = a;
+            }
+    return 0;
+}
+
+void os_free(OSpace *s) {
+    free(s->vdof); free(s->edof); free(s->fdof); free(s->dkind); free(s->dent); free(s->dsub);
+    memset(s, 0, sizeof(*s));
+}
+
+/* does the entity of free DoF d contain vertex v? */
+static int dof_contains_vertex(const OMesh *m, const OSpace *s, int d, int v) {
+    int e = s->dent[d];
+    switch (s->dkind[d]) {
+    case 0: return e == v;
+    case 1: return m->ev[2 * e] == v || m->ev[2 * e + 1] == v;
+    default:
+        if (m->dim == 2) return m->ev[2 * e] == v || m->ev[2 * e + 1] == v;
+        return m->fv[3 * e] == v || m->fv[3 * e + 1] == v || m->fv[3 * e + 2] == v;
+    }
+}
+
+static int cmp_int(const void *a, const void *b) {
+    int x = *(const int *)a, y = *(const int *)b;
+    return x < y ? -1 : x > y;
+}
+
+/* Patch of vertex v: every free DoF of every cell of the star of v whose entity
+ * contains v.  Built from the vertex -> cells incidence.                 */
+int opt_build(OPatches *pt, const OMesh *m, const OSpace *s) {
+    memset(pt, 0, sizeof(*pt));
+    int nvc = m->dim + 1, nle = om_nle(m->dim);
+    /* vertex -> cells */
+    i64 *vcp = calloc((size_t)m->nv + 1, sizeof(i64));
+    for (i64 c = 0; c < m->nc; c++) for (int q = 0; q < nvc; q++) vcp[m->cv[c * nvc + q] + 1]++;
+    for (i64 v = 0; v < m->nv; v++) vcp[v + 1] += vcp[v];
+    int *vc = malloc(sizeof(int) * vcp[m->nv]);
+    i64 *fill = calloc((size_t)m->nv, sizeof(i64));
+    for (i64 c = 0; c < m->nc; c++)
+        for (int q = 0; q < nvc; q++) { int v = m->cv[c * nvc + q]; vc[vcp[v] + fill[v]++] = (int)c; }
+    free(fill);
+
+    int maxloc = 64 * 24;
+    int *buf = malloc(sizeof(int) * maxloc);
+    i64 cap = 1024, used = 0;
+    pt->dofs = malloc(sizeof(int) * cap);
+    pt->vert = malloc(sizeof(int) * m->nv);
+    pt->ptr = malloc(sizeof(i64) * (m->nv + 1));
+    pt->ptr[0] = 0;
+    i64 np = 0;
+    for (i64 v = 0; v < m->nv; v++) {
+        int nb = 0;
+        for (i64 t = vcp[v]; t < vcp[v + 1]; t++) {
+            i64 c = vc[t];
+            /* all free DoFs of cell c */
+            int cand[64]; int nc = 0;
+            if (s->block == ORC_EB) {
+                if (m->dim == 2) for (int q = 0; q < 3; q++) { int d = s->vdof[m->cv[c * 3 + q]]; if (d >= 0) cand[nc++] = d; }
+                else for (int q = 0; q < nle; q++) { int d = s->edof[m->ce[c * nle + q]]; if (d >= 0) cand[nc++] = d; }
+                for (int q = 0; q < nvc; q++) { int d = s->fdof[om_facet_of_cell(m, c, q)]; if (d >= 0) cand[nc++] = d; }
+            } else {
+                for (int q = 0; q < nvc; q++) {
+                    int d = s->fdof[om_facet_of_cell(m, c, q)];
+                    if (d >= 0) for (int a = 0; a < m->dim; a++) cand[nc++] = d + a;
+                }
+            }
+            for (int u = 0; u < nc; u++)
+                if (dof_contains_vertex(m, s, cand[u], (int)v)) buf[nb++] = cand[u];
+        }
+        qsort(buf, (size_t)nb, sizeof(int), cmp_int);
+        int nu = 0;
+        for (int u = 0; u < nb; u++) if (u == 0 || buf[u] != buf[u - 1]) buf[nu++] = buf[u];
+        if (nu == 0) continue;
+        while (used + nu > cap) { cap *= 2; pt->dofs = realloc(pt->dofs, sizeof(int) * cap); }
+        memcpy(pt->dofs + used, buf, sizeof(int) * nu);
+        used += nu;
+        pt->vert[np] = (int)v;
+        pt->ptr[++np] = used;
+    }
+    pt->np = np;
+    free(buf); free(vcp); free(vc);
+    /* multiplicities and DoF -> slot lists (ascending patch order) */
+    i64 n = s->n;
+    pt->mult = calloc((size_t)n, sizeof(int));
+    for (i64 t = 0; t < used; t++) pt->mult[pt->dofs[t]]++;
+    pt->dptr = calloc((size_t)n + 1, sizeof(i64));
+    for (i64 d = 0; d < n; d++) pt->dptr[d + 1] = pt->dptr[d] + pt->mult[d];
+    pt->dslot = malloc(sizeof(i64) * (used ? used : 1));
+    i64 *f2 = calloc((size_t)n, sizeof(i64));
+    for (i64 t = 0; t < used; t++) { int d = pt->dofs[t]; pt->dslot[pt->dptr[d] + f2[d]++] = t; }
+    free(f2);
+    return 0;
+}
+
+void opt_free(OPatches *pt) {
+    free(pt->vert); free(pt->ptr); free(pt->dofs); free(pt->mult); free(pt->dptr); free(pt->dslot);
+    memset(pt, 0, sizeof(*pt));
+}

@@ -1,0 +1,229 @@
+"""Pins of the oracle's finite-element operators against what the paper and the
+mathematics fix: DoF duality, the discrete de Rham complexes
+(P:125-134), divergence-free RT fields, symmetry of the
+symmetric parts, the grad-div kernel, and manufactured-solution convergence.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import mms
+from paper_2104_14855_b200.workloads import CONFIGS, draw, small
+
+
+def make(oracle_mod, cfg, wscale=1.0, pot=None):
+    w, _, _ = draw(cfg, 0, 0)
+    return oracle_mod.Oracle(cfg, w * wscale if pot is None else pot)
+
+
+@pytest.mark.parametrize("name", ["c1", "c3", "c4", "c5"])
+@pytest.mark.parametrize("N", [3, 4])
+def test_dof_duality(oracle_mod, name, N):
+    """N_i(phi_j) = delta_ij on every cell (R-basis)."""
+    o = make(oracle_mod, small(name, N, 1))
+    assert o.duality_error() <= 1e-13
+
+
+def _blocks(o):
+    A = o.csr().to_scipy().toarray()
+    nE = o.info()["nE"]
+    return A, nE
+
+
+def _grad_incidence(m, o, phi):
+    """NED1 coefficients of grad phi for phi in CG1 (exact: int_e grad phi . t = phi(b) - phi(a))."""
+    n = o.n(); nE = o.info()["nE"]
+    x = np.zeros(n)
+    for d in range(nE):
+        a, b = m["ev"][m["dent"][d]]
+        x[d] = phi[b] - phi[a]
+    return x
+
+
+def _curl_incidence_3d(m, o, y_edge):
+    """RT coefficients of curl E for E in NED1 (Stokes on face (a<b<c):
+    circulation = y_ab + y_bc - y_ac)."""
+    n = o.n(); nE = o.info()["nE"]
+    edge_index = {tuple(e): t for t, e in enumerate(m["ev"])}
+    x = np.zeros(n)
+    for d in range(nE, n):
+        a, b, c = m["fv"][m["dent"][d]]
+        x[d] = y_edge[edge_index[(a, b)]] + y_edge[edge_index[(b, c)]] - y_edge[edge_index[(a, c)]]
+    return x
+
+
+def _vcurl_incidence_2d(m, o, psi, sub=None):
+    """RT (2D) coefficients of vcurl psi for psi in CG1: flux through edge (a<b) with
+    n = (t_y, -t_x) is psi(b) - psi(a) (the same +-1 incidence as grad)."""
+    n = o.n()
+    x = np.zeros(n)
+    for d in range(n):
+        if m["dkind"][d] == 2:
+            a, b = m["ev"][m["dent"][d]]
+            x[d] = psi[b] - psi[a]
+    return x
+
+
+def _interior_scalar(m, rng):
+    dim = m["cv"].shape[1] - 1
+    X = m["x"][:, :dim]
+    bnd = np.any((X < 1e-12) | (X > 1 - 1e-12), axis=1)
+    phi = rng.standard_normal(X.shape[0])
+    phi[bnd] = 0.0
+    return phi
+
+
+def test_complex_3d_grad_in_kernel_of_curl(oracle_mod):
+    """grad(CG1) in ker(curl): the assembled (vcurl E, C) block A^T
+    annihilates the NED1 coefficients of a discrete gradient; and
+    curl(NED1) in ker(div): C (div-div) annihilates the RT coefficients of a curl."""
+    cfg = small("c4", 3, 1)
+    o = make(oracle_mod, cfg)
+    m = o.mesh()
+    rng = np.random.default_rng(1)
+    A, nE = _blocks(o)
+    xg = _grad_incidence(m, o, _interior_scalar(m, rng))
+    AT = A[nE:, :nE]
+    assert np.abs(AT @ xg[:nE]).max() <= 1e-13 * np.abs(AT).max() * np.abs(xg).max()
+    # curl of a random NED1 field with zero tangential trace
+    y = rng.standard_normal(len(m["ev"]))
+    free_edges = set(int(m["dent"][d]) for d in range(nE))
+    y = np.array([y[t] if t in free_edges else 0.0 for t in range(len(y))])
+    xc = _curl_incidence_3d(m, o, y)
+    Cb = A[nE:, nE:]
+    assert np.abs(Cb @ xc[nE:]).max() <= 1e-13 * np.abs(Cb).max() * np.abs(xc).max()
+    # and Stokes consistency: the RT field curl E_h equals A^T-based curl, i.e. M_B-free check:
+    # (curl E, C) = A^T E must equal the RT mass-free pairing: <A^T y, x_c> symmetric identity skipped
+
+
+def test_complex_2d_vcurl_divergence_free(oracle_mod):
+    """2D: vcurl(CG1) is in ker(div): C annihilates it."""
+    o = make(oracle_mod, small("c2", 5, 1))
+    m = o.mesh()
+    A, nE = _blocks(o)
+    psi = _interior_scalar(m, np.random.default_rng(2))
+    x = _vcurl_incidence_2d(m, o, psi)
+    Cb = A[nE:, nE:]
+    assert np.abs(Cb @ x[nE:]).max() <= 1e-13 * np.abs(Cb).max() * np.abs(x).max()
+    assert np.abs(x[nE:]).max() > 0.1
+
+
+@pytest.mark.parametrize("name,N", [("c3", 4), ("c5", 2)])
+def test_divergence_free_bdm_in_gamma_kernel(oracle_mod, name, N):
+    """A div-free RT field written in BDM DoFs (F,...,F) (RT_1 in BDM_1) is in the
+    kernel of the grad-div term: A(gamma=1e6) x - A(gamma=1) x is ~0."""
+    base = small(name, N, 1)
+    o1 = make(oracle_mod, dataclasses.replace(base, gamma=1.0))
+    o2 = make(oracle_mod, dataclasses.replace(base, gamma=1e6))
+    m = o1.mesh()
+    n = o1.n(); dim = base.dim
+    rng = np.random.default_rng(3)
+    if dim == 2:
+        psi = _interior_scalar(m, rng)
+        x = np.zeros(n)
+        for d in range(0, n, 2):
+            a, b = m["ev"][m["dent"][d]]
+            x[d] = x[d + 1] = psi[b] - psi[a]
+    else:
+        y = rng.standard_normal(len(m["ev"]))
+        X = m["x"]
+        bnd_v = np.any((X < 1e-12) | (X > 1 - 1e-12), axis=1)
+        # zero tangential trace: zero on edges with both ends on one boundary plane
+        for t, (a, b) in enumerate(m["ev"]):
+            for k in range(3):
+                if (abs(X[a, k]) < 1e-12 and abs(X[b, k]) < 1e-12) or (abs(X[a, k] - 1) < 1e-12 and abs(X[b, k] - 1) < 1e-12):
+                    y[t] = 0.0
+        edge_index = {tuple(e): t for t, e in enumerate(m["ev"])}
+        x = np.zeros(n)
+        for d in range(0, n, 3):
+            a, b, c = m["fv"][m["dent"][d]]
+            x[d:d + 3] = y[edge_index[(a, b)]] + y[edge_index[(b, c)]] - y[edge_index[(a, c)]]
+    A1 = o1.csr().to_scipy(); A2 = o2.csr().to_scipy()
+    diff = (A2 - A1) @ x
+    scale = abs(A2 - A1).max() * np.abs(x).max()
+    assert np.abs(diff).max() <= 1e-10 * scale
+    # and a generic (not div-free) field is NOT in the kernel
+    z = rng.standard_normal(n)
+    assert np.abs((A2 - A1) @ z).max() > 1e-3 * abs(A2 - A1).max()
+
+
+def test_eb_symmetric_parts(oracle_mod):
+    """M_E and C are symmetric (bitwise); with w = 0 the (E,B) block equals
+    -(1/Rem) times the transpose of the (B,E) block A^T (Table 1)."""
+    for name in ("c2", "c4"):
+        cfg = small(name, 3, 1)
+        o = make(oracle_mod, cfg, wscale=0.0)
+        A, nE = _blocks(o)
+        M, C = A[:nE, :nE], A[nE:, nE:]
+        assert np.array_equal(M, M.T)
+        assert np.array_equal(C, C.T)
+        EB, BE = A[:nE, nE:], A[nE:, :nE]
+        assert np.abs(EB + BE.T / cfg.Rem).max() <= 1e-14 * np.abs(BE).max() / cfg.Rem
+        # M_E is SPD (mass matrix)
+        assert np.linalg.eigvalsh(M).min() > 0
+
+
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_velocity_symmetric_without_advection(oracle_mod, name):
+    """SIPG + grad-div is symmetric; with sigma = 10 it is coercive (SPD)."""
+    cfg = small(name, 3 if name == "c3" else 2, 1)
+    o = make(oracle_mod, cfg, wscale=0.0)
+    A = o.csr().to_scipy().toarray()
+    assert np.abs(A - A.T).max() <= 1e-14 * np.abs(A).max()
+    assert np.linalg.eigvalsh(0.5 * (A + A.T)).min() > 0
+
+
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_velocity_advection_coercive(oracle_mod, name):
+    """With an exactly divergence-free, normal-continuous w_h (R-w) the upwind form
+    adds 1/2 |w.n| |[u]|^2 >= 0 to the symmetric part."""
+    cfg = small(name, 4 if name == "c3" else 2, 1)
+    o0 = make(oracle_mod, cfg, wscale=0.0)
+    o1 = make(oracle_mod, cfg, wscale=1.0)
+    A0 = o0.csr().to_scipy().toarray(); A1 = o1.csr().to_scipy().toarray()
+    D = A1 - A0
+    ev = np.linalg.eigvalsh(0.5 * (D + D.T))
+    assert ev.min() >= -1e-10 * np.abs(D).max()
+    assert np.abs(D).max() > 0
+
+
+def _rates(oracle_mod, dim, blk, Ns, **kw):
+    wc = [1.0, 0.5] if dim == 2 else [1.0, 0.5, -0.3]
+    base = dataclasses.replace(CONFIGS["c1" if dim == 2 else "c4"], block=blk, Re=1.0, Rem=1.0, gamma=1.0, levels=1)
+    fs, ex = mms.eb_fields(dim, 1.0, wc, **kw) if blk == "eb" else mms.vel_fields(dim, 1.0, wc)
+    errs = []
+    for N in Ns:
+        cfg = dataclasses.replace(base, N=N)
+        o = oracle_mod.Oracle(cfg, mms.constant_wind_potential(dim, N, wc))
+        errs.append(mms.solve_and_error(o, fs, ex))
+    errs = np.array(errs)
+    return np.log(errs[-2] / errs[-1]) / np.log(Ns[-1] / Ns[-2])
+
+
+def test_mms_rates_2d_eb(oracle_mod):
+    """CG1 E: L2 rate 2; RT1 B: rate 1 (both B choices, incl. a non-div-free one
+    exercising C); Re = Rem = gamma = 1, constant w."""
+    r = _rates(oracle_mod, 2, "eb", [16, 32])
+    assert r[0] >= 1.9 and r[1] >= 0.95 and r[2] >= 0.95
+    r = _rates(oracle_mod, 2, "eb", [16, 32], div_free_B=True)
+    assert r[0] >= 1.9 and min(r[1:]) >= 0.95
+
+
+def test_mms_rates_2d_velocity(oracle_mod):
+    """BDM1 with SIPG: L2 rate 2 for u."""
+    r = _rates(oracle_mod, 2, "vel", [16, 32])
+    assert r.min() >= 1.9
+
+
+def test_mms_rates_3d_eb(oracle_mod):
+    """NED1 E and RT1 B: L2 rate 1."""
+    r = _rates(oracle_mod, 3, "eb", [4, 8])
+    assert r.min() >= 0.9
+
+
+def test_mms_rates_3d_velocity(oracle_mod):
+    """BDM1 3D: pre-asymptotic on these meshes (1.57 at 4->8; measured 1.80 at 8->12
+    and 1.88 at 12->16 offline); the pin requires a clearly super-linear rate."""
+    r = _rates(oracle_mod, 3, "vel", [4, 8])
+    assert r.min() >= 1.5
