@@ -1,0 +1,180 @@
+/*
+ * mhdp.h -- C-ABI of the B200-native vertex-star Schwarz smoother / V-cycle
+ * library (libmhdp.so) for the two specialised multigrid solvers of
+ * arXiv 2104.14855 (PAPER.md = P:line; SURVEY.md §8(b) = the call list):
+ *
+ *   - the augmented-Lagrangian H(div) velocity-block multigrid   (§3.4)
+ *   - the monolithic E-B block multigrid                          (§3.5)
+ *
+ * The smoother is the parallel subspace correction of P:529-538 (eq. decomp) over
+ * the vertex-star decomposition of P:567-571 (eq. stardecomp); the hierarchy is the
+ * nested uniform refinement with the FE-induced prolongation of P:572; the cycle is
+ * the V-cycle of P:643 with Richardson Schwarz sweeps instead of GMRES(6) (DESIGN.md
+ * reading R-smoother).
+ *
+ * Conventions (all entry points)
+ *   - Every function returns an mhdp_status; nothing throws across the ABI.
+ *   - Levels are numbered 0 = coarsest .. n_levels-1 = finest.
+ *   - "_dev" pointers are CUDA device pointers of fp64 vectors of the level's length n
+ *     (contiguous, owned by the CALLER, on the context's device). "_host" pointers are
+ *     host memory owned by the caller. The context owns every internal store.
+ *   - Device work is stream-ordered on the context's stream and does not synchronise
+ *     the host, except where a function says "synchronises".
+ *   - A context is not thread-safe; distinct contexts are independent.
+ *   - On error the context keeps a message (mhdp_last_error).
+ */
+#ifndef MHDP_H
+#define MHDP_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MHDP_OK = 0,
+    MHDP_EINVAL = 1,     /* bad argument: null pointer, bad sizes, bad mesh/params          */
+    MHDP_ENOMEM = 2,     /* host or device allocation failed                                */
+    MHDP_ECUDA = 3,      /* CUDA runtime error, or a device call on a host-only context      */
+    MHDP_ESINGULAR = 4,  /* zero pivot (|pivot| <= 1e-14 max|A_i|) in a patch or coarse LU  */
+    MHDP_ESTATE = 5,     /* call out of order (e.g. smooth before setup)                    */
+    MHDP_ENOCONV = 6     /* GMRES reached maxit (not fatal: x holds the last iterate)       */
+} mhdp_status;
+
+typedef enum {
+    MHDP_BLOCK_EB = 0,    /* E-B block  [[M_E, G~ - A/Rem], [A^T, C]]  */
+    MHDP_BLOCK_ALVEL = 1  /* AL velocity block: (2/Re) eps-form SIPG + upwind advection
+                             + gamma grad-div on BDM1   */
+} mhdp_block;
+
+typedef struct {
+    int dim;       /* 2 (unit square, triangles) or 3 (unit cube, 6 Kuhn tets per cube)      */
+    int n_fine;    /* cells per side on the finest level; n_fine % 2^(n_levels-1) == 0       */
+    int n_levels;  /* >= 1; level l has n_fine >> (n_levels-1-l) cells per side     */
+} mhdp_mesh;
+
+typedef struct {
+    double Re, Rem, S, gamma; /* P:20-35. S is accepted and unused by both blocks
+                                 (reading R-S); Re/gamma used by ALVEL, Rem by EB; > 0      */
+    double sigma;             /* SIPG penalty sigma = 10 k^2 = 10                    */
+    double mu_stab;           /* Burman stabilisation mu; must be 0 (R-mu)       */
+    double theta;             /* outer damping of the additive update (R-weights), 1.0       */
+    int nu_pre, nu_post;      /* smoothing sweeps per level in the V-cycle (R-nu)             */
+} mhdp_params;
+
+typedef struct mhdp_ctx mhdp_ctx;
+
+typedef struct {
+    long long n;          /* free DoFs of the level                                         */
+    long long nnz;        /* operator nonzeros (CSR, structural)                             */
+    long long npatch;     /* vertex-star patches (non-empty stars, ascending vertex)         */
+    long long sum_n;      /* sum_i n_i  (patch slots)                                         */
+    long long sum_n2;     /* sum_i n_i^2 (factor doubles, unpadded)                           */
+    long long max_n;      /* largest patch                                                   */
+    long long p_nnz;      /* nonzeros of the prolongation from level-1 (0 on level 0)        */
+    long long bytes_operator, bytes_factors, bytes_transfer; /* device bytes of each store  */
+} mhdp_level_info;
+
+/* ---- lifecycle ---------------------------------------------------------------------- */
+
+/* Create a context on CUDA device `cuda_device` issuing work on `cuda_stream` (a
+ * cudaStream_t; NULL = the legacy default stream).  cuda_device = -1 creates a
+ * HOST-ONLY context: mhdp_assemble/mhdp_load_level and the export calls work, every
+ * device call returns MHDP_ECUDA (used by the CPU test-suite to check host setup).   */
+mhdp_status mhdp_create(mhdp_ctx **out, int cuda_device, void *cuda_stream);
+void        mhdp_destroy(mhdp_ctx *ctx);
+
+/* Assemble every level of the hierarchy on the host (setup stage a0/a1 of SURVEY §8(a)):
+ * structured nested meshes, canonical numbering, free DoFs, vertex-star patches
+ * (P:567-571), the level operators by rediscretisation (R-coarse) and the exact
+ * prolongations.  w_vertex_host: potential of the advecting field at the
+ * finest-level vertices in vertex order i+(N+1)(j+(N+1)k) (R-w): 2D stream function
+ * psi (1 double per vertex, field = vcurl psi_h), 3D vector potential A (3 doubles per
+ * vertex, field = curl of the NED1 interpolant of A_h).  Coarser levels inject it.
+ * Errors: EINVAL (dims, divisibility, non-positive Re/Rem/gamma, mu_stab != 0, NULL). */
+mhdp_status mhdp_assemble(mhdp_ctx *ctx, mhdp_block block, const mhdp_mesh *mesh,
+                          const mhdp_params *params, const double *w_vertex_host);
+
+/* Algebraic entry (the PCPATCH-style interface): install level `level` of an
+ * n_levels hierarchy from caller data instead of mhdp_assemble.  Host arrays, copied:
+ *   rowptr[n+1] (int64), col[nnz] (int32, ascending within a row), val[nnz]      A_l
+ *   pptr[npatch+1] (int64), pdofs[pptr[npatch]] (int32, ascending within a patch) patches
+ *   prow[n+1], pcol, pval: prolongation from level-1 (n x n_{l-1}); NULL on level 0.
+ * Call mhdp_begin_levels first.  Errors: EINVAL (sizes, unsorted, out of range).     */
+mhdp_status mhdp_begin_levels(mhdp_ctx *ctx, int n_levels, const mhdp_params *params);
+mhdp_status mhdp_load_level(mhdp_ctx *ctx, int level, long long n,
+                            const long long *rowptr, const int *col, const double *val,
+                            long long npatch, const long long *pptr, const int *pdofs,
+                            const long long *prow, const int *pcol, const double *pval);
+
+/* Upload the stores and factor them on the device (synchronises): batched patch LU with
+ * partial pivoting for every level >= 1 (kernel K6) and the dense
+ * coarse LU of level 0 (K7; stand-in for MUMPS).  Errors: ESINGULAR names the
+ * level and patch (mhdp_last_error's `where` = level*2^32 + patch; patch -1 = coarse). */
+mhdp_status mhdp_setup(mhdp_ctx *ctx);
+
+mhdp_status mhdp_get_level_info(const mhdp_ctx *ctx, int level, mhdp_level_info *out);
+int         mhdp_num_levels(const mhdp_ctx *ctx);
+
+/* ---- hot path (device pointers, stream-ordered, no host synchronisation) ----------- */
+
+/* y = A_l x                                                   (operator application)   */
+mhdp_status mhdp_spmv(mhdp_ctx *ctx, int level, const double *x_dev, double *y_dev);
+/* r = b - A_l x   (K1; "(f,v_i) - a(u^k,v_i)")                                     */
+mhdp_status mhdp_residual(mhdp_ctx *ctx, int level, const double *b_dev, const double *x_dev,
+                          double *r_dev);
+/* K2 alone: y_i = A_i^{-1} R_i r for every patch into the context's slot buffer
+ * (exposed for timing/tests; the slot buffer is read back with mhdp_export_slots).     */
+mhdp_status mhdp_patch_apply(mhdp_ctx *ctx, int level, const double *r_dev);
+/* K3 alone: x_d <- fma(theta/m_d, sum_{i ∋ d} y_i[k_i(d)], x_d) from the slot buffer.  */
+mhdp_status mhdp_patch_update(mhdp_ctx *ctx, int level, double *x_dev);
+/* nsweeps Schwarz sweeps S(x; b) in place on level >= 1:
+ *   r = b - A x;  y_i = A_i^{-1} R_i r;  x_d <- fma(theta w_d, sum_i y_i[k_i(d)], x_d).
+ * x_is_zero != 0 declares x = 0 on entry: sweep 1 then skips the SpMV (x is written). */
+mhdp_status mhdp_smooth(mhdp_ctx *ctx, int level, int nsweeps, int x_is_zero,
+                        const double *b_dev, double *x_dev);
+/* rc = P_l^T r   (K4, restriction to level-1)                                         */
+mhdp_status mhdp_restrict(mhdp_ctx *ctx, int level, const double *r_dev, double *rc_dev);
+/* x <- x + P_l ec (K5, prolongation from level-1)                                      */
+mhdp_status mhdp_prolong_add(mhdp_ctx *ctx, int level, const double *ec_dev, double *x_dev);
+/* x = A_0^{-1} b by the dense coarse LU (K8)                                            */
+mhdp_status mhdp_coarse_solve(mhdp_ctx *ctx, const double *b_dev, double *x_dev);
+/* x = V_l(b) with zero initial guess on level `level` (finest: n_levels-1), P:643:
+ * nu_pre sweeps, residual, restrict, recurse, prolong-add, nu_post sweeps.             */
+mhdp_status mhdp_vcycle(mhdp_ctx *ctx, int level, const double *b_dev, double *x_dev);
+/* End-to-end variant for callers holding host data: copies b (host, n doubles) to the
+ * device, runs mhdp_vcycle on the finest level and copies x back (synchronises).       */
+mhdp_status mhdp_vcycle_host(mhdp_ctx *ctx, const double *b_host, double *x_host);
+/* Smoother sweeps with host buffers (b, x in/out; synchronises).                       */
+mhdp_status mhdp_smooth_host(mhdp_ctx *ctx, int level, int nsweeps, int x_is_zero,
+                             const double *b_host, double *x_host);
+/* Right-preconditioned GMRES with the V-cycle on the finest level, x0 = 0, modified
+ * Gram-Schmidt, no restart: stops when the residual estimate <=
+ * max(rtol |b|, atol).  its_out = iterations, relres_out = estimate / |b|.
+ * Synchronises every iteration.  Returns ENOCONV at maxit.                              */
+mhdp_status mhdp_gmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol,
+                       double atol, int maxit, int *its_out, double *relres_out);
+
+/* ---- export for parity checks (host buffers, caller-allocated, sizes from info) ----- */
+mhdp_status mhdp_export_csr(const mhdp_ctx *ctx, int level, long long *rowptr, int *col,
+                            double *val);
+mhdp_status mhdp_export_patches(const mhdp_ctx *ctx, int level, long long *pptr, int *pdofs);
+mhdp_status mhdp_export_prolongation(const mhdp_ctx *ctx, int level, long long *prow,
+                                     int *pcol, double *pval);
+/* Patch `patch` of `level` after setup (synchronises): its LU factors, row-major n_i x n_i
+ * (unit L below the diagonal, U on and above), and perm[k] = original row at position k. */
+mhdp_status mhdp_export_patch_lu(mhdp_ctx *ctx, int level, long long patch, double *lu,
+                                 int *perm);
+/* The slot buffer y (sum_n doubles) of the last patch apply on `level` (synchronises).   */
+mhdp_status mhdp_export_slots(mhdp_ctx *ctx, int level, double *y);
+
+/* ---- diagnostics --------------------------------------------------------------------- */
+mhdp_status mhdp_synchronize(mhdp_ctx *ctx);
+/* Last error message (NUL-terminated, truncated to len) and its location (see setup). */
+mhdp_status mhdp_last_error(const mhdp_ctx *ctx, char *buf, int len, long long *where);
+/* Number of kernels this context has launched since creation (bench gpu_launches).    */
+long long   mhdp_launch_count(const mhdp_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MHDP_H */

@@ -1,0 +1,831 @@
+// api.cu -- the C-ABI of include/mhdp.h: context, device stores, setup (K6/K7), the
+// smoother and V-cycle drivers, GMRES and the export calls.
+//
+// Paper: arXiv 2104.14855.  Sweep = parallel subspace correction P:529-538; stars
+// P:567-571; nested hierarchy + FE prolongation P:572; V-cycle with patch relaxation
+// and a direct coarse solve P:643; right-preconditioned Krylov with the paper's
+// 1e-7 tolerances P:625.  Readings (R-*) are listed in DESIGN.md.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mhdp.h"
+#include "kernels.cuh"
+#include "setup.hpp"
+
+using namespace mhdp;
+
+namespace {
+
+struct DevLevel {
+    int64_t n = 0, nnz = 0;
+    DevSell A;
+    DevBSell3 A3;
+    bool use_b3 = false;
+    DevPatches P;
+    DevCsr Pr, PrT;            // prolongation from level-1 (fine rows) and its transpose
+    double *b = nullptr, *x = nullptr, *r = nullptr;
+    int64_t bytes_op = 0, bytes_fac = 0, bytes_tr = 0;
+};
+
+}  // namespace
+
+struct mhdp_ctx {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    bool host_only = true;
+    int nlev = 0;
+    int block = -1;
+    Params p;
+    std::vector<HostLevel> H;
+    std::vector<char> loaded;
+    std::vector<DevLevel> D;
+    bool setup_done = false;
+    // coarse factor
+    int n0 = 0;
+    double *clut = nullptr;    // column-major LU of A_0
+    int *cperm = nullptr;
+    double *cz = nullptr;
+    // scratch
+    int *d_status = nullptr;
+    double *d_scal = nullptr;  // dot partials + results
+    std::vector<void *> allocs;
+    std::string err;
+    long long where = -1;
+    long long launches0 = 0;
+    // gmres workspace
+    double *gV = nullptr, *gZ = nullptr, *gw = nullptr;
+    int g_cap = 0;
+};
+
+namespace {
+
+mhdp_status fail(mhdp_ctx *c, mhdp_status st, const std::string &msg, long long where = -1) {
+    if (c) { c->err = msg; c->where = where; }
+    return st;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(ctx, MHDP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <class T>
+mhdp_status dalloc(mhdp_ctx *ctx, T **p, int64_t count) {
+    *p = nullptr;
+    if (count <= 0) count = 1;
+    cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (size_t)count);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return fail(ctx, MHDP_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    ctx->allocs.push_back(*p);
+    return MHDP_OK;
+}
+
+template <class T>
+mhdp_status upload(mhdp_ctx *ctx, T **p, const T *src, int64_t count) {
+    mhdp_status st = dalloc(ctx, p, count);
+    if (st) return st;
+    if (count > 0) CK(cudaMemcpy(*p, src, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice));
+    return MHDP_OK;
+}
+
+mhdp_status check_launch(mhdp_ctx *ctx) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ctx, MHDP_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+    return MHDP_OK;
+}
+
+void free_device(mhdp_ctx *c) {
+    if (c->host_only) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (void *p : c->allocs) cudaFree(p);
+    c->allocs.clear();
+    c->D.clear();
+    c->clut = nullptr; c->cperm = nullptr; c->cz = nullptr;
+    c->d_status = nullptr; c->d_scal = nullptr;
+    c->gV = c->gZ = c->gw = nullptr; c->g_cap = 0;
+    c->setup_done = false;
+}
+
+bool valid_level(const mhdp_ctx *c, int l) { return c && l >= 0 && l < c->nlev; }
+
+// ---------------- host -> device store construction ----------------
+
+mhdp_status build_sell(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
+    const int64_t n = H.n, ns = (n + 31) / 32;
+    std::vector<int64_t> sptr(ns + 1, 0);
+    std::vector<int> rlen(n);
+    for (int64_t s = 0; s < ns; ++s) {
+        int mx = 0;
+        for (int64_t r = 32 * s; r < std::min(n, 32 * s + 32); ++r) {
+            rlen[r] = (int)(H.rp[r + 1] - H.rp[r]);
+            mx = std::max(mx, rlen[r]);
+        }
+        sptr[s + 1] = sptr[s] + 32 * (int64_t)mx;
+    }
+    const int64_t stored = sptr[ns];
+    std::vector<int> col(stored, 0);
+    std::vector<double> val(stored, 0.0);
+    for (int64_t r = 0; r < n; ++r) {
+        const int64_t base = sptr[r >> 5] + (r & 31);
+        for (int k = 0; k < rlen[r]; ++k) {
+            col[base + 32 * k] = H.ci[H.rp[r] + k];
+            val[base + 32 * k] = H.v[H.rp[r] + k];
+        }
+    }
+    mhdp_status st;
+    L.A.n = n; L.A.nslices = ns; L.A.stored = stored;
+    if ((st = upload(ctx, &L.A.sptr, sptr.data(), ns + 1))) return st;
+    if ((st = upload(ctx, &L.A.rlen, rlen.data(), n))) return st;
+    if ((st = upload(ctx, &L.A.col, col.data(), stored))) return st;
+    if ((st = upload(ctx, &L.A.val, val.data(), stored))) return st;
+    L.bytes_op = 8 * (ns + 1) + 4 * n + 12 * stored;
+    return MHDP_OK;
+}
+
+// aligned 3x3 block structure: n % 3 == 0, rows 3R..3R+2 share one column list made of
+// complete aligned triples
+bool has_block3(const HostLevel &H) {
+    if (H.n == 0 || H.n % 3) return false;
+    for (int64_t R = 0; R < H.n / 3; ++R) {
+        const int64_t a = H.rp[3 * R], len = H.rp[3 * R + 1] - a;
+        if (len % 3) return false;
+        for (int q = 1; q < 3; ++q) {
+            if (H.rp[3 * R + q + 1] - H.rp[3 * R + q] != len) return false;
+            if (!std::equal(H.ci.begin() + a, H.ci.begin() + a + len, H.ci.begin() + H.rp[3 * R + q])) return false;
+        }
+        for (int64_t t = 0; t < len; t += 3) {
+            const int c = H.ci[a + t];
+            if (c % 3 || H.ci[a + t + 1] != c + 1 || H.ci[a + t + 2] != c + 2) return false;
+        }
+    }
+    return true;
+}
+
+mhdp_status build_b3(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
+    const int64_t nb = H.n / 3, ns = (nb + 31) / 32;
+    std::vector<int64_t> sptr(ns + 1, 0);
+    std::vector<int> rlen(nb);
+    for (int64_t s = 0; s < ns; ++s) {
+        int mx = 0;
+        for (int64_t R = 32 * s; R < std::min(nb, 32 * s + 32); ++R) {
+            rlen[R] = (int)((H.rp[3 * R + 1] - H.rp[3 * R]) / 3);
+            mx = std::max(mx, rlen[R]);
+        }
+        sptr[s + 1] = sptr[s] + 32 * (int64_t)mx;
+    }
+    const int64_t stored = sptr[ns];
+    std::vector<int> col(stored, 0);
+    std::vector<double> val(9 * stored, 0.0);
+    for (int64_t R = 0; R < nb; ++R) {
+        const int64_t base = sptr[R >> 5] + (R & 31);
+        for (int k = 0; k < rlen[R]; ++k) {
+            const int64_t e = base + 32 * (int64_t)k;
+            col[e] = H.ci[H.rp[3 * R] + 3 * k] / 3;
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b) val[(3 * a + b) * stored + e] = H.v[H.rp[3 * R + a] + 3 * k + b];
+        }
+    }
+    mhdp_status st;
+    L.A3.nb = nb; L.A3.nslices = ns; L.A3.stored = stored;
+    if ((st = upload(ctx, &L.A3.sptr, sptr.data(), ns + 1))) return st;
+    if ((st = upload(ctx, &L.A3.rlen, rlen.data(), nb))) return st;
+    if ((st = upload(ctx, &L.A3.col, col.data(), stored))) return st;
+    if ((st = upload(ctx, &L.A3.val, val.data(), 9 * stored))) return st;
+    L.bytes_op = 8 * (ns + 1) + 4 * nb + 76 * stored;
+    return MHDP_OK;
+}
+
+mhdp_status build_csr(mhdp_ctx *ctx, int64_t n, const std::vector<int64_t> &rp, const std::vector<int> &ci,
+                      const std::vector<double> &v, DevCsr &out) {
+    std::vector<int> rp32(n + 1);
+    for (int64_t i = 0; i <= n; ++i) rp32[i] = (int)rp[i];
+    out.n = n; out.nnz = rp[n];
+    mhdp_status st;
+    if ((st = upload(ctx, &out.rp, rp32.data(), n + 1))) return st;
+    if ((st = upload(ctx, &out.ci, ci.data(), out.nnz))) return st;
+    if ((st = upload(ctx, &out.v, v.data(), out.nnz))) return st;
+    return MHDP_OK;
+}
+
+void transpose_csr(int64_t n, int64_t ncols, const std::vector<int64_t> &rp, const std::vector<int> &ci,
+                   const std::vector<double> &v, std::vector<int64_t> &trp, std::vector<int> &tci,
+                   std::vector<double> &tv) {
+    trp.assign(ncols + 1, 0);
+    for (int64_t t = 0; t < rp[n]; ++t) trp[ci[t] + 1]++;
+    for (int64_t j = 0; j < ncols; ++j) trp[j + 1] += trp[j];
+    tci.resize(rp[n]);
+    tv.resize(rp[n]);
+    std::vector<int64_t> pos(trp.begin(), trp.end() - 1);
+    for (int64_t i = 0; i < n; ++i)       // ascending fine rows => each coarse row ascending
+        for (int64_t t = rp[i]; t < rp[i + 1]; ++t) {
+            const int64_t q = pos[ci[t]]++;
+            tci[q] = (int)i;
+            tv[q] = v[t];
+        }
+}
+
+mhdp_status build_patches(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
+    DevPatches &P = L.P;
+    const int64_t np = (int64_t)H.pptr.size() - 1, sum_n = H.pptr[np];
+    P.np = np; P.sum_n = sum_n;
+    std::vector<int> pn(np);
+    std::vector<int64_t> foff(np);
+    int64_t f = 0;
+    int mx = 0;
+    for (int64_t i = 0; i < np; ++i) {
+        pn[i] = (int)(H.pptr[i + 1] - H.pptr[i]);
+        mx = std::max(mx, pn[i]);
+        foff[i] = f;
+        f += ((int64_t)pn[i] * pn[i] + 15) / 16 * 16;   // 128-byte aligned factor blocks
+    }
+    if (mx > 160) return fail(ctx, MHDP_EINVAL, "patch larger than 160 DoFs is not supported");
+    P.max_n = mx;
+    P.fac_doubles = f;
+    std::vector<int> mult(H.n, 0);
+    for (int64_t t = 0; t < sum_n; ++t) mult[H.pdofs[t]]++;
+    std::vector<int> dptr(H.n + 1, 0);
+    for (int64_t d = 0; d < H.n; ++d) {
+        if (mult[d] == 0) return fail(ctx, MHDP_EINVAL, "a DoF is covered by no patch", d);
+        dptr[d + 1] = dptr[d] + mult[d];
+    }
+    std::vector<int> dslot(sum_n), fill(dptr.begin(), dptr.end() - 1);
+    for (int64_t t = 0; t < sum_n; ++t) dslot[fill[H.pdofs[t]]++] = (int)t;   // ascending slot = ascending patch
+    std::vector<double> wd(H.n);
+    for (int64_t d = 0; d < H.n; ++d) wd[d] = ctx->p.theta * (1.0 / mult[d]);  // R-weights
+    mhdp_status st;
+    if ((st = upload(ctx, &P.pn, pn.data(), np))) return st;
+    if ((st = upload(ctx, &P.poff, H.pptr.data(), np))) return st;
+    if ((st = upload(ctx, &P.foff, foff.data(), np))) return st;
+    if ((st = upload(ctx, &P.pdofs, H.pdofs.data(), sum_n))) return st;
+    if ((st = dalloc(ctx, &P.gidx, sum_n))) return st;
+    if ((st = dalloc(ctx, &P.perm, sum_n))) return st;
+    if ((st = dalloc(ctx, &P.fac, f))) return st;
+    if ((st = upload(ctx, &P.dptr, dptr.data(), H.n + 1))) return st;
+    if ((st = upload(ctx, &P.dslot, dslot.data(), sum_n))) return st;
+    if ((st = upload(ctx, &P.wd, wd.data(), H.n))) return st;
+    if ((st = dalloc(ctx, &P.y, sum_n))) return st;
+    L.bytes_fac = 8 * f + 4 * np + 16 * np + 12 * sum_n;
+    return MHDP_OK;
+}
+
+// ---------------- device drivers ----------------
+
+void residual(mhdp_ctx *ctx, int l, const double *b, const double *x, double *r) {
+    DevLevel &L = ctx->D[l];
+    if (L.use_b3) launch_residual_b3(L.A3, b, x, r, ctx->stream);
+    else launch_residual(L.A, b, x, r, ctx->stream);
+}
+
+void sweep(mhdp_ctx *ctx, int l, const double *b, double *x, bool x_zero) {
+    DevLevel &L = ctx->D[l];
+    const double *r = b;
+    if (!x_zero) {
+        residual(ctx, l, b, x, L.r);
+        r = L.r;
+    }
+    launch_patch_apply(L.P, r, ctx->stream);
+    launch_patch_update(L.P, L.n, x, x_zero ? 1 : 0, ctx->stream);
+}
+
+void coarse_solve(mhdp_ctx *ctx, const double *b, double *x) {
+    launch_dense_solve(ctx->clut, ctx->cperm, ctx->n0, b, x, ctx->cz, ctx->stream);
+}
+
+void vcycle(mhdp_ctx *ctx, int l, const double *b, double *x) {
+    if (l == 0) {
+        coarse_solve(ctx, b, x);
+        return;
+    }
+    DevLevel &L = ctx->D[l];
+    DevLevel &C = ctx->D[l - 1];
+    if (ctx->p.nu_pre == 0) launch_fill(x, 0.0, L.n, ctx->stream);
+    for (int s = 0; s < ctx->p.nu_pre; ++s) sweep(ctx, l, b, x, s == 0);
+    residual(ctx, l, b, x, L.r);
+    launch_restrict(L.PrT, L.r, C.b, ctx->stream);
+    vcycle(ctx, l - 1, C.b, C.x);
+    launch_prolong_add(L.Pr, C.x, x, ctx->stream);
+    for (int s = 0; s < ctx->p.nu_post; ++s) sweep(ctx, l, b, x, false);
+}
+
+mhdp_status need_setup(mhdp_ctx *ctx) {
+    if (!ctx) return MHDP_EINVAL;
+    if (ctx->host_only) return fail(ctx, MHDP_ECUDA, "host-only context (created with cuda_device = -1)");
+    if (!ctx->setup_done) return fail(ctx, MHDP_ESTATE, "mhdp_setup has not completed");
+    cudaSetDevice(ctx->device);
+    return MHDP_OK;
+}
+
+mhdp_status validate_level(mhdp_ctx *ctx, const HostLevel &H, int level) {
+    if (H.n < 0 || (int64_t)H.rp.size() != H.n + 1 || H.rp[0] != 0) return fail(ctx, MHDP_EINVAL, "bad row pointer");
+    for (int64_t i = 0; i < H.n; ++i) {
+        if (H.rp[i + 1] < H.rp[i]) return fail(ctx, MHDP_EINVAL, "row pointer not monotone", i);
+        for (int64_t t = H.rp[i]; t < H.rp[i + 1]; ++t) {
+            if (H.ci[t] < 0 || H.ci[t] >= H.n) return fail(ctx, MHDP_EINVAL, "column out of range", i);
+            if (t > H.rp[i] && H.ci[t] <= H.ci[t - 1]) return fail(ctx, MHDP_EINVAL, "columns not ascending", i);
+        }
+    }
+    if (level > 0) {
+        const int64_t np = (int64_t)H.pptr.size() - 1;
+        if (np < 0 || H.pptr[0] != 0) return fail(ctx, MHDP_EINVAL, "bad patch pointer");
+        for (int64_t i = 0; i < np; ++i) {
+            if (H.pptr[i + 1] <= H.pptr[i]) return fail(ctx, MHDP_EINVAL, "empty patch", i);
+            for (int64_t t = H.pptr[i]; t < H.pptr[i + 1]; ++t) {
+                if (H.pdofs[t] < 0 || H.pdofs[t] >= H.n) return fail(ctx, MHDP_EINVAL, "patch DoF out of range", i);
+                if (t > H.pptr[i] && H.pdofs[t] <= H.pdofs[t - 1])
+                    return fail(ctx, MHDP_EINVAL, "patch DoFs not ascending", i);
+            }
+        }
+        if ((int64_t)H.prp.size() != H.n + 1) return fail(ctx, MHDP_EINVAL, "bad prolongation row pointer");
+        for (int64_t t = 0; t < H.prp[H.n]; ++t)
+            if (H.pci[t] < 0 || H.pci[t] >= H.n_coarser) return fail(ctx, MHDP_EINVAL, "prolongation column out of range");
+    }
+    return MHDP_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+mhdp_status mhdp_create(mhdp_ctx **out, int cuda_device, void *cuda_stream) {
+    if (!out) return MHDP_EINVAL;
+    *out = nullptr;
+    mhdp_ctx *ctx = new (std::nothrow) mhdp_ctx();
+    if (!ctx) return MHDP_ENOMEM;
+    if (cuda_device >= 0) {
+        int cnt = 0;
+        if (cudaGetDeviceCount(&cnt) != cudaSuccess || cuda_device >= cnt) {
+            delete ctx;
+            return MHDP_ECUDA;
+        }
+        if (cudaSetDevice(cuda_device) != cudaSuccess) { delete ctx; return MHDP_ECUDA; }
+        ctx->device = cuda_device;
+        ctx->host_only = false;
+        ctx->stream = (cudaStream_t)cuda_stream;
+        ctx->launches0 = g_launches;
+    }
+    *out = ctx;
+    return MHDP_OK;
+}
+
+void mhdp_destroy(mhdp_ctx *ctx) {
+    if (!ctx) return;
+    free_device(ctx);
+    delete ctx;
+}
+
+static mhdp_status check_params(mhdp_ctx *ctx, const mhdp_params *pr) {
+    if (!pr) return fail(ctx, MHDP_EINVAL, "params is NULL");
+    if (!(pr->Re > 0) || !(pr->Rem > 0) || !(pr->gamma > 0) || !(pr->sigma > 0))
+        return fail(ctx, MHDP_EINVAL, "Re, Rem, gamma and sigma must be positive");
+    if (pr->mu_stab != 0.0) return fail(ctx, MHDP_EINVAL, "mu_stab != 0 is not supported (reading R-mu)");
+    if (pr->nu_pre < 0 || pr->nu_post < 0) return fail(ctx, MHDP_EINVAL, "negative sweep counts");
+    if (!(pr->theta > 0)) return fail(ctx, MHDP_EINVAL, "theta must be positive");
+    ctx->p.Re = pr->Re; ctx->p.Rem = pr->Rem; ctx->p.S = pr->S; ctx->p.gamma = pr->gamma;
+    ctx->p.sigma = pr->sigma; ctx->p.mu = pr->mu_stab; ctx->p.theta = pr->theta;
+    ctx->p.nu_pre = pr->nu_pre; ctx->p.nu_post = pr->nu_post;
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_assemble(mhdp_ctx *ctx, mhdp_block block, const mhdp_mesh *mesh, const mhdp_params *params,
+                          const double *w_vertex_host) {
+    if (!ctx) return MHDP_EINVAL;
+    if (!mesh || !w_vertex_host) return fail(ctx, MHDP_EINVAL, "NULL mesh or w_vertex");
+    if (block != MHDP_BLOCK_EB && block != MHDP_BLOCK_ALVEL) return fail(ctx, MHDP_EINVAL, "unknown block");
+    if ((mesh->dim != 2 && mesh->dim != 3) || mesh->n_fine < 1 || mesh->n_levels < 1 || mesh->n_levels > 12)
+        return fail(ctx, MHDP_EINVAL, "bad mesh dimensions");
+    if (mesh->n_fine % (1 << (mesh->n_levels - 1)))
+        return fail(ctx, MHDP_EINVAL, "n_fine must be divisible by 2^(n_levels-1)");
+    mhdp_status st = check_params(ctx, params);
+    if (st) return st;
+    free_device(ctx);
+    ctx->H.clear();
+    std::string e = assemble_hierarchy((int)block, mesh->dim, mesh->n_fine, mesh->n_levels, ctx->p, w_vertex_host, ctx->H);
+    if (!e.empty()) { ctx->H.clear(); ctx->nlev = 0; return fail(ctx, MHDP_EINVAL, e); }
+    ctx->nlev = mesh->n_levels;
+    ctx->block = (int)block;
+    ctx->loaded.assign(ctx->nlev, 1);
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_begin_levels(mhdp_ctx *ctx, int n_levels, const mhdp_params *params) {
+    if (!ctx) return MHDP_EINVAL;
+    if (n_levels < 1 || n_levels > 16) return fail(ctx, MHDP_EINVAL, "bad n_levels");
+    mhdp_status st = check_params(ctx, params);
+    if (st) return st;
+    free_device(ctx);
+    ctx->H.assign(n_levels, HostLevel());
+    ctx->loaded.assign(n_levels, 0);
+    ctx->nlev = n_levels;
+    ctx->block = -1;
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_load_level(mhdp_ctx *ctx, int level, long long n, const long long *rowptr, const int *col,
+                            const double *val, long long npatch, const long long *pptr, const int *pdofs,
+                            const long long *prow, const int *pcol, const double *pval) {
+    if (!ctx) return MHDP_EINVAL;
+    if (!valid_level(ctx, level) || (int)ctx->loaded.size() != ctx->nlev)
+        return fail(ctx, MHDP_ESTATE, "mhdp_begin_levels first / bad level");
+    if (n < 0 || !rowptr || (n > 0 && (!col || !val))) return fail(ctx, MHDP_EINVAL, "NULL operator arrays");
+    if (level > 0 && (npatch < 1 || !pptr || !pdofs || !prow || !pcol || !pval))
+        return fail(ctx, MHDP_EINVAL, "levels >= 1 need patches and a prolongation");
+    if (level > 0 && !ctx->loaded[level - 1]) return fail(ctx, MHDP_ESTATE, "load level-1 first");
+    HostLevel H;
+    H.n = n;
+    H.rp.assign(rowptr, rowptr + n + 1);
+    const int64_t nnz = H.rp[n];
+    if (nnz < 0) return fail(ctx, MHDP_EINVAL, "bad row pointer");
+    H.ci.assign(col, col + nnz);
+    H.v.assign(val, val + nnz);
+    if (level > 0) {
+        H.pptr.assign(pptr, pptr + npatch + 1);
+        H.pdofs.assign(pdofs, pdofs + H.pptr[npatch]);
+        H.prp.assign(prow, prow + n + 1);
+        H.pci.assign(pcol, pcol + H.prp[n]);
+        H.pv.assign(pval, pval + H.prp[n]);
+        H.n_coarser = ctx->H[level - 1].n;
+    }
+    mhdp_status st = validate_level(ctx, H, level);
+    if (st) return st;
+    free_device(ctx);
+    ctx->H[level] = std::move(H);
+    ctx->loaded[level] = 1;
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_setup(mhdp_ctx *ctx) {
+    if (!ctx) return MHDP_EINVAL;
+    if (ctx->host_only) return fail(ctx, MHDP_ECUDA, "host-only context (created with cuda_device = -1)");
+    if (ctx->nlev < 1) return fail(ctx, MHDP_ESTATE, "nothing assembled");
+    for (int l = 0; l < ctx->nlev; ++l)
+        if (!ctx->loaded[l]) return fail(ctx, MHDP_ESTATE, "level not loaded", l);
+    free_device(ctx);
+    CK(cudaSetDevice(ctx->device));
+    mhdp_status st;
+    if ((st = dalloc(ctx, &ctx->d_status, 4))) return st;
+    if ((st = dalloc(ctx, &ctx->d_scal, 2048))) return st;
+    ctx->D.assign(ctx->nlev, DevLevel());
+    for (int l = 0; l < ctx->nlev; ++l) {
+        const HostLevel &H = ctx->H[l];
+        DevLevel &L = ctx->D[l];
+        L.n = H.n;
+        L.nnz = H.rp[H.n];
+        L.use_b3 = l > 0 && has_block3(H);
+        if ((st = L.use_b3 ? build_b3(ctx, H, L) : build_sell(ctx, H, L))) return st;
+        if ((st = dalloc(ctx, &L.b, H.n))) return st;
+        if ((st = dalloc(ctx, &L.x, H.n))) return st;
+        if ((st = dalloc(ctx, &L.r, H.n))) return st;
+        if (l == 0) continue;
+        if ((st = build_patches(ctx, H, L))) return st;
+        if ((st = build_csr(ctx, H.n, H.prp, H.pci, H.pv, L.Pr))) return st;
+        std::vector<int64_t> trp; std::vector<int> tci; std::vector<double> tv;
+        transpose_csr(H.n, H.n_coarser, H.prp, H.pci, H.pv, trp, tci, tv);
+        if ((st = build_csr(ctx, H.n_coarser, trp, tci, tv, L.PrT))) return st;
+        L.bytes_tr = 2 * (12 * (int64_t)H.prp[H.n]) + 4 * (H.n + H.n_coarser + 2);
+        // K6: batched patch LU from a temporary device CSR
+        int64_t *drp = nullptr; int *dci = nullptr; double *dv = nullptr;
+        CK(cudaMalloc(&drp, sizeof(int64_t) * (H.n + 1)));
+        CK(cudaMalloc(&dci, sizeof(int) * std::max<int64_t>(1, L.nnz)));
+        CK(cudaMalloc(&dv, sizeof(double) * std::max<int64_t>(1, L.nnz)));
+        CK(cudaMemcpy(drp, H.rp.data(), sizeof(int64_t) * (H.n + 1), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dci, H.ci.data(), sizeof(int) * L.nnz, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dv, H.v.data(), sizeof(double) * L.nnz, cudaMemcpyHostToDevice));
+        int big = INT_MAX;
+        CK(cudaMemcpy(ctx->d_status, &big, sizeof(int), cudaMemcpyHostToDevice));
+        launch_patch_lu(L.P, drp, dci, dv, ctx->d_status, ctx->stream);
+        if ((st = check_launch(ctx))) return st;
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(drp); cudaFree(dci); cudaFree(dv);
+        int bad = 0;
+        CK(cudaMemcpy(&bad, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost));
+        if (bad != INT_MAX) {
+            const long long patch = bad - 1;
+            char buf[160];
+            snprintf(buf, sizeof buf, "singular patch %lld on level %d", patch, l);
+            return fail(ctx, MHDP_ESINGULAR, buf, ((long long)l << 32) + patch);
+        }
+    }
+    // K7: coarse LU (dense, row-major) then the column-major copy for K8
+    const HostLevel &H0 = ctx->H[0];
+    const int64_t n0 = H0.n;
+    if (n0 > 20000) return fail(ctx, MHDP_EINVAL, "coarse level too large for the dense LU");
+    ctx->n0 = (int)n0;
+    {
+        std::vector<double> dense((size_t)(n0 * n0), 0.0);
+        for (int64_t i = 0; i < n0; ++i)
+            for (int64_t t = H0.rp[i]; t < H0.rp[i + 1]; ++t) dense[(size_t)(i * n0 + H0.ci[t])] = H0.v[t];
+        double *a = nullptr;
+        CK(cudaMalloc(&a, sizeof(double) * std::max<int64_t>(1, n0 * n0)));
+        CK(cudaMemcpy(a, dense.data(), sizeof(double) * n0 * n0, cudaMemcpyHostToDevice));
+        if ((st = dalloc(ctx, &ctx->cperm, n0))) return st;
+        if ((st = dalloc(ctx, &ctx->clut, n0 * n0))) return st;
+        if ((st = dalloc(ctx, &ctx->cz, n0))) return st;
+        CK(cudaMemset(ctx->d_status, 0, sizeof(int)));
+        launch_dense_lu(a, (int)n0, ctx->cperm, ctx->d_status, ctx->d_scal, ctx->stream);
+        launch_transpose(a, ctx->clut, (int)n0, ctx->stream);
+        if ((st = check_launch(ctx))) return st;
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(a);
+        int bad = 0;
+        CK(cudaMemcpy(&bad, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost));
+        if (bad) return fail(ctx, MHDP_ESINGULAR, "singular coarse operator", -1);
+    }
+    ctx->setup_done = true;
+    return MHDP_OK;
+}
+
+int mhdp_num_levels(const mhdp_ctx *ctx) { return ctx ? ctx->nlev : 0; }
+
+mhdp_status mhdp_get_level_info(const mhdp_ctx *ctx, int level, mhdp_level_info *out) {
+    if (!ctx || !out || !valid_level(ctx, level) || !ctx->loaded[level]) return MHDP_EINVAL;
+    const HostLevel &H = ctx->H[level];
+    memset(out, 0, sizeof(*out));
+    out->n = H.n;
+    out->nnz = H.rp.empty() ? 0 : H.rp[H.n];
+    if (level > 0) {
+        const int64_t np = (int64_t)H.pptr.size() - 1;
+        out->npatch = np;
+        out->sum_n = H.pptr[np];
+        for (int64_t i = 0; i < np; ++i) {
+            const int64_t k = H.pptr[i + 1] - H.pptr[i];
+            out->sum_n2 += k * k;
+            out->max_n = std::max<long long>(out->max_n, (long long)k);
+        }
+        out->p_nnz = H.prp[H.n];
+    }
+    if (ctx->setup_done) {
+        const DevLevel &L = ctx->D[level];
+        out->bytes_operator = L.bytes_op;
+        out->bytes_factors = level > 0 ? L.bytes_fac : 8LL * ctx->n0 * ctx->n0;
+        out->bytes_transfer = L.bytes_tr;
+    }
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_spmv(mhdp_ctx *ctx, int level, const double *x_dev, double *y_dev) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!valid_level(ctx, level) || !x_dev || !y_dev) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    residual(ctx, level, nullptr, x_dev, y_dev);
+    return check_launch(ctx);
+}
+
+mhdp_status mhdp_residual(mhdp_ctx *ctx, int level, const double *b_dev, const double *x_dev, double *r_dev) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!valid_level(ctx, level) || !b_dev || !x_dev || !r_dev) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    residual(ctx, level, b_dev, x_dev, r_dev);
+    return check_launch(ctx);
+}
+
+mhdp_status mhdp_patch_apply(mhdp_ctx *ctx, int level, const double *r_dev) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!valid_level(ctx, level) || level < 1 || !r_dev) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    launch_patch_apply(ctx->D[level].P, r_dev, ctx->stream);
+    return check_launch(ctx);
+}
+
+mhdp_status mhdp_patch_update(mhdp_ctx *ctx, int level, double *x_dev) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!valid_level(ctx, level) || level < 1 || !x_dev) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    launch_patch_update(ctx->D[level].P, ctx->D[level].n, x_dev, 0, ctx->stream);
+    return check_launch(ctx);
+}
+
+mhdp_status mhdp_smooth(mhdp_ctx *ctx, int level, int nsweeps, int x_is_zero, const double *b_dev, double *x_dev) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!valid_level(ctx, level) || level < 1 || nsweeps < 0 || !b_dev || !x_dev)
+        return fail(ctx, MHDP_EINVAL, "bad arguments");
+    for (int s = 0; s < nsweeps; ++s) sweep(ctx, level, b_dev, x_dev, x_is_zero && s == 0);
+    return check_launch(ctx);
+}
+
+mhdp_status mhdp_restrict(mhdp_ctx *ctx, int level, const double *r_dev, double *rc_dev) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!valid_level(ctx, level) || level < 1 || !r_dev || !rc_dev) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    launch_restrict(ctx->D[level].PrT, r_dev, rc_dev, ctx->stream);
+    return check_launch(ctx);
+}
+
+mhdp_status mhdp_prolong_add(mhdp_ctx *ctx, int level, const double *ec_dev, double *x_dev) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!valid_level(ctx, level) || level < 1 || !ec_dev || !x_dev) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    launch_prolong_add(ctx->D[level].Pr, ec_dev, x_dev, ctx->stream);
+    return check_launch(ctx);
+}
+
+mhdp_status mhdp_coarse_solve(mhdp_ctx *ctx, const double *b_dev, double *x_dev) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!b_dev || !x_dev) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    coarse_solve(ctx, b_dev, x_dev);
+    return check_launch(ctx);
+}
+
+mhdp_status mhdp_vcycle(mhdp_ctx *ctx, int level, const double *b_dev, double *x_dev) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!valid_level(ctx, level) || !b_dev || !x_dev) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    vcycle(ctx, level, b_dev, x_dev);
+    return check_launch(ctx);
+}
+
+mhdp_status mhdp_vcycle_host(mhdp_ctx *ctx, const double *b_host, double *x_host) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!b_host || !x_host) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    const int l = ctx->nlev - 1;
+    DevLevel &L = ctx->D[l];
+    double *db = L.b, *dx = nullptr;
+    if (l == 0) dx = L.x;
+    else {
+        if (!ctx->gw) { if ((st = dalloc(ctx, &ctx->gw, L.n))) return st; }
+        dx = ctx->gw;
+    }
+    CK(cudaMemcpyAsync(db, b_host, sizeof(double) * L.n, cudaMemcpyHostToDevice, ctx->stream));
+    vcycle(ctx, l, db, dx);
+    CK(cudaMemcpyAsync(x_host, dx, sizeof(double) * L.n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return check_launch(ctx);
+}
+
+mhdp_status mhdp_smooth_host(mhdp_ctx *ctx, int level, int nsweeps, int x_is_zero, const double *b_host,
+                             double *x_host) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!valid_level(ctx, level) || level < 1 || !b_host || !x_host) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    DevLevel &L = ctx->D[level];
+    CK(cudaMemcpyAsync(L.b, b_host, sizeof(double) * L.n, cudaMemcpyHostToDevice, ctx->stream));
+    if (!x_is_zero) CK(cudaMemcpyAsync(L.x, x_host, sizeof(double) * L.n, cudaMemcpyHostToDevice, ctx->stream));
+    for (int s = 0; s < nsweeps; ++s) sweep(ctx, level, L.b, L.x, x_is_zero && s == 0);
+    CK(cudaMemcpyAsync(x_host, L.x, sizeof(double) * L.n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return check_launch(ctx);
+}
+
+mhdp_status mhdp_gmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol, double atol, int maxit,
+                       int *its_out, double *relres_out) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!b_dev || !x_dev || maxit < 1 || maxit > 2000) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    const int l = ctx->nlev - 1;
+    const int64_t n = ctx->D[l].n;
+    cudaStream_t s = ctx->stream;
+    if (ctx->g_cap < maxit) {
+        if ((st = dalloc(ctx, &ctx->gV, n * (int64_t)(maxit + 1)))) return st;
+        if ((st = dalloc(ctx, &ctx->gZ, n * (int64_t)maxit))) return st;
+        if (!ctx->gw && (st = dalloc(ctx, &ctx->gw, n))) return st;
+        ctx->g_cap = maxit;
+    }
+    double *V = ctx->gV, *Z = ctx->gZ, *w = ctx->gw, *part = ctx->d_scal, *res = ctx->d_scal + 1024;
+    auto dot = [&](const double *a, const double *b) -> double {
+        launch_dot(a, b, n, part, res, s);
+        double h = 0;
+        cudaMemcpyAsync(&h, res, sizeof(double), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        return h;
+    };
+    const double beta = std::sqrt(dot(b_dev, b_dev));
+    const double tol = std::max(rtol * beta, atol);
+    launch_fill(x_dev, 0.0, n, s);
+    if (its_out) *its_out = 0;
+    if (relres_out) *relres_out = beta > 0 ? 1.0 : 0.0;
+    if (beta <= tol) { CK(cudaStreamSynchronize(s)); return check_launch(ctx); }
+    std::vector<double> H((size_t)(maxit + 1) * maxit, 0.0), cs(maxit), sn(maxit), g(maxit + 1, 0.0);
+    launch_scale(V, b_dev, 1.0 / beta, n, s);
+    g[0] = beta;
+    int k = 0;
+    bool conv = false;
+    for (k = 0; k < maxit; ++k) {
+        vcycle(ctx, l, V + (int64_t)k * n, Z + (int64_t)k * n);
+        residual(ctx, l, nullptr, Z + (int64_t)k * n, w);
+        for (int i = 0; i <= k; ++i) {
+            const double h = dot(w, V + (int64_t)i * n);
+            H[(size_t)i * maxit + k] = h;
+            launch_axpy(w, -h, V + (int64_t)i * n, n, s);
+        }
+        const double hn = std::sqrt(dot(w, w));
+        H[(size_t)(k + 1) * maxit + k] = hn;
+        launch_scale(V + (int64_t)(k + 1) * n, w, hn > 0 ? 1.0 / hn : 0.0, n, s);
+        for (int i = 0; i < k; ++i) {
+            const double a = H[(size_t)i * maxit + k], bb = H[(size_t)(i + 1) * maxit + k];
+            H[(size_t)i * maxit + k] = cs[i] * a + sn[i] * bb;
+            H[(size_t)(i + 1) * maxit + k] = -sn[i] * a + cs[i] * bb;
+        }
+        const double a = H[(size_t)k * maxit + k], bb = H[(size_t)(k + 1) * maxit + k];
+        const double rr = std::sqrt(a * a + bb * bb);
+        cs[k] = a / rr; sn[k] = bb / rr;
+        H[(size_t)k * maxit + k] = rr; H[(size_t)(k + 1) * maxit + k] = 0.0;
+        g[k + 1] = -sn[k] * g[k];
+        g[k] = cs[k] * g[k];
+        if (std::fabs(g[k + 1]) <= tol) { ++k; conv = true; break; }
+    }
+    std::vector<double> y(std::max(k, 1));
+    for (int i = k - 1; i >= 0; --i) {
+        double acc = g[i];
+        for (int j = i + 1; j < k; ++j) acc -= H[(size_t)i * maxit + j] * y[j];
+        y[i] = acc / H[(size_t)i * maxit + i];
+    }
+    for (int i = 0; i < k; ++i) launch_axpy(x_dev, y[i], Z + (int64_t)i * n, n, s);
+    CK(cudaStreamSynchronize(s));
+    if (its_out) *its_out = k;
+    if (relres_out) *relres_out = std::fabs(g[k]) / beta;
+    if ((st = check_launch(ctx))) return st;
+    return conv ? MHDP_OK : fail(ctx, MHDP_ENOCONV, "GMRES reached maxit");
+}
+
+mhdp_status mhdp_export_csr(const mhdp_ctx *ctx, int level, long long *rowptr, int *col, double *val) {
+    if (!ctx || !valid_level(ctx, level) || !ctx->loaded[level] || !rowptr || !col || !val) return MHDP_EINVAL;
+    const HostLevel &H = ctx->H[level];
+    memcpy(rowptr, H.rp.data(), sizeof(int64_t) * (H.n + 1));
+    memcpy(col, H.ci.data(), sizeof(int) * H.ci.size());
+    memcpy(val, H.v.data(), sizeof(double) * H.v.size());
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_export_patches(const mhdp_ctx *ctx, int level, long long *pptr, int *pdofs) {
+    if (!ctx || !valid_level(ctx, level) || level < 1 || !ctx->loaded[level] || !pptr || !pdofs) return MHDP_EINVAL;
+    const HostLevel &H = ctx->H[level];
+    memcpy(pptr, H.pptr.data(), sizeof(int64_t) * H.pptr.size());
+    memcpy(pdofs, H.pdofs.data(), sizeof(int) * H.pdofs.size());
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_export_prolongation(const mhdp_ctx *ctx, int level, long long *prow, int *pcol, double *pval) {
+    if (!ctx || !valid_level(ctx, level) || level < 1 || !ctx->loaded[level] || !prow || !pcol || !pval)
+        return MHDP_EINVAL;
+    const HostLevel &H = ctx->H[level];
+    memcpy(prow, H.prp.data(), sizeof(int64_t) * H.prp.size());
+    memcpy(pcol, H.pci.data(), sizeof(int) * H.pci.size());
+    memcpy(pval, H.pv.data(), sizeof(double) * H.pv.size());
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_export_patch_lu(mhdp_ctx *ctx, int level, long long patch, double *lu, int *perm) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!valid_level(ctx, level) || level < 1 || !lu || !perm) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    const HostLevel &H = ctx->H[level];
+    const int64_t np = (int64_t)H.pptr.size() - 1;
+    if (patch < 0 || patch >= np) return fail(ctx, MHDP_EINVAL, "bad patch index");
+    const DevPatches &P = ctx->D[level].P;
+    const int n = (int)(H.pptr[patch + 1] - H.pptr[patch]);
+    int64_t foff = 0;
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(&foff, P.foff + patch, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    std::vector<double> cm((size_t)n * n);
+    CK(cudaMemcpy(cm.data(), P.fac + foff, sizeof(double) * n * n, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) lu[(size_t)i * n + j] = cm[(size_t)j * n + i];
+    CK(cudaMemcpy(perm, P.perm + H.pptr[patch], sizeof(int) * n, cudaMemcpyDeviceToHost));
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_export_slots(mhdp_ctx *ctx, int level, double *y) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!valid_level(ctx, level) || level < 1 || !y) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(y, ctx->D[level].P.y, sizeof(double) * ctx->D[level].P.sum_n, cudaMemcpyDeviceToHost));
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_synchronize(mhdp_ctx *ctx) {
+    if (!ctx) return MHDP_EINVAL;
+    if (ctx->host_only) return MHDP_OK;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return check_launch(ctx);
+}
+
+mhdp_status mhdp_last_error(const mhdp_ctx *ctx, char *buf, int len, long long *where) {
+    if (!ctx) return MHDP_EINVAL;
+    if (buf && len > 0) {
+        strncpy(buf, ctx->err.c_str(), (size_t)len - 1);
+        buf[len - 1] = 0;
+    }
+    if (where) *where = ctx->where;
+    return MHDP_OK;
+}
+
+long long mhdp_launch_count(const mhdp_ctx *ctx) { return ctx ? g_launches - ctx->launches0 : 0; }
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+// kernels.cuh -- launchers of the sm_100a kernels of the vertex-star Schwarz
+// smoother / V-cycle.  Every reduction follows the pinned
+// per-element operation order of DESIGN.md reading R-order, so that
+// results do not depend on how the work is parallelised.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace mhdp {
+
+// Sliced ELLPACK (SELL-32) operator store: slice s = rows 32s..32s+31; entry k of row
+// 32s+l at sptr[s] + 32k + l.  Rows keep their ascending column order (R-order).
+struct DevSell {
+    int64_t n = 0, nslices = 0, stored = 0;
+    int64_t *sptr = nullptr;   // nslices+1
+    int *rlen = nullptr;       // n
+    int *col = nullptr;        // stored
+    double *val = nullptr;     // stored
+};
+
+// 3x3-block SELL store for operators whose DoFs come in aligned triples sharing one
+// column pattern (3D BDM1 velocity: the 3 DoFs of a face).  Block-row R = DoFs 3R..3R+2;
+// slice s = block rows 32s..32s+31; block entry e = sptr[s]+32k+l of block row 32s+l:
+// column block index col[e], its 3x3 values (row-major m = 3a+b) at val[m*stored + e].
+struct DevBSell3 {
+    int64_t nb = 0, nslices = 0, stored = 0;
+    int64_t *sptr = nullptr;
+    int *rlen = nullptr;       // per block row
+    int *col = nullptr;        // block column index
+    double *val = nullptr;     // 9 planes of `stored` doubles
+};
+
+struct DevCsr {
+    int64_t n = 0, nnz = 0;
+    int *rp = nullptr;         // n+1 (int32 offsets; transfer operators are small)
+    int *ci = nullptr;
+    double *v = nullptr;
+};
+
+struct DevPatches {
+    int64_t np = 0, sum_n = 0, fac_doubles = 0;
+    int max_n = 0;
+    int *pn = nullptr;         // np   patch sizes
+    int64_t *poff = nullptr;   // np   slot offset (= pptr[i])
+    int64_t *foff = nullptr;   // np   factor offset in doubles (16-double aligned)
+    int *pdofs = nullptr;      // sum_n ascending DoFs of each patch
+    int *gidx = nullptr;       // sum_n pivot-folded gather list  gidx[k] = pdofs[perm[k]]
+    int *perm = nullptr;       // sum_n LU row permutation (export only)
+    double *fac = nullptr;     // packed LU factors, column-major per patch
+    int *dptr = nullptr;       // n+1  DoF -> slot list
+    int *dslot = nullptr;      // sum_n slots of each DoF, ascending patch order
+    double *wd = nullptr;      // n    theta * (1/m_d)
+    double *y = nullptr;       // sum_n slot buffer
+};
+
+// counts every launch made through these wrappers (bench "gpu_launches")
+extern long long g_launches;
+
+// K1: r = b - A x (or y = A x when b == nullptr)
+void launch_residual(const DevSell &A, const double *b, const double *x, double *r, cudaStream_t s);
+void launch_residual_b3(const DevBSell3 &A, const double *b, const double *x, double *r, cudaStream_t s);
+// K6: batched patch LU (gather from the CSR on the device, partial pivoting)
+// rowptr (int64) / col / val: the level operator in CSR; status[0] = first singular patch+1
+void launch_patch_lu(const DevPatches &P, const int64_t *rowptr, const int *col, const double *val,
+                     int *status, cudaStream_t s);
+// K2: y_i = A_i^-1 R_i r for every patch
+void launch_patch_apply(const DevPatches &P, const double *r, cudaStream_t s);
+// K3: x_d <- fma(w_d, sum y, x_d)    (x_is_zero: x_d <- fma(w_d, sum y, 0.0))
+void launch_patch_update(const DevPatches &P, int64_t n, double *x, int x_is_zero, cudaStream_t s);
+// K4: rc = PT r  (PT: coarse rows);  K5: x <- x + P ec  (P: fine rows)
+void launch_restrict(const DevCsr &PT, const double *r, double *rc, cudaStream_t s);
+void launch_prolong_add(const DevCsr &P, const double *ec, double *x, cudaStream_t s);
+// K7: dense LU with partial pivoting of the row-major n x n matrix a (in place)
+// perm[n]; status[0] = 0 or (step+1) of the first singular pivot; amax = max|a|
+void launch_dense_lu(double *a, int n, int *perm, int *status, double *scratch, cudaStream_t s);
+// transpose the row-major factor into the column-major copy used by the solve
+void launch_transpose(const double *a, double *at, int n, cudaStream_t s);
+// K8: x = U^-1 L^-1 P b with the column-major factor lut
+void launch_dense_solve(const double *lut, const int *perm, int n, const double *b, double *x,
+                        double *z, cudaStream_t s);
+// K9 vector ops (deterministic reductions)
+void launch_dot(const double *a, const double *b, int64_t n, double *partials, double *out, cudaStream_t s);
+void launch_axpy(double *y, double alpha, const double *x, int64_t n, cudaStream_t s);   // y = fma(alpha, x, y)
+void launch_scale(double *y, const double *x, double alpha, int64_t n, cudaStream_t s);   // y = x * alpha
+void launch_fill(double *y, double v, int64_t n, cudaStream_t s);
+
+}  // namespace mhdp

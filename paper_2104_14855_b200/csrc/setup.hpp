@@ -1,0 +1,38 @@
+// setup.hpp -- host-side setup stage of libmhdp: nested
+// structured meshes, canonical numbering, free DoFs, vertex-star patches, operator
+// assembly by rediscretisation and the exact FE prolongation.  Product code: it shares
+// nothing with oracle/ (an independent implementation of the same definitions).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace mhdp {
+
+struct Params {
+    double Re = 1, Rem = 1, S = 1, gamma = 1, sigma = 10, mu = 0, theta = 1;
+    int nu_pre = 1, nu_post = 1;
+};
+
+// One level of the hierarchy as host arrays (the form both mhdp_assemble and
+// mhdp_load_level produce).
+struct HostLevel {
+    int64_t n = 0;
+    std::vector<int64_t> rp;   // CSR of A_l
+    std::vector<int> ci;
+    std::vector<double> v;
+    std::vector<int64_t> pptr; // vertex-star patches, ascending DoFs
+    std::vector<int> pdofs;
+    std::vector<int64_t> prp;  // prolongation from level-1 (rows: this level)
+    std::vector<int> pci;
+    std::vector<double> pv;
+    int64_t n_coarser = 0;
+};
+
+// Assemble all levels (0 = coarsest).  block 0 = E-B, 1 = AL velocity.
+// w: potential of the advecting field at the finest vertices (1 or 3 per vertex).
+// Returns "" on success, else an error message.
+std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params &p, const double *w,
+                               std::vector<HostLevel> &out);
+
+}  // namespace mhdp

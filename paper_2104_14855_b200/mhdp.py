@@ -1,0 +1,283 @@
+"""Thin ctypes binding of libmhdp.so (include/mhdp.h) -- argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module converts
+Python/numpy/torch arguments into plain pointers and sizes and raises on a non-zero
+status.  There is no fallback: if libmhdp.so is missing or fails to load, importing
+a Context raises.  Device vectors may be passed as torch CUDA tensors (fp64,
+contiguous) or raw integer device pointers.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .build_lib import LIB
+
+STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ESINGULAR", 5: "ESTATE", 6: "ENOCONV"}
+BLOCK = {"eb": 0, "vel": 1}
+
+
+class MhdpError(RuntimeError):
+    def __init__(self, status, msg, where):
+        super().__init__(f"mhdp {STATUS.get(status, status)}: {msg} (where={where})")
+        self.status, self.msg, self.where = status, msg, where
+
+
+class Mesh(C.Structure):
+    _fields_ = [("dim", C.c_int), ("n_fine", C.c_int), ("n_levels", C.c_int)]
+
+
+class Params(C.Structure):
+    _fields_ = [("Re", C.c_double), ("Rem", C.c_double), ("S", C.c_double), ("gamma", C.c_double),
+                ("sigma", C.c_double), ("mu_stab", C.c_double), ("theta", C.c_double),
+                ("nu_pre", C.c_int), ("nu_post", C.c_int)]
+
+
+class LevelInfo(C.Structure):
+    _fields_ = [(k, C.c_longlong) for k in ("n", "nnz", "npatch", "sum_n", "sum_n2", "max_n", "p_nnz",
+                                            "bytes_operator", "bytes_factors", "bytes_transfer")]
+
+
+_lib = None
+
+# every symbol declared in include/mhdp.h
+SYMBOLS = ["mhdp_create", "mhdp_destroy", "mhdp_assemble", "mhdp_begin_levels", "mhdp_load_level", "mhdp_setup",
+           "mhdp_get_level_info", "mhdp_num_levels", "mhdp_spmv", "mhdp_residual", "mhdp_patch_apply",
+           "mhdp_patch_update", "mhdp_smooth", "mhdp_restrict", "mhdp_prolong_add", "mhdp_coarse_solve",
+           "mhdp_vcycle", "mhdp_vcycle_host", "mhdp_smooth_host", "mhdp_gmres", "mhdp_export_csr",
+           "mhdp_export_patches", "mhdp_export_prolongation", "mhdp_export_patch_lu", "mhdp_export_slots",
+           "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count"]
+
+
+def lib():
+    """Load libmhdp.so (raises OSError if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise OSError(f"{LIB} not built: run paper_2104_14855_b200.build_lib.build()")
+        L = C.CDLL(LIB)
+        vp, i64, i64p, ip, dp = C.c_void_p, C.c_longlong, C.POINTER(C.c_longlong), C.POINTER(C.c_int), C.POINTER(C.c_double)
+        sig = {
+            "mhdp_create": [C.POINTER(vp), C.c_int, vp],
+            "mhdp_assemble": [vp, C.c_int, C.POINTER(Mesh), C.POINTER(Params), dp],
+            "mhdp_begin_levels": [vp, C.c_int, C.POINTER(Params)],
+            "mhdp_load_level": [vp, C.c_int, i64, i64p, ip, dp, i64, i64p, ip, i64p, ip, dp],
+            "mhdp_setup": [vp],
+            "mhdp_get_level_info": [vp, C.c_int, C.POINTER(LevelInfo)],
+            "mhdp_spmv": [vp, C.c_int, vp, vp],
+            "mhdp_residual": [vp, C.c_int, vp, vp, vp],
+            "mhdp_patch_apply": [vp, C.c_int, vp],
+            "mhdp_patch_update": [vp, C.c_int, vp],
+            "mhdp_smooth": [vp, C.c_int, C.c_int, C.c_int, vp, vp],
+            "mhdp_restrict": [vp, C.c_int, vp, vp],
+            "mhdp_prolong_add": [vp, C.c_int, vp, vp],
+            "mhdp_coarse_solve": [vp, vp, vp],
+            "mhdp_vcycle": [vp, C.c_int, vp, vp],
+            "mhdp_vcycle_host": [vp, dp, dp],
+            "mhdp_smooth_host": [vp, C.c_int, C.c_int, C.c_int, dp, dp],
+            "mhdp_gmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp],
+            "mhdp_export_csr": [vp, C.c_int, i64p, ip, dp],
+            "mhdp_export_patches": [vp, C.c_int, i64p, ip],
+            "mhdp_export_prolongation": [vp, C.c_int, i64p, ip, dp],
+            "mhdp_export_patch_lu": [vp, C.c_int, i64, dp, ip],
+            "mhdp_export_slots": [vp, C.c_int, dp],
+            "mhdp_synchronize": [vp],
+            "mhdp_last_error": [vp, C.c_char_p, C.c_int, i64p],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        L.mhdp_destroy.argtypes = [vp]
+        L.mhdp_destroy.restype = None
+        L.mhdp_num_levels.argtypes = [vp]
+        L.mhdp_num_levels.restype = C.c_int
+        L.mhdp_launch_count.argtypes = [vp]
+        L.mhdp_launch_count.restype = C.c_longlong
+        _lib = L
+    return _lib
+
+
+def _d(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _i(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+def _l(a):
+    return a.ctypes.data_as(C.POINTER(C.c_longlong))
+
+
+def _ptr(t):
+    """Device pointer of a torch CUDA tensor (fp64, contiguous) or an int."""
+    if isinstance(t, int):
+        return t
+    import torch
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise TypeError("device vectors must be contiguous float64 CUDA tensors")
+    return t.data_ptr()
+
+
+def make_params(cfg) -> Params:
+    return Params(cfg.Re, cfg.Rem, cfg.S, cfg.gamma, cfg.sigma, cfg.mu, cfg.theta, cfg.nu, cfg.nu)
+
+
+class Context:
+    """One mhdp_ctx.  device=-1: host-only (assembly / export only)."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        self._L = lib()
+        h = C.c_void_p()
+        st = self._L.mhdp_create(C.byref(h), device, C.c_void_p(stream or 0))
+        if st:
+            raise MhdpError(st, "mhdp_create failed", -1)
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.mhdp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def _chk(self, st):
+        if st:
+            buf = C.create_string_buffer(512)
+            where = C.c_longlong(-1)
+            self._L.mhdp_last_error(self.h, buf, 512, C.byref(where))
+            raise MhdpError(st, buf.value.decode(), where.value)
+        return st
+
+    # ---- setup ----
+    def assemble(self, cfg, w, N=None, levels=None):
+        mesh = Mesh(cfg.dim, N if N is not None else cfg.N, levels if levels is not None else cfg.levels)
+        self._w = np.ascontiguousarray(w, np.float64)
+        p = make_params(cfg)
+        return self._chk(self._L.mhdp_assemble(self.h, BLOCK[cfg.block], C.byref(mesh), C.byref(p), _d(self._w)))
+
+    def begin_levels(self, n_levels, cfg):
+        p = make_params(cfg)
+        return self._chk(self._L.mhdp_begin_levels(self.h, n_levels, C.byref(p)))
+
+    def load_level(self, level, rowptr, col, val, pptr=None, pdofs=None, prow=None, pcol=None, pval=None):
+        rowptr = np.ascontiguousarray(rowptr, np.int64); col = np.ascontiguousarray(col, np.int32)
+        val = np.ascontiguousarray(val, np.float64)
+        n = len(rowptr) - 1
+        if pptr is None:
+            return self._chk(self._L.mhdp_load_level(self.h, level, n, _l(rowptr), _i(col), _d(val), 0,
+                                                     None, None, None, None, None))
+        pptr = np.ascontiguousarray(pptr, np.int64); pdofs = np.ascontiguousarray(pdofs, np.int32)
+        prow = np.ascontiguousarray(prow, np.int64); pcol = np.ascontiguousarray(pcol, np.int32)
+        pval = np.ascontiguousarray(pval, np.float64)
+        return self._chk(self._L.mhdp_load_level(self.h, level, n, _l(rowptr), _i(col), _d(val), len(pptr) - 1,
+                                                 _l(pptr), _i(pdofs), _l(prow), _i(pcol), _d(pval)))
+
+    def setup(self):
+        return self._chk(self._L.mhdp_setup(self.h))
+
+    def num_levels(self):
+        return self._L.mhdp_num_levels(self.h)
+
+    def info(self, level=-1):
+        level = level % self.num_levels()
+        out = LevelInfo()
+        self._chk(self._L.mhdp_get_level_info(self.h, level, C.byref(out)))
+        return {k: getattr(out, k) for k, _ in LevelInfo._fields_}
+
+    def n(self, level=-1):
+        return self.info(level)["n"]
+
+    # ---- hot path (device) ----
+    def spmv(self, x, y, level=-1):
+        return self._chk(self._L.mhdp_spmv(self.h, level % self.num_levels(), _ptr(x), _ptr(y)))
+
+    def residual(self, b, x, r, level=-1):
+        return self._chk(self._L.mhdp_residual(self.h, level % self.num_levels(), _ptr(b), _ptr(x), _ptr(r)))
+
+    def patch_apply(self, r, level=-1):
+        return self._chk(self._L.mhdp_patch_apply(self.h, level % self.num_levels(), _ptr(r)))
+
+    def patch_update(self, x, level=-1):
+        return self._chk(self._L.mhdp_patch_update(self.h, level % self.num_levels(), _ptr(x)))
+
+    def smooth(self, b, x, level=-1, nsweeps=1, x_is_zero=False):
+        return self._chk(self._L.mhdp_smooth(self.h, level % self.num_levels(), nsweeps, int(x_is_zero),
+                                             _ptr(b), _ptr(x)))
+
+    def restrict(self, r, rc, level=-1):
+        return self._chk(self._L.mhdp_restrict(self.h, level % self.num_levels(), _ptr(r), _ptr(rc)))
+
+    def prolong_add(self, ec, x, level=-1):
+        return self._chk(self._L.mhdp_prolong_add(self.h, level % self.num_levels(), _ptr(ec), _ptr(x)))
+
+    def coarse_solve(self, b, x):
+        return self._chk(self._L.mhdp_coarse_solve(self.h, _ptr(b), _ptr(x)))
+
+    def vcycle(self, b, x, level=-1):
+        return self._chk(self._L.mhdp_vcycle(self.h, level % self.num_levels(), _ptr(b), _ptr(x)))
+
+    def vcycle_host(self, b, x):
+        """b, x: C-contiguous float64 numpy arrays (pinned or pageable host memory)."""
+        return self._chk(self._L.mhdp_vcycle_host(self.h, _d(b), _d(x)))
+
+    def smooth_host(self, b, x, level=-1, nsweeps=1, x_is_zero=False):
+        return self._chk(self._L.mhdp_smooth_host(self.h, level % self.num_levels(), nsweeps, int(x_is_zero),
+                                                  _d(b), _d(x)))
+
+    def gmres(self, b, x, rtol=1e-7, atol=1e-7, maxit=200):
+        its = C.c_int(0)
+        rel = C.c_double(0)
+        st = self._L.mhdp_gmres(self.h, _ptr(b), _ptr(x), rtol, atol, maxit, C.byref(its), C.byref(rel))
+        if st not in (0, 6):
+            self._chk(st)
+        return its.value, rel.value, st == 0
+
+    def synchronize(self):
+        return self._chk(self._L.mhdp_synchronize(self.h))
+
+    def launch_count(self):
+        return self._L.mhdp_launch_count(self.h)
+
+    # ---- export ----
+    def csr(self, level=-1):
+        level = level % self.num_levels()
+        i = self.info(level)
+        rp = np.zeros(i["n"] + 1, np.int64); ci = np.zeros(max(i["nnz"], 1), np.int32)
+        v = np.zeros(max(i["nnz"], 1), np.float64)
+        self._chk(self._L.mhdp_export_csr(self.h, level, _l(rp), _i(ci), _d(v)))
+        return rp, ci[:i["nnz"]], v[:i["nnz"]]
+
+    def patches(self, level=-1):
+        level = level % self.num_levels()
+        i = self.info(level)
+        ptr = np.zeros(i["npatch"] + 1, np.int64); dofs = np.zeros(max(i["sum_n"], 1), np.int32)
+        self._chk(self._L.mhdp_export_patches(self.h, level, _l(ptr), _i(dofs)))
+        return ptr, dofs[:i["sum_n"]]
+
+    def prolongation(self, level=-1):
+        level = level % self.num_levels()
+        i = self.info(level)
+        rp = np.zeros(i["n"] + 1, np.int64); ci = np.zeros(max(i["p_nnz"], 1), np.int32)
+        v = np.zeros(max(i["p_nnz"], 1), np.float64)
+        self._chk(self._L.mhdp_export_prolongation(self.h, level, _l(rp), _i(ci), _d(v)))
+        return rp, ci[:i["p_nnz"]], v[:i["p_nnz"]]
+
+    def patch_lu(self, patch, level=-1):
+        level = level % self.num_levels()
+        ptr, _ = self.patches(level)
+        k = int(ptr[patch + 1] - ptr[patch])
+        lu = np.zeros(k * k); perm = np.zeros(k, np.int32)
+        self._chk(self._L.mhdp_export_patch_lu(self.h, level, patch, _d(lu), _i(perm)))
+        return lu.reshape(k, k), perm
+
+    def slots(self, level=-1):
+        level = level % self.num_levels()
+        y = np.zeros(max(self.info(level)["sum_n"], 1))
+        self._chk(self._L.mhdp_export_slots(self.h, level, _d(y)))
+        return y

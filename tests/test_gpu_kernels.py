@@ -1,0 +1,132 @@
+"""GPU parity, tier P-C: the library's CUDA kernels on the ORACLE's operator.
+
+The oracle's CSR, patches and prolongations are installed through the C-ABI's
+algebraic entry; the oracle and the GPU then run the same method on the same
+operator.  Every reduction follows the order of reading R-order, so the
+expected result is BIT-EXACT: patch LU factors and pivots, residual, one sweep (x0 = 0
+and x0 = U(-1,1)), two sweeps, restriction, prolongation, coarse solve and V-cycle.
+GMRES(V) iteration counts must agree within +-1 (its dot products reduce in a
+different order, R-gmres).  Sizes span several tiles with ragged tails (patch sizes
+of every boundary class, levels whose n is not a multiple of 32).
+"""
+import numpy as np
+import pytest
+
+from gpu_helpers import bits, cuda_vec, host, load_oracle_levels, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("c1", 8, 2), ("c2", 32, 3), ("c3", 16, 3), ("c4", 8, 2), ("c5", 6, 2)]
+
+
+@pytest.fixture(scope="module", params=CASES, ids=[f"{c}-N{n}L{l}" for c, n, l in CASES])
+def pair(request, oracle_mod):
+    import torch
+    from paper_2104_14855_b200 import mhdp, workloads
+    name, N, L = request.param
+    cfg = workloads.small(name, N, L)
+    # draw with the finest n of this hierarchy
+    probe = oracle_mod.Oracle(cfg, workloads.advecting_potential(cfg, np.array([0.3, -1.1, 0.7])))
+    n = probe.n()
+    w, b, x0 = workloads.draw(cfg, n, seed=1)
+    orc = oracle_mod.Oracle(cfg, w)
+    ctx = mhdp.Context(0, torch.cuda.current_stream().cuda_stream)
+    load_oracle_levels(ctx, orc, cfg)
+    return cfg, orc, ctx, b, x0
+
+
+def test_patch_lu_bitexact(pair):
+    cfg, orc, ctx, b, x0 = pair
+    top = orc.nlev - 1
+    npatch = orc.info(top)["npatch"]
+    ptr = orc.patches(top)[0]
+    sizes = np.diff(ptr)
+    # every size class plus a spread of indices
+    pick = sorted(set([int(np.flatnonzero(sizes == s)[0]) for s in np.unique(sizes)] +
+                      list(np.linspace(0, npatch - 1, 7).astype(int))))
+    for i in pick:
+        lu_o, perm_o, st = orc.patch_lu(i, top)
+        assert st == 0
+        lu_g, perm_g = ctx.patch_lu(i, top)
+        assert np.array_equal(perm_o, perm_g), f"patch {i}: pivot order differs"
+        assert np.array_equal(bits(lu_o), bits(lu_g)), f"patch {i}: factors differ"
+
+
+def test_residual_and_spmv_bitexact(pair):
+    import torch
+    cfg, orc, ctx, b, x0 = pair
+    for l in range(orc.nlev):
+        n = orc.n(l)
+        rng = np.random.default_rng(l)
+        bb, xx = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+        r = torch.empty(n, dtype=torch.float64, device="cuda:0")
+        ctx.residual(cuda_vec(bb), cuda_vec(xx), r, level=l)
+        assert np.array_equal(bits(host(r)), bits(orc.residual(bb, xx, l)))
+        ctx.spmv(cuda_vec(xx), r, level=l)
+        assert np.array_equal(bits(host(r)), bits(orc.spmv(xx, l)))
+
+
+@pytest.mark.parametrize("zero", [True, False])
+@pytest.mark.parametrize("nsweeps", [1, 2])
+def test_sweep_bitexact(pair, zero, nsweeps):
+    cfg, orc, ctx, b, x0 = pair
+    x_in = np.zeros_like(x0) if zero else x0
+    xo = orc.sweep(b, x_in, nsweeps=nsweeps, x_is_zero=zero)
+    xg = cuda_vec(x_in)
+    ctx.smooth(cuda_vec(b), xg, nsweeps=nsweeps, x_is_zero=zero)
+    xg = host(xg)
+    assert rel_l2(xg, xo) <= 1e-10
+    assert np.array_equal(bits(xg), bits(xo))
+
+
+def test_transfer_bitexact(pair):
+    import torch
+    cfg, orc, ctx, b, x0 = pair
+    for l in range(1, orc.nlev):
+        rng = np.random.default_rng(10 + l)
+        r = rng.uniform(-1, 1, orc.n(l)); ec = rng.uniform(-1, 1, orc.n(l - 1)); x = rng.uniform(-1, 1, orc.n(l))
+        rc = torch.empty(orc.n(l - 1), dtype=torch.float64, device="cuda:0")
+        ctx.restrict(cuda_vec(r), rc, level=l)
+        assert np.array_equal(bits(host(rc)), bits(orc.restrict(r, l)))
+        xg = cuda_vec(x)
+        ctx.prolong_add(cuda_vec(ec), xg, level=l)
+        assert np.array_equal(bits(host(xg)), bits(orc.prolong_add(ec, x, l)))
+
+
+def test_coarse_solve_bitexact(pair):
+    import torch
+    cfg, orc, ctx, b, x0 = pair
+    rng = np.random.default_rng(5)
+    bc = rng.uniform(-1, 1, orc.n(0))
+    xg = torch.empty(orc.n(0), dtype=torch.float64, device="cuda:0")
+    ctx.coarse_solve(cuda_vec(bc), xg)
+    assert np.array_equal(bits(host(xg)), bits(orc.coarse_solve(bc)))
+
+
+def test_vcycle_bitexact(pair):
+    import torch
+    cfg, orc, ctx, b, x0 = pair
+    xo = orc.vcycle(b)
+    xg = torch.empty(len(b), dtype=torch.float64, device="cuda:0")
+    ctx.vcycle(cuda_vec(b), xg)
+    xg = host(xg)
+    assert rel_l2(xg, xo) <= 1e-10
+    assert np.array_equal(bits(xg), bits(xo))
+    # host-buffer entry point gives the same bits
+    xh = np.zeros_like(b)
+    ctx.vcycle_host(np.ascontiguousarray(b), xh)
+    assert np.array_equal(bits(xh), bits(xo))
+
+
+def test_gmres_iterations(pair):
+    import torch
+    cfg, orc, ctx, b, x0 = pair
+    _, its_o, hist, conv_o = orc.gmres(b, maxit=60)
+    xg = torch.empty(len(b), dtype=torch.float64, device="cuda:0")
+    its_g, rel_g, conv_g = ctx.gmres(cuda_vec(b), xg, maxit=60)
+    assert conv_o == conv_g
+    assert abs(its_o - its_g) <= 1
+    if conv_g:
+        A = orc.csr().to_scipy()
+        r = b - A @ host(xg)
+        assert np.linalg.norm(r) <= 1.01 * max(1e-7 * np.linalg.norm(b), 1e-7)
