@@ -1,0 +1,311 @@
+"""Benchmark of the vertex-star Schwarz smoother / V-cycle (arXiv 2104.14855) on B200.
+
+Workload (BASELINE.json configs[4], the largest 3D configuration, which fits one GPU):
+  c5 = 3D augmented-Lagrangian velocity block, 48^3 cubes x 6 Kuhn tets, BDM1,
+  Re = gamma = 1e4, 4 levels, V(2,2), vertex-star patches (108 DoFs interior).
+A step is one V-cycle(2,2) of the whole hot path (residual SpMV,
+patch gather + LU apply, weighted gather-update on every level, restriction,
+prolongation, dense coarse solve).  Setup (a0-a2: host assembly, batched patch LU,
+coarse LU) runs once before the timed region.
+
+metric: smoothed DoFs/s (every sweep on level l smooths n_l DoFs: sum_l (nu_pre +
+nu_post) n_l per V-cycle), plus the V-cycle ms, a finest-level single-sweep DoFs/s and
+its achieved HBM GB/s (SURVEY §8(d) algorithmic bytes) against MEASURED_PEAKS.json.
+
+Multi-GPU: the method runs on one GPU (BASELINE north star); --gpus N runs N independent
+replicas (one process per GPU, each its own seeded right-hand side), "replicas only" in
+DESIGN.md, weak scaling with no data-path collective; the step time is the max over ranks.
+
+--impl reference: the reference arm is the ORACLE (plain single-threaded C) as it stands,
+timed on the host on a bounded sample of the same workload family (c5 at N = 12, 3
+levels, V(2,2); setup excluded), same metric and unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+REF_SAMPLE = ("c5", 12, 3)
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------------------
+# reference arm: the oracle
+# ----------------------------------------------------------------------------------------
+def oracle_vcycle_sample(steps, warmup, seed=0):
+    from oracle import oracle
+    from paper_2104_14855_b200 import workloads
+    name, N, L = REF_SAMPLE
+    cfg = workloads.small(name, N, L)
+    w0, _, _ = workloads.draw(cfg, 1, seed)
+    orc = oracle.Oracle(cfg, w0)
+    w, b, _ = workloads.draw(cfg, orc.n(), seed)
+    orc = oracle.Oracle(cfg, w)
+    orc.vcycle(b)                       # factors every level (lazy) -- setup, not timed
+    for _ in range(max(0, warmup - 1)):
+        orc.vcycle(b)
+    smoothed = sum(2 * cfg.nu * orc.n(l) for l in range(1, L))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        orc.vcycle(b)
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": smoothed / dt, "ms_per_step": dt * 1e3, "smoothed_per_step": smoothed,
+            "sample": f"oracle V(2,2) on {name} at N={N}, {L} levels ({orc.n()} finest DoFs; same element, "
+                      f"patch and operator structure as the full c5), setup excluded, {steps} cycles"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_init()
+    if rank != 0:
+        return
+    r = oracle_vcycle_sample(args.steps, args.warmup)
+    line = {"impl": "reference", "metric": "smoothed DoFs/s (V(2,2) cycle)", "value": r["value"],
+            "unit": "DoF/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c5-sample (oracle on the host)", "sample": r["sample"]},
+            "cpu_baseline": {"value": r["value"], "unit": "DoF/s", "cores": 1, "kind": "oracle", "sample": r["sample"]},
+            "e2e": {"value": r["value"], "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    from paper_2104_14855_b200 import mhdp, workloads
+    ws, rank, local = dist_init()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = workloads.CONFIGS[args.config]
+    stream = torch.cuda.current_stream(dev)
+    ctx = mhdp.Context(local, stream.cuda_stream)
+    seed = args.seed + rank
+    t0 = time.perf_counter()
+    w0, _, _ = workloads.draw(cfg, 1, seed)
+    ctx.assemble(cfg, w0)
+    t_asm = time.perf_counter() - t0
+    n = ctx.n()
+    w, b, x0 = workloads.draw(cfg, n, seed)
+    t0 = time.perf_counter()
+    ctx.setup()
+    t_setup = time.perf_counter() - t0
+    L = ctx.num_levels()
+    infos = [ctx.info(l) for l in range(L)]
+    fin = infos[-1]
+    smoothed = sum((cfg.nu + cfg.nu) * infos[l]["n"] for l in range(1, L))
+
+    bd = torch.from_numpy(b).to(dev)
+    xd = torch.empty_like(bd)
+    x0d = torch.from_numpy(x0).to(dev)
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # ---- V-cycle (the step) ----
+    for _ in range(args.warmup):
+        ctx.vcycle(bd, xd)
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    l0 = ctx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            ctx.vcycle(bd, xd)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    launches = ctx.launch_count() - l0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    barrier()
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- finest single sweep (K1+K2+K3) and the dominant kernel K2 alone ----
+    reps = max(3, args.steps)
+    xs = x0d.clone()
+    ctx.smooth(bd, xs, nsweeps=1)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        ctx.smooth(bd, xs, nsweeps=1)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms_sweep = e0.elapsed_time(e1) / reps
+    rd = torch.empty_like(bd)
+    ctx.residual(bd, x0d, rd)
+    ctx.patch_apply(rd)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(reps):
+        ctx.patch_apply(rd)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms_k2 = e0.elapsed_time(e1) / reps
+    e0.record(stream)
+    for _ in range(reps):
+        ctx.residual(bd, x0d, rd)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms_k1 = e0.elapsed_time(e1) / reps
+
+    # algorithmic bytes: K2 per patch i: 8 n_i^2 factor + 8 n_i gathered r
+    # + 8 n_i written y; sweep: 8 sum n_i^2 + 8 nnz + 24 n
+    k2_bytes = 8 * fin["sum_n2"] + 16 * fin["sum_n"]
+    sweep_bytes = 8 * fin["sum_n2"] + 8 * fin["nnz"] + 24 * fin["n"]
+    k1_bytes = 8 * fin["nnz"] + 24 * fin["n"]
+    pk = peaks()
+    peak = pk["hbm_gbs"] if pk else 6650.0
+    k2_gbs = k2_bytes / (ms_k2 * 1e-3) / 1e9
+
+    # ---- e2e: host buffers through the C-ABI (H2D b, V-cycle, D2H x), pinned memory ----
+    bh = torch.from_numpy(b).pin_memory()
+    xh = torch.empty(n, dtype=torch.float64).pin_memory()
+    bnp, xnp = bh.numpy(), xh.numpy()
+    ctx.vcycle_host(bnp, xnp)
+    barrier()
+    te = time.perf_counter()
+    for _ in range(args.steps):
+        ctx.vcycle_host(bnp, xnp)
+    e2e_ms = (time.perf_counter() - te) * 1e3 / args.steps
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        r = oracle_vcycle_sample(steps=2, warmup=1)
+        cpu = {"value": r["value"], "unit": "DoF/s", "cores": 1, "kind": "oracle", "sample": r["sample"]}
+
+    if rank == 0:
+        value = ws * smoothed / (ms * 1e-3)
+        line = {
+            "metric": "smoothed DoFs/s (V(2,2) cycle); achieved HBM GB/s vs peak; V-cycle ms",
+            "value": value, "unit": "DoF/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: 3D AL velocity block, BDM1, {cfg.N}^3 x 6 tets, {L} levels, "
+                                   f"V({cfg.nu},{cfg.nu}), Re=gamma=1e4", "finest_dofs": fin["n"],
+                       "nnz": fin["nnz"], "patches": fin["npatch"], "sum_n2": fin["sum_n2"],
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "l2": "working set per step >> L2 (9.9 GB of patch factors streamed per sweep)"},
+            "vcycle_ms": ms,
+            "sweep": {"ms": ms_sweep, "dofs_per_s": fin["n"] / (ms_sweep * 1e-3),
+                      "gbs": sweep_bytes / (ms_sweep * 1e-3) / 1e9,
+                      "frac": sweep_bytes / (ms_sweep * 1e-3) / 1e9 / peak, "bytes": sweep_bytes},
+            "kernels": {"K2_patch_apply_ms": ms_k2, "K1_residual_ms": ms_k1,
+                        "K1_gbs": k1_bytes / (ms_k1 * 1e-3) / 1e9},
+            "roofline": {"bound": "hbm", "kernel": "K2 patch gather + LU apply (finest level)",
+                         "achieved": k2_gbs, "peak": peak, "unit": "GB/s", "frac": k2_gbs / peak,
+                         "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback"},
+            "e2e": {"value": ws * smoothed / (e2e_ms * 1e-3), "unit": "DoF/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "setup_s": {"host_assembly": t_asm, "device_setup": t_setup},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

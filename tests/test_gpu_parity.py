@@ -1,0 +1,127 @@
+"""GPU parity, tier P-B (the north-star criterion): the LIBRARY's own setup + CUDA path
+against the ORACLE's own setup + CPU path, on the same seeded inputs.
+
+Both sides assemble independently (their operators agree to ~1e-15 of row scale, see
+test_library_host.py), so results are compared by relative l2 difference <= 1e-10 after
+one Schwarz sweep (x0 = 0, which skips K1, and x0 = U(-1,1), which exercises it) and
+after one V-cycle; GMRES(V) iteration counts within +-1.
+Full BASELINE sizes for c1-c4 and a reduced c5 hierarchy; the full-size c5 sweep is
+checked on sampled DoFs that the oracle computes one by one from a masked assembly.
+"""
+import numpy as np
+import pytest
+
+from gpu_helpers import cuda_vec, host, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+CASES = [("c1", None, None, 0), ("c1", None, None, 1), ("c1", None, None, 2), ("c2", None, None, 0),
+         ("c3", None, None, 0), ("c4", None, None, 0), ("c5", 12, 3, 0), ("c5", 24, 3, 1)]
+
+
+def _setup(oracle_mod, name, N, L, seed):
+    import torch
+    from paper_2104_14855_b200 import mhdp, workloads
+    cfg = workloads.CONFIGS[name] if N is None else workloads.small(name, N, L)
+    ctx = mhdp.Context(0, torch.cuda.current_stream().cuda_stream)
+    w0, _, _ = workloads.draw(cfg, 1, seed)
+    ctx.assemble(cfg, w0)
+    n = ctx.n()
+    w, b, x0 = workloads.draw(cfg, n, seed)
+    assert np.array_equal(w, w0)
+    ctx.setup()
+    orc = oracle_mod.Oracle(cfg, w)
+    assert orc.n() == n
+    return cfg, ctx, orc, b, x0
+
+
+@pytest.fixture(scope="module", params=CASES, ids=[f"{c}-{n or 'full'}-s{s}" for c, n, l, s in CASES])
+def pb(request, oracle_mod):
+    name, N, L, seed = request.param
+    return _setup(oracle_mod, name, N, L, seed)
+
+
+def test_sweep_from_zero(pb):
+    cfg, ctx, orc, b, x0 = pb
+    xo = orc.sweep(b, np.zeros_like(b), x_is_zero=True)
+    xg = cuda_vec(np.zeros_like(b))
+    ctx.smooth(cuda_vec(b), xg, nsweeps=1, x_is_zero=True)
+    assert rel_l2(host(xg), xo) <= TOL
+
+
+def test_sweep_from_random(pb):
+    cfg, ctx, orc, b, x0 = pb
+    xo = orc.sweep(b, x0, nsweeps=1)
+    xg = cuda_vec(x0)
+    ctx.smooth(cuda_vec(b), xg, nsweeps=1)
+    assert rel_l2(host(xg), xo) <= TOL
+
+
+def test_vcycle(pb):
+    import torch
+    cfg, ctx, orc, b, x0 = pb
+    xo = orc.vcycle(b)
+    xg = torch.empty(len(b), dtype=torch.float64, device="cuda:0")
+    ctx.vcycle(cuda_vec(b), xg)
+    assert rel_l2(host(xg), xo) <= TOL
+
+
+def test_gmres_iteration_count(pb):
+    import torch
+    cfg, ctx, orc, b, x0 = pb
+    if len(b) > 100_000:
+        pytest.skip("oracle GMRES too slow at this size; counts checked on the smaller cases")
+    _, its_o, _, conv_o = orc.gmres(b, maxit=80)
+    xg = torch.empty(len(b), dtype=torch.float64, device="cuda:0")
+    its_g, _, conv_g = ctx.gmres(cuda_vec(b), xg, maxit=80)
+    assert conv_o == conv_g
+    assert abs(its_o - its_g) <= 1, (its_o, its_g)
+
+
+def _mask_around(cfg, dofs_entities_vertices):
+    """cells of the finest mesh whose vertices all lie within lattice distance 3 of a
+    vertex of a sampled DoF (enough for every row of every patch containing it)"""
+    N = cfg.N
+    near = np.zeros((N + 1,) * 3, bool)
+    for v in dofs_entities_vertices:
+        i, j, k = v % (N + 1), (v // (N + 1)) % (N + 1), v // (N + 1) ** 2
+        near[max(0, k - 3):k + 4, max(0, j - 3):j + 4, max(0, i - 3):i + 4] = True
+    # cube c = i + N(j + N k) is kept if its 8 corners are near
+    cube = near[:-1, :-1, :-1] & near[1:, :-1, :-1] & near[:-1, 1:, :-1] & near[:-1, :-1, 1:] \
+        & near[1:, 1:, :-1] & near[1:, :-1, 1:] & near[:-1, 1:, 1:] & near[1:, 1:, 1:]
+    return np.repeat(cube.ravel(), 6).astype(np.uint8)
+
+
+@pytest.mark.slow
+def test_full_c5_sweep_sampled(oracle_mod):
+    """Full-size c5 (3,939,840 DoFs), the configuration bench.py times: one sweep from
+    x0 = U(-1,1) on the GPU; 48 sampled DoFs (interior, near-wall, corner) recomputed by
+    the oracle one by one from a masked assembly; relative l2 over the sample <= 1e-10."""
+    import torch
+    from paper_2104_14855_b200 import mhdp, workloads
+    cfg = workloads.CONFIGS["c5"]
+    ctx = mhdp.Context(0, torch.cuda.current_stream().cuda_stream)
+    w0, _, _ = workloads.draw(cfg, 1, 0)
+    ctx.assemble(cfg, w0)
+    n = ctx.n()
+    w, b, x0 = workloads.draw(cfg, n, 0)
+    ctx.setup()
+    xg = cuda_vec(x0)
+    ctx.smooth(cuda_vec(b), xg, nsweeps=1)
+    xg = host(xg)
+    rng = np.random.default_rng(7)
+    sample = np.unique(np.concatenate([rng.integers(0, n, 40), [0, 1, 2, n - 1, n - 2, n - 3, n // 2, n // 3]]))
+    # vertices of the sampled DoFs' faces, from the library's exported patch lists
+    ptr, dofs = ctx.patches()
+    pv = np.repeat(np.arange(len(ptr) - 1), np.diff(ptr))
+    # patch index -> vertex: the library's patches are the non-empty stars in vertex order;
+    # recover vertex ids from the oracle-independent count of empty stars (none in 3D BDM)
+    assert len(ptr) - 1 == (cfg.N + 1) ** 3 - 8   # the 8 cube corners have empty stars
+    corners = sorted({i + (cfg.N + 1) * (j + (cfg.N + 1) * k) for i in (0, cfg.N) for j in (0, cfg.N) for k in (0, cfg.N)})
+    allv = np.setdiff1d(np.arange((cfg.N + 1) ** 3), corners)
+    verts = allv[np.unique(pv[np.isin(dofs, sample)])]
+    mask = _mask_around(cfg, verts)
+    orc = oracle_mod.Oracle(cfg, w, nlev=1, cmask=mask)
+    xo = orc.sweep_sample(b, x0, sample.astype(np.int32))
+    assert rel_l2(xg[sample], xo) <= TOL
