@@ -793,10 +793,15 @@ mhdp_status mhdp_export_patch_lu(mhdp_ctx *ctx, int level, long long patch, doub
     int64_t foff = 0;
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaMemcpy(&foff, P.foff + patch, sizeof(int64_t), cudaMemcpyDeviceToHost));
-    std::vector<double> cm((size_t)n * n);
-    CK(cudaMemcpy(cm.data(), P.fac + foff, sizeof(double) * n * n, cudaMemcpyDeviceToHost));
-    for (int i = 0; i < n; ++i)
-        for (int j = 0; j < n; ++j) lu[(size_t)i * n + j] = cm[(size_t)j * n + i];
+    std::vector<double> pk((size_t)n * n);
+    CK(cudaMemcpy(pk.data(), P.fac + foff, sizeof(double) * n * n, cudaMemcpyDeviceToHost));
+    // decode the packed streaming layout (kernels.cu pack_fwd / pack_bwd)
+    for (int j = 0; j < n; ++j) {
+        const int64_t f = (int64_t)j * n - (int64_t)j * (j + 1) / 2;
+        const int64_t b = (int64_t)n * (n - 1) / 2 + (int64_t)n * (n + 1) / 2 - (int64_t)(j + 1) * (j + 2) / 2;
+        for (int i = 0; i < n; ++i)
+            lu[(size_t)i * n + j] = i > j ? pk[f + i - j - 1] : (i == j ? pk[b] : pk[b + 1 + i]);
+    }
     CK(cudaMemcpy(perm, P.perm + H.pptr[patch], sizeof(int) * n, cudaMemcpyDeviceToHost));
     return MHDP_OK;
 }
