@@ -31,6 +31,7 @@
 #include <cstring>
 #include <numeric>
 
+#include "ddreal.hpp"
 #include "setup.hpp"
 
 namespace mhdp {
@@ -254,69 +255,78 @@ int cell_dofs(const Mesh &m, const Space &s, i64 c, int *out) {
 }
 
 // ------------------------------------------------------------------------------------
-// cell geometry: barycentric gradients from the lattice (unimodular => exact integers)
+// cell geometry: barycentric gradients from the lattice (unimodular => exact integers).
+// R = dd for the assembly (reading R-exact), R = double for the prolongation, whose
+// values are exact dyadic rationals on the lattice (reading R-prol).
 // ------------------------------------------------------------------------------------
-struct Geo {
+template <class R>
+struct GeoT {
     int d;
-    double X[4][3];   // physical vertex coordinates
-    double g[4][3];   // physical gradients of the barycentric coordinates
-    double vol;
-    double dvol;      // d |K| = |det| h^d / (d-1)!  (exact on the lattice)
+    R X[4][3];   // vertex coordinates
+    R g[4][3];   // gradients of the barycentric coordinates
+    R vol;
+    R dvol;      // d |K| = |det| h^d / (d-1)!
     int v[4];
 };
+typedef GeoT<double> Geo;
 
-void geo_from_lattice(int d, const int L[4][3], double h, Geo &G) {
-    // J columns = L_a - L_0 (integers); inverse by the adjugate (det = +-1 on these meshes,
-    // +-2^d on the doubled coarse lattice used by the prolongation)
-    double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+// scale = N: physical coordinates X = L/N (gradients x N); scale = 1: lattice units
+template <class R>
+void geo_from_lattice(int d, const int L[4][3], int scale, GeoT<R> &G) {
+    int J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
     for (int a = 1; a <= d; ++a)
         for (int r = 0; r < d; ++r) J[r][a - 1] = L[a][r] - L[0][r];
-    double inv[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, det;
+    long C[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    long det;
     if (d == 2) {
-        det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
-        inv[0][0] = J[1][1] / det; inv[0][1] = -J[0][1] / det;
-        inv[1][0] = -J[1][0] / det; inv[1][1] = J[0][0] / det;
+        det = (long)J[0][0] * J[1][1] - (long)J[0][1] * J[1][0];
+        C[0][0] = J[1][1]; C[0][1] = -J[0][1]; C[1][0] = -J[1][0]; C[1][1] = J[0][0];   // adjugate
     } else {
-        double C[3][3];
+        long Co[3][3];
         for (int r = 0; r < 3; ++r)
             for (int c = 0; c < 3; ++c) {
                 const int r1 = (r + 1) % 3, r2 = (r + 2) % 3, c1 = (c + 1) % 3, c2 = (c + 2) % 3;
-                C[r][c] = J[r1][c1] * J[r2][c2] - J[r1][c2] * J[r2][c1];
+                Co[r][c] = (long)J[r1][c1] * J[r2][c2] - (long)J[r1][c2] * J[r2][c1];
             }
-        det = J[0][0] * C[0][0] + J[0][1] * C[0][1] + J[0][2] * C[0][2];
+        det = J[0][0] * Co[0][0] + J[0][1] * Co[0][1] + J[0][2] * Co[0][2];
         for (int r = 0; r < 3; ++r)
-            for (int c = 0; c < 3; ++c) inv[r][c] = C[c][r] / det;
+            for (int c = 0; c < 3; ++c) C[r][c] = Co[c][r];
     }
     G.d = d;
     for (int a = 0; a < 4; ++a)
-        for (int r = 0; r < 3; ++r) { G.X[a][r] = 0; G.g[a][r] = 0; }
+        for (int r = 0; r < 3; ++r) { G.X[a][r] = R(0.0); G.g[a][r] = R(0.0); }
+    const R sc((double)scale), rdet((double)det);
     for (int a = 0; a <= d; ++a)
-        for (int r = 0; r < d; ++r) G.X[a][r] = L[a][r] * h;
-    // lattice gradient of lam_a (a >= 1) = row a-1 of inv; physical = lattice / h
+        for (int r = 0; r < d; ++r) G.X[a][r] = R((double)L[a][r]) / sc;
+    // gradient of lam_a (a >= 1) = row a-1 of J^-1 = adj/det (times scale)
     for (int a = 1; a <= d; ++a)
-        for (int r = 0; r < d; ++r) G.g[a][r] = inv[a - 1][r] / h;
+        for (int r = 0; r < d; ++r) G.g[a][r] = R((double)C[a - 1][r]) * sc / rdet;
     for (int r = 0; r < d; ++r) {
-        double s = 0;
+        R s(0.0);
         for (int a = 1; a <= d; ++a) s += G.g[a][r];
         G.g[0][r] = -s;
     }
-    const double fact = d == 2 ? 2.0 : 6.0;
-    G.vol = std::fabs(det) * (d == 2 ? h * h : h * h * h) / fact;
-    G.dvol = std::fabs(det) * (d == 2 ? h * h : h * h * h) / (d == 2 ? 1.0 : 2.0);
+    const double adet = (double)(det < 0 ? -det : det);
+    const R hd = d == 2 ? sc * sc : sc * sc * sc;
+    G.vol = R(adet) / (R(d == 2 ? 2.0 : 6.0) * hd);
+    G.dvol = R(adet) / (R(d == 2 ? 1.0 : 2.0) * hd);
 }
 
-void cell_geo(const Mesh &m, i64 c, Geo &G) {
+template <class R>
+void cell_geo(const Mesh &m, i64 c, GeoT<R> &G) {
     const int d = m.dim;
     int L[4][3] = {{0}};
     for (int a = 0; a <= d; ++a) {
         G.v[a] = m.cv[(d + 1) * c + a];
         m.lat(G.v[a], L[a]);
     }
-    geo_from_lattice(d, L, 1.0 / m.N, G);
+    geo_from_lattice(d, L, m.N, G);
 }
 
-inline double dot3(const double *a, const double *b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
-inline void cross3(const double *a, const double *b, double *c) {
+template <class R>
+inline R dot3(const R *a, const R *b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+template <class R>
+inline void cross3(const R *a, const R *b, R *c) {
     c[0] = a[1] * b[2] - a[2] * b[1];
     c[1] = a[2] * b[0] - a[0] * b[2];
     c[2] = a[0] * b[1] - a[1] * b[0];
@@ -324,75 +334,80 @@ inline void cross3(const double *a, const double *b, double *c) {
 
 // area vector |F| n_F of the facet opposite local vertex q, global orientation (R-orient):
 // 2D edge a<b: n = (t_y, -t_x);  3D face a<b<c: (x_b - x_a) x (x_c - x_a) / 2
-void facet_area(const Geo &G, int q, double *A, int *fl) {
+template <class R>
+void facet_area(const GeoT<R> &G, int q, R *A, int *fl) {
     int t = 0;
     for (int a = 0; a <= G.d; ++a) if (a != q) fl[t++] = a;
-    A[0] = A[1] = A[2] = 0;
+    A[0] = A[1] = A[2] = R(0.0);
     if (G.d == 2) {
         A[0] = G.X[fl[1]][1] - G.X[fl[0]][1];
         A[1] = -(G.X[fl[1]][0] - G.X[fl[0]][0]);
     } else {
-        double u[3], w[3];
+        R u[3], w[3];
         for (int r = 0; r < 3; ++r) { u[r] = G.X[fl[1]][r] - G.X[fl[0]][r]; w[r] = G.X[fl[2]][r] - G.X[fl[0]][r]; }
         cross3(u, w, A);
-        for (int r = 0; r < 3; ++r) A[r] *= 0.5;
+        for (int r = 0; r < 3; ++r) A[r] = A[r] * R(0.5);
     }
 }
 
 // +1 if the global normal of facet q points out of the cell
-double facet_sign(const Geo &G, int q, const double *A, const int *fl) {
-    double t[3];
+template <class R>
+double facet_sign(const GeoT<R> &G, int q, const R *A, const int *fl) {
+    R t[3];
     for (int r = 0; r < 3; ++r) t[r] = G.X[fl[0]][r] - G.X[q][r];
-    return dot3(A, t) > 0 ? 1.0 : -1.0;
+    return to_double(dot3(A, t)) > 0 ? 1.0 : -1.0;
 }
 
 // advecting field on the cell (R-w): 2D vcurl of the P1 stream function; 3D curl of the
 // NED1 interpolant of the P1 vector potential (edge circulations of A_h)
-void cell_wind(const Geo &G, const double *pot, double *w) {
-    w[0] = w[1] = w[2] = 0;
+template <class R>
+void cell_wind(const GeoT<R> &G, const double *pot, R *w) {
+    w[0] = w[1] = w[2] = R(0.0);
     if (G.d == 2) {
-        double gx = 0, gy = 0;
-        for (int a = 0; a < 3; ++a) { gx += pot[G.v[a]] * G.g[a][0]; gy += pot[G.v[a]] * G.g[a][1]; }
+        R gx(0.0), gy(0.0);
+        for (int a = 0; a < 3; ++a) { gx += R(pot[G.v[a]]) * G.g[a][0]; gy += R(pot[G.v[a]]) * G.g[a][1]; }
         w[0] = gy; w[1] = -gx;
         return;
     }
     static const int LE[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
     for (int e = 0; e < 6; ++e) {
         const int i = LE[e][0], j = LE[e][1];
-        double circ = 0;
+        R circ(0.0);
         for (int r = 0; r < 3; ++r)
-            circ += 0.5 * (pot[3 * (i64)G.v[i] + r] + pot[3 * (i64)G.v[j] + r]) * (G.X[j][r] - G.X[i][r]);
-        double cr[3];
+            circ += R(0.5) * (R(pot[3 * (i64)G.v[i] + r]) + R(pot[3 * (i64)G.v[j] + r])) * (G.X[j][r] - G.X[i][r]);
+        R cr[3];
         cross3(G.g[i], G.g[j], cr);
-        for (int r = 0; r < 3; ++r) w[r] += 2.0 * circ * cr[r];
+        for (int r = 0; r < 3; ++r) w[r] += R(2.0) * circ * cr[r];
     }
 }
 
-inline double mass_bary(const Geo &G, int a, int b) {   // int_K lam_a lam_b
-    const double den = G.d == 2 ? 12.0 : 20.0;
-    return G.vol * (a == b ? 2.0 : 1.0) / den;
+template <class R>
+inline R mass_bary(const GeoT<R> &G, int a, int b) {   // int_K lam_a lam_b
+    return G.vol * R(a == b ? 2.0 : 1.0) / R(G.d == 2 ? 12.0 : 20.0);
 }
 
 // ------------------------------------------------------------------------------------
 // BDM1 flux-nodal basis (R-basis): phi_{q,s} = lam_a v, a = s-th vertex of facet q,
 // v orthogonal to the normals of the other facets through a, v . A_q = 1
 // ------------------------------------------------------------------------------------
-struct VelBasis {
+template <class R>
+struct VelBasisT {
     int a[12];
-    double v[12][3];
+    R v[12][3];
     double sg[12];     // orientation sign of the basis function's facet in this cell
 };
 
-void vel_basis(const Geo &G, VelBasis &B) {
+template <class R>
+void vel_basis(const GeoT<R> &G, VelBasisT<R> &B) {
     const int d = G.d;
     for (int q = 0; q <= d; ++q) {
-        double A[3];
+        R A[3];
         int fl[3];
         facet_area(G, q, A, fl);
         const double sgn = facet_sign(G, q, A, fl);
         for (int s = 0; s < d; ++s) {
             const int k = d * q + s, a = fl[s];
-            double dir[3] = {0, 0, 0};
+            R dir[3] = {R(0.0), R(0.0), R(0.0)};
             if (d == 2) {
                 const int b = fl[1 - s];
                 dir[0] = -G.g[b][1]; dir[1] = G.g[b][0];
@@ -400,7 +415,7 @@ void vel_basis(const Geo &G, VelBasis &B) {
                 const int b = fl[(s + 1) % 3], c = fl[(s + 2) % 3];
                 cross3(G.g[b], G.g[c], dir);
             }
-            const double sc = dot3(dir, A);
+            const R sc = dot3(dir, A);
             B.a[k] = a;
             for (int r = 0; r < 3; ++r) B.v[k][r] = dir[r] / sc;
             B.sg[k] = sgn;
@@ -440,49 +455,54 @@ void incidence(const Mesh &m, int kind, std::vector<i64> &ptr, std::vector<int> 
     for (i64 c = 0; c < m.nc; ++c) for (int t = 0; t < per; ++t) cells[fill[ent(c, t)]++] = (int)c;
 }
 
+// R-exact: the rounded entry, with exact cancellations (|sum| <= 2^-80 sum|terms|) -> 0
+inline double round_entry(const dd &acc, double abssum) {
+    const double v = acc.value();
+    return std::fabs(v) <= std::ldexp(abssum, -80) ? 0.0 : v;
+}
+
 // ------------------------------------------------------------------------------------
-// E-B block, gather form
+// E-B block, gather form (element data cached per cell, double-double)
 // ------------------------------------------------------------------------------------
 struct EBLocal {
     int nE, nB;
     int gE[6], gB[4];
     double sB[4];
-    double EE[6][6], EB[6][4], BE[4][6];
+    dd EE[6][6], EB[6][4], BE[4][6];
 };
 
 void eb_local(const Mesh &m, const Space &s, i64 c, const double *pot, double Rem, EBLocal &K) {
-    Geo G;
+    GeoT<dd> G;
     cell_geo(m, c, G);
     const int d = m.dim, nvc = d + 1;
     K.nE = d == 2 ? 3 : 6;
     K.nB = nvc;
-    double w[3];
+    dd w[3];
     cell_wind(G, pot, w);
-    // E basis data
     static const int LE[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
-    double curlE[6][3];
+    dd curlE[6][3];
     for (int a = 0; a < K.nE; ++a) {
         if (d == 2) {
             K.gE[a] = s.vdof[G.v[a]];
-            curlE[a][0] = G.g[a][1]; curlE[a][1] = -G.g[a][0]; curlE[a][2] = 0;
+            curlE[a][0] = G.g[a][1]; curlE[a][1] = -G.g[a][0]; curlE[a][2] = dd(0.0);
         } else {
             K.gE[a] = s.edof[m.cedge[6 * c + a]];
             cross3(G.g[LE[a][0]], G.g[LE[a][1]], curlE[a]);
-            for (int r = 0; r < 3; ++r) curlE[a][r] *= 2.0;
+            for (int r = 0; r < 3; ++r) curlE[a][r] = curlE[a][r] * dd(2.0);
         }
     }
     // RT basis psi_q = s_q (x - X_q) / (d |K|)
-    double cq[4], cen[3] = {0, 0, 0};
-    for (int a = 0; a <= d; ++a) for (int r = 0; r < 3; ++r) cen[r] += G.X[a][r] / nvc;
+    dd cq[4], cen[3] = {dd(0.0), dd(0.0), dd(0.0)};
+    for (int a = 0; a <= d; ++a) for (int r = 0; r < 3; ++r) cen[r] += G.X[a][r];
+    for (int r = 0; r < 3; ++r) cen[r] = cen[r] / dd((double)nvc);
     for (int q = 0; q < nvc; ++q) {
-        double A[3];
+        dd A[3];
         int fl[3];
         facet_area(G, q, A, fl);
         K.sB[q] = facet_sign(G, q, A, fl);
-        cq[q] = K.sB[q] / G.dvol;
+        cq[q] = dd(K.sB[q]) / G.dvol;
         K.gB[q] = s.fdof[m.cfacet[nvc * c + q]];
     }
-    // M_E
     for (int i = 0; i < K.nE; ++i)
         for (int j = 0; j < K.nE; ++j) {
             if (d == 2) K.EE[i][j] = mass_bary(G, i, j);
@@ -493,22 +513,21 @@ void eb_local(const Mesh &m, const Space &s, i64 c, const double *pot, double Re
                              mass_bary(G, b, p) * dot3(G.g[a], G.g[q]) + mass_bary(G, b, q) * dot3(G.g[a], G.g[p]);
             }
         }
-    // A_{i,q} = int psi_q . curl phi_i = s_q/d * curl phi_i . (centroid - X_q)
-    // G~_{i,q} = int (w x psi_q) . phi_i
+    // A_{i,q} = int psi_q . curl phi_i = s_q/d curl phi_i . (centroid - X_q);  G~_{i,q} = int (w x psi_q) . phi_i
+    const dd rRem = dd(1.0) / dd(Rem);
     for (int q = 0; q < nvc; ++q) {
-        double dc[3];
+        dd dc[3];
         for (int r = 0; r < 3; ++r) dc[r] = cen[r] - G.X[q][r];
-        // w x (X_b - X_q) for each vertex b
-        double wx[4][3];
+        dd wx[4][3];
         for (int b = 0; b <= d; ++b) {
-            double t[3];
+            dd t[3];
             for (int r = 0; r < 3; ++r) t[r] = G.X[b][r] - G.X[q][r];
-            if (d == 2) { wx[b][0] = w[0] * t[1] - w[1] * t[0]; wx[b][1] = wx[b][2] = 0; }
+            if (d == 2) { wx[b][0] = w[0] * t[1] - w[1] * t[0]; wx[b][1] = wx[b][2] = dd(0.0); }
             else cross3(w, t, wx[b]);
         }
         for (int i = 0; i < K.nE; ++i) {
-            const double a_iq = (K.sB[q] / d) * dot3(curlE[i], dc);
-            double gt = 0;
+            const dd a_iq = dd(K.sB[q]) * dot3(curlE[i], dc) / dd((double)d);
+            dd gt(0.0);
             if (d == 2) {
                 for (int b = 0; b <= 2; ++b) gt += mass_bary(G, b, i) * wx[b][0];
             } else {
@@ -516,17 +535,17 @@ void eb_local(const Mesh &m, const Space &s, i64 c, const double *pot, double Re
                 for (int b = 0; b <= 3; ++b)
                     gt += mass_bary(G, b, a) * dot3(wx[b], G.g[bb]) - mass_bary(G, b, bb) * dot3(wx[b], G.g[a]);
             }
-            gt *= cq[q];
-            K.EB[i][q] = gt - a_iq / Rem;
+            gt = gt * cq[q];
+            K.EB[i][q] = gt - a_iq / dd(Rem);
             K.BE[q][i] = a_iq;
         }
     }
+    (void)rRem;
 }
 
 void assemble_eb(const Mesh &m, const Space &s, const Params &p, const double *pot, Pattern &P,
                  std::vector<double> &val) {
-    const int d = m.dim, nvc = d + 1;
-    // cells of each DoF's entity
+    const int d = m.dim;
     std::vector<i64> vp, ep, fp;
     std::vector<int> vc, ec, fc;
     if (d == 2) incidence(m, 0, vp, vc); else incidence(m, 1, ep, ec);
@@ -562,44 +581,58 @@ void assemble_eb(const Mesh &m, const Space &s, const Params &p, const double *p
     P.ci.resize(P.rp[s.n]);
     for (i64 r = 0; r < s.n; ++r) std::copy(rows[r].begin(), rows[r].end(), P.ci.begin() + P.rp[r]);
     rows.clear();
+    // element data of every cell, once
+    std::vector<EBLocal> loc(m.nc);
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < m.nc; ++c) eb_local(m, s, c, pot, p.Rem, loc[c]);
     val.assign(P.rp[s.n], 0.0);
     const double Kinv = d == 2 ? 2.0 * m.N * m.N : 6.0 * m.N * m.N * m.N;   // 1/|K|
 #pragma omp parallel for schedule(dynamic, 256)
     for (i64 r = 0; r < s.n; ++r) {
         const int *b, *e;
         cells_of(r, b, e);
-        std::vector<int> cnt(P.rp[r + 1] - P.rp[r], 0);
+        const i64 base = P.rp[r], len = P.rp[r + 1] - base;
+        std::vector<dd> acc(len);
+        std::vector<double> mag(len, 0.0);
+        std::vector<int> cnt(len, 0);
+        const bool isB = dkind[r] == 2;
         for (const int *c = b; c != e; ++c) {
-            EBLocal K;
-            eb_local(m, s, *c, pot, p.Rem, K);
+            const EBLocal &K = loc[*c];
             int li = -1;
-            bool isB = dkind[r] == 2;
             if (!isB) { for (int a = 0; a < K.nE; ++a) if (K.gE[a] == r) li = a; }
             else { for (int q = 0; q < K.nB; ++q) if (K.gB[q] == r) li = q; }
+            auto add = [&](int col, const dd &v) {
+                const i64 k = find_col(P, r, col) - base;
+                acc[k] += v;
+                mag[k] += std::fabs(v.value());
+            };
             if (!isB) {
-                for (int j = 0; j < K.nE; ++j) if (K.gE[j] >= 0) val[find_col(P, r, K.gE[j])] += K.EE[li][j];
-                for (int q = 0; q < K.nB; ++q) if (K.gB[q] >= 0) val[find_col(P, r, K.gB[q])] += K.EB[li][q];
+                for (int j = 0; j < K.nE; ++j) if (K.gE[j] >= 0) add(K.gE[j], K.EE[li][j]);
+                for (int q = 0; q < K.nB; ++q) if (K.gB[q] >= 0) add(K.gB[q], K.EB[li][q]);
             } else {
-                for (int j = 0; j < K.nE; ++j) if (K.gE[j] >= 0) val[find_col(P, r, K.gE[j])] += K.BE[li][j];
+                for (int j = 0; j < K.nE; ++j) if (K.gE[j] >= 0) add(K.gE[j], K.BE[li][j]);
                 for (int q = 0; q < K.nB; ++q)
-                    if (K.gB[q] >= 0) cnt[find_col(P, r, K.gB[q]) - P.rp[r]] += (int)(K.sB[li] * K.sB[q]);
+                    if (K.gB[q] >= 0) cnt[find_col(P, r, K.gB[q]) - base] += (int)(K.sB[li] * K.sB[q]);
             }
         }
-        (void)nvc;
-        // C = (1/Rem)(div psi_l, div psi_k): exact form (Kinv m) / Rem (R-gamma)
-        for (i64 t = P.rp[r]; t < P.rp[r + 1]; ++t)
-            if (cnt[t - P.rp[r]]) val[t] += (Kinv * cnt[t - P.rp[r]]) / p.Rem;
+        for (i64 k = 0; k < len; ++k) {
+            double v = round_entry(acc[k], mag[k]);
+            // C = (1/Rem)(div psi_l, div psi_k): exact form (Kinv m) / Rem (R-gamma); B-B entries
+            // receive no other contribution
+            if (cnt[k]) v = (Kinv * cnt[k]) / p.Rem;
+            val[base + k] = v;
+        }
     }
 }
 
 // ------------------------------------------------------------------------------------
-// AL velocity block, gather form by facet row blocks
+// AL velocity block, gather form by facet row blocks (element data cached per cell)
 // ------------------------------------------------------------------------------------
 struct CellVel {
-    Geo G;
-    VelBasis B;
-    double w[3];
-    double eps[12][3][3];
+    GeoT<dd> G;
+    VelBasisT<dd> B;
+    dd w[3];
+    dd eps[12][3][3];
     int gi[12];
 };
 
@@ -610,9 +643,9 @@ void cell_vel(const Mesh &m, const Space &s, i64 c, const double *pot, CellVel &
     const int d = m.dim, nb = d * (d + 1);
     cell_dofs(m, s, c, K.gi);
     for (int k = 0; k < nb; ++k) {
-        const double *g = K.G.g[K.B.a[k]], *v = K.B.v[k];
+        const dd *g = K.G.g[K.B.a[k]], *v = K.B.v[k];
         for (int l = 0; l < 3; ++l)
-            for (int r = 0; r < 3; ++r) K.eps[k][l][r] = 0.5 * (v[l] * g[r] + v[r] * g[l]);
+            for (int r = 0; r < 3; ++r) K.eps[k][l][r] = dd(0.5) * (v[l] * g[r] + v[r] * g[l]);
     }
 }
 
@@ -658,43 +691,51 @@ void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *
     for (i64 t = 0; t < nblk; ++t)
         for (int a = 0; a < d; ++a) std::copy(cols[t].begin(), cols[t].end(), P.ci.begin() + P.rp[s.fdof[freef[t]] + a]);
     cols.clear();
+    // element data of every cell, once
+    std::vector<CellVel> cellv(m.nc);
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < m.nc; ++c) cell_vel(m, s, c, pot, cellv[c]);
     val.assign(P.rp[s.n], 0.0);
-    const double nu2 = 2.0 / p.Re;
+    const dd nu2 = dd(2.0) / dd(p.Re);
     const double Kinv = d == 2 ? 2.0 * m.N * m.N : 6.0 * m.N * m.N * m.N;
-    const double fden = d == 2 ? 6.0 : 12.0;   // int_F mu_a mu_b = |F|(1+d_ab)/fden
+    const dd fden(d == 2 ? 6.0 : 12.0);   // int_F mu_a mu_b = |F|(1+d_ab)/fden
 #pragma omp parallel for schedule(dynamic, 64)
     for (i64 t = 0; t < nblk; ++t) {
         const int f = freef[t];
         const int r0 = s.fdof[f];
         const i64 base = P.rp[r0], len = P.rp[r0 + 1] - base;
-        std::vector<double> acc(d * len, 0.0);
+        std::vector<dd> acc(d * len);
+        std::vector<double> mag(d * len, 0.0);
         std::vector<int> cnt(len, 0);
         auto pos = [&](int col) -> i64 { return find_col(P, r0, col) - base; };
+        auto add = [&](int a, int col, const dd &v) {
+            const i64 k = a * len + pos(col);
+            acc[k] += v;
+            mag[k] += std::fabs(v.value());
+        };
         // ---- cell terms, cells of f ascending ----
         std::vector<int> fcells;
         for (int side = 0; side < 2; ++side) if (m.fcell[2 * f + side] >= 0) fcells.push_back(m.fcell[2 * f + side]);
         for (int c : fcells) {
-            CellVel K;
-            cell_vel(m, s, c, pot, K);
+            const CellVel &K = cellv[c];
             int qf = -1;
             for (int q = 0; q < nvc; ++q) if (m.cfacet[nvc * c + q] == f) qf = q;
-            const double V = K.G.vol;
+            const dd V = K.G.vol, Vn = K.G.vol / dd((double)nvc);
             for (int a = 0; a < d; ++a) {
                 const int i = d * qf + a;                  // test function (this row)
-                const double gw = dot3(K.G.g[K.B.a[i]], K.w);
+                const dd gw = dot3(K.G.g[K.B.a[i]], K.w);
                 for (int j = 0; j < nb; ++j) {
                     if (K.gi[j] < 0) continue;
-                    double ee = 0;
+                    dd ee(0.0);
                     for (int l = 0; l < 3; ++l) for (int r = 0; r < 3; ++r) ee += K.eps[j][l][r] * K.eps[i][l][r];
-                    const double visc = nu2 * V * ee;
-                    const double adv = dot3(K.B.v[j], K.B.v[i]) * gw * (V / nvc);
-                    acc[a * len + pos(K.gi[j])] += visc - adv;
+                    add(a, K.gi[j], nu2 * V * ee);                                 // viscous
+                    add(a, K.gi[j], -(dot3(K.B.v[j], K.B.v[i]) * gw * Vn));         // advection
                 }
             }
             for (int j = 0; j < nb; ++j)
                 if (K.gi[j] >= 0) cnt[pos(K.gi[j])] += (int)(K.B.sg[d * qf] * K.B.sg[j]);
         }
-        // ---- facet terms: every facet of the cells of f, ascending ----
+        // ---- facet terms: every facet of the cells of f ----
         std::vector<int> gs;
         for (int c : fcells) for (int q = 0; q < nvc; ++q) gs.push_back(m.cfacet[nvc * c + q]);
         std::sort(gs.begin(), gs.end());
@@ -702,41 +743,39 @@ void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *
         for (int g : gs) {
             const int cp = m.fcell[2 * g], cm = m.fcell[2 * g + 1];
             const bool interior = cm >= 0;
-            CellVel Kp, Km;
-            cell_vel(m, s, cp, pot, Kp);
-            if (interior) cell_vel(m, s, cm, pot, Km);
+            const CellVel &Kp = cellv[cp];
             int qp = -1, qm = -1;
             for (int q = 0; q < nvc; ++q) {
                 if (m.cfacet[nvc * cp + q] == g) qp = q;
                 if (interior && m.cfacet[nvc * cm + q] == g) qm = q;
             }
-            double A[3];
+            dd A[3];
             int fl[3];
             facet_area(Kp.G, qp, A, fl);
-            const double area = std::sqrt(dot3(A, A));
+            const dd area = sqrt(dot3(A, A));
             const double sgn = facet_sign(Kp.G, qp, A, fl);
-            double n[3];
-            for (int r = 0; r < 3; ++r) n[r] = sgn * A[r] / area;
-            double hF;
+            dd n[3];
+            for (int r = 0; r < 3; ++r) n[r] = dd(sgn) * A[r] / area;
+            dd hF(0.0);
             if (d == 2) hF = area;
-            else {
-                hF = 0;
+            else
                 for (int a = 0; a < 3; ++a)
                     for (int b = a + 1; b < 3; ++b) {
-                        double tt[3];
+                        dd tt[3];
                         for (int r = 0; r < 3; ++r) tt[r] = Kp.G.X[fl[b]][r] - Kp.G.X[fl[a]][r];
-                        hF = std::max(hF, std::sqrt(dot3(tt, tt)));
+                        const dd l = sqrt(dot3(tt, tt));
+                        if (l > hF) hF = l;
                     }
-            }
-            const double avg = interior ? 0.5 : 1.0;
-            const double pen = (1.0 / p.Re) * (p.sigma / hF);
-            const double wn = dot3(Kp.w, n), awn = std::fabs(wn);
-            // basis functions of both sides: global vertex on the facet (or -1), v, eps n
-            struct Fn { int side, vtx, gidx; double v[3], en[3]; };
+            const dd avg(interior ? 0.5 : 1.0);
+            const dd pen = dd(p.sigma) / (dd(p.Re) * hF);
+            const dd wn = dot3(Kp.w, n), awn = fabs(wn);
+            const dd upp = dd(0.5) * (wn + awn), upm = dd(-0.5) * (awn - wn);
+            const dd intF = area / dd((double)d);
+            struct Fn { int side, vtx, gidx; dd v[3], en[3]; };
             Fn fn[24];
             int nf = 0;
             for (int side = 0; side < (interior ? 2 : 1); ++side) {
-                const CellVel &K = side ? Km : Kp;
+                const CellVel &K = side ? cellv[cm] : Kp;
                 const int qq = side ? qm : qp;
                 for (int k = 0; k < nb; ++k) {
                     Fn &F = fn[nf++];
@@ -753,32 +792,36 @@ void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *
                 const Fn &I = fn[ti];
                 if (I.gidx < r0 || I.gidx >= r0 + d) continue;   // rows of this block only
                 const int a = I.gidx - r0;
-                const double Ji = I.side;
-                const double intI = I.vtx >= 0 ? area / d : 0.0;
+                const dd Ji((double)I.side);
                 for (int tj = 0; tj < nf; ++tj) {
                     const Fn &J = fn[tj];
                     if (J.gidx < 0) continue;
-                    const double Jj = J.side;
-                    const double intJ = J.vtx >= 0 ? area / d : 0.0;
-                    const double intIJ = (I.vtx >= 0 && J.vtx >= 0) ? area * (I.vtx == J.vtx ? 2.0 : 1.0) / fden : 0.0;
-                    const double vv = dot3(J.v, I.v) * intIJ;
-                    const double t1 = -nu2 * avg * Ji * dot3(J.en, I.v) * intI;
-                    const double t2 = -nu2 * avg * Jj * dot3(J.v, I.en) * intJ;
-                    const double t3 = pen * Ji * Jj * vv;
-                    double up;
-                    if (interior) up = (J.side > 0 ? 0.5 * (wn + awn) : -0.5 * (-wn + awn)) * vv * Ji;
-                    else up = 0.5 * (wn + awn) * vv;
-                    acc[a * len + pos(J.gidx)] += t1 + t2 + t3 + up;
+                    const dd Jj((double)J.side);
+                    dd term(0.0);
+                    if (I.vtx >= 0) term += -(nu2 * avg * Ji * dot3(J.en, I.v) * intF);     // consistency
+                    if (J.vtx >= 0) term += -(nu2 * avg * Jj * dot3(J.v, I.en) * intF);     // symmetry
+                    if (I.vtx >= 0 && J.vtx >= 0) {
+                        const dd vv = dot3(J.v, I.v) * area * dd(I.vtx == J.vtx ? 2.0 : 1.0) / fden;
+                        term += pen * Ji * Jj * vv;                                         // penalty
+                        if (interior) term += (J.side > 0 ? upp : upm) * vv * Ji;           // upwind
+                        else term += upp * vv;
+                    }
+                    add(a, J.gidx, term);
                 }
             }
         }
-        // ---- gamma (div u, div v): exact form (gamma Kinv m) / d^2 (R-gamma) ----
+        // ---- gamma (div u, div v) = gamma Kinv m / d^2, exact (R-gamma); entry rounded once (R-exact)
         const double Gk = p.gamma * Kinv;
         for (int a = 0; a < d; ++a)
             for (i64 k = 0; k < len; ++k) {
-                double v = acc[a * len + k];
-                if (cnt[k]) v += (Gk * cnt[k]) / (double)(d * d);
-                val[P.rp[r0 + a] + k] = v;
+                dd v = acc[a * len + k];
+                double mg = mag[a * len + k];
+                if (cnt[k]) {
+                    const dd gam = dd(Gk * cnt[k]) / dd((double)(d * d));
+                    v += gam;
+                    mg += std::fabs(gam.value());
+                }
+                val[P.rp[r0 + a] + k] = round_entry(v, mg);
             }
     }
 }
@@ -866,7 +909,7 @@ void build_prolongation(const Mesh &mf, const Space &sf, const Mesh &mc, const S
             for (int r = 0; r < d; ++r) Lc[a][r] *= 2;
         }
         Geo Gc;
-        geo_from_lattice(d, Lc, 1.0, Gc);
+        geo_from_lattice(d, Lc, 1, Gc);
         // coarse basis functions as affine fields on the lattice
         Aff F[12];
         int gJ[12];
@@ -902,7 +945,7 @@ void build_prolongation(const Mesh &mf, const Space &sf, const Mesh &mc, const S
                     gJ[nbc++] = sc.fdof[mc.cfacet[nvc * pc + q]];
                 }
             } else {                 // BDM1: lam_a v
-                VelBasis B;
+                VelBasisT<double> B;
                 vel_basis(Gc, B);
                 for (int q = 0; q < nvc; ++q) {
                     const int f0 = sc.fdof[mc.cfacet[nvc * pc + q]];
@@ -921,7 +964,7 @@ void build_prolongation(const Mesh &mf, const Space &sf, const Mesh &mc, const S
             }
         };
         Geo Gf;
-        geo_from_lattice(d, Lf, 1.0, Gf);
+        geo_from_lattice(d, Lf, 1, Gf);
         int last_kind = -1;
         for (int t = 0; t < k; ++t) {
             const int I = loc[t];

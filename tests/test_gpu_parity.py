@@ -112,15 +112,12 @@ def test_full_c5_sweep_sampled(oracle_mod):
     xg = host(xg)
     rng = np.random.default_rng(7)
     sample = np.unique(np.concatenate([rng.integers(0, n, 40), [0, 1, 2, n - 1, n - 2, n - 3, n // 2, n // 3]]))
-    # vertices of the sampled DoFs' faces, from the library's exported patch lists
+    # vertices of the sampled DoFs' faces: in 3D BDM1 every vertex star is non-empty, so
+    # the library's patch index is the vertex id (reading R-patch)
     ptr, dofs = ctx.patches()
+    assert len(ptr) - 1 == (cfg.N + 1) ** 3
     pv = np.repeat(np.arange(len(ptr) - 1), np.diff(ptr))
-    # patch index -> vertex: the library's patches are the non-empty stars in vertex order;
-    # recover vertex ids from the oracle-independent count of empty stars (none in 3D BDM)
-    assert len(ptr) - 1 == (cfg.N + 1) ** 3 - 8   # the 8 cube corners have empty stars
-    corners = sorted({i + (cfg.N + 1) * (j + (cfg.N + 1) * k) for i in (0, cfg.N) for j in (0, cfg.N) for k in (0, cfg.N)})
-    allv = np.setdiff1d(np.arange((cfg.N + 1) ** 3), corners)
-    verts = allv[np.unique(pv[np.isin(dofs, sample)])]
+    verts = np.unique(pv[np.isin(dofs, sample)])
     mask = _mask_around(cfg, verts)
     orc = oracle_mod.Oracle(cfg, w, nlev=1, cmask=mask)
     xo = orc.sweep_sample(b, x0, sample.astype(np.int32))
