@@ -20,11 +20,12 @@
  * BDM1 flux-nodal (|f| (u.n_f)(x_a) = 1).  Each local basis function is affine and
  * stored as value at the first cell vertex plus its constant gradient.
  *
- * Integration: cell integrals with a collapsed (Duffy) 4x4(x4) Gauss-Legendre
- * rule (exact for degree <= 5 in 3D, <= 6 in 2D; all cell integrands here have
- * degree <= 2).  Facet integrals with a 3-point (2D) / collapsed 3x3 (3D)
- * Gauss-Legendre rule (exact for degree <= 5 / 4; facet integrands have degree
- * <= 2 because the advecting field w_h is constant per cell, reading R-w).
+ * Integration: cell integrals with a collapsed (Duffy) 3x3(x3) Gauss-Legendre
+ * rule (exact for degree <= 5; all cell integrands here have degree <= 2).  Facet
+ * integrals with a 3-point (2D) / collapsed 3x3 (3D) Gauss-Legendre rule (exact for
+ * degree <= 5 / 4; facet integrands have degree <= 2 because the advecting field w_h
+ * is constant per cell, reading R-w).  Nodes and weights are formed in `real` from
+ * their closed forms, so in the exact build the rules are exact to ~1e-34.
  * The grad-div / div-div parts are the exact closed form of reading R-gamma:
  * div of an RT/BDM basis function on K is s/(d|K|) (RT: s/|K|), so those entries
  * equal (G * m) / d^2 with G = gamma/|K| and m an integer sum of orientation signs.
@@ -34,34 +35,52 @@
 #include <string.h>
 #include "orc.h"
 
+/* Precision of the element integrals and of their accumulation (reading R-exact):
+ * the oracle is compiled twice from this file.  liboracle.so uses real = double (fast;
+ * the finite-element pins); liboracle_exact.so uses real = __float128 (113-bit), so every
+ * assembled entry is the fp64 value nearest to the exact discrete bilinear form for the
+ * given fp64 inputs -- the reference for the end-to-end parity tests.  The final
+ * rounding of each row goes through a grid 2^-88 below the row's largest entry (see
+ * finish()), so that exact ties round to even and exact cancellations give 0.         */
+#ifdef ORC_EXACT
+#include <quadmath.h>
+typedef __float128 real;
+#define RSQRT(x) sqrtq(x)
+#define RFABS(x) fabsq(x)
+#else
+typedef double real;
+#define RSQRT(x) sqrt(x)
+#define RFABS(x) fabs(x)
+#endif
+
 /* ------------------------------------------------------------------------- */
 /* geometry                                                                   */
 /* ------------------------------------------------------------------------- */
 typedef struct {
     int dim;
-    double X[4][3];     /* vertices (ascending global id)   */
-    double Ji[3][3];    /* inverse Jacobian                  */
-    double det, vol;
-    double g[4][3];     /* gradients of barycentric coords   */
+    real X[4][3];       /* vertices (ascending global id)   */
+    real Ji[3][3];      /* inverse Jacobian                  */
+    real det, vol;
+    real g[4][3];       /* gradients of barycentric coords   */
 } Cell;
 
-typedef struct { double v0[3]; double G[3][3]; } Aff;  /* f(x) = v0 + G (x - X0) */
+typedef struct { real v0[3]; real G[3][3]; } Aff;  /* f(x) = v0 + G (x - X0) */
 
 /* geometry of the simplex with vertices X (ascending global id) */
-static void cell_geom_from(int d, const double X[4][3], Cell *K) {
+static void cell_geom_from(int d, const real X[4][3], Cell *K) {
     memset(K, 0, sizeof(*K));
     K->dim = d;
     memcpy(K->X, X, sizeof(K->X));
-    double J[3][3] = {{0}};
+    real J[3][3] = {{0}};
     for (int r = 0; r < d; r++)
         for (int col = 0; col < d; col++) J[r][col] = K->X[col + 1][r] - K->X[0][r];
     if (d == 2) {
         K->det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
         K->Ji[0][0] = J[1][1] / K->det; K->Ji[0][1] = -J[0][1] / K->det;
         K->Ji[1][0] = -J[1][0] / K->det; K->Ji[1][1] = J[0][0] / K->det;
-        K->vol = fabs(K->det) / 2.0;
+        K->vol = RFABS(K->det) / 2;
     } else {
-        double co[3][3];
+        real co[3][3];
         co[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
         co[0][1] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
         co[0][2] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
@@ -74,49 +93,50 @@ static void cell_geom_from(int d, const double X[4][3], Cell *K) {
         K->det = J[0][0] * co[0][0] + J[0][1] * co[0][1] + J[0][2] * co[0][2];
         for (int r = 0; r < 3; r++)
             for (int col = 0; col < 3; col++) K->Ji[r][col] = co[col][r] / K->det;
-        K->vol = fabs(K->det) / 6.0;
+        K->vol = RFABS(K->det) / 6;
     }
     for (int a = 1; a <= d; a++)
         for (int k = 0; k < d; k++) K->g[a][k] = K->Ji[a - 1][k];
     for (int k = 0; k < d; k++) {
-        double s = 0;
+        real s = 0;
         for (int a = 1; a <= d; a++) s += K->g[a][k];
         K->g[0][k] = -s;
     }
 }
 
+/* vertex coordinates formed in `real` from the integer lattice: x = (i,j,k)/N */
 static void cell_geom(const OMesh *m, i64 c, Cell *K) {
     int d = m->dim;
-    double X[4][3] = {{0}};
+    real X[4][3] = {{0}};
     for (int a = 0; a <= d; a++)
-        for (int r = 0; r < 3; r++) X[a][r] = m->x[3 * m->cv[c * (d + 1) + a] + r];
+        for (int r = 0; r < d; r++) X[a][r] = (real)m->lat[3 * m->cv[c * (d + 1) + a] + r] / (real)m->N;
     cell_geom_from(d, X, K);
 }
 
-static void aff_eval(const Aff *f, const Cell *K, const double *x, double *out) {
+static void aff_eval(const Aff *f, const Cell *K, const real *x, real *out) {
     for (int l = 0; l < 3; l++) {
-        double s = f->v0[l];
+        real s = f->v0[l];
         for (int k = 0; k < K->dim; k++) s += f->G[l][k] * (x[k] - K->X[0][k]);
         out[l] = s;
     }
 }
 
-static double dot3(const double *a, const double *b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
-static void cross3(const double *a, const double *b, double *c) {
+static real dot3(const real *a, const real *b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+static void cross3(const real *a, const real *b, real *c) {
     c[0] = a[1] * b[2] - a[2] * b[1]; c[1] = a[2] * b[0] - a[0] * b[2]; c[2] = a[0] * b[1] - a[1] * b[0];
 }
 
 /* global facet area vector |f| n_f of the facet with ascending vertices P:
  * 2D edge (a<b): n = (t_y, -t_x) (tangent rotated clockwise);
  * 3D face (a<b<c): n ~ (x_b - x_a) x (x_c - x_a).         reading R-orient    */
-static void facet_area_vector(int dim, const double P[3][3], double *A) {
+static void facet_area_vector(int dim, const real P[3][3], real *A) {
     if (dim == 2) {
         A[0] = P[1][1] - P[0][1]; A[1] = -(P[1][0] - P[0][0]); A[2] = 0;
     } else {
-        double u[3], v[3];
+        real u[3], v[3];
         for (int k = 0; k < 3; k++) { u[k] = P[1][k] - P[0][k]; v[k] = P[2][k] - P[0][k]; }
         cross3(u, v, A);
-        for (int k = 0; k < 3; k++) A[k] *= 0.5;
+        for (int k = 0; k < 3; k++) A[k] /= 2;
     }
 }
 
@@ -129,10 +149,10 @@ static void facet_area_vector(int dim, const double P[3][3], double *A) {
  *       c_e = (A_i + A_j)/2 . (X_j - X_i), curl(lam_i grad lam_j - lam_j grad lam_i)
  *       = 2 grad lam_i x grad lam_j.
  * w_h is constant on K, normal-continuous across facets, and lies in RT_0 in BDM_1. */
-static void cell_wind(const Cell *K, const double pot[4][3], double *wc) {
-    wc[0] = wc[1] = wc[2] = 0.0;
+static void cell_wind(const Cell *K, const double pot[4][3], real *wc) {
+    wc[0] = wc[1] = wc[2] = 0;
     if (K->dim == 2) {
-        double gx = 0, gy = 0;
+        real gx = 0, gy = 0;
         for (int a = 0; a < 3; a++) { gx += pot[a][0] * K->g[a][0]; gy += pot[a][0] * K->g[a][1]; }
         wc[0] = gy; wc[1] = -gx;
         return;
@@ -141,11 +161,11 @@ static void cell_wind(const Cell *K, const double pot[4][3], double *wc) {
         int lv[2];
         om_edge_local_verts(3, q, lv);
         int i = lv[0], j = lv[1];
-        double ce = 0;
-        for (int k = 0; k < 3; k++) ce += 0.5 * (pot[i][k] + pot[j][k]) * (K->X[j][k] - K->X[i][k]);
-        double cr[3];
+        real ce = 0;
+        for (int k = 0; k < 3; k++) ce += ((real)pot[i][k] + (real)pot[j][k]) / 2 * (K->X[j][k] - K->X[i][k]);
+        real cr[3];
         cross3(K->g[i], K->g[j], cr);
-        for (int k = 0; k < 3; k++) wc[k] += ce * 2.0 * cr[k];
+        for (int k = 0; k < 3; k++) wc[k] += ce * 2 * cr[k];
     }
 }
 
@@ -161,7 +181,7 @@ static void cell_pot(const OMesh *m, i64 c, const double *pot, double out[4][3])
 /* ------------------------------------------------------------------------- */
 static Aff basis_cg1(const Cell *K, int a) {
     Aff f; memset(&f, 0, sizeof(f));
-    f.v0[0] = a == 0 ? 1.0 : 0.0;
+    f.v0[0] = a == 0 ? 1 : 0;
     for (int k = 0; k < K->dim; k++) f.G[0][k] = K->g[a][k];
     return f;
 }
@@ -170,25 +190,25 @@ static Aff basis_cg1(const Cell *K, int a) {
 static Aff basis_ned1(const Cell *K, int i, int j) {
     Aff f; memset(&f, 0, sizeof(f));
     for (int l = 0; l < 3; l++) {
-        f.v0[l] = (i == 0 ? K->g[j][l] : 0.0) - (j == 0 ? K->g[i][l] : 0.0);
+        f.v0[l] = (i == 0 ? K->g[j][l] : (real)0) - (j == 0 ? K->g[i][l] : (real)0);
         for (int k = 0; k < 3; k++) f.G[l][k] = K->g[j][l] * K->g[i][k] - K->g[i][l] * K->g[j][k];
     }
     return f;
 }
 
 /* orientation sign of local facet q: +1 if the global facet normal points out of K */
-static double facet_sign(const Cell *K, int q, const double A[3]) {
+static double facet_sign(const Cell *K, int q, const real A[3]) {
     int d = K->dim, opp = om_facet_opp(d, q), lv[3];
     om_facet_local_verts(d, q, lv);
-    double t[3];
+    real t[3];
     for (int k = 0; k < 3; k++) t[k] = K->X[lv[0]][k] - K->X[opp][k];
     return dot3(A, t) > 0 ? 1.0 : -1.0;
 }
 
-static void facet_points(const Cell *K, int q, double P[3][3]) {
+static void facet_points(const Cell *K, int q, real P[3][3]) {
     int lv[3];
     om_facet_local_verts(K->dim, q, lv);
-    memset(P, 0, sizeof(double) * 9);
+    memset(P, 0, sizeof(real) * 9);
     for (int a = 0; a < K->dim; a++)
         for (int k = 0; k < 3; k++) P[a][k] = K->X[lv[a]][k];
 }
@@ -196,15 +216,15 @@ static void facet_points(const Cell *K, int q, double P[3][3]) {
 /* RT1: s (x - X_opp) / (d |K|)  (flux 1 through facet q along its global normal) */
 static Aff basis_rt(const Cell *K, int q, double *sign) {
     Aff f; memset(&f, 0, sizeof(f));
-    double P[3][3], A[3];
+    real P[3][3], A[3];
     facet_points(K, q, P);
     facet_area_vector(K->dim, P, A);
     double s = facet_sign(K, q, A);
     int opp = om_facet_opp(K->dim, q);
-    double c = s / (K->dim * K->vol);
+    real c = s / (K->dim * K->vol);
     for (int l = 0; l < 3; l++) {
         f.v0[l] = c * (K->X[0][l] - K->X[opp][l]);
-        for (int k = 0; k < 3; k++) f.G[l][k] = (l == k && l < K->dim) ? c : 0.0;
+        for (int k = 0; k < 3; k++) f.G[l][k] = (l == k && l < K->dim) ? c : (real)0;
     }
     *sign = s;
     return f;
@@ -216,7 +236,7 @@ static Aff basis_bdm(const Cell *K, int q, int ia, double *sign) {
     Aff f; memset(&f, 0, sizeof(f));
     int d = K->dim, lv[3];
     om_facet_local_verts(d, q, lv);
-    double P[3][3], A[3], dir[3] = {0, 0, 0};
+    real P[3][3], A[3], dir[3] = {0, 0, 0};
     facet_points(K, q, P);
     facet_area_vector(d, P, A);
     int a = lv[ia];
@@ -227,11 +247,11 @@ static Aff basis_bdm(const Cell *K, int q, int ia, double *sign) {
         int b = lv[(ia + 1) % 3], c = lv[(ia + 2) % 3];
         cross3(K->g[b], K->g[c], dir);
     }
-    double sc = 1.0 / dot3(dir, A);
-    double psi[3] = {dir[0] * sc, dir[1] * sc, dir[2] * sc};
+    real sc = dot3(dir, A);
+    real psi[3] = {dir[0] / sc, dir[1] / sc, dir[2] / sc};
     for (int l = 0; l < 3; l++) {
-        f.v0[l] = (a == 0 ? 1.0 : 0.0) * psi[l];
-        for (int k = 0; k < 3; k++) f.G[l][k] = k < d ? psi[l] * K->g[a][k] : 0.0;
+        f.v0[l] = (a == 0 ? psi[l] : (real)0);
+        for (int k = 0; k < 3; k++) f.G[l][k] = k < d ? psi[l] * K->g[a][k] : (real)0;
     }
     *sign = facet_sign(K, q, A);
     return f;
@@ -240,40 +260,45 @@ static Aff basis_bdm(const Cell *K, int q, int ia, double *sign) {
 /* ------------------------------------------------------------------------- */
 /* quadrature                                                                  */
 /* ------------------------------------------------------------------------- */
-static void gauss01(int q, double *x, double *w) {
+static void gauss01(int q, real *x, real *w) {
+    /* Gauss-Legendre nodes / weights on [0,1], formed in `real` from their closed forms */
     if (q == 3) {
-        double r = 0.5 * sqrt(0.6);
-        x[0] = 0.5 - r; x[1] = 0.5; x[2] = 0.5 + r;
-        w[0] = 5.0 / 18.0; w[1] = 8.0 / 18.0; w[2] = 5.0 / 18.0;
+        real r = RSQRT((real)3 / 5) / 2;
+        x[0] = (real)1 / 2 - r; x[1] = (real)1 / 2; x[2] = (real)1 / 2 + r;
+        w[0] = (real)5 / 18; w[1] = (real)8 / 18; w[2] = (real)5 / 18;
     } else { /* q == 4 */
-        double a = sqrt(3.0 / 7.0 - 2.0 / 7.0 * sqrt(6.0 / 5.0));
-        double b = sqrt(3.0 / 7.0 + 2.0 / 7.0 * sqrt(6.0 / 5.0));
-        double wa = (18.0 + sqrt(30.0)) / 36.0, wb = (18.0 - sqrt(30.0)) / 36.0;
-        x[0] = 0.5 * (1 - b); x[1] = 0.5 * (1 - a); x[2] = 0.5 * (1 + a); x[3] = 0.5 * (1 + b);
-        w[0] = 0.5 * wb; w[1] = 0.5 * wa; w[2] = 0.5 * wa; w[3] = 0.5 * wb;
+        real s65 = RSQRT((real)6 / 5), s30 = RSQRT((real)30);
+        real a = RSQRT((real)3 / 7 - (real)2 / 7 * s65);
+        real b = RSQRT((real)3 / 7 + (real)2 / 7 * s65);
+        real wa = (18 + s30) / 36, wb = (18 - s30) / 36;
+        x[0] = (1 - b) / 2; x[1] = (1 - a) / 2; x[2] = (1 + a) / 2; x[3] = (1 + b) / 2;
+        w[0] = wb / 2; w[1] = wa / 2; w[2] = wa / 2; w[3] = wb / 2;
     }
 }
 
-/* collapsed Gauss rule on the cell: fills points (physical) and weights (physical) */
-static int cell_rule(const Cell *K, double (*xq)[3], double *wq) {
-    double g[4], w[4];
-    gauss01(4, g, w);
+/* collapsed (Duffy) Gauss rule with q points per direction on the cell: physical points
+ * and weights.  q = 3 (27 / 9 points) is exact to degree 5 (3D) / 5 (2D) and is used by
+ * the assembly (all cell integrands have degree <= 2); q = 4 serves the manufactured-
+ * solution helpers, whose integrands are not polynomial. */
+static int cell_rule(const Cell *K, int q, real (*xq)[3], real *wq) {
+    real g[4], w[4];
+    gauss01(q, g, w);
     int n = 0;
     if (K->dim == 2) {
-        for (int i = 0; i < 4; i++)
-            for (int j = 0; j < 4; j++) {
-                double xi1 = g[i] * (1 - g[j]), xi2 = g[j];
-                double wt = w[i] * w[j] * (1 - g[j]) * fabs(K->det);
+        for (int i = 0; i < q; i++)
+            for (int j = 0; j < q; j++) {
+                real xi1 = g[i] * (1 - g[j]), xi2 = g[j];
+                real wt = w[i] * w[j] * (1 - g[j]) * RFABS(K->det);
                 for (int k = 0; k < 3; k++)
                     xq[n][k] = K->X[0][k] + xi1 * (K->X[1][k] - K->X[0][k]) + xi2 * (K->X[2][k] - K->X[0][k]);
                 wq[n++] = wt;
             }
     } else {
-        for (int i = 0; i < 4; i++)
-            for (int j = 0; j < 4; j++)
-                for (int l = 0; l < 4; l++) {
-                    double xi1 = g[i] * (1 - g[j]) * (1 - g[l]), xi2 = g[j] * (1 - g[l]), xi3 = g[l];
-                    double wt = w[i] * w[j] * w[l] * (1 - g[j]) * (1 - g[l]) * (1 - g[l]) * fabs(K->det);
+        for (int i = 0; i < q; i++)
+            for (int j = 0; j < q; j++)
+                for (int l = 0; l < q; l++) {
+                    real xi1 = g[i] * (1 - g[j]) * (1 - g[l]), xi2 = g[j] * (1 - g[l]), xi3 = g[l];
+                    real wt = w[i] * w[j] * w[l] * (1 - g[j]) * (1 - g[l]) * (1 - g[l]) * RFABS(K->det);
                     for (int k = 0; k < 3; k++)
                         xq[n][k] = K->X[0][k] + xi1 * (K->X[1][k] - K->X[0][k]) + xi2 * (K->X[2][k] - K->X[0][k]) +
                                    xi3 * (K->X[3][k] - K->X[0][k]);
@@ -283,28 +308,29 @@ static int cell_rule(const Cell *K, double (*xq)[3], double *wq) {
     return n;
 }
 
-/* pinned facet rule (R-quad) on the facet with ascending vertices P */
-static int facet_rule(int dim, const double P[3][3], double (*xq)[3], double *wq) {
-    double g[3], w[3];
+/* facet rule (R-quad): 3-point Gauss-Legendre (2D edge) / collapsed 3x3 (3D triangle),
+ * exact to degree 5 / 4; facet integrands have degree <= 2 */
+static int facet_rule(int dim, const real P[3][3], real (*xq)[3], real *wq) {
+    real g[3], w[3];
     gauss01(3, g, w);
     int n = 0;
     if (dim == 2) {
-        double t[3] = {P[1][0] - P[0][0], P[1][1] - P[0][1], 0};
-        double len = sqrt(dot3(t, t));
+        real t[3] = {P[1][0] - P[0][0], P[1][1] - P[0][1], 0};
+        real len = RSQRT(dot3(t, t));
         for (int i = 0; i < 3; i++) {
             for (int k = 0; k < 3; k++) xq[n][k] = P[0][k] + g[i] * t[k];
             wq[n++] = w[i] * len;
         }
     } else {
-        double A[3];
+        real A[3];
         facet_area_vector(3, P, A);
-        double area = sqrt(dot3(A, A));
+        real area = RSQRT(dot3(A, A));
         for (int i = 0; i < 3; i++)
             for (int j = 0; j < 3; j++) {
-                double xi1 = g[i] * (1 - g[j]), xi2 = g[j];
+                real xi1 = g[i] * (1 - g[j]), xi2 = g[j];
                 for (int k = 0; k < 3; k++)
                     xq[n][k] = P[0][k] + xi1 * (P[1][k] - P[0][k]) + xi2 * (P[2][k] - P[0][k]);
-                wq[n++] = w[i] * w[j] * (1 - g[j]) * 2.0 * area;
+                wq[n++] = w[i] * w[j] * (1 - g[j]) * 2 * area;
             }
     }
     return n;
@@ -401,13 +427,47 @@ static void build_pattern(OCsr *A, const OMesh *m, const OSpace *s) {
     free(buf); free(sp); free(sc);
 }
 
-static void scatter(OCsr *A, const int *gi, int ni, const int *gj, int nj, const double *loc, int ldl) {
+/* accumulator of the assembly: per nonzero, the running sum in `real` */
+typedef struct {
+    real *acc;
+} Accum;
+
+static void scatter(const OCsr *A, Accum *S, const int *gi, int ni, const int *gj, int nj, const real *loc, int ldl) {
     for (int i = 0; i < ni; i++) {
         if (gi[i] < 0) continue;
         for (int j = 0; j < nj; j++) {
             if (gj[j] < 0) continue;
             i64 p = oc_find(A, gi[i], gj[j]);
-            A->v[p] += loc[i * ldl + j];
+            S->acc[p] += loc[i * ldl + j];
+        }
+    }
+}
+
+/* Reading R-exact, row by row: E = exponent of the largest |entry| of the row
+ * (max |x| = m 2^E, 1/2 <= m < 1, after rounding to fp64), G = 2^(E-88); every entry x
+ * becomes RN53(G * nearest_integer(x / G)).  x is split as hi + lo (hi = RN53(x),
+ * lo = RN53(x - hi)) and the grid rounding is done on the two doubles.               */
+static double grid_round(double hi, double lo, int E) {
+    double H = ldexp(hi, 88 - E), L = ldexp(lo, 88 - E);
+    double N = nearbyint(H);
+    double k = nearbyint((H - N) + L);
+    double v = ldexp(N + k, E - 88);
+    return v == 0 ? 0.0 : v;      /* exact cancellation: +0 */
+}
+
+static void finish(OCsr *A, const Accum *S) {
+    for (i64 i = 0; i < A->n; i++) {
+        double mx = 0;
+        for (i64 t = A->rp[i]; t < A->rp[i + 1]; t++) {
+            double h = (double)S->acc[t];
+            if (fabs(h) > mx) mx = fabs(h);
+        }
+        int E = 0;
+        if (mx > 0) frexp(mx, &E);
+        for (i64 t = A->rp[i]; t < A->rp[i + 1]; t++) {
+            double h = (double)S->acc[t];
+            double l = (double)(S->acc[t] - (real)h);
+            A->v[t] = mx > 0 ? grid_round(h, l, E) : 0.0;
         }
     }
 }
@@ -415,11 +475,12 @@ static void scatter(OCsr *A, const int *gi, int ni, const int *gj, int nj, const
 /* ------------------------------------------------------------------------- */
 /* E-B block  (Table 1)                       */
 /* ------------------------------------------------------------------------- */
-static void assemble_eb(OCsr *A, signed char *cnt, const OMesh *m, const OSpace *s, const OParams *p,
-                        const double *w) {
+static void assemble_eb(OCsr *A, Accum *S, signed char *cnt, const OMesh *m, const OSpace *s, const OParams *p,
+                        const double *w, const unsigned char *cmask) {
     int d = m->dim, nEl = d == 2 ? 3 : 6, nBl = d + 1;
-    double xq[64][3], wq[64];
+    real xq[64][3], wq[64];
     for (i64 c = 0; c < m->nc; c++) {
+        if (cmask && !cmask[c]) continue;
         Cell K;
         cell_geom(m, c, &K);
         Aff E[6], B[4];
@@ -436,7 +497,7 @@ static void assemble_eb(OCsr *A, signed char *cnt, const OMesh *m, const OSpace 
         }
         for (int q = 0; q < nBl; q++) { B[q] = basis_rt(&K, q, &sB[q]); gB[q] = s->fdof[om_facet_of_cell(m, c, q)]; }
         /* vcurl / curl of the E basis (constant) */
-        double curlE[6][3];
+        real curlE[6][3];
         for (int a = 0; a < nEl; a++) {
             if (d == 2) { curlE[a][0] = E[a].G[0][1]; curlE[a][1] = -E[a].G[0][0]; curlE[a][2] = 0; }
             else {
@@ -445,31 +506,32 @@ static void assemble_eb(OCsr *A, signed char *cnt, const OMesh *m, const OSpace 
                 curlE[a][2] = E[a].G[1][0] - E[a].G[0][1];
             }
         }
-        double pot[4][3], wx[3];
+        double pot[4][3];
+        real wx[3];
         cell_pot(m, c, w, pot);
         cell_wind(&K, pot, wx);
-        double EE[6 * 6] = {0}, EB[6 * 4] = {0}, BE[4 * 6] = {0};
-        int nq = cell_rule(&K, xq, wq);
+        real EE[6 * 6] = {0}, EB[6 * 4] = {0}, BE[4 * 6] = {0};
+        int nq = cell_rule(&K, 3, xq, wq);
         for (int t = 0; t < nq; t++) {
-            double ev[6][3], bv[4][3];
+            real ev[6][3], bv[4][3];
             for (int a = 0; a < nEl; a++) aff_eval(&E[a], &K, xq[t], ev[a]);
             for (int q = 0; q < nBl; q++) aff_eval(&B[q], &K, xq[t], bv[q]);
             for (int i = 0; i < nEl; i++) {
                 for (int j = 0; j < nEl; j++)
                     EE[i * 6 + j] += wq[t] * (d == 2 ? ev[j][0] * ev[i][0] : dot3(ev[j], ev[i]));
                 for (int k = 0; k < nBl; k++) {
-                    double wxb;
+                    real wxb;
                     if (d == 2) wxb = (wx[0] * bv[k][1] - wx[1] * bv[k][0]) * ev[i][0];
-                    else { double cr[3]; cross3(wx, bv[k], cr); wxb = dot3(cr, ev[i]); }
-                    double ab = dot3(bv[k], curlE[i]);
+                    else { real cr[3]; cross3(wx, bv[k], cr); wxb = dot3(cr, ev[i]); }
+                    real ab = dot3(bv[k], curlE[i]);
                     EB[i * 4 + k] += wq[t] * (wxb - ab / p->Rem);
                     BE[k * 6 + i] += wq[t] * ab;
                 }
             }
         }
-        scatter(A, gE, nEl, gE, nEl, EE, 6);
-        scatter(A, gE, nEl, gB, nBl, EB, 4);
-        scatter(A, gB, nBl, gE, nEl, BE, 6);
+        scatter(A, S, gE, nEl, gE, nEl, EE, 6);
+        scatter(A, S, gE, nEl, gB, nBl, EB, 4);
+        scatter(A, S, gB, nBl, gE, nEl, BE, 6);
         for (int k = 0; k < nBl; k++)
             for (int l = 0; l < nBl; l++)
                 if (gB[k] >= 0 && gB[l] >= 0) cnt[oc_find(A, gB[k], gB[l])] += (signed char)(sB[k] * sB[l]);
@@ -477,7 +539,7 @@ static void assemble_eb(OCsr *A, signed char *cnt, const OMesh *m, const OSpace 
     /* C = (1/Rem)(div psi_l, div psi_k), div psi = s/|K|: exact value (Kinv*m)/Rem (R-gamma) */
     double Kinv = d == 2 ? 2.0 * m->N * m->N : 6.0 * m->N * m->N * m->N;
     for (i64 t = 0; t < A->nnz; t++)
-        if (cnt[t]) A->v[t] += (Kinv * cnt[t]) / p->Rem;
+        if (cnt[t]) S->acc[t] += (real)(Kinv * cnt[t]) / p->Rem;
 }
 
 /* ------------------------------------------------------------------------- */
@@ -498,15 +560,15 @@ static int vel_basis(const OMesh *m, const OSpace *s, i64 c, const Cell *K, Aff 
     return n;
 }
 
-static void sym_grad(const Aff *f, double e[3][3]) {
-    for (int l = 0; l < 3; l++) for (int k = 0; k < 3; k++) e[l][k] = 0.5 * (f->G[l][k] + f->G[k][l]);
+static void sym_grad(const Aff *f, real e[3][3]) {
+    for (int l = 0; l < 3; l++) for (int k = 0; k < 3; k++) e[l][k] = (f->G[l][k] + f->G[k][l]) / 2;
 }
 
-static void assemble_vel(OCsr *A, signed char *cnt, const OMesh *m, const OSpace *s, const OParams *p,
+static void assemble_vel(OCsr *A, Accum *S, signed char *cnt, const OMesh *m, const OSpace *s, const OParams *p,
                          const double *w, const unsigned char *cmask) {
     int d = m->dim;
-    double xq[64][3], wq[64];
-    const double nu2 = 2.0 / p->Re;
+    real xq[64][3], wq[64];
+    const real nu2 = (real)2 / p->Re;
     /* cell terms */
     for (i64 c = 0; c < m->nc; c++) {
         if (cmask && !cmask[c]) continue;
@@ -516,37 +578,39 @@ static void assemble_vel(OCsr *A, signed char *cnt, const OMesh *m, const OSpace
         double sg[12];
         int gi[12];
         int nb = vel_basis(m, s, c, &K, F, sg, gi);
-        double eps[12][3][3];
+        real eps[12][3][3];
         for (int a = 0; a < nb; a++) sym_grad(&F[a], eps[a]);
-        double pot[4][3], wx[3];
+        double pot[4][3];
+        real wx[3];
         cell_pot(m, c, w, pot);
         cell_wind(&K, pot, wx);      /* constant on K, div w_h = 0 */
-        double loc[12 * 12] = {0};
-        int nq = cell_rule(&K, xq, wq);
+        real loc[12 * 12] = {0};
+        int nq = cell_rule(&K, 3, xq, wq);
         for (int t = 0; t < nq; t++) {
-            double fv[12][3];
+            real fv[12][3];
             for (int a = 0; a < nb; a++) aff_eval(&F[a], &K, xq[t], fv[a]);
             for (int i = 0; i < nb; i++) {
                 /* div(v (x) w)_l = sum_k (d_k v_l) w_k + v_l div w, div w_h = 0  (v = test fn i) */
-                double dvw[3];
+                real dvw[3];
                 for (int l = 0; l < 3; l++) {
-                    double sacc = 0.0;
+                    real sacc = 0;
                     for (int k = 0; k < d; k++) sacc += F[i].G[l][k] * wx[k];
                     dvw[l] = sacc;
                 }
                 for (int j = 0; j < nb; j++) {
-                    double ee = 0;
+                    real ee = 0;
                     for (int l = 0; l < 3; l++) for (int k = 0; k < 3; k++) ee += eps[j][l][k] * eps[i][l][k];
                     loc[i * 12 + j] += wq[t] * (nu2 * ee - dot3(fv[j], dvw));
                 }
             }
         }
-        scatter(A, gi, nb, gi, nb, loc, 12);
+        scatter(A, S, gi, nb, gi, nb, loc, 12);
         for (int i = 0; i < nb; i++)
             for (int j = 0; j < nb; j++)
                 if (gi[i] >= 0 && gi[j] >= 0) cnt[oc_find(A, gi[i], gi[j])] += (signed char)(sg[i] * sg[j]);
     }
     /* facet terms: SIPG + upwind (reading R-vel) */
+    static real loc[24 * 24];
     for (i64 f = 0; f < m->nfacet; f++) {
         int cp = m->fcell[2 * f], cm = m->fcell[2 * f + 1];
         if (cmask && !cmask[cp] && !(cm >= 0 && cmask[cm])) continue;
@@ -567,72 +631,75 @@ static void assemble_vel(OCsr *A, signed char *cnt, const OMesh *m, const OSpace
         /* facet vertices (ascending global id) and K+'s outward unit normal */
         int qf = -1;
         for (int q = 0; q <= d; q++) if (om_facet_of_cell(m, cp, q) == f) qf = q;
-        double P[3][3], Av[3];
+        real P[3][3], Av[3];
         facet_points(&Kp, qf, P);
         facet_area_vector(d, P, Av);
-        double an = sqrt(dot3(Av, Av)), n[3];
+        real an = RSQRT(dot3(Av, Av)), n[3];
         double sgn = facet_sign(&Kp, qf, Av);
         for (int k = 0; k < 3; k++) n[k] = sgn * Av[k] / an;
-        double hF;
+        real hF;
         if (d == 2) hF = an;
         else {
             hF = 0;
             for (int a = 0; a < 3; a++)
                 for (int b = a + 1; b < 3; b++) {
-                    double t[3] = {P[b][0] - P[a][0], P[b][1] - P[a][1], P[b][2] - P[a][2]};
-                    double l = sqrt(dot3(t, t));
+                    real t[3] = {P[b][0] - P[a][0], P[b][1] - P[a][1], P[b][2] - P[a][2]};
+                    real l = RSQRT(dot3(t, t));
                     if (l > hF) hF = l;
                 }
         }
-        double avg = interior ? 0.5 : 1.0;
-        double pen = (1.0 / p->Re) * (p->sigma / hF);
-        double pot[4][3], wx[3];
+        real avg = interior ? (real)1 / 2 : (real)1;
+        real pen = (real)p->sigma / ((real)p->Re * hF);
+        double pot[4][3];
+        real wx[3];
         cell_pot(m, cp, w, pot);
         cell_wind(&Kp, pot, wx);     /* w_h . n is continuous; K+'s value is used (R-w) */
-        double wn = dot3(wx, n), awn = fabs(wn);
-        double epsn[24][3];
+        real wn = dot3(wx, n), awn = RFABS(wn);
+        real epsn[24][3];
         for (int a = 0; a < nb; a++) {
-            double e[3][3];
+            real e[3][3];
             sym_grad(&F[a], e);
             for (int l = 0; l < 3; l++) epsn[a][l] = e[l][0] * n[0] + e[l][1] * n[1] + e[l][2] * n[2];
         }
-        static double loc[24 * 24];
         memset(loc, 0, sizeof(loc));
         int nq = facet_rule(d, P, xq, wq);
         for (int t = 0; t < nq; t++) {
-            double fv[24][3];
+            real fv[24][3];
             for (int a = 0; a < nb; a++) aff_eval(&F[a], side[a] > 0 ? &Kp : &Km, xq[t], fv[a]);
             for (int i = 0; i < nb; i++) {
-                double Ji = side[i];
+                real Ji = side[i];
                 for (int j = 0; j < nb; j++) {
-                    double Jj = side[j];
-                    double vv = dot3(fv[j], fv[i]);
-                    double t1 = -nu2 * avg * dot3(epsn[j], fv[i]) * Ji;
-                    double t2 = -nu2 * avg * dot3(fv[j], epsn[i]) * Jj;
-                    double t3 = pen * Jj * Ji * vv;
-                    double up;
-                    if (interior) up = (side[j] > 0 ? 0.5 * (wn + awn) : -0.5 * (-wn + awn)) * vv * Ji;
-                    else up = 0.5 * (wn + awn) * vv;
+                    real Jj = side[j];
+                    real vv = dot3(fv[j], fv[i]);
+                    real t1 = -nu2 * avg * dot3(epsn[j], fv[i]) * Ji;
+                    real t2 = -nu2 * avg * dot3(fv[j], epsn[i]) * Jj;
+                    real t3 = pen * Jj * Ji * vv;
+                    real up;
+                    if (interior) up = (side[j] > 0 ? (wn + awn) / 2 : -(-wn + awn) / 2) * vv * Ji;
+                    else up = (wn + awn) / 2 * vv;
                     loc[i * 24 + j] += wq[t] * (t1 + t2 + t3 + up);
                 }
             }
         }
-        scatter(A, gi, nb, gi, nb, loc, 24);
+        scatter(A, S, gi, nb, gi, nb, loc, 24);
     }
     /* gamma (div u, div v): div phi_{f,a} = s/(d|K|); exact value (G m)/d^2, G = gamma/|K| (R-gamma) */
     double Kinv = d == 2 ? 2.0 * m->N * m->N : 6.0 * m->N * m->N * m->N;
     double G = p->gamma * Kinv;
     for (i64 t = 0; t < A->nnz; t++)
-        if (cnt[t]) A->v[t] += (G * cnt[t]) / (double)(d * d);
+        if (cnt[t]) S->acc[t] += (real)(G * cnt[t]) / (d * d);
 }
 
 int oa_assemble_masked(OCsr *A, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
                        const unsigned char *cmask) {
     build_pattern(A, m, s);
     signed char *cnt = calloc((size_t)(A->nnz ? A->nnz : 1), 1);
-    if (s->block == ORC_EB) assemble_eb(A, cnt, m, s, p, w);
-    else assemble_vel(A, cnt, m, s, p, w, cmask);
-    free(cnt);
+    Accum S;
+    S.acc = calloc((size_t)(A->nnz ? A->nnz : 1), sizeof(real));
+    if (s->block == ORC_EB) assemble_eb(A, &S, cnt, m, s, p, w, cmask);
+    else assemble_vel(A, &S, cnt, m, s, p, w, cmask);
+    finish(A, &S);
+    free(cnt); free(S.acc);
     return 0;
 }
 
@@ -677,22 +744,22 @@ static i64 parent_cell(const OMesh *mf, const OMesh *mc, i64 cf) {
 
 /* the fine DoF functional N_I (R-basis) applied to an affine field F on cell K;
  * V holds the nev vertices of the DoF's entity (same units as K) */
-static double dof_functional(int block, int d, int kind, int sub, const double V[3][3], int nev, const Aff *F,
+static double dof_functional(int block, int d, int kind, int sub, const real V[3][3], int nev, const Aff *F,
                              const Cell *K) {
-    double fx[3];
+    real fx[3];
     if (kind == 0) { aff_eval(F, K, V[0], fx); return fx[0]; }          /* CG1: point value       */
     if (kind == 1 && d == 3) {                                            /* NED1: int_e phi.t      */
-        double mid[3] = {0.5 * (V[0][0] + V[1][0]), 0.5 * (V[0][1] + V[1][1]), 0.5 * (V[0][2] + V[1][2])};
+        real mid[3] = {(V[0][0] + V[1][0]) / 2, (V[0][1] + V[1][1]) / 2, (V[0][2] + V[1][2]) / 2};
         aff_eval(F, K, mid, fx);
-        double t[3] = {V[1][0] - V[0][0], V[1][1] - V[0][1], V[1][2] - V[0][2]};
-        return dot3(fx, t);
+        real t[3] = {V[1][0] - V[0][0], V[1][1] - V[0][1], V[1][2] - V[0][2]};
+        return (double)dot3(fx, t);
     }
-    double A[3];
+    real A[3];
     facet_area_vector(d, V, A);
-    if (block == ORC_VEL) { aff_eval(F, K, V[sub], fx); return dot3(fx, A); }   /* BDM: |f|(phi.n)(x_a) */
-    double sacc = 0;                                                      /* RT: flux of affine field */
+    if (block == ORC_VEL) { aff_eval(F, K, V[sub], fx); return (double)dot3(fx, A); }   /* BDM: |f|(phi.n)(x_a) */
+    real sacc = 0;                                                        /* RT: flux of affine field */
     for (int a = 0; a < nev; a++) { aff_eval(F, K, V[a], fx); sacc += dot3(fx, A); }
-    return sacc / nev;
+    return (double)(sacc / nev);
 }
 
 int op_prolongation(OCsr *P, const OMesh *mf, const OSpace *sf, const OMesh *mc, const OSpace *sc) {
@@ -717,9 +784,9 @@ int op_prolongation(OCsr *P, const OMesh *mf, const OSpace *sf, const OMesh *mc,
         int cf = kind == 0 ? vfirst[ent] : (kind == 1 ? efirst[ent] : ffirst[ent]);
         i64 ccell = parent_cell(mf, mc, cf);
         /* coarse cell geometry in fine lattice units */
-        double X[4][3] = {{0}};
+        real X[4][3] = {{0}};
         for (int a = 0; a < nvc; a++)
-            for (int k = 0; k < d; k++) X[a][k] = 2.0 * mc->lat[3 * mc->cv[ccell * nvc + a] + k];
+            for (int k = 0; k < d; k++) X[a][k] = 2 * mc->lat[3 * mc->cv[ccell * nvc + a] + k];
         Cell K;
         cell_geom_from(d, X, &K);
         /* coarse local basis functions of the same field as DoF I */
@@ -744,7 +811,7 @@ int op_prolongation(OCsr *P, const OMesh *mf, const OSpace *sf, const OMesh *mc,
             }
         }
         /* fine entity vertices (lattice) */
-        double V[3][3] = {{0}};
+        real V[3][3] = {{0}};
         int nev = 0;
         if (kind == 0) { for (int k = 0; k < d; k++) V[0][k] = mf->lat[3 * ent + k]; nev = 1; }
         else if (kind == 1 || (kind == 2 && d == 2)) {
@@ -834,16 +901,21 @@ int oa_nq(int dim) { return dim == 2 ? 16 : 64; }
 
 void oa_quadrature(const OMesh *m, double *pts, double *wts) {
     int nq = oa_nq(m->dim);
+    real xq[64][3], wq[64];
     for (i64 c = 0; c < m->nc; c++) {
         Cell K;
         cell_geom(m, c, &K);
-        cell_rule(&K, (double(*)[3])(pts + 3 * nq * c), wts + nq * c);
+        cell_rule(&K, 4, xq, wq);
+        for (int t = 0; t < nq; t++) {
+            for (int k = 0; k < 3; k++) pts[3 * (nq * c + t) + k] = (double)xq[t][k];
+            wts[nq * c + t] = (double)wq[t];
+        }
     }
 }
 
 void oa_load(const OMesh *m, const OSpace *s, const double *fv, double *out) {
     int nq = oa_nq(m->dim), nc = oa_ncomp(s);
-    double xq[64][3], wq[64];
+    real xq[64][3], wq[64];
     memset(out, 0, sizeof(double) * s->n);
     for (i64 c = 0; c < m->nc; c++) {
         Cell K;
@@ -851,26 +923,26 @@ void oa_load(const OMesh *m, const OSpace *s, const double *fv, double *out) {
         Aff F[16];
         int gi[16], off[16], ncp[16];
         int nb = local_basis(m, s, c, &K, F, gi, off, ncp);
-        cell_rule(&K, xq, wq);
+        cell_rule(&K, 4, xq, wq);
         for (int a = 0; a < nb; a++) {
             if (gi[a] < 0) continue;
-            double acc = 0;
+            real acc = 0;
             for (int t = 0; t < nq; t++) {
-                double v[3];
+                real v[3];
                 aff_eval(&F[a], &K, xq[t], v);
                 const double *f = fv + ((i64)c * nq + t) * nc + off[a];
-                double dd = 0;
+                real dd = 0;
                 for (int k = 0; k < ncp[a]; k++) dd += f[k] * v[k];
                 acc += wq[t] * dd;
             }
-            out[gi[a]] += acc;
+            out[gi[a]] += (double)acc;
         }
     }
 }
 
 void oa_eval(const OMesh *m, const OSpace *s, const double *coef, double *fv) {
     int nq = oa_nq(m->dim), nc = oa_ncomp(s);
-    double xq[64][3], wq[64];
+    real xq[64][3], wq[64];
     memset(fv, 0, sizeof(double) * m->nc * nq * nc);
     for (i64 c = 0; c < m->nc; c++) {
         Cell K;
@@ -878,14 +950,14 @@ void oa_eval(const OMesh *m, const OSpace *s, const double *coef, double *fv) {
         Aff F[16];
         int gi[16], off[16], ncp[16];
         int nb = local_basis(m, s, c, &K, F, gi, off, ncp);
-        cell_rule(&K, xq, wq);
+        cell_rule(&K, 4, xq, wq);
         for (int a = 0; a < nb; a++) {
             if (gi[a] < 0) continue;
             for (int t = 0; t < nq; t++) {
-                double v[3];
+                real v[3];
                 aff_eval(&F[a], &K, xq[t], v);
                 double *f = fv + ((i64)c * nq + t) * nc + off[a];
-                for (int k = 0; k < ncp[a]; k++) f[k] += coef[gi[a]] * v[k];
+                for (int k = 0; k < ncp[a]; k++) f[k] += coef[gi[a]] * (double)v[k];
             }
         }
     }
@@ -906,13 +978,13 @@ double oa_duality_error(const OMesh *m, const OSpace *s) {
         for (int i = 0; i < nb; i++) {
             if (gi[i] < 0) continue;
             int kind = s->dkind[gi[i]], ent = s->dent[gi[i]], sub = s->dsub[gi[i]], nev;
-            double V[3][3] = {{0}};
-            if (kind == 0) { for (int k = 0; k < 3; k++) V[0][k] = m->x[3 * ent + k]; nev = 1; }
+            real V[3][3] = {{0}};
+            if (kind == 0) { for (int k = 0; k < d; k++) V[0][k] = (real)m->lat[3 * ent + k] / m->N; nev = 1; }
             else if (kind == 1 || d == 2) {
-                for (int a = 0; a < 2; a++) for (int k = 0; k < 3; k++) V[a][k] = m->x[3 * m->ev[2 * ent + a] + k];
+                for (int a = 0; a < 2; a++) for (int k = 0; k < d; k++) V[a][k] = (real)m->lat[3 * m->ev[2 * ent + a] + k] / m->N;
                 nev = 2;
             } else {
-                for (int a = 0; a < 3; a++) for (int k = 0; k < 3; k++) V[a][k] = m->x[3 * m->fv[3 * ent + a] + k];
+                for (int a = 0; a < 3; a++) for (int k = 0; k < 3; k++) V[a][k] = (real)m->lat[3 * m->fv[3 * ent + a] + k] / m->N;
                 nev = 3;
             }
             for (int j = 0; j < nb; j++) {

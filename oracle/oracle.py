@@ -16,30 +16,34 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "liboracle.so")
+LIB_EXACT = os.path.join(HERE, "liboracle_exact.so")
 SOURCES = ["mesh.c", "space.c", "fem.c", "solve.c", "api.c"]
 
 
 def build(force: bool = False) -> str:
     """Compile the oracle (plain C, single-threaded, -ffp-contract=off: every fused
-    multiply-add is an explicit fma() call of the pinned rounding order)."""
+    multiply-add is an explicit fma() call of the pinned rounding order) twice:
+    liboracle.so with real = double and liboracle_exact.so with real = __float128 for the
+    element integrals (reading R-exact, see fem.c)."""
     srcs = [os.path.join(HERE, s) for s in SOURCES] + [os.path.join(HERE, "orc.h")]
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(s) for s in srcs):
-        return LIB
-    cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-mfma", "-fPIC", "-shared", "-o", LIB + ".tmp"]
-    cmd += [os.path.join(HERE, s) for s in SOURCES] + ["-lm"]
-    subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
+    newest = max(os.path.getmtime(s) for s in srcs)
+    for lib, extra in ((LIB, []), (LIB_EXACT, ["-DORC_EXACT"])):
+        if not force and os.path.exists(lib) and os.path.getmtime(lib) >= newest:
+            continue
+        cmd = ["gcc", "-O2", "-std=gnu11", "-ffp-contract=off", "-mfma", "-fPIC", "-shared", *extra, "-o", lib + ".tmp"]
+        cmd += [os.path.join(HERE, s) for s in SOURCES] + ["-lquadmath", "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(lib + ".tmp", lib)
     return LIB
 
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
+def lib(exact: bool = False):
+    if exact not in _libs:
         build()
-        L = C.CDLL(LIB)
+        L = C.CDLL(LIB_EXACT if exact else LIB)
         vp, i64p, ip, dp = C.c_void_p, C.POINTER(C.c_longlong), C.POINTER(C.c_int), C.POINTER(C.c_double)
         L.orc_create.restype = vp
         L.orc_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, ip, dp]
@@ -74,8 +78,8 @@ def lib():
         L.orc_duality_error.argtypes = [vp, C.c_int]
         L.orc_set_patches.argtypes = [vp, C.c_int, C.c_longlong, i64p, ip]
         L.orc_dense_lu_solve.argtypes = [C.c_int, dp, dp, dp, dp, ip]
-        _lib = L
-    return _lib
+        _libs[exact] = L
+    return _libs[exact]
 
 
 def _d(a):
@@ -112,8 +116,10 @@ class Csr:
 class Oracle:
     """Hierarchy for one configuration (see paper_2104_14855_b200.workloads.Config)."""
 
-    def __init__(self, cfg, w, nlev=None, N=None, cmask=None):
-        L = lib()
+    def __init__(self, cfg, w, nlev=None, N=None, cmask=None, exact=False):
+        """exact=True: element integrals in __float128 (reading R-exact): every operator
+        entry is the fp64 value nearest to the exact discrete bilinear form."""
+        self._L = L = lib(exact)
         self.cfg = cfg
         self.dim = cfg.dim
         self.nlev = nlev if nlev is not None else cfg.levels
@@ -134,13 +140,13 @@ class Oracle:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().orc_destroy(self.h)
+            self._L.orc_destroy(self.h)
             self.h = None
 
     def info(self, level=-1):
         level = level % self.nlev
         out = np.zeros(11, dtype=np.int64)
-        lib().orc_level_info(self.h, level, _l(out))
+        self._L.orc_level_info(self.h, level, _l(out))
         keys = ["n", "nnz", "npatch", "sum_n", "sum_n2", "nE", "nv", "nc", "ne", "nf", "p_nnz"]
         return dict(zip(keys, (int(v) for v in out)))
 
@@ -153,7 +159,7 @@ class Oracle:
         rp = np.zeros(i["n"] + 1, np.int64)
         ci = np.zeros(i["nnz"], np.int32)
         v = np.zeros(i["nnz"], np.float64)
-        lib().orc_export_csr(self.h, level, _l(rp), _i(ci), _d(v))
+        self._L.orc_export_csr(self.h, level, _l(rp), _i(ci), _d(v))
         return Csr(rp, ci, v)
 
     def prolongation(self, level=-1):
@@ -162,7 +168,7 @@ class Oracle:
         rp = np.zeros(i["n"] + 1, np.int64)
         ci = np.zeros(i["p_nnz"], np.int32)
         v = np.zeros(i["p_nnz"], np.float64)
-        lib().orc_export_prolongation(self.h, level, _l(rp), _i(ci), _d(v))
+        self._L.orc_export_prolongation(self.h, level, _l(rp), _i(ci), _d(v))
         return Csr(rp, ci, v)
 
     def patches(self, level=-1):
@@ -172,7 +178,7 @@ class Oracle:
         dofs = np.zeros(i["sum_n"], np.int32)
         vert = np.zeros(i["npatch"], np.int32)
         mult = np.zeros(i["n"], np.int32)
-        lib().orc_export_patches(self.h, level, _l(ptr), _i(dofs), _i(vert), _i(mult))
+        self._L.orc_export_patches(self.h, level, _l(ptr), _i(dofs), _i(vert), _i(mult))
         return ptr, dofs, vert, mult
 
     def mesh(self, level=-1):
@@ -184,7 +190,7 @@ class Oracle:
         ev = np.zeros(2 * i["ne"], np.int32); fv = np.zeros(max(3 * i["nf"], 1), np.int32)
         fc = np.zeros(2 * nfacet, np.int32)
         dk = np.zeros(i["n"], np.int32); de = np.zeros(i["n"], np.int32); ds = np.zeros(i["n"], np.int32)
-        lib().orc_export_mesh(self.h, level, _d(x), _i(cv), _i(ev), _i(fv), _i(fc), _i(dk), _i(de), _i(ds))
+        self._L.orc_export_mesh(self.h, level, _d(x), _i(cv), _i(ev), _i(fv), _i(fc), _i(dk), _i(de), _i(ds))
         return dict(x=x.reshape(-1, 3), cv=cv.reshape(-1, d + 1), ev=ev.reshape(-1, 2),
                     fv=fv[:3 * i["nf"]].reshape(-1, 3), fcell=fc.reshape(-1, 2), dkind=dk, dent=de, dsub=ds)
 
@@ -192,14 +198,14 @@ class Oracle:
         level = level % self.nlev
         x = np.ascontiguousarray(x, np.float64)
         y = np.zeros(self.n(level))
-        lib().orc_spmv(self.h, level, _d(x), _d(y))
+        self._L.orc_spmv(self.h, level, _d(x), _d(y))
         return y
 
     def residual(self, b, x, level=-1):
         level = level % self.nlev
         b = np.ascontiguousarray(b, np.float64); x = np.ascontiguousarray(x, np.float64)
         r = np.zeros(self.n(level))
-        lib().orc_residual(self.h, level, _d(b), _d(x), _d(r))
+        self._L.orc_residual(self.h, level, _d(b), _d(x), _d(r))
         return r
 
     def patch_matrix(self, patch, level=-1):
@@ -207,7 +213,7 @@ class Oracle:
         ptr = self.patches(level)[0]
         k = int(ptr[patch + 1] - ptr[patch])
         a = np.zeros(k * k)
-        lib().orc_patch_matrix(self.h, level, patch, _d(a))
+        self._L.orc_patch_matrix(self.h, level, patch, _d(a))
         return a.reshape(k, k)
 
     def patch_lu(self, patch, level=-1):
@@ -215,14 +221,14 @@ class Oracle:
         ptr = self.patches(level)[0]
         k = int(ptr[patch + 1] - ptr[patch])
         a = np.zeros(k * k); perm = np.zeros(k, np.int32)
-        st = lib().orc_patch_lu(self.h, level, patch, _d(a), _i(perm))
+        st = self._L.orc_patch_lu(self.h, level, patch, _d(a), _i(perm))
         return a.reshape(k, k), perm, st
 
     def sweep(self, b, x, level=-1, nsweeps=1, x_is_zero=False):
         level = level % self.nlev
         b = np.ascontiguousarray(b, np.float64)
         x = np.array(x, dtype=np.float64, copy=True) if x is not None else np.zeros(self.n(level))
-        st = lib().orc_sweep(self.h, level, nsweeps, int(x_is_zero), _d(b), _d(x))
+        st = self._L.orc_sweep(self.h, level, nsweeps, int(x_is_zero), _d(b), _d(x))
         if st:
             raise ArithmeticError(f"oracle: singular patch {st - 1}")
         return x
@@ -233,7 +239,7 @@ class Oracle:
         x = np.ascontiguousarray(x if x is not None else np.zeros(self.n(level)), np.float64)
         dofs = np.ascontiguousarray(dofs, np.int32)
         out = np.zeros(len(dofs))
-        st = lib().orc_sweep_sample(self.h, level, int(x_is_zero), _d(b), _d(x), len(dofs), _i(dofs), _d(out))
+        st = self._L.orc_sweep_sample(self.h, level, int(x_is_zero), _d(b), _d(x), len(dofs), _i(dofs), _d(out))
         if st:
             raise ArithmeticError(f"oracle: singular patch {st - 1}")
         return out
@@ -242,34 +248,34 @@ class Oracle:
         level = level % self.nlev
         r = np.ascontiguousarray(r, np.float64)
         rc = np.zeros(self.n(level - 1))
-        lib().orc_restrict(self.h, level, _d(r), _d(rc))
+        self._L.orc_restrict(self.h, level, _d(r), _d(rc))
         return rc
 
     def prolong_add(self, ec, x, level=-1):
         level = level % self.nlev
         ec = np.ascontiguousarray(ec, np.float64)
         x = np.array(x, dtype=np.float64, copy=True)
-        lib().orc_prolong_add(self.h, level, _d(ec), _d(x))
+        self._L.orc_prolong_add(self.h, level, _d(ec), _d(x))
         return x
 
     def coarse_solve(self, b):
         b = np.ascontiguousarray(b, np.float64)
         x = np.zeros(self.n(0))
-        if lib().orc_coarse_solve(self.h, _d(b), _d(x)):
+        if self._L.orc_coarse_solve(self.h, _d(b), _d(x)):
             raise ArithmeticError("oracle: singular coarse operator")
         return x
 
     def coarse_lu(self):
         n = self.n(0)
         a = np.zeros(n * n); p = np.zeros(n, np.int32)
-        st = lib().orc_coarse_lu(self.h, _d(a), _i(p))
+        st = self._L.orc_coarse_lu(self.h, _d(a), _i(p))
         return a.reshape(n, n), p, st
 
     def vcycle(self, b, level=None):
         level = self.nlev - 1 if level is None else level % self.nlev
         b = np.ascontiguousarray(b, np.float64)
         x = np.zeros(self.n(level))
-        if lib().orc_vcycle_level(self.h, level, _d(b), _d(x)):
+        if self._L.orc_vcycle_level(self.h, level, _d(b), _d(x)):
             raise ArithmeticError("oracle: V-cycle failed (singular patch or coarse operator)")
         return x
 
@@ -278,7 +284,7 @@ class Oracle:
         x = np.zeros(self.n())
         its = np.zeros(1, np.int32)
         hist = np.zeros(maxit + 1)
-        st = lib().orc_gmres(self.h, _d(b), _d(x), rtol, atol, maxit, _i(its), _d(hist))
+        st = self._L.orc_gmres(self.h, _d(b), _d(x), rtol, atol, maxit, _i(its), _d(hist))
         if st == 2:
             raise ArithmeticError("oracle: GMRES preconditioner failed")
         return x, int(its[0]), hist[: int(its[0]) + 1], st == 0
@@ -287,17 +293,17 @@ class Oracle:
     def quadrature(self, level=-1):
         level = level % self.nlev
         out = np.zeros(2, np.int64)
-        lib().orc_quad_info(self.h, level, _l(out))
+        self._L.orc_quad_info(self.h, level, _l(out))
         npts, ncomp = int(out[0]), int(out[1])
         pts = np.zeros(3 * npts); wts = np.zeros(npts)
-        lib().orc_quadrature(self.h, level, _d(pts), _d(wts))
+        self._L.orc_quadrature(self.h, level, _d(pts), _d(wts))
         return pts.reshape(-1, 3), wts, ncomp
 
     def load(self, fvals, level=-1):
         level = level % self.nlev
         fvals = np.ascontiguousarray(fvals, np.float64)
         out = np.zeros(self.n(level))
-        lib().orc_load(self.h, level, _d(fvals), _d(out))
+        self._L.orc_load(self.h, level, _d(fvals), _d(out))
         return out
 
     def eval(self, coef, level=-1):
@@ -305,13 +311,13 @@ class Oracle:
         npts, ncomp = self.quadrature(level)[1].shape[0], self.quadrature(level)[2]
         coef = np.ascontiguousarray(coef, np.float64)
         fv = np.zeros(npts * ncomp)
-        lib().orc_eval(self.h, level, _d(coef), _d(fv))
+        self._L.orc_eval(self.h, level, _d(coef), _d(fv))
         return fv.reshape(npts, ncomp)
 
     def duality_error(self, level=-1):
-        return lib().orc_duality_error(self.h, level % self.nlev)
+        return self._L.orc_duality_error(self.h, level % self.nlev)
 
     def set_patches(self, ptr, dofs, level=-1):
         """TEST HOOK: override the subspace decomposition of a level."""
         ptr = np.ascontiguousarray(ptr, np.int64); dofs = np.ascontiguousarray(dofs, np.int32)
-        lib().orc_set_patches(self.h, level % self.nlev, len(ptr) - 1, _l(ptr), _i(dofs))
+        self._L.orc_set_patches(self.h, level % self.nlev, len(ptr) - 1, _l(ptr), _i(dofs))

@@ -85,7 +85,8 @@ typedef struct {
  * function (1 per vertex), 3D vector potential (3 per vertex). */
 int oa_assemble(OCsr *A, const OMesh *m, const OSpace *s, const OParams *p, const double *w);
 /* as oa_assemble, but only cells with cmask[c] != 0 (and facets touching one) contribute;
- * rows whose support neighbourhood lies inside the mask are bitwise identical to oa_assemble */
+ * rows whose support neighbourhood lies inside the mask are bitwise identical to oa_assemble
+ * (the row rounding of R-exact depends on the row only) */
 int oa_assemble_masked(OCsr *A, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
                        const unsigned char *cmask);
 

@@ -9,6 +9,9 @@
 
 namespace mhdp {
 
+#ifdef MHDP_QUAD_CHECK
+#include "quadreal_check.hpp"
+#else
 struct dd {
     double hi = 0.0, lo = 0.0;
     dd() = default;
@@ -68,8 +71,10 @@ inline dd sqrt(const dd &a) {
     return fast_two_sum(x, r.hi / (2.0 * x)) + dd((r.lo) / (2.0 * x));
 }
 
+#endif
+
 // uniform helpers for double and dd
 inline double to_double(double x) { return x; }
-inline double to_double(const dd &x) { return x.hi; }
+inline double to_double(const dd &x) { return x.value(); }
 
 }  // namespace mhdp

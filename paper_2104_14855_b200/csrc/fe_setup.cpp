@@ -455,10 +455,29 @@ void incidence(const Mesh &m, int kind, std::vector<i64> &ptr, std::vector<int> 
     for (i64 c = 0; c < m.nc; ++c) for (int t = 0; t < per; ++t) cells[fill[ent(c, t)]++] = (int)c;
 }
 
-// R-exact: the rounded entry, with exact cancellations (|sum| <= 2^-80 sum|terms|) -> 0
-inline double round_entry(const dd &acc, double abssum) {
-    const double v = acc.value();
-    return std::fabs(v) <= std::ldexp(abssum, -80) ? 0.0 : v;
+// R-exact: round the extended-precision entries of one row.  E = exponent of the row's
+// largest |entry| (RN53, frexp convention), G = 2^(E-88): each entry is first rounded to
+// the nearest multiple of G, then to fp64 (ties to even).  Exact values on the G-grid --
+// in particular dyadic values with few significant bits, whose fp64 rounding can be an
+// exact tie -- are rounded exactly; exact cancellations become 0.
+inline double grid_round(const dd &x, int E) {
+    const double H = std::ldexp(x.hi, 88 - E), L = std::ldexp(x.lo, 88 - E);
+    const double N = std::nearbyint(H);
+    const double k = std::nearbyint((H - N) + L);
+    const double v = std::ldexp(N + k, E - 88);
+    return v == 0.0 ? 0.0 : v;   // exact cancellation: +0
+}
+
+void round_row(const dd *x, i64 len, double *out) {
+    double mx = 0.0;
+    for (i64 k = 0; k < len; ++k) mx = std::max(mx, std::fabs(x[k].value()));
+    if (mx == 0.0) {
+        for (i64 k = 0; k < len; ++k) out[k] = 0.0;
+        return;
+    }
+    int E;
+    std::frexp(mx, &E);
+    for (i64 k = 0; k < len; ++k) out[k] = grid_round(x[k], E);
 }
 
 // ------------------------------------------------------------------------------------
@@ -593,7 +612,6 @@ void assemble_eb(const Mesh &m, const Space &s, const Params &p, const double *p
         cells_of(r, b, e);
         const i64 base = P.rp[r], len = P.rp[r + 1] - base;
         std::vector<dd> acc(len);
-        std::vector<double> mag(len, 0.0);
         std::vector<int> cnt(len, 0);
         const bool isB = dkind[r] == 2;
         for (const int *c = b; c != e; ++c) {
@@ -601,11 +619,7 @@ void assemble_eb(const Mesh &m, const Space &s, const Params &p, const double *p
             int li = -1;
             if (!isB) { for (int a = 0; a < K.nE; ++a) if (K.gE[a] == r) li = a; }
             else { for (int q = 0; q < K.nB; ++q) if (K.gB[q] == r) li = q; }
-            auto add = [&](int col, const dd &v) {
-                const i64 k = find_col(P, r, col) - base;
-                acc[k] += v;
-                mag[k] += std::fabs(v.value());
-            };
+            auto add = [&](int col, const dd &v) { acc[find_col(P, r, col) - base] += v; };
             if (!isB) {
                 for (int j = 0; j < K.nE; ++j) if (K.gE[j] >= 0) add(K.gE[j], K.EE[li][j]);
                 for (int q = 0; q < K.nB; ++q) if (K.gB[q] >= 0) add(K.gB[q], K.EB[li][q]);
@@ -615,13 +629,10 @@ void assemble_eb(const Mesh &m, const Space &s, const Params &p, const double *p
                     if (K.gB[q] >= 0) cnt[find_col(P, r, K.gB[q]) - base] += (int)(K.sB[li] * K.sB[q]);
             }
         }
-        for (i64 k = 0; k < len; ++k) {
-            double v = round_entry(acc[k], mag[k]);
-            // C = (1/Rem)(div psi_l, div psi_k): exact form (Kinv m) / Rem (R-gamma); B-B entries
-            // receive no other contribution
-            if (cnt[k]) v = (Kinv * cnt[k]) / p.Rem;
-            val[base + k] = v;
-        }
+        // C = (1/Rem)(div psi_l, div psi_k): exact value Kinv m / Rem (R-gamma)
+        for (i64 k = 0; k < len; ++k)
+            if (cnt[k]) acc[k] += dd(Kinv * cnt[k]) / dd(p.Rem);
+        round_row(acc.data(), len, val.data() + base);
     }
 }
 
@@ -705,14 +716,9 @@ void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *
         const int r0 = s.fdof[f];
         const i64 base = P.rp[r0], len = P.rp[r0 + 1] - base;
         std::vector<dd> acc(d * len);
-        std::vector<double> mag(d * len, 0.0);
         std::vector<int> cnt(len, 0);
         auto pos = [&](int col) -> i64 { return find_col(P, r0, col) - base; };
-        auto add = [&](int a, int col, const dd &v) {
-            const i64 k = a * len + pos(col);
-            acc[k] += v;
-            mag[k] += std::fabs(v.value());
-        };
+        auto add = [&](int a, int col, const dd &v) { acc[a * len + pos(col)] += v; };
         // ---- cell terms, cells of f ascending ----
         std::vector<int> fcells;
         for (int side = 0; side < 2; ++side) if (m.fcell[2 * f + side] >= 0) fcells.push_back(m.fcell[2 * f + side]);
@@ -728,8 +734,7 @@ void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *
                     if (K.gi[j] < 0) continue;
                     dd ee(0.0);
                     for (int l = 0; l < 3; ++l) for (int r = 0; r < 3; ++r) ee += K.eps[j][l][r] * K.eps[i][l][r];
-                    add(a, K.gi[j], nu2 * V * ee);                                 // viscous
-                    add(a, K.gi[j], -(dot3(K.B.v[j], K.B.v[i]) * gw * Vn));         // advection
+                    add(a, K.gi[j], nu2 * V * ee - dot3(K.B.v[j], K.B.v[i]) * gw * Vn);   // viscous - advection
                 }
             }
             for (int j = 0; j < nb; ++j)
@@ -810,19 +815,13 @@ void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *
                 }
             }
         }
-        // ---- gamma (div u, div v) = gamma Kinv m / d^2, exact (R-gamma); entry rounded once (R-exact)
+        // ---- gamma (div u, div v) = gamma Kinv m / d^2, exact (R-gamma); rows rounded once (R-exact)
         const double Gk = p.gamma * Kinv;
-        for (int a = 0; a < d; ++a)
-            for (i64 k = 0; k < len; ++k) {
-                dd v = acc[a * len + k];
-                double mg = mag[a * len + k];
-                if (cnt[k]) {
-                    const dd gam = dd(Gk * cnt[k]) / dd((double)(d * d));
-                    v += gam;
-                    mg += std::fabs(gam.value());
-                }
-                val[P.rp[r0 + a] + k] = round_entry(v, mg);
-            }
+        for (int a = 0; a < d; ++a) {
+            for (i64 k = 0; k < len; ++k)
+                if (cnt[k]) acc[a * len + k] += dd(Gk * cnt[k]) / dd((double)(d * d));
+            round_row(acc.data() + a * len, len, val.data() + P.rp[r0 + a]);
+        }
     }
 }
 

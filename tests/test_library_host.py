@@ -1,11 +1,12 @@
 """Parity tier P-A (CPU, no GPU): the library's own host setup vs the oracle.
 
-The library (paper_2104_14855_b200/csrc/fe_setup.cpp) and the oracle (oracle/*.c) build
-the hierarchy independently.  Bit-exact: free-DoF numbering (through the CSR pattern),
-vertex-star patch lists, the prolongation (all entries are dyadic rationals, reading
-R-prol).  Operator values: |a_lib - a_oracle| <= 1e-13 max|row|.
-Sizes: reduced versions of all five BASELINE configurations with every level, plus
-the full c1 and c2 hierarchies.
+The library (paper_2104_14855_b200/csrc/fe_setup.cpp: closed-form barycentric moments in
+double-double, gather-form assembly) and the oracle (oracle/*.c: Gauss quadrature,
+scatter-form assembly) build the hierarchy independently.  Bit-exact: free-DoF numbering
+(through the CSR pattern), vertex-star patch lists, the prolongation (dyadic rationals,
+reading R-prol) and -- against the oracle's exact build (__float128, reading R-exact) --
+every operator value.  Against the oracle's fp64 build the values agree to
+<= 1e-13 max|row|.
 """
 import numpy as np
 import pytest
@@ -48,6 +49,27 @@ def test_host_setup_matches_oracle(mh, oracle_mod, name, N, L):
         assert np.array_equal(P.v.view(np.uint64), pv.view(np.uint64)), f"level {l}: prolongation values"
         info = ctx.info(l)
         assert info["npatch"] == len(ptr_o) - 1 and info["sum_n"] == len(dofs_o)
+
+
+EXACT_CASES = [("c1", 8, 2), ("c2", 32, 3), ("c3", 16, 3), ("c4", 4, 2), ("c5", 4, 2)]
+
+
+@pytest.mark.parametrize("name,N,L", EXACT_CASES, ids=[f"{c}-N{n}L{l}" for c, n, l in EXACT_CASES])
+def test_operator_bitexact_vs_exact_oracle(mh, oracle_mod, name, N, L):
+    """R-exact: both implementations return, for every entry, the fp64 rounding (through
+    the row grid) of the exact discrete bilinear form -- so the operators are identical."""
+    from paper_2104_14855_b200 import workloads
+    cfg = workloads.small(name, N, L)
+    w, _, _ = workloads.draw(cfg, 1, seed=5)
+    orc = oracle_mod.Oracle(cfg, w, exact=True)
+    ctx = mh.Context(-1)
+    ctx.assemble(cfg, w)
+    for l in range(L):
+        A = orc.csr(l)
+        rp, ci, v = ctx.csr(l)
+        assert np.array_equal(A.rp, rp) and np.array_equal(A.ci, ci)
+        diff = np.flatnonzero(A.v.view(np.uint64) != v.view(np.uint64))
+        assert diff.size == 0, f"level {l}: {diff.size} entries differ, e.g. {A.v[diff[:3]]} vs {v[diff[:3]]}"
 
 
 def test_gamma_and_curl_entries_bitwise(mh, oracle_mod):
