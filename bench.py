@@ -96,6 +96,24 @@ def dist_init():
     return ws, rank, local
 
 
+def max_over_ranks(x: float, device=None) -> float:
+    """Max of a per-rank time over all ranks (identity without a process group).  Each
+    rank runs an independent replica (replicas only), so the whole-job step
+    time is the slowest replica's."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_seed(base: int, rank: int) -> int:
+    """Seed of the right-hand side of rank `rank`'s replica."""
+    return base + rank
+
+
 # ----------------------------------------------------------------------------------------
 # reference arm: the oracle
 # ----------------------------------------------------------------------------------------
@@ -151,7 +169,7 @@ def run_ours(args):
     cfg = workloads.CONFIGS[args.config]
     stream = torch.cuda.current_stream(dev)
     ctx = mhdp.Context(local, stream.cuda_stream)
-    seed = args.seed + rank
+    seed = replica_seed(args.seed, rank)
     t0 = time.perf_counter()
     w0, _, _ = workloads.draw(cfg, 1, seed)
     ctx.assemble(cfg, w0)
@@ -192,11 +210,7 @@ def run_ours(args):
     launches = ctx.launch_count() - l0
     ms = ev0.elapsed_time(ev1) / args.steps
     barrier()
-    if ws > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, dev)
 
     # ---- finest single sweep (K1+K2+K3) and the dominant kernel K2 alone ----
     reps = max(3, args.steps)
@@ -245,12 +259,7 @@ def run_ours(args):
     te = time.perf_counter()
     for _ in range(args.steps):
         ctx.vcycle_host(bnp, xnp)
-    e2e_ms = (time.perf_counter() - te) * 1e3 / args.steps
-    if ws > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks((time.perf_counter() - te) * 1e3 / args.steps, dev)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

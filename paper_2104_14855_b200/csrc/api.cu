@@ -249,7 +249,7 @@ mhdp_status build_patches(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
         pn[i] = (int)(H.pptr[i + 1] - H.pptr[i]);
         mx = std::max(mx, pn[i]);
         foff[i] = f;
-        f += ((int64_t)pn[i] * pn[i] + 15) / 16 * 16;   // 128-byte aligned factor blocks
+        f += ((int64_t)pn[i] * pn[i] + pn[i] + 15) / 16 * 16;   // packed stream n^2+n, 128-byte aligned
     }
     if (mx > 160) return fail(ctx, MHDP_EINVAL, "patch larger than 160 DoFs is not supported");
     P.max_n = mx;
@@ -793,14 +793,14 @@ mhdp_status mhdp_export_patch_lu(mhdp_ctx *ctx, int level, long long patch, doub
     int64_t foff = 0;
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaMemcpy(&foff, P.foff + patch, sizeof(int64_t), cudaMemcpyDeviceToHost));
-    std::vector<double> pk((size_t)n * n);
-    CK(cudaMemcpy(pk.data(), P.fac + foff, sizeof(double) * n * n, cudaMemcpyDeviceToHost));
+    std::vector<double> pk((size_t)n * n + n);
+    CK(cudaMemcpy(pk.data(), P.fac + foff, sizeof(double) * (n * n + n), cudaMemcpyDeviceToHost));
     // decode the packed streaming layout (kernels.cu pack_fwd / pack_bwd)
     for (int j = 0; j < n; ++j) {
         const int64_t f = (int64_t)j * n - (int64_t)j * (j + 1) / 2;
-        const int64_t b = (int64_t)n * (n - 1) / 2 + (int64_t)n * (n + 1) / 2 - (int64_t)(j + 1) * (j + 2) / 2;
+        const int64_t b = (int64_t)n * (n - 1) - (int64_t)j * (j + 1) / 2 + 2 * (n - 1 - j);
         for (int i = 0; i < n; ++i)
-            lu[(size_t)i * n + j] = i > j ? pk[f + i - j - 1] : (i == j ? pk[b] : pk[b + 1 + i]);
+            lu[(size_t)i * n + j] = i > j ? pk[f + i - j - 1] : (i == j ? pk[b] : pk[b + 2 + i]);
     }
     CK(cudaMemcpy(perm, P.perm + H.pptr[patch], sizeof(int) * n, cudaMemcpyDeviceToHost));
     return MHDP_OK;
