@@ -52,7 +52,7 @@ struct mhdp_ctx {
     double *clut = nullptr;    // column-major LU of A_0
     int *cperm = nullptr;
     double *cz = nullptr;
-    int *cflags = nullptr;
+    double *crdiag = nullptr;
     // scratch
     int *d_status = nullptr;
     double *d_scal = nullptr;  // dot partials + results
@@ -113,7 +113,7 @@ void free_device(mhdp_ctx *c) {
     for (void *p : c->allocs) cudaFree(p);
     c->allocs.clear();
     c->D.clear();
-    c->clut = nullptr; c->cperm = nullptr; c->cz = nullptr; c->cflags = nullptr;
+    c->clut = nullptr; c->cperm = nullptr; c->cz = nullptr; c->crdiag = nullptr;
     c->d_status = nullptr; c->d_scal = nullptr;
     c->gV = c->gZ = c->gw = nullptr; c->g_cap = 0;
     c->setup_done = false;
@@ -301,7 +301,7 @@ void sweep(mhdp_ctx *ctx, int l, const double *b, double *x, bool x_zero) {
 }
 
 void coarse_solve(mhdp_ctx *ctx, const double *b, double *x) {
-    launch_dense_solve(ctx->clut, ctx->cperm, ctx->n0, b, x, ctx->cz, ctx->cflags, ctx->stream);
+    launch_dense_solve(ctx->clut, ctx->crdiag, ctx->cperm, ctx->n0, b, x, ctx->cz, ctx->stream);
 }
 
 void vcycle(mhdp_ctx *ctx, int l, const double *b, double *x) {
@@ -533,11 +533,12 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         CK(cudaMemcpy(a, dense.data(), sizeof(double) * n0 * n0, cudaMemcpyHostToDevice));
         if ((st = dalloc(ctx, &ctx->cperm, n0))) return st;
         if ((st = dalloc(ctx, &ctx->clut, n0 * n0))) return st;
-        if ((st = dalloc(ctx, &ctx->cz, n0))) return st;
-        if ((st = dalloc(ctx, &ctx->cflags, 2 * (n0 + 63) / 64 + 2))) return st;
+        if ((st = dalloc(ctx, &ctx->cz, 2 * n0))) return st;
+        if ((st = dalloc(ctx, &ctx->crdiag, n0))) return st;
         CK(cudaMemset(ctx->d_status, 0, sizeof(int)));
         launch_dense_lu(a, (int)n0, ctx->cperm, ctx->d_status, ctx->d_scal, ctx->stream);
         launch_transpose(a, ctx->clut, (int)n0, ctx->stream);
+        launch_recip_diag(ctx->clut, (int)n0, ctx->crdiag, ctx->stream);
         if ((st = check_launch(ctx))) return st;
         CK(cudaStreamSynchronize(ctx->stream));
         cudaFree(a);

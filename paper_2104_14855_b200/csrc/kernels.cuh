@@ -76,9 +76,11 @@ void launch_dense_lu(double *a, int n, int *perm, int *status, double *scratch, 
 // transpose the row-major factor into the column-major copy used by the solve
 void launch_transpose(const double *a, double *at, int n, cudaStream_t s);
 // K8: x = U^-1 L^-1 P b with the column-major factor lut
-// flags: 2*ceil(n/64) ints of scratch
-void launch_dense_solve(const double *lut, const int *perm, int n, const double *b, double *x,
-                        double *z, int *flags, cudaStream_t s);
+// K8: x = U^-1 L^-1 P b; rdiag = RN(1/u_jj) (launch_recip_diag); z: 2n doubles of scratch.
+// x must not alias b (x is pre-filled with a sentinel).
+void launch_dense_solve(const double *lut, const double *rdiag, const int *perm, int n, const double *b, double *x,
+                        double *z, cudaStream_t s);
+void launch_recip_diag(const double *lut, int n, double *rdiag, cudaStream_t s);
 // K9 vector ops (deterministic reductions)
 void launch_dot(const double *a, const double *b, int64_t n, double *partials, double *out, cudaStream_t s);
 void launch_axpy(double *y, double alpha, const double *x, int64_t n, cudaStream_t s);   // y = fma(alpha, x, y)

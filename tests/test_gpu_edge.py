@@ -1,0 +1,168 @@
+"""GPU edge cases of the C-ABI: error paths, degenerate decompositions, determinism.
+
+* ESINGULAR names the level and the patch (mhdp_last_error `where`), and a singular
+  coarse operator is reported as patch -1 (include/mhdp.h, mhdp_setup).
+* ESTATE for device calls before mhdp_setup; EINVAL for patches above 160 DoFs.
+* One patch covering every DoF: a sweep from 0 is the dense LU solve (P:536 with
+  V_1 = V; the oracle pins this against numpy, test_oracle_solver.py) -- on the GPU it
+  exercises the largest patch kernels (T = 3..5 rows per lane) and is compared bit for
+  bit with the oracle using the same decomposition.
+* Patches of size 1 (a diagonal, Jacobi-like decomposition) and a mixed ragged set.
+* Determinism: repeated sweeps / V-cycles are bit-identical.
+"""
+import numpy as np
+import pytest
+
+from gpu_helpers import bits, cuda_vec, host, load_oracle_levels
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx():
+    import torch
+    from paper_2104_14855_b200 import mhdp
+    return mhdp.Context(0, torch.cuda.current_stream().cuda_stream)
+
+
+def test_state_errors():
+    import torch
+    from paper_2104_14855_b200 import mhdp
+    ctx = _ctx()
+    x = torch.zeros(4, dtype=torch.float64, device="cuda:0")
+    assert ctx._L.mhdp_smooth(ctx.h, 1, 1, 0, x.data_ptr(), x.data_ptr()) == 5      # ESTATE: no setup
+    assert ctx._L.mhdp_vcycle(ctx.h, 0, x.data_ptr(), x.data_ptr()) == 5
+
+
+def test_singular_patch_reported(oracle_mod):
+    from paper_2104_14855_b200 import mhdp, workloads
+    cfg = workloads.small("c1", 4, 2)
+    w, _, _ = workloads.draw(cfg, 1, 0)
+    orc = oracle_mod.Oracle(cfg, w)
+    ctx = _ctx()
+    ctx.begin_levels(2, cfg)
+    A0 = orc.csr(0)
+    ctx.load_level(0, A0.rp, A0.ci, A0.v)
+    A = orc.csr(1)
+    v = A.v.copy()
+    ptr, dofs, _, _ = orc.patches(1)
+    bad = 3
+    for d in dofs[ptr[bad]:ptr[bad + 1]]:          # zero the rows of one patch's DoFs
+        v[A.rp[d]:A.rp[d + 1]] = 0.0
+    P = orc.prolongation(1)
+    ctx.load_level(1, A.rp, A.ci, v, ptr, dofs, P.rp, P.ci, P.v)
+    with pytest.raises(mhdp.MhdpError) as e:
+        ctx.setup()
+    assert e.value.status == 4
+    level, patch = e.value.where >> 32, e.value.where & 0xffffffff
+    assert level == 1
+    first = min(i for i in range(len(ptr) - 1) if np.isin(dofs[ptr[i]:ptr[i + 1]], dofs[ptr[bad]:ptr[bad + 1]]).any())
+    assert patch == first      # the first singular patch in patch order
+
+
+def test_singular_coarse_reported(oracle_mod):
+    from paper_2104_14855_b200 import mhdp, workloads
+    cfg = workloads.small("c1", 4, 1)
+    ctx = _ctx()
+    ctx.begin_levels(1, cfg)
+    n = 5
+    rp = np.arange(n + 1, dtype=np.int64)
+    ci = np.arange(n, dtype=np.int32)
+    ctx.load_level(0, rp, ci, np.array([1.0, 2.0, 0.0, 1.0, 1.0]))
+    with pytest.raises(mhdp.MhdpError) as e:
+        ctx.setup()
+    assert e.value.status == 4 and e.value.where == -1
+
+
+def test_patch_too_large_rejected():
+    from paper_2104_14855_b200 import mhdp, workloads
+    cfg = workloads.small("c1", 4, 2)
+    ctx = _ctx()
+    ctx.begin_levels(2, cfg)
+    n0, n = 3, 200
+    ctx.load_level(0, np.arange(n0 + 1), np.arange(n0, dtype=np.int32), np.ones(n0))
+    rp = np.arange(n + 1)
+    P_rp = np.arange(n + 1)
+    P_ci = (np.arange(n) % n0).astype(np.int32)
+    ctx.load_level(1, rp, np.arange(n, dtype=np.int32), np.ones(n), np.array([0, n]), np.arange(n, dtype=np.int32),
+                   P_rp, P_ci, np.ones(n))
+    with pytest.raises(mhdp.MhdpError) as e:
+        ctx.setup()
+    assert e.value.status == 1
+
+
+def _single_patch_case(oracle_mod, name, N, decomposition):
+    from paper_2104_14855_b200 import workloads
+    cfg = workloads.small(name, N, 2)
+    w, _, _ = workloads.draw(cfg, 1, 3)
+    orc = oracle_mod.Oracle(cfg, w)
+    n = orc.n()
+    if decomposition == "single" and n > 160:
+        pytest.skip("above the 160-DoF patch limit")
+    if decomposition == "single":
+        ptr, dofs = np.array([0, n], np.int64), np.arange(n, dtype=np.int32)
+    elif decomposition == "diagonal":
+        ptr, dofs = np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int32)
+    else:   # ragged: blocks of sizes 1, 2, 3, ... cycling, overlapping by one DoF
+        ptr, dofs, start, k = [0], [], 0, 1
+        while start < n:
+            blk = list(range(max(0, start - 1), min(n, start + k)))
+            dofs += blk
+            ptr.append(len(dofs))
+            start += k
+            k = k % 7 + 1
+        ptr, dofs = np.array(ptr, np.int64), np.array(dofs, np.int32)
+    orc.set_patches(ptr, dofs)
+    ctx = _ctx()
+    ctx.begin_levels(2, cfg)
+    A0 = orc.csr(0)
+    ctx.load_level(0, A0.rp, A0.ci, A0.v)
+    A = orc.csr(1)
+    P = orc.prolongation(1)
+    ctx.load_level(1, A.rp, A.ci, A.v, ptr, dofs, P.rp, P.ci, P.v)
+    ctx.setup()
+    return cfg, orc, ctx, n
+
+
+@pytest.mark.parametrize("name,N", [("c1", 4), ("c1", 6), ("c3", 4), ("c4", 2)])
+def test_single_patch_is_direct_solve(oracle_mod, name, N):
+    cfg, orc, ctx, n = _single_patch_case(oracle_mod, name, N, "single")
+    rng = np.random.default_rng(1)
+    b = rng.uniform(-1, 1, n)
+    xo = orc.sweep(b, np.zeros(n), x_is_zero=True)
+    xg = cuda_vec(np.zeros(n))
+    ctx.smooth(cuda_vec(b), xg, nsweeps=1, x_is_zero=True)
+    assert np.array_equal(bits(host(xg)), bits(xo))
+    A = orc.csr().to_scipy().toarray()
+    assert np.linalg.norm(A @ host(xg) - b) <= 1e-9 * np.linalg.norm(b) * np.linalg.cond(A)
+
+
+@pytest.mark.parametrize("decomposition", ["diagonal", "ragged"])
+def test_degenerate_decompositions(oracle_mod, decomposition):
+    cfg, orc, ctx, n = _single_patch_case(oracle_mod, "c3", 8, decomposition)
+    rng = np.random.default_rng(2)
+    b, x0 = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    xo = orc.sweep(b, x0, nsweeps=2)
+    xg = cuda_vec(x0)
+    ctx.smooth(cuda_vec(b), xg, nsweeps=2)
+    assert np.array_equal(bits(host(xg)), bits(xo))
+
+
+def test_determinism_repeated_runs(oracle_mod):
+    import torch
+    from paper_2104_14855_b200 import workloads
+    cfg = workloads.small("c5", 8, 2)
+    w, _, _ = workloads.draw(cfg, 1, 4)
+    ctx = _ctx()
+    ctx.assemble(cfg, w)
+    ctx.setup()
+    n = ctx.n()
+    _, b, x0 = workloads.draw(cfg, n, 4)
+    outs = []
+    for _ in range(3):
+        xg = torch.empty(n, dtype=torch.float64, device="cuda:0")
+        ctx.vcycle(cuda_vec(b), xg)
+        xs = cuda_vec(x0)
+        ctx.smooth(cuda_vec(b), xs, nsweeps=2)
+        outs.append((bits(host(xg)), bits(host(xs))))
+    for o in outs[1:]:
+        assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
