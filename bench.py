@@ -240,6 +240,18 @@ def run_ours(args):
     e1.record(stream)
     torch.cuda.synchronize(dev)
     ms_k1 = e0.elapsed_time(e1) / reps
+    # coarse solve (K8) alone
+    n0 = infos[0]["n"]
+    bc = torch.from_numpy(np.random.default_rng(seed).uniform(-1, 1, n0)).to(dev)
+    xc = torch.empty_like(bc)
+    ctx.coarse_solve(bc, xc)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(reps):
+        ctx.coarse_solve(bc, xc)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms_k8 = e0.elapsed_time(e1) / reps
 
     # algorithmic bytes: K2 per patch i: 8 n_i^2 factor + 8 n_i gathered r
     # + 8 n_i written y; sweep: 8 sum n_i^2 + 8 nnz + 24 n
@@ -283,7 +295,8 @@ def run_ours(args):
                       "gbs": sweep_bytes / (ms_sweep * 1e-3) / 1e9,
                       "frac": sweep_bytes / (ms_sweep * 1e-3) / 1e9 / peak, "bytes": sweep_bytes},
             "kernels": {"K2_patch_apply_ms": ms_k2, "K1_residual_ms": ms_k1,
-                        "K1_gbs": k1_bytes / (ms_k1 * 1e-3) / 1e9},
+                        "K1_gbs": k1_bytes / (ms_k1 * 1e-3) / 1e9, "K8_coarse_solve_ms": ms_k8,
+                        "coarse_n": n0},
             "roofline": {"bound": "hbm", "kernel": "K2 patch gather + LU apply (finest level)",
                          "achieved": k2_gbs, "peak": peak, "unit": "GB/s", "frac": k2_gbs / peak,
                          "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback"},
