@@ -59,6 +59,11 @@ typedef struct {
     double mu_stab;           /* Burman stabilisation mu; must be 0 (R-mu)       */
     double theta;             /* outer damping of the additive update (R-weights), 1.0       */
     int nu_pre, nu_post;      /* smoothing sweeps per level in the V-cycle (R-nu)             */
+    int smoother;             /* 0: nu_pre / nu_post Richardson Schwarz sweeps (north star);
+                                 1: GMRES(smoother_its) left-preconditioned by the Schwarz
+                                 operator, once before and once after the coarse correction
+                                 -- the paper's relaxation, P:643 (R-gmres6)                  */
+    int smoother_its;         /* GMRES iterations of the smoother (6), 1..32           */
 } mhdp_params;
 
 typedef struct mhdp_ctx mhdp_ctx;
@@ -153,6 +158,16 @@ mhdp_status mhdp_smooth_host(mhdp_ctx *ctx, int level, int nsweeps, int x_is_zer
  * Synchronises every iteration.  Returns ENOCONV at maxit.                              */
 mhdp_status mhdp_gmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol,
                        double atol, int maxit, int *its_out, double *relres_out);
+
+/* Flexible GMRES with the current V-cycle as a variable right preconditioner on
+ * the finest level (required when the smoother is GMRES, which makes the V-cycle
+ * nonlinear); x0 = 0; inner products in the pinned order of reading R-dot; stops when
+ * the residual estimate <= max(rtol |b|, atol).  Synchronises every iteration. */
+mhdp_status mhdp_fgmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol,
+                        double atol, int maxit, int *its_out, double *relres_out);
+/* The pinned inner product of reading R-dot of two device vectors (synchronises).      */
+mhdp_status mhdp_dot(mhdp_ctx *ctx, const double *a_dev, const double *b_dev, long long n,
+                     double *out_host);
 
 /* ---- export for parity checks (host buffers, caller-allocated, sizes from info) ----- */
 mhdp_status mhdp_export_csr(const mhdp_ctx *ctx, int level, long long *rowptr, int *col,

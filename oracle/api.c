@@ -34,6 +34,7 @@ typedef struct {
     int block, dim, nlev;
     OParams p;
     double theta;
+    int smoother, smoother_its;   /* 0: nu_pre / nu_post Richardson sweeps; 1: GMRES(m) (NEXT-1) */
     OLevel *lv;
     double *clu;      /* coarse LU (row-major n0*n0) */
     int *cperm;
@@ -353,20 +354,28 @@ int orc_coarse_lu(OCtx *c, double *lu, int *perm) {
     return st;
 }
 
+static int gmres_smooth(OCtx *c, int l, int m, int x_is_zero, const double *b, double *x);
+
 static int vcycle(OCtx *c, int l, const double *b, double *x) {
     if (l == 0) return orc_coarse_solve(c, b, x);
     OLevel *L = &c->lv[l];
     i64 n = L->s.n, nc = c->lv[l - 1].s.n;
     for (i64 d = 0; d < n; d++) x[d] = 0.0;
-    int zero = 1;
-    for (int s = 0; s < c->p.nu_pre; s++) { if (sweep(c, l, zero, b, x)) return 1; zero = 0; }
+    if (c->smoother == 1) {
+        if (gmres_smooth(c, l, c->smoother_its, 1, b, x)) return 1;
+    } else {
+        int zero = 1;
+        for (int s = 0; s < c->p.nu_pre; s++) { if (sweep(c, l, zero, b, x)) return 1; zero = 0; }
+    }
     double *r = malloc(sizeof(double) * n), *rc = malloc(sizeof(double) * nc), *ec = malloc(sizeof(double) * nc);
     residual(&L->A, b, x, r);
     orc_restrict(c, l, r, rc);
     int st = vcycle(c, l - 1, rc, ec);
     if (!st) {
         orc_prolong_add(c, l, ec, x);
-        for (int s = 0; s < c->p.nu_post; s++) if (sweep(c, l, 0, b, x)) { st = 1; break; }
+        if (c->smoother == 1) st = gmres_smooth(c, l, c->smoother_its, 0, b, x) ? 1 : 0;
+        else
+            for (int s = 0; s < c->p.nu_post; s++) if (sweep(c, l, 0, b, x)) { st = 1; break; }
     }
     free(r); free(rc); free(ec);
     return st;
@@ -502,4 +511,167 @@ int orc_dense_lu_solve(int n, const double *a, const double *b, double *x, doubl
     int st = od_lu(lu_out, n, perm_out, amax);
     if (!st) od_lu_solve(lu_out, n, perm_out, b, x);
     return st;
+}
+
+/* ===================================================================================
+ * NEXT-1: the paper's relaxation -- "six preconditioned GMRES iterations
+ * as the smoother on each level" -- and flexible GMRES as the outermost Krylov
+ * solver, with the paper's 1e-7 / 1e-7 Euclidean tolerances.
+ * Readings: R-dot (pinned reduction order of inner products), R-gmres6
+ * (left preconditioning by the Schwarz operator B r = S(0; r), modified Gram-Schmidt,
+ * Givens rotations, x0 = current iterate, exactly m iterations unless breakdown),
+ * R-fgmres (right flexible preconditioning by the GMRES-smoothed V-cycle, x0 = 0).
+ * =================================================================================== */
+
+/* R-dot: blocks of 256 consecutive entries, each an fma chain from +0.0 in ascending
+ * order; block sums combined by a pairwise tree (level by level, s_k = s_2k + s_2k+1,
+ * an odd last entry carried up).                                                    */
+double od_dot(const double *a, const double *b, i64 n) {
+    if (n <= 0) return 0.0;
+    i64 m = (n + 255) / 256;
+    double *s = malloc(sizeof(double) * m);
+    for (i64 B = 0; B < m; B++) {
+        double acc = 0.0;
+        for (i64 i = 256 * B; i < n && i < 256 * (B + 1); i++) acc = fma(a[i], b[i], acc);
+        s[B] = acc;
+    }
+    while (m > 1) {
+        i64 h = m / 2;
+        for (i64 k = 0; k < h; k++) s[k] = s[2 * k] + s[2 * k + 1];
+        if (m & 1) s[h] = s[m - 1];
+        m = h + (m & 1);
+    }
+    double r = s[0];
+    free(s);
+    return r;
+}
+
+/* the Schwarz operator as a preconditioner: z = B r = one sweep from zero with rhs r */
+static int apply_B(OCtx *c, int l, const double *r, double *z) {
+    return sweep(c, l, 1, r, z) ? 1 : 0;
+}
+
+/* Givens / least-squares state shared by GMRES(m) and FGMRES; H is (m+1) x m row-major.
+ * Every product and sum is rounded separately (no fma): the GPU mirrors these steps. */
+static void givens_column(double *H, int m, double *cs, double *sn, double *g, int k) {
+    for (int i = 0; i < k; i++) {
+        double a = H[i * m + k], bb = H[(i + 1) * m + k];
+        H[i * m + k] = cs[i] * a + sn[i] * bb;
+        H[(i + 1) * m + k] = -sn[i] * a + cs[i] * bb;
+    }
+    double a = H[k * m + k], bb = H[(k + 1) * m + k];
+    double rr = sqrt(a * a + bb * bb);
+    cs[k] = a / rr;
+    sn[k] = bb / rr;
+    H[k * m + k] = rr;
+    H[(k + 1) * m + k] = 0.0;
+    g[k + 1] = -sn[k] * g[k];
+    g[k] = cs[k] * g[k];
+}
+
+static void back_substitute(const double *H, int m, const double *g, int kk, double *y) {
+    for (int i = kk - 1; i >= 0; i--) {
+        double s = g[i];
+        for (int j = i + 1; j < kk; j++) s = s - H[i * m + j] * y[j];
+        y[i] = s / H[i * m + i];
+    }
+}
+
+/* GMRES(m) smoothing step (R-gmres6): x <- x + V y minimising ||B(b - A x)|| over the
+ * Krylov space of B A; x_is_zero: x = 0 on entry (the residual is b).               */
+static int gmres_smooth(OCtx *c, int l, int m, int x_is_zero, const double *b, double *x) {
+    OLevel *L = &c->lv[l];
+    i64 n = L->s.n;
+    double *r = malloc(sizeof(double) * n), *t = malloc(sizeof(double) * n), *w = malloc(sizeof(double) * n);
+    double *V = malloc(sizeof(double) * n * (m + 1));
+    double *H = calloc((size_t)(m + 1) * m, sizeof(double)), *cs = calloc(m, sizeof(double)),
+           *sn = calloc(m, sizeof(double)), *g = calloc(m + 1, sizeof(double)), *y = calloc(m, sizeof(double));
+    int st = 0, kk = 0;
+    if (x_is_zero) { for (i64 i = 0; i < n; i++) { r[i] = b[i]; x[i] = 0.0; } }
+    else residual(&L->A, b, x, r);
+    if (apply_B(c, l, r, w)) { st = 1; goto done; }
+    double beta = sqrt(od_dot(w, w, n));
+    if (beta == 0.0) goto done;
+    for (i64 i = 0; i < n; i++) V[i] = w[i] / beta;
+    g[0] = beta;
+    for (int k = 0; k < m; k++) {
+        orc_spmv(c, l, V + k * n, t);
+        if (apply_B(c, l, t, w)) { st = 1; goto done; }
+        for (int i = 0; i <= k; i++) {
+            double h = od_dot(w, V + i * n, n);
+            H[i * m + k] = h;
+            for (i64 j = 0; j < n; j++) w[j] = fma(-h, V[i * n + j], w[j]);
+        }
+        double hn = sqrt(od_dot(w, w, n));
+        H[(k + 1) * m + k] = hn;
+        givens_column(H, m, cs, sn, g, k);
+        kk = k + 1;
+        if (hn == 0.0) break;
+        if (k + 1 < m) for (i64 j = 0; j < n; j++) V[(k + 1) * n + j] = w[j] / hn;
+    }
+    back_substitute(H, m, g, kk, y);
+    for (int i = 0; i < kk; i++)
+        for (i64 j = 0; j < n; j++) x[j] = fma(y[i], V[i * n + j], x[j]);
+done:
+    free(r); free(t); free(w); free(V); free(H); free(cs); free(sn); free(g); free(y);
+    return st;
+}
+
+void orc_set_smoother(OCtx *c, int kind, int its) {
+    c->smoother = kind;
+    c->smoother_its = its;
+}
+
+/* flexible GMRES (R-fgmres) with the current V-cycle as a variable right preconditioner;
+ * hist[k] = |g_k|, k = 0..its.  Returns 0 converged, 1 maxit, 2 preconditioner failure. */
+int orc_fgmres(OCtx *c, const double *b, double *x, double rtol, double atol, int maxit, int *its_out,
+               double *hist) {
+    int l = c->nlev - 1;
+    i64 n = c->lv[l].s.n;
+    double beta = sqrt(od_dot(b, b, n));
+    double tol = rtol * beta > atol ? rtol * beta : atol;
+    for (i64 i = 0; i < n; i++) x[i] = 0.0;
+    hist[0] = beta;
+    *its_out = 0;
+    if (beta <= tol) return 0;
+    int m = maxit;
+    double *V = malloc(sizeof(double) * n * (m + 1)), *Z = malloc(sizeof(double) * n * m);
+    double *H = calloc((size_t)(m + 1) * m, sizeof(double)), *cs = calloc(m, sizeof(double)),
+           *sn = calloc(m, sizeof(double)), *g = calloc(m + 1, sizeof(double)), *y = calloc(m, sizeof(double));
+    double *w = malloc(sizeof(double) * n);
+    for (i64 i = 0; i < n; i++) V[i] = b[i] / beta;
+    g[0] = beta;
+    int k, conv = 0, fail = 0;
+    for (k = 0; k < m; k++) {
+        if (vcycle(c, l, V + k * n, Z + k * n)) { fail = 1; break; }
+        orc_spmv(c, l, Z + k * n, w);
+        for (int i = 0; i <= k; i++) {
+            double h = od_dot(w, V + i * n, n);
+            H[i * m + k] = h;
+            for (i64 j = 0; j < n; j++) w[j] = fma(-h, V[i * n + j], w[j]);
+        }
+        double hn = sqrt(od_dot(w, w, n));
+        H[(k + 1) * m + k] = hn;
+        givens_column(H, m, cs, sn, g, k);
+        hist[k + 1] = fabs(g[k + 1]);
+        if (fabs(g[k + 1]) <= tol) { k++; conv = 1; break; }
+        if (hn == 0.0) { k++; break; }
+        for (i64 j = 0; j < n; j++) V[(k + 1) * n + j] = w[j] / hn;
+    }
+    if (!fail) {
+        back_substitute(H, m, g, k, y);
+        for (int i = 0; i < k; i++)
+            for (i64 j = 0; j < n; j++) x[j] = fma(y[i], Z[i * n + j], x[j]);
+        *its_out = k;
+    }
+    free(V); free(Z); free(H); free(cs); free(sn); free(g); free(y); free(w);
+    return fail ? 2 : (conv ? 0 : 1);
+}
+
+/* test access to the pinned inner product */
+double orc_dot(const double *a, const double *b, i64 n) { return od_dot(a, b, n); }
+
+/* one GMRES(m) smoothing step on level l (test access; x in/out) */
+int orc_gmres_smooth(OCtx *c, int l, int m, int x_is_zero, const double *b, double *x) {
+    return gmres_smooth(c, l, m, x_is_zero, b, x);
 }

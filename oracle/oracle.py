@@ -78,6 +78,12 @@ def lib(exact: bool = False):
         L.orc_duality_error.argtypes = [vp, C.c_int]
         L.orc_set_patches.argtypes = [vp, C.c_int, C.c_longlong, i64p, ip]
         L.orc_dense_lu_solve.argtypes = [C.c_int, dp, dp, dp, dp, ip]
+        L.orc_set_smoother.argtypes = [vp, C.c_int, C.c_int]
+        L.orc_set_smoother.restype = None
+        L.orc_fgmres.argtypes = [vp, dp, dp, C.c_double, C.c_double, C.c_int, ip, dp]
+        L.orc_gmres_smooth.argtypes = [vp, C.c_int, C.c_int, C.c_int, dp, dp]
+        L.orc_dot.argtypes = [dp, dp, C.c_longlong]
+        L.orc_dot.restype = C.c_double
         _libs[exact] = L
     return _libs[exact]
 
@@ -92,6 +98,12 @@ def _i(a):
 
 def _l(a):
     return a.ctypes.data_as(C.POINTER(C.c_longlong))
+
+
+def dot(a, b):
+    """The pinned inner product of reading R-dot."""
+    a = np.ascontiguousarray(a, np.float64); b = np.ascontiguousarray(b, np.float64)
+    return lib().orc_dot(_d(a), _d(b), len(a))
 
 
 def dense_lu_solve(a, b):
@@ -278,6 +290,30 @@ class Oracle:
         if self._L.orc_vcycle_level(self.h, level, _d(b), _d(x)):
             raise ArithmeticError("oracle: V-cycle failed (singular patch or coarse operator)")
         return x
+
+    def set_smoother(self, kind: str = "richardson", its: int = 6):
+        """'richardson': nu sweeps (north star); 'gmres': GMRES(its) smoothing (NEXT-1)."""
+        self._L.orc_set_smoother(self.h, 1 if kind == "gmres" else 0, its)
+
+    def gmres_smooth(self, b, x, m=6, level=-1, x_is_zero=False):
+        """One GMRES(m) smoothing step (R-gmres6) on a level; returns the new x."""
+        level = level % self.nlev
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.array(x, dtype=np.float64, copy=True)
+        if self._L.orc_gmres_smooth(self.h, level, m, int(x_is_zero), _d(b), _d(x)):
+            raise ArithmeticError("oracle: singular patch")
+        return x
+
+    def fgmres(self, b, rtol=1e-7, atol=1e-7, maxit=100):
+        """Flexible GMRES with the V-cycle as variable preconditioner (R-fgmres)."""
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.zeros(self.n())
+        its = np.zeros(1, np.int32)
+        hist = np.zeros(maxit + 1)
+        st = self._L.orc_fgmres(self.h, _d(b), _d(x), rtol, atol, maxit, _i(its), _d(hist))
+        if st == 2:
+            raise ArithmeticError("oracle: FGMRES preconditioner failed")
+        return x, int(its[0]), hist[: int(its[0]) + 1], st == 0
 
     def gmres(self, b, rtol=1e-7, atol=1e-7, maxit=200):
         b = np.ascontiguousarray(b, np.float64)

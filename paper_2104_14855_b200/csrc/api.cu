@@ -32,6 +32,9 @@ struct DevLevel {
     DevCsr Pr, PrT;            // prolongation from level-1 (fine rows) and its transpose
     double *b = nullptr, *x = nullptr, *r = nullptr;
     int64_t bytes_op = 0, bytes_fac = 0, bytes_tr = 0;
+    // GMRES(m) smoother workspace (NEXT-1)
+    double *gV = nullptr, *gt = nullptr, *gw = nullptr, *part = nullptr;
+    double *scal = nullptr;    // H (m+1)m | cs m | sn m | g m+1 | y m | hn m
 };
 
 }  // namespace
@@ -63,6 +66,9 @@ struct mhdp_ctx {
     // gmres workspace
     double *gV = nullptr, *gZ = nullptr, *gw = nullptr;
     int g_cap = 0;
+    // fgmres workspace
+    double *fV = nullptr, *fZ = nullptr, *fw = nullptr, *fpart = nullptr, *fscal = nullptr;
+    int f_cap = 0;
 };
 
 namespace {
@@ -116,6 +122,7 @@ void free_device(mhdp_ctx *c) {
     c->clut = nullptr; c->cperm = nullptr; c->cz = nullptr; c->crdiag = nullptr;
     c->d_status = nullptr; c->d_scal = nullptr;
     c->gV = c->gZ = c->gw = nullptr; c->g_cap = 0;
+    c->fV = c->fZ = c->fw = c->fpart = c->fscal = nullptr; c->f_cap = 0;
     c->setup_done = false;
 }
 
@@ -304,6 +311,47 @@ void coarse_solve(mhdp_ctx *ctx, const double *b, double *x) {
     launch_dense_solve(ctx->clut, ctx->crdiag, ctx->cperm, ctx->n0, b, x, ctx->cz, ctx->stream);
 }
 
+// scalar workspace layout of a GMRES(m) smoother / FGMRES(m)
+struct KrylovScal {
+    double *H, *cs, *sn, *g, *y, *hn;
+    KrylovScal(double *s, int m) {
+        H = s; cs = H + (m + 1) * m; sn = cs + m; g = sn + m; y = g + m + 1; hn = y + m;
+    }
+    static int64_t size(int m) { return (int64_t)(m + 1) * m + 5 * (int64_t)m + 1; }
+};
+
+// NEXT-1 smoothing step (R-gmres6): left-preconditioned GMRES(m) from the current x
+// (x_is_zero: x = 0 on entry), preconditioner B r = one Schwarz sweep from zero.
+void gmres_smooth(mhdp_ctx *ctx, int l, int m, bool x_is_zero, const double *b, double *x) {
+    DevLevel &L = ctx->D[l];
+    cudaStream_t s = ctx->stream;
+    const int64_t n = L.n;
+    KrylovScal S(L.scal, m);
+    auto applyB = [&](const double *rhs, double *out) {
+        launch_patch_apply(L.P, rhs, s);
+        launch_patch_update(L.P, n, out, 1, s);
+    };
+    const double *r = b;
+    if (x_is_zero) launch_fill(x, 0.0, n, s);
+    else { residual(ctx, l, b, x, L.r); r = L.r; }
+    applyB(r, L.gw);
+    launch_dot_pinned(L.gw, L.gw, n, L.part, S.g, 1, s);                  // beta -> g[0]
+    launch_div_dev(L.gV, L.gw, S.g, n, s);                                // V_0 = w / beta
+    for (int k = 0; k < m; ++k) {
+        residual(ctx, l, nullptr, L.gV + (int64_t)k * n, L.gt);           // t = A V_k
+        applyB(L.gt, L.gw);                                               // w = B t
+        for (int i = 0; i <= k; ++i) {
+            launch_dot_pinned(L.gw, L.gV + (int64_t)i * n, n, L.part, S.H + i * m + k, 0, s);
+            launch_axpy_negdev(L.gw, S.H + i * m + k, L.gV + (int64_t)i * n, n, s);
+        }
+        launch_dot_pinned(L.gw, L.gw, n, L.part, S.hn + k, 1, s);
+        launch_givens(S.H, m, S.cs, S.sn, S.g, S.hn + k, k, s);
+        if (k + 1 < m) launch_div_dev(L.gV + (int64_t)(k + 1) * n, L.gw, S.hn + k, n, s);
+    }
+    launch_backsub(S.H, m, S.g, m, S.y, s);
+    launch_basis_update(x, L.gV, n, S.y, m, n, s);
+}
+
 void vcycle(mhdp_ctx *ctx, int l, const double *b, double *x) {
     if (l == 0) {
         coarse_solve(ctx, b, x);
@@ -311,13 +359,19 @@ void vcycle(mhdp_ctx *ctx, int l, const double *b, double *x) {
     }
     DevLevel &L = ctx->D[l];
     DevLevel &C = ctx->D[l - 1];
-    if (ctx->p.nu_pre == 0) launch_fill(x, 0.0, L.n, ctx->stream);
-    for (int s = 0; s < ctx->p.nu_pre; ++s) sweep(ctx, l, b, x, s == 0);
+    const bool krylov = ctx->p.smoother == 1;
+    if (krylov) gmres_smooth(ctx, l, ctx->p.smoother_its, true, b, x);
+    else {
+        if (ctx->p.nu_pre == 0) launch_fill(x, 0.0, L.n, ctx->stream);
+        for (int s = 0; s < ctx->p.nu_pre; ++s) sweep(ctx, l, b, x, s == 0);
+    }
     residual(ctx, l, b, x, L.r);
     launch_restrict(L.PrT, L.r, C.b, ctx->stream);
     vcycle(ctx, l - 1, C.b, C.x);
     launch_prolong_add(L.Pr, C.x, x, ctx->stream);
-    for (int s = 0; s < ctx->p.nu_post; ++s) sweep(ctx, l, b, x, false);
+    if (krylov) gmres_smooth(ctx, l, ctx->p.smoother_its, false, b, x);
+    else
+        for (int s = 0; s < ctx->p.nu_post; ++s) sweep(ctx, l, b, x, false);
 }
 
 mhdp_status need_setup(mhdp_ctx *ctx) {
@@ -397,6 +451,10 @@ static mhdp_status check_params(mhdp_ctx *ctx, const mhdp_params *pr) {
     ctx->p.Re = pr->Re; ctx->p.Rem = pr->Rem; ctx->p.S = pr->S; ctx->p.gamma = pr->gamma;
     ctx->p.sigma = pr->sigma; ctx->p.mu = pr->mu_stab; ctx->p.theta = pr->theta;
     ctx->p.nu_pre = pr->nu_pre; ctx->p.nu_post = pr->nu_post;
+    if (pr->smoother != 0 && pr->smoother != 1) return fail(ctx, MHDP_EINVAL, "smoother must be 0 or 1");
+    if (pr->smoother == 1 && (pr->smoother_its < 1 || pr->smoother_its > 32))
+        return fail(ctx, MHDP_EINVAL, "smoother_its must be in 1..32");
+    ctx->p.smoother = pr->smoother; ctx->p.smoother_its = pr->smoother_its;
     return MHDP_OK;
 }
 
@@ -491,6 +549,14 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         if ((st = dalloc(ctx, &L.r, H.n))) return st;
         if (l == 0) continue;
         if ((st = build_patches(ctx, H, L))) return st;
+        if (ctx->p.smoother == 1) {
+            const int m = ctx->p.smoother_its;
+            if ((st = dalloc(ctx, &L.gV, (int64_t)(m + 1) * H.n))) return st;
+            if ((st = dalloc(ctx, &L.gt, H.n))) return st;
+            if ((st = dalloc(ctx, &L.gw, H.n))) return st;
+            if ((st = dalloc(ctx, &L.part, 2 * ((H.n + 255) / 256) + 2))) return st;
+            if ((st = dalloc(ctx, &L.scal, KrylovScal::size(m)))) return st;
+        }
         if ((st = build_csr(ctx, H.n, H.prp, H.pci, H.pv, L.Pr))) return st;
         std::vector<int64_t> trp; std::vector<int> tci; std::vector<double> tv;
         transpose_csr(H.n, H.n_coarser, H.prp, H.pci, H.pv, trp, tci, tv);
@@ -753,6 +819,82 @@ mhdp_status mhdp_gmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double
     if (relres_out) *relres_out = std::fabs(g[k]) / beta;
     if ((st = check_launch(ctx))) return st;
     return conv ? MHDP_OK : fail(ctx, MHDP_ENOCONV, "GMRES reached maxit");
+}
+
+mhdp_status mhdp_fgmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol, double atol, int maxit,
+                        int *its_out, double *relres_out) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!b_dev || !x_dev || maxit < 1 || maxit > 1000) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    const int l = ctx->nlev - 1;
+    const int64_t n = ctx->D[l].n;
+    cudaStream_t s = ctx->stream;
+    if (ctx->f_cap < maxit) {
+        if ((st = dalloc(ctx, &ctx->fV, n * (int64_t)(maxit + 1)))) return st;
+        if ((st = dalloc(ctx, &ctx->fZ, n * (int64_t)maxit))) return st;
+        if ((st = dalloc(ctx, &ctx->fw, n))) return st;
+        if ((st = dalloc(ctx, &ctx->fpart, 2 * ((n + 255) / 256) + 2))) return st;
+        if ((st = dalloc(ctx, &ctx->fscal, KrylovScal::size(maxit)))) return st;
+        ctx->f_cap = maxit;
+    }
+    const int m = maxit;
+    KrylovScal S(ctx->fscal, m);
+    CK(cudaMemsetAsync(ctx->fscal, 0, sizeof(double) * KrylovScal::size(m), s));
+    double *V = ctx->fV, *Z = ctx->fZ, *w = ctx->fw;
+    auto read = [&](const double *p) {
+        double v = 0;
+        cudaMemcpyAsync(&v, p, sizeof(double), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        return v;
+    };
+    launch_dot_pinned(b_dev, b_dev, n, ctx->fpart, S.g, 1, s);
+    launch_fill(x_dev, 0.0, n, s);
+    const double beta = read(S.g);
+    const double tol = std::max(rtol * beta, atol);
+    if (its_out) *its_out = 0;
+    if (relres_out) *relres_out = beta > 0 ? 1.0 : 0.0;
+    if (beta <= tol) return check_launch(ctx);
+    launch_div_dev(V, b_dev, S.g, n, s);
+    int k = 0;
+    bool conv = false;
+    double gk = beta;
+    for (k = 0; k < m; ++k) {
+        vcycle(ctx, l, V + (int64_t)k * n, Z + (int64_t)k * n);
+        residual(ctx, l, nullptr, Z + (int64_t)k * n, w);
+        for (int i = 0; i <= k; ++i) {
+            launch_dot_pinned(w, V + (int64_t)i * n, n, ctx->fpart, S.H + i * m + k, 0, s);
+            launch_axpy_negdev(w, S.H + i * m + k, V + (int64_t)i * n, n, s);
+        }
+        launch_dot_pinned(w, w, n, ctx->fpart, S.hn + k, 1, s);
+        launch_givens(S.H, m, S.cs, S.sn, S.g, S.hn + k, k, s);
+        gk = std::fabs(read(S.g + k + 1));
+        if (gk <= tol) { ++k; conv = true; break; }
+        if (read(S.hn + k) == 0.0) { ++k; break; }
+        launch_div_dev(V + (int64_t)(k + 1) * n, w, S.hn + k, n, s);
+    }
+    launch_backsub(S.H, m, S.g, k, S.y, s);
+    launch_basis_update(x_dev, Z, n, S.y, k, n, s);
+    CK(cudaStreamSynchronize(s));
+    if (its_out) *its_out = k;
+    if (relres_out) *relres_out = gk / beta;
+    if ((st = check_launch(ctx))) return st;
+    return conv ? MHDP_OK : fail(ctx, MHDP_ENOCONV, "FGMRES reached maxit");
+}
+
+mhdp_status mhdp_dot(mhdp_ctx *ctx, const double *a_dev, const double *b_dev, long long n, double *out_host) {
+    if (!ctx) return MHDP_EINVAL;
+    if (ctx->host_only) return fail(ctx, MHDP_ECUDA, "host-only context");
+    if (!a_dev || !b_dev || !out_host || n < 0) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    cudaSetDevice(ctx->device);
+    double *part = nullptr, *out = nullptr;
+    CK(cudaMalloc(&part, sizeof(double) * (2 * ((n + 255) / 256) + 2)));
+    CK(cudaMalloc(&out, sizeof(double)));
+    launch_dot_pinned(a_dev, b_dev, n, part, out, 0, ctx->stream);
+    CK(cudaMemcpyAsync(out_host, out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(part);
+    cudaFree(out);
+    return check_launch(ctx);
 }
 
 mhdp_status mhdp_export_csr(const mhdp_ctx *ctx, int level, long long *rowptr, int *col, double *val) {

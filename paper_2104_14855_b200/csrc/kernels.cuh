@@ -87,4 +87,15 @@ void launch_axpy(double *y, double alpha, const double *x, int64_t n, cudaStream
 void launch_scale(double *y, const double *x, double alpha, int64_t n, cudaStream_t s);   // y = x * alpha
 void launch_fill(double *y, double v, int64_t n, cudaStream_t s);
 
+// NEXT-1 Krylov pieces (R-dot pinned inner products; explicitly rounded scalar steps)
+// part: 2 * ceil(n/256) doubles of scratch; *out = a.b (or sqrt(a.b))
+void launch_dot_pinned(const double *a, const double *b, int64_t n, double *part, double *out, int do_sqrt,
+                       cudaStream_t s);
+void launch_axpy_negdev(double *w, const double *h, const double *v, int64_t n, cudaStream_t s);  // w -= h[0] v
+void launch_div_dev(double *y, const double *x, const double *d, int64_t n, cudaStream_t s);       // y = x / d[0]
+void launch_givens(double *H, int m, double *cs, double *sn, double *g, const double *hn, int k, cudaStream_t s);
+void launch_backsub(const double *H, int m, const double *g, int kk, double *y, cudaStream_t s);
+void launch_basis_update(double *x, const double *V, int64_t ldv, const double *y, int kk, int64_t n,
+                         cudaStream_t s);
+
 }  // namespace mhdp

@@ -12,6 +12,7 @@ namespace mhdp {
 struct Params {
     double Re = 1, Rem = 1, S = 1, gamma = 1, sigma = 10, mu = 0, theta = 1;
     int nu_pre = 1, nu_post = 1;
+    int smoother = 0, smoother_its = 6;   // 0 Richardson sweeps, 1 GMRES(m) (NEXT-1)
 };
 
 // One level of the hierarchy as host arrays (the form both mhdp_assemble and

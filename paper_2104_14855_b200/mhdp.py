@@ -32,7 +32,7 @@ class Mesh(C.Structure):
 class Params(C.Structure):
     _fields_ = [("Re", C.c_double), ("Rem", C.c_double), ("S", C.c_double), ("gamma", C.c_double),
                 ("sigma", C.c_double), ("mu_stab", C.c_double), ("theta", C.c_double),
-                ("nu_pre", C.c_int), ("nu_post", C.c_int)]
+                ("nu_pre", C.c_int), ("nu_post", C.c_int), ("smoother", C.c_int), ("smoother_its", C.c_int)]
 
 
 class LevelInfo(C.Structure):
@@ -48,7 +48,7 @@ SYMBOLS = ["mhdp_create", "mhdp_destroy", "mhdp_assemble", "mhdp_begin_levels", 
            "mhdp_patch_update", "mhdp_smooth", "mhdp_restrict", "mhdp_prolong_add", "mhdp_coarse_solve",
            "mhdp_vcycle", "mhdp_vcycle_host", "mhdp_smooth_host", "mhdp_gmres", "mhdp_export_csr",
            "mhdp_export_patches", "mhdp_export_prolongation", "mhdp_export_patch_lu", "mhdp_export_slots",
-           "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count"]
+           "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count", "mhdp_fgmres", "mhdp_dot"]
 
 
 def lib():
@@ -78,6 +78,8 @@ def lib():
             "mhdp_vcycle_host": [vp, dp, dp],
             "mhdp_smooth_host": [vp, C.c_int, C.c_int, C.c_int, dp, dp],
             "mhdp_gmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp],
+            "mhdp_fgmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp],
+            "mhdp_dot": [vp, vp, vp, i64, dp],
             "mhdp_export_csr": [vp, C.c_int, i64p, ip, dp],
             "mhdp_export_patches": [vp, C.c_int, i64p, ip],
             "mhdp_export_prolongation": [vp, C.c_int, i64p, ip, dp],
@@ -122,8 +124,11 @@ def _ptr(t):
     return t.data_ptr()
 
 
-def make_params(cfg) -> Params:
-    return Params(cfg.Re, cfg.Rem, cfg.S, cfg.gamma, cfg.sigma, cfg.mu, cfg.theta, cfg.nu, cfg.nu)
+def make_params(cfg, smoother: str = "richardson", smoother_its: int = 6) -> Params:
+    """smoother 'richardson': nu Schwarz sweeps (north star); 'gmres': GMRES(smoother_its)
+    preconditioned by the Schwarz operator, the paper's relaxation."""
+    return Params(cfg.Re, cfg.Rem, cfg.S, cfg.gamma, cfg.sigma, cfg.mu, cfg.theta, cfg.nu, cfg.nu,
+                  1 if smoother == "gmres" else 0, smoother_its)
 
 
 class Context:
@@ -155,14 +160,14 @@ class Context:
         return st
 
     # ---- setup ----
-    def assemble(self, cfg, w, N=None, levels=None):
+    def assemble(self, cfg, w, N=None, levels=None, smoother="richardson", smoother_its=6):
         mesh = Mesh(cfg.dim, N if N is not None else cfg.N, levels if levels is not None else cfg.levels)
         self._w = np.ascontiguousarray(w, np.float64)
-        p = make_params(cfg)
+        p = make_params(cfg, smoother, smoother_its)
         return self._chk(self._L.mhdp_assemble(self.h, BLOCK[cfg.block], C.byref(mesh), C.byref(p), _d(self._w)))
 
-    def begin_levels(self, n_levels, cfg):
-        p = make_params(cfg)
+    def begin_levels(self, n_levels, cfg, smoother="richardson", smoother_its=6):
+        p = make_params(cfg, smoother, smoother_its)
         return self._chk(self._L.mhdp_begin_levels(self.h, n_levels, C.byref(p)))
 
     def load_level(self, level, rowptr, col, val, pptr=None, pdofs=None, prow=None, pcol=None, pval=None):
@@ -237,6 +242,19 @@ class Context:
         if st not in (0, 6):
             self._chk(st)
         return its.value, rel.value, st == 0
+
+    def fgmres(self, b, x, rtol=1e-7, atol=1e-7, maxit=100):
+        its = C.c_int(0)
+        rel = C.c_double(0)
+        st = self._L.mhdp_fgmres(self.h, _ptr(b), _ptr(x), rtol, atol, maxit, C.byref(its), C.byref(rel))
+        if st not in (0, 6):
+            self._chk(st)
+        return its.value, rel.value, st == 0
+
+    def dot(self, a, b):
+        out = C.c_double(0)
+        self._chk(self._L.mhdp_dot(self.h, _ptr(a), _ptr(b), a.numel(), C.byref(out)))
+        return out.value
 
     def synchronize(self):
         return self._chk(self._L.mhdp_synchronize(self.h))

@@ -18,8 +18,8 @@ def rel_l2(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
-def load_oracle_levels(ctx, orc, cfg):
-    ctx.begin_levels(orc.nlev, cfg)
+def load_oracle_levels(ctx, orc, cfg, smoother="richardson", smoother_its=6):
+    ctx.begin_levels(orc.nlev, cfg, smoother, smoother_its)
     for l in range(orc.nlev):
         A = orc.csr(l)
         if l == 0:
