@@ -165,7 +165,8 @@ mhdp_status mhdp_gmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double
  * the residual estimate <= max(rtol |b|, atol).  Synchronises every iteration. */
 mhdp_status mhdp_fgmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol,
                         double atol, int maxit, int *its_out, double *relres_out);
-/* The pinned inner product of reading R-dot of two device vectors (synchronises).      */
+/* The pinned inner product of reading R-dot of two device vectors (synchronises; n = 0
+ * gives +0.0 and the pointers may then be NULL).                                       */
 mhdp_status mhdp_dot(mhdp_ctx *ctx, const double *a_dev, const double *b_dev, long long n,
                      double *out_host);
 

@@ -35,6 +35,7 @@ struct DevLevel {
     // GMRES(m) smoother workspace (NEXT-1)
     double *gV = nullptr, *gt = nullptr, *gw = nullptr, *part = nullptr;
     double *scal = nullptr;    // H (m+1)m | cs m | sn m | g m+1 | y m | hn m
+    int *kk = nullptr;         // device Krylov dimension (breakdown handling)
 };
 
 }  // namespace
@@ -336,6 +337,7 @@ void gmres_smooth(mhdp_ctx *ctx, int l, int m, bool x_is_zero, const double *b, 
     else { residual(ctx, l, b, x, L.r); r = L.r; }
     applyB(r, L.gw);
     launch_dot_pinned(L.gw, L.gw, n, L.part, S.g, 1, s);                  // beta -> g[0]
+    launch_krylov_init(S.g, m, L.kk, s);                                  // kk = 0 if beta == 0
     launch_div_dev(L.gV, L.gw, S.g, n, s);                                // V_0 = w / beta
     for (int k = 0; k < m; ++k) {
         residual(ctx, l, nullptr, L.gV + (int64_t)k * n, L.gt);           // t = A V_k
@@ -345,11 +347,11 @@ void gmres_smooth(mhdp_ctx *ctx, int l, int m, bool x_is_zero, const double *b, 
             launch_axpy_negdev(L.gw, S.H + i * m + k, L.gV + (int64_t)i * n, n, s);
         }
         launch_dot_pinned(L.gw, L.gw, n, L.part, S.hn + k, 1, s);
-        launch_givens(S.H, m, S.cs, S.sn, S.g, S.hn + k, k, s);
+        launch_givens(S.H, m, S.cs, S.sn, S.g, S.hn + k, k, L.kk, s);
         if (k + 1 < m) launch_div_dev(L.gV + (int64_t)(k + 1) * n, L.gw, S.hn + k, n, s);
     }
-    launch_backsub(S.H, m, S.g, m, S.y, s);
-    launch_basis_update(x, L.gV, n, S.y, m, n, s);
+    launch_backsub(S.H, m, S.g, m, L.kk, S.y, s);          // uses the device kk (<= m)
+    launch_basis_update(x, L.gV, n, S.y, m, L.kk, n, s);
 }
 
 void vcycle(mhdp_ctx *ctx, int l, const double *b, double *x) {
@@ -556,6 +558,7 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
             if ((st = dalloc(ctx, &L.gw, H.n))) return st;
             if ((st = dalloc(ctx, &L.part, 2 * ((H.n + 255) / 256) + 2))) return st;
             if ((st = dalloc(ctx, &L.scal, KrylovScal::size(m)))) return st;
+            if ((st = dalloc(ctx, &L.kk, 1))) return st;
         }
         if ((st = build_csr(ctx, H.n, H.prp, H.pci, H.pv, L.Pr))) return st;
         std::vector<int64_t> trp; std::vector<int> tci; std::vector<double> tv;
@@ -866,14 +869,14 @@ mhdp_status mhdp_fgmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, doubl
             launch_axpy_negdev(w, S.H + i * m + k, V + (int64_t)i * n, n, s);
         }
         launch_dot_pinned(w, w, n, ctx->fpart, S.hn + k, 1, s);
-        launch_givens(S.H, m, S.cs, S.sn, S.g, S.hn + k, k, s);
+        launch_givens(S.H, m, S.cs, S.sn, S.g, S.hn + k, k, nullptr, s);
         gk = std::fabs(read(S.g + k + 1));
         if (gk <= tol) { ++k; conv = true; break; }
         if (read(S.hn + k) == 0.0) { ++k; break; }
         launch_div_dev(V + (int64_t)(k + 1) * n, w, S.hn + k, n, s);
     }
-    launch_backsub(S.H, m, S.g, k, S.y, s);
-    launch_basis_update(x_dev, Z, n, S.y, k, n, s);
+    launch_backsub(S.H, m, S.g, k, nullptr, S.y, s);
+    launch_basis_update(x_dev, Z, n, S.y, k, nullptr, n, s);
     CK(cudaStreamSynchronize(s));
     if (its_out) *its_out = k;
     if (relres_out) *relres_out = gk / beta;
@@ -884,7 +887,7 @@ mhdp_status mhdp_fgmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, doubl
 mhdp_status mhdp_dot(mhdp_ctx *ctx, const double *a_dev, const double *b_dev, long long n, double *out_host) {
     if (!ctx) return MHDP_EINVAL;
     if (ctx->host_only) return fail(ctx, MHDP_ECUDA, "host-only context");
-    if (!a_dev || !b_dev || !out_host || n < 0) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    if (!out_host || n < 0 || (n > 0 && (!a_dev || !b_dev))) return fail(ctx, MHDP_EINVAL, "bad arguments");
     cudaSetDevice(ctx->device);
     double *part = nullptr, *out = nullptr;
     CK(cudaMalloc(&part, sizeof(double) * (2 * ((n + 255) / 256) + 2)));

@@ -93,9 +93,12 @@ void launch_dot_pinned(const double *a, const double *b, int64_t n, double *part
                        cudaStream_t s);
 void launch_axpy_negdev(double *w, const double *h, const double *v, int64_t n, cudaStream_t s);  // w -= h[0] v
 void launch_div_dev(double *y, const double *x, const double *d, int64_t n, cudaStream_t s);       // y = x / d[0]
-void launch_givens(double *H, int m, double *cs, double *sn, double *g, const double *hn, int k, cudaStream_t s);
-void launch_backsub(const double *H, int m, const double *g, int kk, double *y, cudaStream_t s);
-void launch_basis_update(double *x, const double *V, int64_t ldv, const double *y, int kk, int64_t n,
-                         cudaStream_t s);
+// kk_dev (optional): device Krylov dimension, set by launch_krylov_init / launch_givens
+void launch_krylov_init(const double *g, int m, int *kk, cudaStream_t s);
+void launch_givens(double *H, int m, double *cs, double *sn, double *g, const double *hn, int k, int *kk_dev,
+                   cudaStream_t s);
+void launch_backsub(const double *H, int m, const double *g, int kk, const int *kk_dev, double *y, cudaStream_t s);
+void launch_basis_update(double *x, const double *V, int64_t ldv, const double *y, int kk, const int *kk_dev,
+                         int64_t n, cudaStream_t s);
 
 }  // namespace mhdp

@@ -79,3 +79,19 @@ def test_gmres_smoothed_end_to_end(oracle_mod, name, N, L):
     its_g, rel, conv_g = ctx.fgmres(cuda_vec(b), xg, maxit=40)
     assert (its_g, conv_g) == (its_o, conv_o)
     assert np.array_equal(bits(host(xg)), bits(xo))
+
+
+def test_gmres_smoother_zero_rhs_breakdown(oracle_mod):
+    """b = 0: the smoother's Krylov space is empty (beta = 0, R-gmres6 breakdown), the
+    V-cycle returns exactly 0 (no NaN from the 0/0 of the first basis vector)."""
+    import torch
+    from paper_2104_14855_b200 import workloads
+    cfg = workloads.small("c5", 4, 2)
+    w, _, _ = workloads.draw(cfg, 1, 0)
+    ctx = _ctx()
+    ctx.assemble(cfg, w, smoother="gmres", smoother_its=6)
+    ctx.setup()
+    n = ctx.n()
+    xg = torch.full((n,), 7.0, dtype=torch.float64, device="cuda:0")
+    ctx.vcycle(torch.zeros(n, dtype=torch.float64, device="cuda:0"), xg)
+    assert torch.count_nonzero(xg).item() == 0
