@@ -253,6 +253,37 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     ms_k8 = e0.elapsed_time(e1) / reps
 
+    # ---- Krylov solves: GMRES(V-cycle) with the Richardson smoother (iteration counts of the
+    # north star), and NEXT-1: the paper's GMRES(6)-smoothed V-cycle inside flexible GMRES
+    # (rtol = atol = 1e-7) ----
+    solves = None
+    if not args.no_solves:
+        xk = torch.empty_like(bd)
+        e0.record(stream)
+        its_r, rel_r, conv_r = ctx.gmres(bd, xk, maxit=60)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms_gr = e0.elapsed_time(e1)
+        ctx.set_smoother("gmres", 6)
+        ctx.vcycle(bd, xk)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(3):
+            ctx.vcycle(bd, xk)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms_vg = e0.elapsed_time(e1) / 3
+        e0.record(stream)
+        its_f, rel_f, conv_f = ctx.fgmres(bd, xk, maxit=60)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms_f = e0.elapsed_time(e1)
+        ctx.set_smoother("richardson", 6)
+        solves = {"gmres_richardson_vcycle": {"its": its_r, "converged": conv_r, "relres": rel_r, "ms": ms_gr},
+                  "next1_gmres6_smoothed_vcycle_ms": ms_vg,
+                  "next1_fgmres": {"its": its_f, "converged": conv_f, "relres": rel_f, "ms": ms_f},
+                  "tolerance": "max(1e-7 |b|, 1e-7), Euclidean (P:654)"}
+
     # algorithmic bytes: K2 per patch i: 8 n_i^2 factor + 8 n_i gathered r
     # + 8 n_i written y; sweep: 8 sum n_i^2 + 8 nnz + 24 n
     k2_bytes = 8 * fin["sum_n2"] + 16 * fin["sum_n"]
@@ -306,6 +337,7 @@ def run_ours(args):
             "clocks": clk.summary(),
             "setup_s": {"host_assembly": t_asm, "device_setup": t_setup},
             "cpu_baseline": cpu,
+            "solves": solves,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -322,6 +354,7 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-solves", action="store_true", help="skip the GMRES / FGMRES solves")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -159,6 +159,9 @@ mhdp_status mhdp_smooth_host(mhdp_ctx *ctx, int level, int nsweeps, int x_is_zer
 mhdp_status mhdp_gmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol,
                        double atol, int maxit, int *its_out, double *relres_out);
 
+/* Switch the V-cycle smoother (see mhdp_params.smoother / smoother_its); may be called
+ * before or after mhdp_setup (the GMRES workspace is allocated on demand).             */
+mhdp_status mhdp_set_smoother(mhdp_ctx *ctx, int smoother, int smoother_its);
 /* Flexible GMRES with the current V-cycle as a variable right preconditioner on
  * the finest level (required when the smoother is GMRES, which makes the V-cycle
  * nonlinear); x0 = 0; inner products in the pinned order of reading R-dot; stops when

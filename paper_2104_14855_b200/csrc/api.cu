@@ -36,6 +36,7 @@ struct DevLevel {
     double *gV = nullptr, *gt = nullptr, *gw = nullptr, *part = nullptr;
     double *scal = nullptr;    // H (m+1)m | cs m | sn m | g m+1 | y m | hn m
     int *kk = nullptr;         // device Krylov dimension (breakdown handling)
+    int gm = 0;                // smoother iterations the workspace holds
 };
 
 }  // namespace
@@ -354,6 +355,20 @@ void gmres_smooth(mhdp_ctx *ctx, int l, int m, bool x_is_zero, const double *b, 
     launch_basis_update(x, L.gV, n, S.y, m, L.kk, n, s);
 }
 
+// GMRES(m) smoother workspace of one level (allocated at setup or by mhdp_set_smoother)
+mhdp_status alloc_smoother(mhdp_ctx *ctx, DevLevel &L, int m) {
+    mhdp_status st;
+    if (L.gm >= m) return MHDP_OK;
+    if ((st = dalloc(ctx, &L.gV, (int64_t)(m + 1) * L.n))) return st;
+    if (!L.gt && (st = dalloc(ctx, &L.gt, L.n))) return st;
+    if (!L.gw && (st = dalloc(ctx, &L.gw, L.n))) return st;
+    if (!L.part && (st = dalloc(ctx, &L.part, 2 * ((L.n + 255) / 256) + 2))) return st;
+    if ((st = dalloc(ctx, &L.scal, KrylovScal::size(m)))) return st;
+    if (!L.kk && (st = dalloc(ctx, &L.kk, 1))) return st;
+    L.gm = m;
+    return MHDP_OK;
+}
+
 void vcycle(mhdp_ctx *ctx, int l, const double *b, double *x) {
     if (l == 0) {
         coarse_solve(ctx, b, x);
@@ -551,15 +566,7 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         if ((st = dalloc(ctx, &L.r, H.n))) return st;
         if (l == 0) continue;
         if ((st = build_patches(ctx, H, L))) return st;
-        if (ctx->p.smoother == 1) {
-            const int m = ctx->p.smoother_its;
-            if ((st = dalloc(ctx, &L.gV, (int64_t)(m + 1) * H.n))) return st;
-            if ((st = dalloc(ctx, &L.gt, H.n))) return st;
-            if ((st = dalloc(ctx, &L.gw, H.n))) return st;
-            if ((st = dalloc(ctx, &L.part, 2 * ((H.n + 255) / 256) + 2))) return st;
-            if ((st = dalloc(ctx, &L.scal, KrylovScal::size(m)))) return st;
-            if ((st = dalloc(ctx, &L.kk, 1))) return st;
-        }
+        if (ctx->p.smoother == 1 && (st = alloc_smoother(ctx, L, ctx->p.smoother_its))) return st;
         if ((st = build_csr(ctx, H.n, H.prp, H.pci, H.pv, L.Pr))) return st;
         std::vector<int64_t> trp; std::vector<int> tci; std::vector<double> tv;
         transpose_csr(H.n, H.n_coarser, H.prp, H.pci, H.pv, trp, tci, tv);
@@ -822,6 +829,23 @@ mhdp_status mhdp_gmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double
     if (relres_out) *relres_out = std::fabs(g[k]) / beta;
     if ((st = check_launch(ctx))) return st;
     return conv ? MHDP_OK : fail(ctx, MHDP_ENOCONV, "GMRES reached maxit");
+}
+
+mhdp_status mhdp_set_smoother(mhdp_ctx *ctx, int smoother, int smoother_its) {
+    if (!ctx) return MHDP_EINVAL;
+    if (smoother != 0 && smoother != 1) return fail(ctx, MHDP_EINVAL, "smoother must be 0 or 1");
+    if (smoother == 1 && (smoother_its < 1 || smoother_its > 32))
+        return fail(ctx, MHDP_EINVAL, "smoother_its must be in 1..32");
+    if (smoother == 1 && ctx->setup_done) {
+        cudaSetDevice(ctx->device);
+        for (int l = 1; l < ctx->nlev; ++l) {
+            mhdp_status st = alloc_smoother(ctx, ctx->D[l], smoother_its);
+            if (st) return st;
+        }
+    }
+    ctx->p.smoother = smoother;
+    ctx->p.smoother_its = smoother_its;
+    return MHDP_OK;
 }
 
 mhdp_status mhdp_fgmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol, double atol, int maxit,

@@ -48,7 +48,7 @@ SYMBOLS = ["mhdp_create", "mhdp_destroy", "mhdp_assemble", "mhdp_begin_levels", 
            "mhdp_patch_update", "mhdp_smooth", "mhdp_restrict", "mhdp_prolong_add", "mhdp_coarse_solve",
            "mhdp_vcycle", "mhdp_vcycle_host", "mhdp_smooth_host", "mhdp_gmres", "mhdp_export_csr",
            "mhdp_export_patches", "mhdp_export_prolongation", "mhdp_export_patch_lu", "mhdp_export_slots",
-           "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count", "mhdp_fgmres", "mhdp_dot"]
+           "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count", "mhdp_fgmres", "mhdp_dot", "mhdp_set_smoother"]
 
 
 def lib():
@@ -80,6 +80,7 @@ def lib():
             "mhdp_gmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp],
             "mhdp_fgmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp],
             "mhdp_dot": [vp, vp, vp, i64, dp],
+            "mhdp_set_smoother": [vp, C.c_int, C.c_int],
             "mhdp_export_csr": [vp, C.c_int, i64p, ip, dp],
             "mhdp_export_patches": [vp, C.c_int, i64p, ip],
             "mhdp_export_prolongation": [vp, C.c_int, i64p, ip, dp],
@@ -242,6 +243,9 @@ class Context:
         if st not in (0, 6):
             self._chk(st)
         return its.value, rel.value, st == 0
+
+    def set_smoother(self, smoother="richardson", its=6):
+        return self._chk(self._L.mhdp_set_smoother(self.h, 1 if smoother == "gmres" else 0, its))
 
     def fgmres(self, b, x, rtol=1e-7, atol=1e-7, maxit=100):
         its = C.c_int(0)
