@@ -144,8 +144,12 @@ mhdp_status mhdp_prolong_add(mhdp_ctx *ctx, int level, const double *ec_dev, dou
 /* x = A_0^{-1} b by the dense coarse LU (K8)                                            */
 mhdp_status mhdp_coarse_solve(mhdp_ctx *ctx, const double *b_dev, double *x_dev);
 /* x = V_l(b) with zero initial guess on level `level` (finest: n_levels-1), P:643:
- * nu_pre sweeps, residual, restrict, recurse, prolong-add, nu_post sweeps.             */
+ * nu_pre sweeps, residual, restrict, recurse, prolong-add, nu_post sweeps.  Repeated
+ * calls with the same (level, b, x) replay a CUDA graph of the cycle (captured on the
+ * second call; env MHDP_NO_GRAPH disables this).                                       */
 mhdp_status mhdp_vcycle(mhdp_ctx *ctx, int level, const double *b_dev, double *x_dev);
+/* number of captured V-cycle graphs currently held (diagnostics)                       */
+int         mhdp_vcycle_graphs_active(const mhdp_ctx *ctx);
 /* End-to-end variant for callers holding host data: copies b (host, n doubles) to the
  * device, runs mhdp_vcycle on the finest level and copies x back (synchronises).       */
 mhdp_status mhdp_vcycle_host(mhdp_ctx *ctx, const double *b_host, double *x_host);

@@ -11,6 +11,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -71,6 +72,20 @@ struct mhdp_ctx {
     // fgmres workspace
     double *fV = nullptr, *fZ = nullptr, *fw = nullptr, *fpart = nullptr, *fscal = nullptr;
     int f_cap = 0;
+    // CUDA graphs of mhdp_vcycle, keyed by (level, b, x, smoother): the first call with a
+    // key runs directly, the second captures the V-cycle on a private stream, later calls
+    // replay it on the context stream
+    struct VGraph {
+        int level, smoother, its;
+        const double *b;
+        double *x;
+        int calls = 0;
+        cudaGraphExec_t exec = nullptr;
+        long long nkern = 0;
+    };
+    std::vector<VGraph> graphs;
+    cudaStream_t cap = nullptr;
+    bool graphs_off = false;
 };
 
 namespace {
@@ -114,10 +129,17 @@ mhdp_status check_launch(mhdp_ctx *ctx) {
     return MHDP_OK;
 }
 
+void drop_graphs(mhdp_ctx *c) {
+    for (auto &g : c->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+}
+
 void free_device(mhdp_ctx *c) {
     if (c->host_only) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    drop_graphs(c);
     for (void *p : c->allocs) cudaFree(p);
     c->allocs.clear();
     c->D.clear();
@@ -455,6 +477,7 @@ mhdp_status mhdp_create(mhdp_ctx **out, int cuda_device, void *cuda_stream) {
 void mhdp_destroy(mhdp_ctx *ctx) {
     if (!ctx) return;
     free_device(ctx);
+    if (ctx->cap) cudaStreamDestroy(ctx->cap);
     delete ctx;
 }
 
@@ -723,7 +746,58 @@ mhdp_status mhdp_vcycle(mhdp_ctx *ctx, int level, const double *b_dev, double *x
     mhdp_status st = need_setup(ctx);
     if (st) return st;
     if (!valid_level(ctx, level) || !b_dev || !x_dev) return fail(ctx, MHDP_EINVAL, "bad arguments");
-    vcycle(ctx, level, b_dev, x_dev);
+    if (ctx->graphs_off || getenv("MHDP_NO_GRAPH")) {
+        vcycle(ctx, level, b_dev, x_dev);
+        return check_launch(ctx);
+    }
+    mhdp_ctx::VGraph *g = nullptr;
+    for (auto &e : ctx->graphs)
+        if (e.level == level && e.b == b_dev && e.x == x_dev && e.smoother == ctx->p.smoother &&
+            e.its == ctx->p.smoother_its)
+            g = &e;
+    if (!g) {
+        mhdp_ctx::VGraph e;
+        e.level = level; e.b = b_dev; e.x = x_dev; e.smoother = ctx->p.smoother; e.its = ctx->p.smoother_its;
+        if (ctx->graphs.size() >= 16) drop_graphs(ctx);
+        ctx->graphs.push_back(e);
+        g = &ctx->graphs.back();
+    }
+    if (g->exec) {
+        CK(cudaGraphLaunch(g->exec, ctx->stream));
+        g_launches += g->nkern;
+        return check_launch(ctx);
+    }
+    if (g->calls++ == 0) {           // first call: run directly (also initialises kernel attributes)
+        vcycle(ctx, level, b_dev, x_dev);
+        return check_launch(ctx);
+    }
+    if ((st = check_launch(ctx))) return st;
+    if (!ctx->cap) CK(cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
+    cudaStream_t saved = ctx->stream;
+    const long long before = g_launches;
+    cudaGraph_t graph = nullptr;
+    bool ok = cudaStreamBeginCapture(ctx->cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+        ctx->stream = ctx->cap;
+        vcycle(ctx, level, b_dev, x_dev);
+        ctx->stream = saved;
+        ok = cudaStreamEndCapture(ctx->cap, &graph) == cudaSuccess && graph;
+    }
+    cudaGraphExec_t exec = nullptr;
+    if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    const long long nk = g_launches - before;
+    g_launches = before;
+    if (!ok) {                       // capture unsupported here: run uncaptured from now on
+        cudaGetLastError();
+        ctx->graphs_off = true;
+        vcycle(ctx, level, b_dev, x_dev);
+        return check_launch(ctx);
+    }
+    g->exec = exec;
+    g->nkern = nk;
+    CK(cudaGraphLaunch(exec, ctx->stream));
+    g_launches += nk;
     return check_launch(ctx);
 }
 
@@ -846,6 +920,13 @@ mhdp_status mhdp_set_smoother(mhdp_ctx *ctx, int smoother, int smoother_its) {
     ctx->p.smoother = smoother;
     ctx->p.smoother_its = smoother_its;
     return MHDP_OK;
+}
+
+int mhdp_vcycle_graphs_active(const mhdp_ctx *ctx) {
+    if (!ctx || ctx->graphs_off) return 0;
+    int n = 0;
+    for (const auto &g : ctx->graphs) n += g.exec != nullptr;
+    return n;
 }
 
 mhdp_status mhdp_fgmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol, double atol, int maxit,

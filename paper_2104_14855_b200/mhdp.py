@@ -48,7 +48,7 @@ SYMBOLS = ["mhdp_create", "mhdp_destroy", "mhdp_assemble", "mhdp_begin_levels", 
            "mhdp_patch_update", "mhdp_smooth", "mhdp_restrict", "mhdp_prolong_add", "mhdp_coarse_solve",
            "mhdp_vcycle", "mhdp_vcycle_host", "mhdp_smooth_host", "mhdp_gmres", "mhdp_export_csr",
            "mhdp_export_patches", "mhdp_export_prolongation", "mhdp_export_patch_lu", "mhdp_export_slots",
-           "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count", "mhdp_fgmres", "mhdp_dot", "mhdp_set_smoother"]
+           "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count", "mhdp_fgmres", "mhdp_dot", "mhdp_set_smoother", "mhdp_vcycle_graphs_active"]
 
 
 def lib():
@@ -97,6 +97,8 @@ def lib():
         L.mhdp_destroy.restype = None
         L.mhdp_num_levels.argtypes = [vp]
         L.mhdp_num_levels.restype = C.c_int
+        L.mhdp_vcycle_graphs_active.argtypes = [vp]
+        L.mhdp_vcycle_graphs_active.restype = C.c_int
         L.mhdp_launch_count.argtypes = [vp]
         L.mhdp_launch_count.restype = C.c_longlong
         _lib = L
@@ -262,6 +264,9 @@ class Context:
 
     def synchronize(self):
         return self._chk(self._L.mhdp_synchronize(self.h))
+
+    def graphs_active(self):
+        return self._L.mhdp_vcycle_graphs_active(self.h)
 
     def launch_count(self):
         return self._L.mhdp_launch_count(self.h)

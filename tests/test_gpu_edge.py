@@ -166,3 +166,29 @@ def test_determinism_repeated_runs(oracle_mod):
         outs.append((bits(host(xg)), bits(host(xs))))
     for o in outs[1:]:
         assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
+
+
+@pytest.mark.parametrize("smoother", ["richardson", "gmres"])
+def test_vcycle_graph_replay_bitexact(oracle_mod, smoother):
+    """mhdp_vcycle replays a captured CUDA graph from the second call with the same
+    (level, b, x); the replayed cycle is bit-identical to the direct one and to the
+    oracle."""
+    import torch
+    from paper_2104_14855_b200 import workloads
+    cfg = workloads.small("c5", 6, 2)
+    w, _, _ = workloads.draw(cfg, 1, 9)
+    ctx = _ctx()
+    ctx.assemble(cfg, w, smoother=smoother)
+    ctx.setup()
+    n = ctx.n()
+    _, b, _ = workloads.draw(cfg, n, 9)
+    orc = oracle_mod.Oracle(cfg, w, exact=True)
+    orc.set_smoother(smoother, 6)
+    ref = bits(orc.vcycle(b))
+    bd = cuda_vec(b)
+    xg = torch.empty(n, dtype=torch.float64, device="cuda:0")
+    for call in range(4):
+        xg.fill_(3.0)
+        ctx.vcycle(bd, xg)
+        assert np.array_equal(bits(host(xg)), ref), f"call {call}"
+    assert ctx.graphs_active() >= 1
