@@ -240,6 +240,20 @@ def run_ours(args):
     e1.record(stream)
     torch.cuda.synchronize(dev)
     ms_k1 = e0.elapsed_time(e1) / reps
+    # one sweep on every level (where the V-cycle's time goes besides the finest level)
+    level_sweep_ms = []
+    for l in range(1, L):
+        nl = infos[l]["n"]
+        bl = torch.from_numpy(np.random.default_rng(l).uniform(-1, 1, nl)).to(dev)
+        xl = torch.zeros_like(bl)
+        ctx.smooth(bl, xl, level=l, nsweeps=1)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(reps):
+            ctx.smooth(bl, xl, level=l, nsweeps=1)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        level_sweep_ms.append(e0.elapsed_time(e1) / reps)
     # coarse solve (K8) alone
     n0 = infos[0]["n"]
     bc = torch.from_numpy(np.random.default_rng(seed).uniform(-1, 1, n0)).to(dev)
@@ -327,7 +341,7 @@ def run_ours(args):
                       "frac": sweep_bytes / (ms_sweep * 1e-3) / 1e9 / peak, "bytes": sweep_bytes},
             "kernels": {"K2_patch_apply_ms": ms_k2, "K1_residual_ms": ms_k1,
                         "K1_gbs": k1_bytes / (ms_k1 * 1e-3) / 1e9, "K8_coarse_solve_ms": ms_k8,
-                        "coarse_n": n0},
+                        "coarse_n": n0, "sweep_ms_per_level": level_sweep_ms},
             "roofline": {"bound": "hbm", "kernel": "K2 patch gather + LU apply (finest level)",
                          "achieved": k2_gbs, "peak": peak, "unit": "GB/s", "frac": k2_gbs / peak,
                          "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback"},

@@ -64,6 +64,11 @@ typedef struct {
                                  operator, once before and once after the coarse correction
                                  -- the paper's relaxation, P:643 (R-gmres6)                  */
     int smoother_its;         /* GMRES iterations of the smoother (6), 1..32           */
+    double dt;                /* NEXT-4: 0 = stationary (eta = 0); > 0 = one implicit step
+                                 (eta = 1): (1/dt)(B, C) in the E-B block, (1/dt)(u, v) in the
+                                 velocity block                            */
+    int picard;               /* NEXT-4: 0 = Newton (delta = 1), 1 = Picard (delta = 0): the
+                                 E-B block loses G~                        */
 } mhdp_params;
 
 typedef struct mhdp_ctx mhdp_ctx;

@@ -56,7 +56,7 @@ void orc_destroy(OCtx *c) {
     free(c->lv); free(c->clu); free(c->cperm); free(c);
 }
 
-/* dparams: Re, Rem, S, gamma, sigma, mu, theta ; iparams: nu_pre, nu_post
+/* dparams: Re, Rem, S, gamma, sigma, mu, theta, dt ; iparams: nu_pre, nu_post, picard
  * w_fine: potential of the advecting field at the finest vertices (vertex order of
  *         R-mesh): 2D stream function psi (1 per vertex), 3D vector potential A (3 per vertex).
  * cmask_fine: NULL, or a finest-level cell mask (only then: assemble the finest
@@ -70,6 +70,7 @@ OCtx *orc_create_masked(int block, int dim, int N, int nlev, const double *dpara
     c->p.Re = dparams[0]; c->p.Rem = dparams[1]; c->p.S = dparams[2]; c->p.gamma = dparams[3];
     c->p.sigma = dparams[4]; c->p.mu = dparams[5]; c->theta = dparams[6];
     c->p.nu_pre = iparams[0]; c->p.nu_post = iparams[1];
+    c->p.dt = dparams[7]; c->p.picard = iparams[2];
     c->lv = calloc((size_t)nlev, sizeof(OLevel));
     int lo = cmask_fine ? nlev - 1 : 0;
     for (int l = nlev - 1; l >= lo; l--) {

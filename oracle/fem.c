@@ -510,7 +510,7 @@ static void assemble_eb(OCsr *A, Accum *S, signed char *cnt, const OMesh *m, con
         real wx[3];
         cell_pot(m, c, w, pot);
         cell_wind(&K, pot, wx);
-        real EE[6 * 6] = {0}, EB[6 * 4] = {0}, BE[4 * 6] = {0};
+        real EE[6 * 6] = {0}, EB[6 * 4] = {0}, BE[4 * 6] = {0}, BB[4 * 4] = {0};
         int nq = cell_rule(&K, 3, xq, wq);
         for (int t = 0; t < nq; t++) {
             real ev[6][3], bv[4][3];
@@ -523,15 +523,21 @@ static void assemble_eb(OCsr *A, Accum *S, signed char *cnt, const OMesh *m, con
                     real wxb;
                     if (d == 2) wxb = (wx[0] * bv[k][1] - wx[1] * bv[k][0]) * ev[i][0];
                     else { real cr[3]; cross3(wx, bv[k], cr); wxb = dot3(cr, ev[i]); }
+                    if (p->picard) wxb = 0;                      /* delta = 0 */
                     real ab = dot3(bv[k], curlE[i]);
                     EB[i * 4 + k] += wq[t] * (wxb - ab / p->Rem);
                     BE[k * 6 + i] += wq[t] * ab;
                 }
             }
+            /* transient (eta = 1): (1/dt)(B, C) in the B-B block */
+            if (p->dt > 0)
+                for (int k = 0; k < nBl; k++)
+                    for (int l = 0; l < nBl; l++) BB[k * 4 + l] += wq[t] * dot3(bv[l], bv[k]) / p->dt;
         }
         scatter(A, S, gE, nEl, gE, nEl, EE, 6);
         scatter(A, S, gE, nEl, gB, nBl, EB, 4);
         scatter(A, S, gB, nBl, gE, nEl, BE, 6);
+        if (p->dt > 0) scatter(A, S, gB, nBl, gB, nBl, BB, 4);
         for (int k = 0; k < nBl; k++)
             for (int l = 0; l < nBl; l++)
                 if (gB[k] >= 0 && gB[l] >= 0) cnt[oc_find(A, gB[k], gB[l])] += (signed char)(sB[k] * sB[l]);
@@ -600,7 +606,8 @@ static void assemble_vel(OCsr *A, Accum *S, signed char *cnt, const OMesh *m, co
                 for (int j = 0; j < nb; j++) {
                     real ee = 0;
                     for (int l = 0; l < 3; l++) for (int k = 0; k < 3; k++) ee += eps[j][l][k] * eps[i][l][k];
-                    loc[i * 12 + j] += wq[t] * (nu2 * ee - dot3(fv[j], dvw));
+                    real mass = p->dt > 0 ? dot3(fv[j], fv[i]) / p->dt : (real)0;   /* (eta/dt)(u, v) */
+                    loc[i * 12 + j] += wq[t] * (nu2 * ee - dot3(fv[j], dvw) + mass);
                 }
             }
         }

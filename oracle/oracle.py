@@ -137,8 +137,9 @@ class Oracle:
         self.nlev = nlev if nlev is not None else cfg.levels
         N = N if N is not None else cfg.N
         self.N = N
-        dp = np.array([cfg.Re, cfg.Rem, cfg.S, cfg.gamma, cfg.sigma, cfg.mu, cfg.theta], dtype=np.float64)
-        ip = np.array([cfg.nu, cfg.nu], dtype=np.int32)
+        dp = np.array([cfg.Re, cfg.Rem, cfg.S, cfg.gamma, cfg.sigma, cfg.mu, cfg.theta,
+                       getattr(cfg, "dt", 0.0)], dtype=np.float64)
+        ip = np.array([cfg.nu, cfg.nu, int(getattr(cfg, "picard", 0))], dtype=np.int32)
         self._w = np.ascontiguousarray(w, dtype=np.float64)
         if cmask is None:
             self.h = L.orc_create(cfg.block_id, cfg.dim, N, self.nlev, _d(dp), _i(ip), _d(self._w))

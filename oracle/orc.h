@@ -78,6 +78,8 @@ i64  oc_find(const OCsr *a, i64 row, int col);   /* position of (row,col) or -1 
 typedef struct {
     double Re, Rem, S, gamma, sigma, mu;
     int nu_pre, nu_post;
+    double dt;     /* NEXT-4: > 0 -> transient (eta = 1): (1/dt) mass terms */
+    int picard;    /* NEXT-4: 1 -> Picard linearisation (delta = 0): no G~ term    */
 } OParams;
 
 /* ---------------- operator assembly ---------------- */

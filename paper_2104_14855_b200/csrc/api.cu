@@ -495,6 +495,9 @@ static mhdp_status check_params(mhdp_ctx *ctx, const mhdp_params *pr) {
     if (pr->smoother == 1 && (pr->smoother_its < 1 || pr->smoother_its > 32))
         return fail(ctx, MHDP_EINVAL, "smoother_its must be in 1..32");
     ctx->p.smoother = pr->smoother; ctx->p.smoother_its = pr->smoother_its;
+    if (pr->dt < 0 || pr->dt != pr->dt) return fail(ctx, MHDP_EINVAL, "dt must be >= 0");
+    if (pr->picard != 0 && pr->picard != 1) return fail(ctx, MHDP_EINVAL, "picard must be 0 or 1");
+    ctx->p.dt = pr->dt; ctx->p.picard = pr->picard;
     return MHDP_OK;
 }
 

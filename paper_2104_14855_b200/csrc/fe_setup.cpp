@@ -487,10 +487,11 @@ struct EBLocal {
     int nE, nB;
     int gE[6], gB[4];
     double sB[4];
-    dd EE[6][6], EB[6][4], BE[4][6];
+    dd EE[6][6], EB[6][4], BE[4][6], BB[4][4];
 };
 
-void eb_local(const Mesh &m, const Space &s, i64 c, const double *pot, double Rem, EBLocal &K) {
+void eb_local(const Mesh &m, const Space &s, i64 c, const double *pot, double Rem, double dt, int picard,
+              EBLocal &K) {
     GeoT<dd> G;
     cell_geo(m, c, G);
     const int d = m.dim, nvc = d + 1;
@@ -554,11 +555,24 @@ void eb_local(const Mesh &m, const Space &s, i64 c, const double *pot, double Re
                 for (int b = 0; b <= 3; ++b)
                     gt += mass_bary(G, b, a) * dot3(wx[b], G.g[bb]) - mass_bary(G, b, bb) * dot3(wx[b], G.g[a]);
             }
-            gt = gt * cq[q];
+            gt = picard ? dd(0.0) : gt * cq[q];                       // delta = 0: no G~ (NEXT-4)
             K.EB[i][q] = gt - a_iq / dd(Rem);
             K.BE[q][i] = a_iq;
         }
     }
+    // transient (eta = 1): (1/dt)(psi_l, psi_k) = (1/dt) c_k c_l sum_ab M_ab (X_a - X_k).(X_b - X_l)
+    for (int k = 0; k < nvc; ++k)
+        for (int l = 0; l < nvc; ++l) {
+            dd acc(0.0);
+            if (dt > 0)
+                for (int a = 0; a <= d; ++a)
+                    for (int b = 0; b <= d; ++b) {
+                        dd ta[3], tb[3];
+                        for (int r = 0; r < 3; ++r) { ta[r] = G.X[a][r] - G.X[k][r]; tb[r] = G.X[b][r] - G.X[l][r]; }
+                        acc += mass_bary(G, a, b) * dot3(ta, tb);
+                    }
+            K.BB[k][l] = dt > 0 ? acc * cq[k] * cq[l] / dd(dt) : dd(0.0);
+        }
     (void)rRem;
 }
 
@@ -603,7 +617,7 @@ void assemble_eb(const Mesh &m, const Space &s, const Params &p, const double *p
     // element data of every cell, once
     std::vector<EBLocal> loc(m.nc);
 #pragma omp parallel for schedule(static)
-    for (i64 c = 0; c < m.nc; ++c) eb_local(m, s, c, pot, p.Rem, loc[c]);
+    for (i64 c = 0; c < m.nc; ++c) eb_local(m, s, c, pot, p.Rem, p.dt, p.picard, loc[c]);
     val.assign(P.rp[s.n], 0.0);
     const double Kinv = d == 2 ? 2.0 * m.N * m.N : 6.0 * m.N * m.N * m.N;   // 1/|K|
 #pragma omp parallel for schedule(dynamic, 256)
@@ -626,7 +640,10 @@ void assemble_eb(const Mesh &m, const Space &s, const Params &p, const double *p
             } else {
                 for (int j = 0; j < K.nE; ++j) if (K.gE[j] >= 0) add(K.gE[j], K.BE[li][j]);
                 for (int q = 0; q < K.nB; ++q)
-                    if (K.gB[q] >= 0) cnt[find_col(P, r, K.gB[q]) - base] += (int)(K.sB[li] * K.sB[q]);
+                    if (K.gB[q] >= 0) {
+                        cnt[find_col(P, r, K.gB[q]) - base] += (int)(K.sB[li] * K.sB[q]);
+                        if (p.dt > 0) add(K.gB[q], K.BB[li][q]);
+                    }
             }
         }
         // C = (1/Rem)(div psi_l, div psi_k): exact value Kinv m / Rem (R-gamma)
@@ -734,7 +751,10 @@ void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *
                     if (K.gi[j] < 0) continue;
                     dd ee(0.0);
                     for (int l = 0; l < 3; ++l) for (int r = 0; r < 3; ++r) ee += K.eps[j][l][r] * K.eps[i][l][r];
-                    add(a, K.gi[j], nu2 * V * ee - dot3(K.B.v[j], K.B.v[i]) * gw * Vn);   // viscous - advection
+                    dd term = nu2 * V * ee - dot3(K.B.v[j], K.B.v[i]) * gw * Vn;          // viscous - advection
+                    if (p.dt > 0)                                                         // (1/dt)(u, v), NEXT-4
+                        term += mass_bary(K.G, K.B.a[j], K.B.a[i]) * dot3(K.B.v[j], K.B.v[i]) / dd(p.dt);
+                    add(a, K.gi[j], term);
                 }
             }
             for (int j = 0; j < nb; ++j)

@@ -13,6 +13,8 @@ struct Params {
     double Re = 1, Rem = 1, S = 1, gamma = 1, sigma = 10, mu = 0, theta = 1;
     int nu_pre = 1, nu_post = 1;
     int smoother = 0, smoother_its = 6;   // 0 Richardson sweeps, 1 GMRES(m) (NEXT-1)
+    double dt = 0;                         // NEXT-4: > 0 -> transient, (1/dt) mass terms
+    int picard = 0;                        // NEXT-4: 1 -> Picard, no G~ term
 };
 
 // One level of the hierarchy as host arrays (the form both mhdp_assemble and

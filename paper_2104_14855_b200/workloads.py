@@ -38,6 +38,8 @@ class Config:
     sigma: float = 10.0  # SIPG penalty 10 k^2, k = 1
     mu: float = 0.0      # Burman stabilisation (off, reading R-mu)
     theta: float = 1.0
+    dt: float = 0.0      # NEXT-4: > 0 -> transient, (1/dt) mass terms
+    picard: int = 0      # NEXT-4: 1 -> Picard linearisation, delta = 0
 
     @property
     def block_id(self) -> int:

@@ -16,7 +16,8 @@ def _lamb(expr, dim):
     return lambda P: np.broadcast_to(np.asarray(f(P[:, 0], P[:, 1], P[:, 2]), dtype=float), (P.shape[0],))
 
 
-def eb_fields(dim, Rem, wconst, div_free_B=False):
+def eb_fields(dim, Rem, wconst, div_free_B=False, dt=0.0, picard=0):
+    """dt > 0: transient B-equation source + B/dt; picard: no w x B term (NEXT-4)."""
     pi = sp.pi
     if dim == 2:
         E = sp.sin(pi * X) * sp.sin(pi * Y)
@@ -26,10 +27,10 @@ def eb_fields(dim, Rem, wconst, div_free_B=False):
             B = [sp.sin(pi * X), sp.sin(pi * Y)]
         curlB = sp.diff(B[1], X) - sp.diff(B[0], Y)
         divB = sp.diff(B[0], X) + sp.diff(B[1], Y)
-        wxB = wconst[0] * B[1] - wconst[1] * B[0]
+        wxB = 0 if picard else wconst[0] * B[1] - wconst[1] * B[0]
         fE = [E - curlB / Rem + wxB]
         vcurlE = [sp.diff(E, Y), -sp.diff(E, X)]
-        fB = [vcurlE[k] - sp.diff(divB, v) / Rem for k, v in enumerate((X, Y))]
+        fB = [vcurlE[k] - sp.diff(divB, v) / Rem + (B[k] / dt if dt > 0 else 0) for k, v in enumerate((X, Y))]
         exact = [E] + B
     else:
         E = [sp.sin(pi * Y) * sp.sin(pi * Z), sp.sin(pi * X) * sp.sin(pi * Z), sp.sin(pi * X) * sp.sin(pi * Y)]
@@ -42,13 +43,16 @@ def eb_fields(dim, Rem, wconst, div_free_B=False):
         divB = sum(sp.diff(B[k], v) for k, v in enumerate((X, Y, Z)))
         w = wconst
         wxB = [w[1] * B[2] - w[2] * B[1], w[2] * B[0] - w[0] * B[2], w[0] * B[1] - w[1] * B[0]]
+        if picard:
+            wxB = [0, 0, 0]
         fE = [E[k] - cB[k] / Rem + wxB[k] for k in range(3)]
-        fB = [cE[k] - sp.diff(divB, v) / Rem for k, v in enumerate((X, Y, Z))]
+        fB = [cE[k] - sp.diff(divB, v) / Rem + (B[k] / dt if dt > 0 else 0) for k, v in enumerate((X, Y, Z))]
         exact = E + B
     return [_lamb(e, dim) for e in fE + fB], [_lamb(e, dim) for e in exact]
 
 
-def vel_fields(dim, Re, wconst):
+def vel_fields(dim, Re, wconst, dt=0.0):
+    """dt > 0: transient source + u/dt (NEXT-4)."""
     pi = sp.pi
     if dim == 2:
         psi = sp.sin(pi * X) ** 2 * sp.sin(pi * Y) ** 2
@@ -65,7 +69,7 @@ def vel_fields(dim, Re, wconst):
     for k in range(dim):
         lap = sum(sp.diff(u[k], v, 2) for v in vs)
         adv = sum(wconst[j] * sp.diff(u[k], vs[j]) for j in range(dim))
-        f.append(-lap / Re + adv)
+        f.append(-lap / Re + adv + (u[k] / dt if dt > 0 else 0))
     return [_lamb(e, dim) for e in f], [_lamb(e, dim) for e in u]
 
 

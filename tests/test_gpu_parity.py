@@ -19,13 +19,21 @@ pytestmark = pytest.mark.gpu
 
 TOL = 1e-10
 CASES = [("c1", None, None, 0), ("c1", None, None, 1), ("c1", None, None, 2), ("c2", None, None, 0),
-         ("c3", 64, 4, 0), ("c4", 16, 3, 0), ("c5", 6, 2, 0), ("c5", 8, 2, 1)]
+         ("c3", 64, 4, 0), ("c4", 16, 3, 0), ("c5", 6, 2, 0), ("c5", 8, 2, 1),
+         ("c4-transient-picard", 8, 2, 0), ("c5-transient", 6, 2, 2)]
 
 
 def _setup(oracle_mod, name, N, L, seed):
     import torch
     from paper_2104_14855_b200 import mhdp, workloads
+    import dataclasses
+    variant = {}
+    if name.endswith("-transient-picard"):
+        name, variant = name.split("-")[0], dict(dt=0.05, picard=1)     # NEXT-4
+    elif name.endswith("-transient"):
+        name, variant = name.split("-")[0], dict(dt=0.01)
     cfg = workloads.CONFIGS[name] if N is None else workloads.small(name, N, L)
+    cfg = dataclasses.replace(cfg, **variant)
     ctx = mhdp.Context(0, torch.cuda.current_stream().cuda_stream)
     w0, _, _ = workloads.draw(cfg, 1, seed)
     ctx.assemble(cfg, w0)

@@ -72,6 +72,28 @@ def test_operator_bitexact_vs_exact_oracle(mh, oracle_mod, name, N, L):
         assert diff.size == 0, f"level {l}: {diff.size} entries differ, e.g. {A.v[diff[:3]]} vs {v[diff[:3]]}"
 
 
+VARIANTS = [("c1", dict(dt=0.01)), ("c3", dict(dt=0.01)), ("c4", dict(picard=1)), ("c5", dict(dt=0.5)),
+            ("c4", dict(dt=0.05, picard=1))]
+
+
+@pytest.mark.parametrize("name,kw", VARIANTS, ids=[f"{c}-{'-'.join(f'{k}{v}' for k, v in kw.items())}" for c, kw in VARIANTS])
+def test_next4_variants_bitexact(mh, oracle_mod, name, kw):
+    """NEXT-4: transient (eta = 1, (1/dt) mass terms) and Picard (delta = 0) operators
+    assembled by the library equal the exact oracle's bit for bit."""
+    import dataclasses
+    from paper_2104_14855_b200 import workloads
+    cfg = dataclasses.replace(workloads.small(name, 4, 2), **kw)
+    w, _, _ = workloads.draw(cfg, 1, seed=8)
+    orc = oracle_mod.Oracle(cfg, w, exact=True)
+    ctx = mh.Context(-1)
+    ctx.assemble(cfg, w)
+    for l in range(2):
+        A = orc.csr(l)
+        rp, ci, v = ctx.csr(l)
+        assert np.array_equal(A.rp, rp) and np.array_equal(A.ci, ci)
+        assert np.array_equal(A.v.view(np.uint64), v.view(np.uint64))
+
+
 def test_gamma_and_curl_entries_bitwise(mh, oracle_mod):
     """The div-div blocks follow the exact single-rounded form of reading R-gamma on both
     sides: on the E-B block the B-B entries (C only) agree bit for bit."""

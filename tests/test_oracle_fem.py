@@ -188,10 +188,12 @@ def test_velocity_advection_coercive(oracle_mod, name):
     assert np.abs(D).max() > 0
 
 
-def _rates(oracle_mod, dim, blk, Ns, **kw):
+def _rates(oracle_mod, dim, blk, Ns, dt=0.0, picard=0, **kw):
     wc = [1.0, 0.5] if dim == 2 else [1.0, 0.5, -0.3]
-    base = dataclasses.replace(CONFIGS["c1" if dim == 2 else "c4"], block=blk, Re=1.0, Rem=1.0, gamma=1.0, levels=1)
-    fs, ex = mms.eb_fields(dim, 1.0, wc, **kw) if blk == "eb" else mms.vel_fields(dim, 1.0, wc)
+    base = dataclasses.replace(CONFIGS["c1" if dim == 2 else "c4"], block=blk, Re=1.0, Rem=1.0, gamma=1.0, levels=1,
+                               dt=dt, picard=picard)
+    fs, ex = (mms.eb_fields(dim, 1.0, wc, dt=dt, picard=picard, **kw) if blk == "eb"
+              else mms.vel_fields(dim, 1.0, wc, dt=dt))
     errs = []
     for N in Ns:
         cfg = dataclasses.replace(base, N=N)
@@ -227,3 +229,35 @@ def test_mms_rates_3d_velocity(oracle_mod):
     and 1.88 at 12->16 offline); the pin requires a clearly super-linear rate."""
     r = _rates(oracle_mod, 3, "vel", [4, 8])
     assert r.min() >= 1.5
+
+
+def test_mms_rates_transient_and_picard_2d_eb(oracle_mod):
+    """NEXT-4: transient (eta = 1, dt = 0.05: the (1/dt)(B, C) mass term) and Picard
+    (delta = 0: no w x B term) E-B variants keep the rates of the stationary Newton block;
+    a mis-scaled or missing term would stall the convergence to the exact fields."""
+    r = _rates(oracle_mod, 2, "eb", [16, 32], dt=0.05)
+    assert r[0] >= 1.9 and min(r[1:]) >= 0.95
+    r = _rates(oracle_mod, 2, "eb", [16, 32], picard=1)
+    assert r[0] >= 1.9 and min(r[1:]) >= 0.95
+
+
+def test_mms_rates_transient_velocity(oracle_mod):
+    """NEXT-4: transient velocity block ((1/dt)(u, v) BDM mass, dt = 0.05): rate 2 in 2D."""
+    r = _rates(oracle_mod, 2, "vel", [16, 32], dt=0.05)
+    assert r.min() >= 1.9
+
+
+def test_mass_terms_symmetric_positive(oracle_mod):
+    """The transient operators differ from the stationary ones by (1/dt) times an SPD
+    mass matrix (RT on the B-B block, BDM on the velocity block)."""
+    from paper_2104_14855_b200 import workloads
+    for name in ("c1", "c3", "c4", "c5"):
+        cfg = workloads.small(name, 2, 1)
+        w, _, _ = workloads.draw(cfg, 1, 0)
+        A0 = oracle_mod.Oracle(cfg, w).csr().to_scipy().toarray()
+        A1 = oracle_mod.Oracle(dataclasses.replace(cfg, dt=0.25), w).csr().to_scipy().toarray()
+        Mm = (A1 - A0) * 0.25
+        assert np.allclose(Mm, Mm.T, atol=1e-12 * np.abs(Mm).max())
+        ev = np.linalg.eigvalsh(0.5 * (Mm + Mm.T))
+        nz = np.abs(Mm).sum(axis=1) > 0
+        assert ev.max() > 0 and np.linalg.eigvalsh(Mm[np.ix_(nz, nz)]).min() > 0
