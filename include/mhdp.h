@@ -103,6 +103,13 @@ void        mhdp_destroy(mhdp_ctx *ctx);
  * Errors: EINVAL (dims, divisibility, non-positive Re/Rem/gamma, mu_stab != 0, NULL). */
 mhdp_status mhdp_assemble(mhdp_ctx *ctx, mhdp_block block, const mhdp_mesh *mesh,
                           const mhdp_params *params, const double *w_vertex_host);
+/* As mhdp_assemble, plus the linearised Lorentz force of the velocity block (NEXT-4,
+ * Table 1 row D): S (B^n x (u x B^n), v) = S (u x B^n, v x B^n), with B^n given
+ * like the advecting field by its potential at the finest vertices (bn_vertex_host, same
+ * layout as w_vertex_host; NULL = no Lorentz term).  EINVAL for the E-B block.         */
+mhdp_status mhdp_assemble_lorentz(mhdp_ctx *ctx, mhdp_block block, const mhdp_mesh *mesh,
+                                  const mhdp_params *params, const double *w_vertex_host,
+                                  const double *bn_vertex_host);
 
 /* Algebraic entry (the PCPATCH-style interface): install level `level` of an
  * n_levels hierarchy from caller data instead of mhdp_assemble.  Host arrays, copied:

@@ -28,6 +28,7 @@ typedef struct {
     int **perm;
     OCsr P, PT;       /* to the next coarser level (l >= 1) */
     double *w;        /* potential of the advecting field on this level's vertices (R-w) */
+    double *bn;       /* potential of B^n on this level's vertices (NEXT-4), or NULL */
 } OLevel;
 
 typedef struct {
@@ -47,7 +48,7 @@ static void level_free(OLevel *L) {
         free(L->lu); free(L->perm);
     }
     oc_free(&L->A); oc_free(&L->P); oc_free(&L->PT);
-    opt_free(&L->pt); os_free(&L->s); om_free(&L->m); free(L->w);
+    opt_free(&L->pt); os_free(&L->s); om_free(&L->m); free(L->w); free(L->bn);
 }
 
 void orc_destroy(OCtx *c) {
@@ -62,7 +63,7 @@ void orc_destroy(OCtx *c) {
  * cmask_fine: NULL, or a finest-level cell mask (only then: assemble the finest
  * level restricted to it and build no coarser level; used for bounded samples). */
 OCtx *orc_create_masked(int block, int dim, int N, int nlev, const double *dparams, const int *iparams,
-                        const double *w_fine, const unsigned char *cmask_fine) {
+                        const double *w_fine, const unsigned char *cmask_fine, const double *bn_fine) {
     if ((block != ORC_EB && block != ORC_VEL) || (dim != 2 && dim != 3) || nlev < 1 || N < 1) return NULL;
     if (N % (1 << (nlev - 1))) return NULL;
     OCtx *c = calloc(1, sizeof(OCtx));
@@ -86,6 +87,15 @@ OCtx *orc_create_masked(int block, int dim, int N, int nlev, const double *dpara
             i64 fv = dim == 2 ? i + (i64)(N + 1) * j : i + (i64)(N + 1) * (j + (i64)(N + 1) * k);
             for (int t = 0; t < nc; t++) L->w[v * nc + t] = w_fine[fv * nc + t];
         }
+        if (bn_fine) {      /* B^n potential, injected like w (NEXT-4) */
+            L->bn = malloc(sizeof(double) * nc * L->m.nv);
+            for (i64 v = 0; v < L->m.nv; v++) {
+                int i = L->m.lat[3 * v] * step, j = L->m.lat[3 * v + 1] * step, k = L->m.lat[3 * v + 2] * step;
+                i64 fv = dim == 2 ? i + (i64)(N + 1) * j : i + (i64)(N + 1) * (j + (i64)(N + 1) * k);
+                for (int t = 0; t < nc; t++) L->bn[v * nc + t] = bn_fine[fv * nc + t];
+            }
+        }
+        c->p.bn = L->bn;
         oa_assemble_masked(&L->A, &L->m, &L->s, &c->p, L->w, l == nlev - 1 ? cmask_fine : NULL);
         opt_build(&L->pt, &L->m, &L->s);
     }
@@ -99,7 +109,7 @@ OCtx *orc_create_masked(int block, int dim, int N, int nlev, const double *dpara
 
 OCtx *orc_create(int block, int dim, int N, int nlev, const double *dparams, const int *iparams,
                  const double *w_fine) {
-    return orc_create_masked(block, dim, N, nlev, dparams, iparams, w_fine, NULL);
+    return orc_create_masked(block, dim, N, nlev, dparams, iparams, w_fine, NULL, NULL);
 }
 
 /* out: n, nnz, npatch, sum_n, sum_n2, nE, nv, nc, ne, nf, P nnz */

@@ -587,9 +587,10 @@ static void assemble_vel(OCsr *A, Accum *S, signed char *cnt, const OMesh *m, co
         real eps[12][3][3];
         for (int a = 0; a < nb; a++) sym_grad(&F[a], eps[a]);
         double pot[4][3];
-        real wx[3];
+        real wx[3], bx[3] = {0, 0, 0};
         cell_pot(m, c, w, pot);
         cell_wind(&K, pot, wx);      /* constant on K, div w_h = 0 */
+        if (p->bn) { double bp[4][3]; cell_pot(m, c, p->bn, bp); cell_wind(&K, bp, bx); }   /* B^n, NEXT-4 */
         real loc[12 * 12] = {0};
         int nq = cell_rule(&K, 3, xq, wq);
         for (int t = 0; t < nq; t++) {
@@ -607,7 +608,13 @@ static void assemble_vel(OCsr *A, Accum *S, signed char *cnt, const OMesh *m, co
                     real ee = 0;
                     for (int l = 0; l < 3; l++) for (int k = 0; k < 3; k++) ee += eps[j][l][k] * eps[i][l][k];
                     real mass = p->dt > 0 ? dot3(fv[j], fv[i]) / p->dt : (real)0;   /* (eta/dt)(u, v) */
-                    loc[i * 12 + j] += wq[t] * (nu2 * ee - dot3(fv[j], dvw) + mass);
+                    real lor = 0;                                 /* S (u x B^n, v x B^n), NEXT-4 */
+                    if (p->bn) {
+                        if (d == 2) lor = (fv[j][0] * bx[1] - fv[j][1] * bx[0]) * (fv[i][0] * bx[1] - fv[i][1] * bx[0]);
+                        else { real cj[3], ci[3]; cross3(fv[j], bx, cj); cross3(fv[i], bx, ci); lor = dot3(cj, ci); }
+                        lor *= p->S;
+                    }
+                    loc[i * 12 + j] += wq[t] * (nu2 * ee - dot3(fv[j], dvw) + mass + lor);
                 }
             }
         }

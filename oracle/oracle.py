@@ -48,7 +48,7 @@ def lib(exact: bool = False):
         L.orc_create.restype = vp
         L.orc_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, ip, dp]
         L.orc_create_masked.restype = vp
-        L.orc_create_masked.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, ip, dp, C.c_void_p]
+        L.orc_create_masked.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, ip, dp, C.c_void_p, C.c_void_p]
         L.orc_destroy.argtypes = [vp]
         L.orc_level_info.argtypes = [vp, C.c_int, i64p]
         L.orc_export_csr.argtypes = [vp, C.c_int, i64p, ip, dp]
@@ -128,7 +128,7 @@ class Csr:
 class Oracle:
     """Hierarchy for one configuration (see paper_2104_14855_b200.workloads.Config)."""
 
-    def __init__(self, cfg, w, nlev=None, N=None, cmask=None, exact=False):
+    def __init__(self, cfg, w, nlev=None, N=None, cmask=None, exact=False, bn=None):
         """exact=True: element integrals in __float128 (reading R-exact): every operator
         entry is the fp64 value nearest to the exact discrete bilinear form."""
         self._L = L = lib(exact)
@@ -141,12 +141,11 @@ class Oracle:
                        getattr(cfg, "dt", 0.0)], dtype=np.float64)
         ip = np.array([cfg.nu, cfg.nu, int(getattr(cfg, "picard", 0))], dtype=np.int32)
         self._w = np.ascontiguousarray(w, dtype=np.float64)
-        if cmask is None:
-            self.h = L.orc_create(cfg.block_id, cfg.dim, N, self.nlev, _d(dp), _i(ip), _d(self._w))
-        else:
-            self._mask = np.ascontiguousarray(cmask, dtype=np.uint8)
-            self.h = L.orc_create_masked(cfg.block_id, cfg.dim, N, self.nlev, _d(dp), _i(ip), _d(self._w),
-                                         self._mask.ctypes.data)
+        self._bn = None if bn is None else np.ascontiguousarray(bn, dtype=np.float64)
+        self._mask = None if cmask is None else np.ascontiguousarray(cmask, dtype=np.uint8)
+        self.h = L.orc_create_masked(cfg.block_id, cfg.dim, N, self.nlev, _d(dp), _i(ip), _d(self._w),
+                                     None if self._mask is None else self._mask.ctypes.data,
+                                     None if self._bn is None else self._bn.ctypes.data)
         if not self.h:
             raise ValueError("oracle: invalid configuration")
         self._info = {}

@@ -80,6 +80,8 @@ typedef struct {
     int nu_pre, nu_post;
     double dt;     /* NEXT-4: > 0 -> transient (eta = 1): (1/dt) mass terms */
     int picard;    /* NEXT-4: 1 -> Picard linearisation (delta = 0): no G~ term    */
+    const double *bn;  /* NEXT-4: potential of B^n at this level's vertices (as w, R-w), or NULL:
+                          velocity block + S (B^n x (u x B^n), v) = S (u x B^n, v x B^n) */
 } OParams;
 
 /* ---------------- operator assembly ---------------- */

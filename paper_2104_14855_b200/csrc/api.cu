@@ -501,8 +501,9 @@ static mhdp_status check_params(mhdp_ctx *ctx, const mhdp_params *pr) {
     return MHDP_OK;
 }
 
-mhdp_status mhdp_assemble(mhdp_ctx *ctx, mhdp_block block, const mhdp_mesh *mesh, const mhdp_params *params,
-                          const double *w_vertex_host) {
+mhdp_status mhdp_assemble_lorentz(mhdp_ctx *ctx, mhdp_block block, const mhdp_mesh *mesh,
+                                  const mhdp_params *params, const double *w_vertex_host,
+                                  const double *bn_vertex_host) {
     if (!ctx) return MHDP_EINVAL;
     if (!mesh || !w_vertex_host) return fail(ctx, MHDP_EINVAL, "NULL mesh or w_vertex");
     if (block != MHDP_BLOCK_EB && block != MHDP_BLOCK_ALVEL) return fail(ctx, MHDP_EINVAL, "unknown block");
@@ -514,12 +515,20 @@ mhdp_status mhdp_assemble(mhdp_ctx *ctx, mhdp_block block, const mhdp_mesh *mesh
     if (st) return st;
     free_device(ctx);
     ctx->H.clear();
-    std::string e = assemble_hierarchy((int)block, mesh->dim, mesh->n_fine, mesh->n_levels, ctx->p, w_vertex_host, ctx->H);
+    if (bn_vertex_host && block != MHDP_BLOCK_ALVEL)
+        return fail(ctx, MHDP_EINVAL, "the Lorentz term belongs to the velocity block");
+    std::string e = assemble_hierarchy((int)block, mesh->dim, mesh->n_fine, mesh->n_levels, ctx->p, w_vertex_host,
+                                       bn_vertex_host, ctx->H);
     if (!e.empty()) { ctx->H.clear(); ctx->nlev = 0; return fail(ctx, MHDP_EINVAL, e); }
     ctx->nlev = mesh->n_levels;
     ctx->block = (int)block;
     ctx->loaded.assign(ctx->nlev, 1);
     return MHDP_OK;
+}
+
+mhdp_status mhdp_assemble(mhdp_ctx *ctx, mhdp_block block, const mhdp_mesh *mesh, const mhdp_params *params,
+                          const double *w_vertex_host) {
+    return mhdp_assemble_lorentz(ctx, block, mesh, params, w_vertex_host, nullptr);
 }
 
 mhdp_status mhdp_begin_levels(mhdp_ctx *ctx, int n_levels, const mhdp_params *params) {

@@ -660,14 +660,17 @@ struct CellVel {
     GeoT<dd> G;
     VelBasisT<dd> B;
     dd w[3];
+    dd bn[3];          // B^n on the cell (NEXT-4), zero when absent
     dd eps[12][3][3];
     int gi[12];
 };
 
-void cell_vel(const Mesh &m, const Space &s, i64 c, const double *pot, CellVel &K) {
+void cell_vel(const Mesh &m, const Space &s, i64 c, const double *pot, const double *bpot, CellVel &K) {
     cell_geo(m, c, K.G);
     vel_basis(K.G, K.B);
     cell_wind(K.G, pot, K.w);
+    K.bn[0] = K.bn[1] = K.bn[2] = dd(0.0);
+    if (bpot) cell_wind(K.G, bpot, K.bn);
     const int d = m.dim, nb = d * (d + 1);
     cell_dofs(m, s, c, K.gi);
     for (int k = 0; k < nb; ++k) {
@@ -677,7 +680,7 @@ void cell_vel(const Mesh &m, const Space &s, i64 c, const double *pot, CellVel &
     }
 }
 
-void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *pot, Pattern &P,
+void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *pot, const double *bpot, Pattern &P,
                   std::vector<double> &val) {
     const int d = m.dim, nvc = d + 1, nb = d * nvc;
     // row blocks = free facets; pattern from the cells of the facet and their facet neighbours
@@ -722,7 +725,7 @@ void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *
     // element data of every cell, once
     std::vector<CellVel> cellv(m.nc);
 #pragma omp parallel for schedule(static)
-    for (i64 c = 0; c < m.nc; ++c) cell_vel(m, s, c, pot, cellv[c]);
+    for (i64 c = 0; c < m.nc; ++c) cell_vel(m, s, c, pot, bpot, cellv[c]);
     val.assign(P.rp[s.n], 0.0);
     const dd nu2 = dd(2.0) / dd(p.Re);
     const double Kinv = d == 2 ? 2.0 * m.N * m.N : 6.0 * m.N * m.N * m.N;
@@ -754,6 +757,18 @@ void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *
                     dd term = nu2 * V * ee - dot3(K.B.v[j], K.B.v[i]) * gw * Vn;          // viscous - advection
                     if (p.dt > 0)                                                         // (1/dt)(u, v), NEXT-4
                         term += mass_bary(K.G, K.B.a[j], K.B.a[i]) * dot3(K.B.v[j], K.B.v[i]) / dd(p.dt);
+                    if (bpot) {                                 // S (u x B^n, v x B^n), NEXT-4
+                        dd cj[3], ci[3];
+                        if (d == 2) {
+                            cj[0] = K.B.v[j][0] * K.bn[1] - K.B.v[j][1] * K.bn[0];
+                            ci[0] = K.B.v[i][0] * K.bn[1] - K.B.v[i][1] * K.bn[0];
+                            cj[1] = cj[2] = ci[1] = ci[2] = dd(0.0);
+                        } else {
+                            cross3(K.B.v[j], K.bn, cj);
+                            cross3(K.B.v[i], K.bn, ci);
+                        }
+                        term += dd(p.S) * mass_bary(K.G, K.B.a[j], K.B.a[i]) * dot3(cj, ci);
+                    }
                     add(a, K.gi[j], term);
                 }
             }
@@ -1045,7 +1060,7 @@ void build_prolongation(const Mesh &mf, const Space &sf, const Mesh &mc, const S
 }  // namespace
 
 std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params &p, const double *w,
-                               std::vector<HostLevel> &out) {
+                               const double *bn, std::vector<HostLevel> &out) {
     if ((block != 0 && block != 1) || (dim != 2 && dim != 3) || N < 1 || nlev < 1) return "bad arguments";
     if (N % (1 << (nlev - 1))) return "N not divisible by 2^(nlev-1)";
     out.assign(nlev, HostLevel());
@@ -1058,17 +1073,19 @@ std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params
         build_mesh(m, dim, Nl);
         build_space(spaces[l], m, block);
         // potential on this level: injection of the finest vertex values (R-w)
-        std::vector<double> pot(ncomp * m.nv);
+        std::vector<double> pot(ncomp * m.nv), bpot(bn ? ncomp * m.nv : 0);
         for (i64 v = 0; v < m.nv; ++v) {
             int q[3];
             m.lat(v, q);
             const i64 fv = q[0] * step + (i64)(N + 1) * (q[1] * step + (i64)(N + 1) * (q[2] * step));
             for (int t = 0; t < ncomp; ++t) pot[ncomp * v + t] = w[ncomp * fv + t];
+            if (bn)
+                for (int t = 0; t < ncomp; ++t) bpot[ncomp * v + t] = bn[ncomp * fv + t];
         }
         Pattern P;
         std::vector<double> val;
         if (block == 0) assemble_eb(m, spaces[l], p, pot.data(), P, val);
-        else assemble_vel(m, spaces[l], p, pot.data(), P, val);
+        else assemble_vel(m, spaces[l], p, pot.data(), bn ? bpot.data() : nullptr, P, val);
         HostLevel &H = out[l];
         H.n = spaces[l].n;
         H.rp = std::move(P.rp);

@@ -35,7 +35,9 @@ struct HostLevel {
 // Assemble all levels (0 = coarsest).  block 0 = E-B, 1 = AL velocity.
 // w: potential of the advecting field at the finest vertices (1 or 3 per vertex).
 // Returns "" on success, else an error message.
+// bn: potential of the magnetic field B^n (as w) for the Lorentz term of the velocity block
+// (NEXT-4), or NULL
 std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params &p, const double *w,
-                               std::vector<HostLevel> &out);
+                               const double *bn, std::vector<HostLevel> &out);
 
 }  // namespace mhdp

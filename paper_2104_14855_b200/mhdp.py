@@ -49,7 +49,7 @@ SYMBOLS = ["mhdp_create", "mhdp_destroy", "mhdp_assemble", "mhdp_begin_levels", 
            "mhdp_patch_update", "mhdp_smooth", "mhdp_restrict", "mhdp_prolong_add", "mhdp_coarse_solve",
            "mhdp_vcycle", "mhdp_vcycle_host", "mhdp_smooth_host", "mhdp_gmres", "mhdp_export_csr",
            "mhdp_export_patches", "mhdp_export_prolongation", "mhdp_export_patch_lu", "mhdp_export_slots",
-           "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count", "mhdp_fgmres", "mhdp_dot", "mhdp_set_smoother", "mhdp_vcycle_graphs_active"]
+           "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count", "mhdp_fgmres", "mhdp_dot", "mhdp_set_smoother", "mhdp_vcycle_graphs_active", "mhdp_assemble_lorentz"]
 
 
 def lib():
@@ -63,6 +63,7 @@ def lib():
         sig = {
             "mhdp_create": [C.POINTER(vp), C.c_int, vp],
             "mhdp_assemble": [vp, C.c_int, C.POINTER(Mesh), C.POINTER(Params), dp],
+            "mhdp_assemble_lorentz": [vp, C.c_int, C.POINTER(Mesh), C.POINTER(Params), dp, C.c_void_p],
             "mhdp_begin_levels": [vp, C.c_int, C.POINTER(Params)],
             "mhdp_load_level": [vp, C.c_int, i64, i64p, ip, dp, i64, i64p, ip, i64p, ip, dp],
             "mhdp_setup": [vp],
@@ -165,11 +166,15 @@ class Context:
         return st
 
     # ---- setup ----
-    def assemble(self, cfg, w, N=None, levels=None, smoother="richardson", smoother_its=6):
+    def assemble(self, cfg, w, N=None, levels=None, smoother="richardson", smoother_its=6, bn=None):
+        """bn: potential of B^n for the Lorentz term of the velocity block (NEXT-4), or None."""
         mesh = Mesh(cfg.dim, N if N is not None else cfg.N, levels if levels is not None else cfg.levels)
         self._w = np.ascontiguousarray(w, np.float64)
+        self._bn = None if bn is None else np.ascontiguousarray(bn, np.float64)
         p = make_params(cfg, smoother, smoother_its)
-        return self._chk(self._L.mhdp_assemble(self.h, BLOCK[cfg.block], C.byref(mesh), C.byref(p), _d(self._w)))
+        return self._chk(self._L.mhdp_assemble_lorentz(self.h, BLOCK[cfg.block], C.byref(mesh), C.byref(p),
+                                                       _d(self._w),
+                                                       None if self._bn is None else self._bn.ctypes.data))
 
     def begin_levels(self, n_levels, cfg, smoother="richardson", smoother_its=6):
         p = make_params(cfg, smoother, smoother_its)

@@ -100,3 +100,25 @@ def draw(cfg: Config, n: int, seed: int):
     b = rng.uniform(-1.0, 1.0, n)
     x0 = rng.uniform(-1.0, 1.0, n)
     return w, b, x0
+
+
+def magnetic_potential(cfg: Config, seed: int) -> np.ndarray:
+    """Potential of a synthetic magnetic field B^n at the finest vertices (NEXT-4, the
+    Lorentz term S(B^n x (u x B^n), v) of the velocity block).  Drawn from its own
+    stream Generator(PCG64(seed + 7919)) so that the draws of draw() are unchanged:
+      2D: phi = sum_{k=1,2} c_k sin(k pi x) sin(k pi y), B^n = vcurl phi_h;
+      3D: A = sum_{k=1..3} c_k sin(k pi x) sin(k pi y) sin(k pi z) e_k, B^n = curl A_h;
+    c_k ~ N(0,1).  B^n . n = 0 on the boundary, as the paper's B."""
+    rng = np.random.Generator(np.random.PCG64(seed + 7919))
+    X = vertex_coords(cfg.dim, cfg.N)
+    pi = math.pi
+    if cfg.dim == 2:
+        c = rng.standard_normal(2)
+        x, y = X[:, 0], X[:, 1]
+        return np.ascontiguousarray(sum(c[k - 1] * np.sin(k * pi * x) * np.sin(k * pi * y) for k in (1, 2)))
+    c = rng.standard_normal(3)
+    x, y, z = X[:, 0], X[:, 1], X[:, 2]
+    A = np.zeros((X.shape[0], 3))
+    for k in (1, 2, 3):
+        A[:, k - 1] = c[k - 1] * np.sin(k * pi * x) * np.sin(k * pi * y) * np.sin(k * pi * z)
+    return np.ascontiguousarray(A.ravel())

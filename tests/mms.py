@@ -51,8 +51,8 @@ def eb_fields(dim, Rem, wconst, div_free_B=False, dt=0.0, picard=0):
     return [_lamb(e, dim) for e in fE + fB], [_lamb(e, dim) for e in exact]
 
 
-def vel_fields(dim, Re, wconst, dt=0.0):
-    """dt > 0: transient source + u/dt (NEXT-4)."""
+def vel_fields(dim, Re, wconst, dt=0.0, S=0.0, bconst=None):
+    """dt > 0: transient source + u/dt; bconst: constant B^n, source + S B x (u x B) (NEXT-4)."""
     pi = sp.pi
     if dim == 2:
         psi = sp.sin(pi * X) ** 2 * sp.sin(pi * Y) ** 2
@@ -70,6 +70,15 @@ def vel_fields(dim, Re, wconst, dt=0.0):
         lap = sum(sp.diff(u[k], v, 2) for v in vs)
         adv = sum(wconst[j] * sp.diff(u[k], vs[j]) for j in range(dim))
         f.append(-lap / Re + adv + (u[k] / dt if dt > 0 else 0))
+    if bconst is not None:
+        Bc = bconst
+        if dim == 2:           # u x B = u1 B2 - u2 B1 (scalar); B x s = (B2 s, -B1 s)
+            s = u[0] * Bc[1] - u[1] * Bc[0]
+            lor = [Bc[1] * s, -Bc[0] * s]
+        else:
+            uxb = [u[1] * Bc[2] - u[2] * Bc[1], u[2] * Bc[0] - u[0] * Bc[2], u[0] * Bc[1] - u[1] * Bc[0]]
+            lor = [Bc[1] * uxb[2] - Bc[2] * uxb[1], Bc[2] * uxb[0] - Bc[0] * uxb[2], Bc[0] * uxb[1] - Bc[1] * uxb[0]]
+        f = [f[k] + S * lor[k] for k in range(dim)]
     return [_lamb(e, dim) for e in f], [_lamb(e, dim) for e in u]
 
 

@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-10
 CASES = [("c1", None, None, 0), ("c1", None, None, 1), ("c1", None, None, 2), ("c2", None, None, 0),
          ("c3", 64, 4, 0), ("c4", 16, 3, 0), ("c5", 6, 2, 0), ("c5", 8, 2, 1),
-         ("c4-transient-picard", 8, 2, 0), ("c5-transient", 6, 2, 2)]
+         ("c4-transient-picard", 8, 2, 0), ("c5-transient", 6, 2, 2), ("c5-lorentz", 6, 2, 3)]
 
 
 def _setup(oracle_mod, name, N, L, seed):
@@ -28,20 +28,24 @@ def _setup(oracle_mod, name, N, L, seed):
     from paper_2104_14855_b200 import mhdp, workloads
     import dataclasses
     variant = {}
+    lorentz = name.endswith("-lorentz")
     if name.endswith("-transient-picard"):
         name, variant = name.split("-")[0], dict(dt=0.05, picard=1)     # NEXT-4
     elif name.endswith("-transient"):
         name, variant = name.split("-")[0], dict(dt=0.01)
+    elif lorentz:
+        name, variant = name.split("-")[0], dict(S=1e3, dt=0.1)
     cfg = workloads.CONFIGS[name] if N is None else workloads.small(name, N, L)
     cfg = dataclasses.replace(cfg, **variant)
     ctx = mhdp.Context(0, torch.cuda.current_stream().cuda_stream)
     w0, _, _ = workloads.draw(cfg, 1, seed)
-    ctx.assemble(cfg, w0)
+    bn = workloads.magnetic_potential(cfg, seed) if lorentz else None
+    ctx.assemble(cfg, w0, bn=bn)
     n = ctx.n()
     w, b, x0 = workloads.draw(cfg, n, seed)
     assert np.array_equal(w, w0)
     ctx.setup()
-    orc = oracle_mod.Oracle(cfg, w, exact=True)
+    orc = oracle_mod.Oracle(cfg, w, exact=True, bn=bn)
     assert orc.n() == n
     return cfg, ctx, orc, b, x0
 

@@ -94,6 +94,22 @@ def test_next4_variants_bitexact(mh, oracle_mod, name, kw):
         assert np.array_equal(A.v.view(np.uint64), v.view(np.uint64))
 
 
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_lorentz_variant_bitexact(mh, oracle_mod, name):
+    """NEXT-4 Lorentz term S(u x B^n, v x B^n), transient, S = 1e3: bit-exact."""
+    import dataclasses
+    from paper_2104_14855_b200 import workloads
+    cfg = dataclasses.replace(workloads.small(name, 4, 2), S=1e3, dt=0.1)
+    w, _, _ = workloads.draw(cfg, 1, seed=4)
+    bn = workloads.magnetic_potential(cfg, 4)
+    orc = oracle_mod.Oracle(cfg, w, exact=True, bn=bn)
+    ctx = mh.Context(-1)
+    ctx.assemble(cfg, w, bn=bn)
+    for l in range(2):
+        A = orc.csr(l)
+        assert np.array_equal(A.v.view(np.uint64), ctx.csr(l)[2].view(np.uint64))
+
+
 def test_gamma_and_curl_entries_bitwise(mh, oracle_mod):
     """The div-div blocks follow the exact single-rounded form of reading R-gamma on both
     sides: on the E-B block the B-B entries (C only) agree bit for bit."""

@@ -261,3 +261,36 @@ def test_mass_terms_symmetric_positive(oracle_mod):
         ev = np.linalg.eigvalsh(0.5 * (Mm + Mm.T))
         nz = np.abs(Mm).sum(axis=1) > 0
         assert ev.max() > 0 and np.linalg.eigvalsh(Mm[np.ix_(nz, nz)]).min() > 0
+
+
+def test_mms_rates_lorentz_velocity_2d(oracle_mod):
+    """NEXT-4: the linearised Lorentz force S(B^n x (u x B^n), v) with a constant
+    B^n = (0.7, -0.4) (potential whose discrete field is exactly constant) and S = 50: the
+    BDM1 velocity still converges at rate 2, so the term is consistent and correctly
+    scaled."""
+    wc, bc, S = [1.0, 0.5], [0.7, -0.4], 50.0
+    base = dataclasses.replace(CONFIGS["c3"], Re=1.0, gamma=1.0, S=S, levels=1)
+    fs, ex = mms.vel_fields(2, 1.0, wc, S=S, bconst=bc)
+    errs = []
+    for N in (16, 32):
+        cfg = dataclasses.replace(base, N=N)
+        o = oracle_mod.Oracle(cfg, mms.constant_wind_potential(2, N, wc), bn=mms.constant_wind_potential(2, N, bc))
+        errs.append(mms.solve_and_error(o, fs, ex))
+    errs = np.array(errs)
+    assert (np.log(errs[0] / errs[1]) / np.log(2)).min() >= 1.9
+
+
+def test_lorentz_term_symmetric_psd_and_linear_in_S(oracle_mod):
+    """D = S (u x B^n, v x B^n) is symmetric positive semi-definite and linear in S."""
+    from paper_2104_14855_b200 import workloads
+    for name in ("c3", "c5"):
+        cfg = workloads.small(name, 2, 1)
+        w, _, _ = workloads.draw(cfg, 1, 0)
+        bn = workloads.magnetic_potential(cfg, 0)
+        A0 = oracle_mod.Oracle(cfg, w).csr().to_scipy().toarray()
+        D1 = oracle_mod.Oracle(dataclasses.replace(cfg, S=1.0), w, bn=bn).csr().to_scipy().toarray() - A0
+        D3 = oracle_mod.Oracle(dataclasses.replace(cfg, S=3.0), w, bn=bn).csr().to_scipy().toarray() - A0
+        assert np.allclose(D1, D1.T, atol=1e-12 * np.abs(D1).max())
+        assert np.linalg.eigvalsh(0.5 * (D1 + D1.T)).min() >= -1e-10 * np.abs(D1).max()
+        assert np.allclose(D3, 3 * D1, rtol=1e-12, atol=1e-12 * np.abs(D3).max())
+        assert np.abs(D1).max() > 0
