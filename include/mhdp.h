@@ -209,6 +209,34 @@ mhdp_status mhdp_last_error(const mhdp_ctx *ctx, char *buf, int len, long long *
 /* Number of kernels this context has launched since creation (bench gpu_launches).    */
 long long   mhdp_launch_count(const mhdp_ctx *ctx);
 
+/* ---- NEXT-3: the coupled Newton system and the paper's outer solver ----------------- */
+/* The 4x4 linearised system (Table 1) over x = [u | p | E | B]
+ * (velocity BDM1 free DoFs, pressure DG0 one per cell in cell order, E and B in the E-B
+ * numbering) on the finest mesh: [[F+D, B^T, J, J~+D~1+D~2], [B, 0, 0, 0],
+ * [G, 0, M_E, G~ - A/Rem], [0, 0, A^T, C]] with u^n = the advecting field, B^n given by
+ * its potential (bn_vertex_host, may be NULL: B^n = 0) and E^n = 0 (so J~ = 0; reading
+ * R-coupled).  The object owns both multigrid hierarchies (velocity and E-B).
+ * cuda_device = -1: host-only (assembly and export).                                    */
+typedef struct mhdp_coupled mhdp_coupled;
+mhdp_status mhdp_coupled_create(mhdp_coupled **out, int cuda_device, void *cuda_stream,
+                                const mhdp_mesh *mesh, const mhdp_params *params,
+                                const double *w_vertex_host, const double *bn_vertex_host);
+void        mhdp_coupled_destroy(mhdp_coupled *c);
+/* out[5] = n_u, n_p, n_E, n_B, nnz of the coupled operator                             */
+mhdp_status mhdp_coupled_sizes(const mhdp_coupled *c, long long *out);
+mhdp_status mhdp_coupled_export_csr(const mhdp_coupled *c, long long *rowptr, int *col, double *val);
+/* y = A x (device vectors of length n_u + n_p + n_E + n_B)                              */
+mhdp_status mhdp_coupled_apply(mhdp_coupled *c, const double *x_dev, double *y_dev);
+/* y = P r, the block upper-triangular preconditioner: two FGMRES iterations
+ * on the E-B block with its V-cycle, z_u = r_u - K y_EB, two FGMRES iterations on the
+ * (u,p) block preconditioned by y_p = -(1/Re+gamma) M_p^-1 s_p, y_u = V_u(s_u - B^T y_p) */
+mhdp_status mhdp_coupled_precondition(mhdp_coupled *c, const double *r_dev, double *y_dev);
+/* outermost flexible GMRES with P, x0 = 0, stop at max(rtol|b|, atol)   */
+mhdp_status mhdp_coupled_fgmres(mhdp_coupled *c, const double *b_dev, double *x_dev, double rtol,
+                                double atol, int maxit, int *its_out, double *relres_out);
+mhdp_status mhdp_coupled_set_smoother(mhdp_coupled *c, int smoother, int smoother_its);
+mhdp_status mhdp_coupled_last_error(const mhdp_coupled *c, char *buf, int len);
+
 #ifdef __cplusplus
 }
 #endif

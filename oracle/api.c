@@ -686,3 +686,208 @@ double orc_dot(const double *a, const double *b, i64 n) { return od_dot(a, b, n)
 int orc_gmres_smooth(OCtx *c, int l, int m, int x_is_zero, const double *b, double *x) {
     return gmres_smooth(c, l, m, x_is_zero, b, x);
 }
+
+/* ===================================================================================
+ * NEXT-3: the paper's outer solver.  FGMRES on the Newton
+ * system [[F+D, B^T, J, J~+D~1+D~2], [B, 0, 0, 0], [G, 0, M_E, G~-A/Rem],
+ * [0, 0, A^T, C]] with the block upper-triangular preconditioner
+ *   P = [[I, -M~^-1 K], [0, I]] diag(M~^-1, S~^-1),   S~ = the E-B block,
+ * M~^-1 = two iterations of FGMRES on the (u,p) block preconditioned by the
+ * hydrodynamic block preconditioner: y_p = -(1/Re + gamma) M_p^-1 s_p,
+ * y_u = V_u(s_u - B^T y_p);  S~^-1 = two iterations of FGMRES on the E-B block with the
+ * E-B V-cycle.  Readings: R-coupled (E^n = 0, so J~ = 0; u^n = w_h, B^n from its
+ * potential), R-outer (orders of the sums, inner FGMRES(2) exactly 2 iterations).
+ * =================================================================================== */
+typedef struct {
+    OCtx *vel, *eb;
+    OCsr A;          /* coupled operator over [u | p | E | B]                     */
+    OCsr Mup;        /* rows/cols (u, p)                                          */
+    OCsr K;          /* u rows x [E | B] columns: [J | J~ + D~1 + D~2]            */
+    OCsr Bt;         /* u rows x p columns                                        */
+    i64 nu, np, nE, nB, n;
+    double cS, Kinv; /* -(1/Re + gamma), 1/|K|                                    */
+} OCoupled;
+
+static void csr_chain(const OCsr *A, const double *x, double *y) {
+    for (i64 i = 0; i < A->n; i++) {
+        double s = 0.0;
+        for (i64 t = A->rp[i]; t < A->rp[i + 1]; t++) s = fma(A->v[t], x[A->ci[t]], s);
+        y[i] = s;
+    }
+}
+
+/* append row r of B (columns shifted by `shift`) to the CSR under construction */
+typedef struct { i64 *rp; int *ci; double *v; i64 used, cap, rows; } Builder;
+static void b_push(Builder *b, const OCsr *B, i64 r, i64 shift) {
+    for (i64 t = B->rp[r]; t < B->rp[r + 1]; t++) {
+        if (b->used == b->cap) { b->cap *= 2; b->ci = realloc(b->ci, sizeof(int) * b->cap); b->v = realloc(b->v, sizeof(double) * b->cap); }
+        b->ci[b->used] = (int)(B->ci[t] + shift); b->v[b->used] = B->v[t]; b->used++;
+    }
+}
+static void b_endrow(Builder *b) { b->rp[++b->rows] = b->used; }
+static void b_init(Builder *b, i64 nrows) {
+    b->rp = malloc(sizeof(i64) * (nrows + 1)); b->rp[0] = 0; b->rows = 0;
+    b->cap = 1024; b->used = 0; b->ci = malloc(sizeof(int) * b->cap); b->v = malloc(sizeof(double) * b->cap);
+}
+static void b_done(Builder *b, OCsr *A) { A->n = b->rows; A->nnz = b->used; A->rp = b->rp; A->ci = b->ci; A->v = b->v; }
+
+void orc_coupled_destroy(OCoupled *c) {
+    if (!c) return;
+    orc_destroy(c->vel); orc_destroy(c->eb);
+    oc_free(&c->A); oc_free(&c->Mup); oc_free(&c->K); oc_free(&c->Bt);
+    free(c);
+}
+
+OCoupled *orc_coupled_create(int dim, int N, int nlev, const double *dparams, const int *iparams, const double *w,
+                             const double *bn) {
+    OCoupled *c = calloc(1, sizeof(OCoupled));
+    c->vel = orc_create_masked(ORC_VEL, dim, N, nlev, dparams, iparams, w, NULL, bn);
+    c->eb = orc_create_masked(ORC_EB, dim, N, nlev, dparams, iparams, w, NULL, bn);
+    if (!c->vel || !c->eb) { orc_coupled_destroy(c); return NULL; }
+    int top = nlev - 1;
+    OLevel *Lv = &c->vel->lv[top], *Le = &c->eb->lv[top];
+    OParams p = c->vel->p;
+    p.bn = Lv->bn;
+    OCsr J, Dt, G, B;
+    double *fu = calloc((size_t)Lv->A.n, sizeof(double)), *fE = calloc((size_t)Le->A.n, sizeof(double));
+    for (i64 i = 0; i < Lv->A.n; i++)
+        for (i64 t = Lv->A.rp[i]; t < Lv->A.rp[i + 1]; t++) if (fabs(Lv->A.v[t]) > fu[i]) fu[i] = fabs(Lv->A.v[t]);
+    for (i64 i = 0; i < Le->A.n; i++)
+        for (i64 t = Le->A.rp[i]; t < Le->A.rp[i + 1]; t++) if (fabs(Le->A.v[t]) > fE[i]) fE[i] = fabs(Le->A.v[t]);
+    oa_assemble_coupling(&c->Bt, &J, &Dt, &G, &Lv->m, &Lv->s, &Le->s, &p, Lv->w, Lv->bn, fu, fE);
+    free(fu); free(fE);
+    oc_transpose(&B, &c->Bt, Lv->m.nc);
+    for (i64 t = 0; t < B.nnz; t++) B.v[t] = B.v[t];   /* B = (B^T)^T: -(div u, q) */
+    c->nu = Lv->s.n; c->np = Lv->m.nc; c->nE = Le->s.nE; c->nB = Le->s.n - Le->s.nE;
+    c->n = c->nu + c->np + c->nE + c->nB;
+    c->cS = -(1.0 / p.Re + p.gamma);
+    c->Kinv = dim == 2 ? 2.0 * N * N : 6.0 * (double)N * N * N;
+    i64 su = 0, sp = c->nu, sE = c->nu + c->np, sB = sE + c->nE;
+    Builder bA, bM, bK;
+    b_init(&bA, c->n); b_init(&bM, c->nu + c->np); b_init(&bK, c->nu);
+    for (i64 i = 0; i < c->nu; i++) {
+        b_push(&bA, &Lv->A, i, su); b_push(&bA, &c->Bt, i, sp); b_push(&bA, &J, i, sE); b_push(&bA, &Dt, i, sB);
+        b_endrow(&bA);
+        b_push(&bM, &Lv->A, i, 0); b_push(&bM, &c->Bt, i, c->nu); b_endrow(&bM);
+        b_push(&bK, &J, i, 0); b_push(&bK, &Dt, i, c->nE); b_endrow(&bK);
+    }
+    for (i64 q = 0; q < c->np; q++) {
+        b_push(&bA, &B, q, su); b_endrow(&bA);
+        b_push(&bM, &B, q, 0); b_endrow(&bM);
+    }
+    for (i64 e = 0; e < c->nE; e++) { b_push(&bA, &G, e, su); b_push(&bA, &Le->A, e, sE); b_endrow(&bA); }
+    for (i64 k = 0; k < c->nB; k++) { b_push(&bA, &Le->A, c->nE + k, sE); b_endrow(&bA); }
+    b_done(&bA, &c->A); b_done(&bM, &c->Mup); b_done(&bK, &c->K);
+    oc_free(&J); oc_free(&Dt); oc_free(&G); oc_free(&B);
+    return c;
+}
+
+/* generic right-preconditioned flexible GMRES; fixed != 0: exactly m iterations (stop
+ * only at breakdown), else stop when |g_k+1| <= max(rtol |b|, atol).  Returns 0/1/2 as
+ * orc_fgmres; hist may be NULL.                                                      */
+typedef int (*opfn)(void *, const double *, double *);
+static int fgmres_gen(i64 n, opfn A, void *ac, opfn P, void *pc, const double *b, double *x, int m, int fixed,
+                      double rtol, double atol, int *its_out, double *hist) {
+    double beta = sqrt(od_dot(b, b, n));
+    double tol = rtol * beta > atol ? rtol * beta : atol;
+    for (i64 i = 0; i < n; i++) x[i] = 0.0;
+    if (hist) hist[0] = beta;
+    if (its_out) *its_out = 0;
+    if (beta == 0.0 || (!fixed && beta <= tol)) return 0;
+    double *V = malloc(sizeof(double) * n * (m + 1)), *Z = malloc(sizeof(double) * n * m), *w = malloc(sizeof(double) * n);
+    double *H = calloc((size_t)(m + 1) * m, sizeof(double)), *cs = calloc(m, sizeof(double)),
+           *sn = calloc(m, sizeof(double)), *g = calloc(m + 1, sizeof(double)), *y = calloc(m, sizeof(double));
+    for (i64 i = 0; i < n; i++) V[i] = b[i] / beta;
+    g[0] = beta;
+    int k, conv = 0, fail = 0;
+    for (k = 0; k < m; k++) {
+        if (P(pc, V + k * n, Z + k * n)) { fail = 1; break; }
+        A(ac, Z + k * n, w);
+        for (int i = 0; i <= k; i++) {
+            double h = od_dot(w, V + i * n, n);
+            H[i * m + k] = h;
+            for (i64 j = 0; j < n; j++) w[j] = fma(-h, V[i * n + j], w[j]);
+        }
+        double hn = sqrt(od_dot(w, w, n));
+        H[(k + 1) * m + k] = hn;
+        givens_column(H, m, cs, sn, g, k);
+        if (hist) hist[k + 1] = fabs(g[k + 1]);
+        if (!fixed && fabs(g[k + 1]) <= tol) { k++; conv = 1; break; }
+        if (hn == 0.0) { k++; break; }
+        if (k + 1 < m) for (i64 j = 0; j < n; j++) V[(k + 1) * n + j] = w[j] / hn;
+    }
+    if (!fail) {
+        back_substitute(H, m, g, k, y);
+        for (int i = 0; i < k; i++)
+            for (i64 j = 0; j < n; j++) x[j] = fma(y[i], Z[i * n + j], x[j]);
+        if (its_out) *its_out = k;
+    }
+    free(V); free(Z); free(w); free(H); free(cs); free(sn); free(g); free(y);
+    return fail ? 2 : (conv || fixed ? 0 : 1);
+}
+
+static int op_csr(void *a, const double *x, double *y) { csr_chain((const OCsr *)a, x, y); return 0; }
+static int op_eb_vcycle(void *cc, const double *r, double *z) {
+    OCoupled *c = cc;
+    return vcycle(c->eb, c->eb->nlev - 1, r, z);
+}
+static int op_eb_A(void *cc, const double *x, double *y) {
+    OCoupled *c = cc;
+    csr_chain(&c->eb->lv[c->eb->nlev - 1].A, x, y);
+    return 0;
+}
+/* hydrodynamic block preconditioner Q: y_p = (cS s_p) Kinv;  y_u = V_u(s_u - B^T y_p) */
+static int op_hydro(void *cc, const double *s, double *y) {
+    OCoupled *c = cc;
+    double *yp = y + c->nu, *t = malloc(sizeof(double) * c->nu);
+    for (i64 q = 0; q < c->np; q++) yp[q] = (c->cS * s[c->nu + q]) * c->Kinv;
+    for (i64 i = 0; i < c->nu; i++) {
+        double acc = 0.0;
+        for (i64 k = c->Bt.rp[i]; k < c->Bt.rp[i + 1]; k++) acc = fma(c->Bt.v[k], yp[c->Bt.ci[k]], acc);
+        t[i] = s[i] - acc;
+    }
+    int st = vcycle(c->vel, c->vel->nlev - 1, t, y);
+    free(t);
+    return st;
+}
+static int op_Mup(void *cc, const double *x, double *y) { csr_chain(&((OCoupled *)cc)->Mup, x, y); return 0; }
+
+/* the block upper-triangular preconditioner (R-outer) */
+int orc_coupled_precondition(OCoupled *c, const double *r, double *y) {
+    i64 nup = c->nu + c->np, neb = c->nE + c->nB;
+    const double *rEB = r + nup;
+    double *yEB = y + nup;
+    if (fgmres_gen(neb, op_eb_A, c, op_eb_vcycle, c, rEB, yEB, 2, 1, 0, 0, NULL, NULL)) return 1;
+    double *z = malloc(sizeof(double) * nup);
+    for (i64 i = 0; i < c->nu; i++) {
+        double acc = 0.0;
+        for (i64 k = c->K.rp[i]; k < c->K.rp[i + 1]; k++) acc = fma(c->K.v[k], yEB[c->K.ci[k]], acc);
+        z[i] = r[i] - acc;
+    }
+    for (i64 q = 0; q < c->np; q++) z[c->nu + q] = r[c->nu + q];
+    int st = fgmres_gen(nup, op_Mup, c, op_hydro, c, z, y, 2, 1, 0, 0, NULL, NULL) ? 1 : 0;
+    free(z);
+    return st;
+}
+static int op_prec(void *cc, const double *r, double *y) { return orc_coupled_precondition((OCoupled *)cc, r, y); }
+
+int orc_coupled_apply(OCoupled *c, const double *x, double *y) { csr_chain(&c->A, x, y); return 0; }
+
+int orc_coupled_fgmres(OCoupled *c, const double *b, double *x, double rtol, double atol, int maxit, int *its,
+                       double *hist) {
+    return fgmres_gen(c->n, op_csr, &c->A, op_prec, c, b, x, maxit, 0, rtol, atol, its, hist);
+}
+
+void orc_coupled_sizes(const OCoupled *c, i64 *out) {
+    out[0] = c->nu; out[1] = c->np; out[2] = c->nE; out[3] = c->nB; out[4] = c->A.nnz;
+}
+int orc_coupled_export(const OCoupled *c, i64 *rp, int *ci, double *v) {
+    memcpy(rp, c->A.rp, sizeof(i64) * (c->n + 1));
+    memcpy(ci, c->A.ci, sizeof(int) * c->A.nnz);
+    memcpy(v, c->A.v, sizeof(double) * c->A.nnz);
+    return 0;
+}
+void orc_coupled_set_smoother(OCoupled *c, int kind, int its) {
+    orc_set_smoother(c->vel, kind, its);
+    orc_set_smoother(c->eb, kind, its);
+}

@@ -455,9 +455,9 @@ static double grid_round(double hi, double lo, int E) {
     return v == 0 ? 0.0 : v;      /* exact cancellation: +0 */
 }
 
-static void finish(OCsr *A, const Accum *S) {
+static void finish_floor(OCsr *A, const Accum *S, const double *floor) {
     for (i64 i = 0; i < A->n; i++) {
-        double mx = 0;
+        double mx = floor ? floor[i] : 0;
         for (i64 t = A->rp[i]; t < A->rp[i + 1]; t++) {
             double h = (double)S->acc[t];
             if (fabs(h) > mx) mx = fabs(h);
@@ -471,6 +471,8 @@ static void finish(OCsr *A, const Accum *S) {
         }
     }
 }
+
+static void finish(OCsr *A, const Accum *S) { finish_floor(A, S, NULL); }
 
 /* ------------------------------------------------------------------------- */
 /* E-B block  (Table 1)                       */
@@ -1010,4 +1012,166 @@ double oa_duality_error(const OMesh *m, const OSpace *s) {
         }
     }
     return worst;
+}
+
+/* ------------------------------------------------------------------------- */
+/* NEXT-3: coupling blocks of the linearised 4x4 system (Table 1   */
+/* P:253-280) between the velocity space (BDM1, u), the pressure (DG0, one    */
+/* indicator per cell, cell order) and the E-B spaces, on one mesh.           */
+/*   Bt_{i,q} = -(q, div v_i)                    (u rows, p columns)          */
+/*   J_{i,e}  = S (B^n x E_e, v_i)               (u rows, E columns)          */
+/*   Dt_{i,k} = S (B_k x (u^n x B^n), v_i) + S (B^n x (u^n x B_k), v_i)       */
+/*              (D~1 + D~2; J~ = S (B x E^n, v) vanishes: E^n = 0, R-coupled) */
+/*   G_{e,i}  = (v_i x B^n, F_e)                 (E rows, u columns)          */
+/* with u^n = w_h and B^n = curl of the B^n potential (both constant per cell,*/
+/* R-w); picard (delta = 0) drops the tilde terms.  2D conventions P:38-53:   */
+/* u x B = u1 B2 - u2 B1 (scalar), B x E = (B2 E, -B1 E).                     */
+/* Cross-space patterns: row and column DoFs couple iff they share a cell.    */
+/* ------------------------------------------------------------------------- */
+static void cross_pattern(OCsr *A, i64 nrows, const OMesh *m, int (*rows_of)(const OMesh *, const void *, i64, int *),
+                          const void *sx, int (*cols_of)(const OMesh *, const void *, i64, int *), const void *sy) {
+    i64 *cnt = calloc((size_t)nrows + 1, sizeof(i64));
+    int rl[32], cl[32];
+    for (i64 c = 0; c < m->nc; c++) {
+        int nr = rows_of(m, sx, c, rl), ncl = cols_of(m, sy, c, cl), k = 0;
+        for (int t = 0; t < ncl; t++) k += cl[t] >= 0;
+        for (int t = 0; t < nr; t++) if (rl[t] >= 0) cnt[rl[t] + 1] += k;
+    }
+    for (i64 r = 0; r < nrows; r++) cnt[r + 1] += cnt[r];
+    int *tmp = malloc(sizeof(int) * (cnt[nrows] ? cnt[nrows] : 1));
+    i64 *fill = calloc((size_t)nrows, sizeof(i64));
+    for (i64 c = 0; c < m->nc; c++) {
+        int nr = rows_of(m, sx, c, rl), ncl = cols_of(m, sy, c, cl);
+        for (int t = 0; t < nr; t++) {
+            if (rl[t] < 0) continue;
+            for (int u = 0; u < ncl; u++) if (cl[u] >= 0) tmp[cnt[rl[t]] + fill[rl[t]]++] = cl[u];
+        }
+    }
+    A->n = nrows;
+    A->rp = malloc(sizeof(i64) * (nrows + 1));
+    A->rp[0] = 0;
+    A->ci = malloc(sizeof(int) * (cnt[nrows] ? cnt[nrows] : 1));
+    i64 used = 0;
+    for (i64 r = 0; r < nrows; r++) {
+        int *b = tmp + cnt[r];
+        i64 k = cnt[r + 1] - cnt[r];
+        qsort(b, (size_t)k, sizeof(int), cmp_int);
+        for (i64 t = 0; t < k; t++) if (t == 0 || b[t] != b[t - 1]) A->ci[used++] = b[t];
+        A->rp[r + 1] = used;
+    }
+    A->nnz = used;
+    A->v = calloc((size_t)(used ? used : 1), sizeof(double));
+    free(tmp); free(cnt); free(fill);
+}
+
+static int vel_dofs_cb(const OMesh *m, const void *s, i64 c, int *out) { return cell_dofs(m, (const OSpace *)s, c, out); }
+static int eb_E_dofs_cb(const OMesh *m, const void *s, i64 c, int *out) {
+    const OSpace *sp = s;
+    int tmp[16], k = cell_dofs(m, sp, c, tmp), nE = m->dim == 2 ? 3 : 6;
+    for (int t = 0; t < nE; t++) out[t] = tmp[t];
+    (void)k;
+    return nE;
+}
+static int eb_B_dofs_cb(const OMesh *m, const void *s, i64 c, int *out) {
+    const OSpace *sp = s;
+    int tmp[16], nE = m->dim == 2 ? 3 : 6;
+    cell_dofs(m, sp, c, tmp);
+    for (int t = 0; t <= m->dim; t++) out[t] = tmp[nE + t] < 0 ? -1 : tmp[nE + t] - (int)sp->nE;   /* B index from 0 */
+    return m->dim + 1;
+}
+static int cell_id_cb(const OMesh *m, const void *s, i64 c, int *out) { (void)m; (void)s; out[0] = (int)c; return 1; }
+
+/* 2D/3D "x" conventions */
+static void xcross(int d, const real *a, const real *b, real *c) {   /* vector x vector */
+    if (d == 2) { c[0] = a[0] * b[1] - a[1] * b[0]; c[1] = c[2] = 0; }   /* scalar in c[0] */
+    else cross3(a, b, c);
+}
+static void xscale(int d, const real *B, const real *s, real *c) {    /* B x (scalar or vector) */
+    if (d == 2) { c[0] = B[1] * s[0]; c[1] = -B[0] * s[0]; c[2] = 0; }
+    else cross3(B, s, c);
+}
+
+int oa_assemble_coupling(OCsr *Bt, OCsr *J, OCsr *Dt, OCsr *G, const OMesh *m, const OSpace *sv, const OSpace *se,
+                         const OParams *p, const double *w, const double *bn, const double *floor_u,
+                         const double *floor_E) {
+    int d = m->dim, nE = d == 2 ? 3 : 6;
+    i64 nB = se->n - se->nE;
+    cross_pattern(Bt, sv->n, m, vel_dofs_cb, sv, cell_id_cb, NULL);
+    cross_pattern(J, sv->n, m, vel_dofs_cb, sv, eb_E_dofs_cb, se);
+    cross_pattern(Dt, sv->n, m, vel_dofs_cb, sv, eb_B_dofs_cb, se);
+    cross_pattern(G, se->nE, m, eb_E_dofs_cb, se, vel_dofs_cb, sv);
+    (void)nB;
+    Accum SB, SJ, SD, SG;
+    SB.acc = calloc((size_t)(Bt->nnz ? Bt->nnz : 1), sizeof(real));
+    SJ.acc = calloc((size_t)(J->nnz ? J->nnz : 1), sizeof(real));
+    SD.acc = calloc((size_t)(Dt->nnz ? Dt->nnz : 1), sizeof(real));
+    SG.acc = calloc((size_t)(G->nnz ? G->nnz : 1), sizeof(real));
+    real xq[64][3], wq[64];
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        Aff F[12], E[6], B[4];
+        double sg[12], sB;
+        int gv[12], gE[6], gB[4], gc = (int)c;
+        int nv = vel_basis(m, sv, c, &K, F, sg, gv);
+        for (int a = 0; a < nE; a++) {
+            if (d == 2) { E[a] = basis_cg1(&K, a); gE[a] = se->vdof[m->cv[c * 3 + a]]; }
+            else {
+                int lv[2];
+                om_edge_local_verts(3, a, lv);
+                E[a] = basis_ned1(&K, lv[0], lv[1]);
+                gE[a] = se->edof[m->ce[c * 6 + a]];
+            }
+        }
+        for (int q = 0; q <= d; q++) {
+            B[q] = basis_rt(&K, q, &sB);
+            int f = se->fdof[om_facet_of_cell(m, c, q)];
+            gB[q] = f < 0 ? -1 : f - (int)se->nE;
+        }
+        double pot[4][3], bp[4][3];
+        real wx[3], bx[3] = {0, 0, 0}, wxb[3];
+        cell_pot(m, c, w, pot);
+        cell_wind(&K, pot, wx);
+        if (bn) { cell_pot(m, c, bn, bp); cell_wind(&K, bp, bx); }
+        xcross(d, wx, bx, wxb);                        /* u^n x B^n (scalar in 2D) */
+        real lB[12] = {0}, lJ[12 * 6] = {0}, lD[12 * 4] = {0}, lG[6 * 12] = {0};
+        int nq = cell_rule(&K, 3, xq, wq);
+        for (int t = 0; t < nq; t++) {
+            real fv[12][3], ev[6][3], bv[4][3];
+            for (int a = 0; a < nv; a++) aff_eval(&F[a], &K, xq[t], fv[a]);
+            for (int a = 0; a < nE; a++) aff_eval(&E[a], &K, xq[t], ev[a]);
+            for (int q = 0; q <= d; q++) aff_eval(&B[q], &K, xq[t], bv[q]);
+            for (int i = 0; i < nv; i++) {
+                real dv = 0;
+                for (int k = 0; k < d; k++) dv += F[i].G[k][k];
+                lB[i] += wq[t] * (-dv);                                   /* -(q, div v) */
+                for (int e = 0; e < nE; e++) {                            /* S (B^n x E, v) */
+                    real c3[3];
+                    xscale(d, bx, ev[e], c3);
+                    lJ[i * 6 + e] += wq[t] * p->S * dot3(c3, fv[i]);
+                    real g3[3];                                          /* (v x B^n, F) */
+                    xcross(d, fv[i], bx, g3);
+                    lG[e * 12 + i] += wq[t] * (d == 2 ? g3[0] * ev[e][0] : dot3(g3, ev[e]));
+                }
+                if (!p->picard)
+                    for (int k = 0; k <= d; k++) {                        /* D~1 + D~2 */
+                        real t1[3], t2[3], ub[3];
+                        xscale(d, bv[k], wxb, t1);                        /* B x (u^n x B^n) */
+                        xcross(d, wx, bv[k], ub);                         /* u^n x B        */
+                        xscale(d, bx, ub, t2);                            /* B^n x (u^n x B) */
+                        lD[i * 4 + k] += wq[t] * p->S * (dot3(t1, fv[i]) + dot3(t2, fv[i]));
+                    }
+            }
+        }
+        scatter(Bt, &SB, gv, nv, &gc, 1, lB, 1);
+        scatter(J, &SJ, gv, nv, gE, nE, lJ, 6);
+        scatter(Dt, &SD, gv, nv, gB, d + 1, lD, 4);
+        scatter(G, &SG, gE, nE, gv, nv, lG, 12);
+    }
+    /* reading R-cgrid: each coupling row is rounded on the grid of the whole Newton row,
+     * i.e. the grid exponent is floored by the max |entry| of the diagonal block's row */
+    finish_floor(Bt, &SB, floor_u); finish_floor(J, &SJ, floor_u); finish_floor(Dt, &SD, floor_u);
+    finish_floor(G, &SG, floor_E);
+    free(SB.acc); free(SJ.acc); free(SD.acc); free(SG.acc);
+    return 0;
 }

@@ -82,6 +82,18 @@ def lib(exact: bool = False):
         L.orc_set_smoother.restype = None
         L.orc_fgmres.argtypes = [vp, dp, dp, C.c_double, C.c_double, C.c_int, ip, dp]
         L.orc_gmres_smooth.argtypes = [vp, C.c_int, C.c_int, C.c_int, dp, dp]
+        L.orc_coupled_create.restype = vp
+        L.orc_coupled_create.argtypes = [C.c_int, C.c_int, C.c_int, dp, ip, dp, C.c_void_p]
+        L.orc_coupled_destroy.argtypes = [vp]
+        L.orc_coupled_destroy.restype = None
+        L.orc_coupled_sizes.argtypes = [vp, i64p]
+        L.orc_coupled_sizes.restype = None
+        L.orc_coupled_export.argtypes = [vp, i64p, ip, dp]
+        L.orc_coupled_apply.argtypes = [vp, dp, dp]
+        L.orc_coupled_precondition.argtypes = [vp, dp, dp]
+        L.orc_coupled_fgmres.argtypes = [vp, dp, dp, C.c_double, C.c_double, C.c_int, ip, dp]
+        L.orc_coupled_set_smoother.argtypes = [vp, C.c_int, C.c_int]
+        L.orc_coupled_set_smoother.restype = None
         L.orc_dot.argtypes = [dp, dp, C.c_longlong]
         L.orc_dot.restype = C.c_double
         _libs[exact] = L
@@ -357,3 +369,57 @@ class Oracle:
         """TEST HOOK: override the subspace decomposition of a level."""
         ptr = np.ascontiguousarray(ptr, np.int64); dofs = np.ascontiguousarray(dofs, np.int32)
         self._L.orc_set_patches(self.h, level % self.nlev, len(ptr) - 1, _l(ptr), _i(dofs))
+
+
+class CoupledOracle:
+    """NEXT-3: the 4x4 Newton system over [u | p | E | B] and the paper's outer
+    solver: FGMRES with the block upper-triangular preconditioner.
+    cfg gives dim, N, levels, Re, Rem, S, gamma, dt, picard; w: advecting potential (u^n);
+    bn: B^n potential (or None: B^n = 0)."""
+
+    def __init__(self, cfg, w, bn=None, exact=False, smoother="richardson", smoother_its=6):
+        self._L = L = lib(exact)
+        dp = np.array([cfg.Re, cfg.Rem, cfg.S, cfg.gamma, cfg.sigma, cfg.mu, cfg.theta,
+                       getattr(cfg, "dt", 0.0)], dtype=np.float64)
+        ip = np.array([cfg.nu, cfg.nu, int(getattr(cfg, "picard", 0))], dtype=np.int32)
+        self._w = np.ascontiguousarray(w, np.float64)
+        self._bn = None if bn is None else np.ascontiguousarray(bn, np.float64)
+        self.h = L.orc_coupled_create(cfg.dim, cfg.N, cfg.levels, _d(dp), _i(ip), _d(self._w),
+                                      None if self._bn is None else self._bn.ctypes.data)
+        if not self.h:
+            raise ValueError("oracle: invalid coupled configuration")
+        if smoother == "gmres":
+            L.orc_coupled_set_smoother(self.h, 1, smoother_its)
+        s = np.zeros(5, np.int64)
+        L.orc_coupled_sizes(self.h, _l(s))
+        self.nu, self.np_, self.nE, self.nB, self.nnz = (int(v) for v in s)
+        self.n = self.nu + self.np_ + self.nE + self.nB
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._L.orc_coupled_destroy(self.h)
+            self.h = None
+
+    def csr(self):
+        rp = np.zeros(self.n + 1, np.int64); ci = np.zeros(self.nnz, np.int32); v = np.zeros(self.nnz)
+        self._L.orc_coupled_export(self.h, _l(rp), _i(ci), _d(v))
+        return Csr(rp, ci, v)
+
+    def apply(self, x):
+        x = np.ascontiguousarray(x, np.float64); y = np.zeros(self.n)
+        self._L.orc_coupled_apply(self.h, _d(x), _d(y))
+        return y
+
+    def precondition(self, r):
+        r = np.ascontiguousarray(r, np.float64); y = np.zeros(self.n)
+        if self._L.orc_coupled_precondition(self.h, _d(r), _d(y)):
+            raise ArithmeticError("oracle: preconditioner failed")
+        return y
+
+    def fgmres(self, b, rtol=1e-7, atol=1e-7, maxit=50):
+        b = np.ascontiguousarray(b, np.float64); x = np.zeros(self.n)
+        its = np.zeros(1, np.int32); hist = np.zeros(maxit + 1)
+        st = self._L.orc_coupled_fgmres(self.h, _d(b), _d(x), rtol, atol, maxit, _i(its), _d(hist))
+        if st == 2:
+            raise ArithmeticError("oracle: preconditioner failed")
+        return x, int(its[0]), hist[: int(its[0]) + 1], st == 0

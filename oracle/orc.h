@@ -94,6 +94,11 @@ int oa_assemble(OCsr *A, const OMesh *m, const OSpace *s, const OParams *p, cons
 int oa_assemble_masked(OCsr *A, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
                        const unsigned char *cmask);
 
+/* NEXT-3 coupling blocks of the 4x4 system on one mesh (see fem.c) */
+int oa_assemble_coupling(OCsr *Bt, OCsr *J, OCsr *Dt, OCsr *G, const OMesh *m, const OSpace *sv, const OSpace *se,
+                         const OParams *p, const double *w, const double *bn, const double *floor_u,
+                         const double *floor_E);   /* row floors of the grid (R-cgrid), or NULL */
+
 /* quadrature / load / evaluation (manufactured-solution pins only) */
 int  oa_ncomp(const OSpace *s);
 int  oa_nq(int dim);

@@ -20,6 +20,8 @@
 #include "kernels.cuh"
 #include "setup.hpp"
 
+#include <functional>
+
 using namespace mhdp;
 
 namespace {
@@ -154,7 +156,7 @@ bool valid_level(const mhdp_ctx *c, int l) { return c && l >= 0 && l < c->nlev; 
 
 // ---------------- host -> device store construction ----------------
 
-mhdp_status build_sell(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
+mhdp_status make_sell(mhdp_ctx *ctx, const HostLevel &H, DevSell &A, int64_t *bytes) {
     const int64_t n = H.n, ns = (n + 31) / 32;
     std::vector<int64_t> sptr(ns + 1, 0);
     std::vector<int> rlen(n);
@@ -177,14 +179,17 @@ mhdp_status build_sell(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
         }
     }
     mhdp_status st;
-    L.A.n = n; L.A.nslices = ns; L.A.stored = stored;
-    if ((st = upload(ctx, &L.A.sptr, sptr.data(), ns + 1))) return st;
-    if ((st = upload(ctx, &L.A.rlen, rlen.data(), n))) return st;
-    if ((st = upload(ctx, &L.A.col, col.data(), stored))) return st;
-    if ((st = upload(ctx, &L.A.val, val.data(), stored))) return st;
-    L.bytes_op = 8 * (ns + 1) + 4 * n + 12 * stored;
+    A.n = n; A.nslices = ns; A.stored = stored;
+    if ((st = upload(ctx, &A.sptr, sptr.data(), ns + 1))) return st;
+    if ((st = upload(ctx, &A.rlen, rlen.data(), n))) return st;
+    if ((st = upload(ctx, &A.col, col.data(), stored))) return st;
+    if ((st = upload(ctx, &A.val, val.data(), stored))) return st;
+    if (bytes) *bytes = 8 * (ns + 1) + 4 * n + 12 * stored;
     return MHDP_OK;
 }
+
+mhdp_status build_sell(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) { return make_sell(ctx, H, L.A, &L.bytes_op); }
+
 
 // aligned 3x3 block structure: n % 3 == 0, rows 3R..3R+2 share one column list made of
 // complete aligned triples
@@ -1097,5 +1102,335 @@ mhdp_status mhdp_last_error(const mhdp_ctx *ctx, char *buf, int len, long long *
 }
 
 long long mhdp_launch_count(const mhdp_ctx *ctx) { return ctx ? g_launches - ctx->launches0 : 0; }
+
+}  // extern "C"
+
+// =====================================================================================
+// NEXT-3: the coupled Newton system over [u | p | E | B] (Table 1) and the
+// paper's outer solver: FGMRES with the block upper-triangular preconditioner
+//   y_EB = S~^-1 r_EB   (two FGMRES iterations on the E-B block, E-B V-cycle)
+//   z_u  = r_u - K y_EB,  K = [J | J~ + D~1 + D~2]
+//   y_up = M~^-1 z      (two FGMRES iterations on the (u,p) block, preconditioned by
+//                        y_p = -(1/Re + gamma) M_p^-1 s_p, y_u = V_u(s_u - B^T y_p))
+// Same operation order as the oracle (reading R-outer); inner products R-dot.
+// =====================================================================================
+struct mhdp_coupled {
+    mhdp_ctx *vel = nullptr, *eb = nullptr;
+    bool host_only = true;
+    int64_t nu = 0, np = 0, nE = 0, nB = 0, n = 0;
+    HostLevel Ah, Muph;           // global operator and the (u,p) block (host copies)
+    HostCsr Kh, Bth;
+    DevSell A, Mup;
+    int64_t *K_rp = nullptr, *Bt_rp = nullptr;
+    int *K_ci = nullptr, *Bt_ci = nullptr;
+    double *K_v = nullptr, *Bt_v = nullptr;
+    double cS = 0, Kinv = 0;
+    struct KWs {
+        int64_t n = 0;
+        int m = 0;
+        double *V = nullptr, *Z = nullptr, *w = nullptr, *part = nullptr, *scal = nullptr;
+        int *kk = nullptr;
+    } Web, Wup, Wout;
+    double *z = nullptr, *t = nullptr;
+    std::string err;
+};
+
+namespace {
+
+mhdp_status kws_alloc(mhdp_ctx *ctx, mhdp_coupled::KWs &W, int64_t n, int m) {
+    if (W.m >= m && W.n == n) return MHDP_OK;
+    mhdp_status st;
+    W.n = n; W.m = m;
+    if ((st = dalloc(ctx, &W.V, n * (int64_t)(m + 1)))) return st;
+    if ((st = dalloc(ctx, &W.Z, n * (int64_t)m))) return st;
+    if ((st = dalloc(ctx, &W.w, n))) return st;
+    if ((st = dalloc(ctx, &W.part, 2 * ((n + 255) / 256) + 2))) return st;
+    if ((st = dalloc(ctx, &W.scal, KrylovScal::size(m)))) return st;
+    if ((st = dalloc(ctx, &W.kk, 1))) return st;
+    return MHDP_OK;
+}
+
+typedef std::function<void(const double *, double *)> DevOp;
+
+// flexible GMRES on the device (R-outer / fgmres_gen of the oracle).  fixed: exactly m
+// iterations, asynchronous, breakdown through the device Krylov dimension; else stop at
+// |g_k+1| <= max(rtol |b|, atol) with one scalar read per iteration.
+int fgmres_dev(mhdp_ctx *ctx, mhdp_coupled::KWs &W, const DevOp &A, const DevOp &P, const double *b, double *x,
+               bool fixed, double rtol, double atol, int m, double *relres, bool *conv_out) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n = W.n;
+    KrylovScal S(W.scal, W.m);
+    const int ld = W.m;
+    auto read = [&](const double *p) {
+        double v = 0;
+        cudaMemcpyAsync(&v, p, sizeof(double), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        return v;
+    };
+    launch_dot_pinned(b, b, n, W.part, S.g, 1, s);
+    launch_fill(x, 0.0, n, s);
+    if (fixed) {
+        launch_krylov_init(S.g, m, W.kk, s);
+        launch_div_dev(W.V, b, S.g, n, s);
+        for (int k = 0; k < m; ++k) {
+            P(W.V + (int64_t)k * n, W.Z + (int64_t)k * n);
+            A(W.Z + (int64_t)k * n, W.w);
+            for (int i = 0; i <= k; ++i) {
+                launch_dot_pinned(W.w, W.V + (int64_t)i * n, n, W.part, S.H + i * ld + k, 0, s);
+                launch_axpy_negdev(W.w, S.H + i * ld + k, W.V + (int64_t)i * n, n, s);
+            }
+            launch_dot_pinned(W.w, W.w, n, W.part, S.hn + k, 1, s);
+            launch_givens(S.H, ld, S.cs, S.sn, S.g, S.hn + k, k, W.kk, s);
+            if (k + 1 < m) launch_div_dev(W.V + (int64_t)(k + 1) * n, W.w, S.hn + k, n, s);
+        }
+        launch_backsub(S.H, ld, S.g, m, W.kk, S.y, s);
+        launch_basis_update(x, W.Z, n, S.y, m, W.kk, n, s);
+        if (conv_out) *conv_out = true;
+        return m;
+    }
+    const double beta = read(S.g);
+    const double tol = std::max(rtol * beta, atol);
+    if (relres) *relres = beta > 0 ? 1.0 : 0.0;
+    if (conv_out) *conv_out = true;
+    if (beta == 0.0 || beta <= tol) return 0;
+    launch_div_dev(W.V, b, S.g, n, s);
+    int k = 0;
+    bool conv = false;
+    double gk = beta;
+    for (k = 0; k < m; ++k) {
+        P(W.V + (int64_t)k * n, W.Z + (int64_t)k * n);
+        A(W.Z + (int64_t)k * n, W.w);
+        for (int i = 0; i <= k; ++i) {
+            launch_dot_pinned(W.w, W.V + (int64_t)i * n, n, W.part, S.H + i * ld + k, 0, s);
+            launch_axpy_negdev(W.w, S.H + i * ld + k, W.V + (int64_t)i * n, n, s);
+        }
+        launch_dot_pinned(W.w, W.w, n, W.part, S.hn + k, 1, s);
+        launch_givens(S.H, ld, S.cs, S.sn, S.g, S.hn + k, k, nullptr, s);
+        gk = std::fabs(read(S.g + k + 1));
+        if (gk <= tol) { ++k; conv = true; break; }
+        if (read(S.hn + k) == 0.0) { ++k; break; }
+        if (k + 1 < m) launch_div_dev(W.V + (int64_t)(k + 1) * n, W.w, S.hn + k, n, s);
+    }
+    launch_backsub(S.H, ld, S.g, k, nullptr, S.y, s);
+    launch_basis_update(x, W.Z, n, S.y, k, nullptr, n, s);
+    if (relres) *relres = gk / beta;
+    if (conv_out) *conv_out = conv;
+    return k;
+}
+
+void coupled_precondition(mhdp_coupled *c, const double *r, double *y) {
+    mhdp_ctx *ve = c->vel, *eb = c->eb;
+    cudaStream_t s = ve->stream;
+    const int te = eb->nlev - 1, tv = ve->nlev - 1;
+    const int64_t nup = c->nu + c->np;
+    const double *rEB = r + nup;
+    double *yEB = y + nup;
+    DevOp A_eb = [&](const double *x, double *out) { residual(eb, te, nullptr, x, out); };
+    DevOp P_eb = [&](const double *in, double *out) { vcycle(eb, te, in, out); };
+    fgmres_dev(ve, c->Web, A_eb, P_eb, rEB, yEB, true, 0, 0, 2, nullptr, nullptr);
+    launch_csr_sub(c->nu, c->K_rp, c->K_ci, c->K_v, yEB, r, c->z, s);                 // z_u = r_u - K y_EB
+    cudaMemcpyAsync(c->z + c->nu, r + c->nu, sizeof(double) * c->np, cudaMemcpyDeviceToDevice, s);
+    DevOp A_up = [&](const double *x, double *out) { launch_residual(c->Mup, nullptr, x, out, s); };
+    DevOp P_up = [&](const double *in, double *out) {
+        launch_scale2(out + c->nu, in + c->nu, c->cS, c->Kinv, c->np, s);            // y_p
+        launch_csr_sub(c->nu, c->Bt_rp, c->Bt_ci, c->Bt_v, out + c->nu, in, c->t, s);   // s_u - B^T y_p
+        vcycle(ve, tv, c->t, out);                                                     // y_u
+    };
+    fgmres_dev(ve, c->Wup, A_up, P_up, c->z, y, true, 0, 0, 2, nullptr, nullptr);
+}
+
+void csr_transpose(const HostCsr &A, HostCsr &T) {
+    T.n = A.ncols; T.ncols = A.n;
+    T.rp.assign(T.n + 1, 0);
+    for (int64_t t = 0; t < A.rp[A.n]; ++t) T.rp[A.ci[t] + 1]++;
+    for (int64_t j = 0; j < T.n; ++j) T.rp[j + 1] += T.rp[j];
+    T.ci.resize(A.rp[A.n]); T.v.resize(A.rp[A.n]);
+    std::vector<int64_t> pos(T.rp.begin(), T.rp.end() - 1);
+    for (int64_t i = 0; i < A.n; ++i)
+        for (int64_t t = A.rp[i]; t < A.rp[i + 1]; ++t) {
+            const int64_t q = pos[A.ci[t]]++;
+            T.ci[q] = (int)i; T.v[q] = A.v[t];
+        }
+}
+
+struct RowCat {   // concatenates rows of several CSRs (column shifts) into one CSR
+    HostLevel &H;
+    explicit RowCat(HostLevel &h, int64_t n) : H(h) { H.n = n; H.rp.assign(1, 0); H.ci.clear(); H.v.clear(); }
+    template <class R>
+    void push(const R &rp, const std::vector<int> &ci, const std::vector<double> &v, int64_t row, int64_t shift) {
+        for (int64_t t = rp[row]; t < rp[row + 1]; ++t) { H.ci.push_back((int)(ci[t] + shift)); H.v.push_back(v[t]); }
+    }
+    void end() { H.rp.push_back((int64_t)H.ci.size()); }
+};
+
+}  // namespace
+
+extern "C" {
+
+void mhdp_coupled_destroy(mhdp_coupled *c) {
+    if (!c) return;
+    mhdp_destroy(c->vel);
+    mhdp_destroy(c->eb);
+    delete c;
+}
+
+mhdp_status mhdp_coupled_create(mhdp_coupled **out, int cuda_device, void *cuda_stream, const mhdp_mesh *mesh,
+                                const mhdp_params *params, const double *w_vertex_host,
+                                const double *bn_vertex_host) {
+    if (!out || !mesh || !params || !w_vertex_host) return MHDP_EINVAL;
+    *out = nullptr;
+    mhdp_coupled *c = new (std::nothrow) mhdp_coupled();
+    if (!c) return MHDP_ENOMEM;
+    mhdp_status st;
+    if ((st = mhdp_create(&c->vel, cuda_device, cuda_stream)) || (st = mhdp_create(&c->eb, cuda_device, cuda_stream))) {
+        mhdp_coupled_destroy(c);
+        return st;
+    }
+    c->host_only = cuda_device < 0;
+    if ((st = mhdp_assemble_lorentz(c->vel, MHDP_BLOCK_ALVEL, mesh, params, w_vertex_host, bn_vertex_host)) ||
+        (st = mhdp_assemble(c->eb, MHDP_BLOCK_EB, mesh, params, w_vertex_host))) {
+        c->err = c->vel->err.empty() ? c->eb->err : c->vel->err;
+        *out = c;
+        return st;
+    }
+    CouplingBlocks cb;
+    auto rowmax = [](const HostLevel &H, int64_t rows) {
+        std::vector<double> m((size_t)rows, 0.0);
+        for (int64_t r = 0; r < rows; ++r)
+            for (int64_t t = H.rp[r]; t < H.rp[r + 1]; ++t) m[r] = std::max(m[r], std::fabs(H.v[t]));
+        return m;
+    };
+    const HostLevel &Hv = c->vel->H[c->vel->nlev - 1], &He = c->eb->H[c->eb->nlev - 1];
+    const std::vector<double> fu = rowmax(Hv, Hv.n), fE = rowmax(He, He.n);   // R-cgrid floors
+    std::string e = assemble_coupling(mesh->dim, mesh->n_fine, c->vel->p, w_vertex_host, bn_vertex_host, fu.data(),
+                                      fE.data(), cb);
+    if (!e.empty()) { c->err = e; *out = c; return MHDP_EINVAL; }
+    c->nu = cb.nu; c->np = cb.np; c->nE = cb.nE; c->nB = cb.nB;
+    c->n = c->nu + c->np + c->nE + c->nB;
+    c->cS = -(1.0 / c->vel->p.Re + c->vel->p.gamma);
+    const int N = mesh->n_fine;
+    c->Kinv = mesh->dim == 2 ? 2.0 * N * N : 6.0 * (double)N * N * N;
+    const HostLevel &Av = c->vel->H[c->vel->nlev - 1], &Ae = c->eb->H[c->eb->nlev - 1];
+    HostCsr B;
+    csr_transpose(cb.Bt, B);
+    const int64_t su = 0, sp = c->nu, sE = c->nu + c->np, sB = sE + c->nE;
+    RowCat ga(c->Ah, c->n), gm(c->Muph, c->nu + c->np);
+    c->Kh.n = c->nu; c->Kh.ncols = c->nE + c->nB; c->Kh.rp.assign(1, 0);
+    for (int64_t i = 0; i < c->nu; ++i) {
+        ga.push(Av.rp, Av.ci, Av.v, i, su); ga.push(cb.Bt.rp, cb.Bt.ci, cb.Bt.v, i, sp);
+        ga.push(cb.J.rp, cb.J.ci, cb.J.v, i, sE); ga.push(cb.Dt.rp, cb.Dt.ci, cb.Dt.v, i, sB); ga.end();
+        gm.push(Av.rp, Av.ci, Av.v, i, 0); gm.push(cb.Bt.rp, cb.Bt.ci, cb.Bt.v, i, c->nu); gm.end();
+        for (int64_t t = cb.J.rp[i]; t < cb.J.rp[i + 1]; ++t) { c->Kh.ci.push_back(cb.J.ci[t]); c->Kh.v.push_back(cb.J.v[t]); }
+        for (int64_t t = cb.Dt.rp[i]; t < cb.Dt.rp[i + 1]; ++t) {
+            c->Kh.ci.push_back((int)(cb.Dt.ci[t] + c->nE)); c->Kh.v.push_back(cb.Dt.v[t]);
+        }
+        c->Kh.rp.push_back((int64_t)c->Kh.ci.size());
+    }
+    for (int64_t q = 0; q < c->np; ++q) {
+        ga.push(B.rp, B.ci, B.v, q, su); ga.end();
+        gm.push(B.rp, B.ci, B.v, q, 0); gm.end();
+    }
+    for (int64_t r = 0; r < c->nE; ++r) {
+        ga.push(cb.G.rp, cb.G.ci, cb.G.v, r, su); ga.push(Ae.rp, Ae.ci, Ae.v, r, sE); ga.end();
+    }
+    for (int64_t r = 0; r < c->nB; ++r) { ga.push(Ae.rp, Ae.ci, Ae.v, c->nE + r, sE); ga.end(); }
+    c->Bth = std::move(cb.Bt);
+    *out = c;
+    if (c->host_only) return MHDP_OK;
+    // device: both hierarchies, the global operator, (u,p) block, K and B^T
+    if ((st = mhdp_setup(c->vel)) || (st = mhdp_setup(c->eb))) {
+        c->err = c->vel->err.empty() ? c->eb->err : c->vel->err;
+        return st;
+    }
+    mhdp_ctx *ctx = c->vel;
+    if ((st = make_sell(ctx, c->Ah, c->A, nullptr))) return st;
+    if ((st = make_sell(ctx, c->Muph, c->Mup, nullptr))) return st;
+    if ((st = upload(ctx, &c->K_rp, c->Kh.rp.data(), c->nu + 1))) return st;
+    if ((st = upload(ctx, &c->K_ci, c->Kh.ci.data(), (int64_t)c->Kh.ci.size()))) return st;
+    if ((st = upload(ctx, &c->K_v, c->Kh.v.data(), (int64_t)c->Kh.v.size()))) return st;
+    if ((st = upload(ctx, &c->Bt_rp, c->Bth.rp.data(), c->nu + 1))) return st;
+    if ((st = upload(ctx, &c->Bt_ci, c->Bth.ci.data(), (int64_t)c->Bth.ci.size()))) return st;
+    if ((st = upload(ctx, &c->Bt_v, c->Bth.v.data(), (int64_t)c->Bth.v.size()))) return st;
+    if ((st = kws_alloc(ctx, c->Web, c->nE + c->nB, 2))) return st;
+    if ((st = kws_alloc(ctx, c->Wup, c->nu + c->np, 2))) return st;
+    if ((st = dalloc(ctx, &c->z, c->nu + c->np))) return st;
+    if ((st = dalloc(ctx, &c->t, c->nu))) return st;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_coupled_sizes(const mhdp_coupled *c, long long *out) {
+    if (!c || !out) return MHDP_EINVAL;
+    out[0] = c->nu; out[1] = c->np; out[2] = c->nE; out[3] = c->nB; out[4] = c->Ah.rp.empty() ? 0 : c->Ah.rp.back();
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_coupled_export_csr(const mhdp_coupled *c, long long *rowptr, int *col, double *val) {
+    if (!c || !rowptr || !col || !val || c->Ah.rp.empty()) return MHDP_EINVAL;
+    memcpy(rowptr, c->Ah.rp.data(), sizeof(int64_t) * c->Ah.rp.size());
+    memcpy(col, c->Ah.ci.data(), sizeof(int) * c->Ah.ci.size());
+    memcpy(val, c->Ah.v.data(), sizeof(double) * c->Ah.v.size());
+    return MHDP_OK;
+}
+
+static mhdp_status coupled_ready(mhdp_coupled *c) {
+    if (!c) return MHDP_EINVAL;
+    if (c->host_only) { c->err = "host-only coupled system"; return MHDP_ECUDA; }
+    if (!c->vel->setup_done || !c->eb->setup_done || !c->A.sptr) { c->err = "coupled system not set up"; return MHDP_ESTATE; }
+    cudaSetDevice(c->vel->device);
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_coupled_apply(mhdp_coupled *c, const double *x_dev, double *y_dev) {
+    mhdp_status st = coupled_ready(c);
+    if (st) return st;
+    if (!x_dev || !y_dev) return MHDP_EINVAL;
+    launch_residual(c->A, nullptr, x_dev, y_dev, c->vel->stream);
+    return check_launch(c->vel);
+}
+
+mhdp_status mhdp_coupled_precondition(mhdp_coupled *c, const double *r_dev, double *y_dev) {
+    mhdp_status st = coupled_ready(c);
+    if (st) return st;
+    if (!r_dev || !y_dev) return MHDP_EINVAL;
+    coupled_precondition(c, r_dev, y_dev);
+    return check_launch(c->vel);
+}
+
+mhdp_status mhdp_coupled_fgmres(mhdp_coupled *c, const double *b_dev, double *x_dev, double rtol, double atol,
+                                int maxit, int *its_out, double *relres_out) {
+    mhdp_status st = coupled_ready(c);
+    if (st) return st;
+    if (!b_dev || !x_dev || maxit < 1 || maxit > 500) return MHDP_EINVAL;
+    mhdp_ctx *ctx = c->vel;
+    if ((st = kws_alloc(ctx, c->Wout, c->n, maxit))) { c->err = ctx->err; return st; }
+    cudaStream_t s = ctx->stream;
+    DevOp A = [&](const double *x, double *y) { launch_residual(c->A, nullptr, x, y, s); };
+    DevOp P = [&](const double *r, double *y) { coupled_precondition(c, r, y); };
+    double rel = 0;
+    bool conv = false;
+    const int its = fgmres_dev(ctx, c->Wout, A, P, b_dev, x_dev, false, rtol, atol, maxit, &rel, &conv);
+    CK(cudaStreamSynchronize(s));
+    if (its_out) *its_out = its;
+    if (relres_out) *relres_out = rel;
+    if ((st = check_launch(ctx))) return st;
+    if (!conv) { c->err = "FGMRES reached maxit"; return MHDP_ENOCONV; }
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_coupled_set_smoother(mhdp_coupled *c, int smoother, int its) {
+    if (!c) return MHDP_EINVAL;
+    mhdp_status st = mhdp_set_smoother(c->vel, smoother, its);
+    if (!st) st = mhdp_set_smoother(c->eb, smoother, its);
+    return st;
+}
+
+mhdp_status mhdp_coupled_last_error(const mhdp_coupled *c, char *buf, int len) {
+    if (!c || !buf || len <= 0) return MHDP_EINVAL;
+    std::string e = !c->err.empty() ? c->err : (!c->vel->err.empty() ? c->vel->err : c->eb->err);
+    strncpy(buf, e.c_str(), (size_t)len - 1);
+    buf[len - 1] = 0;
+    return MHDP_OK;
+}
 
 }  // extern "C"

@@ -468,8 +468,8 @@ inline double grid_round(const dd &x, int E) {
     return v == 0.0 ? 0.0 : v;   // exact cancellation: +0
 }
 
-void round_row(const dd *x, i64 len, double *out) {
-    double mx = 0.0;
+void round_row(const dd *x, i64 len, double *out, double floor = 0.0) {
+    double mx = floor;
     for (i64 k = 0; k < len; ++k) mx = std::max(mx, std::fabs(x[k].value()));
     if (mx == 0.0) {
         for (i64 k = 0; k < len; ++k) out[k] = 0.0;
@@ -1057,7 +1057,200 @@ void build_prolongation(const Mesh &mf, const Space &sf, const Mesh &mc, const S
         for (size_t t = 0; t < rows[I].size(); ++t) { ci[rp[I] + t] = rows[I][t].first; vv[rp[I] + t] = rows[I][t].second; }
 }
 
+// ------------------------------------------------------------------------------------
+// NEXT-3 coupling blocks (Table 1), gather form, double-double, R-exact rows.
+// Closed forms with phi_i = lam_a v (BDM1), psi_k = sum_b lam_b P_b (RT1, P_b =
+// c_k (X_b - X_k)), E = lam_e (CG1) or lam_p g_q - lam_q g_p (NED1); u^n = w, B^n
+// constant per cell.  2D conventions: u x B = u1 B2 - u2 B1, B x s = (B2 s, -B1 s).
+// ------------------------------------------------------------------------------------
+inline void xcr(int d, const dd *a, const dd *b, dd *c) {          // vector x vector
+    if (d == 2) { c[0] = a[0] * b[1] - a[1] * b[0]; c[1] = c[2] = dd(0.0); }
+    else cross3(a, b, c);
+}
+inline void xsc(int d, const dd *B, const dd *s, dd *c) {          // B x (scalar or vector)
+    if (d == 2) { c[0] = B[1] * s[0]; c[1] = -(B[0] * s[0]); c[2] = dd(0.0); }
+    else cross3(B, s, c);
+}
+
+struct CellCoup {
+    GeoT<dd> G;
+    VelBasisT<dd> V;
+    dd w[3], bn[3];
+    dd cq[4];          // RT scale s_q / (d |K|)
+    int gv[12], gE[6], gB[4];
+};
+
+void cell_coup(const Mesh &m, const Space &sv, const Space &se, i64 c, const double *pot, const double *bpot,
+               CellCoup &K) {
+    cell_geo(m, c, K.G);
+    vel_basis(K.G, K.V);
+    cell_wind(K.G, pot, K.w);
+    K.bn[0] = K.bn[1] = K.bn[2] = dd(0.0);
+    if (bpot) cell_wind(K.G, bpot, K.bn);
+    const int d = m.dim, nvc = d + 1;
+    cell_dofs(m, sv, c, K.gv);
+    int ebd[10];
+    cell_dofs(m, se, c, ebd);
+    const int nE = d == 2 ? 3 : 6;
+    for (int t = 0; t < nE; ++t) K.gE[t] = ebd[t];
+    for (int q = 0; q < nvc; ++q) {
+        K.gB[q] = ebd[nE + q] < 0 ? -1 : ebd[nE + q] - (int)se.nE;
+        dd A[3];
+        int fl[3];
+        facet_area(K.G, q, A, fl);
+        K.cq[q] = dd(facet_sign(K.G, q, A, fl)) / K.G.dvol;
+    }
+}
+
+// coupling of velocity test function i with the E basis function e / B basis function k
+inline dd coup_J(const CellCoup &K, int d, int i, int e) {
+    static const int LE[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+    const int ai = K.V.a[i];
+    const dd *v = K.V.v[i];
+    if (d == 2) {                                    // (B^n x lam_e) . v = lam_e (B1 v0 - B0 v1)
+        return mass_bary(K.G, e, ai) * (K.bn[1] * v[0] - K.bn[0] * v[1]);
+    }
+    const int p = LE[e][0], q = LE[e][1];
+    dd c1[3], c2[3];
+    cross3(K.bn, K.G.g[q], c1);
+    cross3(K.bn, K.G.g[p], c2);
+    return mass_bary(K.G, p, ai) * dot3(c1, v) - mass_bary(K.G, q, ai) * dot3(c2, v);
+}
+inline dd coup_G(const CellCoup &K, int d, int e, int i) {      // (v_i x B^n, F_e)
+    static const int LE[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+    const int ai = K.V.a[i];
+    dd vb[3];
+    xcr(d, K.V.v[i], K.bn, vb);
+    if (d == 2) return mass_bary(K.G, ai, e) * vb[0];
+    const int p = LE[e][0], q = LE[e][1];
+    return mass_bary(K.G, ai, p) * dot3(vb, K.G.g[q]) - mass_bary(K.G, ai, q) * dot3(vb, K.G.g[p]);
+}
+inline dd coup_D(const CellCoup &K, int d, int i, int k) {      // D~1 + D~2, without S
+    const int ai = K.V.a[i];
+    dd wb[3];
+    xcr(d, K.w, K.bn, wb);                                      // u^n x B^n
+    dd acc(0.0);
+    for (int b = 0; b <= d; ++b) {
+        dd P[3];
+        for (int r = 0; r < 3; ++r) P[r] = K.cq[k] * (K.G.X[b][r] - K.G.X[k][r]);
+        dd t1[3], ub[3], t2[3];
+        xsc(d, P, wb, t1);                                      // B x (u^n x B^n)
+        xcr(d, K.w, P, ub);                                     // u^n x B
+        xsc(d, K.bn, ub, t2);                                   // B^n x (u^n x B)
+        acc += mass_bary(K.G, b, ai) * (dot3(t1, K.V.v[i]) + dot3(t2, K.V.v[i]));
+    }
+    return acc;
+}
+
 }  // namespace
+
+std::string assemble_coupling(int dim, int N, const Params &p, const double *w, const double *bn, const double *floor_u,
+                              const double *floor_E, CouplingBlocks &out) {
+    Mesh m;
+    build_mesh(m, dim, N);
+    Space sv, se;
+    build_space(sv, m, 1);
+    build_space(se, m, 0);
+    const int d = dim, nvc = d + 1, nb = d * nvc, nE = d == 2 ? 3 : 6;
+    out.nu = sv.n; out.np = m.nc; out.nE = se.nE; out.nB = se.n - se.nE;
+    std::vector<CellCoup> cc(m.nc);
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < m.nc; ++c) cell_coup(m, sv, se, c, w, bn, cc[c]);
+    // ---- u rows (Bt, J, Dt): row block = free facet f, cells of f ascending ----
+    std::vector<int> freef;
+    for (i64 f = 0; f < m.nfacet; ++f) if (sv.fdof[f] >= 0) freef.push_back((int)f);
+    auto init = [](HostCsr &A, i64 n, i64 ncols) { A.n = n; A.ncols = ncols; A.rp.assign(n + 1, 0); };
+    init(out.Bt, out.nu, out.np); init(out.J, out.nu, out.nE); init(out.Dt, out.nu, out.nB); init(out.G, out.nE, out.nu);
+    struct RowData { std::vector<int> cB, cJ, cD; std::vector<dd> vB, vJ, vD; };
+    std::vector<RowData> rows(sv.n);
+#pragma omp parallel for schedule(dynamic, 64)
+    for (i64 t = 0; t < (i64)freef.size(); ++t) {
+        const int f = freef[t], r0 = sv.fdof[f];
+        std::vector<int> cells;
+        for (int side = 0; side < 2; ++side) if (m.fcell[2 * f + side] >= 0) cells.push_back(m.fcell[2 * f + side]);
+        // column sets: union over the cells (sorted unique)
+        std::vector<int> colsE, colsB, colsP;
+        for (int c : cells) {
+            colsP.push_back(c);
+            for (int e = 0; e < nE; ++e) if (cc[c].gE[e] >= 0) colsE.push_back(cc[c].gE[e]);
+            for (int q = 0; q < nvc; ++q) if (cc[c].gB[q] >= 0) colsB.push_back(cc[c].gB[q]);
+        }
+        for (auto *v : {&colsE, &colsB, &colsP}) {
+            std::sort(v->begin(), v->end());
+            v->erase(std::unique(v->begin(), v->end()), v->end());
+        }
+        for (int a = 0; a < d; ++a) {
+            RowData &R = rows[r0 + a];
+            R.cB = colsP; R.cJ = colsE; R.cD = colsB;
+            R.vB.assign(colsP.size(), dd(0.0)); R.vJ.assign(colsE.size(), dd(0.0)); R.vD.assign(colsB.size(), dd(0.0));
+            for (int c : cells) {
+                const CellCoup &K = cc[c];
+                int li = -1;
+                for (int k = 0; k < nb; ++k) if (K.gv[k] == r0 + a) li = k;
+                const dd divv = dot3(K.V.v[li], K.G.g[K.V.a[li]]) * K.G.vol;        // int_K div v
+                R.vB[std::lower_bound(colsP.begin(), colsP.end(), c) - colsP.begin()] += -divv;
+                for (int e = 0; e < nE; ++e)
+                    if (K.gE[e] >= 0)
+                        R.vJ[std::lower_bound(colsE.begin(), colsE.end(), K.gE[e]) - colsE.begin()] +=
+                            dd(p.S) * coup_J(K, d, li, e);
+                if (!p.picard)
+                    for (int q = 0; q < nvc; ++q)
+                        if (K.gB[q] >= 0)
+                            R.vD[std::lower_bound(colsB.begin(), colsB.end(), K.gB[q]) - colsB.begin()] +=
+                                dd(p.S) * coup_D(K, d, li, q);
+            }
+        }
+    }
+    // ---- E rows (G): cells of the E entity ascending ----
+    std::vector<i64> ep;
+    std::vector<int> ec;
+    if (d == 2) incidence(m, 0, ep, ec); else incidence(m, 1, ep, ec);
+    std::vector<std::vector<int>> gcols(out.nE);
+    std::vector<std::vector<dd>> gvals(out.nE);
+    std::vector<int> Eent(out.nE);
+    if (d == 2) { for (i64 v = 0; v < m.nv; ++v) if (se.vdof[v] >= 0) Eent[se.vdof[v]] = (int)v; }
+    else { for (i64 e = 0; e < m.ne; ++e) if (se.edof[e] >= 0) Eent[se.edof[e]] = (int)e; }
+#pragma omp parallel for schedule(dynamic, 256)
+    for (i64 r = 0; r < out.nE; ++r) {
+        const int ent = Eent[r];
+        std::vector<int> cl;
+        for (i64 t = ep[ent]; t < ep[ent + 1]; ++t)
+            for (int k = 0; k < nb; ++k) if (cc[ec[t]].gv[k] >= 0) cl.push_back(cc[ec[t]].gv[k]);
+        std::sort(cl.begin(), cl.end());
+        cl.erase(std::unique(cl.begin(), cl.end()), cl.end());
+        std::vector<dd> vals(cl.size(), dd(0.0));
+        for (i64 t = ep[ent]; t < ep[ent + 1]; ++t) {
+            const CellCoup &K = cc[ec[t]];
+            int le = -1;
+            for (int e = 0; e < nE; ++e) if (K.gE[e] == r) le = e;
+            for (int k = 0; k < nb; ++k)
+                if (K.gv[k] >= 0) vals[std::lower_bound(cl.begin(), cl.end(), K.gv[k]) - cl.begin()] += coup_G(K, d, le, k);
+        }
+        gcols[r] = std::move(cl);
+        gvals[r] = std::move(vals);
+    }
+    // ---- pack with the row rounding of R-exact, on the grid of the whole Newton row
+    // (reading R-cgrid: the grid exponent is floored by the diagonal block's row max) ----
+    auto pack = [](HostCsr &A, i64 n, auto colsOf, auto valsOf, const double *floor) {
+        for (i64 r = 0; r < n; ++r) A.rp[r + 1] = A.rp[r] + (i64)colsOf(r).size();
+        A.ci.resize(A.rp[n]);
+        A.v.resize(A.rp[n]);
+        for (i64 r = 0; r < n; ++r) {
+            const auto &c = colsOf(r);
+            std::copy(c.begin(), c.end(), A.ci.begin() + A.rp[r]);
+            round_row(valsOf(r).data(), (i64)c.size(), A.v.data() + A.rp[r], floor ? floor[r] : 0.0);
+        }
+    };
+    pack(out.Bt, out.nu, [&](i64 r) -> const std::vector<int> & { return rows[r].cB; },
+         [&](i64 r) -> const std::vector<dd> & { return rows[r].vB; }, floor_u);
+    pack(out.J, out.nu, [&](i64 r) -> const std::vector<int> & { return rows[r].cJ; },
+         [&](i64 r) -> const std::vector<dd> & { return rows[r].vJ; }, floor_u);
+    pack(out.Dt, out.nu, [&](i64 r) -> const std::vector<int> & { return rows[r].cD; },
+         [&](i64 r) -> const std::vector<dd> & { return rows[r].vD; }, floor_u);
+    pack(out.G, out.nE, [&](i64 r) -> const std::vector<int> & { return gcols[r]; },
+         [&](i64 r) -> const std::vector<dd> & { return gvals[r]; }, floor_E);
+    return "";
+}
 
 std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params &p, const double *w,
                                const double *bn, std::vector<HostLevel> &out) {

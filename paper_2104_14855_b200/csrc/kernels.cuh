@@ -101,4 +101,9 @@ void launch_backsub(const double *H, int m, const double *g, int kk, const int *
 void launch_basis_update(double *x, const double *V, int64_t ldv, const double *y, int kk, const int *kk_dev,
                          int64_t n, cudaStream_t s);
 
+// NEXT-3: out = b - A x (CSR, int64 row pointer, ascending fma chains); y = (c s) kinv
+void launch_csr_sub(int64_t n, const int64_t *rp, const int *ci, const double *v, const double *x, const double *b,
+                    double *out, cudaStream_t s);
+void launch_scale2(double *y, const double *s, double c, double kinv, int64_t n, cudaStream_t st);
+
 }  // namespace mhdp

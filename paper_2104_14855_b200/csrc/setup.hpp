@@ -40,4 +40,25 @@ struct HostLevel {
 std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params &p, const double *w,
                                const double *bn, std::vector<HostLevel> &out);
 
+// NEXT-3: the coupling blocks of the 4x4 Newton system (Table 1) on the finest
+// mesh, as CSR (rows sorted), and the sizes of the four fields.
+struct HostCsr {
+    int64_t n = 0, ncols = 0;
+    std::vector<int64_t> rp;
+    std::vector<int> ci;
+    std::vector<double> v;
+};
+struct CouplingBlocks {
+    int64_t nu = 0, np = 0, nE = 0, nB = 0;
+    HostCsr Bt;   // u x p   : -(q, div v)
+    HostCsr J;    // u x E   : S (B^n x E, v)
+    HostCsr Dt;   // u x B   : S (B x (u^n x B^n), v) + S (B^n x (u^n x B), v)   (0 under Picard)
+    HostCsr G;    // E x u   : (u x B^n, F)
+};
+// floor_u[r] (r < nu) / floor_E[r] (r < nE): max |entry| of row r of the finest velocity /
+// E-B matrix (fp64), or NULL: the coupling rows are rounded on the grid of the whole
+// Newton row (reading R-cgrid of DESIGN.md).
+std::string assemble_coupling(int dim, int N, const Params &p, const double *w, const double *bn, const double *floor_u,
+                              const double *floor_E, CouplingBlocks &out);
+
 }  // namespace mhdp

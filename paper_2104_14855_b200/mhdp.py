@@ -49,7 +49,10 @@ SYMBOLS = ["mhdp_create", "mhdp_destroy", "mhdp_assemble", "mhdp_begin_levels", 
            "mhdp_patch_update", "mhdp_smooth", "mhdp_restrict", "mhdp_prolong_add", "mhdp_coarse_solve",
            "mhdp_vcycle", "mhdp_vcycle_host", "mhdp_smooth_host", "mhdp_gmres", "mhdp_export_csr",
            "mhdp_export_patches", "mhdp_export_prolongation", "mhdp_export_patch_lu", "mhdp_export_slots",
-           "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count", "mhdp_fgmres", "mhdp_dot", "mhdp_set_smoother", "mhdp_vcycle_graphs_active", "mhdp_assemble_lorentz"]
+           "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count", "mhdp_fgmres", "mhdp_dot", "mhdp_set_smoother", "mhdp_vcycle_graphs_active", "mhdp_assemble_lorentz",
+           "mhdp_coupled_create", "mhdp_coupled_destroy", "mhdp_coupled_sizes", "mhdp_coupled_export_csr",
+           "mhdp_coupled_apply", "mhdp_coupled_precondition", "mhdp_coupled_fgmres", "mhdp_coupled_set_smoother",
+           "mhdp_coupled_last_error"]
 
 
 def lib():
@@ -83,6 +86,14 @@ def lib():
             "mhdp_fgmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp],
             "mhdp_dot": [vp, vp, vp, i64, dp],
             "mhdp_set_smoother": [vp, C.c_int, C.c_int],
+            "mhdp_coupled_create": [C.POINTER(vp), C.c_int, vp, C.POINTER(Mesh), C.POINTER(Params), dp, C.c_void_p],
+            "mhdp_coupled_sizes": [vp, i64p],
+            "mhdp_coupled_export_csr": [vp, i64p, ip, dp],
+            "mhdp_coupled_apply": [vp, vp, vp],
+            "mhdp_coupled_precondition": [vp, vp, vp],
+            "mhdp_coupled_fgmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp],
+            "mhdp_coupled_set_smoother": [vp, C.c_int, C.c_int],
+            "mhdp_coupled_last_error": [vp, C.c_char_p, C.c_int],
             "mhdp_export_csr": [vp, C.c_int, i64p, ip, dp],
             "mhdp_export_patches": [vp, C.c_int, i64p, ip],
             "mhdp_export_prolongation": [vp, C.c_int, i64p, ip, dp],
@@ -99,6 +110,8 @@ def lib():
         L.mhdp_destroy.restype = None
         L.mhdp_num_levels.argtypes = [vp]
         L.mhdp_num_levels.restype = C.c_int
+        L.mhdp_coupled_destroy.argtypes = [vp]
+        L.mhdp_coupled_destroy.restype = None
         L.mhdp_vcycle_graphs_active.argtypes = [vp]
         L.mhdp_vcycle_graphs_active.restype = C.c_int
         L.mhdp_launch_count.argtypes = [vp]
@@ -315,3 +328,63 @@ class Context:
         y = np.zeros(max(self.info(level)["sum_n"], 1))
         self._chk(self._L.mhdp_export_slots(self.h, level, _d(y)))
         return y
+
+
+class Coupled:
+    """NEXT-3: the coupled Newton system over [u | p | E | B] and the paper's outer solver
+    (include/mhdp.h mhdp_coupled_*).  device=-1: host-only (assembly and export)."""
+
+    def __init__(self, cfg, w, bn=None, device: int = 0, stream: int | None = None, smoother="richardson",
+                 smoother_its=6):
+        self._L = lib()
+        self._w = np.ascontiguousarray(w, np.float64)
+        self._bn = None if bn is None else np.ascontiguousarray(bn, np.float64)
+        mesh = Mesh(cfg.dim, cfg.N, cfg.levels)
+        p = make_params(cfg, smoother, smoother_its)
+        h = C.c_void_p()
+        st = self._L.mhdp_coupled_create(C.byref(h), device, C.c_void_p(stream or 0), C.byref(mesh), C.byref(p),
+                                         _d(self._w), None if self._bn is None else self._bn.ctypes.data)
+        self.h = h
+        self._chk(st)
+        s = np.zeros(5, np.int64)
+        self._chk(self._L.mhdp_coupled_sizes(self.h, _l(s)))
+        self.nu, self.np_, self.nE, self.nB, self.nnz = (int(v) for v in s)
+        self.n = self.nu + self.np_ + self.nE + self.nB
+
+    def _chk(self, st):
+        if st:
+            buf = C.create_string_buffer(512)
+            if getattr(self, "h", None):
+                self._L.mhdp_coupled_last_error(self.h, buf, 512)
+            raise MhdpError(st, buf.value.decode(), -1)
+        return st
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.mhdp_coupled_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def csr(self):
+        rp = np.zeros(self.n + 1, np.int64); ci = np.zeros(max(self.nnz, 1), np.int32); v = np.zeros(max(self.nnz, 1))
+        self._chk(self._L.mhdp_coupled_export_csr(self.h, _l(rp), _i(ci), _d(v)))
+        return rp, ci[:self.nnz], v[:self.nnz]
+
+    def apply(self, x, y):
+        return self._chk(self._L.mhdp_coupled_apply(self.h, _ptr(x), _ptr(y)))
+
+    def precondition(self, r, y):
+        return self._chk(self._L.mhdp_coupled_precondition(self.h, _ptr(r), _ptr(y)))
+
+    def fgmres(self, b, x, rtol=1e-7, atol=1e-7, maxit=50):
+        its = C.c_int(0)
+        rel = C.c_double(0)
+        st = self._L.mhdp_coupled_fgmres(self.h, _ptr(b), _ptr(x), rtol, atol, maxit, C.byref(its), C.byref(rel))
+        if st not in (0, 6):
+            self._chk(st)
+        return its.value, rel.value, st == 0
+
+    def set_smoother(self, smoother="richardson", its=6):
+        return self._chk(self._L.mhdp_coupled_set_smoother(self.h, 1 if smoother == "gmres" else 0, its))

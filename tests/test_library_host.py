@@ -142,3 +142,27 @@ def test_appendix_a_counts_full_c5_finest(mh):
     i = ctx.info(0)
     row = [r for r in gold["c5"] if r[0] == 24][0]
     assert (i["n"], i["nnz"]) == (row[1], row[2])
+
+
+COUPLED = [(2, 8, 2, dict()), (3, 4, 2, dict()), (2, 4, 2, dict(picard=1, dt=0.1)), (3, 2, 1, dict(dt=0.05))]
+
+
+@pytest.mark.parametrize("dim,N,L,kw", COUPLED, ids=[f"{d}D-N{n}-{k}" for d, n, l, k in COUPLED])
+def test_coupled_operator_bitexact(mh, oracle_mod, dim, N, L, kw):
+    """NEXT-3: the coupled 4x4 Newton operator over [u | p | E | B] (Table 1) assembled by
+    the library (double-double closed forms) equals the exact oracle's (quadrature in
+    __float128), bit for bit, including every coupling block."""
+    import dataclasses
+    from paper_2104_14855_b200 import workloads
+    cfg = dataclasses.replace(workloads.small("c3" if dim == 2 else "c5", N, L), Re=10.0, Rem=5.0, gamma=100.0,
+                              S=3.0, **kw)
+    w, _, _ = workloads.draw(cfg, 1, 6)
+    bn = workloads.magnetic_potential(cfg, 6)
+    orc = oracle_mod.CoupledOracle(cfg, w, bn, exact=True)
+    lib = mh.Coupled(cfg, w, bn, device=-1)
+    assert (lib.nu, lib.np_, lib.nE, lib.nB) == (orc.nu, orc.np_, orc.nE, orc.nB)
+    A = orc.csr()
+    rp, ci, v = lib.csr()
+    assert np.array_equal(A.rp, rp) and np.array_equal(A.ci, ci)
+    diff = np.flatnonzero(A.v.view(np.uint64) != v.view(np.uint64))
+    assert diff.size == 0, f"{diff.size} entries differ"
