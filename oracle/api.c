@@ -757,7 +757,6 @@ OCoupled *orc_coupled_create(int dim, int N, int nlev, const double *dparams, co
     oa_assemble_coupling(&c->Bt, &J, &Dt, &G, &Lv->m, &Lv->s, &Le->s, &p, Lv->w, Lv->bn, fu, fE);
     free(fu); free(fE);
     oc_transpose(&B, &c->Bt, Lv->m.nc);
-    for (i64 t = 0; t < B.nnz; t++) B.v[t] = B.v[t];   /* B = (B^T)^T: -(div u, q) */
     c->nu = Lv->s.n; c->np = Lv->m.nc; c->nE = Le->s.nE; c->nB = Le->s.n - Le->s.nE;
     c->n = c->nu + c->np + c->nE + c->nB;
     c->cS = -(1.0 / p.Re + p.gamma);
