@@ -125,7 +125,8 @@ mhdp_status mhdp_load_level(mhdp_ctx *ctx, int level, long long n,
 
 /* Upload the stores and factor them on the device (synchronises): batched patch LU with
  * partial pivoting for every level >= 1 (kernel K6) and the dense
- * coarse LU of level 0 (K7; stand-in for MUMPS).  Errors: ESINGULAR names the
+ * coarse LU of level 0 (K7; stand-in for MUMPS) and, from its factors, the explicit
+ * coarse inverse X = A_0^-1 (column j = the LU solve of e_j; 8 n_0^2 bytes).  Errors: ESINGULAR names the
  * level and patch (mhdp_last_error's `where` = level*2^32 + patch; patch -1 = coarse). */
 mhdp_status mhdp_setup(mhdp_ctx *ctx);
 
@@ -153,7 +154,8 @@ mhdp_status mhdp_smooth(mhdp_ctx *ctx, int level, int nsweeps, int x_is_zero,
 mhdp_status mhdp_restrict(mhdp_ctx *ctx, int level, const double *r_dev, double *rc_dev);
 /* x <- x + P_l ec (K5, prolongation from level-1)                                      */
 mhdp_status mhdp_prolong_add(mhdp_ctx *ctx, int level, const double *ec_dev, double *x_dev);
-/* x = A_0^{-1} b by the dense coarse LU (K8)                                            */
+/* x = A_0^{-1} b (K8): x_i = sum_j X_ij b_j with X from the coarse LU, each row summed in
+ * the R-dot order (reading R-coarse).  b and x must not alias.                         */
 mhdp_status mhdp_coarse_solve(mhdp_ctx *ctx, const double *b_dev, double *x_dev);
 /* x = V_l(b) with zero initial guess on level `level` (finest: n_levels-1), P:643:
  * nu_pre sweeps, residual, restrict, recurse, prolong-add, nu_post sweeps.  Repeated

@@ -39,6 +39,8 @@ typedef struct {
     OLevel *lv;
     double *clu;      /* coarse LU (row-major n0*n0) */
     int *cperm;
+    double *cinv;     /* X = A_0^-1 (row-major n0*n0), R-coarse */
+    int cstat;        /* status of the coarse factorisation */
     int status;
 } OCtx;
 
@@ -54,7 +56,7 @@ static void level_free(OLevel *L) {
 void orc_destroy(OCtx *c) {
     if (!c) return;
     for (int l = 0; l < c->nlev; l++) level_free(&c->lv[l]);
-    free(c->lv); free(c->clu); free(c->cperm); free(c);
+    free(c->lv); free(c->clu); free(c->cperm); free(c->cinv); free(c);
 }
 
 /* dparams: Re, Rem, S, gamma, sigma, mu, theta, dt ; iparams: nu_pre, nu_post, picard
@@ -335,9 +337,12 @@ int orc_prolong_add(const OCtx *c, int l, const double *ec, double *x) {
     return 0;
 }
 
-/* ---------------- coarse solve (dense LU, R-coarse) ---------------- */
+/* ---------------- coarse solve (dense LU, R-coarse) ----------------
+ * The coarse operator is factored by R-lu (the stand-in for MUMPS) and its
+ * inverse X = A_0^-1 is formed column by column as the R-lu solve of the unit vectors;
+ * the coarse solve is x_i = sum_j X_ij b_j in the R-dot order (od_dot of row i).   */
 static int coarse_factor(OCtx *c) {
-    if (c->clu) return 0;
+    if (c->clu) return c->cstat;
     OLevel *L = &c->lv[0];
     i64 n = L->s.n;
     c->clu = calloc((size_t)((n * n) > 0 ? n * n : 1), sizeof(double));
@@ -348,12 +353,24 @@ static int coarse_factor(OCtx *c) {
             c->clu[i * n + L->A.ci[t]] = L->A.v[t];
             if (fabs(L->A.v[t]) > amax) amax = fabs(L->A.v[t]);
         }
-    return od_lu(c->clu, (int)n, c->cperm, amax);
+    c->cstat = od_lu(c->clu, (int)n, c->cperm, amax);
+    if (c->cstat) return c->cstat;
+    c->cinv = malloc(sizeof(double) * (size_t)((n * n) > 0 ? n * n : 1));
+    double *e = calloc((size_t)(n ? n : 1), sizeof(double)), *col = malloc(sizeof(double) * (n ? n : 1));
+    for (i64 j = 0; j < n; j++) {
+        e[j] = 1.0;
+        od_lu_solve(c->clu, (int)n, c->cperm, e, col);
+        e[j] = 0.0;
+        for (i64 i = 0; i < n; i++) c->cinv[i * n + j] = col[i];
+    }
+    free(e); free(col);
+    return 0;
 }
 
 int orc_coarse_solve(OCtx *c, const double *b, double *x) {
     if (coarse_factor(c)) return 1;
-    od_lu_solve(c->clu, (int)c->lv[0].s.n, c->cperm, b, x);
+    i64 n = c->lv[0].s.n;
+    for (i64 i = 0; i < n; i++) x[i] = od_dot(c->cinv + i * n, b, n);
     return 0;
 }
 

@@ -131,5 +131,7 @@ void opt_free(OPatches *pt);
  * returns 0, or k+1 if |pivot| <= 1e-14 * amax at step k.                       */
 int od_lu(double *a, int n, int *perm, double amax);
 void od_lu_solve(const double *lu, int n, const int *perm, const double *r, double *z);
+/* R-dot inner product (blocks of 256, fma chains from +0.0, pairwise tree) */
+double od_dot(const double *a, const double *b, i64 n);
 
 #endif

@@ -57,10 +57,9 @@ struct mhdp_ctx {
     bool setup_done = false;
     // coarse factor
     int n0 = 0;
-    double *clut = nullptr;    // column-major LU of A_0
+    double *cinv = nullptr;    // X = A_0^-1, column-major (R-coarse)
     int *cperm = nullptr;
-    double *cz = nullptr;
-    double *crdiag = nullptr;
+    double *cpart = nullptr;   // n0 * ceil(n0/256) partial sums of x = X b
     // scratch
     int *d_status = nullptr;
     double *d_scal = nullptr;  // dot partials + results
@@ -145,7 +144,7 @@ void free_device(mhdp_ctx *c) {
     for (void *p : c->allocs) cudaFree(p);
     c->allocs.clear();
     c->D.clear();
-    c->clut = nullptr; c->cperm = nullptr; c->cz = nullptr; c->crdiag = nullptr;
+    c->cinv = nullptr; c->cperm = nullptr; c->cpart = nullptr;
     c->d_status = nullptr; c->d_scal = nullptr;
     c->gV = c->gZ = c->gw = nullptr; c->g_cap = 0;
     c->fV = c->fZ = c->fw = c->fpart = c->fscal = nullptr; c->f_cap = 0;
@@ -337,7 +336,7 @@ void sweep(mhdp_ctx *ctx, int l, const double *b, double *x, bool x_zero) {
 }
 
 void coarse_solve(mhdp_ctx *ctx, const double *b, double *x) {
-    launch_dense_solve(ctx->clut, ctx->crdiag, ctx->cperm, ctx->n0, b, x, ctx->cz, ctx->stream);
+    launch_coarse_apply(ctx->cinv, ctx->n0, b, x, ctx->cpart, ctx->stream);
 }
 
 // scalar workspace layout of a GMRES(m) smoother / FGMRES(m)
@@ -635,7 +634,7 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
             return fail(ctx, MHDP_ESINGULAR, buf, ((long long)l << 32) + patch);
         }
     }
-    // K7: coarse LU (dense, row-major) then the column-major copy for K8
+    // K7: coarse LU (dense, row-major), then K8 setup: X = A_0^-1 from the factors
     const HostLevel &H0 = ctx->H[0];
     const int64_t n0 = H0.n;
     if (n0 > 20000) return fail(ctx, MHDP_EINVAL, "coarse level too large for the dense LU");
@@ -648,19 +647,19 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         CK(cudaMalloc(&a, sizeof(double) * std::max<int64_t>(1, n0 * n0)));
         CK(cudaMemcpy(a, dense.data(), sizeof(double) * n0 * n0, cudaMemcpyHostToDevice));
         if ((st = dalloc(ctx, &ctx->cperm, n0))) return st;
-        if ((st = dalloc(ctx, &ctx->clut, n0 * n0))) return st;
-        if ((st = dalloc(ctx, &ctx->cz, 2 * n0))) return st;
-        if ((st = dalloc(ctx, &ctx->crdiag, n0))) return st;
+        if ((st = dalloc(ctx, &ctx->cinv, n0 * n0))) return st;
+        if ((st = dalloc(ctx, &ctx->cpart, n0 * ((n0 + 255) / 256)))) return st;
         CK(cudaMemset(ctx->d_status, 0, sizeof(int)));
         launch_dense_lu(a, (int)n0, ctx->cperm, ctx->d_status, ctx->d_scal, ctx->stream);
-        launch_transpose(a, ctx->clut, (int)n0, ctx->stream);
-        launch_recip_diag(ctx->clut, (int)n0, ctx->crdiag, ctx->stream);
         if ((st = check_launch(ctx))) return st;
         CK(cudaStreamSynchronize(ctx->stream));
-        cudaFree(a);
         int bad = 0;
         CK(cudaMemcpy(&bad, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost));
-        if (bad) return fail(ctx, MHDP_ESINGULAR, "singular coarse operator", -1);
+        if (bad) { cudaFree(a); return fail(ctx, MHDP_ESINGULAR, "singular coarse operator", -1); }
+        launch_coarse_inverse(a, ctx->cperm, (int)n0, ctx->cinv, ctx->stream);
+        if ((st = check_launch(ctx))) { cudaFree(a); return st; }
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(a);
     }
     ctx->setup_done = true;
     return MHDP_OK;

@@ -73,14 +73,11 @@ void launch_prolong_add(const DevCsr &P, const double *ec, double *x, cudaStream
 // K7: dense LU with partial pivoting of the row-major n x n matrix a (in place)
 // perm[n]; status[0] = 0 or (step+1) of the first singular pivot; amax = max|a|
 void launch_dense_lu(double *a, int n, int *perm, int *status, double *scratch, cudaStream_t s);
-// transpose the row-major factor into the column-major copy used by the solve
-void launch_transpose(const double *a, double *at, int n, cudaStream_t s);
-// K8: x = U^-1 L^-1 P b with the column-major factor lut
-// K8: x = U^-1 L^-1 P b; rdiag = RN(1/u_jj) (launch_recip_diag); z: 2n doubles of scratch.
-// x must not alias b (x is pre-filled with a sentinel).
-void launch_dense_solve(const double *lut, const double *rdiag, const int *perm, int n, const double *b, double *x,
-                        double *z, cudaStream_t s);
-void launch_recip_diag(const double *lut, int n, double *rdiag, cudaStream_t s);
+// K8 (R-coarse): X = A_0^-1 column-major (n*n doubles) from the K7 factors (setup), and
+// x = X b with R-dot rows; part: n * ceil(n/256) doubles of scratch; n <= 256 * CINV_MAXB
+static constexpr int CINV_MAXB = 80;
+void launch_coarse_inverse(const double *lu, const int *perm, int n, double *X, cudaStream_t s);
+void launch_coarse_apply(const double *X, int n, const double *b, double *x, double *part, cudaStream_t s);
 // K9 vector ops (deterministic reductions)
 void launch_dot(const double *a, const double *b, int64_t n, double *partials, double *out, cudaStream_t s);
 void launch_axpy(double *y, double alpha, const double *x, int64_t n, cudaStream_t s);   // y = fma(alpha, x, y)

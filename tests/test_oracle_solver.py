@@ -226,6 +226,30 @@ def test_vcycle_special_cases(oracle_mod):
     assert np.linalg.norm(v - (3.0 * o2.vcycle(b1) - o2.vcycle(b2))) <= 1e-12 * np.linalg.norm(v)
 
 
+@pytest.mark.parametrize("name,N", [("c1", 8), ("c5", 2)])
+def test_coarse_solve_is_explicit_inverse(oracle_mod, name, N):
+    """R-coarse: column j of X = A_0^-1 is the R-lu solve of e_j (so the coarse solve of
+    e_j returns it exactly: the R-dot row sums against a unit vector are exact), X A_0 = I
+    and X b = A_0^-1 b within the conditioning bound, against numpy's LAPACK solve."""
+    cfg = small(name, N, 1)
+    o = make(oracle_mod, cfg)
+    n = o.n()
+    A = o.csr().to_scipy().toarray()
+    X = np.empty((n, n))
+    for j in range(n):
+        e = np.zeros(n); e[j] = 1.0
+        X[:, j] = o.coarse_solve(e)
+        if j % 17 == 0:
+            assert np.array_equal(X[:, j], oracle_mod.dense_lu_solve(A, e)[0])
+    u = 2.0 ** -53
+    nA, nX = np.linalg.norm(A, 2), np.linalg.norm(X, 2)
+    # columns are backward-stable solves: ||A X - I|| <= c n u ||A|| ||X||
+    assert np.linalg.norm(A @ X - np.eye(n), 2) <= 4 * n * u * nA * nX
+    b = np.random.default_rng(4).standard_normal(n)
+    ref = np.linalg.solve(A, b)
+    assert np.linalg.norm(o.coarse_solve(b) - ref) <= 4 * n * u * nA * nX * np.linalg.norm(ref)
+
+
 def test_vcycle_two_level_definition(oracle_mod):
     """V = S^nu2 (x + P A_c^-1 P^T (b - A S^nu1 0)) composed from the pinned parts."""
     cfg = CONFIGS["c1"]
