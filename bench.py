@@ -157,6 +157,63 @@ def run_reference(args):
 # ----------------------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------------------
+def _timed(stream, fn, reps=1):
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        out = fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, out
+
+
+def run_variants(cfg, seed, dev, stream):
+    """NEXT-4: the c5 operator in the transient (implicit Euler, dt = 0.01 as P:656) Newton
+    variant with the Lorentz term of a seeded B^n (S = 1): V-cycle time and the paper's
+    FGMRES(GMRES(6)-smoothed V) solve.  NEXT-3: the coupled 4x4 Newton system (3D, 24^3,
+    3 levels, Picard, Re = Re_m = 10, S = 1, gamma = 100) solved by outer FGMRES with the
+    block upper-triangular preconditioner (inner FGMRES(2) solves).  Setup excluded."""
+    import dataclasses
+    import torch
+    from paper_2104_14855_b200 import mhdp, workloads
+    out = {}
+    cfg4 = dataclasses.replace(cfg, dt=0.01, S=1.0)
+    ctx = mhdp.Context(dev.index, stream.cuda_stream)
+    w, b, _ = workloads.draw(cfg4, 1, seed)
+    ctx.assemble(cfg4, w, bn=workloads.magnetic_potential(cfg4, seed))
+    w, b, _ = workloads.draw(cfg4, ctx.n(), seed)
+    ctx.setup()
+    bd = torch.from_numpy(b).to(dev)
+    xd = torch.empty_like(bd)
+    ctx.vcycle(bd, xd)
+    ms_v, _ = _timed(stream, lambda: ctx.vcycle(bd, xd), reps=5)
+    ctx.set_smoother("gmres", 6)
+    ms_f, (its, rel, conv) = _timed(stream, lambda: ctx.fgmres(bd, xd, maxit=60))
+    out["next4_c5_transient_lorentz"] = {
+        "config": "c5 operator + (1/dt)(u,v), dt = 0.01, + S(u x B^n, v x B^n), S = 1", "vcycle_ms": ms_v,
+        "fgmres_gmres6_vcycle": {"its": its, "converged": conv, "relres": rel, "ms": ms_f}}
+    ctx.close()
+    del ctx
+    cfg3 = dataclasses.replace(workloads.small("c5", 24, 3), Re=10.0, Rem=10.0, S=1.0, gamma=100.0, picard=1)
+    w3, _, _ = workloads.draw(cfg3, 1, seed)
+    co = mhdp.Coupled(cfg3, w3, workloads.magnetic_potential(cfg3, seed), device=dev.index,
+                      stream=stream.cuda_stream, smoother="gmres", smoother_its=6)
+    r = np.random.default_rng(seed).standard_normal(co.n)
+    r[co.nu:co.nu + co.np_] -= r[co.nu:co.nu + co.np_].mean()     # consistent: Q = L^2_0 (P:106)
+    rd = torch.from_numpy(r).to(dev)
+    yd = torch.empty_like(rd)
+    co.precondition(rd, yd)
+    ms_p, _ = _timed(stream, lambda: co.precondition(rd, yd), reps=3)
+    ms_o, (its3, rel3, conv3) = _timed(stream, lambda: co.fgmres(rd, yd, maxit=40))
+    out["next3_coupled_outer"] = {
+        "config": "3D 24^3 x 6 tets, 3 levels, Picard, Re = Re_m = 10, S = 1, gamma = 100",
+        "dofs": {"u": co.nu, "p": co.np_, "E": co.nE, "B": co.nB}, "precondition_ms": ms_p,
+        "fgmres": {"its": its3, "converged": conv3, "relres": rel3, "ms": ms_o}}
+    co.close()
+    return out
+
+
 def run_ours(args):
     import torch
     from paper_2104_14855_b200 import mhdp, workloads
@@ -298,6 +355,11 @@ def run_ours(args):
                   "next1_fgmres": {"its": its_f, "converged": conv_f, "relres": rel_f, "ms": ms_f},
                   "tolerance": "max(1e-7 |b|, 1e-7), Euclidean (P:654)"}
 
+    # ---- NEXT-4 / NEXT-3 measured on the same kernels (skipped with --no-variants) ----
+    variants = None
+    if not args.no_variants:
+        variants = run_variants(cfg, seed, dev, stream)
+
     # algorithmic bytes: K2 per patch i: 8 n_i^2 factor + 8 n_i gathered r
     # + 8 n_i written y; sweep: 8 sum n_i^2 + 8 nnz + 24 n
     k2_bytes = 8 * fin["sum_n2"] + 16 * fin["sum_n"]
@@ -352,6 +414,7 @@ def run_ours(args):
             "setup_s": {"host_assembly": t_asm, "device_setup": t_setup},
             "cpu_baseline": cpu,
             "solves": solves,
+            "variants": variants,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -369,6 +432,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solves", action="store_true", help="skip the GMRES / FGMRES solves")
+    ap.add_argument("--no-variants", action="store_true", help="skip the NEXT-4 / NEXT-3 measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
