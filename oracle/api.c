@@ -59,7 +59,7 @@ void orc_destroy(OCtx *c) {
     free(c->lv); free(c->clu); free(c->cperm); free(c->cinv); free(c);
 }
 
-/* dparams: Re, Rem, S, gamma, sigma, mu, theta, dt ; iparams: nu_pre, nu_post, picard
+/* dparams: Re, Rem, S, gamma, sigma, mu, theta, dt ; iparams: nu_pre, nu_post, picard, degree
  * w_fine: potential of the advecting field at the finest vertices (vertex order of
  *         R-mesh): 2D stream function psi (1 per vertex), 3D vector potential A (3 per vertex).
  * cmask_fine: NULL, or a finest-level cell mask (only then: assemble the finest
@@ -74,13 +74,15 @@ OCtx *orc_create_masked(int block, int dim, int N, int nlev, const double *dpara
     c->p.sigma = dparams[4]; c->p.mu = dparams[5]; c->theta = dparams[6];
     c->p.nu_pre = iparams[0]; c->p.nu_post = iparams[1];
     c->p.dt = dparams[7]; c->p.picard = iparams[2];
+    int degree = iparams[3];
+    if (!(degree == 1 || (degree == 2 && block == ORC_EB && dim == 2))) { free(c); return NULL; }
     c->lv = calloc((size_t)nlev, sizeof(OLevel));
     int lo = cmask_fine ? nlev - 1 : 0;
     for (int l = nlev - 1; l >= lo; l--) {
         OLevel *L = &c->lv[l];
         int Nl = N >> (nlev - 1 - l), step = 1 << (nlev - 1 - l);
         om_build(&L->m, dim, Nl);
-        os_build(&L->s, &L->m, block);
+        os_build(&L->s, &L->m, block, degree);
         /* w on this level: injection of the finest vertex values (R-w) */
         int nc = dim == 2 ? 1 : 3;
         L->w = malloc(sizeof(double) * nc * L->m.nv);

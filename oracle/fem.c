@@ -354,6 +354,17 @@ i64 oc_find(const OCsr *a, i64 row, int col) {
 /* free DoFs (with -1 for constrained) of the local basis of cell c, in local order */
 static int cell_dofs(const OMesh *m, const OSpace *s, i64 c, int *out) {
     int d = m->dim, n = 0;
+    if (s->degree == 2) {             /* CG2 (vertices, edges) then RT2 (edges x 2, cell x 2) */
+        for (int a = 0; a < 3; a++) out[n++] = s->vdof[m->cv[c * 3 + a]];
+        for (int q = 0; q < 3; q++) out[n++] = s->edof[m->ce[c * 3 + q]];
+        for (int q = 0; q < 3; q++) {
+            int f0 = s->fdof[om_facet_of_cell(m, c, q)];
+            out[n++] = f0 < 0 ? -1 : f0;
+            out[n++] = f0 < 0 ? -1 : f0 + 1;
+        }
+        out[n++] = s->cdof[c]; out[n++] = s->cdof[c] + 1;
+        return n;
+    }
     if (s->block == ORC_EB) {
         if (d == 2) for (int a = 0; a < 3; a++) out[n++] = s->vdof[m->cv[c * 3 + a]];
         else for (int q = 0; q < 6; q++) out[n++] = s->edof[m->ce[c * 6 + q]];
@@ -706,9 +717,20 @@ static void assemble_vel(OCsr *A, Accum *S, signed char *cnt, const OMesh *m, co
         if (cnt[t]) S->acc[t] += (real)(G * cnt[t]) / (d * d);
 }
 
+static void assemble_eb2(OCsr *A, Accum *S, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
+                         const unsigned char *cmask);
+
 int oa_assemble_masked(OCsr *A, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
                        const unsigned char *cmask) {
     build_pattern(A, m, s);
+    if (s->degree == 2) {
+        Accum S2;
+        S2.acc = calloc((size_t)(A->nnz ? A->nnz : 1), sizeof(real));
+        assemble_eb2(A, &S2, m, s, p, w, cmask);
+        finish(A, &S2);
+        free(S2.acc);
+        return 0;
+    }
     signed char *cnt = calloc((size_t)(A->nnz ? A->nnz : 1), 1);
     Accum S;
     S.acc = calloc((size_t)(A->nnz ? A->nnz : 1), sizeof(real));
@@ -778,7 +800,10 @@ static double dof_functional(int block, int d, int kind, int sub, const real V[3
     return (double)(sacc / nev);
 }
 
+static int op_prolongation2(OCsr *P, const OMesh *mf, const OSpace *sf, const OMesh *mc, const OSpace *sc);
+
 int op_prolongation(OCsr *P, const OMesh *mf, const OSpace *sf, const OMesh *mc, const OSpace *sc) {
+    if (sf->degree == 2) return op_prolongation2(P, mf, sf, mc, sc);
     int d = mf->dim, nvc = d + 1, nle = om_nle(d);
     memset(P, 0, sizeof(*P));
     /* lowest-index fine cell containing each entity */
@@ -929,7 +954,12 @@ void oa_quadrature(const OMesh *m, double *pts, double *wts) {
     }
 }
 
+static void oa_load2(const OMesh *m, const OSpace *s, const double *fv, double *out);
+static void oa_eval2(const OMesh *m, const OSpace *s, const double *coef, double *fv);
+static double oa_duality_error2(const OMesh *m, const OSpace *s);
+
 void oa_load(const OMesh *m, const OSpace *s, const double *fv, double *out) {
+    if (s->degree == 2) { oa_load2(m, s, fv, out); return; }
     int nq = oa_nq(m->dim), nc = oa_ncomp(s);
     real xq[64][3], wq[64];
     memset(out, 0, sizeof(double) * s->n);
@@ -957,6 +987,7 @@ void oa_load(const OMesh *m, const OSpace *s, const double *fv, double *out) {
 }
 
 void oa_eval(const OMesh *m, const OSpace *s, const double *coef, double *fv) {
+    if (s->degree == 2) { oa_eval2(m, s, coef, fv); return; }
     int nq = oa_nq(m->dim), nc = oa_ncomp(s);
     real xq[64][3], wq[64];
     memset(fv, 0, sizeof(double) * m->nc * nq * nc);
@@ -983,6 +1014,7 @@ void oa_eval(const OMesh *m, const OSpace *s, const double *coef, double *fv) {
  * (DoF duality of R-basis).  Each cell's functionals are applied to
  * that cell's own basis functions, matched through the global DoF numbering.   */
 double oa_duality_error(const OMesh *m, const OSpace *s) {
+    if (s->degree == 2) return oa_duality_error2(m, s);
     int d = m->dim;
     double worst = 0;
     for (i64 c = 0; c < m->nc; c++) {
@@ -1174,4 +1206,422 @@ int oa_assemble_coupling(OCsr *Bt, OCsr *J, OCsr *Dt, OCsr *G, const OMesh *m, c
     finish_floor(G, &SG, floor_E);
     free(SB.acc); free(SJ.acc); free(SD.acc); free(SG.acc);
     return 0;
+}
+
+/* ========================================================================= */
+/* NEXT-2: degree k = 2 for the 2D E-B block, E in CG2, B in RT2      */
+/* (the 2D complex CG2 -> RT2 -> DG1 of P:188).  Reading R-basis2:      */
+/*   CG2: point values at the vertices and at the edge midpoints;              */
+/*   RT2 (dim 8 = P1^2 + x P1~): per edge e = (a < b) with the global normal   */
+/*     n_e of R-orient, N_{e,s}(B) = int_e (B.n_e) lambda_s ds with lambda_0 = */
+/*     lambda_a, lambda_1 = lambda_b (N_{e,0} + N_{e,1} = the k = 1 flux); per */
+/*     cell N_{K,r}(B) = N int_K B_r dx, r = x, y (N cells per side).          */
+/* Local bases are dual to these functionals: the functionals applied to a    */
+/* primal basis of the local space give a matrix that is inverted in `real`.  */
+/* Every integrand is a polynomial of degree <= 4: the q = 3 cell rule and the */
+/* 3-point edge rule are exact (R-quad).                                       */
+/* ========================================================================= */
+typedef struct { real c[2][6]; } Q2;   /* 2 components in xi = x - X0: 1, xi, eta, xi^2, xi eta, eta^2 */
+
+static void q2_eval(const Q2 *f, const Cell *K, const real *x, real *out) {
+    real a = x[0] - K->X[0][0], b = x[1] - K->X[0][1];
+    real mo[6] = {1, a, b, a * a, a * b, b * b};
+    for (int l = 0; l < 2; l++) {
+        real s = 0;
+        for (int k = 0; k < 6; k++) s += f->c[l][k] * mo[k];
+        out[l] = s;
+    }
+    out[2] = 0;
+}
+
+static void q2_grad(const Q2 *f, const Cell *K, const real *x, real g[2][2]) {
+    real a = x[0] - K->X[0][0], b = x[1] - K->X[0][1];
+    for (int l = 0; l < 2; l++) {
+        g[l][0] = f->c[l][1] + 2 * f->c[l][3] * a + f->c[l][4] * b;
+        g[l][1] = f->c[l][2] + f->c[l][4] * a + 2 * f->c[l][5] * b;
+    }
+}
+
+/* lambda_a = L[0] + L[1] xi + L[2] eta */
+static void bary_lin(const Cell *K, int a, real *L) { L[0] = a == 0 ? 1 : 0; L[1] = K->g[a][0]; L[2] = K->g[a][1]; }
+static real bary_at(const Cell *K, int a, const real *x) {
+    real L[3];
+    bary_lin(K, a, L);
+    return L[0] + L[1] * (x[0] - K->X[0][0]) + L[2] * (x[1] - K->X[0][1]);
+}
+
+/* coefficients of s * A * B for linears A, B */
+static void lin_mul(const real *A, const real *B, real s, real *c) {
+    c[0] = s * A[0] * B[0];
+    c[1] = s * (A[0] * B[1] + A[1] * B[0]);
+    c[2] = s * (A[0] * B[2] + A[2] * B[0]);
+    c[3] = s * A[1] * B[1];
+    c[4] = s * (A[1] * B[2] + A[2] * B[1]);
+    c[5] = s * A[2] * B[2];
+}
+
+/* CG2, local DoF a: a < 3 vertex a, lambda_a (2 lambda_a - 1); a = 3 + q local edge q
+ * (vertices i < j), 4 lambda_i lambda_j.  Scalar in component 0. */
+static Q2 basis_cg2(const Cell *K, int a) {
+    Q2 f;
+    memset(&f, 0, sizeof f);
+    if (a < 3) {
+        real L[3], L2[3];
+        bary_lin(K, a, L);
+        L2[0] = 2 * L[0] - 1; L2[1] = 2 * L[1]; L2[2] = 2 * L[2];
+        lin_mul(L, L2, 1, f.c[0]);
+    } else {
+        int lv[2];
+        om_edge_local_verts(2, a - 3, lv);
+        real Li[3], Lj[3];
+        bary_lin(K, lv[0], Li);
+        bary_lin(K, lv[1], Lj);
+        lin_mul(Li, Lj, 4, f.c[0]);
+    }
+    return f;
+}
+
+/* the 8 RT2 functionals of cell K (local order: edge q = 0..2, s = 0, 1; then r = 0, 1)
+ * applied to the vector field f; Ncells = cells per side of K's mesh */
+static void rt2_functionals(const Cell *K, int Ncells, const Q2 *f, real *out) {
+    real xq[64][3], wq[64];
+    for (int q = 0; q < 3; q++) {
+        int lv[2];
+        om_facet_local_verts(2, q, lv);
+        real P[3][3], A[3];
+        facet_points(K, q, P);
+        facet_area_vector(2, P, A);
+        real len = RSQRT(dot3(A, A));
+        int nq = facet_rule(2, P, xq, wq);
+        for (int s = 0; s < 2; s++) {
+            real acc = 0;
+            for (int t = 0; t < nq; t++) {
+                real v[3];
+                q2_eval(f, K, xq[t], v);
+                acc += wq[t] * (dot3(v, A) / len) * bary_at(K, lv[s], xq[t]);
+            }
+            out[2 * q + s] = acc;
+        }
+    }
+    int nq = cell_rule(K, 3, xq, wq);
+    for (int r = 0; r < 2; r++) {
+        real acc = 0;
+        for (int t = 0; t < nq; t++) {
+            real v[3];
+            q2_eval(f, K, xq[t], v);
+            acc += wq[t] * v[r];
+        }
+        out[6 + r] = (real)Ncells * acc;
+    }
+}
+
+/* Gauss-Jordan inverse with partial pivoting (n <= 8), row-major */
+static int mat_inv(int n, const real *a, real *inv) {
+    real w[8][16];
+    for (int i = 0; i < n; i++)
+        for (int j = 0; j < 2 * n; j++) w[i][j] = j < n ? a[i * n + j] : (real)(j - n == i);
+    for (int k = 0; k < n; k++) {
+        int p = k;
+        for (int i = k + 1; i < n; i++) if (RFABS(w[i][k]) > RFABS(w[p][k])) p = i;
+        if (w[p][k] == 0) return 1;
+        if (p != k) for (int j = 0; j < 2 * n; j++) { real t = w[k][j]; w[k][j] = w[p][j]; w[p][j] = t; }
+        real piv = w[k][k];
+        for (int j = 0; j < 2 * n; j++) w[k][j] /= piv;
+        for (int i = 0; i < n; i++)
+            if (i != k && w[i][k] != 0) {
+                real l = w[i][k];
+                for (int j = 0; j < 2 * n; j++) w[i][j] -= l * w[k][j];
+            }
+    }
+    for (int i = 0; i < n; i++) for (int j = 0; j < n; j++) inv[i * n + j] = w[i][n + j];
+    return 0;
+}
+
+/* RT2 local basis dual to rt2_functionals: primal basis e_x, xi e_x, eta e_x, e_y,
+ * xi e_y, eta e_y, xi (xi, eta), eta (xi, eta) */
+static void basis_rt2(const Cell *K, int Ncells, Q2 *B) {
+    Q2 p[8];
+    memset(p, 0, sizeof p);
+    p[0].c[0][0] = 1; p[1].c[0][1] = 1; p[2].c[0][2] = 1;
+    p[3].c[1][0] = 1; p[4].c[1][1] = 1; p[5].c[1][2] = 1;
+    p[6].c[0][3] = 1; p[6].c[1][4] = 1;
+    p[7].c[0][4] = 1; p[7].c[1][5] = 1;
+    real M[64], C[64], col[8];
+    for (int j = 0; j < 8; j++) {
+        rt2_functionals(K, Ncells, &p[j], col);
+        for (int i = 0; i < 8; i++) M[i * 8 + j] = col[i];
+    }
+    mat_inv(8, M, C);
+    for (int j = 0; j < 8; j++) {
+        memset(&B[j], 0, sizeof(Q2));
+        for (int k = 0; k < 8; k++)
+            for (int l = 0; l < 2; l++)
+                for (int t = 0; t < 6; t++) B[j].c[l][t] += C[k * 8 + j] * p[k].c[l][t];
+    }
+}
+
+/* global free DoFs of the CG2 and RT2 local bases of cell c */
+static void cell_dofs2(const OMesh *m, const OSpace *s, i64 c, int *gE, int *gB) {
+    for (int a = 0; a < 3; a++) gE[a] = s->vdof[m->cv[c * 3 + a]];
+    for (int q = 0; q < 3; q++) gE[3 + q] = s->edof[m->ce[c * 3 + q]];
+    for (int q = 0; q < 3; q++) {
+        int f0 = s->fdof[om_facet_of_cell(m, c, q)];
+        gB[2 * q] = f0 < 0 ? -1 : f0;
+        gB[2 * q + 1] = f0 < 0 ? -1 : f0 + 1;
+    }
+    gB[6] = s->cdof[c]; gB[7] = s->cdof[c] + 1;
+}
+
+/* E-B block at k = 2 (same forms as assemble_eb):
+ *   E rows: (E, F) - (1/Rem)(B, vcurl F) + delta (u^n x B, F)
+ *   B rows: (eta/dt)(B, C) + (vcurl E, C) + (1/Rem)(div B, div C)                 */
+static void assemble_eb2(OCsr *A, Accum *S, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
+                         const unsigned char *cmask) {
+    real xq[64][3], wq[64];
+    for (i64 c = 0; c < m->nc; c++) {
+        if (cmask && !cmask[c]) continue;
+        Cell K;
+        cell_geom(m, c, &K);
+        Q2 E[6], B[8];
+        int gE[6], gB[8];
+        for (int a = 0; a < 6; a++) E[a] = basis_cg2(&K, a);
+        basis_rt2(&K, m->N, B);
+        cell_dofs2(m, s, c, gE, gB);
+        double pot[4][3];
+        real wx[3];
+        cell_pot(m, c, w, pot);
+        cell_wind(&K, pot, wx);
+        real EE[36] = {0}, EB[48] = {0}, BE[48] = {0}, BB[64] = {0};
+        int nq = cell_rule(&K, 3, xq, wq);
+        for (int t = 0; t < nq; t++) {
+            real ev[6][3], curlE[6][2], bv[8][3], divB[8];
+            for (int a = 0; a < 6; a++) {
+                real g[2][2];
+                q2_eval(&E[a], &K, xq[t], ev[a]);
+                q2_grad(&E[a], &K, xq[t], g);
+                curlE[a][0] = g[0][1]; curlE[a][1] = -g[0][0];
+            }
+            for (int k = 0; k < 8; k++) {
+                real g[2][2];
+                q2_eval(&B[k], &K, xq[t], bv[k]);
+                q2_grad(&B[k], &K, xq[t], g);
+                divB[k] = g[0][0] + g[1][1];
+            }
+            for (int i = 0; i < 6; i++) {
+                for (int j = 0; j < 6; j++) EE[i * 6 + j] += wq[t] * ev[j][0] * ev[i][0];
+                for (int k = 0; k < 8; k++) {
+                    real wxb = p->picard ? 0 : (wx[0] * bv[k][1] - wx[1] * bv[k][0]) * ev[i][0];
+                    real ab = bv[k][0] * curlE[i][0] + bv[k][1] * curlE[i][1];
+                    EB[i * 8 + k] += wq[t] * (wxb - ab / p->Rem);
+                    BE[k * 6 + i] += wq[t] * ab;
+                }
+            }
+            for (int k = 0; k < 8; k++)
+                for (int l = 0; l < 8; l++) {
+                    real v = divB[l] * divB[k] / p->Rem;
+                    if (p->dt > 0) v += (bv[l][0] * bv[k][0] + bv[l][1] * bv[k][1]) / p->dt;
+                    BB[k * 8 + l] += wq[t] * v;
+                }
+        }
+        scatter(A, S, gE, 6, gE, 6, EE, 6);
+        scatter(A, S, gE, 6, gB, 8, EB, 8);
+        scatter(A, S, gB, 8, gE, 6, BE, 6);
+        scatter(A, S, gB, 8, gB, 8, BB, 8);
+    }
+}
+
+/* the fine functional of free DoF I (k = 2) applied to the coarse local basis function F
+ * living on coarse cell Kc; physical coordinates */
+static real dof_functional2(const OMesh *mf, const OSpace *sf, i64 I, const Q2 *F, const Cell *Kc) {
+    int kind = sf->dkind[I], ent = sf->dent[I], sub = sf->dsub[I];
+    real v[3];
+    if (kind == 0) {
+        real x[3] = {(real)mf->lat[3 * ent] / mf->N, (real)mf->lat[3 * ent + 1] / mf->N, 0};
+        q2_eval(F, Kc, x, v);
+        return v[0];
+    }
+    real P[3][3] = {{0}};
+    if (kind <= 2)
+        for (int a = 0; a < 2; a++)
+            for (int k = 0; k < 2; k++) P[a][k] = (real)mf->lat[3 * mf->ev[2 * ent + a] + k] / mf->N;
+    if (kind == 1) {
+        real x[3] = {(P[0][0] + P[1][0]) / 2, (P[0][1] + P[1][1]) / 2, 0};
+        q2_eval(F, Kc, x, v);
+        return v[0];
+    }
+    real xq[64][3], wq[64];
+    if (kind == 2) {
+        real A[3];
+        facet_area_vector(2, P, A);
+        real len = RSQRT(dot3(A, A));
+        real t[3] = {P[1][0] - P[0][0], P[1][1] - P[0][1], 0};
+        int nq = facet_rule(2, P, xq, wq);
+        real acc = 0;
+        for (int q = 0; q < nq; q++) {
+            q2_eval(F, Kc, xq[q], v);
+            real d[3] = {xq[q][0] - P[0][0], xq[q][1] - P[0][1], 0};
+            real lam1 = dot3(d, t) / dot3(t, t);
+            acc += wq[q] * (dot3(v, A) / len) * (sub == 0 ? 1 - lam1 : lam1);
+        }
+        return acc;
+    }
+    Cell Kf;
+    cell_geom(mf, ent, &Kf);
+    int nq = cell_rule(&Kf, 3, xq, wq);
+    real acc = 0;
+    for (int q = 0; q < nq; q++) {
+        q2_eval(F, Kc, xq[q], v);
+        acc += wq[q] * v[sub];
+    }
+    return (real)mf->N * acc;
+}
+
+/* R-prol at k = 2: P_IJ = N_I^fine(phi_J^coarse), evaluated on the parent coarse cell of
+ * a fine cell containing DoF I's entity, in `real`; each row rounded as in R-exact. */
+static int op_prolongation2(OCsr *P, const OMesh *mf, const OSpace *sf, const OMesh *mc, const OSpace *sc) {
+    memset(P, 0, sizeof(*P));
+    int *vfirst = malloc(sizeof(int) * mf->nv), *efirst = malloc(sizeof(int) * mf->ne);
+    for (i64 t = 0; t < mf->nv; t++) vfirst[t] = -1;
+    for (i64 t = 0; t < mf->ne; t++) efirst[t] = -1;
+    for (i64 c = 0; c < mf->nc; c++) {
+        for (int a = 0; a < 3; a++) if (vfirst[mf->cv[c * 3 + a]] < 0) vfirst[mf->cv[c * 3 + a]] = (int)c;
+        for (int q = 0; q < 3; q++) if (efirst[mf->ce[c * 3 + q]] < 0) efirst[mf->ce[c * 3 + q]] = (int)c;
+    }
+    i64 cap = 1024, nt = 0;
+    long long *idx = malloc(sizeof(long long) * 3 * cap);
+    real *tv = malloc(sizeof(real) * cap);
+    for (i64 I = 0; I < sf->n; I++) {
+        int kind = sf->dkind[I], ent = sf->dent[I];
+        int cf = kind == 0 ? vfirst[ent] : (kind == 3 ? ent : efirst[ent]);
+        i64 ccell = parent_cell(mf, mc, cf);
+        Cell Kc;
+        cell_geom(mc, ccell, &Kc);
+        Q2 F[8];
+        int gE[6], gB[8], nb;
+        const int *gJ;
+        cell_dofs2(mc, sc, ccell, gE, gB);
+        if (kind <= 1) { for (int a = 0; a < 6; a++) F[a] = basis_cg2(&Kc, a); nb = 6; gJ = gE; }
+        else { basis_rt2(&Kc, mc->N, F); nb = 8; gJ = gB; }
+        for (int b = 0; b < nb; b++) {
+            if (gJ[b] < 0) continue;
+            real val = dof_functional2(mf, sf, I, &F[b], &Kc);
+            if (nt == cap) { cap *= 2; idx = realloc(idx, sizeof(long long) * 3 * cap); tv = realloc(tv, sizeof(real) * cap); }
+            idx[3 * nt] = I; idx[3 * nt + 1] = gJ[b]; idx[3 * nt + 2] = nt; tv[nt] = val; nt++;
+        }
+    }
+    qsort(idx, (size_t)nt, 3 * sizeof(long long), cmp_ij);
+    /* row rounding (R-exact grid); zeros dropped.  Reading R-prol2: the exact entries are
+     * rationals with small denominators, so |x| < 2^-30 max|row| can only be the residue
+     * of an exact cancellation (it is 0 exactly; the fp64 build cannot reach the grid). */
+    P->n = sf->n;
+    P->rp = calloc((size_t)sf->n + 1, sizeof(i64));
+    P->ci = malloc(sizeof(int) * (nt ? nt : 1));
+    P->v = malloc(sizeof(double) * (nt ? nt : 1));
+    i64 used = 0;
+    for (i64 t0 = 0; t0 < nt;) {
+        i64 t1 = t0;
+        while (t1 < nt && idx[3 * t1] == idx[3 * t0]) t1++;
+        double mx = 0;
+        for (i64 t = t0; t < t1; t++) { double h = (double)tv[idx[3 * t + 2]]; if (fabs(h) > mx) mx = fabs(h); }
+        int E = 0;
+        if (mx > 0) frexp(mx, &E);
+        for (i64 t = t0; t < t1; t++) {
+            real x = tv[idx[3 * t + 2]];
+            double h = (double)x, l = (double)(x - (real)h);
+            double v = (mx > 0 && fabs(h) >= ldexp(mx, -30)) ? grid_round(h, l, E) : 0.0;
+            if (v == 0.0) continue;
+            P->ci[used] = (int)idx[3 * t + 1];
+            P->v[used] = v;
+            used++;
+            P->rp[idx[3 * t] + 1]++;
+        }
+        t0 = t1;
+    }
+    for (i64 i = 0; i < sf->n; i++) P->rp[i + 1] += P->rp[i];
+    P->nnz = used;
+    free(idx); free(tv); free(vfirst); free(efirst);
+    return 0;
+}
+
+/* k = 2 local basis for the MMS helpers: E (component 0 of the E-B field triple) then B */
+static int local_basis2(const OMesh *m, const OSpace *s, i64 c, const Cell *K, Q2 *F, int *gi, int *off, int *ncp) {
+    int gE[6], gB[8];
+    cell_dofs2(m, s, c, gE, gB);
+    for (int a = 0; a < 6; a++) { F[a] = basis_cg2(K, a); gi[a] = gE[a]; off[a] = 0; ncp[a] = 1; }
+    basis_rt2(K, m->N, F + 6);
+    for (int k = 0; k < 8; k++) { gi[6 + k] = gB[k]; off[6 + k] = 1; ncp[6 + k] = 2; }
+    return 14;
+}
+
+static void oa_load2(const OMesh *m, const OSpace *s, const double *fv, double *out) {
+    int nq = oa_nq(2), nc = oa_ncomp(s);
+    real xq[64][3], wq[64];
+    memset(out, 0, sizeof(double) * s->n);
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        Q2 F[14];
+        int gi[14], off[14], ncp[14];
+        int nb = local_basis2(m, s, c, &K, F, gi, off, ncp);
+        cell_rule(&K, 4, xq, wq);
+        for (int a = 0; a < nb; a++) {
+            if (gi[a] < 0) continue;
+            real acc = 0;
+            for (int t = 0; t < nq; t++) {
+                real v[3];
+                q2_eval(&F[a], &K, xq[t], v);
+                const double *f = fv + ((i64)c * nq + t) * nc + off[a];
+                real d = 0;
+                for (int k = 0; k < ncp[a]; k++) d += f[k] * v[k];
+                acc += wq[t] * d;
+            }
+            out[gi[a]] += (double)acc;
+        }
+    }
+}
+
+static void oa_eval2(const OMesh *m, const OSpace *s, const double *coef, double *fv) {
+    int nq = oa_nq(2), nc = oa_ncomp(s);
+    real xq[64][3], wq[64];
+    memset(fv, 0, sizeof(double) * m->nc * nq * nc);
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        Q2 F[14];
+        int gi[14], off[14], ncp[14];
+        int nb = local_basis2(m, s, c, &K, F, gi, off, ncp);
+        cell_rule(&K, 4, xq, wq);
+        for (int a = 0; a < nb; a++) {
+            if (gi[a] < 0) continue;
+            for (int t = 0; t < nq; t++) {
+                real v[3];
+                q2_eval(&F[a], &K, xq[t], v);
+                double *f = fv + ((i64)c * nq + t) * nc + off[a];
+                for (int k = 0; k < ncp[a]; k++) f[k] += coef[gi[a]] * (double)v[k];
+            }
+        }
+    }
+}
+
+/* duality N_i(phi_j) = delta_ij at k = 2: the global fine functionals (dof_functional2,
+ * written independently of rt2_functionals) applied to each cell's local basis */
+static double oa_duality_error2(const OMesh *m, const OSpace *s) {
+    double worst = 0;
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        Q2 F[14];
+        int gi[14], off[14], ncp[14];
+        int nb = local_basis2(m, s, c, &K, F, gi, off, ncp);
+        for (int i = 0; i < nb; i++) {
+            if (gi[i] < 0) continue;
+            for (int j = 0; j < nb; j++) {
+                if (gi[j] < 0 || off[j] != off[i]) continue;
+                double v = (double)dof_functional2(m, s, gi[i], &F[j], &K);
+                double e = fabs(v - (gi[i] == gi[j] ? 1.0 : 0.0));
+                if (e > worst) worst = e;
+            }
+        }
+    }
+    return worst;
 }

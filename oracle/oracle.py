@@ -151,7 +151,8 @@ class Oracle:
         self.N = N
         dp = np.array([cfg.Re, cfg.Rem, cfg.S, cfg.gamma, cfg.sigma, cfg.mu, cfg.theta,
                        getattr(cfg, "dt", 0.0)], dtype=np.float64)
-        ip = np.array([cfg.nu, cfg.nu, int(getattr(cfg, "picard", 0))], dtype=np.int32)
+        ip = np.array([cfg.nu, cfg.nu, int(getattr(cfg, "picard", 0)), int(getattr(cfg, "degree", 1))],
+                      dtype=np.int32)
         self._w = np.ascontiguousarray(w, dtype=np.float64)
         self._bn = None if bn is None else np.ascontiguousarray(bn, dtype=np.float64)
         self._mask = None if cmask is None else np.ascontiguousarray(cmask, dtype=np.uint8)
@@ -381,7 +382,8 @@ class CoupledOracle:
         self._L = L = lib(exact)
         dp = np.array([cfg.Re, cfg.Rem, cfg.S, cfg.gamma, cfg.sigma, cfg.mu, cfg.theta,
                        getattr(cfg, "dt", 0.0)], dtype=np.float64)
-        ip = np.array([cfg.nu, cfg.nu, int(getattr(cfg, "picard", 0))], dtype=np.int32)
+        ip = np.array([cfg.nu, cfg.nu, int(getattr(cfg, "picard", 0)), int(getattr(cfg, "degree", 1))],
+                      dtype=np.int32)
         self._w = np.ascontiguousarray(w, np.float64)
         self._bn = None if bn is None else np.ascontiguousarray(bn, np.float64)
         self.h = L.orc_coupled_create(cfg.dim, cfg.N, cfg.levels, _d(dp), _i(ip), _d(self._w),

@@ -51,17 +51,20 @@ enum { ORC_EB = 0, ORC_VEL = 1 };
 
 typedef struct {
     int block, dim;
+    int degree;            /* k = 1, or 2 (NEXT-2: 2D E-B block, CG2 x RT2, reading R-basis2) */
     i64 n;                 /* free DoFs                                                */
     i64 nE;                /* E-B: number of free E DoFs (they come first)             */
     /* global free index per entity (or -1 if constrained) */
     int *vdof;             /* nv (2D E)                                               */
     int *edof;             /* ne (3D E: NED1)                                          */
-    int *fdof;             /* nfacet (B: RT)  or first velocity DoF of the facet (BDM: +0..dim-1) */
-    /* per free DoF: entity kind (0 vertex, 1 edge, 2 facet), entity id, sub index  */
+    int *fdof;             /* nfacet (B: RT)  or first velocity DoF of the facet (BDM: +0..dim-1);
+                              k = 2: first of the 2 RT2 DoFs of the edge                */
+    int *cdof;             /* nc (k = 2 only): first of the 2 interior RT2 DoFs of the cell */
+    /* per free DoF: entity kind (0 vertex, 1 edge, 2 facet, 3 cell), entity id, sub index */
     int *dkind, *dent, *dsub;
 } OSpace;
 
-int  os_build(OSpace *s, const OMesh *m, int block);
+int  os_build(OSpace *s, const OMesh *m, int block, int degree);   /* 0, or 1 if unsupported */
 void os_free(OSpace *s);
 
 /* ---------------- CSR ---------------- */

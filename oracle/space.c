@@ -17,9 +17,43 @@
 #include <string.h>
 #include "orc.h"
 
-int os_build(OSpace *s, const OMesh *m, int block) {
+/* k = 2 (NEXT-2; reading R-num2): 2D E-B only.  E (CG2): free vertex DoFs in
+ * vertex order, then free edge-midpoint DoFs in edge order; B (RT2): 2 DoFs per interior
+ * edge (edge order; sub 0/1 = moment against lambda of the lower/higher vertex), then 2
+ * DoFs per cell (cell order; sub r = component).  Boundary DoFs removed (R-bc).    */
+static int os_build2(OSpace *s, const OMesh *m) {
+    s->vdof = malloc(sizeof(int) * m->nv);
+    s->edof = malloc(sizeof(int) * m->ne);
+    s->fdof = malloc(sizeof(int) * m->nfacet);
+    s->cdof = malloc(sizeof(int) * m->nc);
+    i64 n = 0;
+    for (i64 v = 0; v < m->nv; v++) s->vdof[v] = m->vbnd[v] ? -1 : (int)n++;
+    for (i64 e = 0; e < m->ne; e++) s->edof[e] = m->ebnd[e] ? -1 : (int)n++;
+    s->nE = n;
+    for (i64 f = 0; f < m->nfacet; f++) { s->fdof[f] = m->fcell[2 * f + 1] >= 0 ? (int)n : -1; if (s->fdof[f] >= 0) n += 2; }
+    for (i64 c = 0; c < m->nc; c++) { s->cdof[c] = (int)n; n += 2; }
+    s->n = n;
+    s->dkind = malloc(sizeof(int) * (n ? n : 1));
+    s->dent = malloc(sizeof(int) * (n ? n : 1));
+    s->dsub = malloc(sizeof(int) * (n ? n : 1));
+    for (i64 v = 0; v < m->nv; v++) if (s->vdof[v] >= 0) { s->dkind[s->vdof[v]] = 0; s->dent[s->vdof[v]] = (int)v; s->dsub[s->vdof[v]] = 0; }
+    for (i64 e = 0; e < m->ne; e++) if (s->edof[e] >= 0) { s->dkind[s->edof[e]] = 1; s->dent[s->edof[e]] = (int)e; s->dsub[s->edof[e]] = 0; }
+    for (i64 f = 0; f < m->nfacet; f++)
+        if (s->fdof[f] >= 0)
+            for (int a = 0; a < 2; a++) { s->dkind[s->fdof[f] + a] = 2; s->dent[s->fdof[f] + a] = (int)f; s->dsub[s->fdof[f] + a] = a; }
+    for (i64 c = 0; c < m->nc; c++)
+        for (int a = 0; a < 2; a++) { s->dkind[s->cdof[c] + a] = 3; s->dent[s->cdof[c] + a] = (int)c; s->dsub[s->cdof[c] + a] = a; }
+    return 0;
+}
+
+int os_build(OSpace *s, const OMesh *m, int block, int degree) {
     memset(s, 0, sizeof(*s));
-    s->block = block; s->dim = m->dim;
+    s->block = block; s->dim = m->dim; s->degree = degree;
+    if (degree == 2) {
+        if (block != ORC_EB || m->dim != 2) return 1;
+        return os_build2(s, m);
+    }
+    if (degree != 1) return 1;
     s->vdof = malloc(sizeof(int) * m->nv);
     s->edof = malloc(sizeof(int) * m->ne);
     s->fdof = malloc(sizeof(int) * m->nfacet);
@@ -55,7 +89,7 @@ int os_build(OSpace *s, const OMesh *m, int block) {
 }
 
 void os_free(OSpace *s) {
-    free(s->vdof); free(s->edof); free(s->fdof); free(s->dkind); free(s->dent); free(s->dsub);
+    free(s->vdof); free(s->edof); free(s->fdof); free(s->cdof); free(s->dkind); free(s->dent); free(s->dsub);
     memset(s, 0, sizeof(*s));
 }
 
@@ -65,6 +99,11 @@ static int dof_contains_vertex(const OMesh *m, const OSpace *s, int d, int v) {
     switch (s->dkind[d]) {
     case 0: return e == v;
     case 1: return m->ev[2 * e] == v || m->ev[2 * e + 1] == v;
+    case 3: {
+        int nvc = m->dim + 1;
+        for (int q = 0; q < nvc; q++) if (m->cv[(i64)e * nvc + q] == v) return 1;
+        return 0;
+    }
     default:
         if (m->dim == 2) return m->ev[2 * e] == v || m->ev[2 * e + 1] == v;
         return m->fv[3 * e] == v || m->fv[3 * e + 1] == v || m->fv[3 * e + 2] == v;
@@ -105,7 +144,15 @@ int opt_build(OPatches *pt, const OMesh *m, const OSpace *s) {
             i64 c = vc[t];
             /* all free DoFs of cell c */
             int cand[64]; int nc = 0;
-            if (s->block == ORC_EB) {
+            if (s->degree == 2) {                    /* CG2 x RT2 (2D) */
+                for (int q = 0; q < 3; q++) { int d = s->vdof[m->cv[c * 3 + q]]; if (d >= 0) cand[nc++] = d; }
+                for (int q = 0; q < 3; q++) { int d = s->edof[m->ce[c * 3 + q]]; if (d >= 0) cand[nc++] = d; }
+                for (int q = 0; q < 3; q++) {
+                    int d = s->fdof[om_facet_of_cell(m, c, q)];
+                    if (d >= 0) { cand[nc++] = d; cand[nc++] = d + 1; }
+                }
+                cand[nc++] = s->cdof[c]; cand[nc++] = s->cdof[c] + 1;
+            } else if (s->block == ORC_EB) {
                 if (m->dim == 2) for (int q = 0; q < 3; q++) { int d = s->vdof[m->cv[c * 3 + q]]; if (d >= 0) cand[nc++] = d; }
                 else for (int q = 0; q < nle; q++) { int d = s->edof[m->ce[c * nle + q]]; if (d >= 0) cand[nc++] = d; }
                 for (int q = 0; q < nvc; q++) { int d = s->fdof[om_facet_of_cell(m, c, q)]; if (d >= 0) cand[nc++] = d; }

@@ -40,6 +40,7 @@ class Config:
     theta: float = 1.0
     dt: float = 0.0      # NEXT-4: > 0 -> transient, (1/dt) mass terms
     picard: int = 0      # NEXT-4: 1 -> Picard linearisation, delta = 0
+    degree: int = 1      # NEXT-2: element degree k; k = 2 for the 2D E-B block (CG2 x RT2)
 
     @property
     def block_id(self) -> int:

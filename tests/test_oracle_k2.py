@@ -1,0 +1,167 @@
+"""Oracle pins for NEXT-2: element degree k = 2 for the 2D E-B block, E in CG2 and
+B in RT2 (complex CG2 -> RT2 -> DG1), reading R-basis2 of DESIGN.md.
+
+Pins (none re-types the oracle's formulas):
+* DoF counts against closed forms; star patches against a brute-force support test
+  (V_i = {v : supp v in K_i});
+* DoF duality N_i(phi_j) = delta_ij with the global functionals of the fine-level
+  prolongation code (written apart from the local-basis construction);
+* manufactured solutions: L2 rates 3 (CG2 E) and 2 (RT2 B) -- k = 1 gives 2 and 1 --
+  for the Newton, transient and Picard variants;
+* the discrete complex: div(vcurl CG2) = 0, read off the assembled blocks alone;
+* the Galerkin identity A_c = P^T A_f P for the conforming E-B forms (nested spaces);
+* Picard antisymmetry of the E-B coupling, symmetric positive mass;
+* Re_m-robust star multigrid for Picard.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import mms
+from paper_2104_14855_b200.workloads import CONFIGS, draw, small
+
+
+def _cfg(N, L, **kw):
+    base = dict(degree=2)
+    base.update(kw)
+    return dataclasses.replace(small("c1", N, L), **base)
+
+
+def _orc(oracle_mod, cfg, exact=False, wc=None):
+    pot = draw(cfg, 1, 0)[0] if wc is None else mms.constant_wind_potential(2, cfg.N, wc)
+    return oracle_mod.Oracle(cfg, pot, exact=exact)
+
+
+@pytest.mark.parametrize("N", [2, 5, 8])
+def test_k2_dof_counts_closed_form(oracle_mod, N):
+    """Free E DoFs: interior vertices + interior edges = (N-1)^2 + 3N^2 - 2N; free B DoFs:
+    2 per interior edge + 2 per cell = 10N^2 - 4N (E = 0, B.n = 0 on the boundary)."""
+    o = _orc(oracle_mod, _cfg(N, 1))
+    i = o.info()
+    assert i["nE"] == (N - 1) ** 2 + 3 * N * N - 2 * N
+    assert i["n"] - i["nE"] == 10 * N * N - 4 * N
+
+
+def test_k2_patches_brute_force(oracle_mod):
+    """A free DoF belongs to the star of vertex v iff every cell of its support contains v;
+    the support of a DoF is the set of cells containing its entity.  Interior stars: 1
+    vertex + 6 edge E DoFs, 6 x 2 edge + 6 x 2 cell B DoFs = 31."""
+    o = _orc(oracle_mod, _cfg(6, 1))
+    m = o.mesh()
+    cv, ev = m["cv"], m["ev"]
+    cells_of_vertex = [set() for _ in range(m["x"].shape[0])]
+    for c, vs in enumerate(cv):
+        for v in vs:
+            cells_of_vertex[v].add(c)
+    support = []
+    for d in range(o.n()):
+        k, e = m["dkind"][d], m["dent"][d]
+        if k == 0:
+            support.append(cells_of_vertex[e])
+        elif k in (1, 2):
+            support.append(cells_of_vertex[ev[e][0]] & cells_of_vertex[ev[e][1]])
+        else:
+            support.append({e})
+    ptr, dofs, vert, _ = o.patches()
+    got = {int(vert[i]): sorted(dofs[ptr[i]:ptr[i + 1]].tolist()) for i in range(len(vert))}
+    want = {}
+    for v in range(m["x"].shape[0]):
+        s = sorted(d for d in range(o.n()) if support[d] <= cells_of_vertex[v])
+        if s:
+            want[v] = s
+    assert got == want
+    assert max(len(s) for s in want.values()) == 31
+
+
+def test_k2_duality(oracle_mod):
+    o = _orc(oracle_mod, _cfg(4, 2))
+    assert o.duality_error() <= 1e-13 and o.duality_error(0) <= 1e-13
+    oe = _orc(oracle_mod, _cfg(4, 2), exact=True)
+    assert oe.duality_error() <= 1e-28
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(div_free_B=True), dict(dt=0.05), dict(picard=1)],
+                         ids=["newton", "div-free-B", "transient", "picard"])
+def test_k2_mms_rates(oracle_mod, kw):
+    """L2 rates 3 (E in CG2) and 2 (B in RT2), Re_m = 1, constant w (measured 2.999 / 1.998)."""
+    wc = [1.0, 0.5]
+    dt, pic = kw.get("dt", 0.0), kw.get("picard", 0)
+    base = dataclasses.replace(CONFIGS["c1"], Re=1.0, Rem=1.0, gamma=1.0, levels=1, dt=dt, picard=pic, degree=2)
+    fs, ex = mms.eb_fields(2, 1.0, wc, **kw)
+    errs = []
+    for N in (16, 32):
+        cfg = dataclasses.replace(base, N=N)
+        errs.append(mms.solve_and_error(oracle_mod.Oracle(cfg, mms.constant_wind_potential(2, N, wc)), fs, ex))
+    r = np.log(errs[0] / errs[1]) / np.log(2.0)
+    assert r[0] >= 2.9 and min(r[1:]) >= 1.95, r
+
+
+def test_k2_complex_div_vcurl_zero(oracle_mod):
+    """vcurl CG2 lies in RT2 with zero divergence.  From the assembled blocks only:
+    with BB(dt) = M_B / dt + C / Re_m, the B-E block is (vcurl E, C) = M_B D with D the RT2
+    coefficients of vcurl E, so C M_B^-1 (B-E block) must vanish."""
+    cfg = _cfg(4, 1, Rem=1.0, picard=1)
+    A1 = _orc(oracle_mod, dataclasses.replace(cfg, dt=1.0)).csr().to_scipy().toarray()
+    A2 = _orc(oracle_mod, dataclasses.replace(cfg, dt=0.5)).csr().to_scipy().toarray()
+    nE = _orc(oracle_mod, cfg).info()["nE"]
+    MB = A2[nE:, nE:] - A1[nE:, nE:]
+    C = 2 * A1[nE:, nE:] - A2[nE:, nE:]
+    BE = A1[nE:, :nE]
+    D = np.linalg.solve(MB, BE)
+    assert np.abs(C @ D).max() <= 1e-10 * np.abs(C).max() * np.abs(D).max()
+    assert np.abs(C).max() > 1 and np.abs(D).max() > 0.1
+    # the mass is symmetric positive definite
+    assert np.allclose(MB, MB.T, rtol=0, atol=1e-13 * np.abs(MB).max())
+    assert np.linalg.eigvalsh(0.5 * (MB + MB.T)).min() > 0
+
+
+def test_k2_picard_coupling_antisymmetry(oracle_mod):
+    """Picard: E-row coupling -(1/Re_m)(B, vcurl F) = -(1/Re_m) (B-E block)^T; the E-E block
+    is the CG2 mass (symmetric positive definite)."""
+    rem = 4.0
+    o = _orc(oracle_mod, _cfg(4, 1, Rem=rem, picard=1))
+    A = o.csr().to_scipy().toarray()
+    nE = o.info()["nE"]
+    EB, BE = A[:nE, nE:], A[nE:, :nE]
+    assert np.abs(EB + BE.T / rem).max() <= 1e-13 * np.abs(BE).max()
+    EE = A[:nE, :nE]
+    assert np.allclose(EE, EE.T, rtol=0, atol=1e-14 * np.abs(EE).max())
+    assert np.linalg.eigvalsh(EE).min() > 0
+
+
+def test_k2_galerkin_identity(oracle_mod):
+    """Conforming E-B forms with an exactly nested (constant) w: the rediscretised coarse
+    operator equals P^T A_f P (R-prol), including the u^n x B Newton term."""
+    o = _orc(oracle_mod, _cfg(4, 2, Rem=2.0), wc=[1.0, 0.5])
+    Af = o.csr(1).to_scipy()
+    Ac = o.csr(0).to_scipy().toarray()
+    P = o.prolongation(1).to_scipy(o.n(0))
+    G = (P.T @ Af @ P).toarray()
+    assert np.abs(G - Ac).max() <= 1e-12 * np.abs(Ac).max()
+
+
+def test_k2_prolongation_exact_build_agrees(oracle_mod):
+    """The prolongation and operators of the fp64 and __float128 builds agree to rounding
+    (the exact build is the parity reference)."""
+    cfg = _cfg(4, 2)
+    a, b = _orc(oracle_mod, cfg), _orc(oracle_mod, cfg, exact=True)
+    Pa, Pb = a.prolongation(1), b.prolongation(1)
+    assert np.array_equal(Pa.rp, Pb.rp) and np.array_equal(Pa.ci, Pb.ci)
+    assert np.abs(Pa.v - Pb.v).max() <= 1e-14
+    Aa, Ab = a.csr(), b.csr()
+    assert np.abs(Aa.v - Ab.v).max() <= 1e-12 * np.abs(Ab.v).max()
+
+
+def test_k2_picard_multigrid_rem_robust(oracle_mod):
+    """Star multigrid on the k = 2 Picard E-B block: FGMRES(GMRES(6)-smoothed V) counts
+    bounded for Re_m = 10 ... 1e4 (measured 4)."""
+    its = []
+    for rem in (10.0, 1e2, 1e3, 1e4):
+        cfg = _cfg(32, 4, Re=rem, Rem=rem, picard=1)
+        o = _orc(oracle_mod, cfg)
+        o.set_smoother("gmres", 6)
+        b = np.random.default_rng(3).standard_normal(o.n())
+        _, k, _, conv = o.fgmres(b, maxit=40)
+        its.append(k if conv else None)
+    assert None not in its and max(its) <= 8, its
