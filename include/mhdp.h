@@ -69,6 +69,9 @@ typedef struct {
                                  velocity block                            */
     int picard;               /* NEXT-4: 0 = Newton (delta = 1), 1 = Picard (delta = 0): the
                                  E-B block loses G~                        */
+    int degree;               /* NEXT-2: element degree k.  0 or 1: k = 1 (the
+                                 BASELINE configs); 2: CG2 x RT2 for the 2D E-B block (reading
+                                 R-basis2).  Other blocks / dims with 2 -> MHDP_EINVAL         */
 } mhdp_params;
 
 typedef struct mhdp_ctx mhdp_ctx;

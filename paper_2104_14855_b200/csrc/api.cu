@@ -502,6 +502,8 @@ static mhdp_status check_params(mhdp_ctx *ctx, const mhdp_params *pr) {
     if (pr->dt < 0 || pr->dt != pr->dt) return fail(ctx, MHDP_EINVAL, "dt must be >= 0");
     if (pr->picard != 0 && pr->picard != 1) return fail(ctx, MHDP_EINVAL, "picard must be 0 or 1");
     ctx->p.dt = pr->dt; ctx->p.picard = pr->picard;
+    if (pr->degree < 0 || pr->degree > 2) return fail(ctx, MHDP_EINVAL, "degree must be 1 or 2");
+    ctx->p.degree = pr->degree == 0 ? 1 : pr->degree;
     return MHDP_OK;
 }
 

@@ -1252,11 +1252,480 @@ std::string assemble_coupling(int dim, int N, const Params &p, const double *w, 
     return "";
 }
 
+
+// ------------------------------------------------------------------------------------
+// NEXT-2: element degree k = 2 for the 2D E-B block, E in CG2, B in RT2,
+// reading R-basis2 (DoFs: CG2 point values at vertices and edge midpoints; RT2 normal
+// moments int_e (B.n_e) lam_s ds against the two P1 functions of each edge, s = lower /
+// higher global vertex, and N int_K B_r dx per cell).  Independent of the oracle's
+// quadrature: every function is a homogeneous polynomial in the barycentric coordinates
+// and every integral is the closed form  int_K lam^alpha = 2|K| alpha! / (|alpha| + 2)!
+// (edges: int_e mu^beta = |e| beta! / (|beta| + 1)!).  The RT2 primal basis is
+// {lam_a psi_q} (P1 times the RT0 functions psi_q = s_q (x - X_q)/(2|K|); the relation
+// sum_q lam_q (x - X_q) = 0 removes (a, q) = (2, 2)), made dual to the DoFs by inverting
+// the 8 x 8 DoF matrix in double-double.
+// ------------------------------------------------------------------------------------
+namespace {
+
+inline double fact(int n) { double r = 1; for (int i = 2; i <= n; ++i) r *= i; return r; }
+
+// int_K lam_i1 ... lam_ik (k = 2, 3, 4) / (2|K|)  =  prod n_j! / (k + 2)!
+inline dd bary_int(const int *idx, int k) {
+    int n[3] = {0, 0, 0};
+    for (int t = 0; t < k; ++t) n[idx[t]]++;
+    return dd(fact(n[0]) * fact(n[1]) * fact(n[2])) / dd(fact(k + 2));
+}
+
+struct Space2 {
+    i64 n = 0, nE = 0;
+    std::vector<int> vdof, edof, fdof, cdof;   // edof: CG2 midpoint DoF per edge (2D: edge = facet)
+};
+
+// R-num2 (same order as DESIGN.md): free vertices, free edges (CG2); 2 per interior edge,
+// then 2 per cell (RT2)
+void build_space2(Space2 &s, const Mesh &m) {
+    s.vdof.assign(m.nv, -1); s.edof.assign(m.ne, -1); s.fdof.assign(m.nfacet, -1); s.cdof.assign(m.nc, -1);
+    i64 n = 0;
+    for (i64 v = 0; v < m.nv; ++v) if (!m.on_bnd(v)) s.vdof[v] = (int)n++;
+    for (i64 e = 0; e < m.ne; ++e) if (!m.common_bnd(&m.ev[2 * e], 2)) s.edof[e] = (int)n++;
+    s.nE = n;
+    for (i64 f = 0; f < m.nfacet; ++f) if (!m.common_bnd(&m.ev[2 * f], 2)) { s.fdof[f] = (int)n; n += 2; }
+    for (i64 c = 0; c < m.nc; ++c) { s.cdof[c] = (int)n; n += 2; }
+    s.n = n;
+}
+
+// local order: E: vertices 0..2, edges (0,1) (0,2) (1,2); B: facet q (opposite vertex q)
+// x s = 0, 1, then r = 0, 1
+static const int E2V[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+void cell_dofs2(const Mesh &m, const Space2 &s, i64 c, int *gE, int *gB) {
+    for (int a = 0; a < 3; ++a) gE[a] = s.vdof[m.cv[3 * c + a]];
+    for (int t = 0; t < 3; ++t) gE[3 + t] = s.edof[m.cfacet[3 * c + (2 - t)]];   // edge (i,j) is opposite 3-i-j
+    for (int q = 0; q < 3; ++q) {
+        const int f0 = s.fdof[m.cfacet[3 * c + q]];
+        gB[2 * q] = f0 < 0 ? -1 : f0;
+        gB[2 * q + 1] = f0 < 0 ? -1 : f0 + 1;
+    }
+    gB[6] = s.cdof[c]; gB[7] = s.cdof[c] + 1;
+}
+
+// element of the k = 2 E-B block: CG2 as quadratics sum e[b][d] lam_b lam_d, RT2 as
+// sum V[a][b] lam_a lam_b (2-vectors)
+struct Elem2 {
+    GeoT<dd> G;
+    dd e[6][3][3];
+    dd V[8][3][3][2];
+};
+
+// RT2 functionals (local order) of the field sum V[a][b] lam_a lam_b on cell G
+void rt2_dofs(const GeoT<dd> &G, int Ncells, const dd V[3][3][2], dd *out) {
+    for (int q = 0; q < 3; ++q) {
+        dd A[3];
+        int fl[3];
+        facet_area(G, q, A, fl);
+        // int_e (B.A/|e|) mu_s ds = sum_{a,b in e} (V_ab . A) int_e mu_a mu_b mu_s / |e|
+        for (int s = 0; s < 2; ++s) {
+            dd acc(0.0);
+            for (int ia = 0; ia < 2; ++ia)
+                for (int ib = 0; ib < 2; ++ib) {
+                    const int a = fl[ia], b = fl[ib];
+                    int n[2] = {0, 0};
+                    n[ia]++; n[ib]++; n[s]++;
+                    const dd mom = dd(fact(n[0]) * fact(n[1])) / dd(24.0);     // beta! / 4!
+                    acc += (V[a][b][0] * A[0] + V[a][b][1] * A[1]) * mom;
+                }
+            out[2 * q + s] = acc;
+        }
+    }
+    for (int r = 0; r < 2; ++r) {
+        dd acc(0.0);
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) {
+                const int idx[2] = {a, b};
+                acc += V[a][b][r] * bary_int(idx, 2);
+            }
+        out[6 + r] = acc * dd(2.0) * G.vol * dd((double)Ncells);
+    }
+}
+
+dd dd_fabs(const dd &x) { return x.hi < 0 ? -x : x; }
+
+void elem2(const Mesh &m, i64 c, Elem2 &K) {
+    cell_geo(m, c, K.G);
+    const GeoT<dd> &G = K.G;
+    memset((void *)K.e, 0, sizeof K.e);
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) K.e[a][a][b] = dd(a == b ? 1.0 : -1.0);   // lam_a (2 lam_a - sum lam)
+    for (int t = 0; t < 3; ++t) K.e[3 + t][E2V[t][0]][E2V[t][1]] = dd(4.0);
+    // primal RT2 functions p_{a,q} = lam_a psi_q, psi_q = c_q sum_b lam_b (X_b - X_q)
+    dd cq[3];
+    for (int q = 0; q < 3; ++q) {
+        dd A[3];
+        int fl[3];
+        facet_area(G, q, A, fl);
+        cq[q] = dd(facet_sign(G, q, A, fl)) / G.dvol;
+    }
+    static dd P[8][3][3][2];
+    int np = 0;
+    dd Pv[8][3][3][2];
+    memset((void *)Pv, 0, sizeof Pv);
+    for (int a = 0; a < 3; ++a)
+        for (int q = 0; q < 3; ++q) {
+            if (a == 2 && q == 2) continue;
+            for (int b = 0; b < 3; ++b)
+                for (int r = 0; r < 2; ++r) Pv[np][a][b][r] = cq[q] * (G.X[b][r] - G.X[q][r]);
+            ++np;
+        }
+    (void)P;
+    // DoF matrix M[i][j] = N_i(p_j), Gauss-Jordan in double-double
+    dd W[8][16];
+    for (int j = 0; j < 8; ++j) {
+        dd col[8];
+        rt2_dofs(G, m.N, Pv[j], col);
+        for (int i = 0; i < 8; ++i) W[i][j] = col[i];
+    }
+    for (int i = 0; i < 8; ++i) for (int j = 0; j < 8; ++j) W[i][8 + j] = dd(i == j ? 1.0 : 0.0);
+    for (int k = 0; k < 8; ++k) {
+        int p = k;
+        for (int i = k + 1; i < 8; ++i) if (to_double(dd_fabs(W[i][k])) > to_double(dd_fabs(W[p][k]))) p = i;
+        if (p != k) for (int j = 0; j < 16; ++j) std::swap(W[k][j], W[p][j]);
+        const dd piv = W[k][k];
+        for (int j = 0; j < 16; ++j) W[k][j] = W[k][j] / piv;
+        for (int i = 0; i < 8; ++i) {
+            if (i == k) continue;
+            const dd l = W[i][k];
+            for (int j = 0; j < 16; ++j) W[i][j] = W[i][j] - l * W[k][j];
+        }
+    }
+    // dual basis phi_j = sum_k Cinv[k][j] p_k
+    for (int j = 0; j < 8; ++j)
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b)
+                for (int r = 0; r < 2; ++r) {
+                    dd acc(0.0);
+                    for (int k = 0; k < 8; ++k) acc += W[k][8 + j] * Pv[k][a][b][r];
+                    K.V[j][a][b][r] = acc;
+                }
+}
+
+struct EBLocal2 {
+    int gE[6], gB[8];
+    dd EE[6][6], EB[6][8], BE[8][6], BB[8][8];
+};
+
+void eb_local2(const Mesh &m, const Space2 &s, i64 c, const double *pot, const Params &p, EBLocal2 &L) {
+    Elem2 K;
+    elem2(m, c, K);
+    const GeoT<dd> &G = K.G;
+    cell_dofs2(m, s, c, L.gE, L.gB);
+    dd w[3];
+    cell_wind(G, pot, w);
+    const dd twoK = dd(2.0) * G.vol;
+    // gradient of the CG2 functions: sum_c lam_c Gr[c] ;  vcurl = (Gr_y, -Gr_x)
+    dd R[6][3][2];
+    for (int i = 0; i < 6; ++i)
+        for (int cc = 0; cc < 3; ++cc) {
+            dd gx(0.0), gy(0.0);
+            for (int d2 = 0; d2 < 3; ++d2) {
+                const dd t = K.e[i][cc][d2] + K.e[i][d2][cc];
+                gx += t * G.g[d2][0];
+                gy += t * G.g[d2][1];
+            }
+            R[i][cc][0] = gy; R[i][cc][1] = -gx;
+        }
+    // divergence of the RT2 functions: sum_c lam_c D[c]
+    dd D[8][3];
+    for (int k = 0; k < 8; ++k)
+        for (int cc = 0; cc < 3; ++cc) {
+            dd acc(0.0);
+            for (int b = 0; b < 3; ++b) {
+                acc += G.g[b][0] * K.V[k][cc][b][0] + G.g[b][1] * K.V[k][cc][b][1];
+                acc += G.g[b][0] * K.V[k][b][cc][0] + G.g[b][1] * K.V[k][b][cc][1];
+            }
+            D[k][cc] = acc;
+        }
+    for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 6; ++j) {
+            dd acc(0.0);
+            for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b)
+                for (int cc = 0; cc < 3; ++cc) for (int d2 = 0; d2 < 3; ++d2) {
+                    const int idx[4] = {a, b, cc, d2};
+                    acc += K.e[i][a][b] * K.e[j][cc][d2] * bary_int(idx, 4);
+                }
+            L.EE[i][j] = acc * twoK;
+        }
+    for (int i = 0; i < 6; ++i)
+        for (int k = 0; k < 8; ++k) {
+            dd ab(0.0), gt(0.0);
+            for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b) {
+                for (int cc = 0; cc < 3; ++cc) {
+                    const int idx[3] = {a, b, cc};
+                    ab += (K.V[k][a][b][0] * R[i][cc][0] + K.V[k][a][b][1] * R[i][cc][1]) * bary_int(idx, 3);
+                }
+                if (!p.picard) {
+                    const dd wxb = w[0] * K.V[k][a][b][1] - w[1] * K.V[k][a][b][0];
+                    for (int cc = 0; cc < 3; ++cc) for (int d2 = 0; d2 < 3; ++d2) {
+                        const int idx[4] = {a, b, cc, d2};
+                        gt += wxb * K.e[i][cc][d2] * bary_int(idx, 4);
+                    }
+                }
+            }
+            ab = ab * twoK;
+            gt = gt * twoK;
+            L.EB[i][k] = gt - ab / dd(p.Rem);
+            L.BE[k][i] = ab;
+        }
+    for (int k = 0; k < 8; ++k)
+        for (int l = 0; l < 8; ++l) {
+            dd dv(0.0);
+            for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b) {
+                const int idx[2] = {a, b};
+                dv += D[k][a] * D[l][b] * bary_int(idx, 2);
+            }
+            dd v = dv * twoK / dd(p.Rem);
+            if (p.dt > 0) {
+                dd ms(0.0);
+                for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b)
+                    for (int cc = 0; cc < 3; ++cc) for (int d2 = 0; d2 < 3; ++d2) {
+                        const int idx[4] = {a, b, cc, d2};
+                        ms += (K.V[k][a][b][0] * K.V[l][cc][d2][0] + K.V[k][a][b][1] * K.V[l][cc][d2][1]) *
+                              bary_int(idx, 4);
+                    }
+                v += ms * twoK / dd(p.dt);
+            }
+            L.BB[k][l] = v;
+        }
+}
+
+// gather-form assembly by rows (cells of the row's entity, ascending), R-exact rows
+void assemble_eb2(const Mesh &m, const Space2 &s, const Params &p, const double *pot, Pattern &P,
+                  std::vector<double> &val) {
+    std::vector<i64> vp, fp;
+    std::vector<int> vc, fc;
+    incidence(m, 0, vp, vc);
+    incidence(m, 2, fp, fc);
+    std::vector<int> dkind(s.n), dent(s.n);
+    for (i64 v = 0; v < m.nv; ++v) if (s.vdof[v] >= 0) { dkind[s.vdof[v]] = 0; dent[s.vdof[v]] = (int)v; }
+    for (i64 e = 0; e < m.ne; ++e) if (s.edof[e] >= 0) { dkind[s.edof[e]] = 1; dent[s.edof[e]] = (int)e; }
+    for (i64 f = 0; f < m.nfacet; ++f)
+        if (s.fdof[f] >= 0) for (int a = 0; a < 2; ++a) { dkind[s.fdof[f] + a] = 1; dent[s.fdof[f] + a] = (int)f; }
+    for (i64 c = 0; c < m.nc; ++c) for (int a = 0; a < 2; ++a) { dkind[s.cdof[c] + a] = 2; dent[s.cdof[c] + a] = (int)c; }
+    std::vector<int> self(m.nc);
+    std::iota(self.begin(), self.end(), 0);
+    auto cells_of = [&](i64 row, const int *&b, const int *&e) {
+        const int k = dkind[row], id = dent[row];
+        if (k == 0) { b = vc.data() + vp[id]; e = vc.data() + vp[id + 1]; }
+        else if (k == 1) { b = fc.data() + fp[id]; e = fc.data() + fp[id + 1]; }
+        else { b = self.data() + id; e = b + 1; }
+    };
+    std::vector<EBLocal2> loc(m.nc);
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < m.nc; ++c) eb_local2(m, s, c, pot, p, loc[c]);
+    P.rp.assign(s.n + 1, 0);
+    std::vector<std::vector<int>> rows(s.n);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (i64 r = 0; r < s.n; ++r) {
+        const int *b, *e;
+        cells_of(r, b, e);
+        std::vector<int> cols;
+        for (const int *c = b; c != e; ++c) {
+            for (int t = 0; t < 6; ++t) if (loc[*c].gE[t] >= 0) cols.push_back(loc[*c].gE[t]);
+            for (int t = 0; t < 8; ++t) if (loc[*c].gB[t] >= 0) cols.push_back(loc[*c].gB[t]);
+        }
+        std::sort(cols.begin(), cols.end());
+        cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+        rows[r] = std::move(cols);
+    }
+    for (i64 r = 0; r < s.n; ++r) P.rp[r + 1] = P.rp[r] + (i64)rows[r].size();
+    P.ci.resize(P.rp[s.n]);
+    for (i64 r = 0; r < s.n; ++r) std::copy(rows[r].begin(), rows[r].end(), P.ci.begin() + P.rp[r]);
+    rows.clear();
+    val.assign(P.rp[s.n], 0.0);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (i64 r = 0; r < s.n; ++r) {
+        const int *b, *e;
+        cells_of(r, b, e);
+        const i64 base = P.rp[r], len = P.rp[r + 1] - base;
+        std::vector<dd> acc(len);
+        const bool isB = r >= s.nE;
+        for (const int *c = b; c != e; ++c) {
+            const EBLocal2 &K = loc[*c];
+            int li = -1;
+            if (!isB) { for (int a = 0; a < 6; ++a) if (K.gE[a] == r) li = a; }
+            else { for (int a = 0; a < 8; ++a) if (K.gB[a] == r) li = a; }
+            auto add = [&](int col, const dd &v) { acc[find_col(P, r, col) - base] += v; };
+            for (int j = 0; j < 6; ++j) if (K.gE[j] >= 0) add(K.gE[j], isB ? K.BE[li][j] : K.EE[li][j]);
+            for (int j = 0; j < 8; ++j) if (K.gB[j] >= 0) add(K.gB[j], isB ? K.BB[li][j] : K.EB[li][j]);
+        }
+        round_row(acc.data(), len, val.data() + base);
+    }
+}
+
+void build_patches2(const Mesh &m, const Space2 &s, std::vector<i64> &pptr, std::vector<int> &pdofs) {
+    std::vector<std::vector<int>> vlist(m.nv);
+    for (i64 v = 0; v < m.nv; ++v) if (s.vdof[v] >= 0) vlist[v].push_back(s.vdof[v]);
+    for (i64 e = 0; e < m.ne; ++e)
+        for (int t = 0; t < 2; ++t) {
+            const int v = m.ev[2 * e + t];
+            if (s.edof[e] >= 0) vlist[v].push_back(s.edof[e]);
+            if (s.fdof[e] >= 0) { vlist[v].push_back(s.fdof[e]); vlist[v].push_back(s.fdof[e] + 1); }
+        }
+    for (i64 c = 0; c < m.nc; ++c)
+        for (int t = 0; t < 3; ++t) { vlist[m.cv[3 * c + t]].push_back(s.cdof[c]); vlist[m.cv[3 * c + t]].push_back(s.cdof[c] + 1); }
+    pptr.assign(1, 0);
+    pdofs.clear();
+    for (i64 v = 0; v < m.nv; ++v) {
+        auto &L = vlist[v];
+        if (L.empty()) continue;
+        std::sort(L.begin(), L.end());
+        pdofs.insert(pdofs.end(), L.begin(), L.end());
+        pptr.push_back((i64)pdofs.size());
+    }
+}
+
+// R-prol at k = 2: coarse functions rewritten in the fine cell's barycentrics
+// (lam^c_b = sum_a lam^c_b(X^f_a) lam^f_a, exact dyadic weights), fine functionals in
+// closed form; rows rounded as R-exact, |x| < 2^-30 max|row| dropped (R-prol2)
+void build_prolongation2(const Mesh &mf, const Space2 &sf, const Mesh &mc, const Space2 &sc, std::vector<i64> &rp,
+                         std::vector<int> &ci, std::vector<double> &vv) {
+    std::vector<std::vector<std::pair<int, dd>>> rows(sf.n);
+    std::vector<char> done(sf.n, 0);
+    for (i64 c = 0; c < mf.nc; ++c) {
+        int gE[6], gB[8];
+        cell_dofs2(mf, sf, c, gE, gB);
+        bool any = false;
+        for (int t = 0; t < 6; ++t) any = any || (gE[t] >= 0 && !done[gE[t]]);
+        for (int t = 0; t < 8; ++t) any = any || (gB[t] >= 0 && !done[gB[t]]);
+        if (!any) continue;
+        int Lf[4][3] = {{0}};
+        int sum[2] = {0, 0};
+        for (int a = 0; a < 3; ++a) {
+            mf.lat(mf.cv[3 * c + a], Lf[a]);
+            for (int r = 0; r < 2; ++r) sum[r] += Lf[a][r];
+        }
+        int cube[2], rel[2];
+        for (int r = 0; r < 2; ++r) { cube[r] = sum[r] / 6; rel[r] = sum[r] - 6 * cube[r]; }
+        const i64 sq = cube[0] + (i64)mc.N * cube[1];
+        const i64 pc = rel[0] > rel[1] ? 2 * sq : 2 * sq + 1;
+        Elem2 Kc;
+        elem2(mc, pc, Kc);
+        int cE[6], cB[8];
+        cell_dofs2(mc, sc, pc, cE, cB);
+        GeoT<dd> Gf;
+        cell_geo(mf, c, Gf);
+        // T[b][a] = lam^c_b(X^f_a)
+        dd T[3][3];
+        for (int b = 0; b < 3; ++b)
+            for (int a = 0; a < 3; ++a) {
+                dd v(b == 0 ? 1.0 : 0.0);
+                for (int r = 0; r < 2; ++r) v += Kc.G.g[b][r] * (Gf.X[a][r] - Kc.G.X[0][r]);
+                T[b][a] = v;
+            }
+        auto to_fine = [&](const dd in[3][3], dd out[3][3]) {
+            for (int a = 0; a < 3; ++a)
+                for (int a2 = 0; a2 < 3; ++a2) {
+                    dd acc(0.0);
+                    for (int b = 0; b < 3; ++b)
+                        for (int d2 = 0; d2 < 3; ++d2) acc += in[b][d2] * T[b][a] * T[d2][a2];
+                    out[a][a2] = acc;
+                }
+        };
+        // E DoFs of the fine cell
+        for (int t = 0; t < 6; ++t) {
+            const int I = gE[t];
+            if (I < 0 || done[I]) continue;
+            done[I] = 1;
+            for (int j = 0; j < 6; ++j) {
+                if (cE[j] < 0) continue;
+                dd f[3][3];
+                to_fine(Kc.e[j], f);
+                dd v;
+                if (t < 3) v = f[t][t];
+                else {
+                    const int i = E2V[t - 3][0], k = E2V[t - 3][1];
+                    v = (f[i][i] + f[k][k] + f[i][k] + f[k][i]) * dd(0.25);
+                }
+                rows[I].push_back({cE[j], v});
+            }
+        }
+        // B DoFs of the fine cell
+        for (int t = 0; t < 8; ++t) {
+            const int I = gB[t];
+            if (I < 0 || done[I]) continue;
+            done[I] = 1;
+            for (int j = 0; j < 8; ++j) {
+                if (cB[j] < 0) continue;
+                dd F[3][3][2], comp[3][3], fin[3][3];
+                for (int r = 0; r < 2; ++r) {
+                    for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b) comp[a][b] = Kc.V[j][a][b][r];
+                    to_fine(comp, fin);
+                    for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b) F[a][b][r] = fin[a][b];
+                }
+                dd out[8];
+                rt2_dofs(Gf, mf.N, F, out);
+                rows[I].push_back({cB[j], out[t]});
+            }
+        }
+    }
+    rp.assign(sf.n + 1, 0);
+    std::vector<std::vector<std::pair<int, double>>> fin(sf.n);
+    for (i64 I = 0; I < sf.n; ++I) {
+        auto &R = rows[I];
+        std::sort(R.begin(), R.end(), [](const std::pair<int, dd> &x, const std::pair<int, dd> &y) { return x.first < y.first; });
+        std::vector<dd> xs(R.size());
+        for (size_t t = 0; t < R.size(); ++t) xs[t] = R[t].second;
+        std::vector<double> rounded(R.size());
+        round_row(xs.data(), (i64)xs.size(), rounded.data());
+        double mx = 0;
+        for (double v : rounded) mx = std::max(mx, std::fabs(v));
+        for (size_t t = 0; t < R.size(); ++t)
+            if (rounded[t] != 0.0 && std::fabs(to_double(xs[t])) >= std::ldexp(mx, -30)) fin[I].push_back({R[t].first, rounded[t]});
+        rp[I + 1] = rp[I] + (i64)fin[I].size();
+    }
+    ci.resize(rp[sf.n]);
+    vv.resize(rp[sf.n]);
+    for (i64 I = 0; I < sf.n; ++I)
+        for (size_t t = 0; t < fin[I].size(); ++t) { ci[rp[I] + t] = fin[I][t].first; vv[rp[I] + t] = fin[I][t].second; }
+}
+
+}  // namespace
+
 std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params &p, const double *w,
                                const double *bn, std::vector<HostLevel> &out) {
     if ((block != 0 && block != 1) || (dim != 2 && dim != 3) || N < 1 || nlev < 1) return "bad arguments";
     if (N % (1 << (nlev - 1))) return "N not divisible by 2^(nlev-1)";
+    if (p.degree != 1 && p.degree != 2) return "degree must be 1 or 2";
+    if (p.degree == 2 && !(block == 0 && dim == 2)) return "degree 2 is built for the 2D E-B block only (NEXT-2)";
     out.assign(nlev, HostLevel());
+    if (p.degree == 2) {
+        std::vector<Mesh> meshes(nlev);
+        std::vector<Space2> spaces(nlev);
+        for (int l = nlev - 1; l >= 0; --l) {
+            const int Nl = N >> (nlev - 1 - l), step = 1 << (nlev - 1 - l);
+            Mesh &m = meshes[l];
+            build_mesh(m, dim, Nl);
+            build_space2(spaces[l], m);
+            std::vector<double> pot(m.nv);
+            for (i64 v = 0; v < m.nv; ++v) {
+                int q[3];
+                m.lat(v, q);
+                pot[v] = w[q[0] * step + (i64)(N + 1) * (q[1] * step)];
+            }
+            Pattern P;
+            std::vector<double> val;
+            assemble_eb2(m, spaces[l], p, pot.data(), P, val);
+            HostLevel &H = out[l];
+            H.n = spaces[l].n;
+            H.rp = std::move(P.rp);
+            H.ci = std::move(P.ci);
+            H.v = std::move(val);
+            if (l > 0) build_patches2(m, spaces[l], H.pptr, H.pdofs);
+        }
+        for (int l = 1; l < nlev; ++l) {
+            build_prolongation2(meshes[l], spaces[l], meshes[l - 1], spaces[l - 1], out[l].prp, out[l].pci, out[l].pv);
+            out[l].n_coarser = spaces[l - 1].n;
+        }
+        return "";
+    }
     std::vector<Mesh> meshes(nlev);
     std::vector<Space> spaces(nlev);
     const int ncomp = dim == 2 ? 1 : 3;

@@ -15,6 +15,7 @@ struct Params {
     int smoother = 0, smoother_its = 6;   // 0 Richardson sweeps, 1 GMRES(m) (NEXT-1)
     double dt = 0;                         // NEXT-4: > 0 -> transient, (1/dt) mass terms
     int picard = 0;                        // NEXT-4: 1 -> Picard, no G~ term
+    int degree = 1;                        // NEXT-2: element degree k (2: 2D E-B, CG2 x RT2)
 };
 
 // One level of the hierarchy as host arrays (the form both mhdp_assemble and

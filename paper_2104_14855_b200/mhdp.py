@@ -33,7 +33,7 @@ class Params(C.Structure):
     _fields_ = [("Re", C.c_double), ("Rem", C.c_double), ("S", C.c_double), ("gamma", C.c_double),
                 ("sigma", C.c_double), ("mu_stab", C.c_double), ("theta", C.c_double),
                 ("nu_pre", C.c_int), ("nu_post", C.c_int), ("smoother", C.c_int), ("smoother_its", C.c_int),
-                ("dt", C.c_double), ("picard", C.c_int)]
+                ("dt", C.c_double), ("picard", C.c_int), ("degree", C.c_int)]
 
 
 class LevelInfo(C.Structure):
@@ -147,7 +147,7 @@ def make_params(cfg, smoother: str = "richardson", smoother_its: int = 6) -> Par
     preconditioned by the Schwarz operator, the paper's relaxation."""
     return Params(cfg.Re, cfg.Rem, cfg.S, cfg.gamma, cfg.sigma, cfg.mu, cfg.theta, cfg.nu, cfg.nu,
                   1 if smoother == "gmres" else 0, smoother_its, float(getattr(cfg, "dt", 0.0)),
-                  int(getattr(cfg, "picard", 0)))
+                  int(getattr(cfg, "picard", 0)), int(getattr(cfg, "degree", 1)))
 
 
 class Context:

@@ -16,7 +16,7 @@ from gpu_helpers import bits, cuda_vec, host, load_oracle_levels, rel_l2
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("c1", 8, 2), ("c2", 32, 3), ("c3", 16, 3), ("c4", 8, 2), ("c5", 6, 2)]
+CASES = [("c1", 8, 2), ("c2", 32, 3), ("c3", 16, 3), ("c4", 8, 2), ("c5", 6, 2), ("c2-k2", 32, 3)]
 
 
 @pytest.fixture(scope="module", params=CASES, ids=[f"{c}-N{n}L{l}" for c, n, l in CASES])
@@ -24,7 +24,11 @@ def pair(request, oracle_mod):
     import torch
     from paper_2104_14855_b200 import mhdp, workloads
     name, N, L = request.param
-    cfg = workloads.small(name, N, L)
+    import dataclasses
+    k2 = name.endswith("-k2")                       # NEXT-2: CG2 x RT2 (31-DoF stars)
+    cfg = workloads.small(name.replace("-k2", ""), N, L)
+    if k2:
+        cfg = dataclasses.replace(cfg, degree=2)
     # draw with the finest n of this hierarchy
     probe = oracle_mod.Oracle(cfg, workloads.advecting_potential(cfg, np.array([0.3, -1.1, 0.7])))
     n = probe.n()

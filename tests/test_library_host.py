@@ -166,3 +166,48 @@ def test_coupled_operator_bitexact(mh, oracle_mod, dim, N, L, kw):
     assert np.array_equal(A.rp, rp) and np.array_equal(A.ci, ci)
     diff = np.flatnonzero(A.v.view(np.uint64) != v.view(np.uint64))
     assert diff.size == 0, f"{diff.size} entries differ"
+
+
+K2_CASES = [("c1", 8, 2, dict()), ("c2", 32, 3, dict()), ("c2", 16, 3, dict(picard=1, dt=0.05)),
+            ("c2", 64, 4, dict(Rem=7.0))]
+
+
+@pytest.mark.parametrize("name,N,L,kw", K2_CASES, ids=[f"{c}-N{n}L{l}-{k}" for c, n, l, k in K2_CASES])
+def test_k2_host_setup_bitexact_vs_exact_oracle(mh, oracle_mod, name, N, L, kw):
+    """NEXT-2 (k = 2, 2D E-B, CG2 x RT2): numbering, patches, prolongation (R-prol2) and
+    operator values of the library (closed-form barycentric integrals in double-double,
+    {lam_a psi_q} primal RT2 basis) equal the oracle's exact build (quadrature in
+    __float128, monomial primal basis) bit for bit on every level."""
+    import dataclasses
+    from paper_2104_14855_b200 import workloads
+    cfg = dataclasses.replace(workloads.small(name, N, L), degree=2, **kw)
+    w, _, _ = workloads.draw(cfg, 1, seed=2)
+    orc = oracle_mod.Oracle(cfg, w, exact=True)
+    ctx = mh.Context(-1)
+    ctx.assemble(cfg, w)
+    for l in range(L):
+        A = orc.csr(l)
+        rp, ci, v = ctx.csr(l)
+        assert np.array_equal(A.rp, rp) and np.array_equal(A.ci, ci), f"level {l}: pattern"
+        diff = np.flatnonzero(A.v.view(np.uint64) != v.view(np.uint64))
+        assert diff.size == 0, f"level {l}: {diff.size} values differ"
+        if l == 0:
+            continue
+        ptr_o, dofs_o, _, _ = orc.patches(l)
+        ptr_l, dofs_l = ctx.patches(l)
+        assert np.array_equal(ptr_o, ptr_l) and np.array_equal(dofs_o, dofs_l), f"level {l}: patches"
+        P = orc.prolongation(l)
+        prp, pci, pv = ctx.prolongation(l)
+        assert np.array_equal(P.rp, prp) and np.array_equal(P.ci, pci), f"level {l}: prolongation pattern"
+        assert np.array_equal(P.v.view(np.uint64), pv.view(np.uint64)), f"level {l}: prolongation values"
+
+
+def test_k2_rejected_outside_2d_eb(mh):
+    import dataclasses
+    from paper_2104_14855_b200 import workloads
+    for name in ("c3", "c4"):
+        cfg = dataclasses.replace(workloads.small(name, 4, 1), degree=2)
+        w, _, _ = workloads.draw(cfg, 1, 0)
+        ctx = mh.Context(-1)
+        with pytest.raises(mh.MhdpError):
+            ctx.assemble(cfg, w)
