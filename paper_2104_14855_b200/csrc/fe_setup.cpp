@@ -1270,10 +1270,28 @@ namespace {
 inline double fact(int n) { double r = 1; for (int i = 2; i <= n; ++i) r *= i; return r; }
 
 // int_K lam_i1 ... lam_ik (k = 2, 3, 4) / (2|K|)  =  prod n_j! / (k + 2)!
-inline dd bary_int(const int *idx, int k) {
+dd bary_int_eval(const int *idx, int k) {
     int n[3] = {0, 0, 0};
     for (int t = 0; t < k; ++t) n[idx[t]]++;
     return dd(fact(n[0]) * fact(n[1]) * fact(n[2])) / dd(fact(k + 2));
+}
+struct BaryTables {
+    dd t2[9], t3[27], t4[81];
+    BaryTables() {
+        for (int a = 0; a < 81; ++a) {
+            const int idx[4] = {a / 27, (a / 9) % 3, (a / 3) % 3, a % 3};
+            t4[a] = bary_int_eval(idx, 4);
+            if (a < 27) { const int i3[3] = {a / 9, (a / 3) % 3, a % 3}; t3[a] = bary_int_eval(i3, 3); }
+            if (a < 9) { const int i2[2] = {a / 3, a % 3}; t2[a] = bary_int_eval(i2, 2); }
+        }
+    }
+};
+const BaryTables &bary_tables() { static const BaryTables T; return T; }
+inline const dd &bary_int(const int *idx, int k) {
+    const BaryTables &T = bary_tables();
+    if (k == 2) return T.t2[3 * idx[0] + idx[1]];
+    if (k == 3) return T.t3[9 * idx[0] + 3 * idx[1] + idx[2]];
+    return T.t4[27 * idx[0] + 9 * idx[1] + 3 * idx[2] + idx[3]];
 }
 
 struct Space2 {
@@ -1364,7 +1382,6 @@ void elem2(const Mesh &m, i64 c, Elem2 &K) {
         facet_area(G, q, A, fl);
         cq[q] = dd(facet_sign(G, q, A, fl)) / G.dvol;
     }
-    static dd P[8][3][3][2];
     int np = 0;
     dd Pv[8][3][3][2];
     memset((void *)Pv, 0, sizeof Pv);
@@ -1375,7 +1392,6 @@ void elem2(const Mesh &m, i64 c, Elem2 &K) {
                 for (int r = 0; r < 2; ++r) Pv[np][a][b][r] = cq[q] * (G.X[b][r] - G.X[q][r]);
             ++np;
         }
-    (void)P;
     // DoF matrix M[i][j] = N_i(p_j), Gauss-Jordan in double-double
     dd W[8][16];
     for (int j = 0; j < 8; ++j) {
@@ -1588,14 +1604,22 @@ void build_patches2(const Mesh &m, const Space2 &s, std::vector<i64> &pptr, std:
 void build_prolongation2(const Mesh &mf, const Space2 &sf, const Mesh &mc, const Space2 &sc, std::vector<i64> &rp,
                          std::vector<int> &ci, std::vector<double> &vv) {
     std::vector<std::vector<std::pair<int, dd>>> rows(sf.n);
-    std::vector<char> done(sf.n, 0);
+    // coarse elements once; each fine DoF is computed by its owner, the lowest-index fine
+    // cell containing its entity (deterministic under any schedule)
+    std::vector<Elem2> ce(mc.nc);
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < mc.nc; ++c) elem2(mc, c, ce[c]);
+    std::vector<int> owner(sf.n, INT32_MAX);
+    for (i64 c = mf.nc - 1; c >= 0; --c) {
+        int gE[6], gB[8];
+        cell_dofs2(mf, sf, c, gE, gB);
+        for (int t = 0; t < 6; ++t) if (gE[t] >= 0) owner[gE[t]] = (int)c;
+        for (int t = 0; t < 8; ++t) if (gB[t] >= 0) owner[gB[t]] = (int)c;
+    }
+#pragma omp parallel for schedule(dynamic, 64)
     for (i64 c = 0; c < mf.nc; ++c) {
         int gE[6], gB[8];
         cell_dofs2(mf, sf, c, gE, gB);
-        bool any = false;
-        for (int t = 0; t < 6; ++t) any = any || (gE[t] >= 0 && !done[gE[t]]);
-        for (int t = 0; t < 8; ++t) any = any || (gB[t] >= 0 && !done[gB[t]]);
-        if (!any) continue;
         int Lf[4][3] = {{0}};
         int sum[2] = {0, 0};
         for (int a = 0; a < 3; ++a) {
@@ -1606,8 +1630,7 @@ void build_prolongation2(const Mesh &mf, const Space2 &sf, const Mesh &mc, const
         for (int r = 0; r < 2; ++r) { cube[r] = sum[r] / 6; rel[r] = sum[r] - 6 * cube[r]; }
         const i64 sq = cube[0] + (i64)mc.N * cube[1];
         const i64 pc = rel[0] > rel[1] ? 2 * sq : 2 * sq + 1;
-        Elem2 Kc;
-        elem2(mc, pc, Kc);
+        const Elem2 &Kc = ce[pc];
         int cE[6], cB[8];
         cell_dofs2(mc, sc, pc, cE, cB);
         GeoT<dd> Gf;
@@ -1629,11 +1652,9 @@ void build_prolongation2(const Mesh &mf, const Space2 &sf, const Mesh &mc, const
                     out[a][a2] = acc;
                 }
         };
-        // E DoFs of the fine cell
-        for (int t = 0; t < 6; ++t) {
+        for (int t = 0; t < 6; ++t) {          // E DoFs owned by this fine cell
             const int I = gE[t];
-            if (I < 0 || done[I]) continue;
-            done[I] = 1;
+            if (I < 0 || owner[I] != c) continue;
             for (int j = 0; j < 6; ++j) {
                 if (cE[j] < 0) continue;
                 dd f[3][3];
@@ -1647,23 +1668,21 @@ void build_prolongation2(const Mesh &mf, const Space2 &sf, const Mesh &mc, const
                 rows[I].push_back({cE[j], v});
             }
         }
-        // B DoFs of the fine cell
-        for (int t = 0; t < 8; ++t) {
-            const int I = gB[t];
-            if (I < 0 || done[I]) continue;
-            done[I] = 1;
-            for (int j = 0; j < 8; ++j) {
-                if (cB[j] < 0) continue;
-                dd F[3][3][2], comp[3][3], fin[3][3];
-                for (int r = 0; r < 2; ++r) {
-                    for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b) comp[a][b] = Kc.V[j][a][b][r];
-                    to_fine(comp, fin);
-                    for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b) F[a][b][r] = fin[a][b];
-                }
-                dd out[8];
-                rt2_dofs(Gf, mf.N, F, out);
-                rows[I].push_back({cB[j], out[t]});
+        bool anyB = false;
+        for (int t = 0; t < 8; ++t) anyB = anyB || (gB[t] >= 0 && owner[gB[t]] == c);
+        if (!anyB) continue;
+        for (int j = 0; j < 8; ++j) {          // B DoFs owned by this fine cell
+            if (cB[j] < 0) continue;
+            dd F[3][3][2], comp[3][3], fin[3][3];
+            for (int r = 0; r < 2; ++r) {
+                for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b) comp[a][b] = Kc.V[j][a][b][r];
+                to_fine(comp, fin);
+                for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b) F[a][b][r] = fin[a][b];
             }
+            dd out[8];
+            rt2_dofs(Gf, mf.N, F, out);
+            for (int t = 0; t < 8; ++t)
+                if (gB[t] >= 0 && owner[gB[t]] == c) rows[gB[t]].push_back({cB[j], out[t]});
         }
     }
     rp.assign(sf.n + 1, 0);
