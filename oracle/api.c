@@ -33,6 +33,7 @@ typedef struct {
 
 typedef struct {
     int block, dim, nlev;
+    int degree;       /* element degree k (NEXT-2) */
     OParams p;
     double theta;
     int smoother, smoother_its;   /* 0: nu_pre / nu_post Richardson sweeps; 1: GMRES(m) (NEXT-1) */
@@ -75,7 +76,8 @@ OCtx *orc_create_masked(int block, int dim, int N, int nlev, const double *dpara
     c->p.nu_pre = iparams[0]; c->p.nu_post = iparams[1];
     c->p.dt = dparams[7]; c->p.picard = iparams[2];
     int degree = iparams[3];
-    if (!(degree == 1 || (degree == 2 && block == ORC_EB && dim == 2))) { free(c); return NULL; }
+    if (!(degree == 1 || (degree == 2 && dim == 2))) { free(c); return NULL; }
+    c->degree = degree;
     c->lv = calloc((size_t)nlev, sizeof(OLevel));
     int lo = cmask_fine ? nlev - 1 : 0;
     for (int l = nlev - 1; l >= lo; l--) {
@@ -244,6 +246,16 @@ int orc_patch_lu(OCtx *c, int l, i64 i, double *lu, int *perm) {
 }
 
 /* one sweep S(x; b) on level l (R-sweep). returns 0 / 1+patch if singular */
+/* update weight of DoF d ("u^{k+1} = u^k + sum_i w_i du_i"):
+ * R-weights (k = 1): the partition of unity theta / m_d;
+ * R-weights2 (k = 2): the uniform theta / max_d m_d -- a per-subspace damping parameter,
+ * which keeps every local kernel correction in the kernel (at k = 2 the multiplicities
+ * differ inside a patch: facet DoFs 2, cell DoFs 3, so 1/m_d would not).            */
+static double dof_weight(const OCtx *c, const OPatches *pt, i64 d) {
+    if (c->degree == 2) return c->theta * (1.0 / (pt->mmax > 0 ? pt->mmax : 1));
+    return c->theta * (1.0 / pt->mult[d]);
+}
+
 static i64 sweep(OCtx *c, int l, int x_is_zero, const double *b, double *x) {
     OLevel *L = &c->lv[l];
     i64 bad = factor_level(c, l);
@@ -263,7 +275,7 @@ static i64 sweep(OCtx *c, int l, int x_is_zero, const double *b, double *x) {
     for (i64 d = 0; d < n; d++) {
         double cd = 0.0;
         for (i64 t = pt->dptr[d]; t < pt->dptr[d + 1]; t++) cd += y[pt->dslot[t]];
-        double wd = c->theta * (1.0 / pt->mult[d]);
+        double wd = dof_weight(c, pt, d);
         x[d] = fma(wd, cd, x[d]);
     }
     free(r); free(y); free(rl);
@@ -311,7 +323,7 @@ i64 orc_sweep_sample(OCtx *c, int l, int x_is_zero, const double *b, const doubl
             od_lu_solve(a, ni, perm, rl, yl);
             cd += yl[slot - pt->ptr[i]];
         }
-        double wd = c->theta * (1.0 / pt->mult[d]);
+        double wd = dof_weight(c, pt, d);
         out[s] = fma(wd, cd, x_is_zero ? 0.0 : x[d]);
     }
     free(a); free(perm); free(rl); free(yl);
@@ -525,6 +537,8 @@ int orc_set_patches(OCtx *c, int l, i64 np, const i64 *ptr, const int *dofs) {
     memcpy(pt->dofs, dofs, sizeof(int) * used);
     pt->mult = calloc((size_t)n, sizeof(int));
     for (i64 t = 0; t < used; t++) pt->mult[dofs[t]]++;
+    pt->mmax = 0;
+    for (i64 d = 0; d < n; d++) if (pt->mult[d] > pt->mmax) pt->mmax = pt->mult[d];
     pt->dptr = calloc((size_t)n + 1, sizeof(i64));
     for (i64 d = 0; d < n; d++) pt->dptr[d + 1] = pt->dptr[d] + pt->mult[d];
     pt->dslot = malloc(sizeof(i64) * (used ? used : 1));

@@ -354,6 +354,14 @@ i64 oc_find(const OCsr *a, i64 row, int col) {
 /* free DoFs (with -1 for constrained) of the local basis of cell c, in local order */
 static int cell_dofs(const OMesh *m, const OSpace *s, i64 c, int *out) {
     int d = m->dim, n = 0;
+    if (s->degree == 2 && s->block == ORC_VEL) {   /* BDM2: facets x 3, then cell x 3 */
+        for (int q = 0; q < 3; q++) {
+            int f0 = s->fdof[om_facet_of_cell(m, c, q)];
+            for (int a = 0; a < 3; a++) out[n++] = f0 < 0 ? -1 : f0 + a;
+        }
+        for (int a = 0; a < 3; a++) out[n++] = s->cdof[c] + a;
+        return n;
+    }
     if (s->degree == 2) {             /* CG2 (vertices, edges) then RT2 (edges x 2, cell x 2) */
         for (int a = 0; a < 3; a++) out[n++] = s->vdof[m->cv[c * 3 + a]];
         for (int q = 0; q < 3; q++) out[n++] = s->edof[m->ce[c * 3 + q]];
@@ -719,6 +727,8 @@ static void assemble_vel(OCsr *A, Accum *S, signed char *cnt, const OMesh *m, co
 
 static void assemble_eb2(OCsr *A, Accum *S, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
                          const unsigned char *cmask);
+static void assemble_vel2(OCsr *A, Accum *S, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
+                          const unsigned char *cmask);
 
 int oa_assemble_masked(OCsr *A, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
                        const unsigned char *cmask) {
@@ -726,7 +736,8 @@ int oa_assemble_masked(OCsr *A, const OMesh *m, const OSpace *s, const OParams *
     if (s->degree == 2) {
         Accum S2;
         S2.acc = calloc((size_t)(A->nnz ? A->nnz : 1), sizeof(real));
-        assemble_eb2(A, &S2, m, s, p, w, cmask);
+        if (s->block == ORC_VEL) assemble_vel2(A, &S2, m, s, p, w, cmask);
+        else assemble_eb2(A, &S2, m, s, p, w, cmask);
         finish(A, &S2);
         free(S2.acc);
         return 0;
@@ -1315,9 +1326,9 @@ static void rt2_functionals(const Cell *K, int Ncells, const Q2 *f, real *out) {
     }
 }
 
-/* Gauss-Jordan inverse with partial pivoting (n <= 8), row-major */
+/* Gauss-Jordan inverse with partial pivoting (n <= 12), row-major */
 static int mat_inv(int n, const real *a, real *inv) {
-    real w[8][16];
+    real w[12][24];
     for (int i = 0; i < n; i++)
         for (int j = 0; j < 2 * n; j++) w[i][j] = j < n ? a[i * n + j] : (real)(j - n == i);
     for (int k = 0; k < n; k++) {
@@ -1357,6 +1368,179 @@ static void basis_rt2(const Cell *K, int Ncells, Q2 *B) {
         for (int k = 0; k < 8; k++)
             for (int l = 0; l < 2; l++)
                 for (int t = 0; t < 6; t++) B[j].c[l][t] += C[k * 8 + j] * p[k].c[l][t];
+    }
+}
+
+/* BDM2 (velocity, k = 2; reading R-basis2): per local facet q (vertices lv0 < lv1, area
+ * vector A = |f| n_f of the global orientation) N_{q,s}(u) = u(x_s) . A at x_0 = X_lv0,
+ * x_1 = X_lv1, x_2 = the midpoint; per cell N_{K,e}(u) = int_K u . omega_e for the Whitney
+ * functions omega_e = lam_i grad lam_j - lam_j grad lam_i of the local edges e = (i < j)
+ * in the order (0,1), (0,2), (1,2).  Local order: q = 0..2 x s = 0..2, then e = 0..2. */
+static void whitney_at(const Cell *K, int e, const real *x, real *out) {
+    int lv[2];
+    om_edge_local_verts(2, e, lv);
+    real li = bary_at(K, lv[0], x), lj = bary_at(K, lv[1], x);
+    for (int r = 0; r < 2; r++) out[r] = li * K->g[lv[1]][r] - lj * K->g[lv[0]][r];
+    out[2] = 0;
+}
+
+static void bdm2_functionals(const Cell *K, const Q2 *f, real *out) {
+    for (int q = 0; q < 3; q++) {
+        real P[3][3], A[3], v[3];
+        facet_points(K, q, P);
+        facet_area_vector(2, P, A);
+        real X[3][3] = {{P[0][0], P[0][1], 0}, {P[1][0], P[1][1], 0},
+                        {(P[0][0] + P[1][0]) / 2, (P[0][1] + P[1][1]) / 2, 0}};
+        for (int s = 0; s < 3; s++) { q2_eval(f, K, X[s], v); out[3 * q + s] = v[0] * A[0] + v[1] * A[1]; }
+    }
+    real xq[64][3], wq[64];
+    int nq = cell_rule(K, 3, xq, wq);
+    for (int e = 0; e < 3; e++) {
+        real acc = 0;
+        for (int t = 0; t < nq; t++) {
+            real v[3], om[3];
+            q2_eval(f, K, xq[t], v);
+            whitney_at(K, e, xq[t], om);
+            acc += wq[t] * (v[0] * om[0] + v[1] * om[1]);
+        }
+        out[9 + e] = acc;
+    }
+}
+
+/* BDM2 local basis dual to bdm2_functionals, from the monomial basis of P2^2 */
+static void basis_bdm2(const Cell *K, Q2 *B) {
+    Q2 p[12];
+    memset(p, 0, sizeof p);
+    for (int l = 0; l < 2; l++) for (int k = 0; k < 6; k++) p[6 * l + k].c[l][k] = 1;
+    real M[144], C[144], col[12];
+    for (int j = 0; j < 12; j++) {
+        bdm2_functionals(K, &p[j], col);
+        for (int i = 0; i < 12; i++) M[i * 12 + j] = col[i];
+    }
+    mat_inv(12, M, C);
+    for (int j = 0; j < 12; j++) {
+        memset(&B[j], 0, sizeof(Q2));
+        for (int k = 0; k < 12; k++)
+            for (int l = 0; l < 2; l++)
+                for (int t = 0; t < 6; t++) B[j].c[l][t] += C[k * 12 + j] * p[k].c[l][t];
+    }
+}
+
+static void cell_dofs_vel2(const OMesh *m, const OSpace *s, i64 c, int *g) {
+    for (int q = 0; q < 3; q++) {
+        int f0 = s->fdof[om_facet_of_cell(m, c, q)];
+        for (int a = 0; a < 3; a++) g[3 * q + a] = f0 < 0 ? -1 : f0 + a;
+    }
+    for (int a = 0; a < 3; a++) g[9 + a] = s->cdof[c] + a;
+}
+
+/* AL velocity block at k = 2 (same forms as assemble_vel, R-vel):
+ * cell terms (2/Re)(eps u, eps v) - (u, div(v (x) w)) + gamma (div u, div v)
+ * [+ (1/dt)(u, v) + S (u x B^n, v x B^n)], facet terms SIPG (sigma from the parameters,
+ * 10 k^2 = 40 at k = 2) + upwind; every integrand by quadrature (degree <= 4). */
+static void assemble_vel2(OCsr *A, Accum *S, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
+                          const unsigned char *cmask) {
+    real xq[64][3], wq[64];
+    const real nu2 = (real)2 / p->Re;
+    for (i64 c = 0; c < m->nc; c++) {
+        if (cmask && !cmask[c]) continue;
+        Cell K;
+        cell_geom(m, c, &K);
+        Q2 F[12];
+        int gi[12];
+        basis_bdm2(&K, F);
+        cell_dofs_vel2(m, s, c, gi);
+        double pot[4][3];
+        real wx[3], bx[3] = {0, 0, 0};
+        cell_pot(m, c, w, pot);
+        cell_wind(&K, pot, wx);
+        if (p->bn) { double bp[4][3]; cell_pot(m, c, p->bn, bp); cell_wind(&K, bp, bx); }
+        real loc[144] = {0};
+        int nq = cell_rule(&K, 3, xq, wq);
+        for (int t = 0; t < nq; t++) {
+            real fv[12][3], G[12][2][2], ep[12][2][2], dv[12], gw[12][2];
+            for (int a = 0; a < 12; a++) {
+                q2_eval(&F[a], &K, xq[t], fv[a]);
+                q2_grad(&F[a], &K, xq[t], G[a]);
+                for (int l = 0; l < 2; l++) for (int k = 0; k < 2; k++) ep[a][l][k] = (G[a][l][k] + G[a][k][l]) / 2;
+                dv[a] = G[a][0][0] + G[a][1][1];
+                for (int l = 0; l < 2; l++) gw[a][l] = G[a][l][0] * wx[0] + G[a][l][1] * wx[1];
+            }
+            for (int i = 0; i < 12; i++)
+                for (int j = 0; j < 12; j++) {
+                    real ee = 0;
+                    for (int l = 0; l < 2; l++) for (int k = 0; k < 2; k++) ee += ep[j][l][k] * ep[i][l][k];
+                    real v = nu2 * ee - (fv[j][0] * gw[i][0] + fv[j][1] * gw[i][1]) + (real)p->gamma * dv[j] * dv[i];
+                    if (p->dt > 0) v += (fv[j][0] * fv[i][0] + fv[j][1] * fv[i][1]) / p->dt;
+                    if (p->bn)
+                        v += p->S * (fv[j][0] * bx[1] - fv[j][1] * bx[0]) * (fv[i][0] * bx[1] - fv[i][1] * bx[0]);
+                    loc[i * 12 + j] += wq[t] * v;
+                }
+        }
+        scatter(A, S, gi, 12, gi, 12, loc, 12);
+    }
+    static real floc[24 * 24];
+    for (i64 f = 0; f < m->nfacet; f++) {
+        int cp = m->fcell[2 * f], cm = m->fcell[2 * f + 1];
+        if (cmask && !cmask[cp] && !(cm >= 0 && cmask[cm])) continue;
+        int interior = cm >= 0, nb = 12;
+        Cell Kp, Km;
+        Q2 F[24];
+        int gi[24], side[24];
+        cell_geom(m, cp, &Kp);
+        basis_bdm2(&Kp, F);
+        cell_dofs_vel2(m, s, cp, gi);
+        for (int a = 0; a < 12; a++) side[a] = +1;
+        if (interior) {
+            cell_geom(m, cm, &Km);
+            basis_bdm2(&Km, F + 12);
+            cell_dofs_vel2(m, s, cm, gi + 12);
+            for (int a = 12; a < 24; a++) side[a] = -1;
+            nb = 24;
+        }
+        int qf = -1;
+        for (int q = 0; q < 3; q++) if (om_facet_of_cell(m, cp, q) == f) qf = q;
+        real P[3][3], Av[3];
+        facet_points(&Kp, qf, P);
+        facet_area_vector(2, P, Av);
+        real an = RSQRT(dot3(Av, Av)), n[3];
+        double sgn = facet_sign(&Kp, qf, Av);
+        for (int k = 0; k < 3; k++) n[k] = sgn * Av[k] / an;
+        real avg = interior ? (real)1 / 2 : (real)1;
+        real pen = (real)p->sigma / ((real)p->Re * an);
+        double pot[4][3];
+        real wx[3];
+        cell_pot(m, cp, w, pot);
+        cell_wind(&Kp, pot, wx);
+        real wn = dot3(wx, n), awn = RFABS(wn);
+        memset(floc, 0, sizeof(floc));
+        int nq = facet_rule(2, P, xq, wq);
+        for (int t = 0; t < nq; t++) {
+            real fv[24][3], en[24][2];
+            for (int a = 0; a < nb; a++) {
+                const Cell *Ka = side[a] > 0 ? &Kp : &Km;
+                real G[2][2];
+                q2_eval(&F[a], Ka, xq[t], fv[a]);
+                q2_grad(&F[a], Ka, xq[t], G);
+                for (int l = 0; l < 2; l++)
+                    en[a][l] = (G[l][0] + G[0][l]) / 2 * n[0] + (G[l][1] + G[1][l]) / 2 * n[1];
+            }
+            for (int i = 0; i < nb; i++) {
+                real Ji = side[i];
+                for (int j = 0; j < nb; j++) {
+                    real Jj = side[j];
+                    real vv = fv[j][0] * fv[i][0] + fv[j][1] * fv[i][1];
+                    real t1 = -nu2 * avg * (en[j][0] * fv[i][0] + en[j][1] * fv[i][1]) * Ji;
+                    real t2 = -nu2 * avg * (fv[j][0] * en[i][0] + fv[j][1] * en[i][1]) * Jj;
+                    real t3 = pen * Jj * Ji * vv;
+                    real up;
+                    if (interior) up = (side[j] > 0 ? (wn + awn) / 2 : -(-wn + awn) / 2) * vv * Ji;
+                    else up = (wn + awn) / 2 * vv;
+                    floc[i * 24 + j] += wq[t] * (t1 + t2 + t3 + up);
+                }
+            }
+        }
+        scatter(A, S, gi, nb, gi, nb, floc, 24);
     }
 }
 
@@ -1435,6 +1619,28 @@ static void assemble_eb2(OCsr *A, Accum *S, const OMesh *m, const OSpace *s, con
 static real dof_functional2(const OMesh *mf, const OSpace *sf, i64 I, const Q2 *F, const Cell *Kc) {
     int kind = sf->dkind[I], ent = sf->dent[I], sub = sf->dsub[I];
     real v[3];
+    if (sf->block == ORC_VEL) {                 /* BDM2 functionals of the fine mesh */
+        if (kind == 2) {
+            real P[3][3] = {{0}}, A[3];
+            for (int a = 0; a < 2; a++)
+                for (int k = 0; k < 2; k++) P[a][k] = (real)mf->lat[3 * mf->ev[2 * ent + a] + k] / mf->N;
+            facet_area_vector(2, P, A);
+            real x[3] = {sub == 2 ? (P[0][0] + P[1][0]) / 2 : P[sub][0], sub == 2 ? (P[0][1] + P[1][1]) / 2 : P[sub][1], 0};
+            q2_eval(F, Kc, x, v);
+            return v[0] * A[0] + v[1] * A[1];
+        }
+        Cell Kf;
+        cell_geom(mf, ent, &Kf);
+        real xq[64][3], wq[64], acc = 0;
+        int nq = cell_rule(&Kf, 3, xq, wq);
+        for (int t = 0; t < nq; t++) {
+            real om[3];
+            q2_eval(F, Kc, xq[t], v);
+            whitney_at(&Kf, sub, xq[t], om);
+            acc += wq[t] * (v[0] * om[0] + v[1] * om[1]);
+        }
+        return acc;
+    }
     if (kind == 0) {
         real x[3] = {(real)mf->lat[3 * ent] / mf->N, (real)mf->lat[3 * ent + 1] / mf->N, 0};
         q2_eval(F, Kc, x, v);
@@ -1496,12 +1702,15 @@ static int op_prolongation2(OCsr *P, const OMesh *mf, const OSpace *sf, const OM
         i64 ccell = parent_cell(mf, mc, cf);
         Cell Kc;
         cell_geom(mc, ccell, &Kc);
-        Q2 F[8];
-        int gE[6], gB[8], nb;
+        Q2 F[12];
+        int gE[6], gB[8], gV[12], nb;
         const int *gJ;
-        cell_dofs2(mc, sc, ccell, gE, gB);
-        if (kind <= 1) { for (int a = 0; a < 6; a++) F[a] = basis_cg2(&Kc, a); nb = 6; gJ = gE; }
-        else { basis_rt2(&Kc, mc->N, F); nb = 8; gJ = gB; }
+        if (sf->block == ORC_VEL) { basis_bdm2(&Kc, F); cell_dofs_vel2(mc, sc, ccell, gV); nb = 12; gJ = gV; }
+        else {
+            cell_dofs2(mc, sc, ccell, gE, gB);
+            if (kind <= 1) { for (int a = 0; a < 6; a++) F[a] = basis_cg2(&Kc, a); nb = 6; gJ = gE; }
+            else { basis_rt2(&Kc, mc->N, F); nb = 8; gJ = gB; }
+        }
         for (int b = 0; b < nb; b++) {
             if (gJ[b] < 0) continue;
             real val = dof_functional2(mf, sf, I, &F[b], &Kc);
@@ -1545,6 +1754,12 @@ static int op_prolongation2(OCsr *P, const OMesh *mf, const OSpace *sf, const OM
 
 /* k = 2 local basis for the MMS helpers: E (component 0 of the E-B field triple) then B */
 static int local_basis2(const OMesh *m, const OSpace *s, i64 c, const Cell *K, Q2 *F, int *gi, int *off, int *ncp) {
+    if (s->block == ORC_VEL) {
+        basis_bdm2(K, F);
+        cell_dofs_vel2(m, s, c, gi);
+        for (int a = 0; a < 12; a++) { off[a] = 0; ncp[a] = 2; }
+        return 12;
+    }
     int gE[6], gB[8];
     cell_dofs2(m, s, c, gE, gB);
     for (int a = 0; a < 6; a++) { F[a] = basis_cg2(K, a); gi[a] = gE[a]; off[a] = 0; ncp[a] = 1; }

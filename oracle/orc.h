@@ -122,6 +122,7 @@ typedef struct {
     i64 *ptr;              /* np+1 offsets into dofs                                  */
     int *dofs;             /* ascending global free indices                           */
     int *mult;             /* n : multiplicity m_d                                    */
+    int mmax;              /* max_d m_d (R-weights2)                                   */
     /* DoF -> (slot) lists in ascending patch order */
     i64 *dptr;             /* n+1 */
     i64 *dslot;            /* positions into dofs[] (= slot index)                    */

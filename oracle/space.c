@@ -17,7 +17,32 @@
 #include <string.h>
 #include "orc.h"
 
-/* k = 2 (NEXT-2; reading R-num2): 2D E-B only.  E (CG2): free vertex DoFs in
+/* k = 2 velocity (BDM2, 2D; reading R-num2): 3 DoFs per interior facet (facet order; sub
+ * 0/1 = |f| u.n at the lower/higher vertex, 2 = at the midpoint), then 3 per cell (cell
+ * order; sub e = moment against the Whitney function of local edge e).                  */
+static int os_build2_vel(OSpace *s, const OMesh *m) {
+    s->vdof = malloc(sizeof(int) * m->nv);
+    s->edof = malloc(sizeof(int) * m->ne);
+    s->fdof = malloc(sizeof(int) * m->nfacet);
+    s->cdof = malloc(sizeof(int) * m->nc);
+    for (i64 v = 0; v < m->nv; v++) s->vdof[v] = -1;
+    for (i64 e = 0; e < m->ne; e++) s->edof[e] = -1;
+    i64 n = 0;
+    for (i64 f = 0; f < m->nfacet; f++) { s->fdof[f] = m->fcell[2 * f + 1] >= 0 ? (int)n : -1; if (s->fdof[f] >= 0) n += 3; }
+    for (i64 c = 0; c < m->nc; c++) { s->cdof[c] = (int)n; n += 3; }
+    s->n = n;
+    s->dkind = malloc(sizeof(int) * (n ? n : 1));
+    s->dent = malloc(sizeof(int) * (n ? n : 1));
+    s->dsub = malloc(sizeof(int) * (n ? n : 1));
+    for (i64 f = 0; f < m->nfacet; f++)
+        if (s->fdof[f] >= 0)
+            for (int a = 0; a < 3; a++) { s->dkind[s->fdof[f] + a] = 2; s->dent[s->fdof[f] + a] = (int)f; s->dsub[s->fdof[f] + a] = a; }
+    for (i64 c = 0; c < m->nc; c++)
+        for (int a = 0; a < 3; a++) { s->dkind[s->cdof[c] + a] = 3; s->dent[s->cdof[c] + a] = (int)c; s->dsub[s->cdof[c] + a] = a; }
+    return 0;
+}
+
+/* k = 2 (NEXT-2; reading R-num2): 2D E-B.  E (CG2): free vertex DoFs in
  * vertex order, then free edge-midpoint DoFs in edge order; B (RT2): 2 DoFs per interior
  * edge (edge order; sub 0/1 = moment against lambda of the lower/higher vertex), then 2
  * DoFs per cell (cell order; sub r = component).  Boundary DoFs removed (R-bc).    */
@@ -50,8 +75,8 @@ int os_build(OSpace *s, const OMesh *m, int block, int degree) {
     memset(s, 0, sizeof(*s));
     s->block = block; s->dim = m->dim; s->degree = degree;
     if (degree == 2) {
-        if (block != ORC_EB || m->dim != 2) return 1;
-        return os_build2(s, m);
+        if (m->dim != 2) return 1;
+        return block == ORC_EB ? os_build2(s, m) : os_build2_vel(s, m);
     }
     if (degree != 1) return 1;
     s->vdof = malloc(sizeof(int) * m->nv);
@@ -144,7 +169,13 @@ int opt_build(OPatches *pt, const OMesh *m, const OSpace *s) {
             i64 c = vc[t];
             /* all free DoFs of cell c */
             int cand[64]; int nc = 0;
-            if (s->degree == 2) {                    /* CG2 x RT2 (2D) */
+            if (s->degree == 2 && s->block == ORC_VEL) {   /* BDM2 (2D) */
+                for (int q = 0; q < 3; q++) {
+                    int d = s->fdof[om_facet_of_cell(m, c, q)];
+                    if (d >= 0) { cand[nc++] = d; cand[nc++] = d + 1; cand[nc++] = d + 2; }
+                }
+                for (int a = 0; a < 3; a++) cand[nc++] = s->cdof[c] + a;
+            } else if (s->degree == 2) {                    /* CG2 x RT2 (2D) */
                 for (int q = 0; q < 3; q++) { int d = s->vdof[m->cv[c * 3 + q]]; if (d >= 0) cand[nc++] = d; }
                 for (int q = 0; q < 3; q++) { int d = s->edof[m->ce[c * 3 + q]]; if (d >= 0) cand[nc++] = d; }
                 for (int q = 0; q < 3; q++) {
@@ -181,6 +212,8 @@ int opt_build(OPatches *pt, const OMesh *m, const OSpace *s) {
     i64 n = s->n;
     pt->mult = calloc((size_t)n, sizeof(int));
     for (i64 t = 0; t < used; t++) pt->mult[pt->dofs[t]]++;
+    pt->mmax = 0;
+    for (i64 d = 0; d < n; d++) if (pt->mult[d] > pt->mmax) pt->mmax = pt->mult[d];
     pt->dptr = calloc((size_t)n + 1, sizeof(i64));
     for (i64 d = 0; d < n; d++) pt->dptr[d + 1] = pt->dptr[d] + pt->mult[d];
     pt->dslot = malloc(sizeof(i64) * (used ? used : 1));

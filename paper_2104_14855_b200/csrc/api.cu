@@ -298,8 +298,13 @@ mhdp_status build_patches(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
     }
     std::vector<int> dslot(sum_n), fill(dptr.begin(), dptr.end() - 1);
     for (int64_t t = 0; t < sum_n; ++t) dslot[fill[H.pdofs[t]]++] = (int)t;   // ascending slot = ascending patch
+    // R-weights (k = 1): theta / m_d;  R-weights2 (k = 2): the uniform theta / max_d m_d (a
+    // per-subspace damping parameter of P:538 that keeps local kernel corrections in the kernel)
+    int mmax = 1;
+    for (int64_t d = 0; d < H.n; ++d) mmax = std::max(mmax, mult[d]);
     std::vector<double> wd(H.n);
-    for (int64_t d = 0; d < H.n; ++d) wd[d] = ctx->p.theta * (1.0 / mult[d]);  // R-weights
+    for (int64_t d = 0; d < H.n; ++d)
+        wd[d] = ctx->p.theta * (1.0 / (ctx->p.degree == 2 ? mmax : mult[d]));
     mhdp_status st;
     if ((st = upload(ctx, &P.pn, pn.data(), np))) return st;
     if ((st = upload(ctx, &P.poff, H.pptr.data(), np))) return st;
