@@ -27,6 +27,8 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <array>
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -1706,6 +1708,448 @@ void build_prolongation2(const Mesh &mf, const Space2 &sf, const Mesh &mc, const
         for (size_t t = 0; t < fin[I].size(); ++t) { ci[rp[I] + t] = fin[I][t].first; vv[rp[I] + t] = fin[I][t].second; }
 }
 
+
+// ---------------- k = 2 AL velocity block, BDM2 (R-basis2, R-vel; sigma from the
+// parameters, 10 k^2 = 40) -------------------------------------------------------
+// DoFs: per facet q (opposite vertex q; vertices fl0 < fl1, area vector A = |f| n_f of the
+// global orientation) N_{q,s}(u) = u(x_s) . A at x_0 = X_fl0, x_1 = X_fl1, x_2 = midpoint;
+// per cell N_{K,e}(u) = int_K u . (lam_i g_j - lam_j g_i), e = (i<j) in (0,1), (0,2), (1,2).
+// Local order: q = 0..2 x s = 0..2, then e = 0..2.  Primal basis lam_a lam_b e_r.
+void build_space2_vel(Space2 &s, const Mesh &m) {
+    s.vdof.assign(m.nv, -1); s.edof.assign(m.ne, -1); s.fdof.assign(m.nfacet, -1); s.cdof.assign(m.nc, -1);
+    i64 n = 0;
+    for (i64 f = 0; f < m.nfacet; ++f) if (!m.common_bnd(&m.ev[2 * f], 2)) { s.fdof[f] = (int)n; n += 3; }
+    for (i64 c = 0; c < m.nc; ++c) { s.cdof[c] = (int)n; n += 3; }
+    s.n = n;
+    s.nE = 0;
+}
+
+void cell_dofs_v2(const Mesh &m, const Space2 &s, i64 c, int *g) {
+    for (int q = 0; q < 3; ++q) {
+        const int f0 = s.fdof[m.cfacet[3 * c + q]];
+        for (int t = 0; t < 3; ++t) g[3 * q + t] = f0 < 0 ? -1 : f0 + t;
+    }
+    for (int e = 0; e < 3; ++e) g[9 + e] = s.cdof[c] + e;
+}
+
+struct ElemV2 {
+    GeoT<dd> G;
+    dd V[12][3][3][2];       // basis j = sum V[a][b] lam_a lam_b
+    dd Gr[12][3][2][2];      // grad (row l = component, col k = direction) = sum_c lam_c Gr[c]
+};
+
+// the 12 BDM2 functionals of cell G applied to sum V[a][b] lam_a lam_b
+void bdm2_dofs(const GeoT<dd> &G, const dd V[3][3][2], dd *out) {
+    const BaryTables &T = bary_tables();
+    for (int q = 0; q < 3; ++q) {
+        dd A[3];
+        int fl[3];
+        facet_area(G, q, A, fl);
+        for (int s = 0; s < 3; ++s) {
+            dd lam[3] = {dd(0.0), dd(0.0), dd(0.0)};
+            if (s < 2) lam[fl[s]] = dd(1.0);
+            else { lam[fl[0]] = dd(0.5); lam[fl[1]] = dd(0.5); }
+            dd u[2] = {dd(0.0), dd(0.0)};
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b) {
+                    const dd l2 = lam[a] * lam[b];
+                    u[0] += V[a][b][0] * l2;
+                    u[1] += V[a][b][1] * l2;
+                }
+            out[3 * q + s] = u[0] * A[0] + u[1] * A[1];
+        }
+    }
+    for (int e = 0; e < 3; ++e) {
+        const int i = E2V[e][0], j = E2V[e][1];
+        dd acc(0.0);
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) {
+                const dd vgj = V[a][b][0] * G.g[j][0] + V[a][b][1] * G.g[j][1];
+                const dd vgi = V[a][b][0] * G.g[i][0] + V[a][b][1] * G.g[i][1];
+                acc += vgj * T.t3[9 * a + 3 * b + i] - vgi * T.t3[9 * a + 3 * b + j];
+            }
+        out[9 + e] = acc * dd(2.0) * G.vol;
+    }
+}
+
+void elemv2(const Mesh &m, i64 c, ElemV2 &K) {
+    cell_geo(m, c, K.G);
+    const GeoT<dd> &G = K.G;
+    dd Pv[12][3][3][2];
+    memset((void *)Pv, 0, sizeof Pv);
+    int np = 0;
+    for (int a = 0; a < 3; ++a)
+        for (int b = a; b < 3; ++b)
+            for (int r = 0; r < 2; ++r) Pv[np++][a][b][r] = dd(1.0);
+    dd W[12][24];
+    for (int j = 0; j < 12; ++j) {
+        dd col[12];
+        bdm2_dofs(G, Pv[j], col);
+        for (int i = 0; i < 12; ++i) W[i][j] = col[i];
+    }
+    for (int i = 0; i < 12; ++i) for (int j = 0; j < 12; ++j) W[i][12 + j] = dd(i == j ? 1.0 : 0.0);
+    for (int k = 0; k < 12; ++k) {
+        int p = k;
+        for (int i = k + 1; i < 12; ++i) if (to_double(dd_fabs(W[i][k])) > to_double(dd_fabs(W[p][k]))) p = i;
+        if (p != k) for (int j = 0; j < 24; ++j) std::swap(W[k][j], W[p][j]);
+        const dd piv = W[k][k];
+        for (int j = 0; j < 24; ++j) W[k][j] = W[k][j] / piv;
+        for (int i = 0; i < 12; ++i) {
+            if (i == k) continue;
+            const dd l = W[i][k];
+            for (int j = 0; j < 24; ++j) W[i][j] = W[i][j] - l * W[k][j];
+        }
+    }
+    for (int j = 0; j < 12; ++j)
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b)
+                for (int r = 0; r < 2; ++r) {
+                    dd acc(0.0);
+                    for (int k = 0; k < 12; ++k) acc += W[k][12 + j] * Pv[k][a][b][r];
+                    K.V[j][a][b][r] = acc;
+                }
+    // gradients: d_k (lam_a lam_b) = lam_b g_a,k + lam_a g_b,k
+    for (int j = 0; j < 12; ++j)
+        for (int cc = 0; cc < 3; ++cc)
+            for (int l = 0; l < 2; ++l)
+                for (int k = 0; k < 2; ++k) {
+                    dd acc(0.0);
+                    for (int b = 0; b < 3; ++b) acc += K.V[j][cc][b][l] * G.g[b][k] + K.V[j][b][cc][l] * G.g[b][k];
+                    K.Gr[j][cc][l][k] = acc;
+                }
+}
+
+// row li of the cell matrix of element K (test li, trial j = 0..11), without 2|K|
+void vel2_cell_row(const ElemV2 &K, int li, const dd *w, const dd *bx, bool lorentz, const Params &p, dd *row) {
+    const BaryTables &T = bary_tables();
+    const dd nu2 = dd(2.0) / dd(p.Re);
+    dd epi[3][2][2], gwi[3][2], divi[3];
+    for (int cc = 0; cc < 3; ++cc) {
+        for (int l = 0; l < 2; ++l)
+            for (int k = 0; k < 2; ++k) epi[cc][l][k] = (K.Gr[li][cc][l][k] + K.Gr[li][cc][k][l]) * dd(0.5);
+        for (int l = 0; l < 2; ++l) gwi[cc][l] = K.Gr[li][cc][l][0] * w[0] + K.Gr[li][cc][l][1] * w[1];
+        divi[cc] = K.Gr[li][cc][0][0] + K.Gr[li][cc][1][1];
+    }
+    for (int j = 0; j < 12; ++j) {
+        dd ee(0.0), dv(0.0), adv(0.0), ms(0.0), lor(0.0);
+        for (int c1 = 0; c1 < 3; ++c1) {
+            dd epj[2][2];
+            for (int l = 0; l < 2; ++l)
+                for (int k = 0; k < 2; ++k) epj[l][k] = (K.Gr[j][c1][l][k] + K.Gr[j][c1][k][l]) * dd(0.5);
+            const dd divj = K.Gr[j][c1][0][0] + K.Gr[j][c1][1][1];
+            for (int c2 = 0; c2 < 3; ++c2) {
+                const dd t2 = T.t2[3 * c1 + c2];
+                ee += (epj[0][0] * epi[c2][0][0] + epj[0][1] * epi[c2][0][1] + epj[1][0] * epi[c2][1][0] +
+                       epj[1][1] * epi[c2][1][1]) * t2;
+                dv += divj * divi[c2] * t2;
+            }
+        }
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b)
+                for (int cc = 0; cc < 3; ++cc)
+                    adv += (K.V[j][a][b][0] * gwi[cc][0] + K.V[j][a][b][1] * gwi[cc][1]) * T.t3[9 * a + 3 * b + cc];
+        if (p.dt > 0 || lorentz)
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b)
+                    for (int c1 = 0; c1 < 3; ++c1)
+                        for (int c2 = 0; c2 < 3; ++c2) {
+                            const dd t4 = T.t4[27 * a + 9 * b + 3 * c1 + c2];
+                            if (p.dt > 0)
+                                ms += (K.V[j][a][b][0] * K.V[li][c1][c2][0] + K.V[j][a][b][1] * K.V[li][c1][c2][1]) * t4;
+                            if (lorentz)
+                                lor += (K.V[j][a][b][0] * bx[1] - K.V[j][a][b][1] * bx[0]) *
+                                       (K.V[li][c1][c2][0] * bx[1] - K.V[li][c1][c2][1] * bx[0]) * t4;
+                        }
+        dd v = nu2 * ee - adv + dd(p.gamma) * dv;
+        if (p.dt > 0) v += ms / dd(p.dt);
+        if (lorentz) v += dd(p.S) * lor;
+        row[j] = v;
+    }
+}
+
+// trace of cell-basis data on an edge: lam_c = [c == c0] mu0 + [c == c1] mu1
+// quadratic u -> coefficients on mu0^2, mu0 mu1, mu1^2;  linear eps -> on mu0, mu1
+struct Trace2 { dd u[3][2]; dd en[2][2]; };   // en = eps(u) (sgn A) at mu0 / mu1
+
+void vel2_trace(const ElemV2 &K, int j, int c0, int c1, const dd *sA, Trace2 &T) {
+    for (int r = 0; r < 2; ++r) {
+        T.u[0][r] = K.V[j][c0][c0][r];
+        T.u[1][r] = K.V[j][c0][c1][r] + K.V[j][c1][c0][r];
+        T.u[2][r] = K.V[j][c1][c1][r];
+    }
+    const int cs[2] = {c0, c1};
+    for (int t = 0; t < 2; ++t) {
+        const int cc = cs[t];
+        for (int l = 0; l < 2; ++l) {
+            const dd e0 = K.Gr[j][cc][l][0] + K.Gr[j][cc][0][l];
+            const dd e1 = K.Gr[j][cc][l][1] + K.Gr[j][cc][1][l];
+            T.en[t][l] = (e0 * sA[0] + e1 * sA[1]) * dd(0.5);
+        }
+    }
+}
+
+// int_0^1 mu0^p mu1^q (edge of unit measure) = p! q! / (p+q+1)!
+inline dd emom(int p, int q) { return dd(fact(p) * fact(q)) / dd(fact(p + q + 1)); }
+
+// Q = int u_j . v_i,  E = int (a . b) with a linear, b quadratic  (per unit edge measure)
+dd tr_qq(const Trace2 &A, const Trace2 &B) {
+    static const int P[3][2] = {{2, 0}, {1, 1}, {0, 2}};
+    dd acc(0.0);
+    for (int x = 0; x < 3; ++x)
+        for (int y = 0; y < 3; ++y)
+            acc += (A.u[x][0] * B.u[y][0] + A.u[x][1] * B.u[y][1]) * emom(P[x][0] + P[y][0], P[x][1] + P[y][1]);
+    return acc;
+}
+dd tr_lq(const Trace2 &L, const Trace2 &Q) {       // (eps_L sA) . u_Q
+    static const int P[3][2] = {{2, 0}, {1, 1}, {0, 2}};
+    dd acc(0.0);
+    for (int t = 0; t < 2; ++t)
+        for (int y = 0; y < 3; ++y)
+            acc += (L.en[t][0] * Q.u[y][0] + L.en[t][1] * Q.u[y][1]) * emom((t == 0) + P[y][0], (t == 1) + P[y][1]);
+    return acc;
+}
+
+void assemble_vel2(const Mesh &m, const Space2 &s, const Params &p, const double *pot, const double *bpot,
+                   Pattern &P, std::vector<double> &val) {
+    const i64 nc = m.nc;
+    std::vector<ElemV2> el(nc);
+    std::vector<std::array<dd, 3>> wind(nc), bwind(nc);
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < nc; ++c) {
+        elemv2(m, c, el[c]);
+        dd w[3];
+        cell_wind(el[c].G, pot, w);
+        wind[c] = {w[0], w[1], w[2]};
+        dd b[3] = {dd(0.0), dd(0.0), dd(0.0)};
+        if (bpot) cell_wind(el[c].G, bpot, b);
+        bwind[c] = {b[0], b[1], b[2]};
+    }
+    // DoF -> entity, support cells
+    std::vector<int> dkind(s.n), dent(s.n);
+    for (i64 f = 0; f < m.nfacet; ++f)
+        if (s.fdof[f] >= 0) for (int a = 0; a < 3; ++a) { dkind[s.fdof[f] + a] = 0; dent[s.fdof[f] + a] = (int)f; }
+    for (i64 c = 0; c < nc; ++c) for (int a = 0; a < 3; ++a) { dkind[s.cdof[c] + a] = 1; dent[s.cdof[c] + a] = (int)c; }
+    auto support = [&](i64 r, int *cells) -> int {
+        if (dkind[r] == 1) { cells[0] = dent[r]; return 1; }
+        const int f = dent[r];
+        cells[0] = m.fcell[2 * f];
+        if (m.fcell[2 * f + 1] >= 0) { cells[1] = m.fcell[2 * f + 1]; return 2; }
+        return 1;
+    };
+    // pattern: DoFs of the support cells and of their facet neighbours
+    P.rp.assign(s.n + 1, 0);
+    std::vector<std::vector<int>> rows(s.n);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (i64 r = 0; r < s.n; ++r) {
+        int sc[2];
+        const int ns = support(r, sc);
+        std::vector<int> cols;
+        for (int t = 0; t < ns; ++t) {
+            int nb[4] = {sc[t], -1, -1, -1};
+            for (int q = 0; q < 3; ++q) {
+                const int f = m.cfacet[3 * sc[t] + q];
+                nb[q + 1] = m.fcell[2 * f] == sc[t] ? m.fcell[2 * f + 1] : m.fcell[2 * f];
+            }
+            for (int u = 0; u < 4; ++u) {
+                if (nb[u] < 0) continue;
+                int g[12];
+                cell_dofs_v2(m, s, nb[u], g);
+                for (int k = 0; k < 12; ++k) if (g[k] >= 0) cols.push_back(g[k]);
+            }
+        }
+        std::sort(cols.begin(), cols.end());
+        cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+        rows[r] = std::move(cols);
+    }
+    for (i64 r = 0; r < s.n; ++r) P.rp[r + 1] = P.rp[r] + (i64)rows[r].size();
+    P.ci.resize(P.rp[s.n]);
+    for (i64 r = 0; r < s.n; ++r) std::copy(rows[r].begin(), rows[r].end(), P.ci.begin() + P.rp[r]);
+    rows.clear();
+    val.assign(P.rp[s.n], 0.0);
+    const dd nu2 = dd(2.0) / dd(p.Re), pen = dd(p.sigma) / dd(p.Re);
+#pragma omp parallel for schedule(dynamic, 128)
+    for (i64 r = 0; r < s.n; ++r) {
+        const i64 base = P.rp[r], len = P.rp[r + 1] - base;
+        std::vector<dd> acc(len);
+        auto add = [&](int col, const dd &v) { acc[find_col(P, r, col) - base] += v; };
+        int sc[2];
+        const int ns = support(r, sc);
+        // cell terms
+        for (int t = 0; t < ns; ++t) {
+            const int c = sc[t];
+            int g[12];
+            cell_dofs_v2(m, s, c, g);
+            int li = -1;
+            for (int k = 0; k < 12; ++k) if (g[k] == r) li = k;
+            dd row[12];
+            const dd w[3] = {wind[c][0], wind[c][1], wind[c][2]}, b[3] = {bwind[c][0], bwind[c][1], bwind[c][2]};
+            vel2_cell_row(el[c], li, w, b, bpot != nullptr, p, row);
+            const dd twoK = dd(2.0) * el[c].G.vol;
+            for (int k = 0; k < 12; ++k) if (g[k] >= 0) add(g[k], row[k] * twoK);
+        }
+        // facet terms of every facet of the support cells (ascending facet id)
+        std::vector<int> fs;
+        for (int t = 0; t < ns; ++t) for (int q = 0; q < 3; ++q) fs.push_back(m.cfacet[3 * sc[t] + q]);
+        std::sort(fs.begin(), fs.end());
+        fs.erase(std::unique(fs.begin(), fs.end()), fs.end());
+        for (int f : fs) {
+            const int cp = m.fcell[2 * f], cm = m.fcell[2 * f + 1];
+            const bool interior = cm >= 0;
+            const ElemV2 &Kp = el[cp];
+            int qf = -1;
+            for (int q = 0; q < 3; ++q) if (m.cfacet[3 * cp + q] == f) qf = q;
+            dd A[3];
+            int fl[3];
+            facet_area(Kp.G, qf, A, fl);
+            const double sg = facet_sign(Kp.G, qf, A, fl);
+            const dd sA[2] = {dd(sg) * A[0], dd(sg) * A[1]};          // |f| n, n outward of K+
+            const dd WA = wind[cp][0] * sA[0] + wind[cp][1] * sA[1];   // (w.n)|f|
+            const dd aWA = WA.hi < 0 ? -WA : WA;
+            const int v0 = m.ev[2 * f], v1 = m.ev[2 * f + 1];
+            auto loc_of = [&](const ElemV2 &K, int v) { for (int a = 0; a < 3; ++a) if (K.G.v[a] == v) return a; return -1; };
+            const dd avg = interior ? dd(0.5) : dd(1.0);
+            const int sides = interior ? 2 : 1;
+            const int cells[2] = {cp, cm};
+            // test traces: every support cell of r on this facet (both, for r's own facet)
+            for (int t = 0; t < ns; ++t) {
+                const int ci_ = sc[t];
+                if (ci_ != cp && ci_ != cm) continue;
+                const int Ji = ci_ == cp ? 1 : -1;
+                int gi[12];
+                cell_dofs_v2(m, s, ci_, gi);
+                int li = -1;
+                for (int k = 0; k < 12; ++k) if (gi[k] == r) li = k;
+                const ElemV2 &Ki = el[ci_];
+                Trace2 Ti;
+                vel2_trace(Ki, li, loc_of(Ki, v0), loc_of(Ki, v1), sA, Ti);
+                for (int sd = 0; sd < sides; ++sd) {
+                    const int cj = cells[sd];
+                    const int Jj = sd == 0 ? 1 : -1;
+                    const ElemV2 &Kj = el[cj];
+                    const int a0 = loc_of(Kj, v0), a1 = loc_of(Kj, v1);
+                    int gj[12];
+                    cell_dofs_v2(m, s, cj, gj);
+                    dd upc;
+                    if (interior) upc = Jj > 0 ? (WA + aWA) * dd(0.5) : -((-WA + aWA) * dd(0.5));
+                    else upc = (WA + aWA) * dd(0.5);
+                    for (int j = 0; j < 12; ++j) {
+                        if (gj[j] < 0) continue;
+                        Trace2 Tj;
+                        vel2_trace(Kj, j, a0, a1, sA, Tj);
+                        const dd Q = tr_qq(Tj, Ti);
+                        const dd E1 = tr_lq(Tj, Ti);       // (eps_j n) . v_i
+                        const dd E2 = tr_lq(Ti, Tj);       // u_j . (eps_i n)
+                        dd v = -(nu2 * avg * (dd((double)Ji) * E1 + dd((double)Jj) * E2)) +
+                               pen * dd((double)(Jj * Ji)) * Q;
+                        v += (interior ? upc * dd((double)Ji) : upc) * Q;
+                        add(gj[j], v);
+                    }
+                }
+            }
+        }
+        round_row(acc.data(), len, val.data() + base);
+    }
+}
+
+void build_patches2_vel(const Mesh &m, const Space2 &s, std::vector<i64> &pptr, std::vector<int> &pdofs) {
+    std::vector<std::vector<int>> vlist(m.nv);
+    for (i64 f = 0; f < m.nfacet; ++f)
+        if (s.fdof[f] >= 0)
+            for (int t = 0; t < 2; ++t)
+                for (int a = 0; a < 3; ++a) vlist[m.ev[2 * f + t]].push_back(s.fdof[f] + a);
+    for (i64 c = 0; c < m.nc; ++c)
+        for (int t = 0; t < 3; ++t)
+            for (int a = 0; a < 3; ++a) vlist[m.cv[3 * c + t]].push_back(s.cdof[c] + a);
+    pptr.assign(1, 0);
+    pdofs.clear();
+    for (i64 v = 0; v < m.nv; ++v) {
+        auto &L = vlist[v];
+        if (L.empty()) continue;
+        std::sort(L.begin(), L.end());
+        pdofs.insert(pdofs.end(), L.begin(), L.end());
+        pptr.push_back((i64)pdofs.size());
+    }
+}
+
+void build_prolongation2_vel(const Mesh &mf, const Space2 &sf, const Mesh &mc, const Space2 &sc,
+                             std::vector<i64> &rp, std::vector<int> &ci, std::vector<double> &vv) {
+    std::vector<std::vector<std::pair<int, dd>>> rows(sf.n);
+    std::vector<ElemV2> ce(mc.nc);
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < mc.nc; ++c) elemv2(mc, c, ce[c]);
+    std::vector<int> owner(sf.n, INT32_MAX);
+    for (i64 c = mf.nc - 1; c >= 0; --c) {
+        int g[12];
+        cell_dofs_v2(mf, sf, c, g);
+        for (int t = 0; t < 12; ++t) if (g[t] >= 0) owner[g[t]] = (int)c;
+    }
+#pragma omp parallel for schedule(dynamic, 64)
+    for (i64 c = 0; c < mf.nc; ++c) {
+        int g[12];
+        cell_dofs_v2(mf, sf, c, g);
+        bool any = false;
+        for (int t = 0; t < 12; ++t) any = any || (g[t] >= 0 && owner[g[t]] == c);
+        if (!any) continue;
+        int Lf[4][3] = {{0}};
+        int sum[2] = {0, 0};
+        for (int a = 0; a < 3; ++a) {
+            mf.lat(mf.cv[3 * c + a], Lf[a]);
+            for (int r = 0; r < 2; ++r) sum[r] += Lf[a][r];
+        }
+        int cube[2], rel[2];
+        for (int r = 0; r < 2; ++r) { cube[r] = sum[r] / 6; rel[r] = sum[r] - 6 * cube[r]; }
+        const i64 sq = cube[0] + (i64)mc.N * cube[1];
+        const i64 pc = rel[0] > rel[1] ? 2 * sq : 2 * sq + 1;
+        const ElemV2 &Kc = ce[pc];
+        int cg[12];
+        cell_dofs_v2(mc, sc, pc, cg);
+        GeoT<dd> Gf;
+        cell_geo(mf, c, Gf);
+        dd T[3][3];
+        for (int b = 0; b < 3; ++b)
+            for (int a = 0; a < 3; ++a) {
+                dd v(b == 0 ? 1.0 : 0.0);
+                for (int r = 0; r < 2; ++r) v += Kc.G.g[b][r] * (Gf.X[a][r] - Kc.G.X[0][r]);
+                T[b][a] = v;
+            }
+        for (int j = 0; j < 12; ++j) {
+            if (cg[j] < 0) continue;
+            dd F[3][3][2];
+            for (int r = 0; r < 2; ++r)
+                for (int a = 0; a < 3; ++a)
+                    for (int a2 = 0; a2 < 3; ++a2) {
+                        dd acc(0.0);
+                        for (int b = 0; b < 3; ++b)
+                            for (int d2 = 0; d2 < 3; ++d2) acc += Kc.V[j][b][d2][r] * T[b][a] * T[d2][a2];
+                        F[a][a2][r] = acc;
+                    }
+            dd out[12];
+            bdm2_dofs(Gf, F, out);
+            for (int t = 0; t < 12; ++t)
+                if (g[t] >= 0 && owner[g[t]] == c) rows[g[t]].push_back({cg[j], out[t]});
+        }
+    }
+    rp.assign(sf.n + 1, 0);
+    std::vector<std::vector<std::pair<int, double>>> fin(sf.n);
+    for (i64 I = 0; I < sf.n; ++I) {
+        auto &R = rows[I];
+        std::sort(R.begin(), R.end(), [](const std::pair<int, dd> &x, const std::pair<int, dd> &y) { return x.first < y.first; });
+        std::vector<dd> xs(R.size());
+        for (size_t t = 0; t < R.size(); ++t) xs[t] = R[t].second;
+        std::vector<double> rounded(R.size());
+        round_row(xs.data(), (i64)xs.size(), rounded.data());
+        double mx = 0;
+        for (double v : rounded) mx = std::max(mx, std::fabs(v));
+        for (size_t t = 0; t < R.size(); ++t)
+            if (rounded[t] != 0.0 && std::fabs(to_double(xs[t])) >= std::ldexp(mx, -30)) fin[I].push_back({R[t].first, rounded[t]});
+        rp[I + 1] = rp[I] + (i64)fin[I].size();
+    }
+    ci.resize(rp[sf.n]);
+    vv.resize(rp[sf.n]);
+    for (i64 I = 0; I < sf.n; ++I)
+        for (size_t t = 0; t < fin[I].size(); ++t) { ci[rp[I] + t] = fin[I][t].first; vv[rp[I] + t] = fin[I][t].second; }
+}
+
 }  // namespace
 
 std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params &p, const double *w,
@@ -1713,7 +2157,7 @@ std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params
     if ((block != 0 && block != 1) || (dim != 2 && dim != 3) || N < 1 || nlev < 1) return "bad arguments";
     if (N % (1 << (nlev - 1))) return "N not divisible by 2^(nlev-1)";
     if (p.degree != 1 && p.degree != 2) return "degree must be 1 or 2";
-    if (p.degree == 2 && !(block == 0 && dim == 2)) return "degree 2 is built for the 2D E-B block only (NEXT-2)";
+    if (p.degree == 2 && dim != 2) return "degree 2 is built in 2D only (NEXT-2)";
     out.assign(nlev, HostLevel());
     if (p.degree == 2) {
         std::vector<Mesh> meshes(nlev);
@@ -1722,25 +2166,35 @@ std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params
             const int Nl = N >> (nlev - 1 - l), step = 1 << (nlev - 1 - l);
             Mesh &m = meshes[l];
             build_mesh(m, dim, Nl);
-            build_space2(spaces[l], m);
-            std::vector<double> pot(m.nv);
+            if (block == 0) build_space2(spaces[l], m);
+            else build_space2_vel(spaces[l], m);
+            std::vector<double> pot(m.nv), bpot(bn ? m.nv : 0);
             for (i64 v = 0; v < m.nv; ++v) {
                 int q[3];
                 m.lat(v, q);
                 pot[v] = w[q[0] * step + (i64)(N + 1) * (q[1] * step)];
+                if (bn) bpot[v] = bn[q[0] * step + (i64)(N + 1) * (q[1] * step)];
             }
             Pattern P;
             std::vector<double> val;
-            assemble_eb2(m, spaces[l], p, pot.data(), P, val);
+            if (block == 0) assemble_eb2(m, spaces[l], p, pot.data(), P, val);
+            else assemble_vel2(m, spaces[l], p, pot.data(), bn ? bpot.data() : nullptr, P, val);
             HostLevel &H = out[l];
             H.n = spaces[l].n;
             H.rp = std::move(P.rp);
             H.ci = std::move(P.ci);
             H.v = std::move(val);
-            if (l > 0) build_patches2(m, spaces[l], H.pptr, H.pdofs);
+            if (l > 0) {
+                if (block == 0) build_patches2(m, spaces[l], H.pptr, H.pdofs);
+                else build_patches2_vel(m, spaces[l], H.pptr, H.pdofs);
+            }
         }
         for (int l = 1; l < nlev; ++l) {
-            build_prolongation2(meshes[l], spaces[l], meshes[l - 1], spaces[l - 1], out[l].prp, out[l].pci, out[l].pv);
+            if (block == 0)
+                build_prolongation2(meshes[l], spaces[l], meshes[l - 1], spaces[l - 1], out[l].prp, out[l].pci, out[l].pv);
+            else
+                build_prolongation2_vel(meshes[l], spaces[l], meshes[l - 1], spaces[l - 1], out[l].prp, out[l].pci,
+                                        out[l].pv);
             out[l].n_coarser = spaces[l - 1].n;
         }
         return "";

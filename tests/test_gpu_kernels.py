@@ -16,7 +16,7 @@ from gpu_helpers import bits, cuda_vec, host, load_oracle_levels, rel_l2
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("c1", 8, 2), ("c2", 32, 3), ("c3", 16, 3), ("c4", 8, 2), ("c5", 6, 2), ("c2-k2", 32, 3)]
+CASES = [("c1", 8, 2), ("c2", 32, 3), ("c3", 16, 3), ("c4", 8, 2), ("c5", 6, 2), ("c2-k2", 32, 3), ("c3-k2", 16, 3)]
 
 
 @pytest.fixture(scope="module", params=CASES, ids=[f"{c}-N{n}L{l}" for c, n, l in CASES])
@@ -28,7 +28,7 @@ def pair(request, oracle_mod):
     k2 = name.endswith("-k2")                       # NEXT-2: CG2 x RT2 (31-DoF stars)
     cfg = workloads.small(name.replace("-k2", ""), N, L)
     if k2:
-        cfg = dataclasses.replace(cfg, degree=2)
+        cfg = dataclasses.replace(cfg, degree=2, sigma=40.0 if cfg.block == "vel" else cfg.sigma)
     # draw with the finest n of this hierarchy
     probe = oracle_mod.Oracle(cfg, workloads.advecting_potential(cfg, np.array([0.3, -1.1, 0.7])))
     n = probe.n()

@@ -55,7 +55,7 @@ def test_gmres_smoothed_vcycle_and_fgmres_on_oracle_operator(oracle_mod, name, N
     assert np.array_equal(bits(host(xg)), bits(xo))
 
 
-CASES_PB = [("c1", None, None), ("c3", 32, 4), ("c5", 6, 2), ("c2-k2", 64, 4)]
+CASES_PB = [("c1", None, None), ("c3", 32, 4), ("c5", 6, 2), ("c2-k2", 64, 4), ("c3-k2", 32, 4)]
 
 
 @pytest.mark.parametrize("name,N,L", CASES_PB, ids=[f"{c}-{n or 'full'}" for c, n, l in CASES_PB])
@@ -67,7 +67,7 @@ def test_gmres_smoothed_end_to_end(oracle_mod, name, N, L):
     name = name.replace("-k2", "")
     cfg = workloads.CONFIGS[name] if N is None else workloads.small(name, N, L)
     if k2:
-        cfg = dataclasses.replace(cfg, degree=2)
+        cfg = dataclasses.replace(cfg, degree=2, sigma=40.0 if cfg.block == "vel" else cfg.sigma)
     ctx = _ctx()
     w0, _, _ = workloads.draw(cfg, 1, 7)
     ctx.assemble(cfg, w0, smoother="gmres", smoother_its=6)

@@ -21,7 +21,8 @@ TOL = 1e-10
 CASES = [("c1", None, None, 0), ("c1", None, None, 1), ("c1", None, None, 2), ("c2", None, None, 0),
          ("c3", 64, 4, 0), ("c4", 16, 3, 0), ("c5", 6, 2, 0), ("c5", 8, 2, 1),
          ("c4-transient-picard", 8, 2, 0), ("c5-transient", 6, 2, 2), ("c5-lorentz", 6, 2, 3),
-         ("c1-k2", None, None, 0), ("c2-k2", 64, 4, 1), ("c2-k2-transient-picard", 32, 3, 2)]   # NEXT-2
+         ("c1-k2", None, None, 0), ("c2-k2", 64, 4, 1), ("c2-k2-transient-picard", 32, 3, 2),   # NEXT-2
+         ("c3-k2", 32, 4, 0), ("c3-k2-transient", 16, 3, 1), ("c3-k2-lorentz", 16, 3, 2)]
 
 
 def _setup(oracle_mod, name, N, L, seed):
@@ -29,17 +30,21 @@ def _setup(oracle_mod, name, N, L, seed):
     from paper_2104_14855_b200 import mhdp, workloads
     import dataclasses
     variant = {}
-    if "-k2" in name:                                                    # NEXT-2: CG2 x RT2
+    if "-k2" in name:                                                    # NEXT-2: k = 2
         name = name.replace("-k2", "")
         variant["degree"] = 2
+        if name.startswith("c3"):
+            variant["sigma"] = 40.0                                      # 10 k^2
     lorentz = name.endswith("-lorentz")
     if name.endswith("-transient-picard"):
         name = name.split("-")[0]
         variant.update(dt=0.05, picard=1)                                # NEXT-4
     elif name.endswith("-transient"):
-        name, variant = name.split("-")[0], dict(dt=0.01)
+        name = name.split("-")[0]
+        variant.update(dt=0.01)
     elif lorentz:
-        name, variant = name.split("-")[0], dict(S=1e3, dt=0.1)
+        name = name.split("-")[0]
+        variant.update(S=1e3, dt=0.1)
     cfg = workloads.CONFIGS[name] if N is None else workloads.small(name, N, L)
     cfg = dataclasses.replace(cfg, **variant)
     ctx = mhdp.Context(0, torch.cuda.current_stream().cuda_stream)

@@ -169,22 +169,27 @@ def test_coupled_operator_bitexact(mh, oracle_mod, dim, N, L, kw):
 
 
 K2_CASES = [("c1", 8, 2, dict()), ("c2", 32, 3, dict()), ("c2", 16, 3, dict(picard=1, dt=0.05)),
-            ("c2", 64, 4, dict(Rem=7.0))]
+            ("c2", 64, 4, dict(Rem=7.0)),
+            ("c3", 8, 2, dict(sigma=40.0)), ("c3", 32, 4, dict(sigma=40.0, Re=100.0, gamma=1e4)),
+            ("c3", 16, 3, dict(sigma=40.0, dt=0.05)), ("c3-lorentz", 16, 2, dict(sigma=40.0, S=30.0))]
 
 
 @pytest.mark.parametrize("name,N,L,kw", K2_CASES, ids=[f"{c}-N{n}L{l}-{k}" for c, n, l, k in K2_CASES])
 def test_k2_host_setup_bitexact_vs_exact_oracle(mh, oracle_mod, name, N, L, kw):
-    """NEXT-2 (k = 2, 2D E-B, CG2 x RT2): numbering, patches, prolongation (R-prol2) and
-    operator values of the library (closed-form barycentric integrals in double-double,
-    {lam_a psi_q} primal RT2 basis) equal the oracle's exact build (quadrature in
-    __float128, monomial primal basis) bit for bit on every level."""
+    """NEXT-2 (k = 2, 2D): CG2 x RT2 E-B and BDM2 velocity blocks.  Numbering, patches,
+    prolongation (R-prol2) and operator values of the library (closed-form barycentric
+    and edge integrals in double-double; {lam_a psi_q} / {lam_a lam_b e_r} primal bases)
+    equal the oracle's exact build (quadrature in __float128, monomial primal bases) bit
+    for bit on every level."""
     import dataclasses
     from paper_2104_14855_b200 import workloads
-    cfg = dataclasses.replace(workloads.small(name, N, L), degree=2, **kw)
+    lorentz = name.endswith("-lorentz")
+    cfg = dataclasses.replace(workloads.small(name.replace("-lorentz", ""), N, L), degree=2, **kw)
     w, _, _ = workloads.draw(cfg, 1, seed=2)
-    orc = oracle_mod.Oracle(cfg, w, exact=True)
+    bn = workloads.magnetic_potential(cfg, 2) if lorentz else None
+    orc = oracle_mod.Oracle(cfg, w, exact=True, bn=bn)
     ctx = mh.Context(-1)
-    ctx.assemble(cfg, w)
+    ctx.assemble(cfg, w, bn=bn)
     for l in range(L):
         A = orc.csr(l)
         rp, ci, v = ctx.csr(l)
@@ -202,10 +207,10 @@ def test_k2_host_setup_bitexact_vs_exact_oracle(mh, oracle_mod, name, N, L, kw):
         assert np.array_equal(P.v.view(np.uint64), pv.view(np.uint64)), f"level {l}: prolongation values"
 
 
-def test_k2_rejected_outside_2d_eb(mh):
+def test_k2_rejected_in_3d(mh):
     import dataclasses
     from paper_2104_14855_b200 import workloads
-    for name in ("c3", "c4"):
+    for name in ("c4", "c5"):
         cfg = dataclasses.replace(workloads.small(name, 4, 1), degree=2)
         w, _, _ = workloads.draw(cfg, 1, 0)
         ctx = mh.Context(-1)
