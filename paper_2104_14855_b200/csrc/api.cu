@@ -15,6 +15,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <numeric>
 
 #include "../../include/mhdp.h"
 #include "kernels.cuh"
@@ -318,6 +319,43 @@ mhdp_status build_patches(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
     if ((st = upload(ctx, &P.wd, wd.data(), H.n))) return st;
     if ((st = dalloc(ctx, &P.y, sum_n))) return st;
     L.bytes_fac = 8 * f + 4 * np + 16 * np + 12 * sum_n;
+    return MHDP_OK;
+}
+
+// small stars: group the patches 32 at a time by size and interleave their factor streams
+// (K2 thread-per-patch kernel; MHDP_K2_LANES=0 disables it for A/B timing)
+mhdp_status build_lane_groups(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
+    DevPatches &P = L.P;
+    const char *e = getenv("MHDP_K2_LANES");
+    if (P.max_n > K2L_MAX || (e && e[0] == '0') || P.np == 0) return MHDP_OK;
+    const int64_t np = P.np;
+    std::vector<int64_t> order(np);
+    std::iota(order.begin(), order.end(), 0);
+    auto sz = [&](int64_t i) { return (int)(H.pptr[i + 1] - H.pptr[i]); };
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return sz(a) < sz(b); });
+    std::vector<int> gn, gpatch;
+    std::vector<int64_t> gbase;
+    int64_t tot = 0;
+    for (int64_t k = 0; k < np;) {
+        const int n = sz(order[k]);
+        int64_t k1 = k;
+        while (k1 < np && k1 - k < 32 && sz(order[k1]) == n) ++k1;
+        gn.push_back(n);
+        gbase.push_back(tot);
+        for (int t = 0; t < 32; ++t) gpatch.push_back(k + t < k1 ? (int)order[k + t] : -1);
+        tot += 32 * ((int64_t)n * n + n);
+        k = k1;
+    }
+    P.ng = (int64_t)gn.size();
+    mhdp_status st;
+    if ((st = upload(ctx, &P.gn, gn.data(), P.ng))) return st;
+    if ((st = upload(ctx, &P.gbase, gbase.data(), P.ng))) return st;
+    if ((st = upload(ctx, &P.gpatch, gpatch.data(), 32 * P.ng))) return st;
+    if ((st = dalloc(ctx, &P.facI, tot))) return st;
+    launch_interleave(P, ctx->stream);
+    if ((st = check_launch(ctx))) return st;
+    CK(cudaStreamSynchronize(ctx->stream));
+    L.bytes_fac += 8 * tot;
     return MHDP_OK;
 }
 
@@ -640,6 +678,7 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
             snprintf(buf, sizeof buf, "singular patch %lld on level %d", patch, l);
             return fail(ctx, MHDP_ESINGULAR, buf, ((long long)l << 32) + patch);
         }
+        if ((st = build_lane_groups(ctx, H, L))) return st;
     }
     // K7: coarse LU (dense, row-major), then K8 setup: X = A_0^-1 from the factors
     const HostLevel &H0 = ctx->H[0];
