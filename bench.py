@@ -38,6 +38,16 @@ sys.path.insert(0, ROOT)
 REF_SAMPLE = ("c5", 12, 3)
 
 
+def k2_traffic():
+    """DRAM bytes per K2 launch from the committed `ncu --set full` capture (profiles/), or None."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "k2_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -402,6 +412,7 @@ def run_ours(args):
     pk = peaks()
     peak = pk["hbm_gbs"] if pk else 6650.0
     k2_gbs = k2_bytes / (ms_k2 * 1e-3) / 1e9
+    tr = k2_traffic()
 
     # ---- e2e: host buffers through the C-ABI (H2D b, V-cycle, D2H x), pinned memory ----
     bh = torch.from_numpy(b).pin_memory()
@@ -440,7 +451,10 @@ def run_ours(args):
                         "coarse_n": n0, "sweep_ms_per_level": level_sweep_ms},
             "roofline": {"bound": "hbm", "kernel": "K2 patch gather + LU apply (finest level)",
                          "achieved": k2_gbs, "peak": peak, "unit": "GB/s", "frac": k2_gbs / peak,
-                         "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback"},
+                         "traffic": (tr["traffic_bytes_per_launch"] if tr else None),
+                         "traffic_source": (tr["source"] if tr else None),
+                         "algorithmic_bytes": k2_bytes,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback"},
             "e2e": {"value": ws * smoothed / (e2e_ms * 1e-3), "unit": "DoF/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
             "gpu_launches": launches,
