@@ -255,6 +255,36 @@ def run_variants(cfg, seed, dev, stream):
         "K2_ms": ms_k2, "K2_gbs": k2_bytes / (ms_k2 * 1e-3) / 1e9,
         "fgmres_gmres6_vcycle": {"its": its2, "converged": conv2, "relres": rel2, "ms": ms_f}}
     ctx.close()
+    # NEXT-2: k = 2 (BDM2) 2D AL velocity block, c3 parameters (Re = gamma = 1e4), sigma = 10 k^2
+    cfgv = dataclasses.replace(workloads.CONFIGS["c3"], N=256, levels=6, degree=2, sigma=40.0)
+    ctx = mhdp.Context(dev.index, stream.cuda_stream)
+    wv, _, _ = workloads.draw(cfgv, 1, seed)
+    t0 = time.perf_counter()
+    ctx.assemble(cfgv, wv)
+    t_asm = time.perf_counter() - t0
+    wv, bv, xv = workloads.draw(cfgv, ctx.n(), seed)
+    ctx.setup()
+    Lv = ctx.num_levels()
+    fin = ctx.info(Lv - 1)
+    bd = torch.from_numpy(bv).to(dev)
+    xd = torch.from_numpy(xv).to(dev)
+    ctx.vcycle(bd, xd)
+    ms_v, _ = _timed(stream, lambda: ctx.vcycle(bd, xd), reps=10)
+    rd = torch.empty_like(bd)
+    ctx.residual(bd, xd, rd)
+    ms_k2, _ = _timed(stream, lambda: ctx.patch_apply(rd), reps=10)
+    ms_sw, _ = _timed(stream, lambda: ctx.smooth(bd, xd, nsweeps=1), reps=10)
+    ctx.set_smoother("gmres", 6)
+    ms_f, (itsv, relv, convv) = _timed(stream, lambda: ctx.fgmres(bd, xd, maxit=60))
+    smoothed = sum(2 * cfgv.nu * ctx.info(l)["n"] for l in range(1, Lv))
+    out["next2_k2_vel2d"] = {
+        "config": "2D AL velocity block, BDM2 (k = 2), 256^2 x 2 cells, 6 levels, V(2,2), Re = gamma = 1e4, sigma = 40",
+        "finest_dofs": fin["n"], "patches": fin["npatch"], "max_patch": fin["max_n"], "sum_n2": fin["sum_n2"],
+        "host_assembly_s": t_asm, "vcycle_ms": ms_v, "smoothed_dofs_per_s": smoothed / (ms_v * 1e-3),
+        "sweep_ms": ms_sw, "K2_ms": ms_k2,
+        "K2_gbs": (8 * fin["sum_n2"] + 16 * fin["sum_n"]) / (ms_k2 * 1e-3) / 1e9,
+        "fgmres_gmres6_vcycle": {"its": itsv, "converged": convv, "relres": relv, "ms": ms_f}}
+    ctx.close()
     return out
 
 
