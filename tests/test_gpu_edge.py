@@ -192,3 +192,24 @@ def test_vcycle_graph_replay_bitexact(oracle_mod, smoother):
         ctx.vcycle(bd, xg)
         assert np.array_equal(bits(host(xg)), ref), f"call {call}"
     assert ctx.graphs_active() >= 1
+
+
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_k2_single_level_vcycle_is_coarse_solve(oracle_mod, name):
+    """NEXT-2 degenerate hierarchy: one level at k = 2 -- the V-cycle is the coarse solve
+    (explicit inverse, R-coarse), bit-exact against the oracle's exact build."""
+    import dataclasses
+    import torch
+    from paper_2104_14855_b200 import mhdp, workloads
+    cfg = dataclasses.replace(workloads.small(name, 4, 1), degree=2,
+                              sigma=40.0 if name == "c3" else 10.0)
+    w, _, _ = workloads.draw(cfg, 1, 3)
+    ctx = mhdp.Context(0, torch.cuda.current_stream().cuda_stream)
+    ctx.assemble(cfg, w)
+    ctx.setup()
+    n = ctx.n()
+    b = np.random.default_rng(3).uniform(-1, 1, n)
+    orc = oracle_mod.Oracle(cfg, w, exact=True)
+    x = torch.empty(n, dtype=torch.float64, device="cuda:0")
+    ctx.vcycle(torch.from_numpy(b).cuda(), x)
+    assert np.array_equal(x.cpu().numpy().view(np.uint64), orc.vcycle(b).view(np.uint64))
