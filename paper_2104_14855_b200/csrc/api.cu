@@ -327,11 +327,9 @@ mhdp_status build_patches(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
 mhdp_status build_lane_groups(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
     DevPatches &P = L.P;
     const char *e = getenv("MHDP_K2_LANES");
-    // measured (tools/level_profile.py, profiles/r01_k2_lanes_ab.jsonl): the thread-per-patch
-    // kernel beats the warp kernels only when the level fills the GPU with resident warps
-    // (each thread's substitution is a ~n^2-step chain) and n <= 32 (registers): 2D k = 2
-    // E-B at 263k / 66k stars 3.2 vs 2.3-2.5 TB/s; slower on small levels and for n = 36
-    if (P.max_n > 32 || P.np < 40000 || (e && e[0] == '0')) return MHDP_OK;
+    if ((e && e[0] == '0') || P.np == 0) return MHDP_OK;
+    for (int64_t i = 0; i < P.np; ++i)
+        if (!lring_size_supported((int)(H.pptr[i + 1] - H.pptr[i]))) return MHDP_OK;
     const int64_t np = P.np;
     std::vector<int64_t> order(np);
     std::iota(order.begin(), order.end(), 0);

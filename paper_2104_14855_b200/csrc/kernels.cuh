@@ -51,7 +51,8 @@ struct DevPatches {
     int *dslot = nullptr;      // sum_n slots of each DoF, ascending patch order
     double *wd = nullptr;      // n    theta * (1/m_d)
     double *y = nullptr;       // sum_n slot buffer
-    // small stars (max_n <= K2L_MAX): thread-per-patch K2 on lane-interleaved factors.
+    // small stars (every patch size in LR_SIZES): thread-per-patch K2 on lane-interleaved
+    // factors streamed through TMA rings.
     // Patches grouped 32 at a time by size; element e of lane l of group g at
     // facI[gbase[g] + 32 e + l]; gpatch[32 g + l] = patch or -1 (padding, zero factors).
     int64_t ng = 0;
@@ -60,7 +61,8 @@ struct DevPatches {
     int *gpatch = nullptr;     // 32 ng
     double *facI = nullptr;
 };
-static constexpr int K2L_MAX = 40;
+// the patch sizes the small-star K2 kernel is instantiated for (2D k = 1 and k = 2 stars)
+bool lring_size_supported(int n);
 // copy the packed factors into the lane-interleaved layout (setup)
 void launch_interleave(const DevPatches &P, cudaStream_t s);
 
