@@ -327,7 +327,12 @@ mhdp_status build_patches(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
 mhdp_status build_lane_groups(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
     DevPatches &P = L.P;
     const char *e = getenv("MHDP_K2_LANES");
+    // measured (tools/level_profile.py, profiles/r01_k2_lring_ab.jsonl): the ring-fed
+    // thread-per-patch kernel wins wherever the level has enough 32-patch groups to keep
+    // every warp busy (a group of 31/36-DoF stars is a ~40-50 us chain per thread), or
+    // the stars are small: k = 2 E-B finest 5.7 vs 2.8 TB/s, c3 finest 4.6 vs 2.0 TB/s
     if ((e && e[0] == '0') || P.np == 0) return MHDP_OK;
+    if (!(P.max_n <= 16 || P.np >= 40000)) return MHDP_OK;
     for (int64_t i = 0; i < P.np; ++i)
         if (!lring_size_supported((int)(H.pptr[i + 1] - H.pptr[i]))) return MHDP_OK;
     const int64_t np = P.np;
