@@ -223,19 +223,27 @@ mhdp_status build_b3(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
         sptr[s + 1] = sptr[s] + 32 * (int64_t)mx;
     }
     const int64_t stored = sptr[ns];
+    // value layout: the 9 x 32 values of one (slice, block column) contiguous (one DRAM run
+    // per warp iteration), or 9 separate planes (MHDP_K1_PLANES=1, A/B)
+    const char *pe = getenv("MHDP_K1_PLANES");
+    const int planes = pe && pe[0] == '1';
     std::vector<int> col(stored, 0);
     std::vector<double> val(9 * stored, 0.0);
     for (int64_t R = 0; R < nb; ++R) {
-        const int64_t base = sptr[R >> 5] + (R & 31);
+        const int64_t s0 = sptr[R >> 5], base = s0 + (R & 31);
         for (int k = 0; k < rlen[R]; ++k) {
             const int64_t e = base + 32 * (int64_t)k;
             col[e] = H.ci[H.rp[3 * R] + 3 * k] / 3;
             for (int a = 0; a < 3; ++a)
-                for (int b = 0; b < 3; ++b) val[(3 * a + b) * stored + e] = H.v[H.rp[3 * R + a] + 3 * k + b];
+                for (int b = 0; b < 3; ++b) {
+                    const int m = 3 * a + b;
+                    const int64_t at = planes ? m * stored + e : 9 * s0 + (9 * (int64_t)k + m) * 32 + (R & 31);
+                    val[at] = H.v[H.rp[3 * R + a] + 3 * k + b];
+                }
         }
     }
     mhdp_status st;
-    L.A3.nb = nb; L.A3.nslices = ns; L.A3.stored = stored;
+    L.A3.nb = nb; L.A3.nslices = ns; L.A3.stored = stored; L.A3.planes = planes;
     if ((st = upload(ctx, &L.A3.sptr, sptr.data(), ns + 1))) return st;
     if ((st = upload(ctx, &L.A3.rlen, rlen.data(), nb))) return st;
     if ((st = upload(ctx, &L.A3.col, col.data(), stored))) return st;

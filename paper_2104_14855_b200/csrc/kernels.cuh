@@ -27,7 +27,10 @@ struct DevBSell3 {
     int64_t *sptr = nullptr;
     int *rlen = nullptr;       // per block row
     int *col = nullptr;        // block column index
-    double *val = nullptr;     // 9 planes of `stored` doubles
+    double *val = nullptr;     // planes == 1: 9 planes of `stored` doubles; planes == 0 (default):
+                               // per slice s and block column k the 9 x 32 values contiguous,
+                               // entry m of lane l at val[9 sptr[s] + (9 k + m) 32 + l]
+    int planes = 0;
 };
 
 struct DevCsr {
