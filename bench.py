@@ -55,73 +55,91 @@ def peaks():
         return None
 
 
-class ClockSampler:
-    """SM clocks and clock-event (throttle) reasons sampled during the timed region: NVML
-    every 5 ms (pynvml), else nvidia-smi every 200 ms."""
+_SAMPLER_SRC = r"""
+import sys, time, json
+idx, out = int(sys.argv[1]), sys.argv[2]
+names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+         0x80: "hw_power_brake_slowdown"}
+rows = []
+try:
+    import pynvml as nv
+    nv.nvmlInit()
+    h = nv.nvmlDeviceGetHandleByIndex(idx)
+    mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+    src = "nvml"
+    def sample():
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        return [nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx, [v for k, v in names.items() if bits & k]]
+except Exception:
+    import subprocess
+    src = "nvidia-smi"
+    q = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+        "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+    nm = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    def sample():
+        p = subprocess.run(["nvidia-smi", "-i", str(idx), "--query-gpu=" + q, "--format=csv,noheader,nounits"],
+                           capture_output=True, text=True, timeout=5).stdout.strip().split(",")
+        p = [x.strip() for x in p]
+        return [float(p[0]), float(p[1]), [nm[i] for i in range(4) if p[2 + i] == "Active"]]
+sys.stdout.write("ready\n"); sys.stdout.flush()
+while True:
+    try:
+        rows.append(sample())
+    except Exception:
+        pass
+    if sys.stdin in __import__("select").select([sys.stdin], [], [], 0.005 if src == "nvml" else 0.2)[0]:
+        break
+json.dump({"source": src, "rows": rows}, open(out, "w"))
+"""
 
-    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
-               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+class ClockSampler:
+    """SM clocks and clock-event (throttle) reasons sampled during the timed region by a
+    separate process (no GIL contention with the timed loop): NVML every 5 ms, else
+    nvidia-smi every 200 ms."""
 
     def __init__(self, index=0):
         self.index = index
-        self.samples = []          # (sm_mhz, max_mhz, reason names)
-        self._stop = threading.Event()
-        self._t = None
-        self.source = "nvidia-smi"
-
-    def _run_nvml(self, nv):
-        h = nv.nvmlDeviceGetHandleByIndex(self.index)
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        while not self._stop.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((float(sm), float(mx), [v for k, v in self.REASONS.items() if bits & k]))
-            except Exception:
-                pass
-            self._stop.wait(0.005)
-
-    def _run_smi(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    p = [x.strip() for x in out.split(",")]
-                    self.samples.append((float(p[0]), float(p[1]), [names[i] for i in range(4) if p[2 + i] == "Active"]))
-            except Exception:
-                pass
-            self._stop.wait(0.2)
-
-    def _run(self):
-        try:
-            import pynvml as nv
-            nv.nvmlInit()
-            self.source = "nvml"
-            self._run_nvml(nv)
-        except Exception:
-            self.source = "nvidia-smi"
-            self._run_smi()
+        self.samples = []
+        self.source = None
+        self._p = None
+        self._out = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
-        time.sleep(0.02)           # first sample before the timed region starts
+        import tempfile
+        fd, self._out = tempfile.mkstemp(suffix=".json")
+        os.close(fd)
+        try:
+            self._p = subprocess.Popen([sys.executable, "-c", _SAMPLER_SRC, str(self.index), self._out],
+                                       stdin=subprocess.PIPE, stdout=subprocess.PIPE, text=True)
+            self._p.stdout.readline()          # sampler initialised
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is None:
+            return
+        try:
+            self._p.stdin.write("stop\n")
+            self._p.stdin.flush()
+            self._p.wait(timeout=20)
+            with open(self._out) as f:
+                d = json.load(f)
+            self.samples, self.source = d["rows"], d["source"]
+        except Exception:
+            pass
+        finally:
+            try:
+                os.unlink(self._out)
+            except OSError:
+                pass
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [x[0] for x in self.samples]
-        return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": min(sm), "sm_max_mhz": max(x[1] for x in self.samples),
+        sm = [float(x[0]) for x in self.samples]
+        return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": min(sm), "sm_max_mhz": max(float(x[1]) for x in self.samples),
                 "reasons": sorted({r for x in self.samples for r in x[2]}), "samples": len(self.samples),
                 "source": self.source}
 
