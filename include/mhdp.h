@@ -220,8 +220,14 @@ long long   mhdp_launch_count(const mhdp_ctx *ctx);
  * numbering) on the finest mesh: [[F+D, B^T, J, J~+D~1+D~2], [B, 0, 0, 0],
  * [G, 0, M_E, G~ - A/Rem], [0, 0, A^T, C]] with u^n = the advecting field, B^n given by
  * its potential (bn_vertex_host, may be NULL: B^n = 0) and E^n = 0 (so J~ = 0; reading
- * R-coupled).  The object owns both multigrid hierarchies (velocity and E-B).
- * cuda_device = -1: host-only (assembly and export).                                    */
+ * R-coupled).  The object owns both multigrid hierarchies (velocity and E-B) and every
+ * device store; the caller owns the device vectors it passes (fp64, length n_u + n_p +
+ * n_E + n_B, on the object's device), calls are ordered on cuda_stream.
+ * cuda_device = -1: host-only (assembly and export; device calls return MHDP_ECUDA).
+ * Errors: MHDP_EINVAL for bad arguments or params->degree = 2 (the k = 2 coupling blocks
+ * are not built); the failing stage's status otherwise (ESINGULAR for a singular patch or
+ * coarse operator).  *out is set whenever memory was allocated -- destroy it also on
+ * failure; mhdp_coupled_last_error returns the message.                               */
 typedef struct mhdp_coupled mhdp_coupled;
 mhdp_status mhdp_coupled_create(mhdp_coupled **out, int cuda_device, void *cuda_stream,
                                 const mhdp_mesh *mesh, const mhdp_params *params,
@@ -236,7 +242,10 @@ mhdp_status mhdp_coupled_apply(mhdp_coupled *c, const double *x_dev, double *y_d
  * on the E-B block with its V-cycle, z_u = r_u - K y_EB, two FGMRES iterations on the
  * (u,p) block preconditioned by y_p = -(1/Re+gamma) M_p^-1 s_p, y_u = V_u(s_u - B^T y_p) */
 mhdp_status mhdp_coupled_precondition(mhdp_coupled *c, const double *r_dev, double *y_dev);
-/* outermost flexible GMRES with P, x0 = 0, stop at max(rtol|b|, atol)   */
+/* outermost flexible GMRES with P, x0 = 0, stop at max(rtol|b|, atol);
+ * 1 <= maxit <= 500; MHDP_ENOCONV when maxit is reached (x_dev holds that iterate).
+ * The pressure is determined up to a constant (Q = L^2_0): b must have
+ * mean-zero pressure rows for the system to be consistent.                              */
 mhdp_status mhdp_coupled_fgmres(mhdp_coupled *c, const double *b_dev, double *x_dev, double rtol,
                                 double atol, int maxit, int *its_out, double *relres_out);
 mhdp_status mhdp_coupled_set_smoother(mhdp_coupled *c, int smoother, int smoother_its);
