@@ -1338,6 +1338,7 @@ mhdp_status mhdp_coupled_create(mhdp_coupled **out, int cuda_device, void *cuda_
                                 const mhdp_params *params, const double *w_vertex_host,
                                 const double *bn_vertex_host) {
     if (!out || !mesh || !params || !w_vertex_host) return MHDP_EINVAL;
+    if (params->degree > 1) return MHDP_EINVAL;   // the k = 2 coupling blocks are not built
     *out = nullptr;
     mhdp_coupled *c = new (std::nothrow) mhdp_coupled();
     if (!c) return MHDP_ENOMEM;

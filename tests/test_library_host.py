@@ -216,3 +216,13 @@ def test_k2_rejected_in_3d(mh):
         ctx = mh.Context(-1)
         with pytest.raises(mh.MhdpError):
             ctx.assemble(cfg, w)
+
+
+def test_coupled_rejects_degree_2(mh):
+    """NEXT-3 is built at k = 1 only: a k = 2 coupled system is refused (include/mhdp.h)."""
+    import dataclasses
+    from paper_2104_14855_b200 import workloads
+    cfg = dataclasses.replace(workloads.small("c3", 4, 1), degree=2, sigma=40.0)
+    w, _, _ = workloads.draw(cfg, 1, 0)
+    with pytest.raises(mh.MhdpError):
+        mh.Coupled(cfg, w, None, device=-1)
