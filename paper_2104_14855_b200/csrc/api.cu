@@ -318,6 +318,17 @@ mhdp_status build_patches(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
     if ((st = upload(ctx, &P.pn, pn.data(), np))) return st;
     if ((st = upload(ctx, &P.poff, H.pptr.data(), np))) return st;
     if ((st = upload(ctx, &P.foff, foff.data(), np))) return st;
+    {   // walk order of the persistent K2 kernels: size descending, stable
+        std::vector<int64_t> ord(np);
+        std::iota(ord.begin(), ord.end(), 0);
+        std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return pn[a] > pn[b]; });
+        std::vector<int> pno(np);
+        std::vector<int64_t> poo(np), foo(np);
+        for (int64_t k = 0; k < np; ++k) { pno[k] = pn[ord[k]]; poo[k] = H.pptr[ord[k]]; foo[k] = foff[ord[k]]; }
+        if ((st = upload(ctx, &P.pn_o, pno.data(), np))) return st;
+        if ((st = upload(ctx, &P.poff_o, poo.data(), np))) return st;
+        if ((st = upload(ctx, &P.foff_o, foo.data(), np))) return st;
+    }
     if ((st = upload(ctx, &P.pdofs, H.pdofs.data(), sum_n))) return st;
     if ((st = dalloc(ctx, &P.gidx, sum_n))) return st;
     if ((st = dalloc(ctx, &P.perm, sum_n))) return st;

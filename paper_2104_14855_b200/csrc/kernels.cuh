@@ -46,6 +46,11 @@ struct DevPatches {
     int *pn = nullptr;         // np   patch sizes
     int64_t *poff = nullptr;   // np   slot offset (= pptr[i])
     int64_t *foff = nullptr;   // np   factor offset in doubles (16-double aligned)
+    // the same three arrays with the patches in size-descending (stable) order: the order in
+    // which the persistent warp kernels walk them (patches are independent; the last,
+    // partial round of the round-robin gets the smallest stars -- load balance)
+    int *pn_o = nullptr;
+    int64_t *poff_o = nullptr, *foff_o = nullptr;
     int *pdofs = nullptr;      // sum_n ascending DoFs of each patch
     int *gidx = nullptr;       // sum_n pivot-folded gather list  gidx[k] = pdofs[perm[k]]
     int *perm = nullptr;       // sum_n LU row permutation (export only)
