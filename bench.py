@@ -194,16 +194,32 @@ def oracle_vcycle_sample(steps, warmup, seed=0):
                       f"patch and operator structure as the full c5), setup excluded, {steps} cycles"}
 
 
+METRIC = "smoothed DoFs/s (V(2,2) cycle); achieved HBM GB/s vs peak; V-cycle ms"
+
+
+def workload_config(cfg, L=None, fin=None, ws=1):
+    """The `config` object of both arms (BASELINE.json's metric is quoted on c5)."""
+    c = {"workload": f"{cfg.name}: 3D AL velocity block, BDM1, {cfg.N}^3 x 6 tets, {L or cfg.levels} levels, "
+                     f"V({cfg.nu},{cfg.nu}), Re=gamma=1e4",
+         "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+         "l2": "working set per step >> L2 (9.9 GB of patch factors streamed per sweep)"}
+    if fin is not None:
+        c.update({"finest_dofs": fin["n"], "nnz": fin["nnz"], "patches": fin["npatch"], "sum_n2": fin["sum_n2"]})
+    return c
+
+
 def run_reference(args):
     ws, rank, _ = dist_init()
     if rank != 0:
         return
+    from paper_2104_14855_b200 import workloads
     r = oracle_vcycle_sample(args.steps, args.warmup)
-    line = {"impl": "reference", "metric": "smoothed DoFs/s (V(2,2) cycle)", "value": r["value"],
+    cfg = dict(workload_config(workloads.CONFIGS[args.config]), sample=r["sample"])
+    line = {"impl": "reference", "metric": METRIC, "value": r["value"],
             "unit": "DoF/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "c5-sample (oracle on the host)", "sample": r["sample"]},
+            "config": cfg,
             "cpu_baseline": {"value": r["value"], "unit": "DoF/s", "cores": 1, "kind": "oracle", "sample": r["sample"]},
             "e2e": {"value": r["value"], "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -508,15 +524,11 @@ def run_ours(args):
     if rank == 0:
         value = ws * smoothed / (ms * 1e-3)
         line = {
-            "metric": "smoothed DoFs/s (V(2,2) cycle); achieved HBM GB/s vs peak; V-cycle ms",
+            "metric": METRIC,
             "value": value, "unit": "DoF/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: 3D AL velocity block, BDM1, {cfg.N}^3 x 6 tets, {L} levels, "
-                                   f"V({cfg.nu},{cfg.nu}), Re=gamma=1e4", "finest_dofs": fin["n"],
-                       "nnz": fin["nnz"], "patches": fin["npatch"], "sum_n2": fin["sum_n2"],
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-                       "l2": "working set per step >> L2 (9.9 GB of patch factors streamed per sweep)"},
+            "config": workload_config(cfg, L, fin, ws),
             "vcycle_ms": ms,
             "sweep": {"ms": ms_sweep, "dofs_per_s": fin["n"] / (ms_sweep * 1e-3),
                       "gbs": sweep_bytes / (ms_sweep * 1e-3) / 1e9,
