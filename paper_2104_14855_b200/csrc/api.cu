@@ -97,6 +97,13 @@ mhdp_status fail(mhdp_ctx *c, mhdp_status st, const std::string &msg, long long 
     return st;
 }
 
+// scoped temporary device buffer (freed on every return path of the setup stages)
+template <class T>
+struct TmpDev {
+    T *p = nullptr;
+    ~TmpDev() { if (p) cudaFree(p); }
+};
+
 #define CK(call)                                                                              \
     do {                                                                                      \
         cudaError_t e_ = (call);                                                              \
@@ -683,10 +690,15 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         if ((st = build_csr(ctx, H.n_coarser, trp, tci, tv, L.PrT))) return st;
         L.bytes_tr = 2 * (12 * (int64_t)H.prp[H.n]) + 4 * (H.n + H.n_coarser + 2);
         // K6: batched patch LU from a temporary device CSR
-        int64_t *drp = nullptr; int *dci = nullptr; double *dv = nullptr;
-        CK(cudaMalloc(&drp, sizeof(int64_t) * (H.n + 1)));
-        CK(cudaMalloc(&dci, sizeof(int) * std::max<int64_t>(1, L.nnz)));
-        CK(cudaMalloc(&dv, sizeof(double) * std::max<int64_t>(1, L.nnz)));
+        TmpDev<int64_t> trp;
+        TmpDev<int> tci;
+        TmpDev<double> tv;
+        CK(cudaMalloc(&trp.p, sizeof(int64_t) * (H.n + 1)));
+        CK(cudaMalloc(&tci.p, sizeof(int) * std::max<int64_t>(1, L.nnz)));
+        CK(cudaMalloc(&tv.p, sizeof(double) * std::max<int64_t>(1, L.nnz)));
+        int64_t *drp = trp.p;
+        int *dci = tci.p;
+        double *dv = tv.p;
         CK(cudaMemcpy(drp, H.rp.data(), sizeof(int64_t) * (H.n + 1), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(dci, H.ci.data(), sizeof(int) * L.nnz, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(dv, H.v.data(), sizeof(double) * L.nnz, cudaMemcpyHostToDevice));
@@ -695,7 +707,6 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         launch_patch_lu(L.P, drp, dci, dv, ctx->d_status, ctx->stream);
         if ((st = check_launch(ctx))) return st;
         CK(cudaStreamSynchronize(ctx->stream));
-        cudaFree(drp); cudaFree(dci); cudaFree(dv);
         int bad = 0;
         CK(cudaMemcpy(&bad, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost));
         if (bad != INT_MAX) {
@@ -715,8 +726,9 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         std::vector<double> dense((size_t)(n0 * n0), 0.0);
         for (int64_t i = 0; i < n0; ++i)
             for (int64_t t = H0.rp[i]; t < H0.rp[i + 1]; ++t) dense[(size_t)(i * n0 + H0.ci[t])] = H0.v[t];
-        double *a = nullptr;
-        CK(cudaMalloc(&a, sizeof(double) * std::max<int64_t>(1, n0 * n0)));
+        TmpDev<double> ta;
+        CK(cudaMalloc(&ta.p, sizeof(double) * std::max<int64_t>(1, n0 * n0)));
+        double *a = ta.p;
         CK(cudaMemcpy(a, dense.data(), sizeof(double) * n0 * n0, cudaMemcpyHostToDevice));
         if ((st = dalloc(ctx, &ctx->cperm, n0))) return st;
         if ((st = dalloc(ctx, &ctx->cinv, n0 * n0))) return st;
@@ -727,11 +739,10 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         CK(cudaStreamSynchronize(ctx->stream));
         int bad = 0;
         CK(cudaMemcpy(&bad, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost));
-        if (bad) { cudaFree(a); return fail(ctx, MHDP_ESINGULAR, "singular coarse operator", -1); }
+        if (bad) return fail(ctx, MHDP_ESINGULAR, "singular coarse operator", -1);
         launch_coarse_inverse(a, ctx->cperm, (int)n0, ctx->cinv, ctx->stream);
-        if ((st = check_launch(ctx))) { cudaFree(a); return st; }
+        if ((st = check_launch(ctx))) return st;
         CK(cudaStreamSynchronize(ctx->stream));
-        cudaFree(a);
     }
     ctx->setup_done = true;
     return MHDP_OK;
