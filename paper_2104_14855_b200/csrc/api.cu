@@ -690,15 +690,15 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         if ((st = build_csr(ctx, H.n_coarser, trp, tci, tv, L.PrT))) return st;
         L.bytes_tr = 2 * (12 * (int64_t)H.prp[H.n]) + 4 * (H.n + H.n_coarser + 2);
         // K6: batched patch LU from a temporary device CSR
-        TmpDev<int64_t> trp;
-        TmpDev<int> tci;
-        TmpDev<double> tv;
-        CK(cudaMalloc(&trp.p, sizeof(int64_t) * (H.n + 1)));
-        CK(cudaMalloc(&tci.p, sizeof(int) * std::max<int64_t>(1, L.nnz)));
-        CK(cudaMalloc(&tv.p, sizeof(double) * std::max<int64_t>(1, L.nnz)));
-        int64_t *drp = trp.p;
-        int *dci = tci.p;
-        double *dv = tv.p;
+        TmpDev<int64_t> buf_rp;
+        TmpDev<int> buf_ci;
+        TmpDev<double> buf_v;
+        CK(cudaMalloc(&buf_rp.p, sizeof(int64_t) * (H.n + 1)));
+        CK(cudaMalloc(&buf_ci.p, sizeof(int) * std::max<int64_t>(1, L.nnz)));
+        CK(cudaMalloc(&buf_v.p, sizeof(double) * std::max<int64_t>(1, L.nnz)));
+        int64_t *drp = buf_rp.p;
+        int *dci = buf_ci.p;
+        double *dv = buf_v.p;
         CK(cudaMemcpy(drp, H.rp.data(), sizeof(int64_t) * (H.n + 1), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(dci, H.ci.data(), sizeof(int) * L.nnz, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(dv, H.v.data(), sizeof(double) * L.nnz, cudaMemcpyHostToDevice));
@@ -726,9 +726,9 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         std::vector<double> dense((size_t)(n0 * n0), 0.0);
         for (int64_t i = 0; i < n0; ++i)
             for (int64_t t = H0.rp[i]; t < H0.rp[i + 1]; ++t) dense[(size_t)(i * n0 + H0.ci[t])] = H0.v[t];
-        TmpDev<double> ta;
-        CK(cudaMalloc(&ta.p, sizeof(double) * std::max<int64_t>(1, n0 * n0)));
-        double *a = ta.p;
+        TmpDev<double> buf_a;
+        CK(cudaMalloc(&buf_a.p, sizeof(double) * std::max<int64_t>(1, n0 * n0)));
+        double *a = buf_a.p;
         CK(cudaMemcpy(a, dense.data(), sizeof(double) * n0 * n0, cudaMemcpyHostToDevice));
         if ((st = dalloc(ctx, &ctx->cperm, n0))) return st;
         if ((st = dalloc(ctx, &ctx->cinv, n0 * n0))) return st;
