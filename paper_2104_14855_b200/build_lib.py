@@ -20,9 +20,9 @@ LIB = os.path.join(PKG, "libmhdp.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU = ["kernels.cu", "api.cu"]
+CU = ["kernels.cu", "k2_small.cu", "api.cu"]
 CPP = ["fe_setup.cpp"]
-HEADERS = ["kernels.cuh", "setup.hpp"]
+HEADERS = ["kernels.cuh", "k2_common.cuh", "setup.hpp"]
 
 
 def _stale(target, deps):

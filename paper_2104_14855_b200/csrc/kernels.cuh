@@ -73,6 +73,8 @@ struct DevPatches {
 bool lring_size_supported(int n);
 // copy the packed factors into the lane-interleaved layout (setup)
 void launch_interleave(const DevPatches &P, cudaStream_t s);
+// K2 on the lane-interleaved factors (k2_small.cu)
+void apply_lring(const DevPatches &P, const double *r, cudaStream_t s);
 
 // counts every launch made through these wrappers (bench "gpu_launches")
 extern long long g_launches;
