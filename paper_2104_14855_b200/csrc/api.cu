@@ -302,7 +302,7 @@ mhdp_status build_patches(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
         foff[i] = f;
         f += ((int64_t)pn[i] * pn[i] + pn[i] + 15) / 16 * 16;   // packed stream n^2+n, 128-byte aligned
     }
-    if (mx > 160) return fail(ctx, MHDP_EINVAL, "patch larger than 160 DoFs is not supported");
+    if (mx > K2_MAX_N) return fail(ctx, MHDP_EINVAL, "patch larger than 384 DoFs is not supported");
     P.max_n = mx;
     P.fac_doubles = f;
     std::vector<int> mult(H.n, 0);
@@ -704,7 +704,10 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         CK(cudaMemcpy(dv, H.v.data(), sizeof(double) * L.nnz, cudaMemcpyHostToDevice));
         int big = INT_MAX;
         CK(cudaMemcpy(ctx->d_status, &big, sizeof(int), cudaMemcpyHostToDevice));
-        launch_patch_lu(L.P, drp, dci, dv, ctx->d_status, ctx->stream);
+        TmpDev<double> buf_lu;            // K6 scratch for stars beyond shared memory
+        const int64_t nscr = patch_lu_scratch_doubles(L.P);
+        if (nscr) CK(cudaMalloc(&buf_lu.p, sizeof(double) * nscr));
+        launch_patch_lu(L.P, drp, dci, dv, ctx->d_status, buf_lu.p, ctx->stream);
         if ((st = check_launch(ctx))) return st;
         CK(cudaStreamSynchronize(ctx->stream));
         int bad = 0;

@@ -40,6 +40,11 @@ struct DevCsr {
     double *v = nullptr;
 };
 
+// star sizes: K6 keeps the patch matrix in shared memory up to K6_SMEM_MAX DoFs, in a
+// global scratch above; K2 and K6 support stars up to K2_MAX_N DoFs (3D k = 2 sizes)
+static constexpr int K6_SMEM_MAX = 160;
+static constexpr int K2_MAX_N = 384;
+
 struct DevPatches {
     int64_t np = 0, sum_n = 0, fac_doubles = 0;
     int max_n = 0;
@@ -84,8 +89,9 @@ void launch_residual(const DevSell &A, const double *b, const double *x, double 
 void launch_residual_b3(const DevBSell3 &A, const double *b, const double *x, double *r, cudaStream_t s);
 // K6: batched patch LU (gather from the CSR on the device, partial pivoting)
 // rowptr (int64) / col / val: the level operator in CSR; status[0] = first singular patch+1
-void launch_patch_lu(const DevPatches &P, const int64_t *rowptr, const int *col, const double *val,
-                     int *status, cudaStream_t s);
+int64_t patch_lu_scratch_doubles(const DevPatches &P);
+void launch_patch_lu(const DevPatches &P, const int64_t *rowptr, const int *col, const double *val, int *status,
+                     double *scratch, cudaStream_t s);
 // K2: y_i = A_i^-1 R_i r for every patch
 void launch_patch_apply(const DevPatches &P, const double *r, cudaStream_t s);
 // K3: x_d <- fma(w_d, sum y, x_d)    (x_is_zero: x_d <- fma(w_d, sum y, 0.0))

@@ -134,3 +134,45 @@ def test_gmres_iterations(pair):
         A = orc.csr().to_scipy()
         r = b - A @ host(xg)
         assert np.linalg.norm(r) <= 1.01 * max(1e-7 * np.linalg.norm(b), 1e-7)
+
+
+def _union_patches(orc, N, level, block):
+    """unions of the vertex stars of level `level` over blocks of lattice vertices"""
+    ptr, dofs, verts, _ = orc.patches(level)
+    lat = np.stack([verts % (N + 1), (verts // (N + 1)) % (N + 1), verts // (N + 1) ** 2], axis=1)
+    key = (lat[:, 0] // block[0]) + 1000 * (lat[:, 1] // block[1]) + 1000000 * (lat[:, 2] // block[2])
+    out = [np.unique(np.concatenate([dofs[ptr[i]:ptr[i + 1]] for i in np.flatnonzero(key == k)]))
+           for k in np.unique(key)]
+    nptr = np.concatenate([[0], np.cumsum([len(p) for p in out])]).astype(np.int64)
+    return nptr, np.concatenate(out).astype(np.int32)
+
+
+@pytest.mark.parametrize("block", [(2, 1, 1), (2, 2, 1)], ids=["to198", "to354"])
+def test_large_patches_bitexact(oracle_mod, block):
+    """Stars beyond 160 DoFs, up to the 3D k = 2 sizes: unions of neighbouring
+    c5 vertex stars (up to 198 / 354 DoFs) installed on both sides.  K6 keeps such patch
+    matrices in a global-memory scratch, K2 streams them through 4 KB-chunk rings; factors,
+    sweeps and the V-cycle are bit-exact against the oracle."""
+    import torch
+    from paper_2104_14855_b200 import mhdp, workloads
+    cfg = workloads.small("c5", 6, 2)
+    w, _, _ = workloads.draw(cfg, 1, 4)
+    orc = oracle_mod.Oracle(cfg, w)
+    ptr, dofs = _union_patches(orc, cfg.N, 1, block)
+    assert np.diff(ptr).max() > 160
+    orc.set_patches(ptr, dofs, 1)
+    ctx = mhdp.Context(0, torch.cuda.current_stream().cuda_stream)
+    load_oracle_levels(ctx, orc, cfg)
+    n = orc.n()
+    rng = np.random.default_rng(2)
+    b, x0 = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    big = int(np.argmax(np.diff(ptr)))
+    lu_g, perm_g = ctx.patch_lu(big)
+    lu_o, perm_o, st = orc.patch_lu(big)
+    assert st == 0 and np.array_equal(perm_g, perm_o) and np.array_equal(bits(lu_g), bits(lu_o))
+    xg = cuda_vec(x0)
+    ctx.smooth(cuda_vec(b), xg, nsweeps=1)
+    assert np.array_equal(bits(host(xg)), bits(orc.sweep(b, x0, nsweeps=1)))
+    xv = torch.empty(n, dtype=torch.float64, device="cuda:0")
+    ctx.vcycle(cuda_vec(b), xv)
+    assert np.array_equal(bits(host(xv)), bits(orc.vcycle(b)))
