@@ -463,7 +463,7 @@ def run_ours(args):
     # north star), and NEXT-1: the paper's GMRES(6)-smoothed V-cycle inside flexible GMRES
     # (rtol = atol = 1e-7) ----
     solves = None
-    if not args.no_solves:
+    if not args.no_solves and ws == 1:          # single-GPU line only (not the scaling runs)
         xk = torch.empty_like(bd)
         e0.record(stream)
         its_r, rel_r, conv_r = ctx.gmres(bd, xk, maxit=60)
@@ -492,7 +492,7 @@ def run_ours(args):
 
     # ---- NEXT-4 / NEXT-3 measured on the same kernels (skipped with --no-variants) ----
     variants = None
-    if not args.no_variants:
+    if not args.no_variants and ws == 1:
         variants = run_variants(cfg, seed, dev, stream)
 
     # algorithmic bytes: K2 per patch i: 8 n_i^2 factor + 8 n_i gathered r
