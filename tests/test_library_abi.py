@@ -58,3 +58,14 @@ def test_invalid_arguments(mh):
     ctx.begin_levels(1, cfg)
     with pytest.raises(mh.MhdpError):
         ctx.load_level(0, np.array([0, 2]), np.array([0, 0]), np.array([1.0, 2.0]))
+
+
+def test_missing_library_fails_loudly(mh, monkeypatch):
+    """No CPU fallback: without libmhdp.so the binding raises (it never routes to the oracle
+    or to PyTorch)."""
+    monkeypatch.setattr(mh, "_lib", None)
+    monkeypatch.setattr(mh, "LIB", os.path.join(ROOT, "build", "does_not_exist", "libmhdp.so"))
+    with pytest.raises(OSError):
+        mh.lib()
+    with pytest.raises(OSError):
+        mh.Context(-1)
