@@ -21,7 +21,9 @@
  * stored as value at the first cell vertex plus its constant gradient.
  *
  * Integration: cell integrals with a collapsed (Duffy) 3x3(x3) Gauss-Legendre
- * rule (exact for degree <= 5; all cell integrands here have degree <= 2).  Facet
+ * rule (exact for degree <= 4 in 2D, <= 3 in 3D: the Duffy Jacobian adds one degree
+ * per collapsed direction; all k = 1 cell integrands have degree <= 2; the 3D k = 2
+ * assembly takes the 4-point rule).  Facet
  * integrals with a 3-point (2D) / collapsed 3x3 (3D) Gauss-Legendre rule (exact for
  * degree <= 5 / 4; facet integrands have degree <= 2 because the advecting field w_h
  * is constant per cell, reading R-w).  Nodes and weights are formed in `real` from
@@ -277,9 +279,12 @@ static void gauss01(int q, real *x, real *w) {
 }
 
 /* collapsed (Duffy) Gauss rule with q points per direction on the cell: physical points
- * and weights.  q = 3 (27 / 9 points) is exact to degree 5 (3D) / 5 (2D) and is used by
- * the assembly (all cell integrands have degree <= 2); q = 4 serves the manufactured-
- * solution helpers, whose integrands are not polynomial. */
+ * and weights.  Gauss-Legendre in each direction is exact to degree 2q-1, and the Duffy
+ * Jacobian (1-eta) / (1-eta)(1-zeta)^2 adds one degree per collapsed direction, so the
+ * rule is exact to degree 2q-2 in 2D and 2q-3 in 3D: q = 3 (9 / 27 points) -> 4 / 3,
+ * q = 4 -> 6 / 5.  The k = 1 assembly (cell integrands of degree <= 2) and the 2D k = 2
+ * assembly (degree <= 4) use q = 3; the 3D k = 2 assembly (degree 4) uses q = 4, as do
+ * the manufactured-solution helpers, whose integrands are not polynomial. */
 static int cell_rule(const Cell *K, int q, real (*xq)[3], real *wq) {
     real g[4], w[4];
     gauss01(q, g, w);
@@ -354,6 +359,13 @@ i64 oc_find(const OCsr *a, i64 row, int col) {
 /* free DoFs (with -1 for constrained) of the local basis of cell c, in local order */
 static int cell_dofs(const OMesh *m, const OSpace *s, i64 c, int *out) {
     int d = m->dim, n = 0;
+    if (s->degree == 2 && d == 3) {   /* NED1_2 (edges x 2, faces x 2) then RT2 (faces x 3, cell x 3) */
+        for (int q = 0; q < 6; q++) { int e0 = s->edof[m->ce[c * 6 + q]]; for (int a = 0; a < 2; a++) out[n++] = e0 < 0 ? -1 : e0 + a; }
+        for (int q = 0; q < 4; q++) { int g0 = s->gdof[om_facet_of_cell(m, c, q)]; for (int a = 0; a < 2; a++) out[n++] = g0 < 0 ? -1 : g0 + a; }
+        for (int q = 0; q < 4; q++) { int f0 = s->fdof[om_facet_of_cell(m, c, q)]; for (int a = 0; a < 3; a++) out[n++] = f0 < 0 ? -1 : f0 + a; }
+        for (int a = 0; a < 3; a++) out[n++] = s->cdof[c] + a;
+        return n;
+    }
     if (s->degree == 2 && s->block == ORC_VEL) {   /* BDM2: facets x 3, then cell x 3 */
         for (int q = 0; q < 3; q++) {
             int f0 = s->fdof[om_facet_of_cell(m, c, q)];
@@ -395,7 +407,7 @@ static int cmp_int(const void *a, const void *b) {
  * share a cell or the two cells of one facet (DG velocity).          */
 static void build_pattern(OCsr *A, const OMesh *m, const OSpace *s) {
     i64 n = s->n;
-    int ld[32];
+    int ld[64];
     i64 *sp = calloc((size_t)n + 1, sizeof(i64));
     for (i64 c = 0; c < m->nc; c++) {
         int k = cell_dofs(m, s, c, ld);
@@ -729,6 +741,8 @@ static void assemble_eb2(OCsr *A, Accum *S, const OMesh *m, const OSpace *s, con
                          const unsigned char *cmask);
 static void assemble_vel2(OCsr *A, Accum *S, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
                           const unsigned char *cmask);
+static void assemble_eb2_3d(OCsr *A, Accum *S, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
+                            const unsigned char *cmask);
 
 int oa_assemble_masked(OCsr *A, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
                        const unsigned char *cmask) {
@@ -737,6 +751,7 @@ int oa_assemble_masked(OCsr *A, const OMesh *m, const OSpace *s, const OParams *
         Accum S2;
         S2.acc = calloc((size_t)(A->nnz ? A->nnz : 1), sizeof(real));
         if (s->block == ORC_VEL) assemble_vel2(A, &S2, m, s, p, w, cmask);
+        else if (m->dim == 3) assemble_eb2_3d(A, &S2, m, s, p, w, cmask);
         else assemble_eb2(A, &S2, m, s, p, w, cmask);
         finish(A, &S2);
         free(S2.acc);
@@ -812,8 +827,10 @@ static double dof_functional(int block, int d, int kind, int sub, const real V[3
 }
 
 static int op_prolongation2(OCsr *P, const OMesh *mf, const OSpace *sf, const OMesh *mc, const OSpace *sc);
+static int op_prolongation3(OCsr *P, const OMesh *mf, const OSpace *sf, const OMesh *mc, const OSpace *sc);
 
 int op_prolongation(OCsr *P, const OMesh *mf, const OSpace *sf, const OMesh *mc, const OSpace *sc) {
+    if (sf->degree == 2 && mf->dim == 3) return op_prolongation3(P, mf, sf, mc, sc);
     if (sf->degree == 2) return op_prolongation2(P, mf, sf, mc, sc);
     int d = mf->dim, nvc = d + 1, nle = om_nle(d);
     memset(P, 0, sizeof(*P));
@@ -968,8 +985,12 @@ void oa_quadrature(const OMesh *m, double *pts, double *wts) {
 static void oa_load2(const OMesh *m, const OSpace *s, const double *fv, double *out);
 static void oa_eval2(const OMesh *m, const OSpace *s, const double *coef, double *fv);
 static double oa_duality_error2(const OMesh *m, const OSpace *s);
+static void oa_load3(const OMesh *m, const OSpace *s, const double *fv, double *out);
+static void oa_eval3(const OMesh *m, const OSpace *s, const double *coef, double *fv);
+static double oa_duality_error3(const OMesh *m, const OSpace *s);
 
 void oa_load(const OMesh *m, const OSpace *s, const double *fv, double *out) {
+    if (s->degree == 2 && m->dim == 3) { oa_load3(m, s, fv, out); return; }
     if (s->degree == 2) { oa_load2(m, s, fv, out); return; }
     int nq = oa_nq(m->dim), nc = oa_ncomp(s);
     real xq[64][3], wq[64];
@@ -998,6 +1019,7 @@ void oa_load(const OMesh *m, const OSpace *s, const double *fv, double *out) {
 }
 
 void oa_eval(const OMesh *m, const OSpace *s, const double *coef, double *fv) {
+    if (s->degree == 2 && m->dim == 3) { oa_eval3(m, s, coef, fv); return; }
     if (s->degree == 2) { oa_eval2(m, s, coef, fv); return; }
     int nq = oa_nq(m->dim), nc = oa_ncomp(s);
     real xq[64][3], wq[64];
@@ -1025,6 +1047,7 @@ void oa_eval(const OMesh *m, const OSpace *s, const double *coef, double *fv) {
  * (DoF duality of R-basis).  Each cell's functionals are applied to
  * that cell's own basis functions, matched through the global DoF numbering.   */
 double oa_duality_error(const OMesh *m, const OSpace *s) {
+    if (s->degree == 2 && m->dim == 3) return oa_duality_error3(m, s);
     if (s->degree == 2) return oa_duality_error2(m, s);
     int d = m->dim;
     double worst = 0;
@@ -1326,9 +1349,9 @@ static void rt2_functionals(const Cell *K, int Ncells, const Q2 *f, real *out) {
     }
 }
 
-/* Gauss-Jordan inverse with partial pivoting (n <= 12), row-major */
+/* Gauss-Jordan inverse with partial pivoting (n <= 20), row-major */
 static int mat_inv(int n, const real *a, real *inv) {
-    real w[12][24];
+    real w[20][40];
     for (int i = 0; i < n; i++)
         for (int j = 0; j < 2 * n; j++) w[i][j] = j < n ? a[i * n + j] : (real)(j - n == i);
     for (int k = 0; k < n; k++) {
@@ -1834,6 +1857,432 @@ static double oa_duality_error2(const OMesh *m, const OSpace *s) {
                 if (gi[j] < 0 || off[j] != off[i]) continue;
                 double v = (double)dof_functional2(m, s, gi[i], &F[j], &K);
                 double e = fabs(v - (gi[i] == gi[j] ? 1.0 : 0.0));
+                if (e > worst) worst = e;
+            }
+        }
+    }
+    return worst;
+}
+
+/* ========================================================================= */
+/* NEXT-2 in 3D: degree k = 2 for the E-B block, E in NED1_2, B in RT2 (*/
+/* P:654; complex CG2 -> NED1_2 -> RT2 -> DG1).  Reading R-basis2-3D:   */
+/*   NED1_2 (dim 20): per edge e = (a < b), t_e = x_b - x_a,                  */
+/*     N_{e,s}(E) = int_e (E . t_e / |e|) lambda_s ds (lambda_0 = lambda_a,    */
+/*     lambda_1 = lambda_b); per face f = (a < b < c), t_0 = x_b - x_a,        */
+/*     t_1 = x_c - x_a, N_{f,s}(E) = N int_f E . t_s dA;                       */
+/*   RT2 (dim 15): per face f, unit normal n_f of R-orient,                   */
+/*     N_{f,s}(B) = int_f (B . n_f) lambda_{v_s} dA; per cell N int_K B_r dx.  */
+/* Local bases dual to these functionals (primal bases inverted in `real`).    */
+/* ========================================================================= */
+typedef struct { real c[3][10]; } Q3;   /* 3 components in xi - X0: 1,x,y,z,xx,xy,xz,yy,yz,zz */
+
+static void q3_mono(const Cell *K, const real *x, real *mo) {
+    real a = x[0] - K->X[0][0], b = x[1] - K->X[0][1], c = x[2] - K->X[0][2];
+    mo[0] = 1; mo[1] = a; mo[2] = b; mo[3] = c; mo[4] = a * a; mo[5] = a * b; mo[6] = a * c;
+    mo[7] = b * b; mo[8] = b * c; mo[9] = c * c;
+}
+static void q3_eval(const Q3 *f, const Cell *K, const real *x, real *out) {
+    real mo[10];
+    q3_mono(K, x, mo);
+    for (int l = 0; l < 3; l++) { real s = 0; for (int k = 0; k < 10; k++) s += f->c[l][k] * mo[k]; out[l] = s; }
+}
+/* g[l][k] = d_k f_l */
+static void q3_grad(const Q3 *f, const Cell *K, const real *x, real g[3][3]) {
+    real a = x[0] - K->X[0][0], b = x[1] - K->X[0][1], c = x[2] - K->X[0][2];
+    for (int l = 0; l < 3; l++) {
+        const real *q = f->c[l];
+        g[l][0] = q[1] + 2 * q[4] * a + q[5] * b + q[6] * c;
+        g[l][1] = q[2] + q[5] * a + 2 * q[7] * b + q[8] * c;
+        g[l][2] = q[3] + q[6] * a + q[8] * b + 2 * q[9] * c;
+    }
+}
+static real bary3_at(const Cell *K, int a, const real *x) {
+    real s = a == 0 ? 1 : 0;
+    for (int k = 0; k < 3; k++) s += K->g[a][k] * (x[k] - K->X[0][k]);
+    return s;
+}
+
+/* the 20 NED1_2 functionals of cell K (local order: edge q = 0..5 x s = 0,1; face q = 0..3 x s) */
+static void ned2_functionals(const Cell *K, int Ncells, const Q3 *f, real *out) {
+    real g[3], w[3];
+    gauss01(3, g, w);
+    for (int q = 0; q < 6; q++) {
+        int lv[2];
+        om_edge_local_verts(3, q, lv);
+        real t[3], len2 = 0;
+        for (int k = 0; k < 3; k++) { t[k] = K->X[lv[1]][k] - K->X[lv[0]][k]; len2 += t[k] * t[k]; }
+        real len = RSQRT(len2);
+        for (int s = 0; s < 2; s++) {
+            real acc = 0;
+            for (int i = 0; i < 3; i++) {
+                real x[3], v[3];
+                for (int k = 0; k < 3; k++) x[k] = K->X[lv[0]][k] + g[i] * t[k];
+                q3_eval(f, K, x, v);
+                real lam = s == 0 ? 1 - g[i] : g[i];
+                acc += w[i] * len * (dot3(v, t) / len) * lam;
+            }
+            out[2 * q + s] = acc;
+        }
+    }
+    real xq[64][3], wq[64];
+    for (int q = 0; q < 4; q++) {
+        int lv[3];
+        om_facet_local_verts(3, q, lv);
+        real P[3][3];
+        facet_points(K, q, P);
+        int nq = facet_rule(3, P, xq, wq);
+        for (int s = 0; s < 2; s++) {
+            real t[3];
+            for (int k = 0; k < 3; k++) t[k] = P[s + 1][k] - P[0][k];
+            real acc = 0;
+            for (int i = 0; i < nq; i++) { real v[3]; q3_eval(f, K, xq[i], v); acc += wq[i] * dot3(v, t); }
+            out[12 + 2 * q + s] = (real)Ncells * acc;
+        }
+    }
+}
+
+/* the 15 RT2 functionals of cell K in 3D (local order: face q = 0..3 x s = 0..2, then r) */
+static void rt2_3d_functionals(const Cell *K, int Ncells, const Q3 *f, real *out) {
+    real xq[64][3], wq[64];
+    for (int q = 0; q < 4; q++) {
+        int lv[3];
+        om_facet_local_verts(3, q, lv);
+        real P[3][3], A[3];
+        facet_points(K, q, P);
+        facet_area_vector(3, P, A);
+        real area = RSQRT(dot3(A, A));
+        int nq = facet_rule(3, P, xq, wq);
+        for (int s = 0; s < 3; s++) {
+            real acc = 0;
+            for (int i = 0; i < nq; i++) {
+                real v[3];
+                q3_eval(f, K, xq[i], v);
+                acc += wq[i] * (dot3(v, A) / area) * bary3_at(K, lv[s], xq[i]);
+            }
+            out[3 * q + s] = acc;
+        }
+    }
+    int nq = cell_rule(K, 3, xq, wq);
+    for (int r = 0; r < 3; r++) {
+        real acc = 0;
+        for (int i = 0; i < nq; i++) { real v[3]; q3_eval(f, K, xq[i], v); acc += wq[i] * v[r]; }
+        out[12 + r] = (real)Ncells * acc;
+    }
+}
+
+static int q3_pair(int i, int j) {            /* monomial index of xi_i xi_j */
+    static const int M[3][3] = {{4, 5, 6}, {5, 7, 8}, {6, 8, 9}};
+    return M[i][j];
+}
+
+/* primal bases: P1^3 (12), then RT2: xi_s x (3); NED1_2: xi_s (x cross e_r), s != r (6),
+ * and the diagonal combinations xi_0 (x x e_0) - xi_1 (x x e_1), xi_1 (x x e_1) - xi_2 (x x e_2) */
+static int primal3(int ned, Q3 *p) {
+    int n = 0;
+    memset(p, 0, sizeof(Q3) * 20);
+    for (int r = 0; r < 3; r++)
+        for (int k = 0; k < 4; k++) p[n++].c[r][k] = 1;
+    if (!ned) {
+        for (int s = 0; s < 3; s++) { for (int l = 0; l < 3; l++) p[n].c[l][q3_pair(s, l)] = 1; n++; }
+        return n;
+    }
+    /* x cross e_r: r = 0: (0, z, -y); r = 1: (-z, 0, x); r = 2: (y, -x, 0) */
+    static const int XC[3][3][2] = {{{-1, 0}, {2, 1}, {1, -1}}, {{2, -1}, {-1, 0}, {0, 1}}, {{1, 1}, {0, -1}, {-1, 0}}};
+    Q3 F[3][3];
+    memset(F, 0, sizeof F);
+    for (int s = 0; s < 3; s++)
+        for (int r = 0; r < 3; r++)
+            for (int l = 0; l < 3; l++)
+                if (XC[r][l][0] >= 0) F[s][r].c[l][q3_pair(s, XC[r][l][0])] = XC[r][l][1];
+    for (int s = 0; s < 3; s++)
+        for (int r = 0; r < 3; r++)
+            if (s != r) p[n++] = F[s][r];
+    for (int l = 0; l < 3; l++)
+        for (int k = 0; k < 10; k++) {
+            p[n].c[l][k] = F[0][0].c[l][k] - F[1][1].c[l][k];
+            p[n + 1].c[l][k] = F[1][1].c[l][k] - F[2][2].c[l][k];
+        }
+    n += 2;
+    return n;
+}
+
+static void basis3(const Cell *K, int Ncells, int ned, Q3 *B) {
+    Q3 p[20];
+    int n = primal3(ned, p);
+    real M[400], C[400], col[20];
+    for (int j = 0; j < n; j++) {
+        if (ned) ned2_functionals(K, Ncells, &p[j], col); else rt2_3d_functionals(K, Ncells, &p[j], col);
+        for (int i = 0; i < n; i++) M[i * n + j] = col[i];
+    }
+    mat_inv(n, M, C);
+    for (int j = 0; j < n; j++) {
+        memset(&B[j], 0, sizeof(Q3));
+        for (int k = 0; k < n; k++)
+            for (int l = 0; l < 3; l++)
+                for (int t = 0; t < 10; t++) B[j].c[l][t] += C[k * n + j] * p[k].c[l][t];
+    }
+}
+
+static void cell_dofs3(const OMesh *m, const OSpace *s, i64 c, int *gE, int *gB) {
+    int all[35];
+    cell_dofs(m, s, c, all);
+    for (int a = 0; a < 20; a++) gE[a] = all[a];
+    for (int a = 0; a < 15; a++) gB[a] = all[20 + a];
+}
+
+static void assemble_eb2_3d(OCsr *A, Accum *S, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
+                            const unsigned char *cmask) {
+    real xq[64][3], wq[64];
+    static real EE[400], EB[300], BE[300], BB[225];
+    for (i64 c = 0; c < m->nc; c++) {
+        if (cmask && !cmask[c]) continue;
+        Cell K;
+        cell_geom(m, c, &K);
+        Q3 E[20], B[15];
+        int gE[20], gB[15];
+        basis3(&K, m->N, 1, E);
+        basis3(&K, m->N, 0, B);
+        cell_dofs3(m, s, c, gE, gB);
+        double pot[4][3];
+        real wx[3];
+        cell_pot(m, c, w, pot);
+        cell_wind(&K, pot, wx);
+        memset(EE, 0, sizeof EE); memset(EB, 0, sizeof EB); memset(BE, 0, sizeof BE); memset(BB, 0, sizeof BB);
+        /* q = 4: the collapsed Gauss rule gains degree from its Jacobian ((1-eta)(1-zeta)^2 in
+         * 3D), so 3 points are exact only to degree 3 there; the k = 2 mass and u^n x B
+         * integrands have degree 4 (q = 4: exact to degree 5) */
+        int nq = cell_rule(&K, 4, xq, wq);
+        for (int t = 0; t < nq; t++) {
+            real ev[20][3], ce[20][3], bv[15][3], db[15];
+            for (int a = 0; a < 20; a++) {
+                real g[3][3];
+                q3_eval(&E[a], &K, xq[t], ev[a]);
+                q3_grad(&E[a], &K, xq[t], g);
+                ce[a][0] = g[2][1] - g[1][2]; ce[a][1] = g[0][2] - g[2][0]; ce[a][2] = g[1][0] - g[0][1];
+            }
+            for (int k = 0; k < 15; k++) {
+                real g[3][3];
+                q3_eval(&B[k], &K, xq[t], bv[k]);
+                q3_grad(&B[k], &K, xq[t], g);
+                db[k] = g[0][0] + g[1][1] + g[2][2];
+            }
+            for (int i = 0; i < 20; i++) {
+                for (int j = 0; j < 20; j++) EE[i * 20 + j] += wq[t] * dot3(ev[j], ev[i]);
+                for (int k = 0; k < 15; k++) {
+                    real wxb = 0;
+                    if (!p->picard) { real cr[3]; cross3(wx, bv[k], cr); wxb = dot3(cr, ev[i]); }
+                    real ab = dot3(bv[k], ce[i]);
+                    EB[i * 15 + k] += wq[t] * (wxb - ab / p->Rem);
+                    BE[k * 20 + i] += wq[t] * ab;
+                }
+            }
+            for (int k = 0; k < 15; k++)
+                for (int l = 0; l < 15; l++) {
+                    real v = db[l] * db[k] / p->Rem;
+                    if (p->dt > 0) v += dot3(bv[l], bv[k]) / p->dt;
+                    BB[k * 15 + l] += wq[t] * v;
+                }
+        }
+        scatter(A, S, gE, 20, gE, 20, EE, 20);
+        scatter(A, S, gE, 20, gB, 15, EB, 15);
+        scatter(A, S, gB, 15, gE, 20, BE, 20);
+        scatter(A, S, gB, 15, gB, 15, BB, 15);
+    }
+}
+
+/* local index in cell K (of mesh m, cell c) of global vertex v */
+static int local_vertex(const OMesh *m, i64 c, int v) {
+    for (int a = 0; a < 4; a++) if (m->cv[c * 4 + a] == v) return a;
+    return -1;
+}
+
+/* the fine functional of free DoF I (3D k = 2) applied to F living on coarse cell Kc;
+ * owner = a fine cell containing the DoF's entity */
+static real dof_functional3(const OMesh *mf, const OSpace *sf, i64 I, const Q3 *F, const Cell *Kc, i64 owner) {
+    int kind = sf->dkind[I], ent = sf->dent[I], sub = sf->dsub[I];
+    real v[3], xq[64][3], wq[64];
+    if (kind == 1) {
+        real P0[3], t[3], len2 = 0, g[3], w[3];
+        for (int k = 0; k < 3; k++) {
+            P0[k] = (real)mf->lat[3 * mf->ev[2 * ent] + k] / mf->N;
+            t[k] = (real)mf->lat[3 * mf->ev[2 * ent + 1] + k] / mf->N - P0[k];
+            len2 += t[k] * t[k];
+        }
+        real len = RSQRT(len2), acc = 0;
+        gauss01(3, g, w);
+        for (int i = 0; i < 3; i++) {
+            real x[3];
+            for (int k = 0; k < 3; k++) x[k] = P0[k] + g[i] * t[k];
+            q3_eval(F, Kc, x, v);
+            acc += w[i] * len * (dot3(v, t) / len) * (sub == 0 ? 1 - g[i] : g[i]);
+        }
+        return acc;
+    }
+    if (kind == 3) {
+        Cell Kf;
+        cell_geom(mf, ent, &Kf);
+        int nq = cell_rule(&Kf, 3, xq, wq);
+        real acc = 0;
+        for (int i = 0; i < nq; i++) { q3_eval(F, Kc, xq[i], v); acc += wq[i] * v[sub]; }
+        return (real)mf->N * acc;
+    }
+    real P[3][3];
+    for (int a = 0; a < 3; a++)
+        for (int k = 0; k < 3; k++) P[a][k] = (real)mf->lat[3 * mf->fv[3 * ent + a] + k] / mf->N;
+    int nq = facet_rule(3, P, xq, wq);
+    real acc = 0;
+    if (kind == 4) {
+        real t[3];
+        for (int k = 0; k < 3; k++) t[k] = P[sub + 1][k] - P[0][k];
+        for (int i = 0; i < nq; i++) { q3_eval(F, Kc, xq[i], v); acc += wq[i] * dot3(v, t); }
+        return (real)mf->N * acc;
+    }
+    real A[3];
+    facet_area_vector(3, P, A);
+    real area = RSQRT(dot3(A, A));
+    Cell Kf;
+    cell_geom(mf, owner, &Kf);
+    int la = local_vertex(mf, owner, mf->fv[3 * ent + sub]);
+    for (int i = 0; i < nq; i++) {
+        q3_eval(F, Kc, xq[i], v);
+        acc += wq[i] * (dot3(v, A) / area) * bary3_at(&Kf, la, xq[i]);
+    }
+    return acc;
+}
+
+static int op_prolongation3(OCsr *P, const OMesh *mf, const OSpace *sf, const OMesh *mc, const OSpace *sc) {
+    memset(P, 0, sizeof(*P));
+    int *efirst = malloc(sizeof(int) * mf->ne), *ffirst = malloc(sizeof(int) * mf->nfacet);
+    for (i64 t = 0; t < mf->ne; t++) efirst[t] = -1;
+    for (i64 t = 0; t < mf->nfacet; t++) ffirst[t] = -1;
+    for (i64 c = 0; c < mf->nc; c++) {
+        for (int q = 0; q < 6; q++) if (efirst[mf->ce[c * 6 + q]] < 0) efirst[mf->ce[c * 6 + q]] = (int)c;
+        for (int q = 0; q < 4; q++) { int f = om_facet_of_cell(mf, c, q); if (ffirst[f] < 0) ffirst[f] = (int)c; }
+    }
+    i64 cap = 1024, nt = 0;
+    long long *idx = malloc(sizeof(long long) * 3 * cap);
+    real *tv = malloc(sizeof(real) * cap);
+    for (i64 I = 0; I < sf->n; I++) {
+        int kind = sf->dkind[I], ent = sf->dent[I];
+        int cf = kind == 1 ? efirst[ent] : (kind == 3 ? ent : ffirst[ent]);
+        i64 ccell = parent_cell(mf, mc, cf);
+        Cell Kc;
+        cell_geom(mc, ccell, &Kc);
+        Q3 F[20];
+        int gE[20], gB[15], nb;
+        const int *gJ;
+        cell_dofs3(mc, sc, ccell, gE, gB);
+        if (kind == 1 || kind == 4) { basis3(&Kc, mc->N, 1, F); nb = 20; gJ = gE; }
+        else { basis3(&Kc, mc->N, 0, F); nb = 15; gJ = gB; }
+        for (int b = 0; b < nb; b++) {
+            if (gJ[b] < 0) continue;
+            real val = dof_functional3(mf, sf, I, &F[b], &Kc, cf);
+            if (nt == cap) { cap *= 2; idx = realloc(idx, sizeof(long long) * 3 * cap); tv = realloc(tv, sizeof(real) * cap); }
+            idx[3 * nt] = I; idx[3 * nt + 1] = gJ[b]; idx[3 * nt + 2] = nt; tv[nt] = val; nt++;
+        }
+    }
+    qsort(idx, (size_t)nt, 3 * sizeof(long long), cmp_ij);
+    P->n = sf->n;
+    P->rp = calloc((size_t)sf->n + 1, sizeof(i64));
+    P->ci = malloc(sizeof(int) * (nt ? nt : 1));
+    P->v = malloc(sizeof(double) * (nt ? nt : 1));
+    i64 used = 0;
+    for (i64 t0 = 0; t0 < nt;) {            /* row rounding as R-prol2 */
+        i64 t1 = t0;
+        while (t1 < nt && idx[3 * t1] == idx[3 * t0]) t1++;
+        double mx = 0;
+        for (i64 t = t0; t < t1; t++) { double h = (double)tv[idx[3 * t + 2]]; if (fabs(h) > mx) mx = fabs(h); }
+        int E = 0;
+        if (mx > 0) frexp(mx, &E);
+        for (i64 t = t0; t < t1; t++) {
+            real x = tv[idx[3 * t + 2]];
+            double h = (double)x, l = (double)(x - (real)h);
+            double v = (mx > 0 && fabs(h) >= ldexp(mx, -30)) ? grid_round(h, l, E) : 0.0;
+            if (v == 0.0) continue;
+            P->ci[used] = (int)idx[3 * t + 1];
+            P->v[used] = v;
+            used++;
+            P->rp[idx[3 * t] + 1]++;
+        }
+        t0 = t1;
+    }
+    for (i64 i = 0; i < sf->n; i++) P->rp[i + 1] += P->rp[i];
+    P->nnz = used;
+    free(idx); free(tv); free(efirst); free(ffirst);
+    return 0;
+}
+
+static void oa_load3(const OMesh *m, const OSpace *s, const double *fv, double *out) {
+    int nq = oa_nq(3), nc = oa_ncomp(s);
+    real xq[64][3], wq[64];
+    memset(out, 0, sizeof(double) * s->n);
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        Q3 F[35];
+        int g[35];
+        basis3(&K, m->N, 1, F);
+        basis3(&K, m->N, 0, F + 20);
+        cell_dofs3(m, s, c, g, g + 20);
+        cell_rule(&K, 4, xq, wq);
+        for (int a = 0; a < 35; a++) {
+            if (g[a] < 0) continue;
+            int off = a < 20 ? 0 : 3;
+            real acc = 0;
+            for (int t = 0; t < nq; t++) {
+                real v[3];
+                q3_eval(&F[a], &K, xq[t], v);
+                const double *f = fv + ((i64)c * nq + t) * nc + off;
+                acc += wq[t] * (f[0] * v[0] + f[1] * v[1] + f[2] * v[2]);
+            }
+            out[g[a]] += (double)acc;
+        }
+    }
+}
+
+static void oa_eval3(const OMesh *m, const OSpace *s, const double *coef, double *fv) {
+    int nq = oa_nq(3), nc = oa_ncomp(s);
+    real xq[64][3], wq[64];
+    memset(fv, 0, sizeof(double) * m->nc * nq * nc);
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        Q3 F[35];
+        int g[35];
+        basis3(&K, m->N, 1, F);
+        basis3(&K, m->N, 0, F + 20);
+        cell_dofs3(m, s, c, g, g + 20);
+        cell_rule(&K, 4, xq, wq);
+        for (int a = 0; a < 35; a++) {
+            if (g[a] < 0) continue;
+            int off = a < 20 ? 0 : 3;
+            for (int t = 0; t < nq; t++) {
+                real v[3];
+                q3_eval(&F[a], &K, xq[t], v);
+                double *f = fv + ((i64)c * nq + t) * nc + off;
+                for (int k = 0; k < 3; k++) f[k] += coef[g[a]] * (double)v[k];
+            }
+        }
+    }
+}
+
+static double oa_duality_error3(const OMesh *m, const OSpace *s) {
+    double worst = 0;
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        Q3 F[35];
+        int g[35];
+        basis3(&K, m->N, 1, F);
+        basis3(&K, m->N, 0, F + 20);
+        cell_dofs3(m, s, c, g, g + 20);
+        for (int i = 0; i < 35; i++) {
+            if (g[i] < 0) continue;
+            for (int j = 0; j < 35; j++) {
+                if (g[j] < 0 || (i < 20) != (j < 20)) continue;
+                double v = (double)dof_functional3(m, s, g[i], &F[j], &K, c);
+                double e = fabs(v - (g[i] == g[j] ? 1.0 : 0.0));
                 if (e > worst) worst = e;
             }
         }

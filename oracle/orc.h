@@ -59,8 +59,10 @@ typedef struct {
     int *edof;             /* ne (3D E: NED1)                                          */
     int *fdof;             /* nfacet (B: RT)  or first velocity DoF of the facet (BDM: +0..dim-1);
                               k = 2: first of the 2 RT2 DoFs of the edge                */
-    int *cdof;             /* nc (k = 2 only): first of the 2 interior RT2 DoFs of the cell */
-    /* per free DoF: entity kind (0 vertex, 1 edge, 2 facet, 3 cell), entity id, sub index */
+    int *cdof;             /* nc (k = 2 only): first interior DoF of the cell (RT2: 2 in 2D, 3 in 3D) */
+    int *gdof;             /* nfacet (3D E-B k = 2 only): first of the 2 NED1_2 face DoFs       */
+    /* per free DoF: entity kind (0 vertex, 1 edge, 2 facet, 3 cell, 4 facet of the E field
+       in 3D k = 2), entity id, sub index                                                 */
     int *dkind, *dent, *dsub;
 } OSpace;
 

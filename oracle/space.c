@@ -42,6 +42,42 @@ static int os_build2_vel(OSpace *s, const OMesh *m) {
     return 0;
 }
 
+/* k = 2 in 3D, E-B block (NED1_2 x RT2; reading R-num2): E: 2 DoFs per free edge (edge
+ * order; sub 0/1 = moment against lambda of the lower/higher vertex), then 2 per interior
+ * face (face order; sub s = moment against the tangent x_{v_{s+1}} - x_{v_0}); B: 3 per
+ * interior face (face order; sub s = moment against lambda of the s-th face vertex), then
+ * 3 per cell (cell order; sub r = component).  Boundary DoFs removed (R-bc).           */
+static int os_build2_eb3(OSpace *s, const OMesh *m) {
+    s->vdof = malloc(sizeof(int) * m->nv);
+    s->edof = malloc(sizeof(int) * m->ne);
+    s->fdof = malloc(sizeof(int) * m->nfacet);
+    s->gdof = malloc(sizeof(int) * m->nfacet);
+    s->cdof = malloc(sizeof(int) * m->nc);
+    for (i64 v = 0; v < m->nv; v++) s->vdof[v] = -1;
+    i64 n = 0;
+    for (i64 e = 0; e < m->ne; e++) { s->edof[e] = m->ebnd[e] ? -1 : (int)n; if (s->edof[e] >= 0) n += 2; }
+    for (i64 f = 0; f < m->nfacet; f++) { s->gdof[f] = m->fcell[2 * f + 1] >= 0 ? (int)n : -1; if (s->gdof[f] >= 0) n += 2; }
+    s->nE = n;
+    for (i64 f = 0; f < m->nfacet; f++) { s->fdof[f] = m->fcell[2 * f + 1] >= 0 ? (int)n : -1; if (s->fdof[f] >= 0) n += 3; }
+    for (i64 c = 0; c < m->nc; c++) { s->cdof[c] = (int)n; n += 3; }
+    s->n = n;
+    s->dkind = malloc(sizeof(int) * (n ? n : 1));
+    s->dent = malloc(sizeof(int) * (n ? n : 1));
+    s->dsub = malloc(sizeof(int) * (n ? n : 1));
+    for (i64 e = 0; e < m->ne; e++)
+        if (s->edof[e] >= 0)
+            for (int a = 0; a < 2; a++) { s->dkind[s->edof[e] + a] = 1; s->dent[s->edof[e] + a] = (int)e; s->dsub[s->edof[e] + a] = a; }
+    for (i64 f = 0; f < m->nfacet; f++) {
+        if (s->gdof[f] >= 0)
+            for (int a = 0; a < 2; a++) { s->dkind[s->gdof[f] + a] = 4; s->dent[s->gdof[f] + a] = (int)f; s->dsub[s->gdof[f] + a] = a; }
+        if (s->fdof[f] >= 0)
+            for (int a = 0; a < 3; a++) { s->dkind[s->fdof[f] + a] = 2; s->dent[s->fdof[f] + a] = (int)f; s->dsub[s->fdof[f] + a] = a; }
+    }
+    for (i64 c = 0; c < m->nc; c++)
+        for (int a = 0; a < 3; a++) { s->dkind[s->cdof[c] + a] = 3; s->dent[s->cdof[c] + a] = (int)c; s->dsub[s->cdof[c] + a] = a; }
+    return 0;
+}
+
 /* k = 2 (NEXT-2; reading R-num2): 2D E-B.  E (CG2): free vertex DoFs in
  * vertex order, then free edge-midpoint DoFs in edge order; B (RT2): 2 DoFs per interior
  * edge (edge order; sub 0/1 = moment against lambda of the lower/higher vertex), then 2
@@ -75,7 +111,7 @@ int os_build(OSpace *s, const OMesh *m, int block, int degree) {
     memset(s, 0, sizeof(*s));
     s->block = block; s->dim = m->dim; s->degree = degree;
     if (degree == 2) {
-        if (m->dim != 2) return 1;
+        if (m->dim == 3) return block == ORC_EB ? os_build2_eb3(s, m) : 1;
         return block == ORC_EB ? os_build2(s, m) : os_build2_vel(s, m);
     }
     if (degree != 1) return 1;
@@ -114,7 +150,8 @@ int os_build(OSpace *s, const OMesh *m, int block, int degree) {
 }
 
 void os_free(OSpace *s) {
-    free(s->vdof); free(s->edof); free(s->fdof); free(s->cdof); free(s->dkind); free(s->dent); free(s->dsub);
+    free(s->vdof); free(s->edof); free(s->fdof); free(s->cdof); free(s->gdof); free(s->dkind); free(s->dent);
+    free(s->dsub);
     memset(s, 0, sizeof(*s));
 }
 
@@ -124,6 +161,7 @@ static int dof_contains_vertex(const OMesh *m, const OSpace *s, int d, int v) {
     switch (s->dkind[d]) {
     case 0: return e == v;
     case 1: return m->ev[2 * e] == v || m->ev[2 * e + 1] == v;
+    case 4: return m->fv[3 * e] == v || m->fv[3 * e + 1] == v || m->fv[3 * e + 2] == v;
     case 3: {
         int nvc = m->dim + 1;
         for (int q = 0; q < nvc; q++) if (m->cv[(i64)e * nvc + q] == v) return 1;
@@ -169,7 +207,15 @@ int opt_build(OPatches *pt, const OMesh *m, const OSpace *s) {
             i64 c = vc[t];
             /* all free DoFs of cell c */
             int cand[64]; int nc = 0;
-            if (s->degree == 2 && s->block == ORC_VEL) {   /* BDM2 (2D) */
+            if (s->degree == 2 && m->dim == 3) {              /* NED1_2 x RT2 (3D) */
+                for (int q = 0; q < 6; q++) { int d = s->edof[m->ce[c * 6 + q]]; if (d >= 0) { cand[nc++] = d; cand[nc++] = d + 1; } }
+                for (int q = 0; q < 4; q++) {
+                    int f = om_facet_of_cell(m, c, q);
+                    if (s->gdof[f] >= 0) { cand[nc++] = s->gdof[f]; cand[nc++] = s->gdof[f] + 1; }
+                    if (s->fdof[f] >= 0) for (int a = 0; a < 3; a++) cand[nc++] = s->fdof[f] + a;
+                }
+                for (int a = 0; a < 3; a++) cand[nc++] = s->cdof[c] + a;
+            } else if (s->degree == 2 && s->block == ORC_VEL) {   /* BDM2 (2D) */
                 for (int q = 0; q < 3; q++) {
                     int d = s->fdof[om_facet_of_cell(m, c, q)];
                     if (d >= 0) { cand[nc++] = d; cand[nc++] = d + 1; cand[nc++] = d + 2; }
