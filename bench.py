@@ -239,6 +239,46 @@ def _timed(stream, fn, reps=1):
     return e0.elapsed_time(e1) / reps, out
 
 
+def _k2_variant(cfg, seed, dev, stream, desc):
+    """one NEXT-2 (k = 2) hierarchy: host assembly, V-cycle, K2, sweep, GMRES(6)-smoothed FGMRES"""
+    import torch
+    from paper_2104_14855_b200 import mhdp, workloads
+    ctx = mhdp.Context(dev.index, stream.cuda_stream)
+    w, _, _ = workloads.draw(cfg, 1, seed)
+    t0 = time.perf_counter()
+    ctx.assemble(cfg, w)
+    t_asm = time.perf_counter() - t0
+    w, b, x = workloads.draw(cfg, ctx.n(), seed)
+    t0 = time.perf_counter()
+    ctx.setup()
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    L = ctx.num_levels()
+    fin = ctx.info(L - 1)
+    bd = torch.from_numpy(b).to(dev)
+    xd = torch.from_numpy(x).to(dev)
+    ctx.vcycle(bd, xd)
+    ms_v, _ = _timed(stream, lambda: ctx.vcycle(bd, xd), reps=10)
+    rd = torch.empty_like(bd)
+    ctx.residual(bd, xd, rd)
+    ctx.patch_apply(rd)
+    ms_k2, _ = _timed(stream, lambda: ctx.patch_apply(rd), reps=10)
+    ms_sw, _ = _timed(stream, lambda: ctx.smooth(bd, xd, nsweeps=1), reps=10)
+    k2_bytes = 8 * fin["sum_n2"] + 16 * fin["sum_n"]
+    sweep_bytes = 8 * fin["sum_n2"] + 8 * fin["nnz"] + 24 * fin["n"]
+    ctx.set_smoother("gmres", 6)
+    ms_f, (its, rel, conv) = _timed(stream, lambda: ctx.fgmres(bd, xd, maxit=60))
+    smoothed = sum(2 * cfg.nu * ctx.info(l)["n"] for l in range(1, L))
+    ctx.close()
+    return {"config": desc, "finest_dofs": fin["n"], "nnz": fin["nnz"], "patches": fin["npatch"],
+            "max_patch": fin["max_n"], "sum_n2": fin["sum_n2"], "factor_gb": 8e-9 * fin["sum_n2"],
+            "host_assembly_s": t_asm, "device_setup_s": t_setup,
+            "vcycle_ms": ms_v, "smoothed_dofs_per_s": smoothed / (ms_v * 1e-3),
+            "sweep_ms": ms_sw, "sweep_gbs": sweep_bytes / (ms_sw * 1e-3) / 1e9,
+            "K2_ms": ms_k2, "K2_gbs": k2_bytes / (ms_k2 * 1e-3) / 1e9,
+            "fgmres_gmres6_vcycle": {"its": its, "converged": conv, "relres": rel, "ms": ms_f}}
+
+
 def run_variants(cfg, seed, dev, stream):
     """NEXT-2: the k = 2 (CG2 x RT2) 2D E-B block at 512^2 (V-cycle, sweep, K2, FGMRES).
     NEXT-4: the c5 operator in the transient (implicit Euler, dt = 0.01 as P:656) Newton
@@ -283,69 +323,16 @@ def run_variants(cfg, seed, dev, stream):
         "dofs": {"u": co.nu, "p": co.np_, "E": co.nE, "B": co.nB}, "precondition_ms": ms_p,
         "fgmres": {"its": its3, "converged": conv3, "relres": rel3, "ms": ms_o}}
     co.close()
-    # NEXT-2: k = 2 (CG2 x RT2) 2D E-B block, c2 parameters at 512^2 x 2 cells, 7 levels
-    cfg2 = dataclasses.replace(workloads.CONFIGS["c2"], N=512, levels=7, degree=2)
-    ctx = mhdp.Context(dev.index, stream.cuda_stream)
-    w2, _, _ = workloads.draw(cfg2, 1, seed)
-    t0 = time.perf_counter()
-    ctx.assemble(cfg2, w2)
-    t_asm = time.perf_counter() - t0
-    w2, b2, x2 = workloads.draw(cfg2, ctx.n(), seed)
-    ctx.setup()
-    L2 = ctx.num_levels()
-    fin = ctx.info(L2 - 1)
-    bd = torch.from_numpy(b2).to(dev)
-    xd = torch.from_numpy(x2).to(dev)
-    ctx.vcycle(bd, xd)
-    ms_v, _ = _timed(stream, lambda: ctx.vcycle(bd, xd), reps=10)
-    rd = torch.empty_like(bd)
-    ctx.residual(bd, xd, rd)
-    ctx.patch_apply(rd)
-    ms_k2, _ = _timed(stream, lambda: ctx.patch_apply(rd), reps=10)
-    ms_sw, _ = _timed(stream, lambda: ctx.smooth(bd, xd, nsweeps=1), reps=10)
-    k2_bytes = 8 * fin["sum_n2"] + 16 * fin["sum_n"]
-    sweep_bytes = 8 * fin["sum_n2"] + 8 * fin["nnz"] + 24 * fin["n"]
-    ctx.set_smoother("gmres", 6)
-    ms_f, (its2, rel2, conv2) = _timed(stream, lambda: ctx.fgmres(bd, xd, maxit=60))
-    smoothed = sum(2 * cfg2.nu * ctx.info(l)["n"] for l in range(1, L2))
-    out["next2_k2_eb2d"] = {
-        "config": "2D E-B block, CG2 x RT2 (k = 2), 512^2 x 2 cells, 7 levels, V(2,2), Re_m = S = 1e3",
-        "finest_dofs": fin["n"], "patches": fin["npatch"], "max_patch": fin["max_n"], "sum_n2": fin["sum_n2"],
-        "host_assembly_s": t_asm, "vcycle_ms": ms_v, "smoothed_dofs_per_s": smoothed / (ms_v * 1e-3),
-        "sweep_ms": ms_sw, "sweep_gbs": sweep_bytes / (ms_sw * 1e-3) / 1e9,
-        "K2_ms": ms_k2, "K2_gbs": k2_bytes / (ms_k2 * 1e-3) / 1e9,
-        "fgmres_gmres6_vcycle": {"its": its2, "converged": conv2, "relres": rel2, "ms": ms_f}}
-    ctx.close()
-    # NEXT-2: k = 2 (BDM2) 2D AL velocity block, c3 parameters (Re = gamma = 1e4), sigma = 10 k^2
-    cfgv = dataclasses.replace(workloads.CONFIGS["c3"], N=256, levels=6, degree=2, sigma=40.0)
-    ctx = mhdp.Context(dev.index, stream.cuda_stream)
-    wv, _, _ = workloads.draw(cfgv, 1, seed)
-    t0 = time.perf_counter()
-    ctx.assemble(cfgv, wv)
-    t_asm = time.perf_counter() - t0
-    wv, bv, xv = workloads.draw(cfgv, ctx.n(), seed)
-    ctx.setup()
-    Lv = ctx.num_levels()
-    fin = ctx.info(Lv - 1)
-    bd = torch.from_numpy(bv).to(dev)
-    xd = torch.from_numpy(xv).to(dev)
-    ctx.vcycle(bd, xd)
-    ms_v, _ = _timed(stream, lambda: ctx.vcycle(bd, xd), reps=10)
-    rd = torch.empty_like(bd)
-    ctx.residual(bd, xd, rd)
-    ms_k2, _ = _timed(stream, lambda: ctx.patch_apply(rd), reps=10)
-    ms_sw, _ = _timed(stream, lambda: ctx.smooth(bd, xd, nsweeps=1), reps=10)
-    ctx.set_smoother("gmres", 6)
-    ms_f, (itsv, relv, convv) = _timed(stream, lambda: ctx.fgmres(bd, xd, maxit=60))
-    smoothed = sum(2 * cfgv.nu * ctx.info(l)["n"] for l in range(1, Lv))
-    out["next2_k2_vel2d"] = {
-        "config": "2D AL velocity block, BDM2 (k = 2), 256^2 x 2 cells, 6 levels, V(2,2), Re = gamma = 1e4, sigma = 40",
-        "finest_dofs": fin["n"], "patches": fin["npatch"], "max_patch": fin["max_n"], "sum_n2": fin["sum_n2"],
-        "host_assembly_s": t_asm, "vcycle_ms": ms_v, "smoothed_dofs_per_s": smoothed / (ms_v * 1e-3),
-        "sweep_ms": ms_sw, "K2_ms": ms_k2,
-        "K2_gbs": (8 * fin["sum_n2"] + 16 * fin["sum_n"]) / (ms_k2 * 1e-3) / 1e9,
-        "fgmres_gmres6_vcycle": {"its": itsv, "converged": convv, "relres": relv, "ms": ms_f}}
-    ctx.close()
+    # NEXT-2: k = 2, the paper's element degree, on both blocks (2D) and the 3D E-B block
+    out["next2_k2_eb2d"] = _k2_variant(
+        dataclasses.replace(workloads.CONFIGS["c2"], N=512, levels=7, degree=2), seed, dev, stream,
+        "2D E-B block, CG2 x RT2 (k = 2), 512^2 x 2 cells, 7 levels, V(2,2), Re_m = S = 1e3")
+    out["next2_k2_vel2d"] = _k2_variant(
+        dataclasses.replace(workloads.CONFIGS["c3"], N=256, levels=6, degree=2, sigma=40.0), seed, dev, stream,
+        "2D AL velocity block, BDM2 (k = 2), 256^2 x 2 cells, 6 levels, V(2,2), Re = gamma = 1e4, sigma = 40")
+    out["next2_k2_eb3d"] = _k2_variant(
+        dataclasses.replace(workloads.CONFIGS["c4"], degree=2), seed, dev, stream,
+        "3D E-B block, NED1_2 x RT2 (k = 2), 32^3 x 6 cells, 4 levels, V(2,2), Re_m = S = 1e3 (280-DoF stars)")
     return out
 
 

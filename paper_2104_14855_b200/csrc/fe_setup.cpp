@@ -2150,6 +2150,493 @@ void build_prolongation2_vel(const Mesh &mf, const Space2 &sf, const Mesh &mc, c
         for (size_t t = 0; t < fin[I].size(); ++t) { ci[rp[I] + t] = fin[I][t].first; vv[rp[I] + t] = fin[I][t].second; }
 }
 
+
+// ---------------- k = 2 E-B block in 3D: NED1_2 x RT2 (reading R-basis2-3D, NEXT-2) ------
+// DoFs: per edge e = (a < b), t_e = x_b - x_a: N_{e,s}(E) = int_e (E.t_e/|e|) lam_s ds
+// (lam_0 = lam_a, lam_1 = lam_b); per face f = (a < b < c), t_0 = x_b - x_a, t_1 = x_c - x_a:
+// N_{f,s}(E) = N int_f E.t_s dA; RT2: N_{f,s}(B) = int_f (B.n_f) lam_{v_s} dA (n_f of
+// R-orient), per cell N_{K,r}(B) = N int_K B_r dx.  Numbering (R-num2): 2 per interior
+// edge, 2 per interior face (E), then 3 per interior face, 3 per cell (B).  A field is
+// stored as sum_p c_p lam^p over the 10 barycentric pairs p = (a <= b); every integral is
+// closed-form: int_K lam^beta = 6|K| beta!/(|beta|+3)!, int_f mu^beta = 2|f| beta!/(|beta|+2)!,
+// int_e mu^beta = |e| beta!/(|beta|+1)!.  Primal bases: the Arnold-Falk-Winther sets
+// lam_i W_jk (j < k, i >= j; W Whitney 1-forms, 20) and lam_i phi_jkl (i >= j; phi
+// Whitney 2-forms, 15), made dual to the DoFs by a double-double Gauss-Jordan.
+namespace k2d3 {
+
+static const int PA[10][2] = {{0, 0}, {0, 1}, {0, 2}, {0, 3}, {1, 1}, {1, 2}, {1, 3}, {2, 2}, {2, 3}, {3, 3}};
+static const int PID[4][4] = {{0, 1, 2, 3}, {1, 4, 5, 6}, {2, 5, 7, 8}, {3, 6, 8, 9}};
+static const int LE[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+
+struct Q { dd c[10][3]; };     // vector field sum_p c_p lam^p
+
+inline double bfact(std::initializer_list<int> idx) {   // beta! of a multiset of indices
+    int n[4] = {0, 0, 0, 0};
+    for (int i : idx) n[i]++;
+    return fact(n[0]) * fact(n[1]) * fact(n[2]) * fact(n[3]);
+}
+
+struct Tabs {   // int_K lam^beta / (6|K|) = beta! / (|beta|+3)!
+    dd m4[10][10], m3[10][4], m2[4][4];
+    Tabs() {
+        for (int p = 0; p < 10; ++p) {
+            for (int q = 0; q < 10; ++q)
+                m4[p][q] = dd(bfact({PA[p][0], PA[p][1], PA[q][0], PA[q][1]})) / dd(fact(7));
+            for (int c = 0; c < 4; ++c) m3[p][c] = dd(bfact({PA[p][0], PA[p][1], c})) / dd(fact(6));
+        }
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b) m2[a][b] = dd(bfact({a, b})) / dd(fact(5));
+    }
+};
+const Tabs &tabs() { static const Tabs T; return T; }
+
+struct Space3 {
+    i64 n = 0, nE = 0;
+    std::vector<int> edof, gdof, fdof, cdof;
+};
+
+void build_space3(Space3 &s, const Mesh &m) {
+    s.edof.assign(m.ne, -1); s.gdof.assign(m.nf, -1); s.fdof.assign(m.nf, -1); s.cdof.assign(m.nc, -1);
+    i64 n = 0;
+    for (i64 e = 0; e < m.ne; ++e) if (!m.common_bnd(&m.ev[2 * e], 2)) { s.edof[e] = (int)n; n += 2; }
+    for (i64 f = 0; f < m.nf; ++f) if (!m.common_bnd(&m.fv[3 * f], 3)) { s.gdof[f] = (int)n; n += 2; }
+    s.nE = n;
+    for (i64 f = 0; f < m.nf; ++f) if (!m.common_bnd(&m.fv[3 * f], 3)) { s.fdof[f] = (int)n; n += 3; }
+    for (i64 c = 0; c < m.nc; ++c) { s.cdof[c] = (int)n; n += 3; }
+    s.n = n;
+}
+
+// local order: E: edge q (LE order) x s, then face q (opposite vertex q) x s;
+//              B: face q x s, then r
+void cell_dofs3(const Mesh &m, const Space3 &s, i64 c, int *gE, int *gB) {
+    for (int q = 0; q < 6; ++q) {
+        const int e0 = s.edof[m.cedge[6 * c + q]];
+        for (int t = 0; t < 2; ++t) gE[2 * q + t] = e0 < 0 ? -1 : e0 + t;
+    }
+    for (int q = 0; q < 4; ++q) {
+        const int f = m.cfacet[4 * c + q], g0 = s.gdof[f], f0 = s.fdof[f];
+        for (int t = 0; t < 2; ++t) gE[12 + 2 * q + t] = g0 < 0 ? -1 : g0 + t;
+        for (int t = 0; t < 3; ++t) gB[3 * q + t] = f0 < 0 ? -1 : f0 + t;
+    }
+    for (int r = 0; r < 3; ++r) gB[12 + r] = s.cdof[c] + r;
+}
+
+inline void face_verts(int q, int *fl) { int t = 0; for (int a = 0; a < 4; ++a) if (a != q) fl[t++] = a; }
+
+// the 20 NED1_2 functionals of F on cell G (farea[q] = |face q|)
+void ned_fun(const GeoT<dd> &G, int Ncells, const dd *farea, const Q &F, dd *out) {
+    for (int q = 0; q < 6; ++q) {
+        const int v[2] = {LE[q][0], LE[q][1]};
+        dd t[3];
+        for (int r = 0; r < 3; ++r) t[r] = G.X[v[1]][r] - G.X[v[0]][r];
+        for (int s = 0; s < 2; ++s) {
+            dd acc(0.0);
+            for (int x = 0; x < 2; ++x)
+                for (int y = x; y < 2; ++y)
+                    acc += dot3(F.c[PID[v[x]][v[y]]], t) * dd(bfact({v[x], v[y], v[s]}));
+            out[2 * q + s] = acc / dd(24.0);
+        }
+    }
+    for (int q = 0; q < 4; ++q) {
+        int fl[3];
+        face_verts(q, fl);
+        dd t[2][3];
+        for (int r = 0; r < 3; ++r) {
+            t[0][r] = G.X[fl[1]][r] - G.X[fl[0]][r];
+            t[1][r] = G.X[fl[2]][r] - G.X[fl[0]][r];
+        }
+        for (int s = 0; s < 2; ++s) {
+            dd acc(0.0);
+            for (int x = 0; x < 3; ++x)
+                for (int y = x; y < 3; ++y) acc += dot3(F.c[PID[fl[x]][fl[y]]], t[s]) * dd(bfact({fl[x], fl[y]}));
+            out[12 + 2 * q + s] = acc * dd((double)Ncells) * farea[q] / dd(12.0);
+        }
+    }
+}
+
+// the 15 RT2 functionals of F on cell G
+void rt_fun(const GeoT<dd> &G, int Ncells, const Q &F, dd *out) {
+    for (int q = 0; q < 4; ++q) {
+        dd A[3];
+        int fl[3];
+        facet_area(G, q, A, fl);
+        for (int s = 0; s < 3; ++s) {
+            dd acc(0.0);
+            for (int x = 0; x < 3; ++x)
+                for (int y = x; y < 3; ++y) acc += dot3(F.c[PID[fl[x]][fl[y]]], A) * dd(bfact({fl[x], fl[y], fl[s]}));
+            out[3 * q + s] = acc / dd(60.0);
+        }
+    }
+    for (int r = 0; r < 3; ++r) {
+        dd acc(0.0);
+        for (int p = 0; p < 10; ++p) acc += F.c[p][r] * dd(bfact({PA[p][0], PA[p][1]}));
+        out[12 + r] = acc * dd((double)Ncells) * G.vol / dd(20.0);
+    }
+}
+
+void add_pair(Q &F, int a, int b, const dd *v, double sgn) {
+    dd *c = F.c[PID[a][b]];
+    for (int r = 0; r < 3; ++r) c[r] += v[r] * dd(sgn);
+}
+
+// dual basis: B_j = sum_k Minv[k][j] p_k, M[i][j] = N_i(p_j)
+template <int NB, class Fun>
+void dualize(const Q *p, Fun fun, Q *B) {
+    dd W[NB][2 * NB];
+    for (int j = 0; j < NB; ++j) {
+        dd col[NB];
+        fun(p[j], col);
+        for (int i = 0; i < NB; ++i) { W[i][j] = col[i]; W[i][NB + j] = dd(i == j ? 1.0 : 0.0); }
+    }
+    for (int k = 0; k < NB; ++k) {
+        int piv = k;
+        for (int i = k + 1; i < NB; ++i) if (std::fabs(W[i][k].hi) > std::fabs(W[piv][k].hi)) piv = i;
+        if (piv != k) for (int j = 0; j < 2 * NB; ++j) std::swap(W[k][j], W[piv][j]);
+        const dd d = W[k][k];
+        for (int j = 0; j < 2 * NB; ++j) W[k][j] = W[k][j] / d;
+        for (int i = 0; i < NB; ++i) {
+            if (i == k) continue;
+            const dd l = W[i][k];
+            if (l.hi == 0.0 && l.lo == 0.0) continue;
+            for (int j = 0; j < 2 * NB; ++j) W[i][j] = W[i][j] - l * W[k][j];
+        }
+    }
+    for (int j = 0; j < NB; ++j) {
+        memset((void *)&B[j], 0, sizeof(Q));
+        for (int k = 0; k < NB; ++k)
+            for (int pp = 0; pp < 10; ++pp)
+                for (int r = 0; r < 3; ++r) B[j].c[pp][r] += W[k][NB + j] * p[k].c[pp][r];
+    }
+}
+
+struct Elem3 {
+    GeoT<dd> G;
+    dd farea[4];
+    Q E[20], B[15];
+};
+
+void elem3(const Mesh &m, i64 c, Elem3 &K) {
+    cell_geo(m, c, K.G);
+    const GeoT<dd> &G = K.G;
+    for (int q = 0; q < 4; ++q) {
+        dd A[3];
+        int fl[3];
+        facet_area(G, q, A, fl);
+        K.farea[q] = sqrt(dot3(A, A));
+    }
+    Q p[20];
+    memset((void *)p, 0, sizeof p);
+    int n = 0;
+    for (int e = 0; e < 6; ++e) {                 // lam_i W_jk = lam_i lam_j g_k - lam_i lam_k g_j
+        const int j = LE[e][0], k = LE[e][1];
+        for (int i = j; i < 4; ++i, ++n) { add_pair(p[n], i, j, G.g[k], 1.0); add_pair(p[n], i, k, G.g[j], -1.0); }
+    }
+    dualize<20>(p, [&](const Q &F, dd *out) { ned_fun(G, m.N, K.farea, F, out); }, K.E);
+    memset((void *)p, 0, sizeof p);
+    n = 0;
+    for (int q = 3; q >= 0; --q) {                // faces (j < k < l); lam_i phi_jkl, i >= j
+        int fl[3];
+        face_verts(q, fl);
+        const int j = fl[0], k = fl[1], l = fl[2];
+        dd kl[3], jl[3], jk[3];
+        cross3(G.g[k], G.g[l], kl); cross3(G.g[j], G.g[l], jl); cross3(G.g[j], G.g[k], jk);
+        for (int i = j; i < 4; ++i, ++n) {
+            add_pair(p[n], i, j, kl, 1.0); add_pair(p[n], i, k, jl, -1.0); add_pair(p[n], i, l, jk, 1.0);
+        }
+    }
+    dualize<15>(p, [&](const Q &F, dd *out) { rt_fun(G, m.N, F, out); }, K.B);
+}
+
+struct EBLocal3 {
+    int gE[20], gB[15];
+    dd EE[20][20], EB[20][15], BE[15][20], BB[15][15];
+};
+
+void eb_local3(const Mesh &m, const Space3 &s, i64 c, const double *pot, const Params &p, EBLocal3 &L) {
+    Elem3 K;
+    elem3(m, c, K);
+    const GeoT<dd> &G = K.G;
+    const Tabs &T = tabs();
+    cell_dofs3(m, s, c, L.gE, L.gB);
+    dd w[3];
+    cell_wind(G, pot, w);
+    const dd sixK = dd(6.0) * G.vol;
+    // curl E_i = sum_c lam_c C[i][c]; div B_k = sum_c lam_c D[k][c]
+    dd C[20][4][3], D[15][4];
+    memset((void *)C, 0, sizeof C);
+    memset((void *)D, 0, sizeof D);
+    for (int pp = 0; pp < 10; ++pp) {
+        const int a = PA[pp][0], b = PA[pp][1];
+        for (int i = 0; i < 20; ++i) {
+            dd ca[3], cb[3];
+            cross3(G.g[a], K.E[i].c[pp], ca);
+            cross3(G.g[b], K.E[i].c[pp], cb);
+            for (int r = 0; r < 3; ++r) { C[i][b][r] += ca[r]; C[i][a][r] += cb[r]; }
+        }
+        for (int k = 0; k < 15; ++k) {
+            D[k][b] += dot3(G.g[a], K.B[k].c[pp]);
+            D[k][a] += dot3(G.g[b], K.B[k].c[pp]);
+        }
+    }
+    // mass-weighted coefficients WE_i,p = sum_q m4[p][q] E_i,q (same for B); CW_i,p = sum_c m3[p][c] C_i,c
+    static thread_local dd WE[20][10][3], WB[15][10][3], CW[20][10][3];
+    for (int pp = 0; pp < 10; ++pp)
+        for (int r = 0; r < 3; ++r) {
+            for (int i = 0; i < 20; ++i) {
+                dd acc(0.0), acc2(0.0);
+                for (int qq = 0; qq < 10; ++qq) acc += T.m4[pp][qq] * K.E[i].c[qq][r];
+                for (int cc = 0; cc < 4; ++cc) acc2 += T.m3[pp][cc] * C[i][cc][r];
+                WE[i][pp][r] = acc;
+                CW[i][pp][r] = acc2;
+            }
+            for (int k = 0; k < 15; ++k) {
+                dd acc(0.0);
+                for (int qq = 0; qq < 10; ++qq) acc += T.m4[pp][qq] * K.B[k].c[qq][r];
+                WB[k][pp][r] = acc;
+            }
+        }
+    for (int i = 0; i < 20; ++i)
+        for (int j = 0; j < 20; ++j) {
+            dd acc(0.0);
+            for (int pp = 0; pp < 10; ++pp) acc += dot3(K.E[i].c[pp], WE[j][pp]);
+            L.EE[i][j] = acc * sixK;
+        }
+    for (int k = 0; k < 15; ++k)
+        for (int i = 0; i < 20; ++i) {
+            dd ab(0.0), gt(0.0);
+            for (int pp = 0; pp < 10; ++pp) {
+                ab += dot3(K.B[k].c[pp], CW[i][pp]);
+                if (!p.picard) {
+                    dd wb[3];
+                    cross3(w, K.B[k].c[pp], wb);
+                    gt += dot3(wb, WE[i][pp]);
+                }
+            }
+            ab = ab * sixK;
+            gt = gt * sixK;
+            L.BE[k][i] = ab;
+            L.EB[i][k] = gt - ab / dd(p.Rem);
+        }
+    for (int k = 0; k < 15; ++k)
+        for (int l = 0; l < 15; ++l) {
+            dd dv(0.0);
+            for (int a = 0; a < 4; ++a)
+                for (int b = 0; b < 4; ++b) dv += D[k][a] * D[l][b] * T.m2[a][b];
+            dd v = dv * sixK / dd(p.Rem);
+            if (p.dt > 0) {
+                dd ms(0.0);
+                for (int pp = 0; pp < 10; ++pp) ms += dot3(K.B[k].c[pp], WB[l][pp]);
+                v += ms * sixK / dd(p.dt);
+            }
+            L.BB[k][l] = v;
+        }
+}
+
+// gather-form assembly by rows (cells of the row's entity, ascending), R-exact rows
+void assemble_eb3(const Mesh &m, const Space3 &s, const Params &p, const double *pot, Pattern &P,
+                  std::vector<double> &val) {
+    std::vector<i64> ep, fp;
+    std::vector<int> ec, fc;
+    incidence(m, 1, ep, ec);
+    incidence(m, 2, fp, fc);
+    std::vector<int> dkind(s.n), dent(s.n);
+    for (i64 e = 0; e < m.ne; ++e)
+        if (s.edof[e] >= 0) for (int a = 0; a < 2; ++a) { dkind[s.edof[e] + a] = 1; dent[s.edof[e] + a] = (int)e; }
+    for (i64 f = 0; f < m.nf; ++f) {
+        if (s.gdof[f] >= 0) for (int a = 0; a < 2; ++a) { dkind[s.gdof[f] + a] = 2; dent[s.gdof[f] + a] = (int)f; }
+        if (s.fdof[f] >= 0) for (int a = 0; a < 3; ++a) { dkind[s.fdof[f] + a] = 2; dent[s.fdof[f] + a] = (int)f; }
+    }
+    for (i64 c = 0; c < m.nc; ++c) for (int a = 0; a < 3; ++a) { dkind[s.cdof[c] + a] = 3; dent[s.cdof[c] + a] = (int)c; }
+    std::vector<int> self(m.nc);
+    std::iota(self.begin(), self.end(), 0);
+    auto cells_of = [&](i64 row, const int *&b, const int *&e) {
+        const int k = dkind[row], id = dent[row];
+        if (k == 1) { b = ec.data() + ep[id]; e = ec.data() + ep[id + 1]; }
+        else if (k == 2) { b = fc.data() + fp[id]; e = fc.data() + fp[id + 1]; }
+        else { b = self.data() + id; e = b + 1; }
+    };
+    std::vector<EBLocal3> loc(m.nc);
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < m.nc; ++c) eb_local3(m, s, c, pot, p, loc[c]);
+    P.rp.assign(s.n + 1, 0);
+    std::vector<std::vector<int>> rows(s.n);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (i64 r = 0; r < s.n; ++r) {
+        const int *b, *e;
+        cells_of(r, b, e);
+        std::vector<int> cols;
+        for (const int *c = b; c != e; ++c) {
+            for (int t = 0; t < 20; ++t) if (loc[*c].gE[t] >= 0) cols.push_back(loc[*c].gE[t]);
+            for (int t = 0; t < 15; ++t) if (loc[*c].gB[t] >= 0) cols.push_back(loc[*c].gB[t]);
+        }
+        std::sort(cols.begin(), cols.end());
+        cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+        rows[r] = std::move(cols);
+    }
+    for (i64 r = 0; r < s.n; ++r) P.rp[r + 1] = P.rp[r] + (i64)rows[r].size();
+    P.ci.resize(P.rp[s.n]);
+    for (i64 r = 0; r < s.n; ++r) std::copy(rows[r].begin(), rows[r].end(), P.ci.begin() + P.rp[r]);
+    rows.clear();
+    rows.shrink_to_fit();
+    val.assign(P.rp[s.n], 0.0);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (i64 r = 0; r < s.n; ++r) {
+        const int *b, *e;
+        cells_of(r, b, e);
+        const i64 base = P.rp[r], len = P.rp[r + 1] - base;
+        std::vector<dd> acc(len);
+        const bool isB = r >= s.nE;
+        for (const int *c = b; c != e; ++c) {
+            const EBLocal3 &K = loc[*c];
+            int li = -1;
+            if (!isB) { for (int a = 0; a < 20; ++a) if (K.gE[a] == r) li = a; }
+            else { for (int a = 0; a < 15; ++a) if (K.gB[a] == r) li = a; }
+            auto add = [&](int col, const dd &v) { acc[find_col(P, r, col) - base] += v; };
+            for (int j = 0; j < 20; ++j) if (K.gE[j] >= 0) add(K.gE[j], isB ? K.BE[li][j] : K.EE[li][j]);
+            for (int j = 0; j < 15; ++j) if (K.gB[j] >= 0) add(K.gB[j], isB ? K.BB[li][j] : K.EB[li][j]);
+        }
+        round_row(acc.data(), len, val.data() + base);
+    }
+}
+
+// vertex stars: DoFs of the edges, faces and cells containing the vertex, ascending
+void build_patches3(const Mesh &m, const Space3 &s, std::vector<i64> &pptr, std::vector<int> &pdofs) {
+    std::vector<std::vector<int>> vlist(m.nv);
+    for (i64 e = 0; e < m.ne; ++e)
+        if (s.edof[e] >= 0)
+            for (int t = 0; t < 2; ++t) for (int a = 0; a < 2; ++a) vlist[m.ev[2 * e + t]].push_back(s.edof[e] + a);
+    for (i64 f = 0; f < m.nf; ++f)
+        for (int t = 0; t < 3; ++t) {
+            auto &L = vlist[m.fv[3 * f + t]];
+            if (s.gdof[f] >= 0) for (int a = 0; a < 2; ++a) L.push_back(s.gdof[f] + a);
+            if (s.fdof[f] >= 0) for (int a = 0; a < 3; ++a) L.push_back(s.fdof[f] + a);
+        }
+    for (i64 c = 0; c < m.nc; ++c)
+        for (int t = 0; t < 4; ++t) for (int a = 0; a < 3; ++a) vlist[m.cv[4 * c + t]].push_back(s.cdof[c] + a);
+    pptr.assign(1, 0);
+    pdofs.clear();
+    for (i64 v = 0; v < m.nv; ++v) {
+        auto &L = vlist[v];
+        if (L.empty()) continue;
+        std::sort(L.begin(), L.end());
+        pdofs.insert(pdofs.end(), L.begin(), L.end());
+        pptr.push_back((i64)pdofs.size());
+    }
+}
+
+// R-prol at k = 2 in 3D: coarse functions rewritten in the fine cell's barycentrics
+// (lam^c_b = sum_a lam^c_b(X^f_a) lam^f_a), fine functionals in closed form; each fine DoF
+// is computed by its owner (the lowest-index fine cell containing its entity); rows
+// rounded as R-exact, |x| < 2^-30 max|row| dropped (R-prol2)
+void build_prolongation3(const Mesh &mf, const Space3 &sf, const Mesh &mc, const Space3 &sc, std::vector<i64> &rp,
+                         std::vector<int> &ci, std::vector<double> &vv) {
+    static const int PERM[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    std::vector<std::vector<std::pair<int, dd>>> rows(sf.n);
+    std::vector<Elem3> ce(mc.nc);
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < mc.nc; ++c) elem3(mc, c, ce[c]);
+    std::vector<int> owner(sf.n, INT32_MAX);
+    for (i64 c = mf.nc - 1; c >= 0; --c) {
+        int gE[20], gB[15];
+        cell_dofs3(mf, sf, c, gE, gB);
+        for (int t = 0; t < 20; ++t) if (gE[t] >= 0) owner[gE[t]] = (int)c;
+        for (int t = 0; t < 15; ++t) if (gB[t] >= 0) owner[gB[t]] = (int)c;
+    }
+#pragma omp parallel for schedule(dynamic, 64)
+    for (i64 c = 0; c < mf.nc; ++c) {
+        int gE[20], gB[15];
+        cell_dofs3(mf, sf, c, gE, gB);
+        bool any = false;
+        for (int t = 0; t < 20; ++t) any = any || (gE[t] >= 0 && owner[gE[t]] == c);
+        for (int t = 0; t < 15; ++t) any = any || (gB[t] >= 0 && owner[gB[t]] == c);
+        if (!any) continue;
+        int Lf[4][3] = {{0}};
+        int sum[3] = {0, 0, 0};
+        for (int a = 0; a < 4; ++a) {
+            mf.lat(mf.cv[4 * c + a], Lf[a]);
+            for (int r = 0; r < 3; ++r) sum[r] += Lf[a][r];
+        }
+        int cube[3], rel[3];
+        for (int r = 0; r < 3; ++r) { cube[r] = sum[r] / 8; rel[r] = sum[r] - 8 * cube[r]; }
+        const i64 cb = cube[0] + (i64)mc.N * (cube[1] + (i64)mc.N * cube[2]);
+        i64 pc = -1;
+        for (int q = 0; q < 6; ++q)
+            if (rel[PERM[q][0]] > rel[PERM[q][1]] && rel[PERM[q][1]] > rel[PERM[q][2]]) pc = 6 * cb + q;
+        const Elem3 &Kc = ce[pc];
+        int cE[20], cB[15];
+        cell_dofs3(mc, sc, pc, cE, cB);
+        GeoT<dd> Gf;
+        cell_geo(mf, c, Gf);
+        dd fa[4];
+        for (int q = 0; q < 4; ++q) {
+            dd A[3];
+            int fl[3];
+            facet_area(Gf, q, A, fl);
+            fa[q] = sqrt(dot3(A, A));
+        }
+        dd T[4][4];                                 // T[b][a] = lam^c_b(X^f_a)
+        for (int b = 0; b < 4; ++b)
+            for (int a = 0; a < 4; ++a) {
+                dd v(b == 0 ? 1.0 : 0.0);
+                for (int r = 0; r < 3; ++r) v += Kc.G.g[b][r] * (Gf.X[a][r] - Kc.G.X[0][r]);
+                T[b][a] = v;
+            }
+        auto to_fine = [&](const Q &in, Q &out) {
+            memset((void *)&out, 0, sizeof(Q));
+            for (int pp = 0; pp < 10; ++pp) {
+                const int b = PA[pp][0], d2 = PA[pp][1];
+                for (int a = 0; a < 4; ++a)
+                    for (int a2 = 0; a2 < 4; ++a2) {
+                        const dd tt = T[b][a] * T[d2][a2];
+                        if (tt.hi == 0.0) continue;
+                        dd *o = out.c[PID[a][a2]];
+                        for (int r = 0; r < 3; ++r) o[r] += in.c[pp][r] * tt;
+                    }
+            }
+        };
+        for (int j = 0; j < 20; ++j) {
+            if (cE[j] < 0) continue;
+            Q F;
+            to_fine(Kc.E[j], F);
+            dd out[20];
+            ned_fun(Gf, mf.N, fa, F, out);
+            for (int t = 0; t < 20; ++t)
+                if (gE[t] >= 0 && owner[gE[t]] == c) rows[gE[t]].push_back({cE[j], out[t]});
+        }
+        for (int j = 0; j < 15; ++j) {
+            if (cB[j] < 0) continue;
+            Q F;
+            to_fine(Kc.B[j], F);
+            dd out[15];
+            rt_fun(Gf, mf.N, F, out);
+            for (int t = 0; t < 15; ++t)
+                if (gB[t] >= 0 && owner[gB[t]] == c) rows[gB[t]].push_back({cB[j], out[t]});
+        }
+    }
+    rp.assign(sf.n + 1, 0);
+    std::vector<std::vector<std::pair<int, double>>> fin(sf.n);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (i64 I = 0; I < sf.n; ++I) {
+        auto &R = rows[I];
+        std::sort(R.begin(), R.end(), [](const std::pair<int, dd> &x, const std::pair<int, dd> &y) { return x.first < y.first; });
+        std::vector<dd> xs(R.size());
+        for (size_t t = 0; t < R.size(); ++t) xs[t] = R[t].second;
+        std::vector<double> rounded(R.size());
+        round_row(xs.data(), (i64)xs.size(), rounded.data());
+        double mx = 0;
+        for (double v : rounded) mx = std::max(mx, std::fabs(v));
+        for (size_t t = 0; t < R.size(); ++t)
+            if (rounded[t] != 0.0 && std::fabs(to_double(xs[t])) >= std::ldexp(mx, -30)) fin[I].push_back({R[t].first, rounded[t]});
+    }
+    for (i64 I = 0; I < sf.n; ++I) rp[I + 1] = rp[I] + (i64)fin[I].size();
+    ci.resize(rp[sf.n]);
+    vv.resize(rp[sf.n]);
+    for (i64 I = 0; I < sf.n; ++I)
+        for (size_t t = 0; t < fin[I].size(); ++t) { ci[rp[I] + t] = fin[I][t].first; vv[rp[I] + t] = fin[I][t].second; }
+}
+
+}  // namespace k2d3
+
 }  // namespace
 
 std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params &p, const double *w,
@@ -2157,8 +2644,40 @@ std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params
     if ((block != 0 && block != 1) || (dim != 2 && dim != 3) || N < 1 || nlev < 1) return "bad arguments";
     if (N % (1 << (nlev - 1))) return "N not divisible by 2^(nlev-1)";
     if (p.degree != 1 && p.degree != 2) return "degree must be 1 or 2";
-    if (p.degree == 2 && dim != 2) return "degree 2 is built in 2D only (NEXT-2)";
+    if (p.degree == 2 && dim == 3 && block != 0) return "degree 2 in 3D is built for the E-B block only (NEXT-2)";
     out.assign(nlev, HostLevel());
+    if (p.degree == 2 && dim == 3) {
+        std::vector<Mesh> meshes(nlev);
+        std::vector<k2d3::Space3> spaces(nlev);
+        for (int l = nlev - 1; l >= 0; --l) {
+            const int Nl = N >> (nlev - 1 - l), step = 1 << (nlev - 1 - l);
+            Mesh &m = meshes[l];
+            build_mesh(m, dim, Nl);
+            k2d3::build_space3(spaces[l], m);
+            std::vector<double> pot(3 * m.nv);
+            for (i64 v = 0; v < m.nv; ++v) {
+                int q[3];
+                m.lat(v, q);
+                const i64 fv = q[0] * step + (i64)(N + 1) * (q[1] * step + (i64)(N + 1) * (q[2] * step));
+                for (int t = 0; t < 3; ++t) pot[3 * v + t] = w[3 * fv + t];
+            }
+            Pattern P;
+            std::vector<double> val;
+            k2d3::assemble_eb3(m, spaces[l], p, pot.data(), P, val);
+            HostLevel &H = out[l];
+            H.n = spaces[l].n;
+            H.rp = std::move(P.rp);
+            H.ci = std::move(P.ci);
+            H.v = std::move(val);
+            if (l > 0) k2d3::build_patches3(m, spaces[l], H.pptr, H.pdofs);
+        }
+        for (int l = 1; l < nlev; ++l) {
+            k2d3::build_prolongation3(meshes[l], spaces[l], meshes[l - 1], spaces[l - 1], out[l].prp, out[l].pci,
+                                      out[l].pv);
+            out[l].n_coarser = spaces[l - 1].n;
+        }
+        return "";
+    }
     if (p.degree == 2) {
         std::vector<Mesh> meshes(nlev);
         std::vector<Space2> spaces(nlev);

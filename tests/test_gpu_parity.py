@@ -22,7 +22,8 @@ CASES = [("c1", None, None, 0), ("c1", None, None, 1), ("c1", None, None, 2), ("
          ("c3", 64, 4, 0), ("c4", 16, 3, 0), ("c5", 6, 2, 0), ("c5", 8, 2, 1),
          ("c4-transient-picard", 8, 2, 0), ("c5-transient", 6, 2, 2), ("c5-lorentz", 6, 2, 3),
          ("c1-k2", None, None, 0), ("c2-k2", 64, 4, 1), ("c2-k2-transient-picard", 32, 3, 2),   # NEXT-2
-         ("c3-k2", 32, 4, 0), ("c3-k2-transient", 16, 3, 1), ("c3-k2-lorentz", 16, 3, 2)]
+         ("c3-k2", 32, 4, 0), ("c3-k2-transient", 16, 3, 1), ("c3-k2-lorentz", 16, 3, 2),
+         ("c4-k2", 4, 2, 0), ("c4-k2-transient-picard", 4, 2, 1)]                          # 3D k = 2
 
 
 def _setup(oracle_mod, name, N, L, seed):
