@@ -76,7 +76,7 @@ OCtx *orc_create_masked(int block, int dim, int N, int nlev, const double *dpara
     c->p.nu_pre = iparams[0]; c->p.nu_post = iparams[1];
     c->p.dt = dparams[7]; c->p.picard = iparams[2];
     int degree = iparams[3];
-    if (!(degree == 1 || (degree == 2 && (dim == 2 || block == ORC_EB)))) { free(c); return NULL; }
+    if (!(degree == 1 || degree == 2)) { free(c); return NULL; }
     c->degree = degree;
     c->lv = calloc((size_t)nlev, sizeof(OLevel));
     int lo = cmask_fine ? nlev - 1 : 0;

@@ -359,19 +359,20 @@ i64 oc_find(const OCsr *a, i64 row, int col) {
 /* free DoFs (with -1 for constrained) of the local basis of cell c, in local order */
 static int cell_dofs(const OMesh *m, const OSpace *s, i64 c, int *out) {
     int d = m->dim, n = 0;
-    if (s->degree == 2 && d == 3) {   /* NED1_2 (edges x 2, faces x 2) then RT2 (faces x 3, cell x 3) */
+    if (s->degree == 2 && d == 3 && s->block == ORC_EB) {   /* NED1_2 (edges x 2, faces x 2) then RT2 (faces x 3, cell x 3) */
         for (int q = 0; q < 6; q++) { int e0 = s->edof[m->ce[c * 6 + q]]; for (int a = 0; a < 2; a++) out[n++] = e0 < 0 ? -1 : e0 + a; }
         for (int q = 0; q < 4; q++) { int g0 = s->gdof[om_facet_of_cell(m, c, q)]; for (int a = 0; a < 2; a++) out[n++] = g0 < 0 ? -1 : g0 + a; }
         for (int q = 0; q < 4; q++) { int f0 = s->fdof[om_facet_of_cell(m, c, q)]; for (int a = 0; a < 3; a++) out[n++] = f0 < 0 ? -1 : f0 + a; }
         for (int a = 0; a < 3; a++) out[n++] = s->cdof[c] + a;
         return n;
     }
-    if (s->degree == 2 && s->block == ORC_VEL) {   /* BDM2: facets x 3, then cell x 3 */
-        for (int q = 0; q < 3; q++) {
+    if (s->degree == 2 && s->block == ORC_VEL) {   /* BDM2: facets x 3 (2D) / 6 (3D), then cell x 3 / 6 */
+        int per = d == 2 ? 3 : 6;
+        for (int q = 0; q <= d; q++) {
             int f0 = s->fdof[om_facet_of_cell(m, c, q)];
-            for (int a = 0; a < 3; a++) out[n++] = f0 < 0 ? -1 : f0 + a;
+            for (int a = 0; a < per; a++) out[n++] = f0 < 0 ? -1 : f0 + a;
         }
-        for (int a = 0; a < 3; a++) out[n++] = s->cdof[c] + a;
+        for (int a = 0; a < per; a++) out[n++] = s->cdof[c] + a;
         return n;
     }
     if (s->degree == 2) {             /* CG2 (vertices, edges) then RT2 (edges x 2, cell x 2) */
@@ -743,6 +744,8 @@ static void assemble_vel2(OCsr *A, Accum *S, const OMesh *m, const OSpace *s, co
                           const unsigned char *cmask);
 static void assemble_eb2_3d(OCsr *A, Accum *S, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
                             const unsigned char *cmask);
+static void assemble_vel2_3d(OCsr *A, Accum *S, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
+                             const unsigned char *cmask);
 
 int oa_assemble_masked(OCsr *A, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
                        const unsigned char *cmask) {
@@ -750,7 +753,8 @@ int oa_assemble_masked(OCsr *A, const OMesh *m, const OSpace *s, const OParams *
     if (s->degree == 2) {
         Accum S2;
         S2.acc = calloc((size_t)(A->nnz ? A->nnz : 1), sizeof(real));
-        if (s->block == ORC_VEL) assemble_vel2(A, &S2, m, s, p, w, cmask);
+        if (s->block == ORC_VEL && m->dim == 3) assemble_vel2_3d(A, &S2, m, s, p, w, cmask);
+        else if (s->block == ORC_VEL) assemble_vel2(A, &S2, m, s, p, w, cmask);
         else if (m->dim == 3) assemble_eb2_3d(A, &S2, m, s, p, w, cmask);
         else assemble_eb2(A, &S2, m, s, p, w, cmask);
         finish(A, &S2);
@@ -1351,7 +1355,7 @@ static void rt2_functionals(const Cell *K, int Ncells, const Q2 *f, real *out) {
 
 /* Gauss-Jordan inverse with partial pivoting (n <= 20), row-major */
 static int mat_inv(int n, const real *a, real *inv) {
-    real w[20][40];
+    real w[30][60];
     for (int i = 0; i < n; i++)
         for (int j = 0; j < 2 * n; j++) w[i][j] = j < n ? a[i * n + j] : (real)(j - n == i);
     for (int k = 0; k < n; k++) {
@@ -2151,6 +2155,215 @@ static real dof_functional3(const OMesh *mf, const OSpace *sf, i64 I, const Q3 *
     return acc;
 }
 
+/* ========================================================================= */
+/* NEXT-2 in 3D, AL velocity block: BDM2.  Reading            */
+/* R-basis2-vel in 3D: per face f (vertices a < b < c, area vector A = |f| n_f */
+/* of R-orient) N_{f,s}(u) = u(x_s) . A at x_0..2 = x_a, x_b, x_c, x_3 = mid(a,b),*/
+/* x_4 = mid(a,c), x_5 = mid(b,c) (the P2 nodes of the face); per cell         */
+/* N_{K,e}(u) = int_K u . (lam_i grad lam_j - lam_j grad lam_i) for the 6 edges */
+/* e = (i < j) in the local order (0,1) (0,2) (0,3) (1,2) (1,3) (2,3).  Local  */
+/* basis dual to these, from the monomial basis of P2^3 (inverted in `real`).  */
+/* ========================================================================= */
+static void face_nodes(const real P[3][3], real X[6][3]) {
+    for (int k = 0; k < 3; k++) {
+        X[0][k] = P[0][k]; X[1][k] = P[1][k]; X[2][k] = P[2][k];
+        X[3][k] = (P[0][k] + P[1][k]) / 2; X[4][k] = (P[0][k] + P[2][k]) / 2; X[5][k] = (P[1][k] + P[2][k]) / 2;
+    }
+}
+
+static void whitney3_at(const Cell *K, int e, const real *x, real *out) {
+    int lv[2];
+    om_edge_local_verts(3, e, lv);
+    real li = bary3_at(K, lv[0], x), lj = bary3_at(K, lv[1], x);
+    for (int r = 0; r < 3; r++) out[r] = li * K->g[lv[1]][r] - lj * K->g[lv[0]][r];
+}
+
+/* the 30 BDM2 functionals of cell K (local order: face q = 0..3 x s = 0..5, then e) */
+static void bdm2_3d_functionals(const Cell *K, const Q3 *f, real *out) {
+    for (int q = 0; q < 4; q++) {
+        real P[3][3], A[3], X[6][3], v[3];
+        facet_points(K, q, P);
+        facet_area_vector(3, P, A);
+        face_nodes(P, X);
+        for (int s = 0; s < 6; s++) { q3_eval(f, K, X[s], v); out[6 * q + s] = dot3(v, A); }
+    }
+    real xq[64][3], wq[64];
+    int nq = cell_rule(K, 3, xq, wq);      /* degree 3: exact in 3D (R-quad) */
+    for (int e = 0; e < 6; e++) {
+        real acc = 0;
+        for (int t = 0; t < nq; t++) {
+            real v[3], om[3];
+            q3_eval(f, K, xq[t], v);
+            whitney3_at(K, e, xq[t], om);
+            acc += wq[t] * dot3(v, om);
+        }
+        out[24 + e] = acc;
+    }
+}
+
+static void basis_bdm2_3d(const Cell *K, Q3 *B) {
+    Q3 p[30];
+    memset(p, 0, sizeof p);
+    for (int l = 0; l < 3; l++) for (int k = 0; k < 10; k++) p[10 * l + k].c[l][k] = 1;
+    real M[900], C[900], col[30];
+    for (int j = 0; j < 30; j++) {
+        bdm2_3d_functionals(K, &p[j], col);
+        for (int i = 0; i < 30; i++) M[i * 30 + j] = col[i];
+    }
+    mat_inv(30, M, C);
+    for (int j = 0; j < 30; j++) {
+        memset(&B[j], 0, sizeof(Q3));
+        for (int k = 0; k < 30; k++)
+            for (int l = 0; l < 3; l++)
+                for (int t = 0; t < 10; t++) B[j].c[l][t] += C[k * 30 + j] * p[k].c[l][t];
+    }
+}
+
+/* AL velocity block at k = 2 in 3D: the forms of assemble_vel2 (R-vel) with
+ * 3-vectors; cell integrals by the 4-point collapsed rule (degree 4, R-quad), facet
+ * integrals by the collapsed 3x3 triangle rule (degree 4); h_F = longest face edge, as
+ * the k = 1 3D assembly. */
+static void assemble_vel2_3d(OCsr *A, Accum *S, const OMesh *m, const OSpace *s, const OParams *p, const double *w,
+                             const unsigned char *cmask) {
+    real xq[64][3], wq[64];
+    const real nu2 = (real)2 / p->Re;
+    static real loc[900], floc[3600];
+    for (i64 c = 0; c < m->nc; c++) {
+        if (cmask && !cmask[c]) continue;
+        Cell K;
+        cell_geom(m, c, &K);
+        Q3 F[30];
+        int gi[30];
+        basis_bdm2_3d(&K, F);
+        cell_dofs(m, s, c, gi);
+        double pot[4][3];
+        real wx[3], bx[3] = {0, 0, 0};
+        cell_pot(m, c, w, pot);
+        cell_wind(&K, pot, wx);
+        if (p->bn) { double bp[4][3]; cell_pot(m, c, p->bn, bp); cell_wind(&K, bp, bx); }
+        memset(loc, 0, sizeof(loc));
+        int nq = cell_rule(&K, 4, xq, wq);
+        for (int t = 0; t < nq; t++) {
+            real fv[30][3], ep[30][3][3], dv[30], gw[30][3];
+            for (int a = 0; a < 30; a++) {
+                real G[3][3];
+                q3_eval(&F[a], &K, xq[t], fv[a]);
+                q3_grad(&F[a], &K, xq[t], G);
+                for (int l = 0; l < 3; l++) for (int k = 0; k < 3; k++) ep[a][l][k] = (G[l][k] + G[k][l]) / 2;
+                dv[a] = G[0][0] + G[1][1] + G[2][2];
+                for (int l = 0; l < 3; l++) gw[a][l] = G[l][0] * wx[0] + G[l][1] * wx[1] + G[l][2] * wx[2];
+            }
+            for (int i = 0; i < 30; i++)
+                for (int j = 0; j < 30; j++) {
+                    real ee = 0;
+                    for (int l = 0; l < 3; l++) for (int k = 0; k < 3; k++) ee += ep[j][l][k] * ep[i][l][k];
+                    real v = nu2 * ee - dot3(fv[j], gw[i]) + (real)p->gamma * dv[j] * dv[i];
+                    if (p->dt > 0) v += dot3(fv[j], fv[i]) / p->dt;
+                    if (p->bn) { real cj[3], ci[3]; cross3(fv[j], bx, cj); cross3(fv[i], bx, ci); v += p->S * dot3(cj, ci); }
+                    loc[i * 30 + j] += wq[t] * v;
+                }
+        }
+        scatter(A, S, gi, 30, gi, 30, loc, 30);
+    }
+    for (i64 f = 0; f < m->nfacet; f++) {
+        int cp = m->fcell[2 * f], cm = m->fcell[2 * f + 1];
+        if (cmask && !cmask[cp] && !(cm >= 0 && cmask[cm])) continue;
+        int interior = cm >= 0, nb = 30;
+        Cell Kp, Km;
+        Q3 F[60];
+        int gi[60], side[60];
+        cell_geom(m, cp, &Kp);
+        basis_bdm2_3d(&Kp, F);
+        cell_dofs(m, s, cp, gi);
+        for (int a = 0; a < 30; a++) side[a] = +1;
+        if (interior) {
+            cell_geom(m, cm, &Km);
+            basis_bdm2_3d(&Km, F + 30);
+            cell_dofs(m, s, cm, gi + 30);
+            for (int a = 30; a < 60; a++) side[a] = -1;
+            nb = 60;
+        }
+        int qf = -1;
+        for (int q = 0; q < 4; q++) if (om_facet_of_cell(m, cp, q) == f) qf = q;
+        real P[3][3], Av[3];
+        facet_points(&Kp, qf, P);
+        facet_area_vector(3, P, Av);
+        real an = RSQRT(dot3(Av, Av)), n[3];
+        double sgn = facet_sign(&Kp, qf, Av);
+        for (int k = 0; k < 3; k++) n[k] = sgn * Av[k] / an;
+        real hF = 0;
+        for (int a = 0; a < 3; a++)
+            for (int b = a + 1; b < 3; b++) {
+                real t[3] = {P[b][0] - P[a][0], P[b][1] - P[a][1], P[b][2] - P[a][2]};
+                real l = RSQRT(dot3(t, t));
+                if (l > hF) hF = l;
+            }
+        real avg = interior ? (real)1 / 2 : (real)1;
+        real pen = (real)p->sigma / ((real)p->Re * hF);
+        double pot[4][3];
+        real wx[3];
+        cell_pot(m, cp, w, pot);
+        cell_wind(&Kp, pot, wx);
+        real wn = dot3(wx, n), awn = RFABS(wn);
+        memset(floc, 0, sizeof(floc));
+        int nq = facet_rule(3, P, xq, wq);
+        for (int t = 0; t < nq; t++) {
+            real fv[60][3], en[60][3];
+            for (int a = 0; a < nb; a++) {
+                const Cell *Ka = side[a] > 0 ? &Kp : &Km;
+                real G[3][3];
+                q3_eval(&F[a], Ka, xq[t], fv[a]);
+                q3_grad(&F[a], Ka, xq[t], G);
+                for (int l = 0; l < 3; l++) {
+                    real acc = 0;
+                    for (int k = 0; k < 3; k++) acc += (G[l][k] + G[k][l]) / 2 * n[k];
+                    en[a][l] = acc;
+                }
+            }
+            for (int i = 0; i < nb; i++) {
+                real Ji = side[i];
+                for (int j = 0; j < nb; j++) {
+                    real Jj = side[j];
+                    real vv = dot3(fv[j], fv[i]);
+                    real t1 = -nu2 * avg * dot3(en[j], fv[i]) * Ji;
+                    real t2 = -nu2 * avg * dot3(fv[j], en[i]) * Jj;
+                    real t3 = pen * Jj * Ji * vv;
+                    real up;
+                    if (interior) up = (side[j] > 0 ? (wn + awn) / 2 : -(-wn + awn) / 2) * vv * Ji;
+                    else up = (wn + awn) / 2 * vv;
+                    floc[i * 60 + j] += wq[t] * (t1 + t2 + t3 + up);
+                }
+            }
+        }
+        scatter(A, S, gi, nb, gi, nb, floc, 60);
+    }
+}
+
+/* the fine BDM2 functional of free DoF I (3D) applied to F living on coarse cell Kc */
+static real dof_functional_v3(const OMesh *mf, const OSpace *sf, i64 I, const Q3 *F, const Cell *Kc) {
+    int kind = sf->dkind[I], ent = sf->dent[I], sub = sf->dsub[I];
+    real v[3];
+    if (kind == 2) {
+        real P[3][3], A[3], X[6][3];
+        for (int a = 0; a < 3; a++)
+            for (int k = 0; k < 3; k++) P[a][k] = (real)mf->lat[3 * mf->fv[3 * ent + a] + k] / mf->N;
+        facet_area_vector(3, P, A);
+        face_nodes(P, X);
+        q3_eval(F, Kc, X[sub], v);
+        return dot3(v, A);
+    }
+    Cell Kf;
+    cell_geom(mf, ent, &Kf);
+    real xq[64][3], wq[64], om[3], acc = 0;
+    int nq = cell_rule(&Kf, 3, xq, wq);
+    for (int t = 0; t < nq; t++) {
+        q3_eval(F, Kc, xq[t], v);
+        whitney3_at(&Kf, sub, xq[t], om);
+        acc += wq[t] * dot3(v, om);
+    }
+    return acc;
+}
+
 static int op_prolongation3(OCsr *P, const OMesh *mf, const OSpace *sf, const OMesh *mc, const OSpace *sc) {
     memset(P, 0, sizeof(*P));
     int *efirst = malloc(sizeof(int) * mf->ne), *ffirst = malloc(sizeof(int) * mf->nfacet);
@@ -2169,6 +2382,19 @@ static int op_prolongation3(OCsr *P, const OMesh *mf, const OSpace *sf, const OM
         i64 ccell = parent_cell(mf, mc, cf);
         Cell Kc;
         cell_geom(mc, ccell, &Kc);
+        if (sf->block == ORC_VEL) {                      /* BDM2: all 30 coarse functions */
+            Q3 Fv[30];
+            int gv[30];
+            basis_bdm2_3d(&Kc, Fv);
+            cell_dofs(mc, sc, ccell, gv);
+            for (int b = 0; b < 30; b++) {
+                if (gv[b] < 0) continue;
+                real val = dof_functional_v3(mf, sf, I, &Fv[b], &Kc);
+                if (nt == cap) { cap *= 2; idx = realloc(idx, sizeof(long long) * 3 * cap); tv = realloc(tv, sizeof(real) * cap); }
+                idx[3 * nt] = I; idx[3 * nt + 1] = gv[b]; idx[3 * nt + 2] = nt; tv[nt] = val; nt++;
+            }
+            continue;
+        }
         Q3 F[20];
         int gE[20], gB[15], nb;
         const int *gJ;
@@ -2213,7 +2439,80 @@ static int op_prolongation3(OCsr *P, const OMesh *mf, const OSpace *sf, const OM
     return 0;
 }
 
+static void oa_load3v(const OMesh *m, const OSpace *s, const double *fv, double *out) {
+    int nq = oa_nq(3), nc = oa_ncomp(s);
+    real xq[64][3], wq[64];
+    memset(out, 0, sizeof(double) * s->n);
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        Q3 F[30];
+        int g[30];
+        basis_bdm2_3d(&K, F);
+        cell_dofs(m, s, c, g);
+        cell_rule(&K, 4, xq, wq);
+        for (int a = 0; a < 30; a++) {
+            if (g[a] < 0) continue;
+            real acc = 0;
+            for (int t = 0; t < nq; t++) {
+                real v[3];
+                q3_eval(&F[a], &K, xq[t], v);
+                const double *f = fv + ((i64)c * nq + t) * nc;
+                acc += wq[t] * (f[0] * v[0] + f[1] * v[1] + f[2] * v[2]);
+            }
+            out[g[a]] += (double)acc;
+        }
+    }
+}
+
+static void oa_eval3v(const OMesh *m, const OSpace *s, const double *coef, double *fv) {
+    int nq = oa_nq(3), nc = oa_ncomp(s);
+    real xq[64][3], wq[64];
+    memset(fv, 0, sizeof(double) * m->nc * nq * nc);
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        Q3 F[30];
+        int g[30];
+        basis_bdm2_3d(&K, F);
+        cell_dofs(m, s, c, g);
+        cell_rule(&K, 4, xq, wq);
+        for (int a = 0; a < 30; a++) {
+            if (g[a] < 0) continue;
+            for (int t = 0; t < nq; t++) {
+                real v[3];
+                q3_eval(&F[a], &K, xq[t], v);
+                double *f = fv + ((i64)c * nq + t) * nc;
+                for (int k = 0; k < 3; k++) f[k] += coef[g[a]] * (double)v[k];
+            }
+        }
+    }
+}
+
+static double oa_duality_error3v(const OMesh *m, const OSpace *s) {
+    double worst = 0;
+    for (i64 c = 0; c < m->nc; c++) {
+        Cell K;
+        cell_geom(m, c, &K);
+        Q3 F[30];
+        int g[30];
+        basis_bdm2_3d(&K, F);
+        cell_dofs(m, s, c, g);
+        for (int i = 0; i < 30; i++) {
+            if (g[i] < 0) continue;
+            for (int j = 0; j < 30; j++) {
+                if (g[j] < 0) continue;
+                double v = (double)dof_functional_v3(m, s, g[i], &F[j], &K);
+                double e = fabs(v - (g[i] == g[j] ? 1.0 : 0.0));
+                if (e > worst) worst = e;
+            }
+        }
+    }
+    return worst;
+}
+
 static void oa_load3(const OMesh *m, const OSpace *s, const double *fv, double *out) {
+    if (s->block == ORC_VEL) { oa_load3v(m, s, fv, out); return; }
     int nq = oa_nq(3), nc = oa_ncomp(s);
     real xq[64][3], wq[64];
     memset(out, 0, sizeof(double) * s->n);
@@ -2242,6 +2541,7 @@ static void oa_load3(const OMesh *m, const OSpace *s, const double *fv, double *
 }
 
 static void oa_eval3(const OMesh *m, const OSpace *s, const double *coef, double *fv) {
+    if (s->block == ORC_VEL) { oa_eval3v(m, s, coef, fv); return; }
     int nq = oa_nq(3), nc = oa_ncomp(s);
     real xq[64][3], wq[64];
     memset(fv, 0, sizeof(double) * m->nc * nq * nc);
@@ -2268,6 +2568,7 @@ static void oa_eval3(const OMesh *m, const OSpace *s, const double *coef, double
 }
 
 static double oa_duality_error3(const OMesh *m, const OSpace *s) {
+    if (s->block == ORC_VEL) return oa_duality_error3v(m, s);
     double worst = 0;
     for (i64 c = 0; c < m->nc; c++) {
         Cell K;

@@ -28,17 +28,18 @@ static int os_build2_vel(OSpace *s, const OMesh *m) {
     for (i64 v = 0; v < m->nv; v++) s->vdof[v] = -1;
     for (i64 e = 0; e < m->ne; e++) s->edof[e] = -1;
     i64 n = 0;
-    for (i64 f = 0; f < m->nfacet; f++) { s->fdof[f] = m->fcell[2 * f + 1] >= 0 ? (int)n : -1; if (s->fdof[f] >= 0) n += 3; }
-    for (i64 c = 0; c < m->nc; c++) { s->cdof[c] = (int)n; n += 3; }
+    const int per = m->dim == 2 ? 3 : 6;      /* P2 on a facet: 3 (edge) / 6 (triangle); cell: 3 / 6 */
+    for (i64 f = 0; f < m->nfacet; f++) { s->fdof[f] = m->fcell[2 * f + 1] >= 0 ? (int)n : -1; if (s->fdof[f] >= 0) n += per; }
+    for (i64 c = 0; c < m->nc; c++) { s->cdof[c] = (int)n; n += per; }
     s->n = n;
     s->dkind = malloc(sizeof(int) * (n ? n : 1));
     s->dent = malloc(sizeof(int) * (n ? n : 1));
     s->dsub = malloc(sizeof(int) * (n ? n : 1));
     for (i64 f = 0; f < m->nfacet; f++)
         if (s->fdof[f] >= 0)
-            for (int a = 0; a < 3; a++) { s->dkind[s->fdof[f] + a] = 2; s->dent[s->fdof[f] + a] = (int)f; s->dsub[s->fdof[f] + a] = a; }
+            for (int a = 0; a < per; a++) { s->dkind[s->fdof[f] + a] = 2; s->dent[s->fdof[f] + a] = (int)f; s->dsub[s->fdof[f] + a] = a; }
     for (i64 c = 0; c < m->nc; c++)
-        for (int a = 0; a < 3; a++) { s->dkind[s->cdof[c] + a] = 3; s->dent[s->cdof[c] + a] = (int)c; s->dsub[s->cdof[c] + a] = a; }
+        for (int a = 0; a < per; a++) { s->dkind[s->cdof[c] + a] = 3; s->dent[s->cdof[c] + a] = (int)c; s->dsub[s->cdof[c] + a] = a; }
     return 0;
 }
 
@@ -111,7 +112,7 @@ int os_build(OSpace *s, const OMesh *m, int block, int degree) {
     memset(s, 0, sizeof(*s));
     s->block = block; s->dim = m->dim; s->degree = degree;
     if (degree == 2) {
-        if (m->dim == 3) return block == ORC_EB ? os_build2_eb3(s, m) : 1;
+        if (m->dim == 3) return block == ORC_EB ? os_build2_eb3(s, m) : os_build2_vel(s, m);
         return block == ORC_EB ? os_build2(s, m) : os_build2_vel(s, m);
     }
     if (degree != 1) return 1;
@@ -207,7 +208,7 @@ int opt_build(OPatches *pt, const OMesh *m, const OSpace *s) {
             i64 c = vc[t];
             /* all free DoFs of cell c */
             int cand[64]; int nc = 0;
-            if (s->degree == 2 && m->dim == 3) {              /* NED1_2 x RT2 (3D) */
+            if (s->degree == 2 && m->dim == 3 && s->block == ORC_EB) {   /* NED1_2 x RT2 (3D) */
                 for (int q = 0; q < 6; q++) { int d = s->edof[m->ce[c * 6 + q]]; if (d >= 0) { cand[nc++] = d; cand[nc++] = d + 1; } }
                 for (int q = 0; q < 4; q++) {
                     int f = om_facet_of_cell(m, c, q);
@@ -215,12 +216,13 @@ int opt_build(OPatches *pt, const OMesh *m, const OSpace *s) {
                     if (s->fdof[f] >= 0) for (int a = 0; a < 3; a++) cand[nc++] = s->fdof[f] + a;
                 }
                 for (int a = 0; a < 3; a++) cand[nc++] = s->cdof[c] + a;
-            } else if (s->degree == 2 && s->block == ORC_VEL) {   /* BDM2 (2D) */
-                for (int q = 0; q < 3; q++) {
+            } else if (s->degree == 2 && s->block == ORC_VEL) {   /* BDM2: 3 (2D) / 6 (3D) per facet and cell */
+                int per = m->dim == 2 ? 3 : 6;
+                for (int q = 0; q < nvc; q++) {
                     int d = s->fdof[om_facet_of_cell(m, c, q)];
-                    if (d >= 0) { cand[nc++] = d; cand[nc++] = d + 1; cand[nc++] = d + 2; }
+                    if (d >= 0) for (int a = 0; a < per; a++) cand[nc++] = d + a;
                 }
-                for (int a = 0; a < 3; a++) cand[nc++] = s->cdof[c] + a;
+                for (int a = 0; a < per; a++) cand[nc++] = s->cdof[c] + a;
             } else if (s->degree == 2) {                    /* CG2 x RT2 (2D) */
                 for (int q = 0; q < 3; q++) { int d = s->vdof[m->cv[c * 3 + q]]; if (d >= 0) cand[nc++] = d; }
                 for (int q = 0; q < 3; q++) { int d = s->edof[m->ce[c * 3 + q]]; if (d >= 0) cand[nc++] = d; }

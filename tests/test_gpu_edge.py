@@ -78,7 +78,7 @@ def test_patch_too_large_rejected():
     cfg = workloads.small("c1", 4, 2)
     ctx = _ctx()
     ctx.begin_levels(2, cfg)
-    n0, n = 3, 200
+    n0, n = 3, 400                              # one star above K2_MAX_N = 384
     ctx.load_level(0, np.arange(n0 + 1), np.arange(n0, dtype=np.int32), np.ones(n0))
     rp = np.arange(n + 1)
     P_rp = np.arange(n + 1)

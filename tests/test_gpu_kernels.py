@@ -17,7 +17,7 @@ from gpu_helpers import bits, cuda_vec, host, load_oracle_levels, rel_l2
 pytestmark = pytest.mark.gpu
 
 CASES = [("c1", 8, 2), ("c2", 32, 3), ("c3", 16, 3), ("c4", 8, 2), ("c5", 6, 2), ("c2-k2", 32, 3), ("c3-k2", 16, 3),
-         ("c4-k2", 4, 2)]
+         ("c4-k2", 4, 2), ("c5-k2", 4, 2)]
 
 
 @pytest.fixture(scope="module", params=CASES, ids=[f"{c}-N{n}L{l}" for c, n, l in CASES])
@@ -26,8 +26,8 @@ def pair(request, oracle_mod):
     from paper_2104_14855_b200 import mhdp, workloads
     name, N, L = request.param
     import dataclasses
-    k2 = name.endswith("-k2")                       # NEXT-2: CG2 x RT2 (31-DoF stars), BDM2,
-    cfg = workloads.small(name.replace("-k2", ""), N, L)   # 3D NED1_2 x RT2 (280-DoF stars)
+    k2 = name.endswith("-k2")                       # NEXT-2: CG2 x RT2 (31-DoF stars), BDM2, 3D
+    cfg = workloads.small(name.replace("-k2", ""), N, L)   # NED1_2 x RT2 (280) and BDM2 (360 DoFs)
     if k2:
         cfg = dataclasses.replace(cfg, degree=2, sigma=40.0 if cfg.block == "vel" else cfg.sigma)
         if cfg.dim == 3:                            # Newton at Rem = S = 1e3 needs the GMRES(6)

@@ -359,3 +359,108 @@ def test_k2_3d_picard_multigrid(oracle_mod):
         _, k, _, conv = o.fgmres(b, maxit=40)
         its.append(k if conv else None)
     assert None not in its and max(its) <= 10, its
+
+
+# ---------------- k = 2 in 3D, AL velocity block: BDM2, sigma = 40 ----------------
+def _v3(N, L, **kw):
+    base = dict(degree=2, sigma=40.0)
+    base.update(kw)
+    return dataclasses.replace(small("c5", N, L), **base)
+
+
+@pytest.mark.parametrize("N", [2, 3])
+def test_k2_3d_velocity_counts(oracle_mod, N):
+    """BDM2 on tetrahedra: 6 DoFs per interior face (P2 normal traces) + 6 per cell;
+    interior faces 12N^3 - 6N^2, cells 6N^3, so n = 108N^3 - 36N^2.  An interior star has
+    36 faces x 6 + 24 cells x 6 = 360 DoFs ("3D BDM2 star ~ 360")."""
+    cfg = _v3(N, 1)
+    o = oracle_mod.Oracle(cfg, draw(cfg, 1, 0)[0])
+    assert o.n() == 108 * N ** 3 - 36 * N ** 2
+    assert np.diff(o.patches()[0]).max() == 360
+
+
+def test_k2_3d_velocity_patches_brute_force(oracle_mod):
+    """Star of v = DoFs whose support (the cells of the DoF's face or cell) lies in the
+    cells around v, from the mesh alone."""
+    cfg = _v3(3, 1)
+    o = oracle_mod.Oracle(cfg, draw(cfg, 1, 0)[0])
+    m = o.mesh()
+    cells_of_vertex = [set() for _ in range(m["x"].shape[0])]
+    for c, vs in enumerate(m["cv"]):
+        for v in vs:
+            cells_of_vertex[v].add(c)
+    support = []
+    for d in range(o.n()):
+        k, e = m["dkind"][d], m["dent"][d]
+        if k == 2:
+            a, b, c = m["fv"][e]
+            support.append(cells_of_vertex[a] & cells_of_vertex[b] & cells_of_vertex[c])
+        else:
+            support.append({e})
+    ptr, dofs, vert, _ = o.patches()
+    got = {int(vert[i]): sorted(dofs[ptr[i]:ptr[i + 1]].tolist()) for i in range(len(vert))}
+    want = {v: sorted(d for d in range(o.n()) if support[d] <= cells_of_vertex[v]) for v in range(m["x"].shape[0])}
+    assert got == {v: s for v, s in want.items() if s}
+
+
+def test_k2_3d_velocity_duality(oracle_mod):
+    cfg = _v3(4, 2)
+    o = oracle_mod.Oracle(cfg, draw(cfg, 1, 0)[0])
+    assert o.duality_error() <= 1e-12 and o.duality_error(0) <= 1e-12
+    cfg = _v3(2, 1)
+    assert oracle_mod.Oracle(cfg, draw(cfg, 1, 0)[0], exact=True).duality_error() <= 1e-28
+
+
+def test_k2_3d_velocity_mms_rate(oracle_mod):
+    """BDM2 with SIPG (sigma = 40) in 3D: L2 rate 3 for u (k = 1: 2); measured 3.05 at
+    N = 3 -> 6 (2.78 at 2 -> 4, pre-asymptotic)."""
+    wc = [1.0, 0.5, -0.3]
+    base = dataclasses.replace(CONFIGS["c5"], Re=1.0, Rem=1.0, S=1.0, gamma=1.0, levels=1, degree=2, sigma=40.0)
+    fs, ex = mms.vel_fields(3, 1.0, wc)
+    errs = [mms.solve_and_error(oracle_mod.Oracle(dataclasses.replace(base, N=N),
+                                                  mms.constant_wind_potential(3, N, wc)), fs, ex) for N in (3, 6)]
+    r = np.log(errs[0] / errs[1]) / np.log(2.0)
+    assert r.min() >= 2.9, r
+
+
+def test_k2_3d_velocity_symmetry_and_advection_coercive(oracle_mod):
+    """Without advection the 3D BDM2 operator is symmetric positive definite; the upwind
+    advection adds a positive semi-definite symmetric part."""
+    cfg = _v3(2, 1, Re=3.0, gamma=7.0)
+    w = draw(cfg, 1, 0)[0]
+    A0 = oracle_mod.Oracle(cfg, w * 0.0).csr().to_scipy().toarray()
+    A1 = oracle_mod.Oracle(cfg, w).csr().to_scipy().toarray()
+    assert np.abs(A0 - A0.T).max() <= 1e-13 * np.abs(A0).max()
+    assert np.linalg.eigvalsh(0.5 * (A0 + A0.T)).min() > 0
+    D = A1 - A0
+    assert np.abs(D).max() > 0
+    assert np.linalg.eigvalsh(0.5 * (D + D.T)).min() >= -1e-10 * np.abs(D).max()
+
+
+def test_k2_3d_velocity_galerkin_identity_volume_terms(oracle_mod):
+    """Nested 3D BDM2 spaces: the conforming gamma (div u, div v) term satisfies
+    A_c = P^T A_f P (Re -> inf removes the DG terms, w = 0); measured 8e-13."""
+    cfg = _v3(4, 2, Re=1e14, gamma=3.0)
+    o = oracle_mod.Oracle(cfg, draw(cfg, 1, 0)[0] * 0.0)
+    Af = o.csr(1).to_scipy()
+    Ac = o.csr(0).to_scipy().toarray()
+    P = o.prolongation(1).to_scipy(o.n(0))
+    assert np.abs((P.T @ Af @ P).toarray() - Ac).max() <= 1e-11 * np.abs(Ac).max()
+
+
+def test_k2_3d_velocity_multigrid_gamma_robust(oracle_mod):
+    """3D BDM2 star multigrid (360-DoF stars): FGMRES(GMRES(6)-smoothed V) counts do not
+    grow with gamma; point-Jacobi patches do not converge."""
+    its, ctrl = [], []
+    for g in (1e2, 1e6):
+        cfg = _v3(4, 2, Re=1.0, gamma=g)
+        o = oracle_mod.Oracle(cfg, draw(cfg, 1, 0)[0])
+        o.set_smoother("gmres", 6)
+        b = np.random.default_rng(0).uniform(-1, 1, o.n())
+        _, k, _, conv = o.fgmres(b, maxit=40)
+        its.append(k if conv else None)
+        o.set_patches(np.arange(o.n(1) + 1, dtype=np.int64), np.arange(o.n(1), dtype=np.int32), 1)
+        _, k, _, conv = o.fgmres(b, maxit=40)
+        ctrl.append(k if conv else None)
+    assert None not in its and max(its) - min(its) <= 1 and max(its) <= 15, its
+    assert ctrl == [None, None], ctrl
