@@ -2635,6 +2635,438 @@ void build_prolongation3(const Mesh &mf, const Space3 &sf, const Mesh &mc, const
         for (size_t t = 0; t < fin[I].size(); ++t) { ci[rp[I] + t] = fin[I][t].first; vv[rp[I] + t] = fin[I][t].second; }
 }
 
+
+// ---------------- k = 2 AL velocity block in 3D: BDM2 (R-basis2-vel in 3D, NEXT-2) ---------
+// DoFs: per face f (vertices a < b < c, area vector A of R-orient) N_{f,s}(u) = u(x_s) . A
+// at the P2 nodes x_0..2 = x_a, x_b, x_c, x_3 = mid(a,b), x_4 = mid(a,c), x_5 = mid(b,c);
+// per cell N_{K,e}(u) = int_K u . (lam_i g_j - lam_j g_i), e = (i < j) in LE order.
+// Free DoFs: 6 per interior face (face order), then 6 per cell.  Primal basis
+// lam_a lam_b e_r (30), dual by the double-double Gauss-Jordan.  Forms of R-vel with
+// closed-form cell (6|K| beta!/(|beta|+3)!) and face (2|f| beta!/(|beta|+2)!) moments;
+// h_F = longest face edge, as the k = 1 3D assembly.
+struct SpaceV3 {
+    i64 n = 0;
+    std::vector<int> fdof, cdof;
+};
+
+void build_space_v3(SpaceV3 &s, const Mesh &m) {
+    s.fdof.assign(m.nf, -1); s.cdof.assign(m.nc, -1);
+    i64 n = 0;
+    for (i64 f = 0; f < m.nf; ++f) if (!m.common_bnd(&m.fv[3 * f], 3)) { s.fdof[f] = (int)n; n += 6; }
+    for (i64 c = 0; c < m.nc; ++c) { s.cdof[c] = (int)n; n += 6; }
+    s.n = n;
+}
+
+// local order: face q (opposite vertex q) x s = 0..5, then e = 0..5
+void cell_dofs_v3(const Mesh &m, const SpaceV3 &s, i64 c, int *g) {
+    for (int q = 0; q < 4; ++q) {
+        const int f0 = s.fdof[m.cfacet[4 * c + q]];
+        for (int t = 0; t < 6; ++t) g[6 * q + t] = f0 < 0 ? -1 : f0 + t;
+    }
+    for (int e = 0; e < 6; ++e) g[24 + e] = s.cdof[c] + e;
+}
+
+static const int FP[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};   // face pairs
+static const int NODE[6][2] = {{0, 0}, {1, 1}, {2, 2}, {0, 1}, {0, 2}, {1, 2}};  // P2 face nodes
+
+void bdm3_fun(const GeoT<dd> &G, const Q &F, dd *out) {
+    const Tabs &T = tabs();
+    for (int q = 0; q < 4; ++q) {
+        dd A[3];
+        int fl[3];
+        facet_area(G, q, A, fl);
+        for (int s = 0; s < 6; ++s) {
+            const int x = fl[NODE[s][0]], y = fl[NODE[s][1]];
+            dd u[3];
+            if (x == y) for (int r = 0; r < 3; ++r) u[r] = F.c[PID[x][x]][r];
+            else
+                for (int r = 0; r < 3; ++r) u[r] = (F.c[PID[x][x]][r] + F.c[PID[x][y]][r] + F.c[PID[y][y]][r]) * dd(0.25);
+            out[6 * q + s] = dot3(u, A);
+        }
+    }
+    for (int e = 0; e < 6; ++e) {
+        const int i = LE[e][0], j = LE[e][1];
+        dd acc(0.0);
+        for (int p = 0; p < 10; ++p)
+            acc += dot3(F.c[p], G.g[j]) * T.m3[p][i] - dot3(F.c[p], G.g[i]) * T.m3[p][j];
+        out[24 + e] = acc * dd(6.0) * G.vol;
+    }
+}
+
+struct ElemV3 {
+    GeoT<dd> G;
+    Q V[30];
+    dd Gr[30][4][3][3];      // grad (row l = component, col k = direction) = sum_c lam_c Gr[c]
+};
+
+void elemv3(const Mesh &m, i64 c, ElemV3 &K) {
+    cell_geo(m, c, K.G);
+    const GeoT<dd> &G = K.G;
+    Q p[30];
+    memset((void *)p, 0, sizeof p);
+    for (int pp = 0; pp < 10; ++pp)
+        for (int r = 0; r < 3; ++r) p[3 * pp + r].c[pp][r] = dd(1.0);
+    dualize<30>(p, [&](const Q &F, dd *out) { bdm3_fun(G, F, out); }, K.V);
+    memset((void *)K.Gr, 0, sizeof K.Gr);
+    for (int j = 0; j < 30; ++j)
+        for (int pp = 0; pp < 10; ++pp) {
+            const int a = PA[pp][0], b = PA[pp][1];
+            for (int l = 0; l < 3; ++l)
+                for (int k = 0; k < 3; ++k) {
+                    K.Gr[j][b][l][k] += K.V[j].c[pp][l] * G.g[a][k];
+                    K.Gr[j][a][l][k] += K.V[j].c[pp][l] * G.g[b][k];
+                }
+        }
+}
+
+// row li of the cell matrix (test li, trial j = 0..29), without 6|K|
+void vel3_cell_row(const ElemV3 &K, int li, const dd *w, const dd *bx, bool lorentz, const Params &p, dd *row) {
+    const Tabs &T = tabs();
+    const dd nu2 = dd(2.0) / dd(p.Re);
+    dd epi[4][3][3], gwi[4][3], divi[4];
+    for (int cc = 0; cc < 4; ++cc) {
+        for (int l = 0; l < 3; ++l)
+            for (int k = 0; k < 3; ++k) epi[cc][l][k] = (K.Gr[li][cc][l][k] + K.Gr[li][cc][k][l]) * dd(0.5);
+        for (int l = 0; l < 3; ++l) gwi[cc][l] = K.Gr[li][cc][l][0] * w[0] + K.Gr[li][cc][l][1] * w[1] + K.Gr[li][cc][l][2] * w[2];
+        divi[cc] = K.Gr[li][cc][0][0] + K.Gr[li][cc][1][1] + K.Gr[li][cc][2][2];
+    }
+    dd vxb_i[10][3];
+    if (lorentz) for (int q = 0; q < 10; ++q) cross3(K.V[li].c[q], bx, vxb_i[q]);
+    for (int j = 0; j < 30; ++j) {
+        dd ee(0.0), dv(0.0), adv(0.0), ms(0.0), lor(0.0);
+        for (int c1 = 0; c1 < 4; ++c1) {
+            const dd divj = K.Gr[j][c1][0][0] + K.Gr[j][c1][1][1] + K.Gr[j][c1][2][2];
+            for (int c2 = 0; c2 < 4; ++c2) {
+                dd e(0.0);
+                for (int l = 0; l < 3; ++l)
+                    for (int k = 0; k < 3; ++k) e += (K.Gr[j][c1][l][k] + K.Gr[j][c1][k][l]) * dd(0.5) * epi[c2][l][k];
+                ee += e * T.m2[c1][c2];
+                dv += divj * divi[c2] * T.m2[c1][c2];
+            }
+        }
+        for (int pp = 0; pp < 10; ++pp)
+            for (int cc = 0; cc < 4; ++cc) adv += dot3(K.V[j].c[pp], gwi[cc]) * T.m3[pp][cc];
+        if (p.dt > 0 || lorentz)
+            for (int pp = 0; pp < 10; ++pp) {
+                dd vxb_j[3];
+                if (lorentz) cross3(K.V[j].c[pp], bx, vxb_j);
+                for (int q = 0; q < 10; ++q) {
+                    if (p.dt > 0) ms += dot3(K.V[j].c[pp], K.V[li].c[q]) * T.m4[pp][q];
+                    if (lorentz) lor += dot3(vxb_j, vxb_i[q]) * T.m4[pp][q];
+                }
+            }
+        dd v = nu2 * ee - adv + dd(p.gamma) * dv;
+        if (p.dt > 0) v += ms / dd(p.dt);
+        if (lorentz) v += dd(p.S) * lor;
+        row[j] = v;
+    }
+}
+
+// trace of basis function j of K on a face with cell-local vertices a[0..2] (ascending
+// global id): quadratic u on the 6 face pairs, linear eps(u) sA on the 3 face vertices
+struct Trace3 { dd u[6][3]; dd en[3][3]; };
+
+void vel3_trace(const ElemV3 &K, int j, const int *a, const dd *sA, Trace3 &T) {
+    for (int x = 0; x < 6; ++x)
+        for (int r = 0; r < 3; ++r) T.u[x][r] = K.V[j].c[PID[a[FP[x][0]]][a[FP[x][1]]]][r];
+    for (int t = 0; t < 3; ++t)
+        for (int l = 0; l < 3; ++l) {
+            dd acc(0.0);
+            for (int k = 0; k < 3; ++k) acc += (K.Gr[j][a[t]][l][k] + K.Gr[j][a[t]][k][l]) * sA[k];
+            T.en[t][l] = acc * dd(0.5);
+        }
+}
+
+// int_f mu^beta / |f| = 2 beta! / (|beta| + 2)!
+inline dd fmom(int n0, int n1, int n2) {
+    return dd(2.0 * fact(n0) * fact(n1) * fact(n2)) / dd(fact(n0 + n1 + n2 + 2));
+}
+struct FaceTabs {      // fmom of (pair x, pair y) and of (vertex t, pair y)
+    dd qq[6][6], lq[3][6];
+    FaceTabs() {
+        for (int x = 0; x < 6; ++x)
+            for (int y = 0; y < 6; ++y) {
+                int n[3] = {0, 0, 0};
+                n[FP[x][0]]++; n[FP[x][1]]++; n[FP[y][0]]++; n[FP[y][1]]++;
+                qq[x][y] = fmom(n[0], n[1], n[2]);
+                if (x < 3) {
+                    int k[3] = {0, 0, 0};
+                    k[x]++; k[FP[y][0]]++; k[FP[y][1]]++;
+                    lq[x][y] = fmom(k[0], k[1], k[2]);
+                }
+            }
+    }
+};
+const FaceTabs &face_tabs() { static const FaceTabs T; return T; }
+dd tr3_qq(const Trace3 &A, const Trace3 &B) {
+    const FaceTabs &T = face_tabs();
+    dd acc(0.0);
+    for (int x = 0; x < 6; ++x)
+        for (int y = 0; y < 6; ++y) acc += dot3(A.u[x], B.u[y]) * T.qq[x][y];
+    return acc;
+}
+dd tr3_lq(const Trace3 &L, const Trace3 &Qt) {       // (eps_L sA) . u_Q
+    const FaceTabs &T = face_tabs();
+    dd acc(0.0);
+    for (int t = 0; t < 3; ++t)
+        for (int y = 0; y < 6; ++y) acc += dot3(L.en[t], Qt.u[y]) * T.lq[t][y];
+    return acc;
+}
+
+void assemble_vel3(const Mesh &m, const SpaceV3 &s, const Params &p, const double *pot, const double *bpot, Pattern &P,
+                   std::vector<double> &val) {
+    const i64 nc = m.nc;
+    std::vector<ElemV3> el(nc);
+    std::vector<std::array<dd, 3>> wind(nc), bwind(nc);
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < nc; ++c) {
+        elemv3(m, c, el[c]);
+        dd w[3];
+        cell_wind(el[c].G, pot, w);
+        wind[c] = {w[0], w[1], w[2]};
+        dd b[3] = {dd(0.0), dd(0.0), dd(0.0)};
+        if (bpot) cell_wind(el[c].G, bpot, b);
+        bwind[c] = {b[0], b[1], b[2]};
+    }
+    std::vector<int> dkind(s.n), dent(s.n);
+    for (i64 f = 0; f < m.nf; ++f)
+        if (s.fdof[f] >= 0) for (int a = 0; a < 6; ++a) { dkind[s.fdof[f] + a] = 0; dent[s.fdof[f] + a] = (int)f; }
+    for (i64 c = 0; c < nc; ++c) for (int a = 0; a < 6; ++a) { dkind[s.cdof[c] + a] = 1; dent[s.cdof[c] + a] = (int)c; }
+    auto support = [&](i64 r, int *cells) -> int {
+        if (dkind[r] == 1) { cells[0] = dent[r]; return 1; }
+        const int f = dent[r];
+        cells[0] = m.fcell[2 * f];
+        if (m.fcell[2 * f + 1] >= 0) { cells[1] = m.fcell[2 * f + 1]; return 2; }
+        return 1;
+    };
+    P.rp.assign(s.n + 1, 0);
+    std::vector<std::vector<int>> rows(s.n);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (i64 r = 0; r < s.n; ++r) {
+        int sc[2];
+        const int ns = support(r, sc);
+        std::vector<int> cols;
+        for (int t = 0; t < ns; ++t) {
+            int nb[5] = {sc[t], -1, -1, -1, -1};
+            for (int q = 0; q < 4; ++q) {
+                const int f = m.cfacet[4 * sc[t] + q];
+                nb[q + 1] = m.fcell[2 * f] == sc[t] ? m.fcell[2 * f + 1] : m.fcell[2 * f];
+            }
+            for (int u = 0; u < 5; ++u) {
+                if (nb[u] < 0) continue;
+                int g[30];
+                cell_dofs_v3(m, s, nb[u], g);
+                for (int k = 0; k < 30; ++k) if (g[k] >= 0) cols.push_back(g[k]);
+            }
+        }
+        std::sort(cols.begin(), cols.end());
+        cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+        rows[r] = std::move(cols);
+    }
+    for (i64 r = 0; r < s.n; ++r) P.rp[r + 1] = P.rp[r] + (i64)rows[r].size();
+    P.ci.resize(P.rp[s.n]);
+    for (i64 r = 0; r < s.n; ++r) std::copy(rows[r].begin(), rows[r].end(), P.ci.begin() + P.rp[r]);
+    rows.clear();
+    rows.shrink_to_fit();
+    val.assign(P.rp[s.n], 0.0);
+    const dd nu2 = dd(2.0) / dd(p.Re);
+#pragma omp parallel for schedule(dynamic, 64)
+    for (i64 r = 0; r < s.n; ++r) {
+        const i64 base = P.rp[r], len = P.rp[r + 1] - base;
+        std::vector<dd> acc(len);
+        auto add = [&](int col, const dd &v) { acc[find_col(P, r, col) - base] += v; };
+        int sc[2];
+        const int ns = support(r, sc);
+        for (int t = 0; t < ns; ++t) {
+            const int c = sc[t];
+            int g[30];
+            cell_dofs_v3(m, s, c, g);
+            int li = -1;
+            for (int k = 0; k < 30; ++k) if (g[k] == r) li = k;
+            dd row[30];
+            const dd w[3] = {wind[c][0], wind[c][1], wind[c][2]}, b[3] = {bwind[c][0], bwind[c][1], bwind[c][2]};
+            vel3_cell_row(el[c], li, w, b, bpot != nullptr, p, row);
+            const dd sixK = dd(6.0) * el[c].G.vol;
+            for (int k = 0; k < 30; ++k) if (g[k] >= 0) add(g[k], row[k] * sixK);
+        }
+        std::vector<int> fs;
+        for (int t = 0; t < ns; ++t) for (int q = 0; q < 4; ++q) fs.push_back(m.cfacet[4 * sc[t] + q]);
+        std::sort(fs.begin(), fs.end());
+        fs.erase(std::unique(fs.begin(), fs.end()), fs.end());
+        for (int f : fs) {
+            const int cp = m.fcell[2 * f], cm = m.fcell[2 * f + 1];
+            const bool interior = cm >= 0;
+            const ElemV3 &Kp = el[cp];
+            int qf = -1;
+            for (int q = 0; q < 4; ++q) if (m.cfacet[4 * cp + q] == f) qf = q;
+            dd A[3];
+            int fl[3];
+            facet_area(Kp.G, qf, A, fl);
+            const double sg = facet_sign(Kp.G, qf, A, fl);
+            const dd sA[3] = {dd(sg) * A[0], dd(sg) * A[1], dd(sg) * A[2]};   // |f| n, n outward of K+
+            const dd WA = wind[cp][0] * sA[0] + wind[cp][1] * sA[1] + wind[cp][2] * sA[2];
+            const dd aWA = WA.hi < 0 ? -WA : WA;
+            dd hF(0.0);
+            for (int x = 0; x < 3; ++x)
+                for (int y = x + 1; y < 3; ++y) {
+                    dd t[3];
+                    for (int k = 0; k < 3; ++k) t[k] = Kp.G.X[fl[y]][k] - Kp.G.X[fl[x]][k];
+                    const dd l = sqrt(dot3(t, t));
+                    if (hF < l) hF = l;
+                }
+            const dd pen = dd(p.sigma) / dd(p.Re) * sqrt(dot3(A, A)) / hF;     // sigma/(Re h_F) |f|
+            const int fvv[3] = {m.fv[3 * f], m.fv[3 * f + 1], m.fv[3 * f + 2]};
+            auto locs = [&](const ElemV3 &K, int *a) {
+                for (int t = 0; t < 3; ++t) for (int b = 0; b < 4; ++b) if (K.G.v[b] == fvv[t]) a[t] = b;
+            };
+            const dd avg = interior ? dd(0.5) : dd(1.0);
+            const int sides = interior ? 2 : 1;
+            const int cells[2] = {cp, cm};
+            for (int t = 0; t < ns; ++t) {
+                const int ci_ = sc[t];
+                if (ci_ != cp && ci_ != cm) continue;
+                const int Ji = ci_ == cp ? 1 : -1;
+                int gi[30];
+                cell_dofs_v3(m, s, ci_, gi);
+                int li = -1;
+                for (int k = 0; k < 30; ++k) if (gi[k] == r) li = k;
+                const ElemV3 &Ki = el[ci_];
+                int ai[3];
+                locs(Ki, ai);
+                Trace3 Ti;
+                vel3_trace(Ki, li, ai, sA, Ti);
+                for (int sd = 0; sd < sides; ++sd) {
+                    const int cj = cells[sd];
+                    const int Jj = sd == 0 ? 1 : -1;
+                    const ElemV3 &Kj = el[cj];
+                    int aj[3];
+                    locs(Kj, aj);
+                    int gj[30];
+                    cell_dofs_v3(m, s, cj, gj);
+                    dd upc;
+                    if (interior) upc = Jj > 0 ? (WA + aWA) * dd(0.5) : -((-WA + aWA) * dd(0.5));
+                    else upc = (WA + aWA) * dd(0.5);
+                    for (int j = 0; j < 30; ++j) {
+                        if (gj[j] < 0) continue;
+                        Trace3 Tj;
+                        vel3_trace(Kj, j, aj, sA, Tj);
+                        const dd Qv = tr3_qq(Tj, Ti);
+                        const dd E1 = tr3_lq(Tj, Ti);
+                        const dd E2 = tr3_lq(Ti, Tj);
+                        dd v = -(nu2 * avg * (dd((double)Ji) * E1 + dd((double)Jj) * E2)) + pen * dd((double)(Jj * Ji)) * Qv;
+                        v += (interior ? upc * dd((double)Ji) : upc) * Qv;
+                        add(gj[j], v);
+                    }
+                }
+            }
+        }
+        round_row(acc.data(), len, val.data() + base);
+    }
+}
+
+void build_patches_v3(const Mesh &m, const SpaceV3 &s, std::vector<i64> &pptr, std::vector<int> &pdofs) {
+    std::vector<std::vector<int>> vlist(m.nv);
+    for (i64 f = 0; f < m.nf; ++f)
+        if (s.fdof[f] >= 0)
+            for (int t = 0; t < 3; ++t) for (int a = 0; a < 6; ++a) vlist[m.fv[3 * f + t]].push_back(s.fdof[f] + a);
+    for (i64 c = 0; c < m.nc; ++c)
+        for (int t = 0; t < 4; ++t) for (int a = 0; a < 6; ++a) vlist[m.cv[4 * c + t]].push_back(s.cdof[c] + a);
+    pptr.assign(1, 0);
+    pdofs.clear();
+    for (i64 v = 0; v < m.nv; ++v) {
+        auto &L = vlist[v];
+        if (L.empty()) continue;
+        std::sort(L.begin(), L.end());
+        pdofs.insert(pdofs.end(), L.begin(), L.end());
+        pptr.push_back((i64)pdofs.size());
+    }
+}
+
+void build_prolongation_v3(const Mesh &mf, const SpaceV3 &sf, const Mesh &mc, const SpaceV3 &sc, std::vector<i64> &rp,
+                           std::vector<int> &ci, std::vector<double> &vv) {
+    static const int PERM[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    std::vector<std::vector<std::pair<int, dd>>> rows(sf.n);
+    std::vector<ElemV3> ce(mc.nc);
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < mc.nc; ++c) elemv3(mc, c, ce[c]);
+    std::vector<int> owner(sf.n, INT32_MAX);
+    for (i64 c = mf.nc - 1; c >= 0; --c) {
+        int g[30];
+        cell_dofs_v3(mf, sf, c, g);
+        for (int t = 0; t < 30; ++t) if (g[t] >= 0) owner[g[t]] = (int)c;
+    }
+#pragma omp parallel for schedule(dynamic, 64)
+    for (i64 c = 0; c < mf.nc; ++c) {
+        int g[30];
+        cell_dofs_v3(mf, sf, c, g);
+        bool any = false;
+        for (int t = 0; t < 30; ++t) any = any || (g[t] >= 0 && owner[g[t]] == c);
+        if (!any) continue;
+        int Lf[4][3] = {{0}};
+        int sum[3] = {0, 0, 0};
+        for (int a = 0; a < 4; ++a) {
+            mf.lat(mf.cv[4 * c + a], Lf[a]);
+            for (int r = 0; r < 3; ++r) sum[r] += Lf[a][r];
+        }
+        int cube[3], rel[3];
+        for (int r = 0; r < 3; ++r) { cube[r] = sum[r] / 8; rel[r] = sum[r] - 8 * cube[r]; }
+        const i64 cb = cube[0] + (i64)mc.N * (cube[1] + (i64)mc.N * cube[2]);
+        i64 pc = -1;
+        for (int q = 0; q < 6; ++q)
+            if (rel[PERM[q][0]] > rel[PERM[q][1]] && rel[PERM[q][1]] > rel[PERM[q][2]]) pc = 6 * cb + q;
+        const ElemV3 &Kc = ce[pc];
+        int cg[30];
+        cell_dofs_v3(mc, sc, pc, cg);
+        GeoT<dd> Gf;
+        cell_geo(mf, c, Gf);
+        dd T[4][4];
+        for (int b = 0; b < 4; ++b)
+            for (int a = 0; a < 4; ++a) {
+                dd v(b == 0 ? 1.0 : 0.0);
+                for (int r = 0; r < 3; ++r) v += Kc.G.g[b][r] * (Gf.X[a][r] - Kc.G.X[0][r]);
+                T[b][a] = v;
+            }
+        for (int j = 0; j < 30; ++j) {
+            if (cg[j] < 0) continue;
+            Q F;
+            memset((void *)&F, 0, sizeof(Q));
+            for (int pp = 0; pp < 10; ++pp) {
+                const int b = PA[pp][0], d2 = PA[pp][1];
+                for (int a = 0; a < 4; ++a)
+                    for (int a2 = 0; a2 < 4; ++a2) {
+                        const dd tt = T[b][a] * T[d2][a2];
+                        if (tt.hi == 0.0) continue;
+                        for (int r = 0; r < 3; ++r) F.c[PID[a][a2]][r] += Kc.V[j].c[pp][r] * tt;
+                    }
+            }
+            dd out[30];
+            bdm3_fun(Gf, F, out);
+            for (int t = 0; t < 30; ++t)
+                if (g[t] >= 0 && owner[g[t]] == c) rows[g[t]].push_back({cg[j], out[t]});
+        }
+    }
+    rp.assign(sf.n + 1, 0);
+    std::vector<std::vector<std::pair<int, double>>> fin(sf.n);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (i64 I = 0; I < sf.n; ++I) {
+        auto &R = rows[I];
+        std::sort(R.begin(), R.end(), [](const std::pair<int, dd> &x, const std::pair<int, dd> &y) { return x.first < y.first; });
+        std::vector<dd> xs(R.size());
+        for (size_t t = 0; t < R.size(); ++t) xs[t] = R[t].second;
+        std::vector<double> rounded(R.size());
+        round_row(xs.data(), (i64)xs.size(), rounded.data());
+        double mx = 0;
+        for (double v : rounded) mx = std::max(mx, std::fabs(v));
+        for (size_t t = 0; t < R.size(); ++t)
+            if (rounded[t] != 0.0 && std::fabs(to_double(xs[t])) >= std::ldexp(mx, -30)) fin[I].push_back({R[t].first, rounded[t]});
+    }
+    for (i64 I = 0; I < sf.n; ++I) rp[I + 1] = rp[I] + (i64)fin[I].size();
+    ci.resize(rp[sf.n]);
+    vv.resize(rp[sf.n]);
+    for (i64 I = 0; I < sf.n; ++I)
+        for (size_t t = 0; t < fin[I].size(); ++t) { ci[rp[I] + t] = fin[I][t].first; vv[rp[I] + t] = fin[I][t].second; }
+}
+
 }  // namespace k2d3
 
 }  // namespace
@@ -2644,8 +3076,40 @@ std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params
     if ((block != 0 && block != 1) || (dim != 2 && dim != 3) || N < 1 || nlev < 1) return "bad arguments";
     if (N % (1 << (nlev - 1))) return "N not divisible by 2^(nlev-1)";
     if (p.degree != 1 && p.degree != 2) return "degree must be 1 or 2";
-    if (p.degree == 2 && dim == 3 && block != 0) return "degree 2 in 3D is built for the E-B block only (NEXT-2)";
     out.assign(nlev, HostLevel());
+    if (p.degree == 2 && dim == 3 && block == 1) {
+        std::vector<Mesh> meshes(nlev);
+        std::vector<k2d3::SpaceV3> spaces(nlev);
+        for (int l = nlev - 1; l >= 0; --l) {
+            const int Nl = N >> (nlev - 1 - l), step = 1 << (nlev - 1 - l);
+            Mesh &m = meshes[l];
+            build_mesh(m, dim, Nl);
+            k2d3::build_space_v3(spaces[l], m);
+            std::vector<double> pot(3 * m.nv), bpot(bn ? 3 * m.nv : 0);
+            for (i64 v = 0; v < m.nv; ++v) {
+                int q[3];
+                m.lat(v, q);
+                const i64 fv = q[0] * step + (i64)(N + 1) * (q[1] * step + (i64)(N + 1) * (q[2] * step));
+                for (int t = 0; t < 3; ++t) pot[3 * v + t] = w[3 * fv + t];
+                if (bn) for (int t = 0; t < 3; ++t) bpot[3 * v + t] = bn[3 * fv + t];
+            }
+            Pattern P;
+            std::vector<double> val;
+            k2d3::assemble_vel3(m, spaces[l], p, pot.data(), bn ? bpot.data() : nullptr, P, val);
+            HostLevel &H = out[l];
+            H.n = spaces[l].n;
+            H.rp = std::move(P.rp);
+            H.ci = std::move(P.ci);
+            H.v = std::move(val);
+            if (l > 0) k2d3::build_patches_v3(m, spaces[l], H.pptr, H.pdofs);
+        }
+        for (int l = 1; l < nlev; ++l) {
+            k2d3::build_prolongation_v3(meshes[l], spaces[l], meshes[l - 1], spaces[l - 1], out[l].prp, out[l].pci,
+                                        out[l].pv);
+            out[l].n_coarser = spaces[l - 1].n;
+        }
+        return "";
+    }
     if (p.degree == 2 && dim == 3) {
         std::vector<Mesh> meshes(nlev);
         std::vector<k2d3::Space3> spaces(nlev);

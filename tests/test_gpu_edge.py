@@ -194,7 +194,7 @@ def test_vcycle_graph_replay_bitexact(oracle_mod, smoother):
     assert ctx.graphs_active() >= 1
 
 
-@pytest.mark.parametrize("name,N", [("c1", 4), ("c3", 4), ("c4", 2)])
+@pytest.mark.parametrize("name,N", [("c1", 4), ("c3", 4), ("c4", 2), ("c5", 2)])
 def test_k2_single_level_vcycle_is_coarse_solve(oracle_mod, name, N):
     """NEXT-2 degenerate hierarchy: one level at k = 2 -- the V-cycle is the coarse solve
     (explicit inverse, R-coarse), bit-exact against the oracle's exact build."""
@@ -202,7 +202,7 @@ def test_k2_single_level_vcycle_is_coarse_solve(oracle_mod, name, N):
     import torch
     from paper_2104_14855_b200 import mhdp, workloads
     cfg = dataclasses.replace(workloads.small(name, N, 1), degree=2,
-                              sigma=40.0 if name == "c3" else 10.0)
+                              sigma=40.0 if name in ("c3", "c5") else 10.0)
     w, _, _ = workloads.draw(cfg, 1, 3)
     ctx = mhdp.Context(0, torch.cuda.current_stream().cuda_stream)
     ctx.assemble(cfg, w)

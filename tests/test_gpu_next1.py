@@ -55,7 +55,7 @@ def test_gmres_smoothed_vcycle_and_fgmres_on_oracle_operator(oracle_mod, name, N
     assert np.array_equal(bits(host(xg)), bits(xo))
 
 
-CASES_PB = [("c1", None, None), ("c3", 32, 4), ("c5", 6, 2), ("c2-k2", 64, 4), ("c3-k2", 32, 4), ("c4-k2", 4, 2)]
+CASES_PB = [("c1", None, None), ("c3", 32, 4), ("c5", 6, 2), ("c2-k2", 64, 4), ("c3-k2", 32, 4), ("c4-k2", 4, 2), ("c5-k2", 4, 2)]
 
 
 @pytest.mark.parametrize("name,N,L", CASES_PB, ids=[f"{c}-{n or 'full'}" for c, n, l in CASES_PB])

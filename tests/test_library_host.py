@@ -172,12 +172,13 @@ K2_CASES = [("c1", 8, 2, dict()), ("c2", 32, 3, dict()), ("c2", 16, 3, dict(pica
             ("c2", 64, 4, dict(Rem=7.0)),
             ("c3", 8, 2, dict(sigma=40.0)), ("c3", 32, 4, dict(sigma=40.0, Re=100.0, gamma=1e4)),
             ("c3", 16, 3, dict(sigma=40.0, dt=0.05)), ("c3-lorentz", 16, 2, dict(sigma=40.0, S=30.0)),
-            ("c4", 4, 2, dict())]                                   # 3D NED1_2 x RT2, 280-DoF stars
+            ("c4", 4, 2, dict()),                                   # 3D NED1_2 x RT2, 280-DoF stars
+            ("c5", 2, 1, dict(sigma=40.0, dt=0.05, gamma=1e4))]     # 3D BDM2, 360-DoF stars
 
 
 @pytest.mark.parametrize("name,N,L,kw", K2_CASES, ids=[f"{c}-N{n}L{l}-{k}" for c, n, l, k in K2_CASES])
 def test_k2_host_setup_bitexact_vs_exact_oracle(mh, oracle_mod, name, N, L, kw):
-    """NEXT-2 (k = 2): 2D CG2 x RT2 E-B and BDM2 velocity blocks, 3D NED1_2 x RT2 E-B block.
+    """NEXT-2 (k = 2): 2D CG2 x RT2 E-B and BDM2 velocity blocks, 3D NED1_2 x RT2 and BDM2.
     Numbering, patches, prolongation (R-prol2) and operator values of the library
     (closed-form barycentric, facet and edge integrals in double-double; {lam_a psi_q} /
     {lam_a lam_b e_r} / Arnold-Falk-Winther primal bases) equal the oracle's exact build
@@ -206,18 +207,6 @@ def test_k2_host_setup_bitexact_vs_exact_oracle(mh, oracle_mod, name, N, L, kw):
         prp, pci, pv = ctx.prolongation(l)
         assert np.array_equal(P.rp, prp) and np.array_equal(P.ci, pci), f"level {l}: prolongation pattern"
         assert np.array_equal(P.v.view(np.uint64), pv.view(np.uint64)), f"level {l}: prolongation values"
-
-
-def test_k2_velocity_rejected_in_3d(mh):
-    """3D BDM2 (~360-DoF stars, on-the-fly factorisation) is not built."""
-    import dataclasses
-    from paper_2104_14855_b200 import workloads
-    for name in ("c5",):
-        cfg = dataclasses.replace(workloads.small(name, 4, 1), degree=2)
-        w, _, _ = workloads.draw(cfg, 1, 0)
-        ctx = mh.Context(-1)
-        with pytest.raises(mh.MhdpError):
-            ctx.assemble(cfg, w)
 
 
 def test_coupled_rejects_degree_2(mh):

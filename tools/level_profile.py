@@ -2,7 +2,7 @@
 the launching stream, warm caches), so that kernel changes can be compared without the
 box-to-box variance of separate bench runs.  Not part of the product or the tests.
 
-    python tools/level_profile.py [c5|c4|c3|c2k2|c3k2|c4k2] [reps]
+    python tools/level_profile.py [c5|c4|c3|c2k2|c3k2|c4k2|c5k2] [reps]
 """
 import dataclasses
 import json
@@ -36,6 +36,8 @@ def main():
         cfg = dataclasses.replace(workloads.CONFIGS["c2"], N=512, levels=7, degree=2)
     elif name == "c3k2":
         cfg = dataclasses.replace(workloads.CONFIGS["c3"], N=256, levels=6, degree=2, sigma=40.0)
+    elif name == "c5k2":
+        cfg = dataclasses.replace(workloads.CONFIGS["c5"], N=16, levels=3, degree=2, sigma=40.0)
     elif name == "c4k2":
         cfg = dataclasses.replace(workloads.CONFIGS["c4"], degree=2)
     else:
