@@ -335,9 +335,9 @@ def run_variants(cfg, seed, dev, stream):
         "3D E-B block, NED1_2 x RT2 (k = 2), 32^3 x 6 cells, 4 levels, V(2,2), Re_m = S = 1e3, Picard "
         "(280-DoF stars; the Newton block at Re_m >= 100 is not solved by the star V-cycle, DESIGN 9d)")
     out["next2_k2_vel3d"] = _k2_variant(
-        dataclasses.replace(workloads.CONFIGS["c5"], N=16, levels=3, degree=2, sigma=40.0), seed, dev, stream,
-        "3D AL velocity block, BDM2 (k = 2), 16^3 x 6 cells, 3 levels, V(2,2), Re = gamma = 1e4, sigma = 40 "
-        "(360-DoF stars; 16^3 bounds the double-double host assembly time)")
+        dataclasses.replace(workloads.CONFIGS["c5"], N=24, levels=4, degree=2, sigma=40.0), seed, dev, stream,
+        "3D AL velocity block, BDM2 (k = 2), 24^3 x 6 cells, 4 levels, V(2,2), Re = gamma = 1e4, sigma = 40 "
+        "(360-DoF stars; 24^3 bounds the double-double host assembly time)")
     return out
 
 

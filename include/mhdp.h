@@ -70,8 +70,10 @@ typedef struct {
     int picard;               /* NEXT-4: 0 = Newton (delta = 1), 1 = Picard (delta = 0): the
                                  E-B block loses G~                        */
     int degree;               /* NEXT-2: element degree k.  0 or 1: k = 1 (the
-                                 BASELINE configs); 2: CG2 x RT2 for the 2D E-B block (reading
-                                 R-basis2).  Other blocks / dims with 2 -> MHDP_EINVAL         */
+                                 BASELINE configs); 2: k = 2 for both blocks in 2D and 3D --
+                                 E-B CG2 x RT2 (2D) / NED1_2 x RT2 (3D, 280-DoF stars), AL
+                                 velocity BDM2 (36 / 360-DoF stars); readings R-basis2,
+                                 R-basis2-vel, R-basis2-3D.  Other values -> MHDP_EINVAL       */
 } mhdp_params;
 
 typedef struct mhdp_ctx mhdp_ctx;

@@ -2730,31 +2730,48 @@ void vel3_cell_row(const ElemV3 &K, int li, const dd *w, const dd *bx, bool lore
         for (int l = 0; l < 3; ++l) gwi[cc][l] = K.Gr[li][cc][l][0] * w[0] + K.Gr[li][cc][l][1] * w[1] + K.Gr[li][cc][l][2] * w[2];
         divi[cc] = K.Gr[li][cc][0][0] + K.Gr[li][cc][1][1] + K.Gr[li][cc][2][2];
     }
+    // test side contracted with the moment tables once per row
+    dd Me[4][3][3], Md[4], Ga[10][3], Mv[10][3], Mb[10][3];
+    for (int c1 = 0; c1 < 4; ++c1) {
+        dd d(0.0);
+        for (int c2 = 0; c2 < 4; ++c2) d += T.m2[c1][c2] * divi[c2];
+        Md[c1] = d;
+        for (int l = 0; l < 3; ++l)
+            for (int k = 0; k < 3; ++k) {
+                dd e(0.0);
+                for (int c2 = 0; c2 < 4; ++c2) e += T.m2[c1][c2] * epi[c2][l][k];
+                Me[c1][l][k] = e;
+            }
+    }
     dd vxb_i[10][3];
     if (lorentz) for (int q = 0; q < 10; ++q) cross3(K.V[li].c[q], bx, vxb_i[q]);
+    for (int pp = 0; pp < 10; ++pp)
+        for (int r = 0; r < 3; ++r) {
+            dd a(0.0), mv(0.0), mb(0.0);
+            for (int cc = 0; cc < 4; ++cc) a += T.m3[pp][cc] * gwi[cc][r];
+            for (int q = 0; q < 10; ++q) {
+                mv += T.m4[pp][q] * K.V[li].c[q][r];
+                if (lorentz) mb += T.m4[pp][q] * vxb_i[q][r];
+            }
+            Ga[pp][r] = a; Mv[pp][r] = mv; Mb[pp][r] = mb;
+        }
     for (int j = 0; j < 30; ++j) {
         dd ee(0.0), dv(0.0), adv(0.0), ms(0.0), lor(0.0);
         for (int c1 = 0; c1 < 4; ++c1) {
             const dd divj = K.Gr[j][c1][0][0] + K.Gr[j][c1][1][1] + K.Gr[j][c1][2][2];
-            for (int c2 = 0; c2 < 4; ++c2) {
-                dd e(0.0);
-                for (int l = 0; l < 3; ++l)
-                    for (int k = 0; k < 3; ++k) e += (K.Gr[j][c1][l][k] + K.Gr[j][c1][k][l]) * dd(0.5) * epi[c2][l][k];
-                ee += e * T.m2[c1][c2];
-                dv += divj * divi[c2] * T.m2[c1][c2];
+            for (int l = 0; l < 3; ++l)
+                for (int k = 0; k < 3; ++k) ee += (K.Gr[j][c1][l][k] + K.Gr[j][c1][k][l]) * dd(0.5) * Me[c1][l][k];
+            dv += divj * Md[c1];
+        }
+        for (int pp = 0; pp < 10; ++pp) {
+            adv += dot3(K.V[j].c[pp], Ga[pp]);
+            if (p.dt > 0) ms += dot3(K.V[j].c[pp], Mv[pp]);
+            if (lorentz) {
+                dd vxb_j[3];
+                cross3(K.V[j].c[pp], bx, vxb_j);
+                lor += dot3(vxb_j, Mb[pp]);
             }
         }
-        for (int pp = 0; pp < 10; ++pp)
-            for (int cc = 0; cc < 4; ++cc) adv += dot3(K.V[j].c[pp], gwi[cc]) * T.m3[pp][cc];
-        if (p.dt > 0 || lorentz)
-            for (int pp = 0; pp < 10; ++pp) {
-                dd vxb_j[3];
-                if (lorentz) cross3(K.V[j].c[pp], bx, vxb_j);
-                for (int q = 0; q < 10; ++q) {
-                    if (p.dt > 0) ms += dot3(K.V[j].c[pp], K.V[li].c[q]) * T.m4[pp][q];
-                    if (lorentz) lor += dot3(vxb_j, vxb_i[q]) * T.m4[pp][q];
-                }
-            }
         dd v = nu2 * ee - adv + dd(p.gamma) * dv;
         if (p.dt > 0) v += ms / dd(p.dt);
         if (lorentz) v += dd(p.S) * lor;
@@ -2935,6 +2952,24 @@ void assemble_vel3(const Mesh &m, const SpaceV3 &s, const Params &p, const doubl
                 locs(Ki, ai);
                 Trace3 Ti;
                 vel3_trace(Ki, li, ai, sA, Ti);
+                // test side contracted once: Q = sum_x u_j[x].Wq[x], E1 = sum_t en_j[t].Zl[t],
+                // E2 = sum_y u_j[y].Yl[y]  (tr3_qq(Tj, Ti), tr3_lq(Tj, Ti), tr3_lq(Ti, Tj))
+                const FaceTabs &FT = face_tabs();
+                dd Wq[6][3], Zl[3][3], Yl[6][3];
+                for (int x = 0; x < 6; ++x)
+                    for (int r2 = 0; r2 < 3; ++r2) {
+                        dd a1(0.0), a2(0.0);
+                        for (int y = 0; y < 6; ++y) a1 += FT.qq[x][y] * Ti.u[y][r2];
+                        for (int t2 = 0; t2 < 3; ++t2) a2 += FT.lq[t2][x] * Ti.en[t2][r2];
+                        Wq[x][r2] = a1;
+                        Yl[x][r2] = a2;
+                    }
+                for (int t2 = 0; t2 < 3; ++t2)
+                    for (int r2 = 0; r2 < 3; ++r2) {
+                        dd a1(0.0);
+                        for (int y = 0; y < 6; ++y) a1 += FT.lq[t2][y] * Ti.u[y][r2];
+                        Zl[t2][r2] = a1;
+                    }
                 for (int sd = 0; sd < sides; ++sd) {
                     const int cj = cells[sd];
                     const int Jj = sd == 0 ? 1 : -1;
@@ -2950,9 +2985,9 @@ void assemble_vel3(const Mesh &m, const SpaceV3 &s, const Params &p, const doubl
                         if (gj[j] < 0) continue;
                         Trace3 Tj;
                         vel3_trace(Kj, j, aj, sA, Tj);
-                        const dd Qv = tr3_qq(Tj, Ti);
-                        const dd E1 = tr3_lq(Tj, Ti);
-                        const dd E2 = tr3_lq(Ti, Tj);
+                        dd Qv(0.0), E1(0.0), E2(0.0);
+                        for (int y = 0; y < 6; ++y) { Qv += dot3(Tj.u[y], Wq[y]); E2 += dot3(Tj.u[y], Yl[y]); }
+                        for (int t2 = 0; t2 < 3; ++t2) E1 += dot3(Tj.en[t2], Zl[t2]);
                         dd v = -(nu2 * avg * (dd((double)Ji) * E1 + dd((double)Jj) * E2)) + pen * dd((double)(Jj * Ji)) * Qv;
                         v += (interior ? upc * dd((double)Ji) : upc) * Qv;
                         add(gj[j], v);

@@ -37,7 +37,7 @@ def main():
     elif name == "c3k2":
         cfg = dataclasses.replace(workloads.CONFIGS["c3"], N=256, levels=6, degree=2, sigma=40.0)
     elif name == "c5k2":
-        cfg = dataclasses.replace(workloads.CONFIGS["c5"], N=16, levels=3, degree=2, sigma=40.0)
+        cfg = dataclasses.replace(workloads.CONFIGS["c5"], N=24, levels=4, degree=2, sigma=40.0)
     elif name == "c4k2":
         cfg = dataclasses.replace(workloads.CONFIGS["c4"], degree=2)
     else:
