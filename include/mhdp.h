@@ -172,6 +172,14 @@ int         mhdp_vcycle_graphs_active(const mhdp_ctx *ctx);
 /* End-to-end variant for callers holding host data: copies b (host, n doubles) to the
  * device, runs mhdp_vcycle on the finest level and copies x back (synchronises).       */
 mhdp_status mhdp_vcycle_host(mhdp_ctx *ctx, const double *b_host, double *x_host);
+/* Batched end-to-end V-cycles (one preconditioner application per right-hand
+ * side): b_host holds nrhs right-hand sides of n doubles each (row k = b_k, host,
+ * caller-owned, ideally pinned), x_host receives the nrhs results in the same layout.
+ * The upload of b_{k+1} and the download of x_{k-1} overlap the V-cycle of b_k (two
+ * device slots, two context-owned copy streams); every x_k is bit-identical to
+ * mhdp_vcycle_host(b_k).  Synchronises.  nrhs = 0 is a no-op; nrhs < 0 or NULL
+ * buffers -> MHDP_EINVAL.                                                              */
+mhdp_status mhdp_vcycle_host_batch(mhdp_ctx *ctx, int nrhs, const double *b_host, double *x_host);
 /* Smoother sweeps with host buffers (b, x in/out; synchronises).                       */
 mhdp_status mhdp_smooth_host(mhdp_ctx *ctx, int level, int nsweeps, int x_is_zero,
                              const double *b_host, double *x_host);

@@ -88,6 +88,11 @@ struct mhdp_ctx {
     std::vector<VGraph> graphs;
     cudaStream_t cap = nullptr;
     bool graphs_off = false;
+    // mhdp_vcycle_host_batch: two device (b, x) slots, copy-in / copy-out streams
+    double *hb[2] = {nullptr, nullptr}, *hx[2] = {nullptr, nullptr};
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr},
+                ev_out[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -156,6 +161,7 @@ void free_device(mhdp_ctx *c) {
     c->d_status = nullptr; c->d_scal = nullptr;
     c->gV = c->gZ = c->gw = nullptr; c->g_cap = 0;
     c->fV = c->fZ = c->fw = c->fpart = c->fscal = nullptr; c->f_cap = 0;
+    c->hb[0] = c->hb[1] = c->hx[0] = c->hx[1] = nullptr;
     c->setup_done = false;
 }
 
@@ -558,6 +564,11 @@ void mhdp_destroy(mhdp_ctx *ctx) {
     if (!ctx) return;
     free_device(ctx);
     if (ctx->cap) cudaStreamDestroy(ctx->cap);
+    if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
+    if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
+    for (cudaEvent_t e : {ctx->ev_start, ctx->ev_in[0], ctx->ev_in[1], ctx->ev_done[0], ctx->ev_done[1], ctx->ev_out[0],
+                          ctx->ev_out[1]})
+        if (e) cudaEventDestroy(e);
     delete ctx;
 }
 
@@ -918,6 +929,52 @@ mhdp_status mhdp_vcycle_host(mhdp_ctx *ctx, const double *b_host, double *x_host
     CK(cudaMemcpyAsync(db, b_host, sizeof(double) * L.n, cudaMemcpyHostToDevice, ctx->stream));
     vcycle(ctx, l, db, dx);
     CK(cudaMemcpyAsync(x_host, dx, sizeof(double) * L.n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return check_launch(ctx);
+}
+
+mhdp_status mhdp_vcycle_host_batch(mhdp_ctx *ctx, int nrhs, const double *b_host, double *x_host) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (nrhs < 0 || (nrhs > 0 && (!b_host || !x_host))) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    if (nrhs == 0) return MHDP_OK;
+    const int l = ctx->nlev - 1;
+    const int64_t n = ctx->D[l].n;
+    const size_t bytes = sizeof(double) * (size_t)n;
+    for (int t = 0; t < 2; ++t) {
+        if (!ctx->hb[t] && (st = dalloc(ctx, &ctx->hb[t], n))) return st;
+        if (!ctx->hx[t] && (st = dalloc(ctx, &ctx->hx[t], n))) return st;
+    }
+    if (!ctx->s_in) {
+        CK(cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming));
+        for (int t = 0; t < 2; ++t) {
+            CK(cudaEventCreateWithFlags(&ctx->ev_in[t], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->ev_done[t], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->ev_out[t], cudaEventDisableTiming));
+        }
+    }
+    // the copy streams start after the work already queued on the context stream
+    CK(cudaEventRecord(ctx->ev_start, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->s_in, ctx->ev_start, 0));
+    CK(cudaStreamWaitEvent(ctx->s_out, ctx->ev_start, 0));
+    for (int k = 0; k < nrhs; ++k) {
+        const int t = k & 1;
+        // slot t was last used by right-hand side k - 2: its V-cycle must have read hb[t]
+        // before the upload, its download must have read hx[t] before the next V-cycle
+        if (k >= 2) CK(cudaStreamWaitEvent(ctx->s_in, ctx->ev_done[t], 0));
+        CK(cudaMemcpyAsync(ctx->hb[t], b_host + (int64_t)k * n, bytes, cudaMemcpyHostToDevice, ctx->s_in));
+        CK(cudaEventRecord(ctx->ev_in[t], ctx->s_in));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[t], 0));
+        if (k >= 2) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_out[t], 0));
+        if ((st = mhdp_vcycle(ctx, l, ctx->hb[t], ctx->hx[t]))) return st;
+        CK(cudaEventRecord(ctx->ev_done[t], ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->s_out, ctx->ev_done[t], 0));
+        CK(cudaMemcpyAsync(x_host + (int64_t)k * n, ctx->hx[t], bytes, cudaMemcpyDeviceToHost, ctx->s_out));
+        CK(cudaEventRecord(ctx->ev_out[t], ctx->s_out));
+    }
+    CK(cudaStreamSynchronize(ctx->s_out));
     CK(cudaStreamSynchronize(ctx->stream));
     return check_launch(ctx);
 }

@@ -47,7 +47,7 @@ _lib = None
 SYMBOLS = ["mhdp_create", "mhdp_destroy", "mhdp_assemble", "mhdp_begin_levels", "mhdp_load_level", "mhdp_setup",
            "mhdp_get_level_info", "mhdp_num_levels", "mhdp_spmv", "mhdp_residual", "mhdp_patch_apply",
            "mhdp_patch_update", "mhdp_smooth", "mhdp_restrict", "mhdp_prolong_add", "mhdp_coarse_solve",
-           "mhdp_vcycle", "mhdp_vcycle_host", "mhdp_smooth_host", "mhdp_gmres", "mhdp_export_csr",
+           "mhdp_vcycle", "mhdp_vcycle_host", "mhdp_vcycle_host_batch", "mhdp_smooth_host", "mhdp_gmres", "mhdp_export_csr",
            "mhdp_export_patches", "mhdp_export_prolongation", "mhdp_export_patch_lu", "mhdp_export_slots",
            "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count", "mhdp_fgmres", "mhdp_dot", "mhdp_set_smoother", "mhdp_vcycle_graphs_active", "mhdp_assemble_lorentz",
            "mhdp_coupled_create", "mhdp_coupled_destroy", "mhdp_coupled_sizes", "mhdp_coupled_export_csr",
@@ -81,6 +81,7 @@ def lib():
             "mhdp_coarse_solve": [vp, vp, vp],
             "mhdp_vcycle": [vp, C.c_int, vp, vp],
             "mhdp_vcycle_host": [vp, dp, dp],
+            "mhdp_vcycle_host_batch": [vp, C.c_int, dp, dp],
             "mhdp_smooth_host": [vp, C.c_int, C.c_int, C.c_int, dp, dp],
             "mhdp_gmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp],
             "mhdp_fgmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp],
@@ -249,6 +250,12 @@ class Context:
 
     def vcycle(self, b, x, level=-1):
         return self._chk(self._L.mhdp_vcycle(self.h, level % self.num_levels(), _ptr(b), _ptr(x)))
+
+    def vcycle_host_batch(self, b, x):
+        """b, x: C-contiguous float64 host arrays of shape (nrhs, n) (pinned for overlap)"""
+        assert b.dtype == np.float64 and x.dtype == np.float64 and b.shape == x.shape and b.ndim == 2
+        assert b.flags.c_contiguous and x.flags.c_contiguous
+        return self._chk(self._L.mhdp_vcycle_host_batch(self.h, b.shape[0], _d(b), _d(x)))
 
     def vcycle_host(self, b, x):
         """b, x: C-contiguous float64 numpy arrays (pinned or pageable host memory)."""

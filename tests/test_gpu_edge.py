@@ -213,3 +213,26 @@ def test_k2_single_level_vcycle_is_coarse_solve(oracle_mod, name, N):
     x = torch.empty(n, dtype=torch.float64, device="cuda:0")
     ctx.vcycle(torch.from_numpy(b).cuda(), x)
     assert np.array_equal(x.cpu().numpy().view(np.uint64), orc.vcycle(b).view(np.uint64))
+
+
+def test_vcycle_host_batch_matches_serial():
+    """mhdp_vcycle_host_batch (copies overlapped on two device slots) returns, for every
+    right-hand side, the bits of mhdp_vcycle_host; nrhs = 0 is a no-op, odd counts and
+    repeated calls reuse the slots' captured graphs."""
+    from paper_2104_14855_b200 import workloads
+    cfg = workloads.small("c5", 6, 2)
+    ctx = _ctx()
+    w, _, _ = workloads.draw(cfg, 1, 2)
+    ctx.assemble(cfg, w)
+    ctx.setup()
+    n = ctx.n()
+    rng = np.random.default_rng(8)
+    B = np.ascontiguousarray(rng.uniform(-1, 1, (5, n)))
+    ref = np.zeros_like(B)
+    for k in range(5):
+        ctx.vcycle_host(np.ascontiguousarray(B[k]), ref[k])
+    for count in (5, 3, 1):
+        X = np.full((count, n), 7.0)
+        ctx.vcycle_host_batch(np.ascontiguousarray(B[:count]), X)
+        assert np.array_equal(X.view(np.uint64), ref[:count].view(np.uint64)), count
+    ctx.vcycle_host_batch(np.zeros((0, n)), np.zeros((0, n)))
