@@ -91,6 +91,14 @@ def main():
     rep["c5"] = level_report(workloads.small("c5", 24, 3))      # levels 1 (12^3) and 2 (24^3) of c5
     rep["c5"].append(c5_finest_sample())
     print("c5", [(r["level"], f'{r["max_kappa"]:.2e}') for r in rep["c5"]], flush=True)
+    # NEXT-2 (k = 2): 2D CG2 x RT2 / BDM2, 3D NED1_2 x RT2 (280-DoF stars) / BDM2 (360)
+    k2 = {"c2k2": dataclasses.replace(workloads.small("c2", 64, 3), degree=2),
+          "c3k2": dataclasses.replace(workloads.small("c3", 64, 3), degree=2, sigma=40.0),
+          "c4k2": dataclasses.replace(workloads.small("c4", 8, 3), degree=2),
+          "c5k2": dataclasses.replace(workloads.small("c5", 8, 3), degree=2, sigma=40.0)}
+    for name, cfg in k2.items():
+        rep[name] = level_report(cfg)
+        print(name, [(r["level"], f'{r["max_kappa"]:.2e}') for r in rep[name]], flush=True)
     rep["seconds"] = time.time() - t0
     json.dump(rep, open(out, "w"), indent=1)
 
