@@ -40,7 +40,6 @@ typedef struct {
     OLevel *lv;
     double *clu;      /* coarse LU (row-major n0*n0) */
     int *cperm;
-    double *cinv;     /* X = A_0^-1 (row-major n0*n0), R-coarse */
     int cstat;        /* status of the coarse factorisation */
     int status;
 } OCtx;
@@ -57,7 +56,7 @@ static void level_free(OLevel *L) {
 void orc_destroy(OCtx *c) {
     if (!c) return;
     for (int l = 0; l < c->nlev; l++) level_free(&c->lv[l]);
-    free(c->lv); free(c->clu); free(c->cperm); free(c->cinv); free(c);
+    free(c->lv); free(c->clu); free(c->cperm); free(c);
 }
 
 /* dparams: Re, Rem, S, gamma, sigma, mu, theta, dt ; iparams: nu_pre, nu_post, picard, degree
@@ -352,9 +351,9 @@ int orc_prolong_add(const OCtx *c, int l, const double *ec, double *x) {
 }
 
 /* ---------------- coarse solve (dense LU, R-coarse) ----------------
- * The coarse operator is factored by R-lu (the stand-in for MUMPS) and its
- * inverse X = A_0^-1 is formed column by column as the R-lu solve of the unit vectors;
- * the coarse solve is x_i = sum_j X_ij b_j in the R-dot order (od_dot of row i).   */
+ * SURVEY 8(c.8) "l = 0: return the coarse LU solve": the coarse operator is factored
+ * by R-lu (od_lu, the stand-in for MUMPS) and every coarse solve is the R-lu
+ * forward/back substitution of c.6 (od_lu_solve) -- no other arithmetic.          */
 static int coarse_factor(OCtx *c) {
     if (c->clu) return c->cstat;
     OLevel *L = &c->lv[0];
@@ -368,23 +367,12 @@ static int coarse_factor(OCtx *c) {
             if (fabs(L->A.v[t]) > amax) amax = fabs(L->A.v[t]);
         }
     c->cstat = od_lu(c->clu, (int)n, c->cperm, amax);
-    if (c->cstat) return c->cstat;
-    c->cinv = malloc(sizeof(double) * (size_t)((n * n) > 0 ? n * n : 1));
-    double *e = calloc((size_t)(n ? n : 1), sizeof(double)), *col = malloc(sizeof(double) * (n ? n : 1));
-    for (i64 j = 0; j < n; j++) {
-        e[j] = 1.0;
-        od_lu_solve(c->clu, (int)n, c->cperm, e, col);
-        e[j] = 0.0;
-        for (i64 i = 0; i < n; i++) c->cinv[i * n + j] = col[i];
-    }
-    free(e); free(col);
-    return 0;
+    return c->cstat;
 }
 
 int orc_coarse_solve(OCtx *c, const double *b, double *x) {
     if (coarse_factor(c)) return 1;
-    i64 n = c->lv[0].s.n;
-    for (i64 i = 0; i < n; i++) x[i] = od_dot(c->cinv + i * n, b, n);
+    od_lu_solve(c->clu, (int)c->lv[0].s.n, c->cperm, b, x);
     return 0;
 }
 
@@ -426,73 +414,17 @@ static int vcycle(OCtx *c, int l, const double *b, double *x) {
 int orc_vcycle(OCtx *c, const double *b, double *x) { return vcycle(c, c->nlev - 1, b, x); }
 int orc_vcycle_level(OCtx *c, int l, const double *b, double *x) { return vcycle(c, l, b, x); }
 
-/* right-preconditioned GMRES (R-gmres). hist[k] = |g_{k}| estimate, k = 0..its */
+/* GMRES(V) (c.9): right-preconditioned by the V-cycle, x0 = 0, modified
+ * Gram-Schmidt, Givens rotations, no restart; stop when |g_{k+1}| <= max(rtol |b|, atol).
+ * The V-cycle is linear (fixed sweep counts), so GMRES that stores Z_k = V v_k is the
+ * same iteration as FGMRES: both run orc_fgmres.  c.9 fixes no reduction order for the
+ * inner products; they follow reading R-dot, so that the residual history
+ * is order-defined and can be compared bit for bit.  hist[k] = |g_k|.   */
+int orc_fgmres(OCtx *c, const double *b, double *x, double rtol, double atol, int maxit, int *its_out,
+               double *hist);
 int orc_gmres(OCtx *c, const double *b, double *x, double rtol, double atol, int maxit, int *its_out,
               double *hist) {
-    OLevel *L = &c->lv[c->nlev - 1];
-    i64 n = L->s.n;
-    double beta = 0;
-    for (i64 i = 0; i < n; i++) beta += b[i] * b[i];
-    beta = sqrt(beta);
-    double tol = rtol * beta > atol ? rtol * beta : atol;
-    for (i64 i = 0; i < n; i++) x[i] = 0.0;
-    hist[0] = beta;
-    *its_out = 0;
-    if (beta <= tol) return 0;
-    double *V = malloc(sizeof(double) * n * (maxit + 1));
-    double *Z = malloc(sizeof(double) * n * maxit);
-    double *H = calloc((size_t)(maxit + 1) * maxit, sizeof(double));
-    double *cs = malloc(sizeof(double) * maxit), *sn = malloc(sizeof(double) * maxit);
-    double *g = calloc((size_t)maxit + 1, sizeof(double));
-    double *w = malloc(sizeof(double) * n);
-    for (i64 i = 0; i < n; i++) V[i] = b[i] / beta;
-    g[0] = beta;
-    int k, conv = 0;
-    for (k = 0; k < maxit; k++) {
-        if (vcycle(c, c->nlev - 1, V + k * n, Z + k * n)) { k = -1; break; }
-        orc_spmv(c, c->nlev - 1, Z + k * n, w);
-        for (int i = 0; i <= k; i++) {
-            double h = 0;
-            for (i64 t = 0; t < n; t++) h += w[t] * V[i * n + t];
-            H[i * maxit + k] = h;
-            for (i64 t = 0; t < n; t++) w[t] -= h * V[i * n + t];
-        }
-        double hn = 0;
-        for (i64 t = 0; t < n; t++) hn += w[t] * w[t];
-        hn = sqrt(hn);
-        H[(k + 1) * maxit + k] = hn;
-        for (i64 t = 0; t < n; t++) V[(k + 1) * n + t] = hn > 0 ? w[t] / hn : 0.0;
-        for (int i = 0; i < k; i++) {
-            double a = H[i * maxit + k], bb = H[(i + 1) * maxit + k];
-            H[i * maxit + k] = cs[i] * a + sn[i] * bb;
-            H[(i + 1) * maxit + k] = -sn[i] * a + cs[i] * bb;
-        }
-        double a = H[k * maxit + k], bb = H[(k + 1) * maxit + k];
-        double rr = sqrt(a * a + bb * bb);
-        cs[k] = a / rr; sn[k] = bb / rr;
-        H[k * maxit + k] = rr; H[(k + 1) * maxit + k] = 0;
-        g[k + 1] = -sn[k] * g[k];
-        g[k] = cs[k] * g[k];
-        hist[k + 1] = fabs(g[k + 1]);
-        if (fabs(g[k + 1]) <= tol) { k++; conv = 1; break; }
-    }
-    int st = 0;
-    if (k < 0) st = 2;
-    else {
-        double *yv = malloc(sizeof(double) * (k > 0 ? k : 1));
-        for (int i = k - 1; i >= 0; i--) {
-            double sacc = g[i];
-            for (int j = i + 1; j < k; j++) sacc -= H[i * maxit + j] * yv[j];
-            yv[i] = sacc / H[i * maxit + i];
-        }
-        for (int i = 0; i < k; i++)
-            for (i64 t = 0; t < n; t++) x[t] += yv[i] * Z[i * n + t];
-        free(yv);
-        *its_out = k;
-        if (!conv) st = 1;
-    }
-    free(V); free(Z); free(H); free(cs); free(sn); free(g); free(w);
-    return st;
+    return orc_fgmres(c, b, x, rtol, atol, maxit, its_out, hist);
 }
 
 /* manufactured-solution helpers: quadrature points/weights of every cell, load

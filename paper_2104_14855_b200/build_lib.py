@@ -17,6 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libmhdp.so")
+PROBE = os.path.join(ROOT, "tools", "libprobe.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -67,6 +68,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         tmp = LIB + ".tmp"
         run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp"])
         os.replace(tmp, LIB)
+    # measurement probes (FP64 peak, dependency latencies): tools/libprobe.so
+    psrc = os.path.join(ROOT, "tools", "probe.cu")
+    if os.path.exists(psrc) and (force or _stale(PROBE, [psrc])):
+        tmp = PROBE + ".tmp"
+        run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", psrc, "-o", tmp])
+        os.replace(tmp, PROBE)
     return LIB
 
 

@@ -226,28 +226,54 @@ def test_vcycle_special_cases(oracle_mod):
     assert np.linalg.norm(v - (3.0 * o2.vcycle(b1) - o2.vcycle(b2))) <= 1e-12 * np.linalg.norm(v)
 
 
-@pytest.mark.parametrize("name,N", [("c1", 8), ("c5", 2)])
-def test_coarse_solve_is_explicit_inverse(oracle_mod, name, N):
-    """R-coarse: column j of X = A_0^-1 is the R-lu solve of e_j (so the coarse solve of
-    e_j returns it exactly: the R-dot row sums against a unit vector are exact), X A_0 = I
-    and X b = A_0^-1 b within the conditioning bound, against numpy's LAPACK solve."""
+def test_lu_exact_on_dyadic_factors():
+    """R-lu on A = Q L U with dyadic L (|l_ij| <= 1/2, unit diagonal) and U (power-of-two
+    diagonal, small dyadic entries): every elimination and substitution step is exact in
+    binary, partial pivoting must pick the unit-l row at every step (so perm recovers Q),
+    and the solve must return the integer x it was built from bit for bit.  A dropped
+    term, a wrong index or a wrong pivot anywhere gives a different x."""
+    from oracle import oracle as om
+    rng = np.random.default_rng(11)
+    for n in (1, 3, 17, 40):
+        L = np.tril(rng.choice([-0.5, -0.25, 0.0, 0.25, 0.5], size=(n, n)), -1) + np.eye(n)
+        U = np.triu(rng.choice([-2.0, -1.0, -0.5, 0.5, 1.0, 2.0], size=(n, n)), 1)
+        U += np.diag(rng.choice([-4.0, -2.0, 2.0, 4.0, 8.0], size=n))
+        Q = rng.permutation(n)
+        A = np.empty((n, n))
+        A[Q] = L @ U                      # row Q[k] of A is row k of L U
+        xt = rng.integers(-9, 10, size=n).astype(float)
+        b = A @ xt
+        x, lu, perm, st = om.dense_lu_solve(A, b)
+        assert st == 0
+        assert list(perm) == list(Q)
+        assert np.array_equal(np.tril(lu, -1), np.tril(L, -1)) and np.array_equal(np.triu(lu), U)
+        assert np.array_equal(x, xt)
+
+
+@pytest.mark.parametrize("name,N", [("c1", 8), ("c5", 2), ("c3", 8)])
+def test_coarse_solve_is_lu_solve(oracle_mod, name, N):
+    """SURVEY 8(c.8) "l = 0: return the coarse LU solve" (stand-in for MUMPS): the
+    coarse solve is the R-lu solve of the coarse operator -- bit-identical to the dense
+    R-lu routine pinned above on the exported operator -- and, against LAPACK's
+    getrf/getrs (same method, another rounding order), a backward-stable solve:
+    ||A x - b|| <= 4 n u ||A|| ||x|| and ||x - x_lapack|| <= 8 n u kappa(A) ||x||."""
     cfg = small(name, N, 1)
     o = make(oracle_mod, cfg)
     n = o.n()
     A = o.csr().to_scipy().toarray()
-    X = np.empty((n, n))
-    for j in range(n):
-        e = np.zeros(n); e[j] = 1.0
-        X[:, j] = o.coarse_solve(e)
-        if j % 17 == 0:
-            assert np.array_equal(X[:, j], oracle_mod.dense_lu_solve(A, e)[0])
+    rng = np.random.default_rng(4)
     u = 2.0 ** -53
-    nA, nX = np.linalg.norm(A, 2), np.linalg.norm(X, 2)
-    # columns are backward-stable solves: ||A X - I|| <= c n u ||A|| ||X||
-    assert np.linalg.norm(A @ X - np.eye(n), 2) <= 4 * n * u * nA * nX
-    b = np.random.default_rng(4).standard_normal(n)
-    ref = np.linalg.solve(A, b)
-    assert np.linalg.norm(o.coarse_solve(b) - ref) <= 4 * n * u * nA * nX * np.linalg.norm(ref)
+    kap = np.linalg.cond(A, 2)
+    for _ in range(3):
+        b = rng.uniform(-1, 1, n)
+        x = o.coarse_solve(b)
+        assert np.array_equal(x, oracle_mod.dense_lu_solve(A, b)[0])
+        nA = np.linalg.norm(A, 2)
+        assert np.linalg.norm(A @ x - b) <= 4 * n * u * nA * np.linalg.norm(x)
+        ref = sla.lu_solve(sla.lu_factor(A), b)
+        assert np.linalg.norm(x - ref) <= 8 * n * u * kap * np.linalg.norm(x)
+    e = np.zeros(n)
+    assert np.array_equal(o.coarse_solve(e), e)            # A^-1 0 = 0 exactly
 
 
 def test_vcycle_two_level_definition(oracle_mod):
