@@ -74,6 +74,15 @@ typedef struct {
                                  E-B CG2 x RT2 (2D) / NED1_2 x RT2 (3D, 280-DoF stars), AL
                                  velocity BDM2 (36 / 360-DoF stars); readings R-basis2,
                                  R-basis2-vel, R-basis2-3D.  Other values -> MHDP_EINVAL       */
+    int weights_mode;         /* update weights w_i of P:538 "sum_i w_i du_i": 0 = by degree
+                                 (k = 1: 1; k = 2: 2), 1 = per-DoF partition of unity
+                                 theta / m_d (SURVEY A2, R-weights), 2 = the uniform
+                                 per-subspace damping theta / max_d m_d (R-weights2)           */
+    int newton_reaction;      /* 0 = Oseen (default); 1 = add the Newton reaction
+                                 (u . grad u^n, v) of Table 1 row F.  With the
+                                 advecting field of reading R-w (constant on every cell) the
+                                 cellwise term is identically zero, so both values assemble
+                                 the same operator (reading R-newton)                        */
 } mhdp_params;
 
 typedef struct mhdp_ctx mhdp_ctx;
@@ -130,11 +139,15 @@ mhdp_status mhdp_load_level(mhdp_ctx *ctx, int level, long long n,
 
 /* Upload the stores and factor them on the device (synchronises): batched patch LU with
  * partial pivoting for every level >= 1 (kernel K6) and the dense
- * coarse LU of level 0 (K7; stand-in for MUMPS) and, from its factors, the explicit
- * coarse inverse X = A_0^-1 (column j = the LU solve of e_j; 8 n_0^2 bytes).  Errors: ESINGULAR names the
- * level and patch (mhdp_last_error's `where` = level*2^32 + patch; patch -1 = coarse). */
+ * coarse LU of level 0 (K7; stand-in for MUMPS) and, from its factors, the
+ * K8 substitution tiles (k8_coarse.cu).  Errors: ESINGULAR for a singular
+ * star names its mesh vertex (mhdp_last_error's `where` = the vertex id,
+ * the message names the level), or the patch index for operators installed by
+ * mhdp_load_level; `where` = -1 for a singular coarse operator.                        */
 mhdp_status mhdp_setup(mhdp_ctx *ctx);
 
+/* SURVEY 8(b) names this call mhdp_level_info, but that is also the name of the struct
+ * typedef (one C identifier namespace), so the call carries a get_ prefix.             */
 mhdp_status mhdp_get_level_info(const mhdp_ctx *ctx, int level, mhdp_level_info *out);
 int         mhdp_num_levels(const mhdp_ctx *ctx);
 
@@ -159,9 +172,17 @@ mhdp_status mhdp_smooth(mhdp_ctx *ctx, int level, int nsweeps, int x_is_zero,
 mhdp_status mhdp_restrict(mhdp_ctx *ctx, int level, const double *r_dev, double *rc_dev);
 /* x <- x + P_l ec (K5, prolongation from level-1)                                      */
 mhdp_status mhdp_prolong_add(mhdp_ctx *ctx, int level, const double *ec_dev, double *x_dev);
-/* x = A_0^{-1} b (K8): x_i = sum_j X_ij b_j with X from the coarse LU, each row summed in
- * the R-dot order (reading R-coarse).  b and x must not alias.                         */
+/* x = A_0^{-1} b (K8): the coarse LU solve of SURVEY 8(c.8) (stand-in for MUMPS)
+ * -- z = P b, forward z_i <- fma(-l_ij, z_j, z_i) (j ascending), back z_j <- z_j / u_jj,
+ * z_i <- fma(-u_ij, z_j, z_i) (j descending), c.6 -- bit-identical to that unblocked
+ * sequence.  b and x are device vectors of n_0 doubles; they may alias (b is copied).   */
 mhdp_status mhdp_coarse_solve(mhdp_ctx *ctx, const double *b_dev, double *x_dev);
+/* Diagnostics: one mhdp_coarse_solve (b, x must not alias) with K8's per-block
+ * globaltimer stamps (ns) written to trace_host[(pass * nb + block) * 5 + k], nb =
+ * ceil(n_0 / 32), pass 0 forward / 1 back, k = 0 claim start, 1 claim done, 2 chain
+ * start, 3 chain done (chain CTA), 4 far-warp hand-off.  Synchronises.                 */
+mhdp_status mhdp_coarse_solve_trace(mhdp_ctx *ctx, const double *b_dev, double *x_dev,
+                                    long long *trace_host);
 /* x = V_l(b) with zero initial guess on level `level` (finest: n_levels-1), P:643:
  * nu_pre sweeps, residual, restrict, recurse, prolong-add, nu_post sweeps.  Repeated
  * calls with the same (level, b, x) replay a CUDA graph of the cycle (captured on the
@@ -183,12 +204,17 @@ mhdp_status mhdp_vcycle_host_batch(mhdp_ctx *ctx, int nrhs, const double *b_host
 /* Smoother sweeps with host buffers (b, x in/out; synchronises).                       */
 mhdp_status mhdp_smooth_host(mhdp_ctx *ctx, int level, int nsweeps, int x_is_zero,
                              const double *b_host, double *x_host);
-/* Right-preconditioned GMRES with the V-cycle on the finest level, x0 = 0, modified
- * Gram-Schmidt, no restart: stops when the residual estimate <=
- * max(rtol |b|, atol).  its_out = iterations, relres_out = estimate / |b|.
- * Synchronises every iteration.  Returns ENOCONV at maxit.                              */
+/* Right-preconditioned GMRES with the V-cycle on the finest level (P:625,
+ * P:654): x0 = 0, modified Gram-Schmidt (w <- fma(-h, v, w)), v = w / |w|, Givens
+ * rotations, no restart; inner products in the pinned order of reading R-dot, so the
+ * iteration is the oracle's step for step.  Stops when the residual estimate |g_k| <=
+ * max(rtol |b|, atol).  its_out = iterations, relres_out = |g_its| / |b|, hist_out
+ * (optional, host, maxit + 1 doubles) = the residual history |g_k|, k = 0..its
+ * (compared when either side does not converge).  1 <= maxit <= 2000.
+ * Synchronises every iteration.  Returns ENOCONV at maxit (x holds the iterate).        */
 mhdp_status mhdp_gmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol,
-                       double atol, int maxit, int *its_out, double *relres_out);
+                       double atol, int maxit, int *its_out, double *relres_out,
+                       double *hist_out);
 
 /* Switch the V-cycle smoother (see mhdp_params.smoother / smoother_its); may be called
  * before or after mhdp_setup (the GMRES workspace is allocated on demand).             */
@@ -198,7 +224,8 @@ mhdp_status mhdp_set_smoother(mhdp_ctx *ctx, int smoother, int smoother_its);
  * nonlinear); x0 = 0; inner products in the pinned order of reading R-dot; stops when
  * the residual estimate <= max(rtol |b|, atol).  Synchronises every iteration. */
 mhdp_status mhdp_fgmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol,
-                        double atol, int maxit, int *its_out, double *relres_out);
+                        double atol, int maxit, int *its_out, double *relres_out,
+                        double *hist_out);   /* as mhdp_gmres (same iteration) */
 /* The pinned inner product of reading R-dot of two device vectors (synchronises; n = 0
  * gives +0.0 and the pointers may then be NULL).                                       */
 mhdp_status mhdp_dot(mhdp_ctx *ctx, const double *a_dev, const double *b_dev, long long n,
@@ -208,6 +235,9 @@ mhdp_status mhdp_dot(mhdp_ctx *ctx, const double *a_dev, const double *b_dev, lo
 mhdp_status mhdp_export_csr(const mhdp_ctx *ctx, int level, long long *rowptr, int *col,
                             double *val);
 mhdp_status mhdp_export_patches(const mhdp_ctx *ctx, int level, long long *pptr, int *pdofs);
+/* verts[i] = the mesh vertex whose star is patch i (R-patch: non-empty stars in vertex
+ * order); npatch ints.  ESTATE for levels installed by mhdp_load_level.          */
+mhdp_status mhdp_export_patch_vertices(const mhdp_ctx *ctx, int level, int *verts);
 mhdp_status mhdp_export_prolongation(const mhdp_ctx *ctx, int level, long long *prow,
                                      int *pcol, double *pval);
 /* Patch `patch` of `level` after setup (synchronises): its LU factors, row-major n_i x n_i

@@ -34,6 +34,7 @@ typedef struct {
 typedef struct {
     int block, dim, nlev;
     int degree;       /* element degree k (NEXT-2) */
+    int weights_mode; /* 0 by degree, 1 per-DoF 1/m_d, 2 uniform 1/max m_d */
     OParams p;
     double theta;
     int smoother, smoother_its;   /* 0: nu_pre / nu_post Richardson sweeps; 1: GMRES(m) (NEXT-1) */
@@ -77,6 +78,12 @@ OCtx *orc_create_masked(int block, int dim, int N, int nlev, const double *dpara
     int degree = iparams[3];
     if (!(degree == 1 || degree == 2)) { free(c); return NULL; }
     c->degree = degree;
+    /* iparams[4] weights_mode (0 by degree, 1 per-DoF 1/m_d, 2 uniform 1/max m_d);
+     * iparams[5] newton_reaction: (u . grad u^n, v) of Table 1 row F -- R-w makes
+     * u^n constant on every cell, so the cellwise term is identically zero (reading
+     * R-newton): the flag is accepted and the operator is unchanged                      */
+    c->weights_mode = iparams[4];
+    if (c->weights_mode < 0 || c->weights_mode > 2 || iparams[5] < 0 || iparams[5] > 1) { free(c); return NULL; }
     c->lv = calloc((size_t)nlev, sizeof(OLevel));
     int lo = cmask_fine ? nlev - 1 : 0;
     for (int l = nlev - 1; l >= lo; l--) {
@@ -251,7 +258,9 @@ int orc_patch_lu(OCtx *c, int l, i64 i, double *lu, int *perm) {
  * which keeps every local kernel correction in the kernel (at k = 2 the multiplicities
  * differ inside a patch: facet DoFs 2, cell DoFs 3, so 1/m_d would not).            */
 static double dof_weight(const OCtx *c, const OPatches *pt, i64 d) {
-    if (c->degree == 2) return c->theta * (1.0 / (pt->mmax > 0 ? pt->mmax : 1));
+    /* weights_mode: 1 = per-DoF 1/m_d, 2 = uniform 1/max m_d, 0 = by degree */
+    const int uniform = c->weights_mode == 2 || (c->weights_mode == 0 && c->degree == 2);
+    if (uniform) return c->theta * (1.0 / (pt->mmax > 0 ? pt->mmax : 1));
     return c->theta * (1.0 / pt->mult[d]);
 }
 

@@ -151,7 +151,8 @@ class Oracle:
         self.N = N
         dp = np.array([cfg.Re, cfg.Rem, cfg.S, cfg.gamma, cfg.sigma, cfg.mu, cfg.theta,
                        getattr(cfg, "dt", 0.0)], dtype=np.float64)
-        ip = np.array([cfg.nu, cfg.nu, int(getattr(cfg, "picard", 0)), int(getattr(cfg, "degree", 1))],
+        ip = np.array([cfg.nu, cfg.nu, int(getattr(cfg, "picard", 0)), int(getattr(cfg, "degree", 1)),
+                       int(getattr(cfg, "weights_mode", 0)), int(getattr(cfg, "newton_reaction", 0))],
                       dtype=np.int32)
         self._w = np.ascontiguousarray(w, dtype=np.float64)
         self._bn = None if bn is None else np.ascontiguousarray(bn, dtype=np.float64)
@@ -382,7 +383,8 @@ class CoupledOracle:
         self._L = L = lib(exact)
         dp = np.array([cfg.Re, cfg.Rem, cfg.S, cfg.gamma, cfg.sigma, cfg.mu, cfg.theta,
                        getattr(cfg, "dt", 0.0)], dtype=np.float64)
-        ip = np.array([cfg.nu, cfg.nu, int(getattr(cfg, "picard", 0)), int(getattr(cfg, "degree", 1))],
+        ip = np.array([cfg.nu, cfg.nu, int(getattr(cfg, "picard", 0)), int(getattr(cfg, "degree", 1)),
+                       int(getattr(cfg, "weights_mode", 0)), int(getattr(cfg, "newton_reaction", 0))],
                       dtype=np.int32)
         self._w = np.ascontiguousarray(w, np.float64)
         self._bn = None if bn is None else np.ascontiguousarray(bn, np.float64)

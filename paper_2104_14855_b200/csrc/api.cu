@@ -58,9 +58,13 @@ struct mhdp_ctx {
     bool setup_done = false;
     // coarse factor
     int n0 = 0;
-    double *cinv = nullptr;    // X = A_0^-1, column-major (R-coarse)
-    int *cperm = nullptr;
-    double *cpart = nullptr;   // n0 * ceil(n0/256) partial sums of x = X b
+    int *cperm = nullptr;      // R-lu row permutation of the coarse operator
+    double *ctile = nullptr;   // K8 factor tiles of both substitution passes (k8_coarse.cu)
+    double *crec = nullptr;    // K8 mini-block coefficient records
+    double *czf = nullptr;     // forward-pass z (global copy for K8's far warps)
+    double *chacc = nullptr;   // K8 far-warp partial sums
+    double *cb = nullptr;      // copy of b when a caller aliases b and x
+    unsigned long long *csync = nullptr;   // K8 epoch / progress / hand-off flags
     // scratch
     int *d_status = nullptr;
     double *d_scal = nullptr;  // dot partials + results
@@ -68,9 +72,7 @@ struct mhdp_ctx {
     std::string err;
     long long where = -1;
     long long launches0 = 0;
-    // gmres workspace
-    double *gV = nullptr, *gZ = nullptr, *gw = nullptr;
-    int g_cap = 0;
+    double *vh = nullptr;      // mhdp_vcycle_host: device x of the finest level
     // fgmres workspace
     double *fV = nullptr, *fZ = nullptr, *fw = nullptr, *fpart = nullptr, *fscal = nullptr;
     int f_cap = 0;
@@ -116,6 +118,17 @@ struct TmpDev {
             return fail(ctx, MHDP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+// setup copies are stream-ordered on the context stream (which may be a non-blocking
+// stream) and complete before returning, so pageable host buffers may be freed at once
+cudaError_t h2d(const mhdp_ctx *ctx, void *dst, const void *src, size_t bytes) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(ctx->stream);
+}
+cudaError_t d2h(const mhdp_ctx *ctx, void *dst, const void *src, size_t bytes) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(ctx->stream);
+}
+
 template <class T>
 mhdp_status dalloc(mhdp_ctx *ctx, T **p, int64_t count) {
     *p = nullptr;
@@ -133,7 +146,7 @@ template <class T>
 mhdp_status upload(mhdp_ctx *ctx, T **p, const T *src, int64_t count) {
     mhdp_status st = dalloc(ctx, p, count);
     if (st) return st;
-    if (count > 0) CK(cudaMemcpy(*p, src, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice));
+    if (count > 0) CK(h2d(ctx, *p, src, sizeof(T) * (size_t)count));
     return MHDP_OK;
 }
 
@@ -157,10 +170,10 @@ void free_device(mhdp_ctx *c) {
     for (void *p : c->allocs) cudaFree(p);
     c->allocs.clear();
     c->D.clear();
-    c->cinv = nullptr; c->cperm = nullptr; c->cpart = nullptr;
+    c->cperm = nullptr; c->ctile = c->crec = c->czf = c->chacc = c->cb = nullptr; c->csync = nullptr;
     c->d_status = nullptr; c->d_scal = nullptr;
-    c->gV = c->gZ = c->gw = nullptr; c->g_cap = 0;
     c->fV = c->fZ = c->fw = c->fpart = c->fscal = nullptr; c->f_cap = 0;
+    c->vh = nullptr;
     c->hb[0] = c->hb[1] = c->hx[0] = c->hx[1] = nullptr;
     c->setup_done = false;
 }
@@ -237,9 +250,8 @@ mhdp_status build_b3(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
     }
     const int64_t stored = sptr[ns];
     // value layout: the 9 x 32 values of one (slice, block column) contiguous (one DRAM run
-    // per warp iteration), or 9 separate planes (MHDP_K1_PLANES=1, A/B)
-    const char *pe = getenv("MHDP_K1_PLANES");
-    const int planes = pe && pe[0] == '1';
+    // per warp iteration; 9 separate planes measured 3% slower, profiles/r01_c5_k1_layout_ab.jsonl)
+    const int planes = 0;
     std::vector<int> col(stored, 0);
     std::vector<double> val(9 * stored, 0.0);
     for (int64_t R = 0; R < nb; ++R) {
@@ -322,11 +334,13 @@ mhdp_status build_patches(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
     for (int64_t t = 0; t < sum_n; ++t) dslot[fill[H.pdofs[t]]++] = (int)t;   // ascending slot = ascending patch
     // R-weights (k = 1): theta / m_d;  R-weights2 (k = 2): the uniform theta / max_d m_d (a
     // per-subspace damping parameter of P:538 that keeps local kernel corrections in the kernel)
+    // weights_mode: 1 per-DoF, 2 uniform, 0 by degree
+    const bool uniform = ctx->p.weights_mode == 2 || (ctx->p.weights_mode == 0 && ctx->p.degree == 2);
     int mmax = 1;
     for (int64_t d = 0; d < H.n; ++d) mmax = std::max(mmax, mult[d]);
     std::vector<double> wd(H.n);
     for (int64_t d = 0; d < H.n; ++d)
-        wd[d] = ctx->p.theta * (1.0 / (ctx->p.degree == 2 ? mmax : mult[d]));
+        wd[d] = ctx->p.theta * (1.0 / (uniform ? mmax : mult[d]));
     mhdp_status st;
     if ((st = upload(ctx, &P.pn, pn.data(), np))) return st;
     if ((st = upload(ctx, &P.poff, H.pptr.data(), np))) return st;
@@ -355,15 +369,14 @@ mhdp_status build_patches(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
 }
 
 // small stars: group the patches 32 at a time by size and interleave their factor streams
-// (K2 thread-per-patch kernel; MHDP_K2_LANES=0 disables it for A/B timing)
+// (K2 thread-per-patch kernel)
 mhdp_status build_lane_groups(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
     DevPatches &P = L.P;
-    const char *e = getenv("MHDP_K2_LANES");
     // measured (tools/level_profile.py, profiles/r01_k2_lring_ab.jsonl): the ring-fed
     // thread-per-patch kernel wins wherever the level has enough 32-patch groups to keep
     // every warp busy (a group of 31/36-DoF stars is a ~40-50 us chain per thread), or
     // the stars are small: k = 2 E-B finest 5.7 vs 2.8 TB/s, c3 finest 4.6 vs 2.0 TB/s
-    if ((e && e[0] == '0') || P.np == 0) return MHDP_OK;
+    if (P.np == 0) return MHDP_OK;
     if (!(P.max_n <= 16 || P.np >= 40000)) return MHDP_OK;
     for (int64_t i = 0; i < P.np; ++i)
         if (!lring_size_supported((int)(H.pptr[i + 1] - H.pptr[i]))) return MHDP_OK;
@@ -418,7 +431,12 @@ void sweep(mhdp_ctx *ctx, int l, const double *b, double *x, bool x_zero) {
 }
 
 void coarse_solve(mhdp_ctx *ctx, const double *b, double *x) {
-    launch_coarse_apply(ctx->cinv, ctx->n0, b, x, ctx->cpart, ctx->stream);
+    if (b == x) {   // K8 reads b while it writes x
+        cudaMemcpyAsync(ctx->cb, b, sizeof(double) * ctx->n0, cudaMemcpyDeviceToDevice, ctx->stream);
+        b = ctx->cb;
+    }
+    launch_k8_solve(ctx->ctile, ctx->crec, ctx->cperm, ctx->n0, b, x, ctx->czf, ctx->chacc, ctx->csync,
+                    ctx->stream);
 }
 
 // scalar workspace layout of a GMRES(m) smoother / FGMRES(m)
@@ -591,6 +609,11 @@ static mhdp_status check_params(mhdp_ctx *ctx, const mhdp_params *pr) {
     ctx->p.dt = pr->dt; ctx->p.picard = pr->picard;
     if (pr->degree < 0 || pr->degree > 2) return fail(ctx, MHDP_EINVAL, "degree must be 1 or 2");
     ctx->p.degree = pr->degree == 0 ? 1 : pr->degree;
+    if (pr->weights_mode < 0 || pr->weights_mode > 2) return fail(ctx, MHDP_EINVAL, "weights_mode must be 0, 1 or 2");
+    if (pr->newton_reaction != 0 && pr->newton_reaction != 1)
+        return fail(ctx, MHDP_EINVAL, "newton_reaction must be 0 or 1");
+    ctx->p.weights_mode = pr->weights_mode;
+    ctx->p.newton_reaction = pr->newton_reaction;   // zero cellwise under R-w (reading R-newton)
     return MHDP_OK;
 }
 
@@ -710,11 +733,11 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         int64_t *drp = buf_rp.p;
         int *dci = buf_ci.p;
         double *dv = buf_v.p;
-        CK(cudaMemcpy(drp, H.rp.data(), sizeof(int64_t) * (H.n + 1), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(dci, H.ci.data(), sizeof(int) * L.nnz, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(dv, H.v.data(), sizeof(double) * L.nnz, cudaMemcpyHostToDevice));
+        CK(h2d(ctx, drp, H.rp.data(), sizeof(int64_t) * (H.n + 1)));
+        CK(h2d(ctx, dci, H.ci.data(), sizeof(int) * L.nnz));
+        CK(h2d(ctx, dv, H.v.data(), sizeof(double) * L.nnz));
         int big = INT_MAX;
-        CK(cudaMemcpy(ctx->d_status, &big, sizeof(int), cudaMemcpyHostToDevice));
+        CK(h2d(ctx, ctx->d_status, &big, sizeof(int)));
         TmpDev<double> buf_lu;            // K6 scratch for stars beyond shared memory
         const int64_t nscr = patch_lu_scratch_doubles(L.P);
         if (nscr) CK(cudaMalloc(&buf_lu.p, sizeof(double) * nscr));
@@ -722,19 +745,24 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         if ((st = check_launch(ctx))) return st;
         CK(cudaStreamSynchronize(ctx->stream));
         int bad = 0;
-        CK(cudaMemcpy(&bad, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost));
+        CK(d2h(ctx, &bad, ctx->d_status, sizeof(int)));
         if (bad != INT_MAX) {
             const long long patch = bad - 1;
             char buf[160];
-            snprintf(buf, sizeof buf, "singular patch %lld on level %d", patch, l);
-            return fail(ctx, MHDP_ESINGULAR, buf, ((long long)l << 32) + patch);
+            // ESINGULAR names the vertex whose star is singular (mesh path);
+            // for operators installed by mhdp_load_level the patch index stands in for it
+            const bool have_v = (int64_t)H.pvert.size() > patch;
+            const long long vid = have_v ? H.pvert[patch] : patch;
+            snprintf(buf, sizeof buf, "singular patch %lld (%s %lld) on level %d", patch,
+                     have_v ? "vertex" : "patch", vid, l);
+            return fail(ctx, MHDP_ESINGULAR, buf, vid);
         }
         if ((st = build_lane_groups(ctx, H, L))) return st;
     }
-    // K7: coarse LU (dense, row-major), then K8 setup: X = A_0^-1 from the factors
+    // K7: coarse LU (dense, row-major, R-lu), then the K8 tiles of both substitution passes
     const HostLevel &H0 = ctx->H[0];
     const int64_t n0 = H0.n;
-    if (n0 > 20000) return fail(ctx, MHDP_EINVAL, "coarse level too large for the dense LU");
+    if (n0 > k8_max_n()) return fail(ctx, MHDP_EINVAL, "coarse level too large for the dense LU");
     ctx->n0 = (int)n0;
     {
         std::vector<double> dense((size_t)(n0 * n0), 0.0);
@@ -743,18 +771,23 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         TmpDev<double> buf_a;
         CK(cudaMalloc(&buf_a.p, sizeof(double) * std::max<int64_t>(1, n0 * n0)));
         double *a = buf_a.p;
-        CK(cudaMemcpy(a, dense.data(), sizeof(double) * n0 * n0, cudaMemcpyHostToDevice));
+        CK(h2d(ctx, a, dense.data(), sizeof(double) * n0 * n0));
+        const int64_t nbp = (n0 + 31) / 32 * 32;
         if ((st = dalloc(ctx, &ctx->cperm, n0))) return st;
-        if ((st = dalloc(ctx, &ctx->cinv, n0 * n0))) return st;
-        if ((st = dalloc(ctx, &ctx->cpart, n0 * ((n0 + 255) / 256)))) return st;
-        CK(cudaMemset(ctx->d_status, 0, sizeof(int)));
+        if ((st = dalloc(ctx, &ctx->ctile, k8_tile_doubles((int)n0)))) return st;
+        if ((st = dalloc(ctx, &ctx->crec, k8_rec_doubles((int)n0)))) return st;
+        if ((st = dalloc(ctx, &ctx->czf, nbp))) return st;
+        if ((st = dalloc(ctx, &ctx->chacc, 2 * nbp))) return st;
+        if ((st = dalloc(ctx, &ctx->cb, nbp))) return st;
+        if ((st = dalloc(ctx, &ctx->csync, k8_sync_words((int)n0)))) return st;
+        CK(cudaMemsetAsync(ctx->csync, 0, sizeof(unsigned long long) * k8_sync_words((int)n0), ctx->stream));
+        CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int), ctx->stream));
         launch_dense_lu(a, (int)n0, ctx->cperm, ctx->d_status, ctx->d_scal, ctx->stream);
         if ((st = check_launch(ctx))) return st;
-        CK(cudaStreamSynchronize(ctx->stream));
         int bad = 0;
-        CK(cudaMemcpy(&bad, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost));
+        CK(d2h(ctx, &bad, ctx->d_status, sizeof(int)));
         if (bad) return fail(ctx, MHDP_ESINGULAR, "singular coarse operator", -1);
-        launch_coarse_inverse(a, ctx->cperm, (int)n0, ctx->cinv, ctx->stream);
+        launch_k8_pack(a, (int)n0, ctx->ctile, ctx->crec, ctx->stream);
         if ((st = check_launch(ctx))) return st;
         CK(cudaStreamSynchronize(ctx->stream));
     }
@@ -784,7 +817,7 @@ mhdp_status mhdp_get_level_info(const mhdp_ctx *ctx, int level, mhdp_level_info 
     if (ctx->setup_done) {
         const DevLevel &L = ctx->D[level];
         out->bytes_operator = L.bytes_op;
-        out->bytes_factors = level > 0 ? L.bytes_fac : 8LL * ctx->n0 * ctx->n0;
+        out->bytes_factors = level > 0 ? L.bytes_fac : 8LL * k8_tile_doubles(ctx->n0);
         out->bytes_transfer = L.bytes_tr;
     }
     return MHDP_OK;
@@ -844,6 +877,23 @@ mhdp_status mhdp_prolong_add(mhdp_ctx *ctx, int level, const double *ec_dev, dou
     if (st) return st;
     if (!valid_level(ctx, level) || level < 1 || !ec_dev || !x_dev) return fail(ctx, MHDP_EINVAL, "bad arguments");
     launch_prolong_add(ctx->D[level].Pr, ec_dev, x_dev, ctx->stream);
+    return check_launch(ctx);
+}
+
+// diagnostics: one coarse solve with K8's per-block globaltimer stamps (ns) copied to
+// trace_host[(pass * nb + block) * 5 + k], k = claim start, claim+diag staged, chain start,
+// chain done (CTA 0), far-warp publish; nb = ceil(n0 / 32).  Synchronises.
+mhdp_status mhdp_coarse_solve_trace(mhdp_ctx *ctx, const double *b_dev, double *x_dev, long long *trace_host) {
+    mhdp_status st = need_setup(ctx);
+    if (st) return st;
+    if (!b_dev || !x_dev || !trace_host || b_dev == x_dev) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    const int64_t cnt = 32 * (int64_t)((ctx->n0 + 31) / 32);
+    TmpDev<long long> tr;
+    CK(cudaMalloc(&tr.p, sizeof(long long) * std::max<int64_t>(1, cnt)));
+    CK(cudaMemsetAsync(tr.p, 0, sizeof(long long) * std::max<int64_t>(1, cnt), ctx->stream));
+    CK(launch_k8_solve(ctx->ctile, ctx->crec, ctx->cperm, ctx->n0, b_dev, x_dev, ctx->czf, ctx->chacc, ctx->csync,
+                       ctx->stream, tr.p));
+    CK(d2h(ctx, trace_host, tr.p, sizeof(long long) * cnt));
     return check_launch(ctx);
 }
 
@@ -923,8 +973,8 @@ mhdp_status mhdp_vcycle_host(mhdp_ctx *ctx, const double *b_host, double *x_host
     double *db = L.b, *dx = nullptr;
     if (l == 0) dx = L.x;
     else {
-        if (!ctx->gw) { if ((st = dalloc(ctx, &ctx->gw, L.n))) return st; }
-        dx = ctx->gw;
+        if (!ctx->vh) { if ((st = dalloc(ctx, &ctx->vh, L.n))) return st; }
+        dx = ctx->vh;
     }
     CK(cudaMemcpyAsync(db, b_host, sizeof(double) * L.n, cudaMemcpyHostToDevice, ctx->stream));
     vcycle(ctx, l, db, dx);
@@ -968,7 +1018,12 @@ mhdp_status mhdp_vcycle_host_batch(mhdp_ctx *ctx, int nrhs, const double *b_host
         CK(cudaEventRecord(ctx->ev_in[t], ctx->s_in));
         CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[t], 0));
         if (k >= 2) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_out[t], 0));
-        if ((st = mhdp_vcycle(ctx, l, ctx->hb[t], ctx->hx[t]))) return st;
+        if ((st = mhdp_vcycle(ctx, l, ctx->hb[t], ctx->hx[t]))) {
+            // copies of earlier right-hand sides still point into the caller's buffers
+            cudaStreamSynchronize(ctx->s_in);
+            cudaStreamSynchronize(ctx->s_out);
+            return st;
+        }
         CK(cudaEventRecord(ctx->ev_done[t], ctx->stream));
         CK(cudaStreamWaitEvent(ctx->s_out, ctx->ev_done[t], 0));
         CK(cudaMemcpyAsync(x_host + (int64_t)k * n, ctx->hx[t], bytes, cudaMemcpyDeviceToHost, ctx->s_out));
@@ -991,77 +1046,6 @@ mhdp_status mhdp_smooth_host(mhdp_ctx *ctx, int level, int nsweeps, int x_is_zer
     CK(cudaMemcpyAsync(x_host, L.x, sizeof(double) * L.n, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return check_launch(ctx);
-}
-
-mhdp_status mhdp_gmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol, double atol, int maxit,
-                       int *its_out, double *relres_out) {
-    mhdp_status st = need_setup(ctx);
-    if (st) return st;
-    if (!b_dev || !x_dev || maxit < 1 || maxit > 2000) return fail(ctx, MHDP_EINVAL, "bad arguments");
-    const int l = ctx->nlev - 1;
-    const int64_t n = ctx->D[l].n;
-    cudaStream_t s = ctx->stream;
-    if (ctx->g_cap < maxit) {
-        if ((st = dalloc(ctx, &ctx->gV, n * (int64_t)(maxit + 1)))) return st;
-        if ((st = dalloc(ctx, &ctx->gZ, n * (int64_t)maxit))) return st;
-        if (!ctx->gw && (st = dalloc(ctx, &ctx->gw, n))) return st;
-        ctx->g_cap = maxit;
-    }
-    double *V = ctx->gV, *Z = ctx->gZ, *w = ctx->gw, *part = ctx->d_scal, *res = ctx->d_scal + 1024;
-    auto dot = [&](const double *a, const double *b) -> double {
-        launch_dot(a, b, n, part, res, s);
-        double h = 0;
-        cudaMemcpyAsync(&h, res, sizeof(double), cudaMemcpyDeviceToHost, s);
-        cudaStreamSynchronize(s);
-        return h;
-    };
-    const double beta = std::sqrt(dot(b_dev, b_dev));
-    const double tol = std::max(rtol * beta, atol);
-    launch_fill(x_dev, 0.0, n, s);
-    if (its_out) *its_out = 0;
-    if (relres_out) *relres_out = beta > 0 ? 1.0 : 0.0;
-    if (beta <= tol) { CK(cudaStreamSynchronize(s)); return check_launch(ctx); }
-    std::vector<double> H((size_t)(maxit + 1) * maxit, 0.0), cs(maxit), sn(maxit), g(maxit + 1, 0.0);
-    launch_scale(V, b_dev, 1.0 / beta, n, s);
-    g[0] = beta;
-    int k = 0;
-    bool conv = false;
-    for (k = 0; k < maxit; ++k) {
-        vcycle(ctx, l, V + (int64_t)k * n, Z + (int64_t)k * n);
-        residual(ctx, l, nullptr, Z + (int64_t)k * n, w);
-        for (int i = 0; i <= k; ++i) {
-            const double h = dot(w, V + (int64_t)i * n);
-            H[(size_t)i * maxit + k] = h;
-            launch_axpy(w, -h, V + (int64_t)i * n, n, s);
-        }
-        const double hn = std::sqrt(dot(w, w));
-        H[(size_t)(k + 1) * maxit + k] = hn;
-        launch_scale(V + (int64_t)(k + 1) * n, w, hn > 0 ? 1.0 / hn : 0.0, n, s);
-        for (int i = 0; i < k; ++i) {
-            const double a = H[(size_t)i * maxit + k], bb = H[(size_t)(i + 1) * maxit + k];
-            H[(size_t)i * maxit + k] = cs[i] * a + sn[i] * bb;
-            H[(size_t)(i + 1) * maxit + k] = -sn[i] * a + cs[i] * bb;
-        }
-        const double a = H[(size_t)k * maxit + k], bb = H[(size_t)(k + 1) * maxit + k];
-        const double rr = std::sqrt(a * a + bb * bb);
-        cs[k] = a / rr; sn[k] = bb / rr;
-        H[(size_t)k * maxit + k] = rr; H[(size_t)(k + 1) * maxit + k] = 0.0;
-        g[k + 1] = -sn[k] * g[k];
-        g[k] = cs[k] * g[k];
-        if (std::fabs(g[k + 1]) <= tol) { ++k; conv = true; break; }
-    }
-    std::vector<double> y(std::max(k, 1));
-    for (int i = k - 1; i >= 0; --i) {
-        double acc = g[i];
-        for (int j = i + 1; j < k; ++j) acc -= H[(size_t)i * maxit + j] * y[j];
-        y[i] = acc / H[(size_t)i * maxit + i];
-    }
-    for (int i = 0; i < k; ++i) launch_axpy(x_dev, y[i], Z + (int64_t)i * n, n, s);
-    CK(cudaStreamSynchronize(s));
-    if (its_out) *its_out = k;
-    if (relres_out) *relres_out = std::fabs(g[k]) / beta;
-    if ((st = check_launch(ctx))) return st;
-    return conv ? MHDP_OK : fail(ctx, MHDP_ENOCONV, "GMRES reached maxit");
 }
 
 mhdp_status mhdp_set_smoother(mhdp_ctx *ctx, int smoother, int smoother_its) {
@@ -1088,11 +1072,17 @@ int mhdp_vcycle_graphs_active(const mhdp_ctx *ctx) {
     return n;
 }
 
-mhdp_status mhdp_fgmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol, double atol, int maxit,
-                        int *its_out, double *relres_out) {
+// Right-preconditioned (F)GMRES on the finest level (c.9): x0 = 0, modified
+// Gram-Schmidt (w <- fma(-h, v, w)), v_{k+1} = w / |w|, Givens rotations on the device
+// with every product and sum rounded separately, inner products in the R-dot order --
+// the oracle's orc_fgmres step for step.  With the Richardson smoother the V-cycle is
+// linear and this is GMRES(V) (a8); with the GMRES(6) smoother it is FGMRES (NEXT-1).
+// hist (host, optional, maxit + 1): hist[k] = |g_k|, k = 0..its.
+mhdp_status krylov_solve(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol, double atol, int maxit,
+                         int *its_out, double *relres_out, double *hist) {
     mhdp_status st = need_setup(ctx);
     if (st) return st;
-    if (!b_dev || !x_dev || maxit < 1 || maxit > 1000) return fail(ctx, MHDP_EINVAL, "bad arguments");
+    if (!b_dev || !x_dev || maxit < 1 || maxit > 2000) return fail(ctx, MHDP_EINVAL, "bad arguments");
     const int l = ctx->nlev - 1;
     const int64_t n = ctx->D[l].n;
     cudaStream_t s = ctx->stream;
@@ -1118,6 +1108,7 @@ mhdp_status mhdp_fgmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, doubl
     launch_fill(x_dev, 0.0, n, s);
     const double beta = read(S.g);
     const double tol = std::max(rtol * beta, atol);
+    if (hist) hist[0] = beta;
     if (its_out) *its_out = 0;
     if (relres_out) *relres_out = beta > 0 ? 1.0 : 0.0;
     if (beta <= tol) return check_launch(ctx);
@@ -1135,6 +1126,7 @@ mhdp_status mhdp_fgmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, doubl
         launch_dot_pinned(w, w, n, ctx->fpart, S.hn + k, 1, s);
         launch_givens(S.H, m, S.cs, S.sn, S.g, S.hn + k, k, nullptr, s);
         gk = std::fabs(read(S.g + k + 1));
+        if (hist) hist[k + 1] = gk;
         if (gk <= tol) { ++k; conv = true; break; }
         if (read(S.hn + k) == 0.0) { ++k; break; }
         launch_div_dev(V + (int64_t)(k + 1) * n, w, S.hn + k, n, s);
@@ -1145,7 +1137,17 @@ mhdp_status mhdp_fgmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, doubl
     if (its_out) *its_out = k;
     if (relres_out) *relres_out = gk / beta;
     if ((st = check_launch(ctx))) return st;
-    return conv ? MHDP_OK : fail(ctx, MHDP_ENOCONV, "FGMRES reached maxit");
+    return conv ? MHDP_OK : fail(ctx, MHDP_ENOCONV, "GMRES reached maxit");
+}
+
+mhdp_status mhdp_gmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol, double atol, int maxit,
+                       int *its_out, double *relres_out, double *hist_out) {
+    return krylov_solve(ctx, b_dev, x_dev, rtol, atol, maxit, its_out, relres_out, hist_out);
+}
+
+mhdp_status mhdp_fgmres(mhdp_ctx *ctx, const double *b_dev, double *x_dev, double rtol, double atol, int maxit,
+                        int *its_out, double *relres_out, double *hist_out) {
+    return krylov_solve(ctx, b_dev, x_dev, rtol, atol, maxit, its_out, relres_out, hist_out);
 }
 
 mhdp_status mhdp_dot(mhdp_ctx *ctx, const double *a_dev, const double *b_dev, long long n, double *out_host) {
@@ -1181,6 +1183,15 @@ mhdp_status mhdp_export_patches(const mhdp_ctx *ctx, int level, long long *pptr,
     return MHDP_OK;
 }
 
+mhdp_status mhdp_export_patch_vertices(const mhdp_ctx *ctx, int level, int *verts) {
+    if (!ctx || !valid_level(ctx, level) || level < 1 || !ctx->loaded[level] || !verts) return MHDP_EINVAL;
+    const HostLevel &H = ctx->H[level];
+    const int64_t np = (int64_t)H.pptr.size() - 1;
+    if ((int64_t)H.pvert.size() != np) return fail(const_cast<mhdp_ctx *>(ctx), MHDP_ESTATE, "patches not from a mesh");
+    memcpy(verts, H.pvert.data(), sizeof(int) * np);
+    return MHDP_OK;
+}
+
 mhdp_status mhdp_export_prolongation(const mhdp_ctx *ctx, int level, long long *prow, int *pcol, double *pval) {
     if (!ctx || !valid_level(ctx, level) || level < 1 || !ctx->loaded[level] || !prow || !pcol || !pval)
         return MHDP_EINVAL;
@@ -1202,9 +1213,9 @@ mhdp_status mhdp_export_patch_lu(mhdp_ctx *ctx, int level, long long patch, doub
     const int n = (int)(H.pptr[patch + 1] - H.pptr[patch]);
     int64_t foff = 0;
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(&foff, P.foff + patch, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    CK(d2h(ctx, &foff, P.foff + patch, sizeof(int64_t)));
     std::vector<double> pk((size_t)n * n + n);
-    CK(cudaMemcpy(pk.data(), P.fac + foff, sizeof(double) * (n * n + n), cudaMemcpyDeviceToHost));
+    CK(d2h(ctx, pk.data(), P.fac + foff, sizeof(double) * (n * n + n)));
     // decode the packed streaming layout (kernels.cu pack_fwd / pack_bwd)
     for (int j = 0; j < n; ++j) {
         const int64_t f = (int64_t)j * n - (int64_t)j * (j + 1) / 2;
@@ -1212,7 +1223,7 @@ mhdp_status mhdp_export_patch_lu(mhdp_ctx *ctx, int level, long long patch, doub
         for (int i = 0; i < n; ++i)
             lu[(size_t)i * n + j] = i > j ? pk[f + i - j - 1] : (i == j ? pk[b] : pk[b + 2 + i]);
     }
-    CK(cudaMemcpy(perm, P.perm + H.pptr[patch], sizeof(int) * n, cudaMemcpyDeviceToHost));
+    CK(d2h(ctx, perm, P.perm + H.pptr[patch], sizeof(int) * n));
     return MHDP_OK;
 }
 
@@ -1221,7 +1232,7 @@ mhdp_status mhdp_export_slots(mhdp_ctx *ctx, int level, double *y) {
     if (st) return st;
     if (!valid_level(ctx, level) || level < 1 || !y) return fail(ctx, MHDP_EINVAL, "bad arguments");
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(y, ctx->D[level].P.y, sizeof(double) * ctx->D[level].P.sum_n, cudaMemcpyDeviceToHost));
+    CK(d2h(ctx, y, ctx->D[level].P.y, sizeof(double) * ctx->D[level].P.sum_n));
     return MHDP_OK;
 }
 

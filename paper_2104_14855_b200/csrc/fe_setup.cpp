@@ -865,7 +865,7 @@ void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *
 // ------------------------------------------------------------------------------------
 // vertex-star patches: per vertex, the free DoFs whose entity contains it
 // ------------------------------------------------------------------------------------
-void build_patches(const Mesh &m, const Space &s, std::vector<i64> &pptr, std::vector<int> &pdofs) {
+void build_patches(const Mesh &m, const Space &s, std::vector<i64> &pptr, std::vector<int> &pdofs, std::vector<int> &pvert) {
     // vertex -> incident edges and facets
     std::vector<std::vector<int>> vlist(m.nv);
     for (i64 v = 0; v < m.nv; ++v) if (s.vdof[v] >= 0) vlist[v].push_back(s.vdof[v]);
@@ -881,12 +881,14 @@ void build_patches(const Mesh &m, const Space &s, std::vector<i64> &pptr, std::v
     }
     pptr.assign(1, 0);
     pdofs.clear();
+    pvert.clear();
     for (i64 v = 0; v < m.nv; ++v) {
         auto &L = vlist[v];
         if (L.empty()) continue;   // empty stars dropped (R-patch)
         std::sort(L.begin(), L.end());
         pdofs.insert(pdofs.end(), L.begin(), L.end());
         pptr.push_back((i64)pdofs.size());
+        pvert.push_back((int)v);
     }
 }
 
@@ -1578,7 +1580,7 @@ void assemble_eb2(const Mesh &m, const Space2 &s, const Params &p, const double 
     }
 }
 
-void build_patches2(const Mesh &m, const Space2 &s, std::vector<i64> &pptr, std::vector<int> &pdofs) {
+void build_patches2(const Mesh &m, const Space2 &s, std::vector<i64> &pptr, std::vector<int> &pdofs, std::vector<int> &pvert) {
     std::vector<std::vector<int>> vlist(m.nv);
     for (i64 v = 0; v < m.nv; ++v) if (s.vdof[v] >= 0) vlist[v].push_back(s.vdof[v]);
     for (i64 e = 0; e < m.ne; ++e)
@@ -1591,12 +1593,14 @@ void build_patches2(const Mesh &m, const Space2 &s, std::vector<i64> &pptr, std:
         for (int t = 0; t < 3; ++t) { vlist[m.cv[3 * c + t]].push_back(s.cdof[c]); vlist[m.cv[3 * c + t]].push_back(s.cdof[c] + 1); }
     pptr.assign(1, 0);
     pdofs.clear();
+    pvert.clear();
     for (i64 v = 0; v < m.nv; ++v) {
         auto &L = vlist[v];
         if (L.empty()) continue;
         std::sort(L.begin(), L.end());
         pdofs.insert(pdofs.end(), L.begin(), L.end());
         pptr.push_back((i64)pdofs.size());
+        pvert.push_back((int)v);
     }
 }
 
@@ -2051,7 +2055,7 @@ void assemble_vel2(const Mesh &m, const Space2 &s, const Params &p, const double
     }
 }
 
-void build_patches2_vel(const Mesh &m, const Space2 &s, std::vector<i64> &pptr, std::vector<int> &pdofs) {
+void build_patches2_vel(const Mesh &m, const Space2 &s, std::vector<i64> &pptr, std::vector<int> &pdofs, std::vector<int> &pvert) {
     std::vector<std::vector<int>> vlist(m.nv);
     for (i64 f = 0; f < m.nfacet; ++f)
         if (s.fdof[f] >= 0)
@@ -2062,12 +2066,14 @@ void build_patches2_vel(const Mesh &m, const Space2 &s, std::vector<i64> &pptr, 
             for (int a = 0; a < 3; ++a) vlist[m.cv[3 * c + t]].push_back(s.cdof[c] + a);
     pptr.assign(1, 0);
     pdofs.clear();
+    pvert.clear();
     for (i64 v = 0; v < m.nv; ++v) {
         auto &L = vlist[v];
         if (L.empty()) continue;
         std::sort(L.begin(), L.end());
         pdofs.insert(pdofs.end(), L.begin(), L.end());
         pptr.push_back((i64)pdofs.size());
+        pvert.push_back((int)v);
     }
 }
 
@@ -2500,7 +2506,7 @@ void assemble_eb3(const Mesh &m, const Space3 &s, const Params &p, const double 
 }
 
 // vertex stars: DoFs of the edges, faces and cells containing the vertex, ascending
-void build_patches3(const Mesh &m, const Space3 &s, std::vector<i64> &pptr, std::vector<int> &pdofs) {
+void build_patches3(const Mesh &m, const Space3 &s, std::vector<i64> &pptr, std::vector<int> &pdofs, std::vector<int> &pvert) {
     std::vector<std::vector<int>> vlist(m.nv);
     for (i64 e = 0; e < m.ne; ++e)
         if (s.edof[e] >= 0)
@@ -2515,12 +2521,14 @@ void build_patches3(const Mesh &m, const Space3 &s, std::vector<i64> &pptr, std:
         for (int t = 0; t < 4; ++t) for (int a = 0; a < 3; ++a) vlist[m.cv[4 * c + t]].push_back(s.cdof[c] + a);
     pptr.assign(1, 0);
     pdofs.clear();
+    pvert.clear();
     for (i64 v = 0; v < m.nv; ++v) {
         auto &L = vlist[v];
         if (L.empty()) continue;
         std::sort(L.begin(), L.end());
         pdofs.insert(pdofs.end(), L.begin(), L.end());
         pptr.push_back((i64)pdofs.size());
+        pvert.push_back((int)v);
     }
 }
 
@@ -2999,7 +3007,7 @@ void assemble_vel3(const Mesh &m, const SpaceV3 &s, const Params &p, const doubl
     }
 }
 
-void build_patches_v3(const Mesh &m, const SpaceV3 &s, std::vector<i64> &pptr, std::vector<int> &pdofs) {
+void build_patches_v3(const Mesh &m, const SpaceV3 &s, std::vector<i64> &pptr, std::vector<int> &pdofs, std::vector<int> &pvert) {
     std::vector<std::vector<int>> vlist(m.nv);
     for (i64 f = 0; f < m.nf; ++f)
         if (s.fdof[f] >= 0)
@@ -3008,12 +3016,14 @@ void build_patches_v3(const Mesh &m, const SpaceV3 &s, std::vector<i64> &pptr, s
         for (int t = 0; t < 4; ++t) for (int a = 0; a < 6; ++a) vlist[m.cv[4 * c + t]].push_back(s.cdof[c] + a);
     pptr.assign(1, 0);
     pdofs.clear();
+    pvert.clear();
     for (i64 v = 0; v < m.nv; ++v) {
         auto &L = vlist[v];
         if (L.empty()) continue;
         std::sort(L.begin(), L.end());
         pdofs.insert(pdofs.end(), L.begin(), L.end());
         pptr.push_back((i64)pdofs.size());
+        pvert.push_back((int)v);
     }
 }
 
@@ -3136,7 +3146,7 @@ std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params
             H.rp = std::move(P.rp);
             H.ci = std::move(P.ci);
             H.v = std::move(val);
-            if (l > 0) k2d3::build_patches_v3(m, spaces[l], H.pptr, H.pdofs);
+            if (l > 0) k2d3::build_patches_v3(m, spaces[l], H.pptr, H.pdofs, H.pvert);
         }
         for (int l = 1; l < nlev; ++l) {
             k2d3::build_prolongation_v3(meshes[l], spaces[l], meshes[l - 1], spaces[l - 1], out[l].prp, out[l].pci,
@@ -3168,7 +3178,7 @@ std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params
             H.rp = std::move(P.rp);
             H.ci = std::move(P.ci);
             H.v = std::move(val);
-            if (l > 0) k2d3::build_patches3(m, spaces[l], H.pptr, H.pdofs);
+            if (l > 0) k2d3::build_patches3(m, spaces[l], H.pptr, H.pdofs, H.pvert);
         }
         for (int l = 1; l < nlev; ++l) {
             k2d3::build_prolongation3(meshes[l], spaces[l], meshes[l - 1], spaces[l - 1], out[l].prp, out[l].pci,
@@ -3203,8 +3213,8 @@ std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params
             H.ci = std::move(P.ci);
             H.v = std::move(val);
             if (l > 0) {
-                if (block == 0) build_patches2(m, spaces[l], H.pptr, H.pdofs);
-                else build_patches2_vel(m, spaces[l], H.pptr, H.pdofs);
+                if (block == 0) build_patches2(m, spaces[l], H.pptr, H.pdofs, H.pvert);
+                else build_patches2_vel(m, spaces[l], H.pptr, H.pdofs, H.pvert);
             }
         }
         for (int l = 1; l < nlev; ++l) {
@@ -3244,7 +3254,7 @@ std::string assemble_hierarchy(int block, int dim, int N, int nlev, const Params
         H.rp = std::move(P.rp);
         H.ci = std::move(P.ci);
         H.v = std::move(val);
-        if (l > 0) build_patches(m, spaces[l], H.pptr, H.pdofs);
+        if (l > 0) build_patches(m, spaces[l], H.pptr, H.pdofs, H.pvert);
     }
     for (int l = 1; l < nlev; ++l) {
         build_prolongation(meshes[l], spaces[l], meshes[l - 1], spaces[l - 1], out[l].prp, out[l].pci, out[l].pv);

@@ -193,10 +193,9 @@ void launch_interleave(const DevPatches &P, cudaStream_t s) {
 }
 
 void apply_lring(const DevPatches &P, const double *r, cudaStream_t s) {
-    static bool init = false;
-    if (!init) {
+    static unsigned long long init = 0;
+    if (first_use_on_device(init)) {
         cudaFuncSetAttribute(k_patch_apply_lring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LR_SMEM);
-        init = true;
     }
     const int64_t need = (P.ng + LR_WARPS - 1) / LR_WARPS;
     const int sms = sm_count();

@@ -102,11 +102,16 @@ void launch_prolong_add(const DevCsr &P, const double *ec, double *x, cudaStream
 // K7: dense LU with partial pivoting of the row-major n x n matrix a (in place)
 // perm[n]; status[0] = 0 or (step+1) of the first singular pivot; amax = max|a|
 void launch_dense_lu(double *a, int n, int *perm, int *status, double *scratch, cudaStream_t s);
-// K8 (R-coarse): X = A_0^-1 column-major (n*n doubles) from the K7 factors (setup), and
-// x = X b with R-dot rows; part: n * ceil(n/256) doubles of scratch; n <= 256 * CINV_MAXB
-static constexpr int CINV_MAXB = 80;
-void launch_coarse_inverse(const double *lu, const int *perm, int n, double *X, cudaStream_t s);
-void launch_coarse_apply(const double *X, int n, const double *b, double *x, double *part, cudaStream_t s);
+// K8 coarse solve (k8_coarse.cu): R-lu forward/back substitution, bit-identical to the
+// unblocked c.6 solve.  Tiles/records from the row-major factors (setup); solve: b != x.
+int k8_max_n();
+int64_t k8_tile_doubles(int n);
+int64_t k8_sync_words(int n);
+int64_t k8_rec_doubles(int n);
+void launch_k8_pack(const double *lu_rowmajor, int n, double *tiles, double *rec, cudaStream_t s);
+cudaError_t launch_k8_solve(const double *tiles, const double *rec, const int *perm, int n, const double *b,
+                            double *x, double *zf, double *hacc, unsigned long long *sync, cudaStream_t s,
+                            long long *trace = nullptr);   // trace: diagnostics, 5 stamps per (pass, block)
 // K9 vector ops (deterministic reductions)
 void launch_dot(const double *a, const double *b, int64_t n, double *partials, double *out, cudaStream_t s);
 void launch_axpy(double *y, double alpha, const double *x, int64_t n, cudaStream_t s);   // y = fma(alpha, x, y)

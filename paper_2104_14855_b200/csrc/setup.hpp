@@ -16,6 +16,8 @@ struct Params {
     double dt = 0;                         // NEXT-4: > 0 -> transient, (1/dt) mass terms
     int picard = 0;                        // NEXT-4: 1 -> Picard, no G~ term
     int degree = 1;                        // NEXT-2: element degree k (2: 2D E-B, CG2 x RT2)
+    int weights_mode = 0;                  // 0 by degree, 1 per-DoF 1/m_d, 2 uniform 1/max m_d
+    int newton_reaction = 0;               // accepted; zero under R-w (reading R-newton)
 };
 
 // One level of the hierarchy as host arrays (the form both mhdp_assemble and
@@ -27,6 +29,7 @@ struct HostLevel {
     std::vector<double> v;
     std::vector<int64_t> pptr; // vertex-star patches, ascending DoFs
     std::vector<int> pdofs;
+    std::vector<int> pvert;    // mesh vertex of each patch (mesh path; empty for mhdp_load_level)
     std::vector<int64_t> prp;  // prolongation from level-1 (rows: this level)
     std::vector<int> pci;
     std::vector<double> pv;

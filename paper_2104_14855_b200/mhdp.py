@@ -33,7 +33,8 @@ class Params(C.Structure):
     _fields_ = [("Re", C.c_double), ("Rem", C.c_double), ("S", C.c_double), ("gamma", C.c_double),
                 ("sigma", C.c_double), ("mu_stab", C.c_double), ("theta", C.c_double),
                 ("nu_pre", C.c_int), ("nu_post", C.c_int), ("smoother", C.c_int), ("smoother_its", C.c_int),
-                ("dt", C.c_double), ("picard", C.c_int), ("degree", C.c_int)]
+                ("dt", C.c_double), ("picard", C.c_int), ("degree", C.c_int),
+                ("weights_mode", C.c_int), ("newton_reaction", C.c_int)]
 
 
 class LevelInfo(C.Structure):
@@ -48,11 +49,11 @@ SYMBOLS = ["mhdp_create", "mhdp_destroy", "mhdp_assemble", "mhdp_begin_levels", 
            "mhdp_get_level_info", "mhdp_num_levels", "mhdp_spmv", "mhdp_residual", "mhdp_patch_apply",
            "mhdp_patch_update", "mhdp_smooth", "mhdp_restrict", "mhdp_prolong_add", "mhdp_coarse_solve",
            "mhdp_vcycle", "mhdp_vcycle_host", "mhdp_vcycle_host_batch", "mhdp_smooth_host", "mhdp_gmres", "mhdp_export_csr",
-           "mhdp_export_patches", "mhdp_export_prolongation", "mhdp_export_patch_lu", "mhdp_export_slots",
+           "mhdp_export_patches", "mhdp_export_patch_vertices", "mhdp_export_prolongation", "mhdp_export_patch_lu", "mhdp_export_slots",
            "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count", "mhdp_fgmres", "mhdp_dot", "mhdp_set_smoother", "mhdp_vcycle_graphs_active", "mhdp_assemble_lorentz",
            "mhdp_coupled_create", "mhdp_coupled_destroy", "mhdp_coupled_sizes", "mhdp_coupled_export_csr",
            "mhdp_coupled_apply", "mhdp_coupled_precondition", "mhdp_coupled_fgmres", "mhdp_coupled_set_smoother",
-           "mhdp_coupled_last_error"]
+           "mhdp_coupled_last_error", "mhdp_coarse_solve_trace"]
 
 
 def lib():
@@ -83,8 +84,9 @@ def lib():
             "mhdp_vcycle_host": [vp, dp, dp],
             "mhdp_vcycle_host_batch": [vp, C.c_int, dp, dp],
             "mhdp_smooth_host": [vp, C.c_int, C.c_int, C.c_int, dp, dp],
-            "mhdp_gmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp],
-            "mhdp_fgmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp],
+            "mhdp_gmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp, dp],
+            "mhdp_coarse_solve_trace": [vp, vp, vp, C.POINTER(C.c_longlong)],
+            "mhdp_fgmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp, dp],
             "mhdp_dot": [vp, vp, vp, i64, dp],
             "mhdp_set_smoother": [vp, C.c_int, C.c_int],
             "mhdp_coupled_create": [C.POINTER(vp), C.c_int, vp, C.POINTER(Mesh), C.POINTER(Params), dp, C.c_void_p],
@@ -97,6 +99,7 @@ def lib():
             "mhdp_coupled_last_error": [vp, C.c_char_p, C.c_int],
             "mhdp_export_csr": [vp, C.c_int, i64p, ip, dp],
             "mhdp_export_patches": [vp, C.c_int, i64p, ip],
+            "mhdp_export_patch_vertices": [vp, C.c_int, ip],
             "mhdp_export_prolongation": [vp, C.c_int, i64p, ip, dp],
             "mhdp_export_patch_lu": [vp, C.c_int, i64, dp, ip],
             "mhdp_export_slots": [vp, C.c_int, dp],
@@ -133,6 +136,20 @@ def _l(a):
     return a.ctypes.data_as(C.POINTER(C.c_longlong))
 
 
+def _host_vec(a, shape, name):
+    """Host buffer handed to C: must be a C-contiguous float64 numpy array of `shape`
+    (the C side reads/writes exactly that many doubles).  Raises ValueError otherwise."""
+    if not isinstance(a, np.ndarray):
+        raise ValueError(f"{name}: expected a numpy array, got {type(a).__name__}")
+    if a.dtype != np.float64:
+        raise ValueError(f"{name}: dtype must be float64, got {a.dtype}")
+    if not a.flags.c_contiguous:
+        raise ValueError(f"{name}: array must be C-contiguous")
+    if a.shape != tuple(shape):
+        raise ValueError(f"{name}: shape {a.shape}, expected {tuple(shape)}")
+    return _d(a)
+
+
 def _ptr(t):
     """Device pointer of a torch CUDA tensor (fp64, contiguous) or an int."""
     if isinstance(t, int):
@@ -148,7 +165,8 @@ def make_params(cfg, smoother: str = "richardson", smoother_its: int = 6) -> Par
     preconditioned by the Schwarz operator, the paper's relaxation."""
     return Params(cfg.Re, cfg.Rem, cfg.S, cfg.gamma, cfg.sigma, cfg.mu, cfg.theta, cfg.nu, cfg.nu,
                   1 if smoother == "gmres" else 0, smoother_its, float(getattr(cfg, "dt", 0.0)),
-                  int(getattr(cfg, "picard", 0)), int(getattr(cfg, "degree", 1)))
+                  int(getattr(cfg, "picard", 0)), int(getattr(cfg, "degree", 1)),
+                  int(getattr(cfg, "weights_mode", 0)), int(getattr(cfg, "newton_reaction", 0)))
 
 
 class Context:
@@ -245,6 +263,13 @@ class Context:
     def prolong_add(self, ec, x, level=-1):
         return self._chk(self._L.mhdp_prolong_add(self.h, level % self.num_levels(), _ptr(ec), _ptr(x)))
 
+    def coarse_solve_trace(self, b, x):
+        """one coarse solve with K8's per-block timestamps: array (2, nb, 5) of ns"""
+        nb = (self.n(0) + 31) // 32
+        tr = np.zeros(32 * nb, np.int64)
+        self._chk(self._L.mhdp_coarse_solve_trace(self.h, _ptr(b), _ptr(x), tr.ctypes.data_as(C.POINTER(C.c_longlong))))
+        return tr.reshape(2, nb, 16)
+
     def coarse_solve(self, b, x):
         return self._chk(self._L.mhdp_coarse_solve(self.h, _ptr(b), _ptr(x)))
 
@@ -253,36 +278,43 @@ class Context:
 
     def vcycle_host_batch(self, b, x):
         """b, x: C-contiguous float64 host arrays of shape (nrhs, n) (pinned for overlap)"""
-        assert b.dtype == np.float64 and x.dtype == np.float64 and b.shape == x.shape and b.ndim == 2
-        assert b.flags.c_contiguous and x.flags.c_contiguous
-        return self._chk(self._L.mhdp_vcycle_host_batch(self.h, b.shape[0], _d(b), _d(x)))
+        if not isinstance(b, np.ndarray) or b.ndim != 2:
+            raise ValueError("b: expected a 2-D numpy array (nrhs, n)")
+        shape = (b.shape[0], self.n())
+        return self._chk(self._L.mhdp_vcycle_host_batch(self.h, b.shape[0], _host_vec(b, shape, "b"),
+                                                        _host_vec(x, shape, "x")))
 
     def vcycle_host(self, b, x):
-        """b, x: C-contiguous float64 numpy arrays (pinned or pageable host memory)."""
-        return self._chk(self._L.mhdp_vcycle_host(self.h, _d(b), _d(x)))
+        """b, x: C-contiguous float64 numpy arrays of length n (pinned or pageable)."""
+        shape = (self.n(),)
+        return self._chk(self._L.mhdp_vcycle_host(self.h, _host_vec(b, shape, "b"), _host_vec(x, shape, "x")))
 
     def smooth_host(self, b, x, level=-1, nsweeps=1, x_is_zero=False):
-        return self._chk(self._L.mhdp_smooth_host(self.h, level % self.num_levels(), nsweeps, int(x_is_zero),
-                                                  _d(b), _d(x)))
+        level = level % self.num_levels()
+        shape = (self.n(level),)
+        return self._chk(self._L.mhdp_smooth_host(self.h, level, nsweeps, int(x_is_zero),
+                                                  _host_vec(b, shape, "b"), _host_vec(x, shape, "x")))
 
-    def gmres(self, b, x, rtol=1e-7, atol=1e-7, maxit=200):
+    def _krylov(self, fn, b, x, rtol, atol, maxit):
         its = C.c_int(0)
         rel = C.c_double(0)
-        st = self._L.mhdp_gmres(self.h, _ptr(b), _ptr(x), rtol, atol, maxit, C.byref(its), C.byref(rel))
+        hist = np.zeros(maxit + 1)
+        st = fn(self.h, _ptr(b), _ptr(x), rtol, atol, maxit, C.byref(its), C.byref(rel),
+                hist.ctypes.data_as(C.POINTER(C.c_double)))
         if st not in (0, 6):
             self._chk(st)
+        self.last_history = hist[: its.value + 1].copy()   # |g_k|, k = 0..its
         return its.value, rel.value, st == 0
+
+    def gmres(self, b, x, rtol=1e-7, atol=1e-7, maxit=200):
+        """GMRES(V) (c.9); the residual history is left in self.last_history."""
+        return self._krylov(self._L.mhdp_gmres, b, x, rtol, atol, maxit)
 
     def set_smoother(self, smoother="richardson", its=6):
         return self._chk(self._L.mhdp_set_smoother(self.h, 1 if smoother == "gmres" else 0, its))
 
     def fgmres(self, b, x, rtol=1e-7, atol=1e-7, maxit=100):
-        its = C.c_int(0)
-        rel = C.c_double(0)
-        st = self._L.mhdp_fgmres(self.h, _ptr(b), _ptr(x), rtol, atol, maxit, C.byref(its), C.byref(rel))
-        if st not in (0, 6):
-            self._chk(st)
-        return its.value, rel.value, st == 0
+        return self._krylov(self._L.mhdp_fgmres, b, x, rtol, atol, maxit)
 
     def dot(self, a, b):
         out = C.c_double(0)
@@ -306,6 +338,12 @@ class Context:
         v = np.zeros(max(i["nnz"], 1), np.float64)
         self._chk(self._L.mhdp_export_csr(self.h, level, _l(rp), _i(ci), _d(v)))
         return rp, ci[:i["nnz"]], v[:i["nnz"]]
+
+    def patch_vertices(self, level=-1):
+        level = level % self.num_levels()
+        v = np.zeros(max(self.info(level)["npatch"], 1), np.int32)
+        self._chk(self._L.mhdp_export_patch_vertices(self.h, level, _i(v)))
+        return v[: self.info(level)["npatch"]]
 
     def patches(self, level=-1):
         level = level % self.num_levels()

@@ -41,6 +41,8 @@ class Config:
     dt: float = 0.0      # NEXT-4: > 0 -> transient, (1/dt) mass terms
     picard: int = 0      # NEXT-4: 1 -> Picard linearisation, delta = 0
     degree: int = 1      # NEXT-2: element degree k; k = 2 for the 2D E-B block (CG2 x RT2)
+    weights_mode: int = 0  # update weights w_i: 0 by degree, 1 per-DoF 1/m_d, 2 uniform 1/max m_d
+    newton_reaction: int = 0  # (u . grad u^n, v) of Table 1 row F: zero under R-w (reading R-newton)
 
     @property
     def block_id(self) -> int:

@@ -98,16 +98,35 @@ def test_vcycle(pb):
     _same(host(xg), xo)
 
 
-def test_gmres_iteration_count(pb):
+# GMRES(V) maxit per case: 200 where the oracle converges only after 80 (c3 N64 L4: 154,
+# c5 N8 L2: 136 iterations), else 80
+MAXIT = {("c3", 64): 200, ("c5", 8): 200}
+
+
+def test_gmres_iteration_count(pb, request):
+    """a8 (c.9): GMRES(V) counts within +-1 where either side converges, and
+    convergence exactly where the oracle converges; where either side stops at maxit, the
+    residual histories are compared instead (<= 1e-6 relative per iteration
+    over the first 20 iterations).  Both sides run the same order-defined iteration, so
+    the histories are also expected bit for bit."""
     import torch
     cfg, ctx, orc, b, x0 = pb
     if len(b) > 100_000:
         pytest.skip("oracle GMRES too slow at this size; counts checked on the smaller cases")
-    _, its_o, _, conv_o = orc.gmres(b, maxit=80)
+    name, N = request.node.callspec.params["pb"][:2]
+    maxit = MAXIT.get((name, N), 80)
+    _, its_o, hist_o, conv_o = orc.gmres(b, maxit=maxit)
     xg = torch.empty(len(b), dtype=torch.float64, device="cuda:0")
-    its_g, _, conv_g = ctx.gmres(cuda_vec(b), xg, maxit=80)
-    assert conv_o == conv_g
-    assert abs(its_o - its_g) <= 1, (its_o, its_g)
+    its_g, _, conv_g = ctx.gmres(cuda_vec(b), xg, maxit=maxit)
+    hist_g = ctx.last_history
+    assert conv_g == conv_o
+    if conv_o and conv_g:
+        assert abs(its_o - its_g) <= 1, (its_o, its_g)
+    else:
+        k = min(20, len(hist_o), len(hist_g))
+        rel = np.abs(hist_g[:k] - hist_o[:k]) / np.abs(hist_o[:k])
+        assert rel.max() <= 1e-6, rel.max()
+    assert its_g == its_o and np.array_equal(hist_g, hist_o)
 
 
 def _mask_around(cfg, verts, radius=3):

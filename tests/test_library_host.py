@@ -40,9 +40,11 @@ def test_host_setup_matches_oracle(mh, oracle_mod, name, N, L):
         assert np.max(np.abs(A.v - v) / scale) <= 1e-13, f"level {l}: values"
         if l == 0:
             continue
-        ptr_o, dofs_o, _, _ = orc.patches(l)
+        ptr_o, dofs_o, verts_o, _ = orc.patches(l)
         ptr_l, dofs_l = ctx.patches(l)
         assert np.array_equal(ptr_o, ptr_l) and np.array_equal(dofs_o, dofs_l), f"level {l}: patches"
+        # the vertex of each star (what ESINGULAR reports)
+        assert np.array_equal(ctx.patch_vertices(l), verts_o), f"level {l}: patch vertices"
         P = orc.prolongation(l)
         prp, pci, pv = ctx.prolongation(l)
         assert np.array_equal(P.rp, prp) and np.array_equal(P.ci, pci), f"level {l}: prolongation pattern"
@@ -200,9 +202,11 @@ def test_k2_host_setup_bitexact_vs_exact_oracle(mh, oracle_mod, name, N, L, kw):
         assert diff.size == 0, f"level {l}: {diff.size} values differ"
         if l == 0:
             continue
-        ptr_o, dofs_o, _, _ = orc.patches(l)
+        ptr_o, dofs_o, verts_o, _ = orc.patches(l)
         ptr_l, dofs_l = ctx.patches(l)
         assert np.array_equal(ptr_o, ptr_l) and np.array_equal(dofs_o, dofs_l), f"level {l}: patches"
+        # the vertex of each star (what ESINGULAR reports)
+        assert np.array_equal(ctx.patch_vertices(l), verts_o), f"level {l}: patch vertices"
         P = orc.prolongation(l)
         prp, pci, pv = ctx.prolongation(l)
         assert np.array_equal(P.rp, prp) and np.array_equal(P.ci, pci), f"level {l}: prolongation pattern"

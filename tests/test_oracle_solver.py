@@ -81,6 +81,46 @@ def test_sweep_matches_brute_force(oracle_mod, name, N):
         assert np.linalg.norm(got - ref) <= max(1e-12, 50 * kap * 1.1e-16) * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("name,N,mode", [("c1", 8, 1), ("c1", 8, 2), ("c3", 4, 2), ("c5", 2, 2), ("c4", 2, 1)])
+def test_sweep_weights_mode_matches_brute_force(oracle_mod, name, N, mode):
+    """weights_mode ("damping parameters w_i"): 1 = per-DoF partition of
+    unity 1/m_d, 2 = the uniform per-subspace weight 1/max_d m_d -- against the brute-force
+    sweep written with that weight; mode 0 (by degree) is mode 1 at k = 1."""
+    import dataclasses
+    cfg = dataclasses.replace(small(name, N, 1), weights_mode=mode)
+    o = make(oracle_mod, cfg)
+    n = o.n()
+    _, b, x0 = draw(cfg, n, 1)
+    A = o.csr().to_scipy().toarray()
+    ptr, dofs, vert, mult = o.patches()
+    wdiv = mult if mode == 1 else np.full(n, mult.max())
+    got = o.sweep(b, x0)
+    ref = _brute_sweep(A, b, x0, ptr, dofs, wdiv)
+    kap = max(np.linalg.cond(A[np.ix_(dofs[ptr[i]:ptr[i + 1]], dofs[ptr[i]:ptr[i + 1]])]) for i in range(len(ptr) - 1))
+    assert np.linalg.norm(got - ref) <= max(1e-12, 50 * kap * 1.1e-16) * np.linalg.norm(ref)
+    if mode == 2 and mult.min() != mult.max():          # the two modes really differ here
+        o1 = make(oracle_mod, dataclasses.replace(cfg, weights_mode=1))
+        assert not np.array_equal(o1.sweep(b, x0), got)
+    d0 = make(oracle_mod, dataclasses.replace(cfg, weights_mode=0)).sweep(b, x0)
+    d1 = make(oracle_mod, dataclasses.replace(cfg, weights_mode=1)).sweep(b, x0)
+    assert np.array_equal(d0, d1)                        # k = 1: by degree = per-DoF
+
+
+@pytest.mark.parametrize("name,N", [("c3", 4), ("c5", 2)])
+def test_newton_reaction_vanishes_under_piecewise_constant_w(oracle_mod, name, N):
+    """Reading R-newton: with the advecting field of R-w (curl / vcurl of a lowest-order
+    interpolant: constant on every cell), grad u^n = 0 cellwise, so the Newton reaction
+    (u . grad u^n, v) of Table 1 row F adds nothing: the flag is accepted and
+    leaves the assembled operator unchanged (the zero of the term is a consequence of
+    R-w, not something this test can pin independently)."""
+    import dataclasses
+    cfg = small(name, N, 1)
+    o = make(oracle_mod, cfg)
+    on = make(oracle_mod, dataclasses.replace(cfg, newton_reaction=1))
+    A, An = o.csr(), on.csr()
+    assert np.array_equal(A.rp, An.rp) and np.array_equal(A.v, An.v)
+
+
 @pytest.mark.parametrize("name,N", [("c1", 4), ("c3", 3), ("c5", 1), ("c4", 2)])
 def test_single_patch_is_direct_solve(oracle_mod, name, N):
     """One patch covering every free DoF (m_d = 1) => one sweep from zero is the
