@@ -8,9 +8,11 @@ patch gather + LU apply, weighted gather-update on every level, restriction,
 prolongation, dense coarse solve).  Setup (a0-a2: host assembly, batched patch LU,
 coarse LU) runs once before the timed region.
 
-metric: smoothed DoFs/s (every sweep on level l smooths n_l DoFs: sum_l (nu_pre +
-nu_post) n_l per V-cycle), plus the V-cycle ms, a finest-level single-sweep DoFs/s and
-its achieved HBM GB/s (SURVEY §8(d) algorithmic bytes) against MEASURED_PEAKS.json.
+metric: smoothed DoFs/s in SURVEY A26's sense -- free DoFs of the finest level per sweep,
+(nu_pre + nu_post) n_finest per V-cycle -- plus the V-cycle ms, a finest-level single
+sweep's DoFs/s and its achieved HBM GB/s (SURVEY §8(d) algorithmic bytes) against
+MEASURED_PEAKS.json.  `value_all_levels` counts every level's sweeps (sum_l (nu_pre +
+nu_post) n_l), the round-1 definition.
 
 Multi-GPU: the method runs on one GPU (BASELINE north star); --gpus N runs N independent
 replicas (one process per GPU, each its own seeded right-hand side), "replicas only" in
@@ -53,6 +55,53 @@ def peaks():
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return None
+
+
+def fp64_peak_flops(device=0):
+    """FP64 FMA throughput of the GPU measured by tools/probe.cu ("FP64 peak
+    is not in MP. Measure it"), or None when the probe library is missing."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import probe
+        v = probe.fp64_peak(device)
+        return v if v > 0 else None
+    except Exception:
+        return None
+
+
+def host_info():
+    """CPU model, logical cores and a single-thread STREAM-copy figure of the host the
+    oracle baseline runs on."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    a = np.ones(1 << 25)            # 256 MB
+    b = np.empty_like(a)
+    best = 1e9
+    for _ in range(3):
+        t = time.perf_counter()
+        np.copyto(b, a)
+        best = min(best, time.perf_counter() - t)
+    return {"cpu_model": model, "nproc": os.cpu_count(),
+            "stream_copy_gbs_1thread": 2 * a.nbytes / best / 1e9}
+
+
+def oracle_full_size_record():
+    """Full-size oracle timings recorded by tools/golden_full.py (the exact build, one
+    core, on the build container -- not this host), when the golden file exists."""
+    p = os.path.join(ROOT, "tests", "golden", "c5_full_seed0.json")
+    try:
+        g = json.load(open(p))
+    except (OSError, ValueError):
+        return None
+    return {"config": "c5 full (48^3 x 6, 4 levels)", "setup_s": g.get("setup_s"), "sweep_s": g.get("sweep_s"),
+            "vcycle_s": g.get("vcycle_s"), "cores": 1, "where": "build container (tools/golden_full.py), exact build",
+            "vcycle_dofs_per_s": (4 * g["n"] / g["vcycle_s"]) if g.get("vcycle_s") else None}
 
 
 _SAMPLER_SRC = r"""
@@ -180,16 +229,19 @@ def oracle_vcycle_sample(steps, warmup, seed=0):
     w0, _, _ = workloads.draw(cfg, 1, seed)
     orc = oracle.Oracle(cfg, w0)
     w, b, _ = workloads.draw(cfg, orc.n(), seed)
+    ts = time.perf_counter()
     orc = oracle.Oracle(cfg, w)
     orc.vcycle(b)                       # factors every level (lazy) -- setup, not timed
+    setup_s = time.perf_counter() - ts
     for _ in range(max(0, warmup - 1)):
         orc.vcycle(b)
-    smoothed = sum(2 * cfg.nu * orc.n(l) for l in range(1, L))
+    smoothed = 2 * cfg.nu * orc.n()              # A26: finest-level DoFs per sweep
     t0 = time.perf_counter()
     for _ in range(steps):
         orc.vcycle(b)
     dt = (time.perf_counter() - t0) / steps
     return {"value": smoothed / dt, "ms_per_step": dt * 1e3, "smoothed_per_step": smoothed,
+            "setup_s": setup_s,
             "sample": f"oracle V(2,2) on {name} at N={N}, {L} levels ({orc.n()} finest DoFs; same element, "
                       f"patch and operator structure as the full c5), setup excluded, {steps} cycles"}
 
@@ -268,7 +320,7 @@ def _k2_variant(cfg, seed, dev, stream, desc):
     sweep_bytes = 8 * fin["sum_n2"] + 8 * fin["nnz"] + 24 * fin["n"]
     ctx.set_smoother("gmres", 6)
     ms_f, (its, rel, conv) = _timed(stream, lambda: ctx.fgmres(bd, xd, maxit=60))
-    smoothed = sum(2 * cfg.nu * ctx.info(l)["n"] for l in range(1, L))
+    smoothed = 2 * cfg.nu * fin["n"]             # A26: finest-level DoFs per sweep
     ctx.close()
     return {"config": desc, "finest_dofs": fin["n"], "nnz": fin["nnz"], "patches": fin["npatch"],
             "max_patch": fin["max_n"], "sum_n2": fin["sum_n2"], "factor_gb": 8e-9 * fin["sum_n2"],
@@ -366,7 +418,31 @@ def run_ours(args):
     L = ctx.num_levels()
     infos = [ctx.info(l) for l in range(L)]
     fin = infos[-1]
-    smoothed = sum((cfg.nu + cfg.nu) * infos[l]["n"] for l in range(1, L))
+    smoothed = (cfg.nu + cfg.nu) * fin["n"]                                    # A26
+    smoothed_all = sum((cfg.nu + cfg.nu) * infos[l]["n"] for l in range(1, L))  # every level
+    # setup kernels against the FP64 FMA peak: K6 (2/3) sum_i n_i^3 per level,
+    # K7 (2/3) n0^3
+    stt = ctx.setup_timings()
+    fp64 = fp64_peak_flops(dev.index)
+    k6 = []
+    for l in range(1, L):
+        ptr, _ = ctx.patches(l)
+        sz = np.diff(ptr).astype(np.float64)
+        fl = float((2.0 / 3.0) * np.sum(sz ** 3))
+        ms6 = stt["K6_ms"][l]
+        k6.append({"level": l, "ms": ms6, "flop": fl, "tflops": fl / (ms6 * 1e-3) / 1e12 if ms6 > 0 else None})
+    n0c = infos[0]["n"]
+    fl7 = (2.0 / 3.0) * float(n0c) ** 3
+    setup_kernels = {
+        "fp64_peak_tflops": fp64 / 1e12 if fp64 else None,
+        "fp64_peak_source": "tools/probe.cu: DFMA chains on every SM (measured in this run)",
+        "K6_patch_lu": k6,
+        "K6_finest_frac_fp64_peak": (k6[-1]["tflops"] * 1e12 / fp64) if (fp64 and k6 and k6[-1]["tflops"]) else None,
+        "K6_all_levels_ms": float(sum(k["ms"] for k in k6)),
+        "K7_coarse_lu": {"n0": n0c, "ms": stt["K7_ms"], "flop": fl7,
+                         "tflops": fl7 / (stt["K7_ms"] * 1e-3) / 1e12 if stt["K7_ms"] > 0 else None,
+                         "frac_fp64_peak": (fl7 / (stt["K7_ms"] * 1e-3) / fp64) if (fp64 and stt["K7_ms"] > 0) else None},
+        "K8_pack_ms": stt["K8_pack_ms"], "device_setup_wall_s": stt["wall_s"]}
 
     bd = torch.from_numpy(b).to(dev)
     xd = torch.empty_like(bd)
@@ -458,7 +534,7 @@ def run_ours(args):
     if not args.no_solves and ws == 1:          # single-GPU line only (not the scaling runs)
         xk = torch.empty_like(bd)
         e0.record(stream)
-        its_r, rel_r, conv_r = ctx.gmres(bd, xk, maxit=60)
+        its_r, rel_r, conv_r = ctx.gmres(bd, xk, maxit=600)   # basis of 2 x 601 x 31.5 MB
         e1.record(stream)
         torch.cuda.synchronize(dev)
         ms_gr = e0.elapsed_time(e1)
@@ -525,7 +601,9 @@ def run_ours(args):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         r = oracle_vcycle_sample(steps=2, warmup=1)
-        cpu = {"value": r["value"], "unit": "DoF/s", "cores": 1, "kind": "oracle", "sample": r["sample"]}
+        cpu = {"value": r["value"], "unit": "DoF/s", "cores": 1, "kind": "oracle", "sample": r["sample"],
+               "oracle_setup_s_of_sample": r["setup_s"], "host": host_info(),
+               "full_size_record": oracle_full_size_record()}
 
     if rank == 0:
         value = ws * smoothed / (ms * 1e-3)
@@ -536,6 +614,9 @@ def run_ours(args):
             "dtype": "f64", "data": "synthetic",
             "config": workload_config(cfg, L, fin, ws),
             "vcycle_ms": ms,
+            "value_all_levels": ws * smoothed_all / (ms * 1e-3),
+            "value_definition": "A26: (nu_pre + nu_post) x finest-level free DoFs per V-cycle; "
+                                "value_all_levels: every level's sweeps",
             "sweep": {"ms": ms_sweep, "dofs_per_s": fin["n"] / (ms_sweep * 1e-3),
                       "gbs": sweep_bytes / (ms_sweep * 1e-3) / 1e9,
                       "frac": sweep_bytes / (ms_sweep * 1e-3) / 1e9 / peak, "bytes": sweep_bytes},
@@ -556,6 +637,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "setup_s": {"host_assembly": t_asm, "device_setup": t_setup},
+            "setup_kernels": setup_kernels,
             "cpu_baseline": cpu,
             "solves": solves,
             "variants": variants,

@@ -145,6 +145,11 @@ mhdp_status mhdp_load_level(mhdp_ctx *ctx, int level, long long n,
  * the message names the level), or the patch index for operators installed by
  * mhdp_load_level; `where` = -1 for a singular coarse operator.                        */
 mhdp_status mhdp_setup(mhdp_ctx *ctx);
+/* Timings of the last mhdp_setup (diagnostics; len >= 3 + n_levels): out[0] = K7 dense
+ * coarse LU (device ms), out[1] = K8 tile packing (ms), out[2] = wall time of the whole
+ * setup (s: host packing, uploads and kernels), out[3 + l] = K6 batched patch LU of level
+ * l (ms; 0 for level 0).  ESTATE before setup.                                          */
+mhdp_status mhdp_setup_timings(const mhdp_ctx *ctx, double *out, int len);
 
 /* SURVEY 8(b) names this call mhdp_level_info, but that is also the name of the struct
  * typedef (one C identifier namespace), so the call carries a get_ prefix.             */

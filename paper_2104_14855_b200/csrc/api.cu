@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -73,6 +74,9 @@ struct mhdp_ctx {
     long long where = -1;
     long long launches0 = 0;
     double *vh = nullptr;      // mhdp_vcycle_host: device x of the finest level
+    // setup timings (mhdp_setup_timings): device ms of K6 per level, K7, K8 pack; wall s
+    std::vector<double> t_k6;
+    double t_k7 = 0, t_k8pack = 0, t_setup_wall = 0;
     // fgmres workspace
     double *fV = nullptr, *fZ = nullptr, *fw = nullptr, *fpart = nullptr, *fscal = nullptr;
     int f_cap = 0;
@@ -109,6 +113,28 @@ template <class T>
 struct TmpDev {
     T *p = nullptr;
     ~TmpDev() { if (p) cudaFree(p); }
+};
+
+// CUDA-event stopwatch on a stream (setup diagnostics); stop() synchronises the event
+struct EvTimer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaStream_t s;
+    explicit EvTimer(cudaStream_t st) : s(st) {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+    }
+    double stop() {
+        float ms = 0;
+        cudaEventRecord(b, s);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        return ms;
+    }
+    ~EvTimer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
 };
 
 #define CK(call)                                                                              \
@@ -701,6 +727,8 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         if (!ctx->loaded[l]) return fail(ctx, MHDP_ESTATE, "level not loaded", l);
     free_device(ctx);
     CK(cudaSetDevice(ctx->device));
+    const auto wall0 = std::chrono::steady_clock::now();
+    ctx->t_k6.assign(ctx->nlev, 0.0);
     mhdp_status st;
     if ((st = dalloc(ctx, &ctx->d_status, 4))) return st;
     if ((st = dalloc(ctx, &ctx->d_scal, 2048))) return st;
@@ -741,7 +769,9 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         TmpDev<double> buf_lu;            // K6 scratch for stars beyond shared memory
         const int64_t nscr = patch_lu_scratch_doubles(L.P);
         if (nscr) CK(cudaMalloc(&buf_lu.p, sizeof(double) * nscr));
+        EvTimer tk6(ctx->stream);
         launch_patch_lu(L.P, drp, dci, dv, ctx->d_status, buf_lu.p, ctx->stream);
+        ctx->t_k6[l] = tk6.stop();
         if ((st = check_launch(ctx))) return st;
         CK(cudaStreamSynchronize(ctx->stream));
         int bad = 0;
@@ -782,16 +812,31 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         if ((st = dalloc(ctx, &ctx->csync, k8_sync_words((int)n0)))) return st;
         CK(cudaMemsetAsync(ctx->csync, 0, sizeof(unsigned long long) * k8_sync_words((int)n0), ctx->stream));
         CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int), ctx->stream));
+        EvTimer tk7(ctx->stream);
         launch_dense_lu(a, (int)n0, ctx->cperm, ctx->d_status, ctx->d_scal, ctx->stream);
+        ctx->t_k7 = tk7.stop();
         if ((st = check_launch(ctx))) return st;
         int bad = 0;
         CK(d2h(ctx, &bad, ctx->d_status, sizeof(int)));
         if (bad) return fail(ctx, MHDP_ESINGULAR, "singular coarse operator", -1);
+        EvTimer tk8(ctx->stream);
         launch_k8_pack(a, (int)n0, ctx->ctile, ctx->crec, ctx->stream);
+        ctx->t_k8pack = tk8.stop();
         if ((st = check_launch(ctx))) return st;
         CK(cudaStreamSynchronize(ctx->stream));
     }
     ctx->setup_done = true;
+    ctx->t_setup_wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_setup_timings(const mhdp_ctx *ctx, double *out, int len) {
+    if (!ctx || !out || len < 3 + ctx->nlev) return MHDP_EINVAL;
+    if (!ctx->setup_done) return MHDP_ESTATE;
+    out[0] = ctx->t_k7;
+    out[1] = ctx->t_k8pack;
+    out[2] = ctx->t_setup_wall;
+    for (int l = 0; l < ctx->nlev; ++l) out[3 + l] = ctx->t_k6[l];
     return MHDP_OK;
 }
 

@@ -53,7 +53,7 @@ SYMBOLS = ["mhdp_create", "mhdp_destroy", "mhdp_assemble", "mhdp_begin_levels", 
            "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count", "mhdp_fgmres", "mhdp_dot", "mhdp_set_smoother", "mhdp_vcycle_graphs_active", "mhdp_assemble_lorentz",
            "mhdp_coupled_create", "mhdp_coupled_destroy", "mhdp_coupled_sizes", "mhdp_coupled_export_csr",
            "mhdp_coupled_apply", "mhdp_coupled_precondition", "mhdp_coupled_fgmres", "mhdp_coupled_set_smoother",
-           "mhdp_coupled_last_error", "mhdp_coarse_solve_trace"]
+           "mhdp_coupled_last_error", "mhdp_coarse_solve_trace", "mhdp_setup_timings"]
 
 
 def lib():
@@ -86,6 +86,7 @@ def lib():
             "mhdp_smooth_host": [vp, C.c_int, C.c_int, C.c_int, dp, dp],
             "mhdp_gmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp, dp],
             "mhdp_coarse_solve_trace": [vp, vp, vp, C.POINTER(C.c_longlong)],
+            "mhdp_setup_timings": [vp, dp, C.c_int],
             "mhdp_fgmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp, dp],
             "mhdp_dot": [vp, vp, vp, i64, dp],
             "mhdp_set_smoother": [vp, C.c_int, C.c_int],
@@ -227,6 +228,13 @@ class Context:
 
     def setup(self):
         return self._chk(self._L.mhdp_setup(self.h))
+
+    def setup_timings(self):
+        """{'K7_ms', 'K8_pack_ms', 'wall_s', 'K6_ms': [per level]} of the last setup"""
+        L = self.num_levels()
+        out = np.zeros(3 + L)
+        self._chk(self._L.mhdp_setup_timings(self.h, _d(out), len(out)))
+        return {"K7_ms": out[0], "K8_pack_ms": out[1], "wall_s": out[2], "K6_ms": out[3:].tolist()}
 
     def num_levels(self):
         return self._L.mhdp_num_levels(self.h)
