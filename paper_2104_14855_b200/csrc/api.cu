@@ -792,7 +792,7 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
     // K7: coarse LU (dense, row-major, R-lu), then the K8 tiles of both substitution passes
     const HostLevel &H0 = ctx->H[0];
     const int64_t n0 = H0.n;
-    if (n0 > k8_max_n()) return fail(ctx, MHDP_EINVAL, "coarse level too large for the dense LU");
+    if (n0 > std::min(k8_max_n(), k7_max_n())) return fail(ctx, MHDP_EINVAL, "coarse level too large for the dense LU");
     ctx->n0 = (int)n0;
     {
         std::vector<double> dense((size_t)(n0 * n0), 0.0);

@@ -44,14 +44,13 @@ __device__ __forceinline__ unsigned long long ld_acq(const unsigned long long *p
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-// polling without invalidating L1 on every probe (an acquire load is LD + CCTL.IVALL,
-// which stalls the SM's memory pipe for the chain warp); acquire once it is seen
+// relaxed probe: the publishing lane only needs to see its predecessor's release before it
+// releases in turn (release order is all that matters there; no data is read after it)
 __device__ __forceinline__ unsigned long long ld_rlx(const unsigned long long *p) {
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_rel(unsigned long long *p, unsigned long long v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }

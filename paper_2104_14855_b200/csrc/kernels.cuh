@@ -102,6 +102,7 @@ void launch_prolong_add(const DevCsr &P, const double *ec, double *x, cudaStream
 // K7: dense LU with partial pivoting of the row-major n x n matrix a (in place)
 // perm[n]; status[0] = 0 or (step+1) of the first singular pivot; amax = max|a|
 void launch_dense_lu(double *a, int n, int *perm, int *status, double *scratch, cudaStream_t s);
+int k7_max_n();   // largest n whose panel slices fit the cluster's shared memory
 // K8 coarse solve (k8_coarse.cu): R-lu forward/back substitution, bit-identical to the
 // unblocked c.6 solve.  Tiles/records from the row-major factors (setup); solve: b != x.
 int k8_max_n();
