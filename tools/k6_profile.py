@@ -5,7 +5,6 @@ run mhdp_setup once (K6 on every level), for ncu:
       gpu__time_duration.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,\
       sm__inst_executed_pipe_fp64.sum --csv python tools/k6_profile.py c5
 
-MHDP_K6_SMEM=1 selects the shared-memory K6 (k_patch_lu) for every level (A/B).
 Without ncu it prints the wall time of mhdp_setup (host->device copies included).
 """
 import os

@@ -38,7 +38,7 @@ def main():
     ms = e0.elapsed_time(e1) / reps
     tr = ctx.coarse_solve_trace(b, x).astype(np.float64)
     t0 = tr[0, 0, 0]
-    LFs = int(__import__("os").environ.get("MHDP_K8_LF", "6"))
+    LFs = 7   # k8_lf() in k8_coarse.cu
     out = {"n0": n, "ms_per_solve": ms}
     for p, name in ((0, "forward"), (1, "back")):
         T = tr[p] - t0
