@@ -56,7 +56,10 @@ typedef struct {
     double Re, Rem, S, gamma; /* P:20-35. S is accepted and unused by both blocks
                                  (reading R-S); Re/gamma used by ALVEL, Rem by EB; > 0      */
     double sigma;             /* SIPG penalty sigma = 10 k^2 = 10                    */
-    double mu_stab;           /* Burman stabilisation mu; must be 0 (R-mu)       */
+    double mu_stab;           /* Burman stabilisation mu >= 0 of the velocity
+                                 block: every interior facet adds mu h_F^2 int_F [grad u] :
+                                 [grad v] (reading R-mu); 0 for the BASELINE configs; k = 1
+                                 only (EINVAL with degree 2); unused by the E-B block        */
     double theta;             /* outer damping of the additive update (R-weights), 1.0       */
     int nu_pre, nu_post;      /* smoothing sweeps per level in the V-cycle (R-nu)             */
     int smoother;             /* 0: nu_pre / nu_post Richardson Schwarz sweeps (north star);

@@ -698,6 +698,19 @@ static void assemble_vel(OCsr *A, Accum *S, signed char *cnt, const OMesh *m, co
         }
         real avg = interior ? (real)1 / 2 : (real)1;
         real pen = (real)p->sigma / ((real)p->Re * hF);
+        /* Burman stabilisation: (1/2) sum_K int_{dK} mu h^2 [grad u]:[grad v] ds.
+         * Reading R-mu: the jump lives on interior facets, each met from both of its cells
+         * (the 1/2), so every interior facet adds mu h_F^2 int_F [grad u]:[grad v]; h_F as for
+         * SIPG (edge length / longest face edge), h_F^2 taken without the square root.   */
+        real hF2 = 0;
+        if (d == 2) hF2 = dot3(Av, Av);
+        else
+            for (int a = 0; a < 3; a++)
+                for (int b = a + 1; b < 3; b++) {
+                    real t[3] = {P[b][0] - P[a][0], P[b][1] - P[a][1], P[b][2] - P[a][2]};
+                    if (dot3(t, t) > hF2) hF2 = dot3(t, t);
+                }
+        real burman = interior ? (real)p->mu * hF2 : (real)0;
         double pot[4][3];
         real wx[3];
         cell_pot(m, cp, w, pot);
@@ -725,7 +738,10 @@ static void assemble_vel(OCsr *A, Accum *S, signed char *cnt, const OMesh *m, co
                     real up;
                     if (interior) up = (side[j] > 0 ? (wn + awn) / 2 : -(-wn + awn) / 2) * vv * Ji;
                     else up = (wn + awn) / 2 * vv;
-                    loc[i * 24 + j] += wq[t] * (t1 + t2 + t3 + up);
+                    real gj = 0;                 /* [grad phi_j] : [grad phi_i] */
+                    if (burman != 0)
+                        for (int l = 0; l < 3; l++) for (int k = 0; k < 3; k++) gj += F[j].G[l][k] * F[i].G[l][k];
+                    loc[i * 24 + j] += wq[t] * (t1 + t2 + t3 + up + burman * Jj * Ji * gj);
                 }
             }
         }

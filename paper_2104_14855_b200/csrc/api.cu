@@ -620,7 +620,9 @@ static mhdp_status check_params(mhdp_ctx *ctx, const mhdp_params *pr) {
     if (!pr) return fail(ctx, MHDP_EINVAL, "params is NULL");
     if (!(pr->Re > 0) || !(pr->Rem > 0) || !(pr->gamma > 0) || !(pr->sigma > 0))
         return fail(ctx, MHDP_EINVAL, "Re, Rem, gamma and sigma must be positive");
-    if (pr->mu_stab != 0.0) return fail(ctx, MHDP_EINVAL, "mu_stab != 0 is not supported (reading R-mu)");
+    if (!(pr->mu_stab >= 0.0)) return fail(ctx, MHDP_EINVAL, "mu_stab must be >= 0");
+    if (pr->mu_stab != 0.0 && pr->degree == 2)
+        return fail(ctx, MHDP_EINVAL, "mu_stab > 0 is assembled for k = 1 only (reading R-mu)");
     if (pr->nu_pre < 0 || pr->nu_post < 0) return fail(ctx, MHDP_EINVAL, "negative sweep counts");
     if (!(pr->theta > 0)) return fail(ctx, MHDP_EINVAL, "theta must be positive");
     ctx->p.Re = pr->Re; ctx->p.Rem = pr->Rem; ctx->p.S = pr->S; ctx->p.gamma = pr->gamma;

@@ -810,10 +810,24 @@ void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *
                     }
             const dd avg(interior ? 0.5 : 1.0);
             const dd pen = dd(p.sigma) / (dd(p.Re) * hF);
+            // Burman stabilisation (reading R-mu): interior facets add
+            // mu h_F^2 int_F [grad u]:[grad v]; grad (lam_a v) = v (x) grad lam_a is constant per
+            // cell, so [grad phi_I]:[grad phi_J] = J_I J_J (v_I . v_J)(g_I . g_J); h_F^2 exact
+            dd hF2(0.0);
+            if (d == 2) hF2 = dot3(A, A);
+            else
+                for (int a = 0; a < 3; ++a)
+                    for (int b = a + 1; b < 3; ++b) {
+                        dd tt[3];
+                        for (int r = 0; r < 3; ++r) tt[r] = Kp.G.X[fl[b]][r] - Kp.G.X[fl[a]][r];
+                        if (dot3(tt, tt) > hF2) hF2 = dot3(tt, tt);
+                    }
+            const dd burman = interior ? dd(p.mu) * hF2 * area : dd(0.0);
+            const bool use_burman = interior && p.mu != 0.0;
             const dd wn = dot3(Kp.w, n), awn = fabs(wn);
             const dd upp = dd(0.5) * (wn + awn), upm = dd(-0.5) * (awn - wn);
             const dd intF = area / dd((double)d);
-            struct Fn { int side, vtx, gidx; dd v[3], en[3]; };
+            struct Fn { int side, vtx, gidx; dd v[3], en[3], g[3]; };
             Fn fn[24];
             int nf = 0;
             for (int side = 0; side < (interior ? 2 : 1); ++side) {
@@ -827,6 +841,7 @@ void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *
                     for (int r = 0; r < 3; ++r) {
                         F.v[r] = K.B.v[k][r];
                         F.en[r] = K.eps[k][r][0] * n[0] + K.eps[k][r][1] * n[1] + K.eps[k][r][2] * n[2];
+                        F.g[r] = K.G.g[K.B.a[k]][r];
                     }
                 }
             }
@@ -848,6 +863,7 @@ void assemble_vel(const Mesh &m, const Space &s, const Params &p, const double *
                         if (interior) term += (J.side > 0 ? upp : upm) * vv * Ji;           // upwind
                         else term += upp * vv;
                     }
+                    if (use_burman) term += burman * Ji * Jj * dot3(J.v, I.v) * dot3(J.g, I.g);  // Burman
                     add(a, J.gidx, term);
                 }
             }

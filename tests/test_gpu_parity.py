@@ -23,7 +23,8 @@ CASES = [("c1", None, None, 0), ("c1", None, None, 1), ("c1", None, None, 2), ("
          ("c4-transient-picard", 8, 2, 0), ("c5-transient", 6, 2, 2), ("c5-lorentz", 6, 2, 3),
          ("c1-k2", None, None, 0), ("c2-k2", 64, 4, 1), ("c2-k2-transient-picard", 32, 3, 2),   # NEXT-2
          ("c3-k2", 32, 4, 0), ("c3-k2-transient", 16, 3, 1), ("c3-k2-lorentz", 16, 3, 2),
-         ("c4-k2", 4, 2, 0), ("c4-k2-transient-picard", 4, 2, 1), ("c5-k2", 4, 2, 0)]      # 3D k = 2
+         ("c4-k2", 4, 2, 0), ("c4-k2-transient-picard", 4, 2, 1), ("c5-k2", 4, 2, 0),      # 3D k = 2
+         ("c3-burman", 32, 4, 0), ("c5-burman", 6, 2, 1)]                                   # R-mu
 
 
 def _setup(oracle_mod, name, N, L, seed):
@@ -36,6 +37,9 @@ def _setup(oracle_mod, name, N, L, seed):
         variant["degree"] = 2
         if name.startswith("c3") or name.startswith("c5"):
             variant["sigma"] = 40.0                                      # 10 k^2
+    if name.endswith("-burman"):                                          # P:190-194, R-mu
+        name = name.split("-")[0]
+        variant["mu"] = 5e-3
     lorentz = name.endswith("-lorentz")
     if name.endswith("-transient-picard"):
         name = name.split("-")[0]

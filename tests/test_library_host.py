@@ -75,7 +75,8 @@ def test_operator_bitexact_vs_exact_oracle(mh, oracle_mod, name, N, L):
 
 
 VARIANTS = [("c1", dict(dt=0.01)), ("c3", dict(dt=0.01)), ("c4", dict(picard=1)), ("c5", dict(dt=0.5)),
-            ("c4", dict(dt=0.05, picard=1))]
+            ("c4", dict(dt=0.05, picard=1)),
+            ("c3", dict(mu=5e-3)), ("c5", dict(mu=5e-3)), ("c5", dict(mu=0.25, dt=0.5))]   # Burman, R-mu
 
 
 @pytest.mark.parametrize("name,kw", VARIANTS, ids=[f"{c}-{'-'.join(f'{k}{v}' for k, v in kw.items())}" for c, kw in VARIANTS])

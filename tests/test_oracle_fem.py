@@ -294,3 +294,49 @@ def test_lorentz_term_symmetric_psd_and_linear_in_S(oracle_mod):
         assert np.linalg.eigvalsh(0.5 * (D1 + D1.T)).min() >= -1e-10 * np.abs(D1).max()
         assert np.allclose(D3, 3 * D1, rtol=1e-12, atol=1e-12 * np.abs(D3).max())
         assert np.abs(D1).max() > 0
+
+
+@pytest.mark.parametrize("name,N", [("c3", 3), ("c5", 2)])
+def test_burman_term_brute_force(oracle_mod, name, N):
+    """Burman stabilisation (reading R-mu): A(mu) - A(0) equals the brute-force
+    sum over interior facets of mu h_F^2 |F| [grad phi_i] : [grad phi_j], where the
+    cellwise gradients are least-squares fits of each basis function's values at the
+    quadrature points (BDM1 is affine per cell, so the fit is exact) and h_F is the edge
+    length (2D) / longest face edge (3D).  It is symmetric positive semi-definite and
+    linear in mu; boundary facets add nothing."""
+    mu = 5e-3                                         # SPEC's value (S:231)
+    cfg = small(name, N, 1)
+    o0 = make(oracle_mod, cfg)
+    o1 = make(oracle_mod, dataclasses.replace(cfg, mu=mu))
+    o2 = make(oracle_mod, dataclasses.replace(cfg, mu=2 * mu))
+    A0 = o0.csr().to_scipy().toarray()
+    D = o1.csr().to_scipy().toarray() - A0
+    D2 = o2.csr().to_scipy().toarray() - A0
+    d, n = cfg.dim, o0.n()
+    m = o0.mesh()
+    pts, wts, ncomp = o0.quadrature()
+    nc = m["cv"].shape[0]
+    nq = len(wts) // nc
+    X = np.hstack([np.ones((len(wts), 1)), pts[:, :d]]).reshape(nc, nq, d + 1)
+    G = np.zeros((n, nc, ncomp, d))
+    for j in range(n):
+        e = np.zeros(n); e[j] = 1.0
+        vals = o0.eval(e).reshape(nc, nq, ncomp)
+        for c in range(nc):
+            coef = np.linalg.lstsq(X[c], vals[c], rcond=None)[0]      # (1 + d, ncomp)
+            G[j, c] = coef[1:].T
+    facets = m["ev"] if d == 2 else m["fv"]
+    B = np.zeros((n, n))
+    for f, (cp, cm) in enumerate(m["fcell"]):
+        if cm < 0:
+            continue
+        V = m["x"][facets[f]]
+        h2 = max(np.sum((V[a] - V[b]) ** 2) for a in range(len(V)) for b in range(a + 1, len(V)))
+        area = np.sqrt(h2) if d == 2 else 0.5 * np.linalg.norm(np.cross(V[1] - V[0], V[2] - V[0]))
+        Jg = (G[:, cp] - G[:, cm]).reshape(n, -1)
+        B += mu * h2 * area * Jg @ Jg.T
+    assert np.abs(B).max() > 0
+    assert np.abs(D - B).max() <= 1e-9 * np.abs(B).max()
+    assert np.abs(D2 - 2 * D).max() <= 1e-12 * np.abs(D).max() + 1e-15 * np.abs(A0).max()
+    assert np.abs(D - D.T).max() <= 1e-12 * np.abs(D).max() + 1e-15 * np.abs(A0).max()
+    assert np.linalg.eigvalsh(0.5 * (D + D.T)).min() >= -1e-9 * np.abs(D).max()
