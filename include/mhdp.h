@@ -198,6 +198,9 @@ mhdp_status mhdp_coarse_solve_trace(mhdp_ctx *ctx, const double *b_dev, double *
 mhdp_status mhdp_vcycle(mhdp_ctx *ctx, int level, const double *b_dev, double *x_dev);
 /* number of captured V-cycle graphs currently held (diagnostics)                       */
 int         mhdp_vcycle_graphs_active(const mhdp_ctx *ctx);
+/* enable = 0: mhdp_vcycle launches its kernels directly instead of replaying a captured
+ * CUDA graph (diagnostics / profiling); 1 (default): graphs.                         */
+mhdp_status mhdp_set_graphs(mhdp_ctx *ctx, int enable);
 /* End-to-end variant for callers holding host data: copies b (host, n doubles) to the
  * device, runs mhdp_vcycle on the finest level and copies x back (synchronises).       */
 mhdp_status mhdp_vcycle_host(mhdp_ctx *ctx, const double *b_host, double *x_host);

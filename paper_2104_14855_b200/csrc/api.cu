@@ -93,7 +93,8 @@ struct mhdp_ctx {
     };
     std::vector<VGraph> graphs;
     cudaStream_t cap = nullptr;
-    bool graphs_off = false;
+    bool graphs_off = false;       // capture failed once: run uncaptured from then on
+    bool graphs_disabled = false;  // mhdp_set_graphs(ctx, 0)
     // mhdp_vcycle_host_batch: two device (b, x) slots, copy-in / copy-out streams
     double *hb[2] = {nullptr, nullptr}, *hx[2] = {nullptr, nullptr};
     cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -956,7 +957,7 @@ mhdp_status mhdp_vcycle(mhdp_ctx *ctx, int level, const double *b_dev, double *x
     mhdp_status st = need_setup(ctx);
     if (st) return st;
     if (!valid_level(ctx, level) || !b_dev || !x_dev) return fail(ctx, MHDP_EINVAL, "bad arguments");
-    if (ctx->graphs_off || getenv("MHDP_NO_GRAPH")) {
+    if (ctx->graphs_off || ctx->graphs_disabled) {
         vcycle(ctx, level, b_dev, x_dev);
         return check_launch(ctx);
     }
@@ -1109,6 +1110,12 @@ mhdp_status mhdp_set_smoother(mhdp_ctx *ctx, int smoother, int smoother_its) {
     }
     ctx->p.smoother = smoother;
     ctx->p.smoother_its = smoother_its;
+    return MHDP_OK;
+}
+
+mhdp_status mhdp_set_graphs(mhdp_ctx *ctx, int enable) {
+    if (!ctx) return MHDP_EINVAL;
+    ctx->graphs_disabled = !enable;
     return MHDP_OK;
 }
 

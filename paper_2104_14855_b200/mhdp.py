@@ -53,7 +53,7 @@ SYMBOLS = ["mhdp_create", "mhdp_destroy", "mhdp_assemble", "mhdp_begin_levels", 
            "mhdp_synchronize", "mhdp_last_error", "mhdp_launch_count", "mhdp_fgmres", "mhdp_dot", "mhdp_set_smoother", "mhdp_vcycle_graphs_active", "mhdp_assemble_lorentz",
            "mhdp_coupled_create", "mhdp_coupled_destroy", "mhdp_coupled_sizes", "mhdp_coupled_export_csr",
            "mhdp_coupled_apply", "mhdp_coupled_precondition", "mhdp_coupled_fgmres", "mhdp_coupled_set_smoother",
-           "mhdp_coupled_last_error", "mhdp_coarse_solve_trace", "mhdp_setup_timings"]
+           "mhdp_coupled_last_error", "mhdp_coarse_solve_trace", "mhdp_setup_timings", "mhdp_set_graphs"]
 
 
 def lib():
@@ -87,6 +87,7 @@ def lib():
             "mhdp_gmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp, dp],
             "mhdp_coarse_solve_trace": [vp, vp, vp, C.POINTER(C.c_longlong)],
             "mhdp_setup_timings": [vp, dp, C.c_int],
+            "mhdp_set_graphs": [vp, C.c_int],
             "mhdp_fgmres": [vp, vp, vp, C.c_double, C.c_double, C.c_int, ip, dp, dp],
             "mhdp_dot": [vp, vp, vp, i64, dp],
             "mhdp_set_smoother": [vp, C.c_int, C.c_int],
@@ -331,6 +332,9 @@ class Context:
 
     def synchronize(self):
         return self._chk(self._L.mhdp_synchronize(self.h))
+
+    def set_graphs(self, enable=True):
+        return self._chk(self._L.mhdp_set_graphs(self.h, int(bool(enable))))
 
     def graphs_active(self):
         return self._L.mhdp_vcycle_graphs_active(self.h)
