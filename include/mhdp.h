@@ -151,7 +151,9 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx);
 /* Timings of the last mhdp_setup (diagnostics; len >= 3 + n_levels): out[0] = K7 dense
  * coarse LU (device ms), out[1] = K8 tile packing (ms), out[2] = wall time of the whole
  * setup (s: host packing, uploads and kernels), out[3 + l] = K6 batched patch LU of level
- * l (ms; 0 for level 0).  ESTATE before setup.                                          */
+ * l (ms; 0 for level 0); if len >= 9 + n_levels, out[3 + n_levels + k] = host wall s of
+ * the stages k = 0 operator stores, 1 patch stores, 2 transfers, 3 K6 incl. its CSR
+ * upload, 4 lane groups, 5 coarse (dense build, upload, K7, K8 pack).  ESTATE before setup. */
 mhdp_status mhdp_setup_timings(const mhdp_ctx *ctx, double *out, int len);
 
 /* SURVEY 8(b) names this call mhdp_level_info, but that is also the name of the struct

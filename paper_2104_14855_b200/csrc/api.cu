@@ -77,6 +77,7 @@ struct mhdp_ctx {
     // setup timings (mhdp_setup_timings): device ms of K6 per level, K7, K8 pack; wall s
     std::vector<double> t_k6;
     double t_k7 = 0, t_k8pack = 0, t_setup_wall = 0;
+    std::vector<double> t_stage;   // host wall s per setup stage (mhdp_setup_timings)
     // fgmres workspace
     double *fV = nullptr, *fZ = nullptr, *fw = nullptr, *fpart = nullptr, *fscal = nullptr;
     int f_cap = 0;
@@ -224,6 +225,7 @@ mhdp_status make_sell(mhdp_ctx *ctx, const HostLevel &H, DevSell &A, int64_t *by
     const int64_t stored = sptr[ns];
     std::vector<int> col(stored, 0);
     std::vector<double> val(stored, 0.0);
+#pragma omp parallel for schedule(static)
     for (int64_t r = 0; r < n; ++r) {
         const int64_t base = sptr[r >> 5] + (r & 31);
         for (int k = 0; k < rlen[r]; ++k) {
@@ -248,19 +250,22 @@ mhdp_status build_sell(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) { return 
 // complete aligned triples
 bool has_block3(const HostLevel &H) {
     if (H.n == 0 || H.n % 3) return false;
+    bool ok = true;
+#pragma omp parallel for schedule(static) reduction(&& : ok)
     for (int64_t R = 0; R < H.n / 3; ++R) {
         const int64_t a = H.rp[3 * R], len = H.rp[3 * R + 1] - a;
-        if (len % 3) return false;
-        for (int q = 1; q < 3; ++q) {
-            if (H.rp[3 * R + q + 1] - H.rp[3 * R + q] != len) return false;
-            if (!std::equal(H.ci.begin() + a, H.ci.begin() + a + len, H.ci.begin() + H.rp[3 * R + q])) return false;
+        bool r_ok = len % 3 == 0;
+        for (int q = 1; q < 3 && r_ok; ++q) {
+            if (H.rp[3 * R + q + 1] - H.rp[3 * R + q] != len) r_ok = false;
+            else if (!std::equal(H.ci.begin() + a, H.ci.begin() + a + len, H.ci.begin() + H.rp[3 * R + q])) r_ok = false;
         }
-        for (int64_t t = 0; t < len; t += 3) {
+        for (int64_t t = 0; t < len && r_ok; t += 3) {
             const int c = H.ci[a + t];
-            if (c % 3 || H.ci[a + t + 1] != c + 1 || H.ci[a + t + 2] != c + 2) return false;
+            if (c % 3 || H.ci[a + t + 1] != c + 1 || H.ci[a + t + 2] != c + 2) r_ok = false;
         }
+        ok = ok && r_ok;
     }
-    return true;
+    return ok;
 }
 
 mhdp_status build_b3(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
@@ -281,6 +286,7 @@ mhdp_status build_b3(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
     const int planes = 0;
     std::vector<int> col(stored, 0);
     std::vector<double> val(9 * stored, 0.0);
+#pragma omp parallel for schedule(static)
     for (int64_t R = 0; R < nb; ++R) {
         const int64_t s0 = sptr[R >> 5], base = s0 + (R & 31);
         for (int k = 0; k < rlen[R]; ++k) {
@@ -732,6 +738,12 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
     CK(cudaSetDevice(ctx->device));
     const auto wall0 = std::chrono::steady_clock::now();
     ctx->t_k6.assign(ctx->nlev, 0.0);
+    ctx->t_stage.assign(6, 0.0);   // operator stores, patch stores, transfers, K6 (+ CSR upload), lane groups, coarse
+    auto tick = [last = std::chrono::steady_clock::now()](double &acc) mutable {
+        const auto now = std::chrono::steady_clock::now();
+        acc += std::chrono::duration<double>(now - last).count();
+        last = now;
+    };
     mhdp_status st;
     if ((st = dalloc(ctx, &ctx->d_status, 4))) return st;
     if ((st = dalloc(ctx, &ctx->d_scal, 2048))) return st;
@@ -743,17 +755,21 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         L.nnz = H.rp[H.n];
         L.use_b3 = l > 0 && has_block3(H);
         if ((st = L.use_b3 ? build_b3(ctx, H, L) : build_sell(ctx, H, L))) return st;
+        tick(ctx->t_stage[0]);
         if ((st = dalloc(ctx, &L.b, H.n))) return st;
         if ((st = dalloc(ctx, &L.x, H.n))) return st;
         if ((st = dalloc(ctx, &L.r, H.n))) return st;
         if (l == 0) continue;
+        tick(ctx->t_stage[0]);
         if ((st = build_patches(ctx, H, L))) return st;
+        tick(ctx->t_stage[1]);
         if (ctx->p.smoother == 1 && (st = alloc_smoother(ctx, L, ctx->p.smoother_its))) return st;
         if ((st = build_csr(ctx, H.n, H.prp, H.pci, H.pv, L.Pr))) return st;
         std::vector<int64_t> trp; std::vector<int> tci; std::vector<double> tv;
         transpose_csr(H.n, H.n_coarser, H.prp, H.pci, H.pv, trp, tci, tv);
         if ((st = build_csr(ctx, H.n_coarser, trp, tci, tv, L.PrT))) return st;
         L.bytes_tr = 2 * (12 * (int64_t)H.prp[H.n]) + 4 * (H.n + H.n_coarser + 2);
+        tick(ctx->t_stage[2]);
         // K6: batched patch LU from a temporary device CSR
         TmpDev<int64_t> buf_rp;
         TmpDev<int> buf_ci;
@@ -790,7 +806,9 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
                      have_v ? "vertex" : "patch", vid, l);
             return fail(ctx, MHDP_ESINGULAR, buf, vid);
         }
+        tick(ctx->t_stage[3]);
         if ((st = build_lane_groups(ctx, H, L))) return st;
+        tick(ctx->t_stage[4]);
     }
     // K7: coarse LU (dense, row-major, R-lu), then the K8 tiles of both substitution passes
     const HostLevel &H0 = ctx->H[0];
@@ -828,6 +846,7 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         if ((st = check_launch(ctx))) return st;
         CK(cudaStreamSynchronize(ctx->stream));
     }
+    tick(ctx->t_stage[5]);
     ctx->setup_done = true;
     ctx->t_setup_wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
     return MHDP_OK;
@@ -840,6 +859,7 @@ mhdp_status mhdp_setup_timings(const mhdp_ctx *ctx, double *out, int len) {
     out[1] = ctx->t_k8pack;
     out[2] = ctx->t_setup_wall;
     for (int l = 0; l < ctx->nlev; ++l) out[3 + l] = ctx->t_k6[l];
+    for (int k = 0; k < 6 && 3 + ctx->nlev + k < len; ++k) out[3 + ctx->nlev + k] = ctx->t_stage[k];
     return MHDP_OK;
 }
 

@@ -233,9 +233,12 @@ class Context:
     def setup_timings(self):
         """{'K7_ms', 'K8_pack_ms', 'wall_s', 'K6_ms': [per level]} of the last setup"""
         L = self.num_levels()
-        out = np.zeros(3 + L)
+        out = np.zeros(9 + L)
         self._chk(self._L.mhdp_setup_timings(self.h, _d(out), len(out)))
-        return {"K7_ms": out[0], "K8_pack_ms": out[1], "wall_s": out[2], "K6_ms": out[3:].tolist()}
+        st = out[3 + L:]
+        return {"K7_ms": out[0], "K8_pack_ms": out[1], "wall_s": out[2], "K6_ms": out[3:3 + L].tolist(),
+                "host_stage_s": dict(zip(["operator", "patches", "transfers", "K6", "lane_groups", "coarse"],
+                                         st.tolist()))}
 
     def num_levels(self):
         return self._L.mhdp_num_levels(self.h)

@@ -23,7 +23,7 @@ t = ctx.setup_timings()
 peak = probe.fp64_peak(0)
 L = ctx.num_levels()
 out = {"config": name, "fp64_peak_tflops": peak / 1e12, "K7_ms": t["K7_ms"], "K8_pack_ms": t["K8_pack_ms"],
-       "wall_s": t["wall_s"], "K6": []}
+       "wall_s": t["wall_s"], "host_stage_s": t["host_stage_s"], "K6": []}
 n0 = ctx.n(0)
 out["K7_tflops"] = (2 / 3) * n0 ** 3 / (t["K7_ms"] * 1e-3) / 1e12
 for l in range(1, L):
