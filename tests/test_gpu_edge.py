@@ -237,3 +237,28 @@ def test_vcycle_host_batch_matches_serial():
         ctx.vcycle_host_batch(np.ascontiguousarray(B[:count]), X)
         assert np.array_equal(X.view(np.uint64), ref[:count].view(np.uint64)), count
     ctx.vcycle_host_batch(np.zeros((0, n)), np.zeros((0, n)))
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 63, 65, 257, 300])
+def test_coarse_lu_solve_ragged_sizes(oracle_mod, n):
+    """K7 + K8 on dense coarse operators whose order is not a multiple of the 32-row
+    blocks / 32-column panels (ragged tails, one-block and few-block chains, with and
+    without far warps): the solve equals the oracle's pinned R-lu routine bit for bit,
+    and row pivoting is exercised (a permuted diagonally weighted random matrix)."""
+    import torch
+    from paper_2104_14855_b200 import workloads
+    rng = np.random.default_rng(n)
+    A = rng.uniform(-1, 1, (n, n)) + np.diag(rng.uniform(1, 2, n)) * n ** 0.5
+    A = A[rng.permutation(n)]                       # pivots away from the diagonal
+    b = rng.uniform(-1, 1, n)
+    ref = oracle_mod.dense_lu_solve(A, b)[0]
+    cfg = workloads.small("c1", 4, 1)
+    ctx = _ctx()
+    ctx.begin_levels(1, cfg)
+    rp = np.arange(0, n * n + 1, n, dtype=np.int64)
+    ci = np.tile(np.arange(n, dtype=np.int32), n)
+    ctx.load_level(0, rp, ci, A.ravel())
+    ctx.setup()
+    x = torch.empty(n, dtype=torch.float64, device="cuda:0")
+    ctx.coarse_solve(cuda_vec(b), x)
+    assert np.array_equal(bits(host(x)), bits(ref))
