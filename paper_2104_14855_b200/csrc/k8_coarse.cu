@@ -99,6 +99,8 @@ struct K8Shared {
     double *rc;                 // this warp's mini-block records (8 x 32)
     volatile int *vblk;         // blocks of the current pass finalised (CTA 0)
     unsigned long long tgt, base;
+    uint64_t *dbar = nullptr;         // chain warps: diagonal tile + records staged
+    uint32_t dcount = 0;              // (phase of dbar)
     double *ring = nullptr;           // far warps: RING tile slots in shared memory (or null)
     uint64_t *ring_bar = nullptr;     // their mbarriers
     uint32_t ring_count = 0;          // tiles streamed so far by this warp (slot / phase)
@@ -112,7 +114,7 @@ __device__ __forceinline__ int row_of(int n, int s) { return P == 0 ? s : n - 1 
 // completes the older column blocks, applies block r-1 as its warp solves it, then
 // solves block r in mini-blocks of four rows (see the file comment).
 template <int P>
-__device__ void chain_pass(const K8Args &A, const K8Shared &S, int w, int lane) {
+__device__ void chain_pass(const K8Args &A, K8Shared &S, int w, int lane) {
     const int n = A.n, nb = A.nb, LF = A.lf;
     unsigned long long *prog = A.sync + 2, *hflag = A.sync + 4;
     double *zs = S.zs, *dt = S.dt;
@@ -128,12 +130,11 @@ __device__ void chain_pass(const K8Args &A, const K8Shared &S, int w, int lane) 
             const char *pb = reinterpret_cast<const char *>(tile_ptr(A, P, r, J0));
             const int lines = (r - J0 + 1) * (TILE * 8 / 128);
             for (int k = lane; k < lines; k += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + 128 * (size_t)k));
-            const double *tp = tile_ptr(A, P, r, r);
-#pragma unroll 8
-            for (int c = 0; c < TB; ++c) dt[c * TB + lane] = __ldcg(tp + c * TB + lane);
-            const double *rp = A.rec + ((long long)P * nb + r) * 256;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) S.rc[c * TB + lane] = __ldcg(rp + c * TB + lane);
+            if (lane == 0) {            // diagonal tile + records: two bulk copies, one barrier
+                mbar_expect_tx(S.dbar, (TILE + 256) * 8);
+                bulk_g2s(dt, tile_ptr(A, P, r, r), TILE * 8, S.dbar);
+                bulk_g2s(S.rc, A.rec + ((long long)P * nb + r) * 256, 256 * 8, S.dbar);
+            }
         }
         double ma[TB], mb[TB];
         if (J0 < r) load_tile(ma, tile_ptr(A, P, r, J0), lane);
@@ -199,6 +200,8 @@ __device__ void chain_pass(const K8Args &A, const K8Shared &S, int w, int lane) 
             }
         }
         // ---- solve the 32 rows of block r ----
+        while (!mbar_try(S.dbar, S.dcount & 1)) {}
+        ++S.dcount;
         K8_STAMP(p, r, 2);
         const bool consumer = r + 1 < nb;    // the warp of block r+1 waits on us
         double zmine = 0.0;
@@ -415,6 +418,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k8_solve(K8Args A) {
     S.tgt = s_tgt;
     S.base = s_tgt << 10;   // nb <= 1023
     if (blockIdx.x == 0) {
+        __shared__ uint64_t dbar[NW];
+        S.dbar = dbar + w;
+        if (lane == 0) {
+            mbar_init(S.dbar, 1);
+            fence_mbar_init();
+        }
         if (threadIdx.x == 0) s_prog = 0;
         __syncthreads();
         chain_pass<0>(A, S, w, lane);
