@@ -395,6 +395,19 @@ mhdp_status build_patches(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
     if ((st = dalloc(ctx, &P.fac, f))) return st;
     if ((st = upload(ctx, &P.dptr, dptr.data(), H.n + 1))) return st;
     if ((st = upload(ctx, &P.dslot, dslot.data(), sum_n))) return st;
+    // DoF triples (3D velocity: the 3 DoFs of a face) whose slot lists are the same patches
+    // at consecutive slots: K3 can update a triple per thread from one slot list
+    P.triples = H.n % 3 == 0 && H.n > 0;
+    for (int64_t R = 0; P.triples && R < H.n / 3; ++R) {
+        const int64_t d = 3 * R;
+        const int m = dptr[d + 1] - dptr[d];
+        if (dptr[d + 2] - dptr[d + 1] != m || dptr[d + 3] - dptr[d + 2] != m) { P.triples = false; break; }
+        for (int k = 0; k < m; ++k)
+            if (dslot[dptr[d + 1] + k] != dslot[dptr[d] + k] + 1 || dslot[dptr[d + 2] + k] != dslot[dptr[d] + k] + 2) {
+                P.triples = false;
+                break;
+            }
+    }
     if ((st = upload(ctx, &P.wd, wd.data(), H.n))) return st;
     if ((st = dalloc(ctx, &P.y, sum_n))) return st;
     L.bytes_fac = 8 * f + 4 * np + 16 * np + 12 * sum_n;

@@ -63,6 +63,7 @@ struct DevPatches {
     int *dptr = nullptr;       // n+1  DoF -> slot list
     int *dslot = nullptr;      // sum_n slots of each DoF, ascending patch order
     double *wd = nullptr;      // n    theta * (1/m_d)
+    bool triples = false;      // DoFs 3R..3R+2 share one slot list at consecutive slots (K3 per triple)
     double *y = nullptr;       // sum_n slot buffer
     // small stars (every patch size in LR_SIZES): thread-per-patch K2 on lane-interleaved
     // factors streamed through TMA rings.
