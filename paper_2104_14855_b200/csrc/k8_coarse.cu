@@ -140,7 +140,7 @@ __device__ void chain_pass(const K8Args &A, K8Shared &S, int w, int lane) {
         if (J0 < r) load_tile(ma, tile_ptr(A, P, r, J0), lane);
         double acc;
         if (r >= LF) {                  // claim the far warp's partial sums (J <= r - LF)
-            while (ld_acq(hflag + P * nb + r) != S.tgt) __nanosleep(32);
+            while (ld_acq(hflag + P * nb + r) != S.tgt) {}
             acc = __ldcg(A.hacc + ((long long)P * nb + r) * TB + lane);
         } else {
             acc = t < n ? (P == 0 ? __ldg(A.b + __ldg(A.perm + t)) : zs[n - 1 - t]) : 0.0;
@@ -324,10 +324,7 @@ __device__ void far_pass(const K8Args &A, K8Shared &S, int w, int lane) {
         int have = 0, nxt = 0;                    // nxt: first block not yet fetched
         auto refill = [&](bool block_until) {
             if (done <= nxt) done = poll();
-            while (block_until && done <= nxt) {
-                __nanosleep(32);
-                done = poll();
-            }
+            while (block_until && done <= nxt) done = poll();
             const int cnt = (int)min((long long)(4 - have), min(done, (long long)Jend + 1) - nxt);
             // append cnt blocks behind the `have` already held
             for (int k = 0; k < cnt; ++k) {
@@ -517,7 +514,7 @@ __global__ void k8_pack_rec(const double *__restrict__ a, int n, int nb, double 
 }  // namespace
 
 // far-warp lag in blocks, measured on the c5 coarse level (n0 = 7128, tools/k8_trace.py,
-// profiles/r02_k8_trace_summary.txt): 5 -> 0.669 ms, 6 -> 0.638, 7 -> 0.633, 9 -> 0.684
+// profiles/r02_k8_trace_summary.txt): 6 -> 0.585 ms, 7 -> 0.561, 8 -> 0.593, 9 -> 0.620
 int k8_lf() { return 7; }
 
 int k8_max_n() {
