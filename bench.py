@@ -331,6 +331,47 @@ def _k2_variant(cfg, seed, dev, stream, desc):
             "fgmres_gmres6_vcycle": {"its": its, "converged": conv, "relres": rel, "ms": ms_f}}
 
 
+def run_configs(seed, dev, stream):
+    """SURVEY 8(d) "per config": the other BASELINE.json configurations (c1-c4) on the same
+    kernels -- V-cycle ms (median of 20 after 3 warm-ups), finest sweep ms, finest K2
+    algorithmic GB/s and fraction of the measured HBM peak, A26 DoFs/s.  Setup excluded."""
+    import torch
+    from paper_2104_14855_b200 import mhdp, workloads
+    pk = peaks()
+    peak = pk["hbm_gbs"] if pk else 6650.0
+    out = {}
+    for name in ("c1", "c2", "c3", "c4"):
+        cfg = workloads.CONFIGS[name]
+        ctx = mhdp.Context(dev.index, stream.cuda_stream)
+        w, _, _ = workloads.draw(cfg, 1, seed)
+        ctx.assemble(cfg, w)
+        n = ctx.n()
+        _, b, x0 = workloads.draw(cfg, n, seed)
+        ctx.setup()
+        fin = ctx.info(ctx.num_levels() - 1)
+        bd = torch.from_numpy(b).to(dev)
+        xd = torch.empty_like(bd)
+        for _ in range(3):
+            ctx.vcycle(bd, xd)
+        ts = []
+        for _ in range(20):
+            t, _ = _timed(stream, lambda: ctx.vcycle(bd, xd))
+            ts.append(t)
+        ms_v = float(np.median(ts))
+        xs = torch.from_numpy(x0).to(dev)
+        ms_s, _ = _timed(stream, lambda: ctx.smooth(bd, xs, nsweeps=1), reps=20)
+        rd = torch.empty_like(bd)
+        ctx.residual(bd, xs, rd)
+        ms_k2, _ = _timed(stream, lambda: ctx.patch_apply(rd), reps=20)
+        k2_bytes = 8 * fin["sum_n2"] + 16 * fin["sum_n"]
+        out[name] = {"finest_dofs": n, "levels": ctx.num_levels(), "vcycle_ms": ms_v, "sweep_ms": ms_s,
+                     "K2_ms": ms_k2, "K2_gbs": k2_bytes / (ms_k2 * 1e-3) / 1e9,
+                     "K2_frac": k2_bytes / (ms_k2 * 1e-3) / 1e9 / peak,
+                     "dofs_per_s": 2 * cfg.nu * n / (ms_v * 1e-3)}
+        ctx.close()
+    return out
+
+
 def run_variants(cfg, seed, dev, stream):
     """NEXT-2: the k = 2 (CG2 x RT2) 2D E-B block at 512^2 (V-cycle, sweep, K2, FGMRES).
     NEXT-4: the c5 operator in the transient (implicit Euler, dt = 0.01 as P:656) Newton
@@ -560,8 +601,10 @@ def run_ours(args):
 
     # ---- NEXT-4 / NEXT-3 measured on the same kernels (skipped with --no-variants) ----
     variants = None
+    configs = None
     if not args.no_variants and ws == 1:
         variants = run_variants(cfg, seed, dev, stream)
+        configs = run_configs(seed, dev, stream)
 
     # algorithmic bytes: K2 per patch i: 8 n_i^2 factor + 8 n_i gathered r
     # + 8 n_i written y; sweep: 8 sum n_i^2 + 8 nnz + 24 n
@@ -641,6 +684,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "solves": solves,
             "variants": variants,
+            "other_configs": configs,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
