@@ -160,9 +160,11 @@ def _patch_vertices(cfg):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+@pytest.mark.parametrize("name", ["c3", "c4"])
 def test_full_size_sweep_sampled(oracle_mod, name):
-    """Full-size c3 / c4 / c5 (c5 = 3,939,840 DoFs, the configuration bench.py times): one
+    """Full-size c3 / c4 (c5, the configuration bench.py times, is checked whole against
+    the oracle's golden sweep and V-cycle in test_gpu_golden.py, which replaced its ~300 s
+    sampled case here; c3 / c4 are checked both ways): one
     sweep from x0 = U(-1,1) on the GPU; the DoFs of the patches of ~40 sampled vertices
     (interior, wall, edge, corner) recomputed one by one by the exact oracle from a
     masked assembly; bit-exact, and relative l2 over the sample <= 1e-10."""
