@@ -21,7 +21,7 @@ PROBE = os.path.join(ROOT, "tools", "libprobe.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU = ["kernels.cu", "k2_small.cu", "k7_dense_lu.cu", "k8_coarse.cu", "api.cu"]
+CU = ["kernels.cu", "k2_small.cu", "k6_patch_lu.cu", "k7_dense_lu.cu", "k8_coarse.cu", "api.cu"]
 CPP = ["fe_setup.cpp"]
 HEADERS = ["kernels.cuh", "k2_common.cuh", "setup.hpp"]
 

@@ -93,6 +93,10 @@ void launch_residual_b3(const DevBSell3 &A, const double *b, const double *x, do
 int64_t patch_lu_scratch_doubles(const DevPatches &P);
 void launch_patch_lu(const DevPatches &P, const int64_t *rowptr, const int *col, const double *val, int *status,
                      double *scratch, cudaStream_t s);
+// K6 for stars of 33..128 DoFs (k6_patch_lu.cu): column-major, look-ahead panel warp
+bool patch_lu_cm_supported(int max_n);
+void launch_patch_lu_cm(const DevPatches &P, const int64_t *rowptr, const int *col, const double *val, int *status,
+                        cudaStream_t s);
 // K2: y_i = A_i^-1 R_i r for every patch
 void launch_patch_apply(const DevPatches &P, const double *r, cudaStream_t s);
 // K3: x_d <- fma(w_d, sum y, x_d)    (x_is_zero: x_d <- fma(w_d, sum y, 0.0))
