@@ -1,26 +1,36 @@
-// k6_patch_lu.cu -- K6 for the 3D k = 1 stars (32 < n <= 128 DoFs): batched patch LU with a
-// look-ahead panel warp.  Same arithmetic as k_patch_lu (kernels.cu): the unblocked
-// right-looking LU with partial pivoting of reading R-lu (first index of max |a_ik|, whole
-// rows swapped, singular if !(|a_kk| > 1e-14 max|A_i|), l_ik = a_ik / a_kk (IEEE),
-// a_ij = fma(-l_ik, a_kj, a_ij) for k ascending), so factors and pivots are bit-identical.
+// k6_patch_lu.cu -- K6 for the 3D k = 1 stars (32 < n <= 128 DoFs): batched patch LU, blocked
+// in panels of B = 4 steps with a look-ahead panel group.  Same arithmetic as k_patch_lu
+// (kernels.cu): the unblocked right-looking LU with partial pivoting of reading R-lu (first
+// index of max |a_ik|, whole rows swapped, singular if !(|a_kk| > 1e-14 max|A_i|),
+// l_ik = a_ik / a_kk (IEEE), a_ij = fma(-l_ik, a_kj, a_ij) for k ascending), so factors and
+// pivots are bit-identical.
 //
-// Why another kernel: k_patch_lu spends ~4300 warp instructions per elimination step and
-// patch, of which ~120 are the step's DFMAs -- the per-step bookkeeping (staging the pivot
-// row, divisions, candidate reduction, two barriers) is replicated in all 8 warps and bounds
-// the kernel (profiles/k6/summary.txt).  Here
-//   * the matrix is COLUMN-major in shared memory (ld odd), lanes run over rows, so a column
-//     is one conflict-free run and a row swap inside a column is two broadcast loads;
-//   * warp 0 is the PANEL warp: during phase k (the other warps apply step k to columns
-//     j >= k+2) it applies step k to column k+1 in registers, finds the pivot of step k+1
-//     (three redux.sync on the bit pattern of |a| and the row index: first maximum), forms
-//     the multipliers l_{.,k+1} by IEEE division and publishes them and the pivot row index;
-//   * warps 1..7 own the columns j = k+2 + (w-1) + 7m of phase k.  For each they swap rows
-//     k / p_k of that column (two broadcast loads, one store; the lane that owns row p_k takes
-//     the old a_kj from a register) and update the rows i > k: one LDS, one DFMA, one STS per
-//     32 rows, chunks of rows <= k skipped by a uniform switch;
-//   * ONE barrier per step; the swaps of the already finished L columns (R-lu swaps whole
-//     rows) are applied at the end, column by column in step order.
-// The packed store (k2_common.cuh) copies contiguous column pieces.
+// Why another kernel (profiles/k6/): k_patch_lu is bound by its per-step chain -- pivot
+// search, divisions, staging and two barriers per step, replicated in 8 warps (~4300 warp
+// instructions per step, ~120 of them DFMAs).  A first rewrite with ONE look-ahead panel warp
+// holding four 32-row chunks per lane was bound by that warp's own instruction stream (~320
+// dependent instructions per step, 87% of all stall samples on the phase barrier).  Here
+//   * one CTA per star, 12 warps; the matrix is COLUMN-major in shared memory (ld odd), lanes
+//     run over rows;
+//   * warps 0..3 are the PANEL GROUP: warp w owns rows 32w..32w+31, one row per lane, so the
+//     four columns of a panel are four registers per thread.  Per step: warp arg-max by
+//     redux.sync on the high word of |a| and a ballot (the low word only on ties; first
+//     maximum), while every candidate lane forms the reciprocal of its own entry; the four
+//     candidates (value, reciprocal, row) and row kk meet in a double-buffered exchange area
+//     (ONE named barrier per step), the multipliers follow by PivotDiv's Markstein correction
+//     (k2_common.cuh) from the winner's reciprocal, and the panel's remaining columns are
+//     updated in registers.  While the other warps apply panel K, the group already factors
+//     panel K+1;
+//   * warps 4..11 apply a finished panel to the trailing columns (a contiguous range of
+//     columns per warp): the B row swaps and the 4 x 4 triangular solve for u_{k0..k0+3, j} run
+//     with lanes over the warp's columns (stride ld: conflict-free), then element (i, j) takes
+//     fma(-l_ik, u_kj, .) for k = k0..k0+3 in ascending order between ONE load and ONE store
+//     (the rank-1 form is bound by shared-memory bandwidth: 512 B per 32 DFMAs);
+//   * the same warps apply the panel's swaps to the finished L columns on its left (R-lu
+//     swaps whole rows), lanes over columns, so the packed store at the end is a plain copy;
+//   * ONE CTA barrier per panel.
+// The CSR rows are gathered through a 1024-slot hash DoF -> patch row (loads of five rows in
+// flight per warp).  Packed factor layout: k2_common.cuh.
 #include <climits>
 #include <cstdio>
 #include <type_traits>
@@ -32,84 +42,101 @@ namespace mhdp {
 
 #ifdef MHDP_K6_PROF   // diagnostics build only: SM cycles per phase, summed over CTAs (thread 0)
 __device__ unsigned long long g_k6prof[4];
-#define K6_STAMP(slot)                                                  \
-    do {                                                                \
-        if (tid == 0) {                                                 \
-            const long long now_ = clock64();                           \
+#define K6_STAMP(slot)                                                       \
+    do {                                                                     \
+        if (tid == 0) {                                                      \
+            const long long now_ = clock64();                                \
             atomicAdd(&g_k6prof[slot], (unsigned long long)(now_ - stamp_)); \
-            stamp_ = now_;                                              \
-        }                                                               \
+            stamp_ = now_;                                                   \
+        }                                                                    \
     } while (0)
 #else
 #define K6_STAMP(slot) do { } while (0)
 #endif
 
+namespace {
+constexpr int K6_B = 4;            // panel width
+constexpr int K6_PW = 4;           // panel warps (one 32-row chunk each)
+constexpr int K6_UW = 8;           // update warps
+constexpr int K6_THREADS = 32 * (K6_PW + K6_UW);
+constexpr int K6_HASH = 1024;      // hash slots (load <= 1/8)
+
+// exchange area of the panel group, one per step parity
+struct PanelXchg {
+    double val[K6_PW];               // the warp's max |a| over its candidate rows (-1: none)
+    double rcp[K6_PW];               // RN(1 / that entry), 0 outside PivotDiv's guarded range
+    double row[K6_PW][K6_B];         // that row's entries in the panel's columns
+    double rowk[K6_B];               // row kk's entries
+    int lane[K6_PW];                 // lane of the warp's first maximum
+};
+
+__device__ __forceinline__ void panel_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * K6_PW) : "memory"); }
+}  // namespace
+
 template <int NCH>   // 32-row chunks per column: stars up to 32 NCH DoFs
-__global__ void __launch_bounds__(256, 2) k_patch_lu_cm(int64_t np, const int *__restrict__ pn,
-                                                        const int64_t *__restrict__ poff,
-                                                        const int64_t *__restrict__ foff,
-                                                        const int *__restrict__ pdofs,
-                                                        const int64_t *__restrict__ rowptr,
-                                                        const int *__restrict__ col, const double *__restrict__ val,
-                                                        double *__restrict__ fac, int *__restrict__ gidx,
-                                                        int *__restrict__ perm_out, int *__restrict__ status, int ld,
-                                                        int maxn) {
-    extern __shared__ double sm[];   // a[maxn][ld] column-major, then dofs / prm / spv / rlen, the hash, rp0
-    __shared__ double red[8];
+__global__ void __launch_bounds__(K6_THREADS, 2)
+k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict__ poff,
+              const int64_t *__restrict__ foff, const int *__restrict__ pdofs, const int64_t *__restrict__ rowptr,
+              const int *__restrict__ col, const double *__restrict__ val, double *__restrict__ fac,
+              int *__restrict__ gidx, int *__restrict__ perm_out, int *__restrict__ status, int ld, int maxn) {
+    constexpr int B = K6_B;
+    extern __shared__ double sm[];   // a[maxn][ld] column-major, rp0, the exchange area, int tables, the hash
+    __shared__ double red[K6_PW + K6_UW];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     double *const a = sm;
-    int *const dofs = reinterpret_cast<int *>(sm + (size_t)maxn * ld);
-    int *const prm = dofs + 32 * NCH;
-    int *const spv = prm + 32 * NCH;
-    int *const rlen = spv + 32 * NCH;
-    int *const hkey = rlen + 32 * NCH;                                    // 256
-    unsigned char *const hval = reinterpret_cast<unsigned char *>(hkey + 256);   // 256
-    int64_t *const rp0 = reinterpret_cast<int64_t *>(hval + 256);          // 32 NCH (8-byte aligned)
+    int64_t *const rp0 = reinterpret_cast<int64_t *>(sm + (((size_t)maxn * ld + 1) & ~(size_t)1));   // 128 (16-byte aligned)
+    PanelXchg *const xch = reinterpret_cast<PanelXchg *>(rp0 + 128);            // 2
+    int *const dofs = reinterpret_cast<int *>(xch + 2);                          // 128
+    int *const prm = dofs + 128;
+    int *const spv = prm + 128;
+    int *const rlen = spv + 128;
+    int *const hkey = rlen + 128;                                                // K6_HASH
+    unsigned char *const hval = reinterpret_cast<unsigned char *>(hkey + K6_HASH);
     for (int64_t p = blockIdx.x; p < np; p += gridDim.x) {
         const int n = pn[p];
         const int64_t off = poff[p];
 #ifdef MHDP_K6_PROF
         long long stamp_ = clock64();
 #endif
-        for (int e = tid; e < n * ld; e += 256) a[e] = 0.0;
-        hkey[tid] = -1;
+        for (int e = tid; e < n * ld; e += K6_THREADS) a[e] = 0.0;
+        for (int e = tid; e < K6_HASH; e += K6_THREADS) hkey[e] = -1;
         __syncthreads();
-        // stage 1: DoF list, CSR row extents and an open-addressing hash DoF -> patch row
-        // (256 slots, load <= 1/2), all rows at once: one round of global latency
-        for (int e = tid; e < n; e += 256) {
+        // stage 1: DoF list, CSR row extents and an open-addressing hash DoF -> patch row,
+        // all rows at once: one round of global latency
+        for (int e = tid; e < n; e += K6_THREADS) {
             const int d = pdofs[off + e];
             dofs[e] = d;
             prm[e] = e;
             const int64_t t0 = rowptr[d];
             rp0[e] = t0;
             rlen[e] = (int)(rowptr[d + 1] - t0);
-            unsigned h = ((unsigned)d * 2654435761u) >> 24;
-            while (atomicCAS(&hkey[h], -1, d) != -1) h = (h + 1) & 255u;
+            unsigned h = ((unsigned)d * 2654435761u) >> 22;
+            while (atomicCAS(&hkey[h], -1, d) != -1) h = (h + 1) & (K6_HASH - 1);
             hval[h] = (unsigned char)e;
         }
         __syncthreads();
         // stage 2: gather A_i = R_i A R_i^T: warp per patch row, lanes over the CSR row;
-        // the loads of four rows (up to 96 entries each) are issued before the first lookup
+        // the loads of five rows (up to 96 entries each) are issued before the first lookup
         double mx = 0.0;
         auto place = [&](int rr, int c, double v) {
-            unsigned h = ((unsigned)c * 2654435761u) >> 24;
-            for (;;) {
-                const int kk = hkey[h];
-                if (kk == c) {
-                    a[(int)hval[h] * ld + rr] = v;
-                    mx = fmax(mx, fabs(v));
-                    return;
-                }
-                if (kk == -1) return;
-                h = (h + 1) & 255u;
+            unsigned h = ((unsigned)c * 2654435761u) >> 22;
+            int kk = hkey[h];
+            while (kk != c && kk != -1) {   // rare at this load
+                h = (h + 1) & (K6_HASH - 1);
+                kk = hkey[h];
+            }
+            if (kk == c) {
+                a[(int)hval[h] * ld + rr] = v;
+                mx = fmax(mx, fabs(v));
             }
         };
-        for (int r0 = wid; r0 < n; r0 += 32) {
-            int c[4][3];
-            double v[4][3];
+        constexpr int NW = K6_PW + K6_UW, GR = 5;
+        for (int r0 = wid; r0 < n; r0 += NW * GR) {
+            int c[GR][3];
+            double v[GR][3];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int rr = r0 + 8 * q;
+            for (int q = 0; q < GR; ++q) {
+                const int rr = r0 + NW * q;
                 const int64_t t0 = rr < n ? rp0[rr] : 0;
                 const int len = rr < n ? rlen[rr] : 0;
 #pragma unroll
@@ -120,8 +147,8 @@ __global__ void __launch_bounds__(256, 2) k_patch_lu_cm(int64_t np, const int *_
                 }
             }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int rr = r0 + 8 * q;
+            for (int q = 0; q < GR; ++q) {
+                const int rr = r0 + NW * q;
 #pragma unroll
                 for (int u = 0; u < 3; ++u)
                     if (c[q][u] >= 0) place(rr, c[q][u], v[q][u]);
@@ -136,126 +163,232 @@ __global__ void __launch_bounds__(256, 2) k_patch_lu_cm(int64_t np, const int *_
         if (lane == 0) red[wid] = mx;
         __syncthreads();
         double amax = red[0];
-        for (int w = 1; w < 8; ++w) amax = fmax(amax, red[w]);
+#pragma unroll
+        for (int w = 1; w < NW; ++w) amax = fmax(amax, red[w]);
         const double thr = 1e-14 * amax;
         K6_STAMP(0);
 
-        // panel warp state: multipliers of the last finished step (rows lane + 32 t) and its pivot row
-        double lreg[NCH];
-        int pvprev = 0;
-        // column j: apply step j-1 (registers), pivot search, multipliers; publishes spv[j]
-        auto panel_col = [&](int j) {
-            double *cj = a + (size_t)j * ld;
-            double c[NCH];
-            if (j > 0) {
-                const int k = j - 1;
-                const double u = cj[pvprev], tt = cj[k];
-#pragma unroll
-                for (int t = 0; t < NCH; ++t) {
-                    const int i = lane + 32 * t;
-                    double x = i < n ? cj[i] : 0.0;
-                    if (i == pvprev) x = tt;
-                    if (i > k && i < n) x = fma(-lreg[t], u, x);
-                    c[t] = x;
-                }
-                __syncwarp();
-                if (lane == 0) cj[k] = u;
-            } else {
-#pragma unroll
-                for (int t = 0; t < NCH; ++t) {
-                    const int i = lane + 32 * t;
-                    c[t] = i < n ? cj[i] : 0.0;
-                }
-            }
-            // first index of max |a_ij| over i >= j (NaN never wins; R-lu / od_lu order)
-            double best = -1.0, bs = 0.0, sj = 0.0;   // bs: the signed entry at the lane's first maximum
-            int bi = INT_MAX;
-#pragma unroll
-            for (int t = 0; t < NCH; ++t) {
-                const int i = lane + 32 * t;
-                const double v = fabs(c[t]);
-                if (i == j) sj = c[t];
-                if (i >= j && i < n && v > best) { best = v; bi = i; bs = c[t]; }
-            }
-            const unsigned long long key =
-                bi == INT_MAX ? 0ull : (unsigned long long)__double_as_longlong(best) + 1ull;
-            const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
-            const unsigned mhi = __reduce_max_sync(FULL, khi);
-            const unsigned mlo = __reduce_max_sync(FULL, khi == mhi ? klo : 0u);
-            int pv = __reduce_min_sync(FULL, (khi == mhi && klo == mlo && bi != INT_MAX) ? bi : INT_MAX);
-            const bool none = pv == INT_MAX;   // every candidate is NaN: od_lu keeps p = j (singular)
-            if (none) pv = j;
-            const double piv = __shfl_sync(FULL, bs, pv & 31);   // the winning lane has bi == pv
-            const double ajj = __shfl_sync(FULL, sj, j & 31);
-            // od_lu starts from best = |a_jj|: a NaN there keeps p = j and the step is singular
-            if (none || !(fabs(piv) > thr) || isnan(ajj)) {
-                if (lane == 0) spv[j] = -1;
-                return;
-            }
-#pragma unroll
-            for (int t = 0; t < NCH; ++t) {
-                const int i = lane + 32 * t;
-                double l = 0.0;
-                if (i > j && i < n) {
-                    l = (i == pv ? ajj : c[t]) / piv;
-                    cj[i] = l;
-                }
-                lreg[t] = l;
-            }
-            if (lane == 0) {
-                cj[j] = piv;
-                spv[j] = pv;
-                if (pv != j) { const int t = prm[j]; prm[j] = prm[pv]; prm[pv] = t; }
-            }
-            pvprev = pv;
-        };
+        // ---------------- blocked LU ----------------
+        const int row = tid;         // panel group: the row this thread owns (tid < 128)
+        double cp[B] = {0.0, 0.0, 0.0, 0.0};   // panel group: this row's entries in the last factored panel
         bool bad = false;
-        for (int k = -1; k < n; ++k) {   // phase -1: the panel warp alone prepares step 0
-            int pv = 0;
-            if (k >= 0) {
-                __syncthreads();   // step k's multipliers and pivot are published; phase k-1's updates are done
-                pv = spv[k];
-                if (pv < 0) { bad = true; break; }
+        const int nphase = (n + B - 1) / B;
+        for (int K = -1; K < nphase; ++K) {   // phase -1: the panel group alone factors panel 0
+            const int k0 = K * B, k1 = k0 + B;   // panel K = steps k0..k0+3 (published); trailing rows from k1
+            int pvk[B] = {0, 0, 0, 0};
+            if (K >= 0) {
+                __syncthreads();   // panel K's multipliers and pivots are published; phase K-1's updates are done
+#pragma unroll
+                for (int s = 0; s < B; ++s) {
+                    pvk[s] = k0 + s < n ? spv[k0 + s] : k0 + s;
+                    bad = bad || pvk[s] < 0;
+                }
+                if (bad) break;
             }
-            if (wid == 0) {
-                if (k + 1 < n) panel_col(k + 1);
+            // rows k0..k0+3 of a trailing column: the B swaps, then u = L11^-1 x (fma chains, k ascending)
+            double l10 = 0, l20 = 0, l21 = 0, l30 = 0, l31 = 0, l32 = 0;
+            if (K >= 0 && k1 < n) {
+                const double *c0 = a + (size_t)k0 * ld + k0, *c1 = c0 + ld, *c2 = c1 + ld;
+                l10 = c0[1]; l20 = c0[2]; l30 = c0[3];
+                l21 = c1[2]; l31 = c1[3];
+                l32 = c2[3];
+            }
+            auto top_rows = [&](double *cj) {
+#pragma unroll
+                for (int s = 0; s < B; ++s) {
+                    const int A = k0 + s, Bp = pvk[s];
+                    if (Bp != A) { const double tA = cj[A], tB = cj[Bp]; cj[A] = tB; cj[Bp] = tA; }
+                }
+                const double u0 = cj[k0];
+                const double u1 = fma(-l10, u0, cj[k0 + 1]);
+                const double u2 = fma(-l21, u1, fma(-l20, u0, cj[k0 + 2]));
+                const double u3 = fma(-l32, u2, fma(-l31, u1, fma(-l30, u0, cj[k0 + 3])));
+                cj[k0 + 1] = u1; cj[k0 + 2] = u2; cj[k0 + 3] = u3;
+            };
+            if (wid < K6_PW) {
+                // ======== panel group: factor panel K+1 (columns k1..k1+nb-1) ========
+                if (k1 >= n) continue;
+                const int nb = min(B, n - k1);
+                if (K >= 0) {
+                    if (tid < nb) top_rows(a + (size_t)(k1 + tid) * ld);
+                    panel_bar();
+                }
+                double c[B];
+#pragma unroll
+                for (int s = 0; s < B; ++s) {
+                    const double *cj = a + (size_t)(k1 + (s < nb ? s : 0)) * ld;
+                    double x = (s < nb && row < n) ? cj[row] : 0.0;
+                    if (K >= 0 && row >= k1) {
+                        x = fma(-cp[0], cj[k0], x);
+                        x = fma(-cp[1], cj[k0 + 1], x);
+                        x = fma(-cp[2], cj[k0 + 2], x);
+                        x = fma(-cp[3], cj[k0 + 3], x);
+                    }
+                    c[s] = x;
+                }
+                int pvs[B] = {0, 0, 0, 0};
+                int fail = -1;
+#pragma unroll
+                for (int s = 0; s < B; ++s) {
+                    if (s < nb && fail < 0) {
+                        const int kk = k1 + s;
+                        PanelXchg &X = xch[s & 1];
+                        // Warp arg-max over its rows >= kk (NaN never wins; first maximum): redux.sync
+                        // on the high word of |a|, the low word only when several lanes tie on it.
+                        // Meanwhile every candidate lane forms RN(1 / own entry): the winner's is the
+                        // step's reciprocal, so no division sits behind the exchange barrier.
+                        const double cs = c[s];
+                        const double v = fabs(cs);
+                        const bool cand = row >= kk && row < n && v >= 0.0;
+                        const unsigned long long vb = (unsigned long long)__double_as_longlong(v);
+                        double rown = 0.0;
+                        if (cand && v > 0x1p-400 && v < 0x1p400 && (vb & 0xfffffffffffffull) != 0xfffffffffffffull)
+                            rown = 1.0 / cs;
+                        const unsigned khi = cand ? (unsigned)(vb >> 32) + 1u : 0u;
+                        const unsigned mhi = __reduce_max_sync(FULL, khi);
+                        const bool top = cand && khi == mhi;
+                        unsigned ball = __ballot_sync(FULL, top);
+                        if (__popc(ball) > 1) {
+                            const unsigned klo = top ? (unsigned)vb : 0u;
+                            const unsigned mlo = __reduce_max_sync(FULL, klo);
+                            ball = __ballot_sync(FULL, top && klo == mlo);
+                        }
+                        const int wl = ball ? __ffs(ball) - 1 : 0;
+                        if (lane == wl) {
+                            X.val[wid] = ball ? v : -1.0;
+                            X.rcp[wid] = rown;
+                            X.lane[wid] = wl;
+                            *reinterpret_cast<double2 *>(&X.row[wid][0]) = make_double2(c[0], c[1]);
+                            *reinterpret_cast<double2 *>(&X.row[wid][2]) = make_double2(c[2], c[3]);
+                        }
+                        if (row == kk) {
+                            *reinterpret_cast<double2 *>(&X.rowk[0]) = make_double2(c[0], c[1]);
+                            *reinterpret_cast<double2 *>(&X.rowk[2]) = make_double2(c[2], c[3]);
+                        }
+                        panel_bar();
+                        const double2 v01 = *reinterpret_cast<const double2 *>(&X.val[0]);
+                        const double2 v23 = *reinterpret_cast<const double2 *>(&X.val[2]);
+                        double bv = v01.x;
+                        int bw = 0;
+                        if (v01.y > bv) { bv = v01.y; bw = 1; }
+                        if (v23.x > bv) { bv = v23.x; bw = 2; }
+                        if (v23.y > bv) { bv = v23.y; bw = 3; }
+                        const bool none = !(bv >= 0.0);   // every candidate is NaN: od_lu keeps p = kk (singular)
+                        const int pv = none ? kk : 32 * bw + X.lane[bw];
+                        const double piv = X.row[bw][s];
+                        const double r = X.rcp[bw];
+                        const double akk = X.rowk[s];
+                        // od_lu starts from best = |a_kk|: a NaN there keeps p = kk and the step is singular
+                        if (none || !(fabs(piv) > thr) || isnan(akk)) {
+                            fail = s;
+                        } else {
+                            if (pv != kk) {   // swap rows kk / pv in every column of the panel
+                                if (row == kk) {
+#pragma unroll
+                                    for (int s2 = 0; s2 < B; ++s2) c[s2] = X.row[bw][s2];
+                                } else if (row == pv) {
+#pragma unroll
+                                    for (int s2 = 0; s2 < B; ++s2) c[s2] = X.rowk[s2];
+                                }
+                            }
+                            const bool below = row > kk && row < n;
+                            if (below) {   // l = a_ik / piv: PivotDiv's arithmetic with the published reciprocal
+                                const double x = c[s], ax = fabs(x);
+                                const double q0 = x * r;
+                                double q = fma(fma(-q0, piv, x), r, q0);
+                                if (ax == 0.0) q = q0;
+                                if (!(r != 0.0 && (ax == 0.0 || (ax > 0x1p-400 && ax < 0x1p400)))) q = x / piv;
+                                c[s] = q;
+                            }
+#pragma unroll
+                            for (int s2 = s + 1; s2 < B; ++s2) {
+                                const double u = X.row[bw][s2];   // row kk of column s2 after the swap
+                                if (below) c[s2] = fma(-c[s], u, c[s2]);
+                            }
+                            pvs[s] = pv;
+                        }
+                    }
+                }
+                // write the panel back (rows >= k1: its U and L parts) and publish the pivots
+#pragma unroll
+                for (int s = 0; s < B; ++s) {
+                    if (s < nb && row >= k1 && row < n) a[(size_t)(k1 + s) * ld + row] = c[s];
+                    cp[s] = c[s];
+                }
+                if (tid == 0) {
+#pragma unroll
+                    for (int s = 0; s < B; ++s) {
+                        if (s < nb && (fail < 0 || s <= fail)) {
+                            const int kk = k1 + s;
+                            if (s == fail) { spv[kk] = -1; }
+                            else {
+                                spv[kk] = pvs[s];
+                                if (pvs[s] != kk) { const int t = prm[kk]; prm[kk] = prm[pvs[s]]; prm[pvs[s]] = t; }
+                            }
+                        }
+                    }
+                }
                 continue;
             }
-            if (k < 0) continue;
-            const double *ck = a + (size_t)k * ld;
+            if (K < 0) continue;
+            // ======== update warps ========
+            const int uw = wid - K6_PW;
+            // panel K's swaps on the finished L columns to its left (16 columns per warp, lanes over
+            // columns); after the trailing update: nothing in this phase waits for them
+            auto left_swaps = [&]() {
+                const int j = 16 * uw + lane;
+                if (lane < 16 && j < k0) {
+                    double *cj = a + (size_t)j * ld;
+#pragma unroll
+                    for (int s = 0; s < B; ++s) {
+                        const int A = k0 + s, Bp = pvk[s];
+                        if (Bp != A) { const double tA = cj[A], tB = cj[Bp]; cj[A] = tB; cj[Bp] = tA; }
+                    }
+                }
+            };
+            if (k1 + B >= n) { left_swaps(); continue; }
+            // trailing columns beyond the next panel: a contiguous range per warp
+            const int ncol = n - (k1 + B), per = (ncol + K6_UW - 1) / K6_UW;
+            const int j0 = k1 + B + uw * per, j1 = min(n, j0 + per);
+            if (j0 + lane < j1) top_rows(a + (size_t)(j0 + lane) * ld);
+            __syncwarp();
+            const double *ck = a + (size_t)k0 * ld;
             auto cols = [&](auto t0c) {
-                constexpr int T0 = decltype(t0c)::value;   // chunks < T0 hold only rows <= k
-                double lr[NCH];
-                bool act[NCH], isp[NCH];
+                constexpr int T0 = decltype(t0c)::value;   // chunks < T0 hold only rows < k1
+                double l[B][NCH];
+                bool act[NCH];
 #pragma unroll
                 for (int t = T0; t < NCH; ++t) {
                     const int i = lane + 32 * t;
-                    act[t] = i > k && i < n;
-                    isp[t] = i == pv;
-                    lr[t] = act[t] ? ck[i] : 0.0;
+                    act[t] = i >= k1 && i < n;
+#pragma unroll
+                    for (int s = 0; s < B; ++s) l[s][t] = act[t] ? ck[(size_t)s * ld + i] : 0.0;
                 }
 #pragma unroll 2
-                for (int j = k + 1 + wid; j < n; j += 7) {
+                for (int j = j0; j < j1; ++j) {
                     double *cj = a + (size_t)j * ld;
-                    const double u = cj[pv], tt = cj[k];
+                    const double u0 = cj[k0], u1 = cj[k0 + 1], u2 = cj[k0 + 2], u3 = cj[k0 + 3];
 #pragma unroll
                     for (int t = T0; t < NCH; ++t) {
                         if (act[t]) {
                             const int i = lane + 32 * t;
-                            const double x = isp[t] ? tt : cj[i];
-                            cj[i] = fma(-lr[t], u, x);
+                            double x = cj[i];
+                            x = fma(-l[0][t], u0, x);
+                            x = fma(-l[1][t], u1, x);
+                            x = fma(-l[2][t], u2, x);
+                            x = fma(-l[3][t], u3, x);
+                            cj[i] = x;
                         }
                     }
-                    __syncwarp();
-                    if (lane == 0) cj[k] = u;
                 }
             };
-            switch ((k + 1) >> 5) {
+            switch (k1 >> 5) {
                 case 0: cols(std::integral_constant<int, 0>{}); break;
                 case 1: cols(std::integral_constant<int, NCH >= 2 ? 1 : 0>{}); break;
                 case 2: cols(std::integral_constant<int, NCH >= 3 ? 2 : 0>{}); break;
                 default: cols(std::integral_constant<int, NCH >= 4 ? 3 : 0>{}); break;
             }
+            left_swaps();
         }
         __syncthreads();
         K6_STAMP(1);
@@ -264,26 +397,24 @@ __global__ void __launch_bounds__(256, 2) k_patch_lu_cm(int64_t np, const int *_
             __syncthreads();
             continue;
         }
-        // R-lu swaps whole rows: apply the swaps of steps k > j to the finished L column j
-        if (tid < n) {
-            double *cj = a + (size_t)tid * ld;
-            for (int k = tid + 1; k < n; ++k) {
-                const int pv = spv[k];
-                if (pv != k) { const double t = cj[k]; cj[k] = cj[pv]; cj[pv] = t; }
-            }
-        }
-        __syncthreads();
         // packed streaming layout (k2_common.cuh): column pieces are contiguous on both sides
         double *F = fac + foff[p];
-        for (int j = wid; j < n; j += 8) {
+        for (int j = wid; j < n; j += NW) {
             const double *cj = a + (size_t)j * ld;
             double *Lf = F + pack_fwd(n, j) - (j + 1);   // l_ij at Lf[i], i > j
-            for (int i = j + 1 + lane; i < n; i += 32) Lf[i] = cj[i];
-            double *Ub = F + pack_bwd(n, j);
-            if (lane == 0) { const double v = cj[j]; Ub[0] = v; Ub[1] = 1.0 / v; }
-            for (int i = lane; i < j; i += 32) Ub[2 + i] = cj[i];
+            double *Ub = F + pack_bwd(n, j);             // [u_jj, RN(1/u_jj), u_0j .. u_{j-1,j}]
+#pragma unroll
+            for (int t = 0; t < NCH; ++t) {
+                const int i = lane + 32 * t;
+                if (i < n) {
+                    const double v = cj[i];
+                    if (i > j) Lf[i] = v;
+                    else if (i < j) Ub[2 + i] = v;
+                    else { Ub[0] = v; Ub[1] = 1.0 / v; }
+                }
+            }
         }
-        for (int e = tid; e < n; e += 256) {
+        for (int e = tid; e < n; e += K6_THREADS) {
             gidx[off + e] = dofs[prm[e]];
             perm_out[off + e] = prm[e];
         }
@@ -297,18 +428,18 @@ bool patch_lu_cm_supported(int max_n) { return max_n > 32 && max_n <= 128; }
 
 void launch_patch_lu_cm(const DevPatches &P, const int64_t *rowptr, const int *col, const double *val, int *status,
                         cudaStream_t s) {
-    const int ld = P.max_n | 1;   // odd: the end-of-factorisation swaps run one thread per column
+    const int ld = P.max_n | 1;   // odd: lanes over columns (swaps, triangular solves) are conflict-free
     const int nch = (P.max_n + 31) / 32;
-    size_t smem = sizeof(double) * (size_t)P.max_n * ld + sizeof(int) * (4 * 32 * nch + 256) + 256 +
-                  sizeof(int64_t) * 32 * nch;
+    size_t smem = sizeof(double) * (((size_t)P.max_n * ld + 1) & ~(size_t)1) + sizeof(int64_t) * 128 + 2 * sizeof(PanelXchg) +
+                  sizeof(int) * (4 * 128 + K6_HASH) + K6_HASH;
     smem = (smem + 15) & ~(size_t)15;
-    const int per_sm = smem > 110 * 1024 ? 1 : (smem > 70 * 1024 ? 2 : (smem > 50 * 1024 ? 3 : 4));
+    const int per_sm = smem > 110 * 1024 ? 1 : 2;
     const int64_t cap = (int64_t)sm_count() * per_sm * 4;
     const unsigned g = (unsigned)(P.np < cap ? P.np : cap);
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<g, 256, smem, s>>>(P.np, P.pn, P.poff, P.foff, P.pdofs, rowptr, col, val, P.fac, P.gidx, P.perm,
-                                  status, ld, P.max_n);
+        kern<<<g, K6_THREADS, smem, s>>>(P.np, P.pn, P.poff, P.foff, P.pdofs, rowptr, col, val, P.fac, P.gidx,
+                                         P.perm, status, ld, P.max_n);
     };
     if (nch <= 2) go(k_patch_lu_cm<2>);
     else if (nch == 3) go(k_patch_lu_cm<3>);

@@ -162,11 +162,12 @@ __global__ void __launch_bounds__(PT) k_lu_panel_cl(double *__restrict__ a, int 
         if (!(fabs(piv) > thr)) return;                    // uniform over the cluster
         __syncthreads();
         // ---- multipliers and the panel update of owned rows below the pivot ----
+        const PivotDiv dv(piv);   // IEEE quotients without the slow path of '/' on zero numerators
         for (int lr = tid; lr < nr; lr += PT) {
             const int i = row0 + lr;
             if (i <= gj) continue;
             double *ri = sp + lr * LU_NB;
-            const double l = ri[j] / piv;
+            const double l = dv(ri[j]);
             ri[j] = l;
             for (int c = j + 1; c < kb; ++c) ri[c] = fma(-l, prow[c], ri[c]);
         }
