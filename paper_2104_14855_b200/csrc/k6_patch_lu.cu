@@ -32,6 +32,7 @@
 // The CSR rows are gathered through a 1024-slot hash DoF -> patch row (loads of five rows in
 // flight per warp).  Packed factor layout: k2_common.cuh.
 #include <climits>
+#include <cstdint>
 #include <cstdio>
 #include <type_traits>
 
@@ -41,7 +42,7 @@
 namespace mhdp {
 
 #ifdef MHDP_K6_PROF   // diagnostics build only: SM cycles per phase, summed over CTAs (thread 0)
-__device__ unsigned long long g_k6prof[4];
+__device__ unsigned long long g_k6prof[16];
 #define K6_STAMP(slot)                                                       \
     do {                                                                     \
         if (tid == 0) {                                                      \
@@ -50,8 +51,20 @@ __device__ unsigned long long g_k6prof[4];
             stamp_ = now_;                                                   \
         }                                                                    \
     } while (0)
+// finer timeline of the LU phase: thread 0 (panel group) and thread 128 (first update warp)
+#define K6_T0() long long t0_ = clock64()
+#define K6_LAP(slot, who)                                                    \
+    do {                                                                     \
+        if (tid == (who)) {                                                  \
+            const long long now_ = clock64();                                \
+            atomicAdd(&g_k6prof[slot], (unsigned long long)(now_ - t0_));    \
+            t0_ = now_;                                                      \
+        }                                                                    \
+    } while (0)
 #else
 #define K6_STAMP(slot) do { } while (0)
+#define K6_T0() do { } while (0)
+#define K6_LAP(slot, who) do { } while (0)
 #endif
 
 namespace {
@@ -61,13 +74,12 @@ constexpr int K6_UW = 8;           // update warps
 constexpr int K6_THREADS = 32 * (K6_PW + K6_UW);
 constexpr int K6_HASH = 1024;      // hash slots (load <= 1/8)
 
-// exchange area of the panel group, one per step parity
+// exchange area of the panel group, one per step parity (16-byte aligned fields)
 struct PanelXchg {
-    double val[K6_PW];               // the warp's max |a| over its candidate rows (-1: none)
-    double rcp[K6_PW];               // RN(1 / that entry), 0 outside PivotDiv's guarded range
+    double2 vr[K6_PW];               // per panel warp: max |a| over its live rows (-1: none), rcp_nr of that entry
     double row[K6_PW][K6_B];         // that row's entries in the panel's columns
-    double rowk[K6_B];               // row kk's entries
-    int lane[K6_PW];                 // lane of the warp's first maximum
+    int pos[K6_PW];                  // its position
+    double akk, pad;                 // the entry at position kk
 };
 
 __device__ __forceinline__ void panel_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * K6_PW) : "memory"); }
@@ -92,6 +104,33 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
     int *const rlen = spv + 128;
     int *const hkey = rlen + 128;                                                // K6_HASH
     unsigned char *const hval = reinterpret_cast<unsigned char *>(hkey + K6_HASH);
+    // Update-warp thread 128 + e carries, in registers, DoF e of the star `pt` this CTA factors
+    // next, its CSR row start and length, and prefetches that row into L2 -- one step per early
+    // LU phase of the current star (stages: 1 size, 2 DoF, 3 row extent, 4 prefetched),
+    // so the gather of the next star starts from registers and reads L2-resident rows.
+    int64_t nx_t0 = 0;
+    int nx_stage = 0, nx_n = 0, nx_d = 0, nx_len = 0;
+    auto nx_advance = [&](int want, int64_t pt) {
+        const int e = tid - 32 * K6_PW;
+        while (nx_stage < want) {
+            if (nx_stage == 0) {
+                nx_n = pt < np ? pn[pt] : 0;
+            } else if (nx_stage == 1) {
+                if (e < nx_n) nx_d = pdofs[poff[pt] + e];
+            } else if (nx_stage == 2) {
+                if (e < nx_n) { nx_t0 = rowptr[nx_d]; nx_len = (int)(rowptr[nx_d + 1] - nx_t0); }
+            } else if (e < nx_n) {
+                const char *q = reinterpret_cast<const char *>(col + nx_t0), *qe = reinterpret_cast<const char *>(col + nx_t0 + nx_len);
+                for (q = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(q) & ~(uintptr_t)127); q < qe; q += 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+                q = reinterpret_cast<const char *>(val + nx_t0);
+                qe = reinterpret_cast<const char *>(val + nx_t0 + nx_len);
+                for (q = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(q) & ~(uintptr_t)127); q < qe; q += 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+            }
+            ++nx_stage;
+        }
+    };
     for (int64_t p = blockIdx.x; p < np; p += gridDim.x) {
         const int n = pn[p];
         const int64_t off = poff[p];
@@ -101,18 +140,21 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
         for (int e = tid; e < n * ld; e += K6_THREADS) a[e] = 0.0;
         for (int e = tid; e < K6_HASH; e += K6_THREADS) hkey[e] = -1;
         __syncthreads();
-        // stage 1: DoF list, CSR row extents and an open-addressing hash DoF -> patch row,
-        // all rows at once: one round of global latency
-        for (int e = tid; e < n; e += K6_THREADS) {
-            const int d = pdofs[off + e];
-            dofs[e] = d;
-            prm[e] = e;
-            const int64_t t0 = rowptr[d];
-            rp0[e] = t0;
-            rlen[e] = (int)(rowptr[d + 1] - t0);
-            unsigned h = ((unsigned)d * 2654435761u) >> 22;
-            while (atomicCAS(&hkey[h], -1, d) != -1) h = (h + 1) & (K6_HASH - 1);
-            hval[h] = (unsigned char)e;
+        // stage 1: DoF list, CSR row extents and an open-addressing hash DoF -> patch row, from
+        // the registers filled during the previous star's LU (the CTA's first star loads them here)
+        if (tid >= 32 * K6_PW) {
+            nx_advance(3, p);   // no-op except for the CTA's first star
+            const int e = tid - 32 * K6_PW;
+            if (e < n) {
+                dofs[e] = nx_d;
+                prm[e] = e;
+                rp0[e] = nx_t0;
+                rlen[e] = nx_len;
+                unsigned h = ((unsigned)nx_d * 2654435761u) >> 22;
+                while (atomicCAS(&hkey[h], -1, nx_d) != -1) h = (h + 1) & (K6_HASH - 1);
+                hval[h] = (unsigned char)e;
+            }
+            nx_stage = 0;
         }
         __syncthreads();
         // stage 2: gather A_i = R_i A R_i^T: warp per patch row, lanes over the CSR row;
@@ -170,14 +212,18 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
 
         // ---------------- blocked LU ----------------
         const int row = tid;         // panel group: the row this thread owns (tid < 128)
-        double cp[B] = {0.0, 0.0, 0.0, 0.0};   // panel group: this row's entries in the last factored panel
         bool bad = false;
         const int nphase = (n + B - 1) / B;
+        K6_T0();
         for (int K = -1; K < nphase; ++K) {   // phase -1: the panel group alone factors panel 0
             const int k0 = K * B, k1 = k0 + B;   // panel K = steps k0..k0+3 (published); trailing rows from k1
             int pvk[B] = {0, 0, 0, 0};
+            K6_LAP(3, 0);     // panel thread: its phase work (rest)
+            K6_LAP(9, 128);   // update thread: its phase work
             if (K >= 0) {
                 __syncthreads();   // panel K's multipliers and pivots are published; phase K-1's updates are done
+                K6_LAP(8, 0);      // waits at the phase barrier
+                K6_LAP(10, 128);
 #pragma unroll
                 for (int s = 0; s < B; ++s) {
                     pvk[s] = k0 + s < n ? spv[k0 + s] : k0 + s;
@@ -207,25 +253,39 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
             };
             if (wid < K6_PW) {
                 // ======== panel group: factor panel K+1 (columns k1..k1+nb-1) ========
+                // Inside a panel the rows stay with their threads (no register swaps): `mypos` is
+                // the position R-lu's physical swaps would have given the thread's row, `live`
+                // says it has not been a pivot yet; the write-back scatters the rows to their
+                // positions, so shared memory is in R-lu's physical order again at every phase.
                 if (k1 >= n) continue;
                 const int nb = min(B, n - k1);
+                const bool inb = row < n;
+                double cp0 = 0.0, cp1 = 0.0, cp2 = 0.0, cp3 = 0.0;   // this row's multipliers of panel K
                 if (K >= 0) {
+                    if (inb && row >= k1) {
+                        const double *lk = a + (size_t)k0 * ld + row;
+                        cp0 = lk[0]; cp1 = lk[ld]; cp2 = lk[2 * ld]; cp3 = lk[3 * ld];
+                    }
                     if (tid < nb) top_rows(a + (size_t)(k1 + tid) * ld);
                     panel_bar();
                 }
+                K6_LAP(4, 0);   // top rows of the panel's columns
                 double c[B];
 #pragma unroll
                 for (int s = 0; s < B; ++s) {
                     const double *cj = a + (size_t)(k1 + (s < nb ? s : 0)) * ld;
-                    double x = (s < nb && row < n) ? cj[row] : 0.0;
+                    double x = (s < nb && inb) ? cj[row] : 0.0;
                     if (K >= 0 && row >= k1) {
-                        x = fma(-cp[0], cj[k0], x);
-                        x = fma(-cp[1], cj[k0 + 1], x);
-                        x = fma(-cp[2], cj[k0 + 2], x);
-                        x = fma(-cp[3], cj[k0 + 3], x);
+                        x = fma(-cp0, cj[k0], x);
+                        x = fma(-cp1, cj[k0 + 1], x);
+                        x = fma(-cp2, cj[k0 + 2], x);
+                        x = fma(-cp3, cj[k0 + 3], x);
                     }
                     c[s] = x;
                 }
+                K6_LAP(5, 0);   // panel load + rank-4 update
+                int mypos = row;
+                bool live = inb && row >= k1;
                 int pvs[B] = {0, 0, 0, 0};
                 int fail = -1;
 #pragma unroll
@@ -233,87 +293,84 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
                     if (s < nb && fail < 0) {
                         const int kk = k1 + s;
                         PanelXchg &X = xch[s & 1];
-                        // Warp arg-max over its rows >= kk (NaN never wins; first maximum): redux.sync
-                        // on the high word of |a|, the low word only when several lanes tie on it.
-                        // Meanwhile every candidate lane forms RN(1 / own entry): the winner's is the
-                        // step's reciprocal, so no division sits behind the exchange barrier.
+                        // Warp arg-max over its live rows (NaN never wins; first maximum by position):
+                        // redux.sync on the high word of |a|; the low word and the position only when
+                        // several lanes tie.  The winner publishes |a|, rcp_nr(a), its position and row.
                         const double cs = c[s];
-                        const double v = fabs(cs);
-                        const bool cand = row >= kk && row < n && v >= 0.0;
-                        const unsigned long long vb = (unsigned long long)__double_as_longlong(v);
-                        double rown = 0.0;
-                        if (cand && v > 0x1p-400 && v < 0x1p400 && (vb & 0xfffffffffffffull) != 0xfffffffffffffull)
-                            rown = 1.0 / cs;
-                        const unsigned khi = cand ? (unsigned)(vb >> 32) + 1u : 0u;
+                        const unsigned hi = (unsigned)__double2hiint(cs) & 0x7fffffffu, lo = (unsigned)__double2loint(cs);
+                        const bool cand = live && !(hi > 0x7ff00000u || (hi == 0x7ff00000u && lo != 0u));
+                        const unsigned khi = cand ? hi + 1u : 0u;
+                        double rc = rcp_nr(cs);   // every lane, before the reduction: its latency hides this chain
+                        asm volatile("" : "+d"(rc));
                         const unsigned mhi = __reduce_max_sync(FULL, khi);
-                        const bool top = cand && khi == mhi;
+                        bool top = cand && khi == mhi;
                         unsigned ball = __ballot_sync(FULL, top);
-                        if (__popc(ball) > 1) {
-                            const unsigned klo = top ? (unsigned)vb : 0u;
+                        if (ball & (ball - 1)) {
+                            const unsigned klo = top ? lo : 0u;
                             const unsigned mlo = __reduce_max_sync(FULL, klo);
-                            ball = __ballot_sync(FULL, top && klo == mlo);
+                            top = top && klo == mlo;
+                            ball = __ballot_sync(FULL, top);
+                            if (ball & (ball - 1)) {
+                                const int mp = __reduce_min_sync(FULL, top ? mypos : INT_MAX);
+                                top = top && mypos == mp;
+                            }
                         }
-                        const int wl = ball ? __ffs(ball) - 1 : 0;
-                        if (lane == wl) {
-                            X.val[wid] = ball ? v : -1.0;
-                            X.rcp[wid] = rown;
-                            X.lane[wid] = wl;
+                        if (top) {
+                            X.vr[wid] = make_double2(fabs(cs), rc);
+                            X.pos[wid] = mypos;
                             *reinterpret_cast<double2 *>(&X.row[wid][0]) = make_double2(c[0], c[1]);
                             *reinterpret_cast<double2 *>(&X.row[wid][2]) = make_double2(c[2], c[3]);
                         }
-                        if (row == kk) {
-                            *reinterpret_cast<double2 *>(&X.rowk[0]) = make_double2(c[0], c[1]);
-                            *reinterpret_cast<double2 *>(&X.rowk[2]) = make_double2(c[2], c[3]);
-                        }
+                        if (ball == 0u && lane == 0) X.vr[wid] = make_double2(-1.0, 0.0);
+                        if (live && mypos == kk) X.akk = cs;
                         panel_bar();
-                        const double2 v01 = *reinterpret_cast<const double2 *>(&X.val[0]);
-                        const double2 v23 = *reinterpret_cast<const double2 *>(&X.val[2]);
-                        double bv = v01.x;
-                        int bw = 0;
-                        if (v01.y > bv) { bv = v01.y; bw = 1; }
-                        if (v23.x > bv) { bv = v23.x; bw = 2; }
-                        if (v23.y > bv) { bv = v23.y; bw = 3; }
+                        const double2 q0 = X.vr[0], q1 = X.vr[1], q2 = X.vr[2], q3 = X.vr[3];
+                        const int4 ps = *reinterpret_cast<const int4 *>(&X.pos[0]);
+                        double bv = q0.x;
+                        int bw = 0, bp = ps.x;
+                        if (q1.x > bv || (q1.x == bv && ps.y < bp)) { bv = q1.x; bw = 1; bp = ps.y; }
+                        if (q2.x > bv || (q2.x == bv && ps.z < bp)) { bv = q2.x; bw = 2; bp = ps.z; }
+                        if (q3.x > bv || (q3.x == bv && ps.w < bp)) { bv = q3.x; bw = 3; bp = ps.w; }
                         const bool none = !(bv >= 0.0);   // every candidate is NaN: od_lu keeps p = kk (singular)
-                        const int pv = none ? kk : 32 * bw + X.lane[bw];
-                        const double piv = X.row[bw][s];
-                        const double r = X.rcp[bw];
-                        const double akk = X.rowk[s];
+                        const int pv = none ? kk : bp;
+                        const double2 rp01 = *reinterpret_cast<const double2 *>(&X.row[bw][0]);
+                        const double2 rp23 = *reinterpret_cast<const double2 *>(&X.row[bw][2]);
+                        const double rowp[B] = {rp01.x, rp01.y, rp23.x, rp23.y};   // the pivot row in the panel's columns
+                        const double piv = rowp[s];
+                        const double akk = X.akk;
                         // od_lu starts from best = |a_kk|: a NaN there keeps p = kk and the step is singular
                         if (none || !(fabs(piv) > thr) || isnan(akk)) {
                             fail = s;
                         } else {
-                            if (pv != kk) {   // swap rows kk / pv in every column of the panel
-                                if (row == kk) {
-#pragma unroll
-                                    for (int s2 = 0; s2 < B; ++s2) c[s2] = X.row[bw][s2];
-                                } else if (row == pv) {
-#pragma unroll
-                                    for (int s2 = 0; s2 < B; ++s2) c[s2] = X.rowk[s2];
-                                }
-                            }
-                            const bool below = row > kk && row < n;
-                            if (below) {   // l = a_ik / piv: PivotDiv's arithmetic with the published reciprocal
-                                const double x = c[s], ax = fabs(x);
-                                const double q0 = x * r;
-                                double q = fma(fma(-q0, piv, x), r, q0);
-                                if (ax == 0.0) q = q0;
-                                if (!(r != 0.0 && (ax == 0.0 || (ax > 0x1p-400 && ax < 0x1p400)))) q = x / piv;
+                            // reciprocal of the winner; 0 (-> IEEE division) outside 2^-400 <= |piv| < 2^401
+                            const unsigned epv = ((unsigned)__double2hiint(piv) >> 20) & 0x7ffu;
+                            const double r = epv - 623u < 801u ? (bw == 0 ? q0.y : bw == 1 ? q1.y : bw == 2 ? q2.y : q3.y) : 0.0;
+                            // R-lu's swap of positions kk and pv: the row at kk moves to pv, the pivot row retires to kk
+                            const bool isp = live && mypos == pv;
+                            if (mypos == kk) mypos = pv;
+                            if (isp) { mypos = kk; live = false; }
+                            if (live) {   // l = a_ik / piv: PivotDiv's arithmetic with the published reciprocal
+                                const double x = c[s];
+                                const unsigned ex = ((unsigned)__double2hiint(x) >> 20) & 0x7ffu;
+                                const double qa = x * r;
+                                double q = fma(fma(-qa, piv, x), r, qa);
+                                if (x == 0.0) q = qa;
+                                if (!(r != 0.0 && (x == 0.0 || ex - 623u < 801u))) q = ieee_div_cold(x, piv);
                                 c[s] = q;
-                            }
 #pragma unroll
-                            for (int s2 = s + 1; s2 < B; ++s2) {
-                                const double u = X.row[bw][s2];   // row kk of column s2 after the swap
-                                if (below) c[s2] = fma(-c[s], u, c[s2]);
+                                for (int s2 = s + 1; s2 < B; ++s2) c[s2] = fma(-q, rowp[s2], c[s2]);
                             }
                             pvs[s] = pv;
                         }
                     }
                 }
-                // write the panel back (rows >= k1: its U and L parts) and publish the pivots
+                K6_LAP(6, 0);   // the panel's steps
+                // write the panel back: every row to its position (rows >= k1: the panel's U and L
+                // parts), and publish the pivots
+                if (inb && row >= k1) {
 #pragma unroll
-                for (int s = 0; s < B; ++s) {
-                    if (s < nb && row >= k1 && row < n) a[(size_t)(k1 + s) * ld + row] = c[s];
-                    cp[s] = c[s];
+                    for (int s = 0; s < B; ++s)
+                        if (s < nb) a[(size_t)(k1 + s) * ld + mypos] = c[s];
                 }
                 if (tid == 0) {
 #pragma unroll
@@ -330,6 +387,7 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
                 }
                 continue;
             }
+            nx_advance(K + 3, p + gridDim.x);   // phases -1, 0, 1: the next star's DoFs, row extents, L2 prefetch
             if (K < 0) continue;
             // ======== update warps ========
             const int uw = wid - K6_PW;
@@ -390,6 +448,7 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
             }
             left_swaps();
         }
+        if (tid >= 32 * K6_PW) nx_advance(4, p + gridDim.x);
         __syncthreads();
         K6_STAMP(1);
         if (bad) {
@@ -447,11 +506,13 @@ void launch_patch_lu_cm(const DevPatches &P, const int64_t *rowptr, const int *c
     ++g_launches;
 #ifdef MHDP_K6_PROF
     cudaStreamSynchronize(s);
-    unsigned long long h[4] = {0, 0, 0, 0};
+    unsigned long long h[16] = {0};
     cudaMemcpyFromSymbol(h, g_k6prof, sizeof(h));
     fprintf(stderr, "K6 prof np=%lld max_n=%d grid=%u: gather %.3e LU %.3e tail %.3e cycles (sum over CTAs)\n",
             (long long)P.np, P.max_n, g, (double)h[0], (double)h[1], (double)h[2]);
-    unsigned long long z[4] = {0, 0, 0, 0};
+    fprintf(stderr, "   panel thread: top rows %.3e load %.3e steps %.3e rest %.3e barrier wait %.3e | update thread: work %.3e "
+            "barrier wait %.3e\n", (double)h[4], (double)h[5], (double)h[6], (double)h[3], (double)h[8], (double)h[9], (double)h[10]);
+    unsigned long long z[16] = {0};
     cudaMemcpyToSymbol(g_k6prof, z, sizeof(z));
 #endif
 }
