@@ -70,7 +70,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         os.replace(tmp, LIB)
     # measurement probes (FP64 peak, dependency latencies): tools/libprobe.so
     psrc = os.path.join(ROOT, "tools", "probe.cu")
-    if os.path.exists(psrc) and (force or _stale(PROBE, [psrc])):
+    if os.path.exists(psrc) and (force or _stale(PROBE, [psrc, os.path.join(CSRC, "k2_common.cuh")])):
         tmp = PROBE + ".tmp"
         run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", psrc, "-o", tmp])
         os.replace(tmp, PROBE)

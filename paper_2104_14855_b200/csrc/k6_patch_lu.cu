@@ -260,28 +260,50 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
                 if (k1 >= n) continue;
                 const int nb = min(B, n - k1);
                 const bool inb = row < n;
-                double cp0 = 0.0, cp1 = 0.0, cp2 = 0.0, cp3 = 0.0;   // this row's multipliers of panel K
+                // Load the panel's columns with panel K applied.  Nothing is swapped in shared memory
+                // here: the thread reads the entry that R-lu's four swaps would leave at its position
+                // (src_of undoes them in registers), forms u = L11^-1 x for rows k0..k0+3 itself
+                // (every thread, redundantly) and applies the four steps to its row.  Thread s stores
+                // column s's u after the first exchange barrier; the rows below are rewritten by the
+                // panel's write-back, so shared memory is in R-lu's order again when the phase ends.
+                auto src_of = [&](int q) {
+#pragma unroll
+                    for (int s = B - 1; s >= 0; --s) {
+                        const int A = k0 + s, Bp = pvk[s];
+                        q = q == A ? Bp : (q == Bp ? A : q);
+                    }
+                    return q;
+                };
+                double c[B];
+                double us0 = 0.0, us1 = 0.0, us2 = 0.0, us3 = 0.0;   // thread s < nb: u of column k1 + s
                 if (K >= 0) {
+                    double cp0 = 0.0, cp1 = 0.0, cp2 = 0.0, cp3 = 0.0;   // this row's multipliers of panel K
                     if (inb && row >= k1) {
                         const double *lk = a + (size_t)k0 * ld + row;
                         cp0 = lk[0]; cp1 = lk[ld]; cp2 = lk[2 * ld]; cp3 = lk[3 * ld];
                     }
-                    if (tid < nb) top_rows(a + (size_t)(k1 + tid) * ld);
-                    panel_bar();
-                }
-                K6_LAP(4, 0);   // top rows of the panel's columns
-                double c[B];
+                    const int srow = src_of(row);
+                    const int g0 = src_of(k0), g1 = src_of(k0 + 1), g2 = src_of(k0 + 2), g3 = src_of(k0 + 3);
 #pragma unroll
-                for (int s = 0; s < B; ++s) {
-                    const double *cj = a + (size_t)(k1 + (s < nb ? s : 0)) * ld;
-                    double x = (s < nb && inb) ? cj[row] : 0.0;
-                    if (K >= 0 && row >= k1) {
-                        x = fma(-cp0, cj[k0], x);
-                        x = fma(-cp1, cj[k0 + 1], x);
-                        x = fma(-cp2, cj[k0 + 2], x);
-                        x = fma(-cp3, cj[k0 + 3], x);
+                    for (int s = 0; s < B; ++s) {
+                        const double *cj = a + (size_t)(k1 + (s < nb ? s : 0)) * ld;
+                        const double u0 = cj[g0];
+                        const double u1 = fma(-l10, u0, cj[g1]);
+                        const double u2 = fma(-l21, u1, fma(-l20, u0, cj[g2]));
+                        const double u3 = fma(-l32, u2, fma(-l31, u1, fma(-l30, u0, cj[g3])));
+                        double x = (s < nb && inb) ? cj[srow] : 0.0;
+                        if (row >= k1) {
+                            x = fma(-cp0, u0, x);
+                            x = fma(-cp1, u1, x);
+                            x = fma(-cp2, u2, x);
+                            x = fma(-cp3, u3, x);
+                        }
+                        c[s] = x;
+                        if (tid == s) { us0 = u0; us1 = u1; us2 = u2; us3 = u3; }
                     }
-                    c[s] = x;
+                } else {
+#pragma unroll
+                    for (int s = 0; s < B; ++s) c[s] = (s < nb && inb) ? a[(size_t)(k1 + s) * ld + row] : 0.0;
                 }
                 K6_LAP(5, 0);   // panel load + rank-4 update
                 int mypos = row;
@@ -324,6 +346,10 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
                         if (ball == 0u && lane == 0) X.vr[wid] = make_double2(-1.0, 0.0);
                         if (live && mypos == kk) X.akk = cs;
                         panel_bar();
+                        if (s == 0 && K >= 0 && tid < nb) {   // every thread has read the columns: store u
+                            double *cj = a + (size_t)(k1 + tid) * ld;
+                            cj[k0] = us0; cj[k0 + 1] = us1; cj[k0 + 2] = us2; cj[k0 + 3] = us3;
+                        }
                         const double2 q0 = X.vr[0], q1 = X.vr[1], q2 = X.vr[2], q3 = X.vr[3];
                         const int4 ps = *reinterpret_cast<const int4 *>(&X.pos[0]);
                         double bv = q0.x;
@@ -378,10 +404,7 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
                         if (s < nb && (fail < 0 || s <= fail)) {
                             const int kk = k1 + s;
                             if (s == fail) { spv[kk] = -1; }
-                            else {
-                                spv[kk] = pvs[s];
-                                if (pvs[s] != kk) { const int t = prm[kk]; prm[kk] = prm[pvs[s]]; prm[pvs[s]] = t; }
-                            }
+                            else spv[kk] = pvs[s];
                         }
                     }
                 }
@@ -391,6 +414,13 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
             if (K < 0) continue;
             // ======== update warps ========
             const int uw = wid - K6_PW;
+            if (tid == 32 * K6_PW) {   // the row permutation follows the published pivots (read after the LU)
+#pragma unroll
+                for (int s = 0; s < B; ++s) {
+                    const int kk = k0 + s, pv = pvk[s];
+                    if (kk < n && pv != kk) { const int t = prm[kk]; prm[kk] = prm[pv]; prm[pv] = t; }
+                }
+            }
             // panel K's swaps on the finished L columns to its left (16 columns per warp, lanes over
             // columns); after the trailing update: nothing in this phase waits for them
             auto left_swaps = [&]() {

@@ -262,3 +262,36 @@ def test_coarse_lu_solve_ragged_sizes(oracle_mod, n):
     x = torch.empty(n, dtype=torch.float64, device="cuda:0")
     ctx.coarse_solve(cuda_vec(b), x)
     assert np.array_equal(bits(host(x)), bits(ref))
+
+
+def test_pivot_div_is_the_ieee_quotient():
+    """PivotDiv (k2_common.cuh) forms the LU multipliers l = a_ik / a_kk of K6 / K7 from one
+    reciprocal per pivot (the instruction sequence of the inline fast path of '/').  R-lu
+    asks for the IEEE quotient: compared bit for bit with numpy's division (IEEE RN) on
+    numerators over the whole exponent range, exact and signed zeros, subnormals, operands
+    outside the guarded range (IEEE fallback), infinities and NaN, and on pivots that are
+    random, powers of two, of both signs, with an all-ones significand, tiny and huge."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import probe
+    rng = np.random.Generator(np.random.PCG64(20260421))
+    mant = rng.uniform(1.0, 2.0, 200000)
+    x = np.concatenate([
+        mant[:100000] * np.exp2(rng.integers(-30, 30, 100000)) * rng.choice([-1.0, 1.0], 100000),
+        mant[100000:] * np.exp2(rng.integers(-1000, 1000, 100000)) * rng.choice([-1.0, 1.0], 100000),
+        [0.0, -0.0, 5e-324, -5e-324, 2.2250738585072014e-308, 1.7976931348623157e308, -1.7976931348623157e308,
+         np.inf, -np.inf, np.nan, 1.0, -1.0, 3.0, 1.0 / 3.0, 2.0 ** -400, 2.0 ** 400, 2.0 ** -401, 2.0 ** 401],
+        np.nextafter(np.exp2(np.arange(-60.0, 60.0)), 0.0), np.nextafter(np.exp2(np.arange(-60.0, 60.0)), np.inf)])
+    allones = np.array([0x3FFFFFFFFFFFFFFF, 0xBFEFFFFFFFFFFFFF, 0x40AFFFFFFFFFFFFF], dtype=np.uint64).view(np.float64)
+    piv = np.concatenate([
+        rng.uniform(1.0, 2.0, 40) * np.exp2(rng.integers(-40, 40, 40)) * rng.choice([-1.0, 1.0], 40),
+        [1.0, -1.0, 2.0, 0.5, 3.0, -7.0, 1e4, -1e-4, 1.0 / 3.0, 2.0 ** -399, 2.0 ** 399, 2.0 ** -420, 2.0 ** 420,
+         5e-324, 1.7976931348623157e308],
+        allones, np.nextafter(np.exp2(np.arange(-8.0, 8.0)), 0.0)])
+    got = probe.pivot_div(x, piv)
+    with np.errstate(all="ignore"):
+        want = x[None, :] / piv[:, None]
+    nan = np.isnan(want)
+    assert np.array_equal(np.isnan(got), nan)
+    assert np.array_equal(bits(got[~nan]), bits(want[~nan]))

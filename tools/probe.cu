@@ -6,11 +6,16 @@
 //                           a warp shuffle broadcast, a shared-memory flag round trip
 //                           between two warps of one CTA and a global-memory flag round
 //                           trip between two CTAs on different SMs.
+//   mhdp_probe_pivot_div  : PivotDiv (k2_common.cuh: the multipliers of K6 / K7) applied to
+//                           caller-supplied numerators and pivots, for the test that pins it
+//                           to the IEEE quotient (tests/test_gpu_edge.py)
 // Built by paper_2104_14855_b200/build_lib.py into tools/libprobe.so; bench.py reports
 // the FP64 peak next to the K6 / K7 flop rates.
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+
+#include "../paper_2104_14855_b200/csrc/k2_common.cuh"   // PivotDiv (header-only use)
 
 namespace {
 
@@ -91,6 +96,14 @@ __global__ void k_gmem_pingpong(long long *cyc, int *flag, int n) {
 
 }  // namespace
 
+namespace {
+__global__ void __launch_bounds__(256) k_pivot_div(const double *__restrict__ x, int n, const double *__restrict__ piv,
+                                                   double *__restrict__ out) {
+    const mhdp::PivotDiv dv(piv[blockIdx.x]);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[(size_t)blockIdx.x * n + i] = dv(x[i]);
+}
+}  // namespace
+
 extern "C" {
 
 // FP64 FMA throughput in flop/s (2 per FMA); returns < 0 on a CUDA error
@@ -149,6 +162,22 @@ int mhdp_probe_latencies(int device, double *out) {
     out[4] = (double)h[4] / np;   // one round trip = two flag handoffs
     out[5] = (double)h[5] / np;
     return 0;
+}
+
+// out[j * n + i] = PivotDiv(piv[j])(x[i]) for n numerators and m pivots (host arrays)
+int mhdp_probe_pivot_div(int device, const double *x, int n, const double *piv, int m, double *out) {
+    if (cudaSetDevice(device) != cudaSuccess) return 1;
+    double *dx = nullptr, *dp = nullptr, *dout = nullptr;
+    if (cudaMalloc(&dx, sizeof(double) * n) != cudaSuccess || cudaMalloc(&dp, sizeof(double) * m) != cudaSuccess ||
+        cudaMalloc(&dout, sizeof(double) * (size_t)n * m) != cudaSuccess)
+        return 2;
+    cudaMemcpy(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice);
+    cudaMemcpy(dp, piv, sizeof(double) * m, cudaMemcpyHostToDevice);
+    k_pivot_div<<<(unsigned)m, 256>>>(dx, n, dp, dout);
+    cudaMemcpy(out, dout, sizeof(double) * (size_t)n * m, cudaMemcpyDeviceToHost);
+    const int err = cudaGetLastError() != cudaSuccess;
+    cudaFree(dx); cudaFree(dp); cudaFree(dout);
+    return err ? 3 : 0;
 }
 
 }  // extern "C"
