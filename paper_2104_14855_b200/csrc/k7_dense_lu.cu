@@ -4,7 +4,9 @@
 // l_ik = a_ik / a_kk, a_ij <- fma(-l_ik, a_kj, a_ij).  Blocked so that every element still
 // receives its updates at k = 0, 1, 2, ... in order (R-order):
 //   * panel (NB = 32 columns, all rows below k0) factored by ONE thread-block cluster of
-//     16 CTAs: each CTA holds a contiguous slice of the panel's rows in shared memory, the
+//     16 CTAs: each CTA holds a contiguous slice of the panel's rows in shared memory (row
+//     stride 33 doubles: with 32, the column walks of the pivot search and of the row-per-thread
+//     update were 32-way bank conflicts, which bounded the panel), the
 //     pivot candidates meet in CTA 0 over distributed shared memory, the pivot row is read
 //     remotely, two cluster barriers per column (round 1 factored the panel with one CTA
 //     walking the row-major matrix in global memory: 583 ms of the c5 setup);
@@ -27,6 +29,7 @@ namespace mhdp {
 namespace {
 
 constexpr int LU_NB = 32;     // panel width
+constexpr int LU_LD = LU_NB + 1;   // row stride of a panel slice in shared memory (odd: a column walk is conflict-free)
 constexpr int CL = 16;        // CTAs in the panel cluster (non-portable cluster size)
 constexpr int PT = 256;       // threads per panel CTA
 
@@ -89,7 +92,7 @@ __global__ void __launch_bounds__(PT) k_lu_panel_cl(double *__restrict__ a, int 
     if (!dead)
         for (int e = tid; e < nr * LU_NB; e += PT) {
             const int lr = e / LU_NB, c = e % LU_NB;
-            sp[e] = c < kb ? a[(int64_t)(row0 + lr) * n + k0 + c] : 0.0;
+            sp[lr * LU_LD + c] = c < kb ? a[(int64_t)(row0 + lr) * n + k0 + c] : 0.0;
         }
     const double thr = 1e-14 * __longlong_as_double((long long)amaxbits[0]);
     cluster.sync();
@@ -103,7 +106,7 @@ __global__ void __launch_bounds__(PT) k_lu_panel_cl(double *__restrict__ a, int 
         for (int lr = tid; lr < nr; lr += PT) {
             const int i = row0 + lr;
             if (i < gj) continue;
-            const double v = fabs(sp[lr * LU_NB + j]);
+            const double v = fabs(sp[lr * LU_LD + j]);
             if (v == v && better(v, i, bv, bi)) { bv = v; bi = i; }
         }
         for (int o = 16; o; o >>= 1) {
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(PT) k_lu_panel_cl(double *__restrict__ a, int 
             cv[rank] = bv;
             ci[rank] = bi;
             // the oracle keeps row k when a_kk is NaN (no |a_ik| compares greater)
-            cn[rank] = (gj >= row0 && gj < row0 + nr) ? (sp[(gj - row0) * LU_NB + j] != sp[(gj - row0) * LU_NB + j]) : 0;
+            cn[rank] = (gj >= row0 && gj < row0 + nr) ? (sp[(gj - row0) * LU_LD + j] != sp[(gj - row0) * LU_LD + j]) : 0;
         }
         cluster.sync();                                    // #1: candidates in CTA 0
         if (tid == 0) {
@@ -141,17 +144,17 @@ __global__ void __launch_bounds__(PT) k_lu_panel_cl(double *__restrict__ a, int 
         const int p = s_p;
         // ---- every CTA reads the new pivot row (old row p); owner(p) also reads old row gj ----
         if (tid < LU_NB) {
-            const double *src = cluster.map_shared_rank(sp, owner(p)) + (int64_t)(p - (k0 + owner(p) * R)) * LU_NB;
+            const double *src = cluster.map_shared_rank(sp, owner(p)) + (int64_t)(p - (k0 + owner(p) * R)) * LU_LD;
             prow[tid] = src[tid];
             if (p != gj && owner(p) == rank) {
-                const double *sg = cluster.map_shared_rank(sp, owner(gj)) + (int64_t)(gj - (k0 + owner(gj) * R)) * LU_NB;
+                const double *sg = cluster.map_shared_rank(sp, owner(gj)) + (int64_t)(gj - (k0 + owner(gj) * R)) * LU_LD;
                 sbuf[tid] = sg[tid];
             }
         }
         cluster.sync();                                    // #2: all remote reads done
         if (tid < LU_NB) {
-            if (owner(gj) == rank) sp[(gj - row0) * LU_NB + tid] = prow[tid];
-            if (p != gj && owner(p) == rank) sp[(p - row0) * LU_NB + tid] = sbuf[tid];
+            if (owner(gj) == rank) sp[(gj - row0) * LU_LD + tid] = prow[tid];
+            if (p != gj && owner(p) == rank) sp[(p - row0) * LU_LD + tid] = sbuf[tid];
         }
         const double piv = prow[j];
         if (rank == 0 && tid == 0) {
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(PT) k_lu_panel_cl(double *__restrict__ a, int 
         for (int lr = tid; lr < nr; lr += PT) {
             const int i = row0 + lr;
             if (i <= gj) continue;
-            double *ri = sp + lr * LU_NB;
+            double *ri = sp + lr * LU_LD;
             const double l = dv(ri[j]);
             ri[j] = l;
             for (int c = j + 1; c < kb; ++c) ri[c] = fma(-l, prow[c], ri[c]);
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(PT) k_lu_panel_cl(double *__restrict__ a, int 
     cluster.sync();
     for (int e = tid; e < nr * LU_NB; e += PT) {
         const int lr = e / LU_NB, c = e % LU_NB;
-        if (c < kb) a[(int64_t)(row0 + lr) * n + k0 + c] = sp[e];
+        if (c < kb) a[(int64_t)(row0 + lr) * n + k0 + c] = sp[lr * LU_LD + c];
     }
 }
 
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(256) k_lu_gemm(double *__restrict__ a, int n, 
 
 int k7_max_n() {
     // shared memory of a panel CTA: ceil(n / CL) rows x NB doubles within 227 KB
-    return (227 * 1024 / (8 * LU_NB) - 4) * CL;
+    return (227 * 1024 / (8 * LU_LD) - 4) * CL;
 }
 
 // scratch: >= 8 + 32 ints / 2 u64 of device memory (amax bits, swap list)
@@ -270,7 +273,7 @@ void launch_dense_lu(double *a, int n, int *perm, int *status, double *scratch, 
     k_absmax_grid<<<sm_count() * 4, PT, 0, s>>>(a, (int64_t)n * n, amax);
     g_launches += 2;
     const int Rmax = (n + CL - 1) / CL;
-    const size_t smem = sizeof(double) * (size_t)Rmax * LU_NB;
+    const size_t smem = sizeof(double) * (size_t)Rmax * LU_LD;
     static unsigned long long init = 0;
     if (first_use_on_device(init)) cudaFuncSetAttribute(k_lu_panel_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(k_lu_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -279,7 +282,7 @@ void launch_dense_lu(double *a, int n, int *perm, int *status, double *scratch, 
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(CL);
         cfg.blockDim = dim3(PT);
-        cfg.dynamicSmemBytes = sizeof(double) * (size_t)((n - k0 + CL - 1) / CL) * LU_NB;
+        cfg.dynamicSmemBytes = sizeof(double) * (size_t)((n - k0 + CL - 1) / CL) * LU_LD;
         cfg.stream = s;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
