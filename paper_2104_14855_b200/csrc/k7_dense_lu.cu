@@ -210,13 +210,13 @@ __global__ void k_lu_trsm(double *__restrict__ a, int n, int k0, int kb, const i
     }
 }
 
-// trailing update: 64x64 output tile per 256-thread CTA, 4x4 per thread
-__global__ void __launch_bounds__(256) k_lu_gemm(double *__restrict__ a, int n, int k0, int kb,
+// trailing update of the columns [cbeg, cend): 64x64 output tile per 256-thread CTA, 4x4 per thread
+__global__ void __launch_bounds__(256) k_lu_gemm(double *__restrict__ a, int n, int k0, int kb, int cbeg, int cend,
                                                  const int *__restrict__ status) {
     __shared__ double Ls[64][LU_NB + 1];
     __shared__ double Us[LU_NB][64 + 1];
     if (*status) return;
-    const int r0 = k0 + kb + blockIdx.y * 64, c0 = k0 + kb + blockIdx.x * 64;
+    const int r0 = k0 + kb + blockIdx.y * 64, c0 = cbeg + blockIdx.x * 64;
     const int tid = threadIdx.x;
     for (int e = tid; e < 64 * LU_NB; e += 256) {
         const int rr = e / LU_NB, kk = e % LU_NB;
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(256) k_lu_gemm(double *__restrict__ a, int n, 
     for (int e = tid; e < 64 * LU_NB; e += 256) {
         const int kk = e / 64, cc = e % 64;
         const int gc = c0 + cc;
-        Us[kk][cc] = (gc < n && kk < kb) ? a[(int64_t)(k0 + kk) * n + gc] : 0.0;
+        Us[kk][cc] = (gc < cend && kk < kb) ? a[(int64_t)(k0 + kk) * n + gc] : 0.0;
     }
     __syncthreads();
     const int ty = tid / 16, tx = tid % 16;
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(256) k_lu_gemm(double *__restrict__ a, int n, 
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const int gr = r0 + ty + 16 * u, gc = c0 + tx + 16 * v;
-            acc[u][v] = (gr < n && gc < n) ? a[(int64_t)gr * n + gc] : 0.0;
+            acc[u][v] = (gr < n && gc < cend) ? a[(int64_t)gr * n + gc] : 0.0;
         }
     for (int kk = 0; kk < kb; ++kk) {
 #pragma unroll
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(256) k_lu_gemm(double *__restrict__ a, int n, 
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const int gr = r0 + ty + 16 * u, gc = c0 + tx + 16 * v;
-            if (gr < n && gc < n) a[(int64_t)gr * n + gc] = acc[u][v];
+            if (gr < n && gc < cend) a[(int64_t)gr * n + gc] = acc[u][v];
         }
 }
 
@@ -263,7 +263,7 @@ int k7_max_n() {
     return (227 * 1024 / (8 * LU_LD) - 4) * CL;
 }
 
-// scratch: >= 8 + 32 ints / 2 u64 of device memory (amax bits, swap list)
+// scratch: >= 2 doubles (amax bits) + 2 * 32 ints (two swap lists) of device memory
 void launch_dense_lu(double *a, int n, int *perm, int *status, double *scratch, cudaStream_t s) {
     if (n == 0) return;
     unsigned long long *amax = reinterpret_cast<unsigned long long *>(scratch);
@@ -277,13 +277,24 @@ void launch_dense_lu(double *a, int n, int *perm, int *status, double *scratch, 
     static unsigned long long init = 0;
     if (first_use_on_device(init)) cudaFuncSetAttribute(k_lu_panel_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(k_lu_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    for (int k0 = 0; k0 < n; k0 += LU_NB) {
+    // Look-ahead: the trailing update of panel k is split at the next panel's columns.  Once
+    // those 32 columns are updated, panel k+1 is factored on a second (high-priority) stream by
+    // its 16-CTA cluster while the other SMs update the remaining columns; the two touch
+    // disjoint columns, and the swaps / substitution / update of panel k+1 follow after both.
+    cudaStream_t sa = nullptr;
+    cudaEvent_t e1 = nullptr, e2 = nullptr;
+    int plo = 0, phi = 0;
+    cudaDeviceGetStreamPriorityRange(&plo, &phi);
+    const bool la = cudaStreamCreateWithPriority(&sa, cudaStreamNonBlocking, phi) == cudaSuccess &&
+                    cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) == cudaSuccess &&
+                    cudaEventCreateWithFlags(&e2, cudaEventDisableTiming) == cudaSuccess;
+    auto panel = [&](int k0, cudaStream_t st) {
         const int kb = n - k0 < LU_NB ? n - k0 : LU_NB;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(CL);
         cfg.blockDim = dim3(PT);
         cfg.dynamicSmemBytes = sizeof(double) * (size_t)((n - k0 + CL - 1) / CL) * LU_LD;
-        cfg.stream = s;
+        cfg.stream = st;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = CL;
@@ -292,17 +303,38 @@ void launch_dense_lu(double *a, int n, int *perm, int *status, double *scratch, 
         cfg.attrs = at;
         cfg.numAttrs = 1;
         cudaLaunchKernelEx(&cfg, k_lu_panel_cl, a, n, k0, kb, perm, status,
-                           (const unsigned long long *)amax, swaps);
-        k_lu_laswp<<<grid_for(n, 256), 256, 0, s>>>(a, n, k0, kb, swaps, status);
+                           (const unsigned long long *)amax, swaps + (k0 / LU_NB & 1) * LU_NB);
+        ++g_launches;
+    };
+    panel(0, s);
+    for (int k0 = 0; k0 < n; k0 += LU_NB) {
+        const int kb = n - k0 < LU_NB ? n - k0 : LU_NB;
+        const int *sw = swaps + (k0 / LU_NB & 1) * LU_NB;   // two swap lists: panel k+1 writes its own while k's is read
+        k_lu_laswp<<<grid_for(n, 256), 256, 0, s>>>(a, n, k0, kb, sw, status);
+        ++g_launches;
+        const int k1 = k0 + kb, rest = n - k1;
+        if (rest <= 0) break;
+        k_lu_trsm<<<grid_for(rest, 128), 128, 0, s>>>(a, n, k0, kb, status);
+        const int cmid = k1 + LU_NB < n ? k1 + LU_NB : n;   // end of the next panel's columns
+        k_lu_gemm<<<dim3(1, grid_for(rest, 64)), 256, 0, s>>>(a, n, k0, kb, k1, cmid, status);
         g_launches += 2;
-        const int rest = n - k0 - kb;
-        if (rest > 0) {
-            k_lu_trsm<<<grid_for(rest, 128), 128, 0, s>>>(a, n, k0, kb, status);
-            dim3 g(grid_for(rest, 64), grid_for(rest, 64));
-            k_lu_gemm<<<g, 256, 0, s>>>(a, n, k0, kb, status);
-            g_launches += 2;
+        if (la) {
+            cudaEventRecord(e1, s);
+            cudaStreamWaitEvent(sa, e1, 0);
+            panel(k1, sa);
+            cudaEventRecord(e2, sa);
         }
+        if (cmid < n) {
+            k_lu_gemm<<<dim3(grid_for(n - cmid, 64), grid_for(rest, 64)), 256, 0, s>>>(a, n, k0, kb, cmid, n, status);
+            ++g_launches;
+        }
+        if (la) cudaStreamWaitEvent(s, e2, 0);
+        else panel(k1, s);
     }
+    if (la) cudaStreamSynchronize(sa);   // setup path: the helper stream is drained before it is destroyed
+    if (sa) cudaStreamDestroy(sa);
+    if (e1) cudaEventDestroy(e1);
+    if (e2) cudaEventDestroy(e2);
 }
 
 }  // namespace mhdp
