@@ -213,3 +213,42 @@ def test_coarse_solve_large_bitexact(oracle_mod):
     xa = cuda_vec(bc)
     ctx.coarse_solve(xa, xa)
     assert np.array_equal(bits(host(xa)), bits(ref))
+
+
+def test_patch_lu_every_size_33_to_128(oracle_mod):
+    """k_patch_lu_cm (k6_patch_lu.cu: panels of 4, four-warp panel group) on one patch of EVERY
+    size 33..128 -- every ragged last panel (n mod 4), every count of 32-row chunks, last chunks
+    of 1..32 rows -- next to the c5 vertex stars: random sorted subsets of unions of neighbouring
+    stars, installed on both sides.  Principal submatrices of the (coercive) velocity operator
+    are nonsingular; on the uniform mesh they are full of exact zeros and exactly tied pivot
+    candidates.  Factors and pivots bit for bit against the oracle's od_lu, then one sweep."""
+    import torch
+    from paper_2104_14855_b200 import mhdp, workloads
+    cfg = workloads.small("c5", 6, 2)
+    w, _, _ = workloads.draw(cfg, 1, 4)
+    orc = oracle_mod.Oracle(cfg, w)
+    ptr0, dofs0 = orc.patches(1)[:2]
+    uptr, udofs = _union_patches(orc, cfg.N, 1, (2, 1, 1))
+    big = [udofs[uptr[i]:uptr[i + 1]] for i in range(len(uptr) - 1) if uptr[i + 1] - uptr[i] >= 128]
+    assert big
+    rng = np.random.default_rng(5)
+    extra = [np.sort(rng.choice(big[m % len(big)], size=m, replace=False)).astype(np.int32) for m in range(33, 129)]
+    stars = [dofs0[ptr0[i]:ptr0[i + 1]] for i in range(len(ptr0) - 1)]
+    allp = stars + extra
+    ptr = np.concatenate([[0], np.cumsum([len(p) for p in allp])]).astype(np.int64)
+    dofs = np.concatenate(allp).astype(np.int32)
+    assert np.diff(ptr).max() == 128
+    orc.set_patches(ptr, dofs, 1)
+    ctx = mhdp.Context(0, torch.cuda.current_stream().cuda_stream)
+    load_oracle_levels(ctx, orc, cfg)
+    for i in range(len(stars), len(allp)):
+        lu_o, perm_o, st = orc.patch_lu(i)
+        assert st == 0
+        lu_g, perm_g = ctx.patch_lu(i)
+        assert np.array_equal(perm_o, perm_g), f"size {len(allp[i])}: pivot order differs"
+        assert np.array_equal(bits(lu_o), bits(lu_g)), f"size {len(allp[i])}: factors differ"
+    n = orc.n()
+    b, x0 = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    xg = cuda_vec(x0)
+    ctx.smooth(cuda_vec(b), xg, nsweeps=1)
+    assert np.array_equal(bits(host(xg)), bits(orc.sweep(b, x0, nsweeps=1)))
