@@ -74,11 +74,15 @@ constexpr int K6_UW = 8;           // update warps
 constexpr int K6_THREADS = 32 * (K6_PW + K6_UW);
 constexpr int K6_HASH = 1024;      // hash slots (load <= 1/8)
 
-// exchange area of the panel group, one per step parity (16-byte aligned fields)
+// exchange area of the panel group, one per step parity: a 64-byte record per panel warp
+struct PanelCand {
+    double2 vr;                      // max |a| over the warp's live rows (-1: none), rcp_nr of that entry
+    double2 r01, r23;                // that row's entries in the panel's columns
+    int pos, pad0;                   // its position
+    double pad1;
+};
 struct PanelXchg {
-    double2 vr[K6_PW];               // per panel warp: max |a| over its live rows (-1: none), rcp_nr of that entry
-    double row[K6_PW][K6_B];         // that row's entries in the panel's columns
-    int pos[K6_PW];                  // its position
+    PanelCand c[K6_PW];
     double akk, pad;                 // the entry at position kk
 };
 
@@ -338,39 +342,42 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
                             }
                         }
                         if (top) {
-                            X.vr[wid] = make_double2(fabs(cs), rc);
-                            X.pos[wid] = mypos;
-                            *reinterpret_cast<double2 *>(&X.row[wid][0]) = make_double2(c[0], c[1]);
-                            *reinterpret_cast<double2 *>(&X.row[wid][2]) = make_double2(c[2], c[3]);
+                            PanelCand &W = X.c[wid];
+                            W.vr = make_double2(fabs(cs), rc);
+                            W.r01 = make_double2(c[0], c[1]);
+                            W.r23 = make_double2(c[2], c[3]);
+                            W.pos = mypos;
                         }
-                        if (ball == 0u && lane == 0) X.vr[wid] = make_double2(-1.0, 0.0);
+                        if (ball == 0u && lane == 0) X.c[wid].vr = make_double2(-1.0, 0.0);
                         if (live && mypos == kk) X.akk = cs;
                         panel_bar();
                         if (s == 0 && K >= 0 && tid < nb) {   // every thread has read the columns: store u
                             double *cj = a + (size_t)(k1 + tid) * ld;
                             cj[k0] = us0; cj[k0 + 1] = us1; cj[k0 + 2] = us2; cj[k0 + 3] = us3;
                         }
-                        const double2 q0 = X.vr[0], q1 = X.vr[1], q2 = X.vr[2], q3 = X.vr[3];
-                        const int4 ps = *reinterpret_cast<const int4 *>(&X.pos[0]);
-                        double bv = q0.x;
-                        int bw = 0, bp = ps.x;
-                        if (q1.x > bv || (q1.x == bv && ps.y < bp)) { bv = q1.x; bw = 1; bp = ps.y; }
-                        if (q2.x > bv || (q2.x == bv && ps.z < bp)) { bv = q2.x; bw = 2; bp = ps.z; }
-                        if (q3.x > bv || (q3.x == bv && ps.w < bp)) { bv = q3.x; bw = 3; bp = ps.w; }
+                        // best of the four candidates: largest |a|, lowest position among equals (branch-free)
+                        const double v0 = X.c[0].vr.x, v1 = X.c[1].vr.x, v2 = X.c[2].vr.x, v3 = X.c[3].vr.x;
+                        const int p0 = X.c[0].pos, p1 = X.c[1].pos, p2 = X.c[2].pos, p3 = X.c[3].pos;
+                        const double akk = X.akk;
+                        const double m01 = v1 > v0 ? v1 : v0, m23 = v3 > v2 ? v3 : v2;
+                        const double bv = m23 > m01 ? m23 : m01;
+                        const int e0 = v0 == bv ? p0 : INT_MAX, e1 = v1 == bv ? p1 : INT_MAX;
+                        const int e2 = v2 == bv ? p2 : INT_MAX, e3 = v3 == bv ? p3 : INT_MAX;
+                        const int bp = min(min(e0, e1), min(e2, e3));
+                        const int bw = e0 == bp ? 0 : (e1 == bp ? 1 : (e2 == bp ? 2 : 3));
                         const bool none = !(bv >= 0.0);   // every candidate is NaN: od_lu keeps p = kk (singular)
                         const int pv = none ? kk : bp;
-                        const double2 rp01 = *reinterpret_cast<const double2 *>(&X.row[bw][0]);
-                        const double2 rp23 = *reinterpret_cast<const double2 *>(&X.row[bw][2]);
+                        const PanelCand &W = X.c[bw];
+                        const double2 wvr = W.vr, rp01 = W.r01, rp23 = W.r23;
                         const double rowp[B] = {rp01.x, rp01.y, rp23.x, rp23.y};   // the pivot row in the panel's columns
                         const double piv = rowp[s];
-                        const double akk = X.akk;
                         // od_lu starts from best = |a_kk|: a NaN there keeps p = kk and the step is singular
-                        if (none || !(fabs(piv) > thr) || isnan(akk)) {
+                        if (none | !(fabs(piv) > thr) | isnan(akk)) {
                             fail = s;
                         } else {
                             // reciprocal of the winner; 0 (-> IEEE division) outside 2^-400 <= |piv| < 2^401
                             const unsigned epv = ((unsigned)__double2hiint(piv) >> 20) & 0x7ffu;
-                            const double r = epv - 623u < 801u ? (bw == 0 ? q0.y : bw == 1 ? q1.y : bw == 2 ? q2.y : q3.y) : 0.0;
+                            const double r = epv - 623u < 801u ? wvr.y : 0.0;
                             // R-lu's swap of positions kk and pv: the row at kk moves to pv, the pivot row retires to kk
                             const bool isp = live && mypos == pv;
                             if (mypos == kk) mypos = pv;
@@ -414,7 +421,7 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
             if (K < 0) continue;
             // ======== update warps ========
             const int uw = wid - K6_PW;
-            if (tid == 32 * K6_PW) {   // the row permutation follows the published pivots (read after the LU)
+            if (tid == K6_THREADS - 32) {   // the row permutation follows the published pivots (read after the LU)
 #pragma unroll
                 for (int s = 0; s < B; ++s) {
                     const int kk = k0 + s, pv = pvk[s];
@@ -438,8 +445,10 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
             // trailing columns beyond the next panel: a contiguous range per warp
             const int ncol = n - (k1 + B), per = (ncol + K6_UW - 1) / K6_UW;
             const int j0 = k1 + B + uw * per, j1 = min(n, j0 + per);
+            K6_LAP(11, 128);   // update thread: phase head (prefetch step, ranges)
             if (j0 + lane < j1) top_rows(a + (size_t)(j0 + lane) * ld);
             __syncwarp();
+            K6_LAP(12, 128);   // top rows of its columns
             const double *ck = a + (size_t)k0 * ld;
             auto cols = [&](auto t0c) {
                 constexpr int T0 = decltype(t0c)::value;   // chunks < T0 hold only rows < k1
@@ -476,7 +485,9 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
                 case 2: cols(std::integral_constant<int, NCH >= 3 ? 2 : 0>{}); break;
                 default: cols(std::integral_constant<int, NCH >= 4 ? 3 : 0>{}); break;
             }
+            K6_LAP(13, 128);   // trailing columns
             left_swaps();
+            K6_LAP(14, 128);   // left swaps
         }
         if (tid >= 32 * K6_PW) nx_advance(4, p + gridDim.x);
         __syncthreads();
@@ -541,7 +552,8 @@ void launch_patch_lu_cm(const DevPatches &P, const int64_t *rowptr, const int *c
     fprintf(stderr, "K6 prof np=%lld max_n=%d grid=%u: gather %.3e LU %.3e tail %.3e cycles (sum over CTAs)\n",
             (long long)P.np, P.max_n, g, (double)h[0], (double)h[1], (double)h[2]);
     fprintf(stderr, "   panel thread: top rows %.3e load %.3e steps %.3e rest %.3e barrier wait %.3e | update thread: work %.3e "
-            "barrier wait %.3e\n", (double)h[4], (double)h[5], (double)h[6], (double)h[3], (double)h[8], (double)h[9], (double)h[10]);
+            "barrier wait %.3e (head %.3e top rows %.3e columns %.3e left swaps %.3e)\n", (double)h[4], (double)h[5], (double)h[6],
+            (double)h[3], (double)h[8], (double)h[9], (double)h[10], (double)h[11], (double)h[12], (double)h[13], (double)h[14]);
     unsigned long long z[16] = {0};
     cudaMemcpyToSymbol(g_k6prof, z, sizeof(z));
 #endif
