@@ -116,7 +116,7 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
     int nx_stage = 0, nx_n = 0, nx_d = 0, nx_len = 0;
     auto nx_advance = [&](int want, int64_t pt) {
         const int e = tid - 32 * K6_PW;
-        while (nx_stage < want) {
+        while (nx_stage < want && nx_stage < 4) {
             if (nx_stage == 0) {
                 nx_n = pt < np ? pn[pt] : 0;
             } else if (nx_stage == 1) {
@@ -417,7 +417,7 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
                 }
                 continue;
             }
-            nx_advance(K + 3, p + gridDim.x);   // phases -1, 0, 1: the next star's DoFs, row extents, L2 prefetch
+            if (K <= 1) nx_advance(K + 3, p + gridDim.x);   // phases -1, 0, 1: the next star's DoFs, row extents, L2 prefetch
             if (K < 0) continue;
             // ======== update warps ========
             const int uw = wid - K6_PW;
