@@ -9,7 +9,7 @@ timeout 1500 python -m pytest tests -m gpu -q --durations=20 > gpurun_out/final_
 timeout 900 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err
 timeout 600 python bench.py --steps 2 --warmup 3 --no-solves --no-variants --no-cpu-baseline \
     > gpurun_out/final_bench_plain.json 2> gpurun_out/final_bench_plain.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
     --log-file gpurun_out/final_launches.csv python bench.py --steps 2 --warmup 3 --no-solves \
     --no-variants --no-cpu-baseline > gpurun_out/final_launches_run.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_patch_apply_tma -c 1 \
