@@ -268,7 +268,12 @@ bool has_block3(const HostLevel &H) {
     return ok;
 }
 
-mhdp_status build_b3(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
+// The 3x3-block SELL store is filled on the device from the level's CSR (drp / dci / dv, the
+// temporary copy K6 factors from): only the slice pointers and row lengths are formed on the
+// host.  (Round 1 filled 2.4 GB of values on the host and uploaded them from pageable memory:
+// 1.4 s of the c5 device setup.)
+mhdp_status build_b3(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L, const int64_t *drp, const int *dci,
+                     const double *dv) {
     const int64_t nb = H.n / 3, ns = (nb + 31) / 32;
     std::vector<int64_t> sptr(ns + 1, 0);
     std::vector<int> rlen(nb);
@@ -283,29 +288,16 @@ mhdp_status build_b3(mhdp_ctx *ctx, const HostLevel &H, DevLevel &L) {
     const int64_t stored = sptr[ns];
     // value layout: the 9 x 32 values of one (slice, block column) contiguous (one DRAM run
     // per warp iteration; 9 separate planes measured 3% slower, profiles/r01_c5_k1_layout_ab.jsonl)
-    const int planes = 0;
-    std::vector<int> col(stored, 0);
-    std::vector<double> val(9 * stored, 0.0);
-#pragma omp parallel for schedule(static)
-    for (int64_t R = 0; R < nb; ++R) {
-        const int64_t s0 = sptr[R >> 5], base = s0 + (R & 31);
-        for (int k = 0; k < rlen[R]; ++k) {
-            const int64_t e = base + 32 * (int64_t)k;
-            col[e] = H.ci[H.rp[3 * R] + 3 * k] / 3;
-            for (int a = 0; a < 3; ++a)
-                for (int b = 0; b < 3; ++b) {
-                    const int m = 3 * a + b;
-                    const int64_t at = planes ? m * stored + e : 9 * s0 + (9 * (int64_t)k + m) * 32 + (R & 31);
-                    val[at] = H.v[H.rp[3 * R + a] + 3 * k + b];
-                }
-        }
-    }
     mhdp_status st;
-    L.A3.nb = nb; L.A3.nslices = ns; L.A3.stored = stored; L.A3.planes = planes;
+    L.A3.nb = nb; L.A3.nslices = ns; L.A3.stored = stored; L.A3.planes = 0;
     if ((st = upload(ctx, &L.A3.sptr, sptr.data(), ns + 1))) return st;
     if ((st = upload(ctx, &L.A3.rlen, rlen.data(), nb))) return st;
-    if ((st = upload(ctx, &L.A3.col, col.data(), stored))) return st;
-    if ((st = upload(ctx, &L.A3.val, val.data(), 9 * stored))) return st;
+    if ((st = dalloc(ctx, &L.A3.col, stored))) return st;
+    if ((st = dalloc(ctx, &L.A3.val, 9 * stored))) return st;
+    CK(cudaMemsetAsync(L.A3.col, 0, sizeof(int) * (size_t)std::max<int64_t>(1, stored), ctx->stream));
+    CK(cudaMemsetAsync(L.A3.val, 0, sizeof(double) * (size_t)std::max<int64_t>(1, 9 * stored), ctx->stream));
+    launch_build_b3(L.A3, drp, dci, dv, ctx->stream);
+    if ((st = check_launch(ctx))) return st;
     L.bytes_op = 8 * (ns + 1) + 4 * nb + 76 * stored;
     return MHDP_OK;
 }
@@ -751,7 +743,7 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
     CK(cudaSetDevice(ctx->device));
     const auto wall0 = std::chrono::steady_clock::now();
     ctx->t_k6.assign(ctx->nlev, 0.0);
-    ctx->t_stage.assign(6, 0.0);   // operator stores, patch stores, transfers, K6 (+ CSR upload), lane groups, coarse
+    ctx->t_stage.assign(6, 0.0);   // operator stores (+ CSR upload), patch stores, transfers, K6, lane groups, coarse
     auto tick = [last = std::chrono::steady_clock::now()](double &acc) mutable {
         const auto now = std::chrono::steady_clock::now();
         acc += std::chrono::duration<double>(now - last).count();
@@ -767,7 +759,19 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         L.n = H.n;
         L.nnz = H.rp[H.n];
         L.use_b3 = l > 0 && has_block3(H);
-        if ((st = L.use_b3 ? build_b3(ctx, H, L) : build_sell(ctx, H, L))) return st;
+        // temporary device CSR of the level: the block store is filled from it and K6 factors from it
+        TmpDev<int64_t> buf_rp;
+        TmpDev<int> buf_ci;
+        TmpDev<double> buf_v;
+        if (l > 0) {
+            CK(cudaMalloc(&buf_rp.p, sizeof(int64_t) * (H.n + 1)));
+            CK(cudaMalloc(&buf_ci.p, sizeof(int) * std::max<int64_t>(1, L.nnz)));
+            CK(cudaMalloc(&buf_v.p, sizeof(double) * std::max<int64_t>(1, L.nnz)));
+            CK(h2d(ctx, buf_rp.p, H.rp.data(), sizeof(int64_t) * (H.n + 1)));
+            CK(h2d(ctx, buf_ci.p, H.ci.data(), sizeof(int) * L.nnz));
+            CK(h2d(ctx, buf_v.p, H.v.data(), sizeof(double) * L.nnz));
+        }
+        if ((st = L.use_b3 ? build_b3(ctx, H, L, buf_rp.p, buf_ci.p, buf_v.p) : build_sell(ctx, H, L))) return st;
         tick(ctx->t_stage[0]);
         if ((st = dalloc(ctx, &L.b, H.n))) return st;
         if ((st = dalloc(ctx, &L.x, H.n))) return st;
@@ -783,19 +787,10 @@ mhdp_status mhdp_setup(mhdp_ctx *ctx) {
         if ((st = build_csr(ctx, H.n_coarser, trp, tci, tv, L.PrT))) return st;
         L.bytes_tr = 2 * (12 * (int64_t)H.prp[H.n]) + 4 * (H.n + H.n_coarser + 2);
         tick(ctx->t_stage[2]);
-        // K6: batched patch LU from a temporary device CSR
-        TmpDev<int64_t> buf_rp;
-        TmpDev<int> buf_ci;
-        TmpDev<double> buf_v;
-        CK(cudaMalloc(&buf_rp.p, sizeof(int64_t) * (H.n + 1)));
-        CK(cudaMalloc(&buf_ci.p, sizeof(int) * std::max<int64_t>(1, L.nnz)));
-        CK(cudaMalloc(&buf_v.p, sizeof(double) * std::max<int64_t>(1, L.nnz)));
+        // K6: batched patch LU from the temporary device CSR
         int64_t *drp = buf_rp.p;
         int *dci = buf_ci.p;
         double *dv = buf_v.p;
-        CK(h2d(ctx, drp, H.rp.data(), sizeof(int64_t) * (H.n + 1)));
-        CK(h2d(ctx, dci, H.ci.data(), sizeof(int) * L.nnz));
-        CK(h2d(ctx, dv, H.v.data(), sizeof(double) * L.nnz));
         int big = INT_MAX;
         CK(h2d(ctx, ctx->d_status, &big, sizeof(int)));
         TmpDev<double> buf_lu;            // K6 scratch for stars beyond shared memory

@@ -88,6 +88,8 @@ extern long long g_launches;
 // K1: r = b - A x (or y = A x when b == nullptr)
 void launch_residual(const DevSell &A, const double *b, const double *x, double *r, cudaStream_t s);
 void launch_residual_b3(const DevBSell3 &A, const double *b, const double *x, double *r, cudaStream_t s);
+// fill the 3x3-block SELL store (col, val: zero-initialised) from the level's device CSR (setup)
+void launch_build_b3(const DevBSell3 &A, const int64_t *rp, const int *ci, const double *v, cudaStream_t s);
 // K6: batched patch LU (gather from the CSR on the device, partial pivoting)
 // rowptr (int64) / col / val: the level operator in CSR; status[0] = first singular patch+1
 int64_t patch_lu_scratch_doubles(const DevPatches &P);
