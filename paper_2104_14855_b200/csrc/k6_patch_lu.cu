@@ -14,13 +14,17 @@
 //     run over rows;
 //   * warps 0..3 are the PANEL GROUP: warp w owns rows 32w..32w+31, one row per lane, so the
 //     four columns of a panel are four registers per thread.  Per step: warp arg-max by
-//     redux.sync on the high word of |a| and a ballot (the low word only on ties; first
-//     maximum), while every candidate lane forms the reciprocal of its own entry; the four
-//     candidates (value, reciprocal, row) and row kk meet in a double-buffered exchange area
-//     (ONE named barrier per step), the multipliers follow by PivotDiv's Markstein correction
-//     (k2_common.cuh) from the winner's reciprocal, and the panel's remaining columns are
-//     updated in registers.  While the other warps apply panel K, the group already factors
-//     panel K+1;
+//     redux.sync on the high word of |a| and a ballot (the low word and the position only on
+//     ties; first maximum), while every lane forms rcp_nr of its own entry; the four
+//     candidates (|a|, reciprocal, position, row: a 64-byte record each) and the entry at
+//     position kk meet in a double-buffered exchange area (ONE named barrier per step), the
+//     best of the four is picked branch-free, the multipliers follow by PivotDiv's correction
+//     step (k2_common.cuh) from the winner's reciprocal, and the panel's remaining columns are
+//     updated in registers.  Rows are not moved inside a panel: each thread tracks the position
+//     R-lu's swaps would give its row and the write-back scatters rows to positions.  While
+//     the other warps apply panel K, the group loads panel K+1's columns with panel K applied
+//     (reading through the traced-back swap permutation; the 4 x 4 triangular solve redundantly
+//     per thread: no barrier) and factors it;
 //   * warps 4..11 apply a finished panel to the trailing columns (a contiguous range of
 //     columns per warp): the B row swaps and the 4 x 4 triangular solve for u_{k0..k0+3, j} run
 //     with lanes over the warp's columns (stride ld: conflict-free), then element (i, j) takes
@@ -30,7 +34,10 @@
 //     swaps whole rows), lanes over columns, so the packed store at the end is a plain copy;
 //   * ONE CTA barrier per panel.
 // The CSR rows are gathered through a 1024-slot hash DoF -> patch row (loads of five rows in
-// flight per warp).  Packed factor layout: k2_common.cuh.
+// flight per warp); the next star's DoFs, row extents and an L2 prefetch of its rows are produced
+// by the update warps during the first LU phases (registers carried across the star loop).
+// Packed factor layout: k2_common.cuh.  Measurements and the variants not kept: DESIGN 6.2,
+// profiles/k6/summary.txt; -DMHDP_K6_PROF (tools/k6_prof.sh) prints a cycle timeline.
 #include <climits>
 #include <cstdint>
 #include <cstdio>
