@@ -93,7 +93,7 @@ struct PanelXchg {
     double akk, pad;                 // the entry at position kk
 };
 
-__device__ __forceinline__ void panel_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * K6_PW) : "memory"); }
+__device__ __forceinline__ void panel_bar(int threads) { asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory"); }
 }  // namespace
 
 template <int NCH>   // 32-row chunks per column: stars up to 32 NCH DoFs
@@ -269,6 +269,12 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
                 // says it has not been a pivot yet; the write-back scatters the rows to their
                 // positions, so shared memory is in R-lu's physical order again at every phase.
                 if (k1 >= n) continue;
+                // Only the warps owning rows k1..n-1 take part in this panel (warp 0 drops out after
+                // row 32, ...): the others would execute every step for nothing and lengthen the
+                // exchange barrier.  tl = thread index within the participating warps.
+                const int wlo = k1 >> 5, whi = (n - 1) >> 5;
+                if (wid < wlo || wid > whi) continue;
+                const int pth = 32 * (whi - wlo + 1), tl = tid - 32 * wlo;
                 const int nb = min(B, n - k1);
                 const bool inb = row < n;
                 // Load the panel's columns with panel K applied.  Nothing is swapped in shared memory
@@ -310,7 +316,7 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
                             x = fma(-cp3, u3, x);
                         }
                         c[s] = x;
-                        if (tid == s) { us0 = u0; us1 = u1; us2 = u2; us3 = u3; }
+                        if (tl == s) { us0 = u0; us1 = u1; us2 = u2; us3 = u3; }
                     }
                 } else {
 #pragma unroll
@@ -357,13 +363,14 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
                         }
                         if (ball == 0u && lane == 0) X.c[wid].vr = make_double2(-1.0, 0.0);
                         if (live && mypos == kk) X.akk = cs;
-                        panel_bar();
-                        if (s == 0 && K >= 0 && tid < nb) {   // every thread has read the columns: store u
-                            double *cj = a + (size_t)(k1 + tid) * ld;
+                        panel_bar(pth);
+                        if (s == 0 && K >= 0 && tl < nb) {   // every thread has read the columns: store u
+                            double *cj = a + (size_t)(k1 + tl) * ld;
                             cj[k0] = us0; cj[k0 + 1] = us1; cj[k0 + 2] = us2; cj[k0 + 3] = us3;
                         }
                         // best of the four candidates: largest |a|, lowest position among equals (branch-free)
-                        const double v0 = X.c[0].vr.x, v1 = X.c[1].vr.x, v2 = X.c[2].vr.x, v3 = X.c[3].vr.x;
+                        const double v0 = wlo <= 0 ? X.c[0].vr.x : -1.0, v1 = (wlo <= 1 && whi >= 1) ? X.c[1].vr.x : -1.0;
+                        const double v2 = (wlo <= 2 && whi >= 2) ? X.c[2].vr.x : -1.0, v3 = whi >= 3 ? X.c[3].vr.x : -1.0;
                         const int p0 = X.c[0].pos, p1 = X.c[1].pos, p2 = X.c[2].pos, p3 = X.c[3].pos;
                         const double akk = X.akk;
                         const double m01 = v1 > v0 ? v1 : v0, m23 = v3 > v2 ? v3 : v2;
@@ -412,7 +419,7 @@ k_patch_lu_cm(int64_t np, const int *__restrict__ pn, const int64_t *__restrict_
                     for (int s = 0; s < B; ++s)
                         if (s < nb) a[(size_t)(k1 + s) * ld + mypos] = c[s];
                 }
-                if (tid == 0) {
+                if (tl == 0) {
 #pragma unroll
                     for (int s = 0; s < B; ++s) {
                         if (s < nb && (fail < 0 || s <= fail)) {
